@@ -1,0 +1,247 @@
+/*
+ * bsccs_b200.h -- C ABI of the B200-native CCD hot path.
+ *
+ * This is the drop-in boundary for the cyclic-coordinate-descent (CCD)
+ * MAP fit of the Bayesian self-controlled case series model
+ * (arXiv 1208.0945).  The reference (`bsccs`, header-only C++20 under
+ * /root/reference/proj/include/bsccs) has no FFI: its engine is templated
+ * over EngineState<RealType> and called directly by the solver.  Every entry
+ * point below names the reference symbol it replaces (file:line relative to
+ * /root/reference/proj/include/bsccs/).  Plain pointers and sizes only; no
+ * C++ or torch types cross this boundary.
+ *
+ * Conventions
+ *   - Every function returns a bsccs_status.  BSCCS_OK == 0.  On failure the
+ *     thread-local message is available from bsccs_last_error().  The status
+ *     codes mirror the reference exception types (common.hpp:10-35):
+ *       BSCCS_INPUT_ERROR       <- bsccs::input_error
+ *       BSCCS_NUMERIC_ERROR     <- bsccs::numeric_error
+ *       BSCCS_CONVERGENCE_ERROR <- bsccs::convergence_error
+ *       BSCCS_INTERNAL_ERROR    <- bsccs::internal_error
+ *       BSCCS_CUDA_ERROR        a CUDA runtime failure (no reference analogue)
+ *   - Host arrays are borrowed for the duration of the call only.
+ *   - A dataset handle owns its device-resident copy and may be shared
+ *     read-only by any number of state handles on the same device.
+ *   - A state handle owns one fit's mutable device vectors and its stream.
+ *     Distinct handles may be used from distinct host threads.
+ *   - index type is int32 (common.hpp:8); pair offsets are int64.
+ */
+#ifndef BSCCS_B200_H
+#define BSCCS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BSCCS_B200_ABI_VERSION 1
+
+typedef enum bsccs_status {
+    BSCCS_OK = 0,
+    BSCCS_INPUT_ERROR = 1,
+    BSCCS_NUMERIC_ERROR = 2,
+    BSCCS_INTERNAL_ERROR = 3,
+    BSCCS_CONVERGENCE_ERROR = 4,
+    BSCCS_CUDA_ERROR = 5
+} bsccs_status;
+
+/* PriorSpec (prior.hpp:17-25).  kind: 0 none, 1 normal, 2 laplace
+ * (PriorKind, prior.hpp:10). */
+typedef struct bsccs_prior {
+    int32_t kind;
+    int32_t variance_is_laplace_scale;
+    double variance;
+} bsccs_prior;
+
+/* SolverConfig (solver.hpp:21-46).  convergence: 0 raw_sum, 1 normalized.
+ * precision: 1 Double (0 Single is rejected with BSCCS_INPUT_ERROR: the
+ * device path is fp64 only).  path: 0 sparse (1 dense is rejected).
+ * partitions / min_parallel_nnz are accepted and ignored: the device
+ * reduction fixes its own partition (one per CTA), see DESIGN.md. */
+typedef struct bsccs_solver_config {
+    double epsilon;
+    int32_t max_cycles;
+    int32_t convergence;
+    double trust_init;
+    int32_t precision;
+    int32_t path;
+    int32_t partitions;
+    int32_t dense_refresh_interval;
+    int32_t random_cycle;
+    int32_t reserved0;
+    uint64_t cycle_seed;
+    uint64_t min_parallel_nnz;
+} bsccs_solver_config;
+
+/* FitResult (solver.hpp:66-72); beta_map goes to a caller buffer. */
+typedef struct bsccs_fit_result {
+    double log_posterior;
+    double final_criterion;
+    int32_t cycles_run;
+    int32_t converged;
+    /* instrumentation, not in the reference struct */
+    int64_t coordinates_visited; /* non-skipped coordinate steps, all cycles */
+    int64_t coordinates_moved;   /* of those, steps with delta != 0        */
+    int64_t dense_refreshes;     /* dense_recompute calls incl. the final */
+    double device_seconds;       /* fit() entry -> FitResult, CUDA events  */
+    double sweep_seconds;        /* sum of sweep-kernel durations (events on
+                                    the launching stream)                  */
+    double algorithmic_bytes;    /* SURVEY §8(d) byte model summed over the
+                                    sweep kernels of this fit              */
+    int64_t kernel_launches;     /* library kernels launched by this fit   */
+} bsccs_fit_result;
+
+typedef struct bsccs_dataset bsccs_dataset;
+typedef struct bsccs_state bsccs_state;
+
+/* ---- library ---------------------------------------------------------- */
+int32_t bsccs_abi_version(void);
+const char* bsccs_last_error(void);
+/* Number of CTAs the persistent sweep kernel uses on `device` (one per SM
+ * times the resident count).  Fixed per dataset at creation. */
+bsccs_status bsccs_device_info(int32_t device, int32_t* sm_count, int32_t* ctas);
+/* Process-wide count of kernels this library has launched (evidence that
+ * the device path ran; bench.py reports it as gpu_launches). */
+int64_t bsccs_launch_count(void);
+
+/* ---- dataset (dataset.hpp:53-68 Dataset / SparseColumn) ---------------
+ * Flat CSC form of bsccs::Dataset: column j's pairs are
+ * [col_ptr[j], col_ptr[j+1]) of rows[] / subjects[] (SparseColumn::rows and
+ * ::subjects concatenated, dataset.hpp:38-43).  y_dot_x may be NULL (it is
+ * then recomputed on device from event_counts).  Validates the structural
+ * invariants of build_dataset (dataset.hpp:74-152): offsets fenceposts,
+ * rows ascending within a column, subject[p] owning rows[p].
+ * num_ctas_override <= 0 selects the device default. */
+bsccs_status bsccs_dataset_create(
+    int32_t num_subjects, int32_t num_eras, int32_t num_drugs, int64_t nnz,
+    const int32_t* subject_offsets,    /* [num_subjects + 1] */
+    const int32_t* events_per_subject, /* [num_subjects]     */
+    const int32_t* era_lengths,        /* [num_eras]         */
+    const int32_t* event_counts,       /* [num_eras]         */
+    const int64_t* col_ptr,            /* [num_drugs + 1]    */
+    const int32_t* rows,               /* [nnz]              */
+    const int32_t* subjects,           /* [nnz]              */
+    const int64_t* y_dot_x,            /* [num_drugs] or NULL */
+    int32_t device, int32_t num_ctas_override,
+    bsccs_dataset** out);
+
+/* Shard of a patient-partitioned dataset: the arrays are the
+ * shard's own (subjects/eras renumbered from 0), while y_dot_x_global and
+ * col_nnz_global describe the whole dataset so that the gradient and the
+ * skip rule (solver.hpp:119-121) are the global ones. */
+bsccs_status bsccs_dataset_create_shard(
+    int32_t num_subjects, int32_t num_eras, int32_t num_drugs, int64_t nnz,
+    const int32_t* subject_offsets, const int32_t* events_per_subject,
+    const int32_t* era_lengths, const int32_t* event_counts,
+    const int64_t* col_ptr, const int32_t* rows, const int32_t* subjects,
+    const int64_t* y_dot_x_global, const int64_t* col_nnz_global,
+    int32_t device, int32_t num_ctas_override,
+    bsccs_dataset** out);
+
+bsccs_status bsccs_dataset_destroy(bsccs_dataset* ds);
+/* sizes: N, K, J, nnz, ctas, device bytes resident */
+bsccs_status bsccs_dataset_info(const bsccs_dataset* ds, int64_t out[6]);
+
+/* ---- tier 1: engine (engine.hpp) --------------------------------------- */
+/* init_state (engine.hpp:137-166); beta may be NULL (zeros). */
+bsccs_status bsccs_state_create(const bsccs_dataset* ds, const double* beta,
+                                bsccs_state** out);
+/* EngineState copy (engine.hpp:36-45 is a value type). */
+bsccs_status bsccs_state_clone(const bsccs_state* src, bsccs_state** out);
+bsccs_status bsccs_state_destroy(bsccs_state* st);
+/* dense_recompute (engine.hpp:170-200); beta NULL = rebuild from state. */
+bsccs_status bsccs_dense_recompute(bsccs_state* st, const double* beta);
+/* fused_grad_hess / parallel_fused_grad_hess (engine.hpp:285-361). */
+bsccs_status bsccs_grad_hess(bsccs_state* st, int32_t j, double* gradient,
+                             double* hessian);
+/* sparse_delta_update (engine.hpp:205-231). */
+bsccs_status bsccs_sparse_update(bsccs_state* st, int32_t j, double delta);
+/* log_likelihood (engine.hpp:404-425). */
+bsccs_status bsccs_log_likelihood(bsccs_state* st, double* out);
+/* Copies EngineState vectors to host; any pointer may be NULL. */
+bsccs_status bsccs_state_get(bsccs_state* st, double* beta, double* xbeta,
+                             double* l_exp_xbeta, double* denominators);
+
+/* ---- prior (prior.hpp) -- host evaluation of the device code --------- */
+bsccs_status bsccs_penalized_step(const bsccs_prior* prior, double beta_j,
+                                  double g, double h, double* step);
+bsccs_status bsccs_log_density(const bsccs_prior* prior, const double* beta,
+                               int32_t n, double* out);
+
+/* ---- tier 2: solver (solver.hpp) --------------------------------------- */
+/* run_cycle (solver.hpp:101-166): one persistent-kernel sweep.  trust is the
+ * per-coordinate radius vector (SolverState::trust, solver.hpp:88), in/out on
+ * host; order is the visit order (NULL = ascending). */
+bsccs_status bsccs_run_cycle(bsccs_state* st, const bsccs_prior* prior,
+                             const bsccs_solver_config* cfg,
+                             const int32_t* order, double* trust,
+                             double* criterion);
+/* fit (solver.hpp:206-220) on a resident dataset.  init_beta may be NULL;
+ * beta_out has num_drugs entries. */
+bsccs_status bsccs_fit(const bsccs_dataset* ds, const bsccs_prior* prior,
+                       const bsccs_solver_config* cfg, const double* init_beta,
+                       double* beta_out, bsccs_fit_result* result);
+/* Defaults of SolverConfig{} (solver.hpp:21-46). */
+void bsccs_solver_config_default(bsccs_solver_config* cfg);
+
+/* ---- multi-GPU patient sharding ------------------------ */
+/* A group binds the shards that exchange (gradient, hessian) partials each
+ * coordinate.  Local groups (all shards on one device, one process) are the
+ * single-GPU test of the cross-shard protocol; multi-process groups bind the
+ * per-rank exchange buffer of every peer through CUDA IPC. */
+typedef struct bsccs_group bsccs_group;
+/* Size in bytes of one exchange-slot buffer for `total_ctas` participants. */
+int64_t bsccs_group_slot_bytes(int32_t total_ctas);
+/* Local group over n shards of one device (one cooperative launch). */
+bsccs_status bsccs_group_create_local(bsccs_dataset* const* shards, int32_t n,
+                                      bsccs_group** out);
+/* Multi-process: rank r of world w with its one local shard. */
+bsccs_status bsccs_group_create_rank(bsccs_dataset* shard, int32_t rank,
+                                     int32_t world, const int32_t* ctas_per_rank,
+                                     bsccs_group** out);
+/* 64-byte cudaIpcMemHandle of this rank's slot buffer. */
+bsccs_status bsccs_group_ipc_handle(bsccs_group* g, uint8_t out[64]);
+/* Open the peers' handles (world x 64 bytes, own entry ignored). */
+bsccs_status bsccs_group_open_peers(bsccs_group* g, const uint8_t* handles);
+bsccs_status bsccs_group_destroy(bsccs_group* g);
+/* fit over a group; beta_out / result identical on every shard. */
+bsccs_status bsccs_group_fit(bsccs_group* g, const bsccs_prior* prior,
+                             const bsccs_solver_config* cfg,
+                             const double* init_beta, double* beta_out,
+                             bsccs_fit_result* result);
+
+/* ---- synthetic data (simulate.hpp, SURVEY §8(d) generators) ----------- */
+typedef struct bsccs_host_dataset bsccs_host_dataset;
+/* simulate() restated (simulate.hpp:50-137); prevalence / true_beta have
+ * `drugs` entries. */
+bsccs_status bsccs_synth_simulate(int32_t subjects, int32_t drugs,
+                                  int32_t min_eras, int32_t max_eras,
+                                  int32_t min_era_length, int32_t max_era_length,
+                                  const double* prevalence, const double* true_beta,
+                                  double baseline_log_rate_mean,
+                                  double baseline_log_rate_sd, uint64_t seed,
+                                  bsccs_host_dataset** out);
+/* Fast SCCS generator of SURVEY §8(d); zipf != 0 selects the skewed
+ * P(drug j) ~ 1/(j+1) variant.  threads <= 0: all hardware threads. */
+bsccs_status bsccs_synth_fast(int64_t attempts, int32_t drugs, double lambda_x,
+                              int32_t zipf, uint64_t seed, int32_t threads,
+                              bsccs_host_dataset** out);
+/* N, K, J, nnz */
+bsccs_status bsccs_host_dataset_sizes(const bsccs_host_dataset* h, int64_t out[4]);
+/* Borrowed pointers into the handle (valid until destroy). */
+bsccs_status bsccs_host_dataset_arrays(const bsccs_host_dataset* h,
+                                       const int32_t** subject_offsets,
+                                       const int32_t** events_per_subject,
+                                       const int32_t** era_lengths,
+                                       const int32_t** event_counts,
+                                       const int64_t** col_ptr,
+                                       const int32_t** rows,
+                                       const int32_t** subjects,
+                                       const int64_t** y_dot_x);
+bsccs_status bsccs_host_dataset_destroy(bsccs_host_dataset* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BSCCS_B200_H */

@@ -1,0 +1,277 @@
+// ref_shim.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// extern "C" wrapper around the UNMODIFIED reference headers
+// (/root/reference/proj/include/bsccs/*.hpp), built by oracle/Makefile into
+// oracle/_ref/libbsccs_ref.so.  Nothing of the reference is copied: this file
+// only converts the flat CSC form used across our C ABI into bsccs::Dataset
+// and calls the reference's own functions.  Used (a) to pin the C
+// restatement oracle/ccd_oracle.c bit for bit, (b) to generate the golden
+// fixtures in tests/golden/, and (c) as bench.py's CPU baseline
+// (cpu_baseline.kind = "reference").
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include <bsccs/bsccs.hpp>
+
+#include "../include/bsccs_b200.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guard(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const bsccs::input_error& e) {
+        g_err = e.what();
+        return BSCCS_INPUT_ERROR;
+    } catch (const bsccs::numeric_error& e) {
+        g_err = e.what();
+        return BSCCS_NUMERIC_ERROR;
+    } catch (const bsccs::convergence_error& e) {
+        g_err = e.what();
+        return BSCCS_CONVERGENCE_ERROR;
+    } catch (const bsccs::internal_error& e) {
+        g_err = e.what();
+        return BSCCS_INTERNAL_ERROR;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return BSCCS_INTERNAL_ERROR;
+    }
+}
+
+bsccs::PriorSpec to_prior(const bsccs_prior* p) {
+    bsccs::PriorSpec out;
+    out.kind = static_cast<bsccs::PriorKind>(p->kind);
+    out.variance = p->variance;
+    out.variance_is_laplace_scale = p->variance_is_laplace_scale != 0;
+    return out;
+}
+
+bsccs::SolverConfig to_cfg(const bsccs_solver_config* c) {
+    bsccs::SolverConfig out;
+    out.epsilon = c->epsilon;
+    out.max_cycles = c->max_cycles;
+    out.trust_init = c->trust_init;
+    out.convergence = c->convergence ? bsccs::ConvergenceMode::normalized
+                                     : bsccs::ConvergenceMode::raw_sum;
+    out.precision = c->precision == 0 ? bsccs::Precision::Single : bsccs::Precision::Double;
+    out.path = c->path == 1 ? bsccs::UpdatePath::dense : bsccs::UpdatePath::sparse;
+    out.partitions = c->partitions;
+    out.dense_refresh_interval = c->dense_refresh_interval;
+    out.random_cycle = c->random_cycle != 0;
+    out.cycle_seed = c->cycle_seed;
+    out.min_parallel_nnz = c->min_parallel_nnz;
+    return out;
+}
+
+struct RefState {
+    bsccs::EngineState<double> st;
+    std::unique_ptr<bsccs::SolverState<double>> solver;
+    std::unique_ptr<bsccs::ThreadPool> pool;
+};
+
+} // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+// Flat CSC -> bsccs::Dataset (public-field struct, dataset.hpp:53-68).
+int ref_dataset_create(int32_t N, int32_t K, int32_t J, int64_t nnz,
+                       const int32_t* subject_offsets, const int32_t* events_per_subject,
+                       const int32_t* era_lengths, const int32_t* event_counts,
+                       const int64_t* col_ptr, const int32_t* rows, const int32_t* subjects,
+                       const int64_t* y_dot_x, void** out) {
+    return guard([&] {
+        auto* ds = new bsccs::Dataset();
+        ds->num_subjects = N;
+        ds->num_eras = K;
+        ds->num_drugs = J;
+        ds->subject_offsets.assign(subject_offsets, subject_offsets + N + 1);
+        ds->events_per_subject.assign(events_per_subject, events_per_subject + N);
+        ds->era_lengths.assign(era_lengths, era_lengths + K);
+        ds->event_counts.assign(event_counts, event_counts + K);
+        ds->y_dot_x.assign(y_dot_x, y_dot_x + J);
+        ds->columns.resize(static_cast<size_t>(J));
+        for (int32_t j = 0; j < J; ++j) {
+            auto& col = ds->columns[static_cast<size_t>(j)];
+            col.rows.assign(rows + col_ptr[j], rows + col_ptr[j + 1]);
+            col.subjects.assign(subjects + col_ptr[j], subjects + col_ptr[j + 1]);
+            ds->max_column_nnz = std::max<int32_t>(ds->max_column_nnz,
+                                                   static_cast<int32_t>(col.rows.size()));
+        }
+        (void)nnz;
+        *out = ds;
+    });
+}
+
+void ref_dataset_destroy(void* ds) { delete static_cast<bsccs::Dataset*>(ds); }
+
+int64_t ref_dataset_nnz(void* dsp) {
+    auto* ds = static_cast<bsccs::Dataset*>(dsp);
+    int64_t n = 0;
+    for (auto& c : ds->columns) n += static_cast<int64_t>(c.rows.size());
+    return n;
+}
+
+// sizes: N K J nnz
+void ref_dataset_sizes(void* dsp, int64_t out[4]) {
+    auto* ds = static_cast<bsccs::Dataset*>(dsp);
+    out[0] = ds->num_subjects;
+    out[1] = ds->num_eras;
+    out[2] = ds->num_drugs;
+    out[3] = ref_dataset_nnz(dsp);
+}
+
+// bsccs::Dataset -> flat CSC (caller-sized buffers)
+void ref_dataset_flatten(void* dsp, int32_t* subject_offsets, int32_t* events_per_subject,
+                         int32_t* era_lengths, int32_t* event_counts, int64_t* col_ptr,
+                         int32_t* rows, int32_t* subjects, int64_t* y_dot_x) {
+    auto* ds = static_cast<bsccs::Dataset*>(dsp);
+    std::memcpy(subject_offsets, ds->subject_offsets.data(), sizeof(int32_t) * ds->subject_offsets.size());
+    std::memcpy(events_per_subject, ds->events_per_subject.data(), sizeof(int32_t) * ds->events_per_subject.size());
+    std::memcpy(era_lengths, ds->era_lengths.data(), sizeof(int32_t) * ds->era_lengths.size());
+    std::memcpy(event_counts, ds->event_counts.data(), sizeof(int32_t) * ds->event_counts.size());
+    std::memcpy(y_dot_x, ds->y_dot_x.data(), sizeof(int64_t) * ds->y_dot_x.size());
+    int64_t p = 0;
+    col_ptr[0] = 0;
+    for (size_t j = 0; j < ds->columns.size(); ++j) {
+        const auto& c = ds->columns[j];
+        std::memcpy(rows + p, c.rows.data(), sizeof(int32_t) * c.rows.size());
+        std::memcpy(subjects + p, c.subjects.data(), sizeof(int32_t) * c.subjects.size());
+        p += static_cast<int64_t>(c.rows.size());
+        col_ptr[j + 1] = p;
+    }
+}
+
+// simulate() (simulate.hpp:50-137) -> Dataset handle
+int ref_simulate(int32_t subjects, int32_t drugs, int32_t min_eras, int32_t max_eras,
+                 int32_t min_len, int32_t max_len, const double* prevalence,
+                 const double* true_beta, double mean, double sd, uint64_t seed, void** out) {
+    return guard([&] {
+        bsccs::SimConfig cfg;
+        cfg.subjects = subjects;
+        cfg.drugs = drugs;
+        cfg.min_eras = min_eras;
+        cfg.max_eras = max_eras;
+        cfg.min_era_length = min_len;
+        cfg.max_era_length = max_len;
+        cfg.prevalence.assign(prevalence, prevalence + drugs);
+        cfg.true_beta.assign(true_beta, true_beta + drugs);
+        cfg.baseline_log_rate_mean = mean;
+        cfg.baseline_log_rate_sd = sd;
+        cfg.seed = seed;
+        auto sim = bsccs::simulate(cfg);
+        *out = new bsccs::Dataset(std::move(sim.dataset));
+    });
+}
+
+// subset_dataset (dataset.hpp:157-217)
+int ref_subset(void* dsp, const int32_t* idx, int64_t n, void** out) {
+    return guard([&] {
+        std::vector<bsccs::index_t> sel(idx, idx + n);
+        *out = new bsccs::Dataset(bsccs::subset_dataset(*static_cast<bsccs::Dataset*>(dsp), sel));
+    });
+}
+
+// fit (solver.hpp:206-220).  threads > 1 supplies ThreadPool(threads - 1)
+// (the caller participates, thread_pool.hpp:22-28).  seconds = fit() wall.
+int ref_fit(void* dsp, const bsccs_prior* prior, const bsccs_solver_config* cfg,
+            const double* init_beta, int32_t threads, double* beta_out,
+            bsccs_fit_result* res, double* seconds) {
+    return guard([&] {
+        auto* ds = static_cast<bsccs::Dataset*>(dsp);
+        std::vector<double> init;
+        if (init_beta) init.assign(init_beta, init_beta + ds->num_drugs);
+        std::unique_ptr<bsccs::ThreadPool> pool;
+        if (threads > 1) pool = std::make_unique<bsccs::ThreadPool>(threads - 1);
+        const auto t0 = std::chrono::steady_clock::now();
+        bsccs::FitResult r = bsccs::fit(*ds, to_prior(prior), to_cfg(cfg), init, pool.get());
+        const auto t1 = std::chrono::steady_clock::now();
+        if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+        std::memcpy(beta_out, r.beta_map.data(), sizeof(double) * r.beta_map.size());
+        std::memset(res, 0, sizeof *res);
+        res->log_posterior = r.log_posterior;
+        res->final_criterion = r.final_criterion;
+        res->cycles_run = r.cycles_run;
+        res->converged = r.converged ? 1 : 0;
+    });
+}
+
+// ---- engine-level handles --------------------------------------------------
+int ref_state_create(void* dsp, const double* beta, const bsccs_solver_config* cfg, void** out) {
+    return guard([&] {
+        auto* ds = static_cast<bsccs::Dataset*>(dsp);
+        std::vector<double> b;
+        if (beta) b.assign(beta, beta + ds->num_drugs);
+        auto* s = new RefState{bsccs::init_state<double>(*ds, b), nullptr, nullptr};
+        bsccs::SolverConfig c = cfg ? to_cfg(cfg) : bsccs::SolverConfig{};
+        s->solver = std::make_unique<bsccs::SolverState<double>>(*ds, c);
+        *out = s;
+    });
+}
+void ref_state_destroy(void* s) { delete static_cast<RefState*>(s); }
+
+int ref_grad_hess(void* dsp, void* sp, int32_t j, int32_t partitions, double* g, double* h) {
+    return guard([&] {
+        auto gh = bsccs::parallel_fused_grad_hess(*static_cast<bsccs::Dataset*>(dsp),
+                                                  static_cast<RefState*>(sp)->st, j, partitions);
+        *g = gh.gradient;
+        *h = gh.hessian;
+    });
+}
+int ref_sparse_update(void* dsp, void* sp, int32_t j, double delta) {
+    return guard([&] {
+        bsccs::sparse_delta_update(*static_cast<bsccs::Dataset*>(dsp), static_cast<RefState*>(sp)->st, j, delta);
+    });
+}
+int ref_dense_recompute(void* dsp, void* sp, const double* beta) {
+    return guard([&] {
+        auto* ds = static_cast<bsccs::Dataset*>(dsp);
+        auto& st = static_cast<RefState*>(sp)->st;
+        if (beta) bsccs::dense_recompute(*ds, st, std::vector<double>(beta, beta + ds->num_drugs));
+        else bsccs::dense_recompute(*ds, st);
+    });
+}
+int ref_log_likelihood(void* dsp, void* sp, double* out) {
+    return guard([&] { *out = bsccs::log_likelihood(*static_cast<bsccs::Dataset*>(dsp), static_cast<RefState*>(sp)->st); });
+}
+void ref_state_get(void* sp, double* beta, double* xbeta, double* lexp, double* den) {
+    auto& st = static_cast<RefState*>(sp)->st;
+    if (beta) std::memcpy(beta, st.beta.data(), sizeof(double) * st.beta.size());
+    if (xbeta) std::memcpy(xbeta, st.xbeta.data(), sizeof(double) * st.xbeta.size());
+    if (lexp) std::memcpy(lexp, st.l_exp_xbeta.data(), sizeof(double) * st.l_exp_xbeta.size());
+    if (den) std::memcpy(den, st.denominators.data(), sizeof(double) * st.denominators.size());
+}
+// threads > 1: the reference's parallel route (ThreadPool(threads-1) passed
+// to run_cycle; cfg.partitions selects the chunking, solver.hpp:127-128).
+void ref_state_set_threads(void* sp, int32_t threads) {
+    auto* s = static_cast<RefState*>(sp);
+    s->pool.reset();
+    if (threads > 1) s->pool = std::make_unique<bsccs::ThreadPool>(threads - 1);
+}
+// run_cycle (solver.hpp:101-166) with the handle's SolverState
+int ref_run_cycle(void* dsp, void* sp, const bsccs_prior* prior, const bsccs_solver_config* cfg,
+                  double* criterion, double* trust_out) {
+    return guard([&] {
+        auto* s = static_cast<RefState*>(sp);
+        *criterion = bsccs::run_cycle(*static_cast<bsccs::Dataset*>(dsp), s->st, *s->solver,
+                                      to_prior(prior), to_cfg(cfg), s->pool.get());
+        if (trust_out) std::memcpy(trust_out, s->solver->trust.data(), sizeof(double) * s->solver->trust.size());
+    });
+}
+int ref_penalized_step(const bsccs_prior* prior, double beta_j, double g, double h, double* out) {
+    return guard([&] { *out = bsccs::penalized_step(to_prior(prior), beta_j, g, h); });
+}
+int ref_log_density(const bsccs_prior* prior, const double* beta, int32_t n, double* out) {
+    return guard([&] { *out = bsccs::log_density(to_prior(prior), std::vector<double>(beta, beta + n)); });
+}
+
+} // extern "C"

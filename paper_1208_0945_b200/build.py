@@ -1,0 +1,90 @@
+"""Builds the in-tree native library (and the test-only oracle libraries).
+
+libbsccs_b200.so holds the sm_100a kernels, the C ABI of
+include/bsccs_b200.h, the host CCD driver and the synthetic generators.  It
+is compiled in-tree with explicit nvcc flags so the built file travels with
+the gpurun snapshot (no JIT cache).
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+LIB_DIR = PKG / "_lib"
+LIB = LIB_DIR / "libbsccs_b200.so"
+
+SOURCES = ["ccd_kernels.cu", "capi.cpp", "datagen.cpp"]
+HEADERS = ["engine.h", "prior.h", "rng.h", "status.h"]
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-lineinfo", "-O3", "-std=c++17",
+    "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
+    "--expt-relaxed-constexpr",
+]
+
+
+def _nvcc() -> str:
+    cand = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    return cand if Path(cand).exists() else "nvcc"
+
+
+def _stale(target: Path, deps: list[Path]) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(d.stat().st_mtime > t for d in deps)
+
+
+def build_native(force: bool = False, verbose: bool = False) -> Path:
+    LIB_DIR.mkdir(exist_ok=True)
+    deps = [CSRC / s for s in SOURCES + HEADERS] + [ROOT / "include" / "bsccs_b200.h"]
+    if not force and not _stale(LIB, deps):
+        return LIB
+    objs = []
+    for src in SOURCES:
+        obj = LIB_DIR / (Path(src).stem + ".o")
+        cmd = [_nvcc(), *NVCC_FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+        if src.endswith(".cu"):
+            cmd += ["-Xptxas", "-v"] if verbose else []
+        else:
+            cmd += ["-x", "cu"] if False else []
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+        objs.append(str(obj))
+    tmp = LIB.with_suffix(".so.tmp")
+    cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp), *objs,
+           "-lpthread", "-cudart", "static"]
+    subprocess.run(cmd, check=True)
+    os.replace(tmp, LIB)
+    for o in objs:
+        Path(o).unlink(missing_ok=True)
+    return LIB
+
+
+def build_oracle(verbose: bool = False) -> None:
+    """Test infrastructure: C restatement always; the reference shim only
+    where /root/reference exists (this container), else the prebuilt copy."""
+    targets = ["oracle"]
+    if Path(os.environ.get("REF_INCLUDE", "/root/reference/proj/include")).exists():
+        targets.append("ref")
+    subprocess.run(["make", "-s", "-C", str(ROOT / "oracle"), *targets], check=True,
+                   stdout=None if verbose else subprocess.DEVNULL)
+
+
+def main(argv: list[str]) -> None:
+    force = "--force" in argv
+    verbose = "-v" in argv
+    build_native(force=force, verbose=verbose)
+    build_oracle(verbose=verbose)
+    print(f"built {LIB}")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])

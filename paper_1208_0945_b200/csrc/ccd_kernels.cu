@@ -1,0 +1,1363 @@
+// ccd_kernels.cu -- sm_100a kernels of the CCD hot path and their launchers.
+//
+// Kernels (DESIGN.md §4 gives the roofline of each):
+//   k_ccd            persistent cooperative kernel, one CTA per SM.  A launch
+//                    runs one full cycle (run_cycle, solver.hpp:101-166) or a
+//                    single tier-1 op.  Per coordinate: fused grad/hess over
+//                    the CTA's subject-aligned slice of the column
+//                    (engine.hpp:97-132), a 32-byte all-gather of the
+//                    per-CTA partials through self-validating slots, the
+//                    penalized step evaluated redundantly by every CTA
+//                    (prior.hpp:72-122), and the sparse update of the
+//                    slice's runs (engine.hpp:205-231) -- no atomics, no
+//                    grid barrier, one exchange per coordinate.
+//   k_dense_xb       dense_recompute xbeta / l*exp rebuild (engine.hpp:68-90,
+//                    170-183) from the row-major copy, reference add order
+//   k_dense_den      per-subject ascending sum of l*exp (engine.hpp:81-89)
+//   k_ll_partial/    log_likelihood (engine.hpp:404-425), fixed-order
+//   k_ll_final       two-level reduction
+//   dataset build    interleave, row histogram, stable radix sort (CUB) to
+//                    build the CSR, nnz-balanced CTA subject ranges, split.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "engine.h"
+
+namespace bsccs_b200 {
+
+namespace {
+std::atomic<long long> g_launches{0};
+}
+void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        fail(BSCCS_CUDA_ERROR, std::string("CUDA error: ") + cudaGetErrorString(e) + " at " + what);
+    }
+}
+
+namespace {
+
+constexpr int kModeSweep = 0;
+constexpr int kModeGradHess = 1;
+constexpr int kModeUpdate = 2;
+constexpr int kCached = 2;          // register-cached tiles of the slice
+constexpr int kWarps = kSweepThreads / 32;
+constexpr int kRecPerLane = 4;      // exchange records polled per lane
+constexpr int kMaxPollWarps = kWarps;
+constexpr int kLLBlocks = 592;      // fixed => deterministic LL reduction
+constexpr int kLLThreads = 256;
+constexpr double kXbBound = 700.0;  // xbeta_bound<double> engine.hpp:20-23
+
+struct ShardArgs {
+    const int2* pairs;
+    const int64_t* col_ptr;
+    const int32_t* col_runs;
+    const int64_t* split;
+    const int32_t* cta_era;
+    EraRec* era;
+    SubjRec* subj;
+    double* beta;
+    double* trust;
+    DevErr* err;
+    DevResult* res;
+    int ctas;
+    int cta_begin;
+    int pid_base;
+    int K;
+};
+
+struct SweepArgs {
+    ShardArgs sh[kMaxLocalShards];
+    int nsh;
+    const int32_t* order; // nullptr: ascending
+    const double* y_dot_x;
+    const uint8_t* col_nonempty;
+    int J;
+    PriorParams prior;
+    int mode;
+    int single_j;
+    double single_delta;
+    int normalized;
+    unsigned long long* dst[kMaxRanks];
+    int ndst;
+    const unsigned long long* slots;
+    int P;
+    unsigned long long* counter;
+};
+
+struct Smem {
+    double ra[kWarps], rb[kWarps];
+    int re[kWarps];
+    double pa[kMaxPollWarps], pb[kMaxPollWarps];
+    int pe[kMaxPollWarps];
+};
+
+__device__ __forceinline__ void st_vol_v2(unsigned long long* p, unsigned long long a, unsigned long long b) {
+    asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void ld_vol_v2(const unsigned long long* p, unsigned long long& a, unsigned long long& b) {
+    asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+__device__ __forceinline__ int2 ld_pair(const int2* p) { return __ldg(p); }
+
+__device__ __forceinline__ void record_error(DevErr* e, int code, double value) {
+    if (atomicCAS(&e->code, 0, code) == 0) e->value = value;
+}
+
+__device__ __forceinline__ unsigned tag_of(unsigned long long seq) {
+    return static_cast<unsigned>(1ull + seq % 0x7fffffffull);
+}
+
+// Reduce (a, b, e) over the CTA; result valid in thread 0.
+__device__ __forceinline__ void block_reduce(double& a, double& b, int& e, Smem& sm) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a = __dadd_rn(a, __shfl_xor_sync(0xffffffffu, a, o));
+        b = __dadd_rn(b, __shfl_xor_sync(0xffffffffu, b, o));
+    }
+    e = __reduce_or_sync(0xffffffffu, e);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        sm.ra[w] = a;
+        sm.rb[w] = b;
+        sm.re[w] = e;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double x = 0.0, y = 0.0;
+        int z = 0;
+        for (int i = 0; i < kWarps; ++i) {
+            x = __dadd_rn(x, sm.ra[i]);
+            y = __dadd_rn(y, sm.rb[i]);
+            z |= sm.re[i];
+        }
+        a = x;
+        b = y;
+        e = z;
+    }
+}
+
+// All-gather of one 2-double record per participant, LL-protocol style:
+// every 8-byte word carries 32 data bits and the 32-bit tag (31-bit sequence
+// tag + error bit), so a word is valid on its own and one L2 round trip
+// suffices.  Double-buffered by sequence parity.  Every CTA sums the P
+// records in the same fixed order, so all compute bit-identical totals.
+// (a, b, e) are read from thread 0; totals returned to every thread.
+__device__ __forceinline__ void exchange(const SweepArgs& A, int pid, unsigned long long seq, double a,
+                                         double b, int e, double& ta, double& tb, int& te, Smem& sm) {
+    const unsigned tag = tag_of(seq);
+    const size_t slot_base = static_cast<size_t>(seq & 1ull) * static_cast<size_t>(A.P) * 4;
+    if (threadIdx.x == 0) {
+        const unsigned long long t =
+            static_cast<unsigned long long>(tag | (e ? 0x80000000u : 0u)) << 32;
+        const unsigned long long ab = static_cast<unsigned long long>(__double_as_longlong(a));
+        const unsigned long long bb = static_cast<unsigned long long>(__double_as_longlong(b));
+        const unsigned long long w0 = t | (ab & 0xffffffffull), w1 = t | (ab >> 32);
+        const unsigned long long w2 = t | (bb & 0xffffffffull), w3 = t | (bb >> 32);
+        const size_t off = slot_base + static_cast<size_t>(pid) * 4;
+        for (int d = 0; d < A.ndst; ++d) {
+            st_vol_v2(A.dst[d] + off, w0, w1);
+            st_vol_v2(A.dst[d] + off + 2, w2, w3);
+        }
+    }
+    const int nwp = (A.P + 32 * kRecPerLane - 1) / (32 * kRecPerLane);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (w < nwp) {
+        unsigned long long r0[kRecPerLane], r1[kRecPerLane], r2[kRecPerLane], r3[kRecPerLane];
+        bool ok[kRecPerLane];
+#pragma unroll
+        for (int i = 0; i < kRecPerLane; ++i) ok[i] = (w * 32 * kRecPerLane + i * 32 + l) >= A.P;
+        for (;;) {
+#pragma unroll
+            for (int i = 0; i < kRecPerLane; ++i) {
+                if (!ok[i]) {
+                    const size_t off = slot_base + static_cast<size_t>(w * 32 * kRecPerLane + i * 32 + l) * 4;
+                    ld_vol_v2(A.slots + off, r0[i], r1[i]);
+                    ld_vol_v2(A.slots + off + 2, r2[i], r3[i]);
+                }
+            }
+            bool all = true;
+#pragma unroll
+            for (int i = 0; i < kRecPerLane; ++i) {
+                if (!ok[i]) {
+                    ok[i] = ((static_cast<unsigned>(r0[i] >> 32) & 0x7fffffffu) == tag) &&
+                            ((static_cast<unsigned>(r1[i] >> 32) & 0x7fffffffu) == tag) &&
+                            ((static_cast<unsigned>(r2[i] >> 32) & 0x7fffffffu) == tag) &&
+                            ((static_cast<unsigned>(r3[i] >> 32) & 0x7fffffffu) == tag);
+                    all = all && ok[i];
+                }
+            }
+            if (__all_sync(0xffffffffu, all)) break;
+        }
+        double sa = 0.0, sb = 0.0;
+        int se = 0;
+#pragma unroll
+        for (int i = 0; i < kRecPerLane; ++i) {
+            if ((w * 32 * kRecPerLane + i * 32 + l) < A.P) {
+                const double va = __longlong_as_double(static_cast<long long>((r1[i] << 32) | (r0[i] & 0xffffffffull)));
+                const double vb = __longlong_as_double(static_cast<long long>((r3[i] << 32) | (r2[i] & 0xffffffffull)));
+                sa = __dadd_rn(sa, va);
+                sb = __dadd_rn(sb, vb);
+                se |= static_cast<int>(((r0[i] | r1[i] | r2[i] | r3[i]) >> 63) & 1ull);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            sa = __dadd_rn(sa, __shfl_xor_sync(0xffffffffu, sa, o));
+            sb = __dadd_rn(sb, __shfl_xor_sync(0xffffffffu, sb, o));
+        }
+        se = __reduce_or_sync(0xffffffffu, se);
+        if (l == 0) {
+            sm.pa[w] = sa;
+            sm.pb[w] = sb;
+            sm.pe[w] = se;
+        }
+    }
+    __syncthreads();
+    double x = 0.0, y = 0.0;
+    int z = 0;
+    for (int i = 0; i < nwp; ++i) {
+        x = __dadd_rn(x, sm.pa[i]);
+        y = __dadd_rn(y, sm.pb[i]);
+        z |= sm.pe[i];
+    }
+    ta = x;
+    tb = y;
+    te = z;
+}
+
+// Index data of one pair slot: the pair, whether it starts a subject run
+// (head) and whether the run continues past it.  Read-only; computed ahead
+// of the coordinate (prefetch) for the register-cached tiles.
+struct PairSlot {
+    int2 pr;
+    bool head;
+    bool cont;
+};
+
+__device__ __forceinline__ PairSlot load_slot(const int2* __restrict__ pairs, int64_t p, int64_t p0, int64_t p1) {
+    PairSlot s;
+    const bool valid = p < p1;
+    s.pr = valid ? ld_pair(pairs + p) : make_int2(-1, -1);
+    const int l = threadIdx.x & 31;
+    int prev = __shfl_up_sync(0xffffffffu, s.pr.y, 1);
+    int next = __shfl_down_sync(0xffffffffu, s.pr.y, 1);
+    if (l == 0) prev = (valid && p > p0) ? ld_pair(pairs + p - 1).y : -1;
+    if (l == 31) next = (p + 1 < p1) ? ld_pair(pairs + p + 1).y : -1;
+    s.head = valid && (p == p0 || prev != s.pr.y);
+    s.cont = valid && (p + 1 < p1) && next == s.pr.y;
+    return s;
+}
+
+// Fused per-run reduction term (engine.hpp:108-129): numerator summed in
+// ascending row order, w = min(num/den, 1), nw = n*w, (nw, nw*(1-w)).
+__device__ __forceinline__ void run_terms(double num, double den, int n, double& gs, double& hs, int& err) {
+    if (!(den > 0.0)) err = DERR_DEN_NONPOSITIVE;
+    double w = num / den;
+    if (w > 1.0) w = 1.0;
+    const double nw = __dmul_rn(static_cast<double>(n), w);
+    gs = __dadd_rn(gs, nw);
+    hs = __dadd_rn(hs, __dmul_rn(nw, __dsub_rn(1.0, w)));
+}
+
+// Continuation of a run past its head pair: numerator terms in order.
+__device__ __forceinline__ double run_tail_numerator(const int2* __restrict__ pairs, const EraRec* era, int64_t q,
+                                                     int64_t p1, int s, double num) {
+    for (;;) {
+        num = __dadd_rn(num, era[ld_pair(pairs + q).x].le);
+        ++q;
+        if (q >= p1 || ld_pair(pairs + q).y != s) break;
+    }
+    return num;
+}
+
+// Sparse update of one era in the reference's statement order
+// (engine.hpp:219-229); returns the new denominator.
+__device__ __forceinline__ double update_era(EraRec* era, int row, double xb, double le, int len, double d,
+                                             double den, int& err, double& errv) {
+    const double updated = __dadd_rn(xb, d);
+    if (!(fabs(updated) <= kXbBound)) {
+        err = DERR_OVERFLOW;
+        errv = fabs(updated);
+        return den;
+    }
+    const double fresh = __dmul_rn(static_cast<double>(len), exp(updated));
+    den = __dadd_rn(den, __dsub_rn(fresh, le));
+    double2* rec = reinterpret_cast<double2*>(era + row);
+    *rec = make_double2(updated, fresh);
+    return den;
+}
+
+// Update of the rest of a run after its head (pairs q.. of subject s).
+__device__ __forceinline__ double run_tail_update(const int2* __restrict__ pairs, EraRec* era, int64_t q, int64_t p1,
+                                                  int s, double d, double den, int& err, double& errv) {
+    for (;;) {
+        const int row = ld_pair(pairs + q).x;
+        const double2 xl = *reinterpret_cast<const double2*>(era + row);
+        const int len = era[row].len;
+        den = update_era(era, row, xl.x, xl.y, len, d, den, err, errv);
+        ++q;
+        if (q >= p1 || ld_pair(pairs + q).y != s) break;
+    }
+    return den;
+}
+
+struct Cached {
+    PairSlot slot[kCached];
+};
+
+// Grad/hess partial of this CTA's slice [p0, p1) of a column.  The first
+// kCached*T pairs come from prefetched slots and keep their era/subject data
+// in registers for the update; the rest stream tile by tile.
+struct HeadRegs {
+    double xb[kCached], le[kCached], den[kCached];
+    int len[kCached];
+};
+
+__device__ __forceinline__ void gh_slice(const ShardArgs& S, const Cached& C, int64_t p0, int64_t p1, HeadRegs& H,
+                                         double& gs, double& hs, int& err) {
+    const int2* __restrict__ pairs = S.pairs;
+    EraRec* era = S.era;
+    SubjRec* subj = S.subj;
+    int n[kCached];
+#pragma unroll
+    for (int v = 0; v < kCached; ++v) {
+        if (C.slot[v].head) {
+            const double2 xl = *reinterpret_cast<const double2*>(era + C.slot[v].pr.x);
+            H.xb[v] = xl.x;
+            H.le[v] = xl.y;
+            H.len[v] = era[C.slot[v].pr.x].len;
+            const SubjRec sr = subj[C.slot[v].pr.y];
+            H.den[v] = sr.den;
+            n[v] = sr.n;
+        }
+    }
+#pragma unroll
+    for (int v = 0; v < kCached; ++v) {
+        if (C.slot[v].head) {
+            double num = H.le[v];
+            if (C.slot[v].cont) {
+                const int64_t p = p0 + static_cast<int64_t>(v) * kSweepThreads + threadIdx.x;
+                num = run_tail_numerator(pairs, era, p + 1, p1, C.slot[v].pr.y, num);
+            }
+            run_terms(num, H.den[v], n[v], gs, hs, err);
+        }
+    }
+    // streamed remainder
+    for (int64_t base = p0 + static_cast<int64_t>(kCached) * kSweepThreads; base < p1; base += kSweepThreads) {
+        const int64_t p = base + threadIdx.x;
+        const PairSlot s = load_slot(pairs, p, p0, p1);
+        if (s.head) {
+            const double le = era[s.pr.x].le;
+            const SubjRec sr = subj[s.pr.y];
+            double num = le;
+            if (s.cont) num = run_tail_numerator(pairs, era, p + 1, p1, s.pr.y, num);
+            run_terms(num, sr.den, sr.n, gs, hs, err);
+        }
+    }
+}
+
+__device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C, const HeadRegs& H, bool cached,
+                                             int64_t p0, int64_t p1, double d, int& err, double& errv) {
+    const int2* __restrict__ pairs = S.pairs;
+    EraRec* era = S.era;
+    SubjRec* subj = S.subj;
+    if (cached) {
+#pragma unroll
+        for (int v = 0; v < kCached; ++v) {
+            if (C.slot[v].head) {
+                const int64_t p = p0 + static_cast<int64_t>(v) * kSweepThreads + threadIdx.x;
+                double den = update_era(era, C.slot[v].pr.x, H.xb[v], H.le[v], H.len[v], d, H.den[v], err, errv);
+                if (C.slot[v].cont) den = run_tail_update(pairs, era, p + 1, p1, C.slot[v].pr.y, d, den, err, errv);
+                subj[C.slot[v].pr.y].den = den;
+            }
+        }
+    }
+    const int64_t start = cached ? p0 + static_cast<int64_t>(kCached) * kSweepThreads : p0;
+    for (int64_t base = start; base < p1; base += kSweepThreads) {
+        const int64_t p = base + threadIdx.x;
+        const PairSlot s = load_slot(pairs, p, p0, p1);
+        if (s.head) {
+            const double2 xl = *reinterpret_cast<const double2*>(era + s.pr.x);
+            const int len = era[s.pr.x].len;
+            double den = subj[s.pr.y].den;
+            den = update_era(era, s.pr.x, xl.x, xl.y, len, d, den, err, errv);
+            if (s.cont) den = run_tail_update(pairs, era, p + 1, p1, s.pr.y, d, den, err, errv);
+            subj[s.pr.y].den = den;
+        }
+    }
+}
+
+__device__ __forceinline__ void load_cached(const ShardArgs& S, int64_t p0, int64_t p1, Cached& C) {
+#pragma unroll
+    for (int v = 0; v < kCached; ++v) {
+        const int64_t p = p0 + static_cast<int64_t>(v) * kSweepThreads + threadIdx.x;
+        C.slot[v] = load_slot(S.pairs, p, p0, p1);
+    }
+}
+
+__device__ __forceinline__ bool visited(const SweepArgs& A, const ShardArgs& S, int j) {
+    return A.col_nonempty[j] != 0 || S.beta[j] != 0.0;
+}
+
+__device__ __forceinline__ int coord_at(const SweepArgs& A, int idx) { return A.order ? A.order[idx] : idx; }
+
+__global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant__ SweepArgs A) {
+    __shared__ Smem sm;
+    int si = 0;
+    while (si + 1 < A.nsh && static_cast<int>(blockIdx.x) >= A.sh[si + 1].cta_begin) ++si;
+    const ShardArgs& S = A.sh[si];
+    const int c = static_cast<int>(blockIdx.x) - S.cta_begin;
+    const int pid = S.pid_base + c;
+    const int64_t* split_c = S.split + c;
+    const int stride = S.ctas + 1;
+    unsigned long long seq = *A.counter;
+    int err = 0;
+    double errv = 0.0;
+    Cached C;
+    HeadRegs H;
+
+    if (A.mode == kModeUpdate) {
+        const int j = A.single_j;
+        const int64_t p0 = split_c[static_cast<int64_t>(j) * stride], p1 = split_c[static_cast<int64_t>(j) * stride + 1];
+        update_slice(S, C, H, false, p0, p1, A.single_delta, err, errv);
+        if (err) record_error(S.err, err, errv);
+        if (c == 0 && threadIdx.x == 0) S.beta[j] = __dadd_rn(S.beta[j], A.single_delta);
+        return;
+    }
+
+    if (A.mode == kModeGradHess) {
+        const int j = A.single_j;
+        const int64_t p0 = split_c[static_cast<int64_t>(j) * stride], p1 = split_c[static_cast<int64_t>(j) * stride + 1];
+        load_cached(S, p0, p1, C);
+        double gs = 0.0, hs = 0.0;
+        gh_slice(S, C, p0, p1, H, gs, hs, err);
+        if (err) record_error(S.err, err, 0.0);
+        block_reduce(gs, hs, err, sm);
+        double tg, th;
+        int te;
+        exchange(A, pid, seq, gs, hs, err, tg, th, te, sm);
+        ++seq;
+        if (c == 0 && threadIdx.x == 0) {
+            S.res->g = __dsub_rn(A.y_dot_x[j], tg);
+            S.res->h = th == 0.0 ? 0.0 : -th;
+            S.res->err_remote = te;
+            if (si == 0) *A.counter = seq;
+        }
+        return;
+    }
+
+    // ---- one full cycle -------------------------------------------------
+    long long nvisit = 0, nmoved = 0;
+    double abytes = 0.0; // SURVEY §8(d) byte model, tracked by CTA 0
+    int idx = 0;
+    while (idx < A.J && !visited(A, S, coord_at(A, idx))) ++idx;
+    int j = idx < A.J ? coord_at(A, idx) : 0;
+    int64_t p0 = 0, p1 = 0;
+    if (idx < A.J) {
+        p0 = split_c[static_cast<int64_t>(j) * stride];
+        p1 = split_c[static_cast<int64_t>(j) * stride + 1];
+        load_cached(S, p0, p1, C);
+    }
+    bool aborted = false;
+    while (idx < A.J) {
+        const double bj = S.beta[j];
+        const double rj = S.trust[j];
+        const double ydx = A.y_dot_x[j];
+        double gs = 0.0, hs = 0.0;
+        gh_slice(S, C, p0, p1, H, gs, hs, err);
+        if (err) record_error(S.err, err, errv);
+        // The publish below must not be observable before this coordinate's
+        // beta/trust loads complete (CTA 0 overwrites them after the
+        // exchange): folding them into the published error word makes the
+        // record store data-dependent on the loads.
+        int e = err | ((bj != bj) || (rj != rj) ? 1 : 0);
+        block_reduce(gs, hs, e, sm);
+        // prefetch the next visited coordinate's index slice while the
+        // partials travel
+        int nidx = idx + 1;
+        while (nidx < A.J && !visited(A, S, coord_at(A, nidx))) ++nidx;
+        const int nj = nidx < A.J ? coord_at(A, nidx) : 0;
+        int64_t np0 = 0, np1 = 0;
+        Cached N;
+        if (nidx < A.J) {
+            np0 = split_c[static_cast<int64_t>(nj) * stride];
+            np1 = split_c[static_cast<int64_t>(nj) * stride + 1];
+            load_cached(S, np0, np1, N);
+        }
+        double tg, th;
+        int te;
+        exchange(A, pid, seq, gs, hs, e, tg, th, te, sm);
+        ++seq;
+        if (te) { // an overflow or bad denominator somewhere: stop everywhere
+            aborted = true;
+            if (c == 0 && threadIdx.x == 0) S.res->err_remote = 1;
+            break;
+        }
+        const double g = __dsub_rn(ydx, tg);
+        const double h = th == 0.0 ? 0.0 : -th;
+        double step = 0.0;
+        const int serr = penalized_step(A.prior, bj, g, h, &step);
+        if (serr) {
+            if (c == 0 && threadIdx.x == 0) record_error(S.err, serr, h);
+            aborted = true;
+            break;
+        }
+        const double delta = clamp_step(step, rj);
+        ++nvisit;
+        const double nnzj = static_cast<double>(S.col_ptr[j + 1] - S.col_ptr[j]);
+        const double runj = static_cast<double>(S.col_runs[j]);
+        abytes += 16.0 * nnzj + 12.0 * runj;
+        if (delta != 0.0) abytes += 28.0 * nnzj + 8.0 * runj;
+        double bnew = bj;
+        if (delta != 0.0) {
+            if (!isfinite(delta)) {
+                if (c == 0 && threadIdx.x == 0) record_error(S.err, DERR_STEP_NONFINITE, delta);
+                aborted = true;
+                break;
+            }
+            ++nmoved;
+            update_slice(S, C, H, true, p0, p1, delta, err, errv);
+            bnew = __dadd_rn(bj, delta);
+        }
+        if (c == 0 && threadIdx.x == 0) {
+            S.beta[j] = bnew;
+            S.trust[j] = next_trust(delta, rj);
+        }
+        __syncthreads(); // slice writes of this coordinate before the next reads
+        idx = nidx;
+        j = nj;
+        p0 = np0;
+        p1 = np1;
+        C = N;
+    }
+
+    if (!aborted) {
+        // criterion (solver.hpp:154-165) over the CTA's eras, snapshot for
+        // the next cycle taken in the same pass
+        const int e0 = S.cta_era[c], e1 = S.cta_era[c + 1];
+        double ch = 0.0, mg = 0.0;
+        for (int k = e0 + static_cast<int>(threadIdx.x); k < e1; k += kSweepThreads) {
+            EraRec* r = S.era + k;
+            const double xb = r->xb;
+            ch = __dadd_rn(ch, fabs(__dsub_rn(xb, r->snap)));
+            if (A.normalized) mg = __dadd_rn(mg, fabs(xb));
+            r->snap = xb;
+        }
+        if (err) record_error(S.err, err, errv);
+        int e = err;
+        block_reduce(ch, mg, e, sm);
+        double tch, tmg;
+        int te;
+        exchange(A, pid, seq, ch, mg, e, tch, tmg, te, sm);
+        ++seq;
+        if (c == 0 && threadIdx.x == 0) {
+            S.res->change = tch;
+            S.res->magnitude = tmg;
+            S.res->criterion = A.normalized ? tch / (1.0 + tmg) : tch;
+            S.res->err_remote = te;
+        }
+    } else if (err) {
+        record_error(S.err, err, errv);
+    }
+    if (c == 0 && threadIdx.x == 0) {
+        S.res->visited = nvisit;
+        S.res->alg_bytes = abytes + (aborted ? 0.0 : 32.0 * static_cast<double>(S.K));
+        S.res->moved = nmoved;
+        S.res->counter = seq;
+        if (si == 0) *A.counter = seq;
+    }
+}
+
+// ---- dense kernels ---------------------------------------------------------
+
+__global__ void k_init_records(EraRec* era, SubjRec* subj, const int32_t* len, const int32_t* y, const int32_t* n,
+                               int32_t K, int32_t N) {
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < K;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        EraRec r;
+        r.xb = 0.0;
+        r.le = 0.0;
+        r.snap = 0.0;
+        r.len = len[k];
+        r.y = y[k];
+        era[k] = r;
+    }
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < N;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        SubjRec s;
+        s.den = 0.0;
+        s.n = n[i];
+        s.pad = 0;
+        subj[i] = s;
+    }
+}
+
+// xbeta_k = sum over drugs of row k in ascending j of beta_j, skipping
+// zeros (engine.hpp:173-181); then l*exp with the overflow guard
+// (engine.hpp:70-79).  snapshot := xbeta.
+__global__ void k_dense_xb(EraRec* era, const int64_t* __restrict__ csr_ptr, const int32_t* __restrict__ csr_col,
+                           const double* __restrict__ beta, int32_t K, DevErr* err) {
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < K;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double xb = 0.0;
+        for (int64_t q = csr_ptr[k]; q < csr_ptr[k + 1]; ++q) {
+            const double b = beta[csr_col[q]];
+            if (b != 0.0) xb = __dadd_rn(xb, b);
+        }
+        if (!(fabs(xb) <= kXbBound)) record_error(err, DERR_OVERFLOW, fabs(xb));
+        const int len = era[k].len;
+        const double le = __dmul_rn(static_cast<double>(len), exp(xb));
+        double2* rec = reinterpret_cast<double2*>(era + k);
+        rec[0] = make_double2(xb, le);
+        era[k].snap = xb;
+    }
+}
+
+__global__ void k_dense_den(const EraRec* era, SubjRec* subj, const int32_t* __restrict__ off, int32_t N) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < N;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double total = 0.0;
+        for (int32_t k = off[i]; k < off[i + 1]; ++k) total = __dadd_rn(total, era[k].le);
+        subj[i].den = total;
+    }
+}
+
+__global__ void k_snapshot(EraRec* era, int32_t K) {
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < K;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        era[k].snap = era[k].xb;
+}
+
+__global__ void k_ll_partial(const EraRec* era, const SubjRec* subj, int32_t K, int32_t N, double* partial,
+                             DevErr* err) {
+    double lin = 0.0, lg = 0.0;
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < K;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int y = era[k].y;
+        if (y != 0) lin = __dadd_rn(lin, __dmul_rn(static_cast<double>(y), era[k].xb));
+    }
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < N;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const SubjRec s = subj[i];
+        if (!(s.den > 0.0)) record_error(err, DERR_LL_DEN_NONPOSITIVE, s.den);
+        lg = __dadd_rn(lg, __dmul_rn(static_cast<double>(s.n), log(s.den)));
+    }
+    __shared__ double sa[kLLThreads / 32], sb[kLLThreads / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lin = __dadd_rn(lin, __shfl_xor_sync(0xffffffffu, lin, o));
+        lg = __dadd_rn(lg, __shfl_xor_sync(0xffffffffu, lg, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        sa[threadIdx.x >> 5] = lin;
+        sb[threadIdx.x >> 5] = lg;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double x = 0.0, y = 0.0;
+        for (int w = 0; w < kLLThreads / 32; ++w) {
+            x = __dadd_rn(x, sa[w]);
+            y = __dadd_rn(y, sb[w]);
+        }
+        partial[2 * blockIdx.x] = x;
+        partial[2 * blockIdx.x + 1] = y;
+    }
+}
+
+__global__ void k_ll_final(const double* partial, int n, DevResult* res) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double x = 0.0, y = 0.0;
+        for (int b = 0; b < n; ++b) {
+            x = __dadd_rn(x, partial[2 * b]);
+            y = __dadd_rn(y, partial[2 * b + 1]);
+        }
+        res->ll_linear = x;
+        res->ll_logden = y;
+    }
+}
+
+// ---- dataset build kernels -------------------------------------------------
+
+__global__ void k_interleave(const int32_t* rows, const int32_t* subjects, int2* pairs, int64_t nnz) {
+    for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < nnz;
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        pairs[p] = make_int2(rows[p], subjects[p]);
+}
+
+// column of every pair (upper_bound on col_ptr), row histogram, and the
+// structural checks of build_dataset (dataset.hpp:135-175): row in range,
+// subject in range and owning the row, rows strictly ascending in a column.
+__global__ void k_pair_meta(const int2* pairs, const int64_t* __restrict__ col_ptr, int32_t J,
+                            const int32_t* __restrict__ off, int32_t N, int32_t K, int64_t nnz, int32_t* col_of,
+                            unsigned long long* row_cnt, int* bad) {
+    for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < nnz;
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        int lo = 0, hi = J; // first j with col_ptr[j+1] > p
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (col_ptr[mid + 1] > p) hi = mid;
+            else lo = mid + 1;
+        }
+        col_of[p] = lo;
+        const int2 pr = pairs[p];
+        bool ok = pr.x >= 0 && pr.x < K && pr.y >= 0 && pr.y < N;
+        if (ok) ok = off[pr.y] <= pr.x && pr.x < off[pr.y + 1];
+        if (ok && p > col_ptr[lo]) ok = pairs[p - 1].x < pr.x;
+        if (!ok) {
+            atomicExch(bad, 1);
+        } else {
+            atomicAdd(row_cnt + pr.x, 1ull);
+        }
+    }
+}
+
+__global__ void k_subject_weight(const int32_t* off, const int64_t* csr_ptr, int32_t N, long long* w) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < N;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int32_t a = off[i], b = off[i + 1];
+        w[i] = static_cast<long long>(b - a) + (csr_ptr[b] - csr_ptr[a]);
+    }
+}
+
+// cta_subj[c] = first subject whose exclusive weight prefix >= ceil(total*c/C)
+__global__ void k_cta_bounds(const long long* excl, int32_t N, int C, const int32_t* off, int32_t* cta_subj,
+                             int32_t* cta_era) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c > C) return;
+    const long long total = excl[N];
+    int s;
+    if (c == C) {
+        s = N;
+    } else {
+        const long long target = (total * c + C - 1) / C;
+        int lo = 0, hi = N;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (excl[mid] >= target) hi = mid;
+            else lo = mid + 1;
+        }
+        s = lo;
+    }
+    cta_subj[c] = s;
+    cta_era[c] = off[s];
+}
+
+__global__ void k_split(const int2* pairs, const int64_t* col_ptr, int32_t J, const int32_t* cta_subj, int C,
+                        int64_t* split) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t >= static_cast<int64_t>(J) * (C + 1)) return;
+    const int j = static_cast<int>(t / (C + 1));
+    const int c = static_cast<int>(t % (C + 1));
+    int64_t lo = col_ptr[j], hi = col_ptr[j + 1];
+    const int target = cta_subj[c];
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (pairs[mid].y >= target) hi = mid;
+        else lo = mid + 1;
+    }
+    split[t] = lo;
+}
+
+// subject runs per column (heads of the CSC pair list)
+__global__ void k_col_runs(const int2* pairs, const int64_t* col_ptr, int32_t* runs, int J) {
+    const int j = blockIdx.x;
+    if (j >= J) return;
+    __shared__ int part[256];
+    int acc = 0;
+    for (int64_t p = col_ptr[j] + threadIdx.x; p < col_ptr[j + 1]; p += blockDim.x)
+        acc += (p == col_ptr[j] || pairs[p - 1].y != pairs[p].y) ? 1 : 0;
+    part[threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int i = 0; i < static_cast<int>(blockDim.x); ++i) t += part[i];
+        runs[j] = t;
+    }
+}
+
+__global__ void k_ydotx(const int2* pairs, const int64_t* col_ptr, const int32_t* y, double* out, int J) {
+    const int j = blockIdx.x;
+    if (j >= J) return;
+    __shared__ long long part[256];
+    long long acc = 0;
+    for (int64_t p = col_ptr[j] + threadIdx.x; p < col_ptr[j + 1]; p += blockDim.x) acc += y[pairs[p].x];
+    part[threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long t = 0;
+        for (int i = 0; i < static_cast<int>(blockDim.x); ++i) t += part[i];
+        out[j] = static_cast<double>(t);
+    }
+}
+
+int grid_for(int64_t n, int threads, int dev_sms) {
+    const int64_t g = (n + threads - 1) / threads;
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(g, static_cast<int64_t>(dev_sms) * 32)));
+}
+
+template <typename T>
+T* dalloc(int64_t count, int64_t& bytes) {
+    T* p = nullptr;
+    if (count <= 0) count = 1;
+    CUDA_TRY(cudaMalloc(&p, sizeof(T) * static_cast<size_t>(count)));
+    bytes += static_cast<int64_t>(sizeof(T)) * count;
+    return p;
+}
+
+int sm_count(int device) {
+    int n = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device));
+    return n;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        CUDA_TRY(cudaGetDevice(&prev));
+        if (prev != dev) CUDA_TRY(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+void sync_and_check(bsccs_state* st) {
+    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    CUDA_TRY(cudaGetLastError());
+}
+
+void check_err_block(bsccs_state* st) {
+    DevErr e;
+    CUDA_TRY(cudaMemcpyAsync(&e, st->err, sizeof e, cudaMemcpyDeviceToHost, st->stream));
+    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    if (e.code != 0) {
+        CUDA_TRY(cudaMemsetAsync(st->err, 0, sizeof(DevErr), st->stream));
+        CUDA_TRY(cudaStreamSynchronize(st->stream));
+        throw_device_error(e.code, e.value);
+    }
+}
+
+int build_grid(int device) { return sm_count(device) * 8; }
+
+} // namespace
+
+void throw_device_error(int code, double value) {
+    char buf[256];
+    switch (code) {
+    case DERR_OVERFLOW:
+        std::snprintf(buf, sizeof buf,
+                      "linear predictor overflow: |x'beta| reached %f (bound 700.000000); the fit has diverged",
+                      value);
+        numeric_error(buf);
+    case DERR_DEN_NONPOSITIVE:
+        internal_error("fused reduction: nonpositive subject denominator");
+    case DERR_STEP_NONFINITE:
+        numeric_error("sparse_delta_update: non-finite step");
+    case DERR_FLAT_NO_PRIOR:
+        numeric_error("undefined Newton step: flat likelihood direction with no prior");
+    case DERR_POS_CURVATURE:
+        internal_error("penalized_step: positive likelihood curvature");
+    case DERR_LL_DEN_NONPOSITIVE:
+        internal_error("log_likelihood: nonpositive subject denominator");
+    default:
+        std::snprintf(buf, sizeof buf, "device error code %d", code);
+        internal_error(buf);
+    }
+}
+
+int default_ctas(int device) {
+    // one persistent CTA per SM (launch bounds force 1 resident CTA of 512)
+    int per_sm = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ccd, kSweepThreads, 0));
+    if (per_sm < 1) internal_error("sweep kernel cannot be resident");
+    return sm_count(device);
+}
+
+// ---------------------------------------------------------------------------
+bsccs_dataset* dataset_create(int32_t N, int32_t K, int32_t J, int64_t nnz, const int32_t* subject_offsets,
+                              const int32_t* events_per_subject, const int32_t* era_lengths,
+                              const int32_t* event_counts, const int64_t* col_ptr, const int32_t* rows,
+                              const int32_t* subjects, const int64_t* y_dot_x_global,
+                              const int64_t* col_nnz_global, int device, int ctas_override) {
+    if (N < 1) input_error("dataset: no subjects");
+    if (K < 1 || J < 1 || nnz < 0) input_error("dataset: invalid sizes");
+    if (!subject_offsets || !events_per_subject || !era_lengths || !event_counts || !col_ptr)
+        input_error("dataset: null array");
+    if (nnz > 0 && (!rows || !subjects)) input_error("dataset: null pair arrays");
+    // small-array invariants on the host (dataset.hpp:45-60)
+    if (subject_offsets[0] != 0 || subject_offsets[N] != K) input_error("dataset: subject offsets must span [0, num_eras]");
+    for (int32_t i = 0; i < N; ++i)
+        if (subject_offsets[i + 1] <= subject_offsets[i]) input_error("dataset: every subject needs at least one era");
+    if (col_ptr[0] != 0 || col_ptr[J] != nnz) input_error("dataset: column pointers must span [0, nnz]");
+    for (int32_t j = 0; j < J; ++j)
+        if (col_ptr[j + 1] < col_ptr[j]) input_error("dataset: column pointers must be non-decreasing");
+    for (int32_t k = 0; k < K; ++k)
+        if (era_lengths[k] <= 0) input_error("dataset: era length must be positive");
+
+    DeviceGuard g(device);
+    auto* ds = new bsccs_dataset();
+    try {
+        ds->device = device;
+        ds->N = N;
+        ds->K = K;
+        ds->J = J;
+        ds->nnz = nnz;
+        ds->ctas = ctas_override > 0 ? ctas_override : default_ctas(device);
+        const int C = ds->ctas;
+        const int sms = sm_count(device);
+        int64_t& B = ds->device_bytes;
+        cudaStream_t s;
+        CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+
+        ds->pairs = dalloc<int2>(nnz, B);
+        ds->col_ptr = dalloc<int64_t>(J + 1, B);
+        ds->split = dalloc<int64_t>(static_cast<int64_t>(J) * (C + 1), B);
+        ds->cta_era = dalloc<int32_t>(C + 1, B);
+        ds->cta_subj = dalloc<int32_t>(C + 1, B);
+        ds->subject_offsets = dalloc<int32_t>(N + 1, B);
+        ds->events_per_subject = dalloc<int32_t>(N, B);
+        ds->era_lengths = dalloc<int32_t>(K, B);
+        ds->event_counts = dalloc<int32_t>(K, B);
+        ds->csr_ptr = dalloc<int64_t>(static_cast<int64_t>(K) + 1, B);
+        ds->csr_col = dalloc<int32_t>(nnz, B);
+        ds->y_dot_x = dalloc<double>(J, B);
+        ds->col_nonempty = dalloc<uint8_t>(J, B);
+        ds->col_runs = dalloc<int32_t>(J, B);
+
+        CUDA_TRY(cudaMemcpyAsync(ds->col_ptr, col_ptr, sizeof(int64_t) * (J + 1), cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(ds->subject_offsets, subject_offsets, sizeof(int32_t) * (N + 1), cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(ds->events_per_subject, events_per_subject, sizeof(int32_t) * N, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(ds->era_lengths, era_lengths, sizeof(int32_t) * K, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(ds->event_counts, event_counts, sizeof(int32_t) * K, cudaMemcpyHostToDevice, s));
+
+        // scratch for the build: rows, subjects, column ids, sort buffers
+        int64_t scratch_bytes = 0;
+        int32_t* d_rows = dalloc<int32_t>(nnz, scratch_bytes);
+        int32_t* d_subj = dalloc<int32_t>(nnz, scratch_bytes);
+        int32_t* d_col = dalloc<int32_t>(nnz, scratch_bytes);
+        unsigned long long* d_cnt = dalloc<unsigned long long>(static_cast<int64_t>(K) + 1, scratch_bytes);
+        long long* d_w = dalloc<long long>(static_cast<int64_t>(N) + 1, scratch_bytes);
+        long long* d_excl = dalloc<long long>(static_cast<int64_t>(N) + 1, scratch_bytes);
+        int* d_bad = dalloc<int>(1, scratch_bytes);
+        if (nnz > 0) {
+            CUDA_TRY(cudaMemcpyAsync(d_rows, rows, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, s));
+            CUDA_TRY(cudaMemcpyAsync(d_subj, subjects, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, s));
+        }
+        CUDA_TRY(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * (static_cast<size_t>(K) + 1), s));
+        CUDA_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
+        if (nnz > 0) {
+            k_interleave<<<grid_for(nnz, 256, sms), 256, 0, s>>>(d_rows, d_subj, ds->pairs, nnz);
+            k_pair_meta<<<grid_for(nnz, 256, sms), 256, 0, s>>>(ds->pairs, ds->col_ptr, J, ds->subject_offsets, N, K,
+                                                               nnz, d_col, d_cnt, d_bad);
+        }
+        // CSR: exclusive scan of the row histogram, stable sort by row
+        {
+            size_t tmp_bytes = 0;
+            CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_cnt,
+                                                   reinterpret_cast<unsigned long long*>(ds->csr_ptr), K + 1, s));
+            size_t sort_bytes = 0;
+            int end_bit = 1;
+            while ((1ll << end_bit) < static_cast<long long>(K)) ++end_bit;
+            if (nnz > 0)
+                CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, d_rows, d_subj, d_col, ds->csr_col,
+                                                         nnz, 0, end_bit, s));
+            size_t scan2 = 0;
+            CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, scan2, d_w, d_excl, N + 1, s));
+            const size_t tb = std::max(std::max(tmp_bytes, sort_bytes), scan2);
+            void* tmp = nullptr;
+            CUDA_TRY(cudaMalloc(&tmp, std::max<size_t>(tb, 16)));
+            CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, d_cnt,
+                                                   reinterpret_cast<unsigned long long*>(ds->csr_ptr), K + 1, s));
+            if (nnz > 0) {
+                // keys: copy of rows (d_rows is consumed as the key input;
+                // d_subj is free after interleave and receives sorted keys)
+                CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, d_rows, d_subj, d_col, ds->csr_col, nnz, 0,
+                                                         end_bit, s));
+            }
+            // nnz-balanced CTA subject ranges
+            k_subject_weight<<<grid_for(N, 256, sms), 256, 0, s>>>(ds->subject_offsets, ds->csr_ptr, N, d_w);
+            CUDA_TRY(cudaMemsetAsync(d_w + N, 0, sizeof(long long), s));
+            CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, scan2, d_w, d_excl, N + 1, s));
+            k_cta_bounds<<<(C + 1 + 127) / 128, 128, 0, s>>>(d_excl, N, C, ds->subject_offsets, ds->cta_subj,
+                                                             ds->cta_era);
+            k_col_runs<<<J, 256, 0, s>>>(ds->pairs, ds->col_ptr, ds->col_runs, J);
+            const int64_t nsplit = static_cast<int64_t>(J) * (C + 1);
+            k_split<<<static_cast<int>((nsplit + 255) / 256), 256, 0, s>>>(ds->pairs, ds->col_ptr, J, ds->cta_subj,
+                                                                            C, ds->split);
+            if (y_dot_x_global) {
+                std::vector<double> yd(static_cast<size_t>(J));
+                for (int32_t j = 0; j < J; ++j) yd[static_cast<size_t>(j)] = static_cast<double>(y_dot_x_global[j]);
+                CUDA_TRY(cudaMemcpyAsync(ds->y_dot_x, yd.data(), sizeof(double) * J, cudaMemcpyHostToDevice, s));
+                CUDA_TRY(cudaStreamSynchronize(s)); // yd is stack-owned
+            } else {
+                k_ydotx<<<J, 256, 0, s>>>(ds->pairs, ds->col_ptr, ds->event_counts, ds->y_dot_x, J);
+            }
+            CUDA_TRY(cudaStreamSynchronize(s));
+            CUDA_TRY(cudaFree(tmp));
+        }
+        int bad = 0;
+        CUDA_TRY(cudaMemcpy(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost));
+        cudaFree(d_rows);
+        cudaFree(d_subj);
+        cudaFree(d_col);
+        cudaFree(d_cnt);
+        cudaFree(d_w);
+        cudaFree(d_excl);
+        cudaFree(d_bad);
+        CUDA_TRY(cudaStreamDestroy(s));
+        if (bad) input_error("dataset: invalid pair (row/subject out of range, subject not owning its row, "
+                             "or rows not strictly ascending within a column)");
+
+        ds->col_ptr_h.assign(col_ptr, col_ptr + J + 1);
+        ds->col_nonempty_h.resize(static_cast<size_t>(J));
+        for (int32_t j = 0; j < J; ++j) {
+            const int64_t cnt = col_nnz_global ? col_nnz_global[j] : (col_ptr[j + 1] - col_ptr[j]);
+            ds->col_nonempty_h[static_cast<size_t>(j)] = cnt > 0 ? 1 : 0;
+        }
+        CUDA_TRY(cudaMemcpy(ds->col_nonempty, ds->col_nonempty_h.data(), J, cudaMemcpyHostToDevice));
+    } catch (...) {
+        dataset_destroy(ds);
+        throw;
+    }
+    return ds;
+}
+
+void dataset_destroy(bsccs_dataset* ds) {
+    if (!ds) return;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(ds->device);
+    cudaFree(ds->pairs);
+    cudaFree(ds->col_ptr);
+    cudaFree(ds->split);
+    cudaFree(ds->cta_era);
+    cudaFree(ds->cta_subj);
+    cudaFree(ds->subject_offsets);
+    cudaFree(ds->events_per_subject);
+    cudaFree(ds->era_lengths);
+    cudaFree(ds->event_counts);
+    cudaFree(ds->csr_ptr);
+    cudaFree(ds->csr_col);
+    cudaFree(ds->y_dot_x);
+    cudaFree(ds->col_nonempty);
+    cudaFree(ds->col_runs);
+    if (prev >= 0) cudaSetDevice(prev);
+    delete ds;
+}
+
+namespace {
+
+void launch_dense(bsccs_state* st) {
+    const bsccs_dataset* ds = st->ds;
+    const int g = build_grid(ds->device);
+    k_dense_xb<<<g, 256, 0, st->stream>>>(st->era, ds->csr_ptr, ds->csr_col, st->beta, ds->K, st->err);
+    k_dense_den<<<g, 256, 0, st->stream>>>(st->era, st->subj, ds->subject_offsets, ds->N);
+    CUDA_TRY(cudaGetLastError());
+    count_launches(2);
+    st->snap_valid = true;
+}
+
+void alloc_state(bsccs_state* st, const bsccs_dataset* ds) {
+    int64_t b = 0;
+    st->ds = ds;
+    CUDA_TRY(cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking));
+    st->era = dalloc<EraRec>(ds->K, b);
+    st->subj = dalloc<SubjRec>(ds->N, b);
+    st->beta = dalloc<double>(ds->J, b);
+    st->trust = dalloc<double>(ds->J, b);
+    st->order = dalloc<int32_t>(ds->J, b);
+    st->slots = dalloc<unsigned long long>(static_cast<int64_t>(2) * ds->ctas * 4, b);
+    st->counter = dalloc<unsigned long long>(1, b);
+    st->err = dalloc<DevErr>(1, b);
+    st->res = dalloc<DevResult>(1, b);
+    st->scratch = dalloc<double>(2 * kLLBlocks, b);
+    CUDA_TRY(cudaMallocHost(&st->res_h, sizeof(DevResult)));
+    CUDA_TRY(cudaEventCreate(&st->ev0));
+    CUDA_TRY(cudaEventCreate(&st->ev1));
+    CUDA_TRY(cudaMemsetAsync(st->slots, 0, sizeof(unsigned long long) * 2 * ds->ctas * 4, st->stream));
+    CUDA_TRY(cudaMemsetAsync(st->counter, 0, sizeof(unsigned long long), st->stream));
+    CUDA_TRY(cudaMemsetAsync(st->err, 0, sizeof(DevErr), st->stream));
+    CUDA_TRY(cudaMemsetAsync(st->res, 0, sizeof(DevResult), st->stream));
+}
+
+} // namespace
+
+bsccs_state* state_create(const bsccs_dataset* ds, const double* beta_host) {
+    if (!ds) input_error("null dataset");
+    if (beta_host)
+        for (int32_t j = 0; j < ds->J; ++j)
+            if (!std::isfinite(beta_host[j])) input_error("init_state: non-finite coefficient");
+    DeviceGuard g(ds->device);
+    auto* st = new bsccs_state();
+    try {
+        alloc_state(st, ds);
+        const int grid = build_grid(ds->device);
+        k_init_records<<<grid, 256, 0, st->stream>>>(st->era, st->subj, ds->era_lengths, ds->event_counts,
+                                                     ds->events_per_subject, ds->K, ds->N);
+        count_launches(1);
+        if (beta_host)
+            CUDA_TRY(cudaMemcpyAsync(st->beta, beta_host, sizeof(double) * ds->J, cudaMemcpyHostToDevice, st->stream));
+        else
+            CUDA_TRY(cudaMemsetAsync(st->beta, 0, sizeof(double) * ds->J, st->stream));
+        launch_dense(st);
+        sync_and_check(st);
+        check_err_block(st);
+    } catch (...) {
+        state_destroy(st);
+        throw;
+    }
+    return st;
+}
+
+bsccs_state* state_clone(const bsccs_state* src) {
+    const bsccs_dataset* ds = src->ds;
+    DeviceGuard g(ds->device);
+    auto* st = new bsccs_state();
+    try {
+        alloc_state(st, ds);
+        CUDA_TRY(cudaStreamSynchronize(src->stream));
+        CUDA_TRY(cudaMemcpyAsync(st->era, src->era, sizeof(EraRec) * ds->K, cudaMemcpyDeviceToDevice, st->stream));
+        CUDA_TRY(cudaMemcpyAsync(st->subj, src->subj, sizeof(SubjRec) * ds->N, cudaMemcpyDeviceToDevice, st->stream));
+        CUDA_TRY(cudaMemcpyAsync(st->beta, src->beta, sizeof(double) * ds->J, cudaMemcpyDeviceToDevice, st->stream));
+        st->snap_valid = src->snap_valid;
+        sync_and_check(st);
+    } catch (...) {
+        state_destroy(st);
+        throw;
+    }
+    return st;
+}
+
+void state_destroy(bsccs_state* st) {
+    if (!st) return;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    if (st->ds) cudaSetDevice(st->ds->device);
+    if (st->stream) cudaStreamSynchronize(st->stream);
+    cudaFree(st->era);
+    cudaFree(st->subj);
+    cudaFree(st->beta);
+    cudaFree(st->trust);
+    cudaFree(st->order);
+    cudaFree(st->slots);
+    cudaFree(st->counter);
+    cudaFree(st->err);
+    cudaFree(st->res);
+    cudaFree(st->scratch);
+    if (st->res_h) cudaFreeHost(st->res_h);
+    if (st->ev0) cudaEventDestroy(st->ev0);
+    if (st->ev1) cudaEventDestroy(st->ev1);
+    if (st->stream) cudaStreamDestroy(st->stream);
+    if (prev >= 0) cudaSetDevice(prev);
+    delete st;
+}
+
+void dense_recompute(bsccs_state* st, const double* beta_host) {
+    const bsccs_dataset* ds = st->ds;
+    if (beta_host)
+        for (int32_t j = 0; j < ds->J; ++j)
+            if (!std::isfinite(beta_host[j])) input_error("dense_recompute: non-finite coefficient");
+    DeviceGuard g(ds->device);
+    if (beta_host)
+        CUDA_TRY(cudaMemcpyAsync(st->beta, beta_host, sizeof(double) * ds->J, cudaMemcpyHostToDevice, st->stream));
+    launch_dense(st);
+    sync_and_check(st);
+    check_err_block(st);
+}
+
+namespace {
+
+SweepArgs base_args(const ExchangePlan& plan) {
+    SweepArgs a;
+    std::memset(&a, 0, sizeof a);
+    if (plan.shards.empty() || plan.shards.size() > static_cast<size_t>(kMaxLocalShards))
+        internal_error("exchange plan: bad shard count");
+    int begin = 0;
+    for (size_t i = 0; i < plan.shards.size(); ++i) {
+        bsccs_state* st = plan.shards[i];
+        ShardArgs& s = a.sh[i];
+        s.pairs = st->ds->pairs;
+        s.col_ptr = st->ds->col_ptr;
+        s.col_runs = st->ds->col_runs;
+        s.K = st->ds->K;
+        s.split = st->ds->split;
+        s.cta_era = st->ds->cta_era;
+        s.era = st->era;
+        s.subj = st->subj;
+        s.beta = st->beta;
+        s.trust = st->trust;
+        s.err = st->err;
+        s.res = st->res;
+        s.ctas = st->ds->ctas;
+        s.cta_begin = begin;
+        s.pid_base = plan.participant_base + begin;
+        begin += s.ctas;
+    }
+    a.nsh = static_cast<int>(plan.shards.size());
+    const bsccs_state* s0 = plan.shards[0];
+    a.order = s0->order_identity ? nullptr : s0->order;
+    a.y_dot_x = s0->ds->y_dot_x;
+    a.col_nonempty = s0->ds->col_nonempty;
+    a.J = s0->ds->J;
+    if (plan.dst.empty() || plan.dst.size() > static_cast<size_t>(kMaxRanks)) internal_error("exchange plan: bad peers");
+    for (size_t d = 0; d < plan.dst.size(); ++d) a.dst[d] = plan.dst[d];
+    a.ndst = static_cast<int>(plan.dst.size());
+    a.slots = plan.local_slots;
+    a.P = plan.total_participants;
+    a.counter = plan.counter;
+    if (a.P > kMaxPollWarps * 32 * kRecPerLane) internal_error("exchange plan: too many participants");
+    return a;
+}
+
+int plan_ctas(const ExchangePlan& plan) {
+    int n = 0;
+    for (auto* st : plan.shards) n += st->ds->ctas;
+    return n;
+}
+
+void launch_ccd(const ExchangePlan& plan, SweepArgs& a) {
+    bsccs_state* s0 = plan.shards[0];
+    void* params[] = {&a};
+    CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_ccd), dim3(plan_ctas(plan)), dim3(kSweepThreads),
+                                         params, 0, s0->stream));
+    count_launches(1);
+}
+
+ExchangePlan single_plan(bsccs_state* st) {
+    ExchangePlan p;
+    p.shards = {st};
+    p.dst = {st->slots};
+    p.local_slots = st->slots;
+    p.counter = st->counter;
+    p.total_participants = st->ds->ctas;
+    p.participant_base = 0;
+    return p;
+}
+
+} // namespace
+
+void grad_hess(bsccs_state* st, int32_t j, double* g, double* h) {
+    const bsccs_dataset* ds = st->ds;
+    if (j < 0 || j >= ds->J) input_error("fused_grad_hess: coordinate out of range");
+    DeviceGuard dg(ds->device);
+    ExchangePlan plan = single_plan(st);
+    SweepArgs a = base_args(plan);
+    a.mode = kModeGradHess;
+    a.single_j = j;
+    launch_ccd(plan, a);
+    CUDA_TRY(cudaMemcpyAsync(st->res_h, st->res, sizeof(DevResult), cudaMemcpyDeviceToHost, st->stream));
+    sync_and_check(st);
+    check_err_block(st);
+    *g = st->res_h->g;
+    *h = st->res_h->h;
+}
+
+void sparse_update(bsccs_state* st, int32_t j, double delta) {
+    const bsccs_dataset* ds = st->ds;
+    if (j < 0 || j >= ds->J) input_error("sparse_delta_update: coordinate out of range");
+    if (!std::isfinite(delta)) numeric_error("sparse_delta_update: non-finite step");
+    if (delta == 0.0) return;
+    DeviceGuard dg(ds->device);
+    ExchangePlan plan = single_plan(st);
+    SweepArgs a = base_args(plan);
+    a.mode = kModeUpdate;
+    a.single_j = j;
+    a.single_delta = delta;
+    launch_ccd(plan, a);
+    st->snap_valid = false;
+    sync_and_check(st);
+    check_err_block(st);
+}
+
+double log_likelihood(bsccs_state* st) {
+    const bsccs_dataset* ds = st->ds;
+    DeviceGuard dg(ds->device);
+    k_ll_partial<<<kLLBlocks, kLLThreads, 0, st->stream>>>(st->era, st->subj, ds->K, ds->N, st->scratch, st->err);
+    k_ll_final<<<1, 32, 0, st->stream>>>(st->scratch, kLLBlocks, st->res);
+    count_launches(2);
+    CUDA_TRY(cudaMemcpyAsync(st->res_h, st->res, sizeof(DevResult), cudaMemcpyDeviceToHost, st->stream));
+    sync_and_check(st);
+    check_err_block(st);
+    return st->res_h->ll_linear - st->res_h->ll_logden;
+}
+
+void state_get(bsccs_state* st, double* beta, double* xbeta, double* le, double* den) {
+    const bsccs_dataset* ds = st->ds;
+    DeviceGuard dg(ds->device);
+    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    if (beta) CUDA_TRY(cudaMemcpy(beta, st->beta, sizeof(double) * ds->J, cudaMemcpyDeviceToHost));
+    if (xbeta || le) {
+        std::vector<EraRec> e(static_cast<size_t>(ds->K));
+        CUDA_TRY(cudaMemcpy(e.data(), st->era, sizeof(EraRec) * ds->K, cudaMemcpyDeviceToHost));
+        for (int32_t k = 0; k < ds->K; ++k) {
+            if (xbeta) xbeta[k] = e[static_cast<size_t>(k)].xb;
+            if (le) le[k] = e[static_cast<size_t>(k)].le;
+        }
+    }
+    if (den) {
+        std::vector<SubjRec> s(static_cast<size_t>(ds->N));
+        CUDA_TRY(cudaMemcpy(s.data(), st->subj, sizeof(SubjRec) * ds->N, cudaMemcpyDeviceToHost));
+        for (int32_t i = 0; i < ds->N; ++i) den[i] = s[static_cast<size_t>(i)].den;
+    }
+}
+
+void prepare_snapshot(bsccs_state* st) {
+    if (st->snap_valid) return;
+    const bsccs_dataset* ds = st->ds;
+    DeviceGuard dg(ds->device);
+    k_snapshot<<<build_grid(ds->device), 256, 0, st->stream>>>(st->era, ds->K);
+    CUDA_TRY(cudaGetLastError());
+    count_launches(1);
+    st->snap_valid = true;
+}
+
+SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool normalized) {
+    bsccs_state* s0 = plan.shards[0];
+    DeviceGuard dg(s0->ds->device);
+    for (auto* st : plan.shards) {
+        prepare_snapshot(st);
+        if (st->stream != s0->stream) CUDA_TRY(cudaStreamSynchronize(st->stream));
+    }
+    SweepArgs a = base_args(plan);
+    a.mode = kModeSweep;
+    a.prior = prior;
+    a.normalized = normalized ? 1 : 0;
+    CUDA_TRY(cudaEventRecord(s0->ev0, s0->stream));
+    launch_ccd(plan, a);
+    CUDA_TRY(cudaEventRecord(s0->ev1, s0->stream));
+    SweepOutcome out{0.0, 0, 0};
+    for (size_t i = 0; i < plan.shards.size(); ++i) {
+        bsccs_state* st = plan.shards[i];
+        CUDA_TRY(cudaMemcpyAsync(st->res_h, st->res, sizeof(DevResult), cudaMemcpyDeviceToHost, s0->stream));
+    }
+    CUDA_TRY(cudaStreamSynchronize(s0->stream));
+    CUDA_TRY(cudaGetLastError());
+    for (auto* st : plan.shards) {
+        st->snap_valid = true;
+        check_err_block(st);
+    }
+    for (auto* st : plan.shards)
+        if (st->res_h->err_remote) numeric_error("sweep aborted: a device error was raised on another shard");
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, s0->ev0, s0->ev1));
+    s0->sweep_ms += ms;
+    for (auto* st : plan.shards) s0->alg_bytes += st->res_h->alg_bytes;
+    out.criterion = s0->res_h->criterion;
+    out.visited = s0->res_h->visited;
+    out.moved = s0->res_h->moved;
+    return out;
+}
+
+} // namespace bsccs_b200

@@ -1,0 +1,173 @@
+// engine.h -- device-resident dataset / state and the internal engine API.
+//
+// HBM layout:
+//   pairs     int2[nnz]      {row, subject} of every nonzero, CSC order
+//                            (SparseColumn::rows/::subjects interleaved,
+//                            dataset.hpp:38-43) -> one 8-byte load per pair
+//   split     int64[J][C+1]  first pair of column j owned by CTA c; CTAs own
+//                            contiguous subject ranges, so a column's pairs
+//                            split into C contiguous, subject-aligned slices
+//   csr_ptr/  row -> drug list (ascending), built once by a stable radix sort;
+//   csr_col                  gives dense_recompute the reference's per-row
+//                            addition order (engine.hpp:173-181) w/o atomics
+//   EraRec    32 B / era     {x'beta, l*exp(x'beta), snapshot, len, y}: one
+//                            32-byte sector per scattered era access
+//   SubjRec   16 B / subject {denominator, n_i}
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "prior.h"
+#include "status.h"
+
+namespace bsccs_b200 {
+
+struct __align__(32) EraRec {
+    double xb;   // x'_k beta                      (EngineState::xbeta)
+    double le;   // l_k exp(x'_k beta)             (EngineState::l_exp_xbeta)
+    double snap; // criterion snapshot             (SolverState::xbeta_snapshot)
+    int32_t len; // era length l_k                 (Dataset::era_lengths)
+    int32_t y;   // event count y_k                (Dataset::event_counts)
+};
+static_assert(sizeof(EraRec) == 32, "EraRec must be one sector");
+
+struct __align__(16) SubjRec {
+    double den; // sum of le over the subject's eras (EngineState::denominators)
+    int32_t n;  // events_per_subject
+    int32_t pad;
+};
+static_assert(sizeof(SubjRec) == 16, "SubjRec must be 16 bytes");
+
+// Per-state device scalars written by kernels, mirrored to pinned host.
+struct DevResult {
+    double g, h;              // tier-1 grad/hess
+    double criterion;         // last sweep
+    double change, magnitude; // criterion components
+    double ll_linear, ll_logden;
+    double err_value;
+    double alg_bytes; // SURVEY §8(d) bytes of this sweep (this shard)
+    long long visited, moved;
+    unsigned long long counter; // exchange sequence after the launch
+    int err_code;
+    int err_remote; // error seen in the exchange (possibly another shard)
+};
+
+struct DevErr {
+    int code;
+    int pad;
+    double value;
+};
+
+constexpr int kSweepThreads = 512;
+constexpr int kMaxLocalShards = 8;
+constexpr int kMaxRanks = 8;
+
+struct bsccs_dataset_impl;
+} // namespace bsccs_b200
+
+// Opaque handle types of the C ABI.
+struct bsccs_dataset {
+    int device = 0;
+    int32_t N = 0, K = 0, J = 0;
+    int64_t nnz = 0;
+    int ctas = 0;
+    // device arrays
+    int2* pairs = nullptr;
+    int64_t* col_ptr = nullptr;
+    int64_t* split = nullptr;         // [J*(ctas+1)]
+    int32_t* cta_era = nullptr;       // [ctas+1]
+    int32_t* cta_subj = nullptr;      // [ctas+1]
+    int32_t* subject_offsets = nullptr;
+    int32_t* events_per_subject = nullptr;
+    int32_t* era_lengths = nullptr;
+    int32_t* event_counts = nullptr;
+    int64_t* csr_ptr = nullptr;       // [K+1]
+    int32_t* csr_col = nullptr;       // [nnz]
+    double* y_dot_x = nullptr;        // [J] global y_dot_x as double
+    uint8_t* col_nonempty = nullptr;  // [J] global
+    int32_t* col_runs = nullptr;      // [J] subject runs per column (this shard)
+    // host copies of small metadata
+    std::vector<int64_t> col_ptr_h;
+    std::vector<uint8_t> col_nonempty_h;
+    int64_t device_bytes = 0;
+};
+
+struct bsccs_group;
+
+struct bsccs_state {
+    const bsccs_dataset* ds = nullptr;
+    cudaStream_t stream = nullptr;
+    bsccs_b200::EraRec* era = nullptr;
+    bsccs_b200::SubjRec* subj = nullptr;
+    double* beta = nullptr;
+    double* trust = nullptr;
+    int32_t* order = nullptr;
+    // exchange (own slot buffer; a group overrides it)
+    unsigned long long* slots = nullptr; // [2][ctas][4]
+    unsigned long long* counter = nullptr;
+    bsccs_b200::DevErr* err = nullptr;
+    bsccs_b200::DevResult* res = nullptr;   // device
+    bsccs_b200::DevResult* res_h = nullptr; // pinned host mirror
+    double* scratch = nullptr;              // reduction partials
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    double sweep_ms = 0.0;  // accumulated sweep-kernel time
+    double alg_bytes = 0.0; // accumulated algorithmic bytes of the sweeps
+    bool snap_valid = false;
+    bool order_identity = true;
+};
+
+namespace bsccs_b200 {
+
+void cuda_check(cudaError_t e, const char* what);
+void count_launches(int n);
+long long launch_count();
+#define CUDA_TRY(x) ::bsccs_b200::cuda_check((x), #x)
+
+int default_ctas(int device);
+
+// ---- dataset / state -------------------------------------------------------
+bsccs_dataset* dataset_create(int32_t N, int32_t K, int32_t J, int64_t nnz,
+                              const int32_t* subject_offsets, const int32_t* events_per_subject,
+                              const int32_t* era_lengths, const int32_t* event_counts,
+                              const int64_t* col_ptr, const int32_t* rows, const int32_t* subjects,
+                              const int64_t* y_dot_x_global, const int64_t* col_nnz_global,
+                              int device, int ctas_override);
+void dataset_destroy(bsccs_dataset* ds);
+
+bsccs_state* state_create(const bsccs_dataset* ds, const double* beta_host);
+bsccs_state* state_clone(const bsccs_state* src);
+void state_destroy(bsccs_state* st);
+
+// ---- engine ops (all synchronous on the state's stream) -----------------
+void dense_recompute(bsccs_state* st, const double* beta_host); // nullptr: from state beta
+void grad_hess(bsccs_state* st, int32_t j, double* g, double* h);
+void sparse_update(bsccs_state* st, int32_t j, double delta);
+double log_likelihood(bsccs_state* st);
+void state_get(bsccs_state* st, double* beta, double* xbeta, double* le, double* den);
+
+// ---- sweep ---------------------------------------------------------------
+struct SweepOutcome {
+    double criterion;
+    long long visited, moved;
+};
+
+// One cycle over `order` (device array already uploaded, or identity) on a
+// set of shards that exchange through the given slot buffers.
+struct ExchangePlan {
+    std::vector<bsccs_state*> shards;      // local shards (same device)
+    std::vector<unsigned long long*> dst;  // slot buffers to publish into
+    unsigned long long* local_slots;       // slot buffer to poll
+    unsigned long long* counter;           // sequence word (local)
+    int total_participants;                // CTAs across all ranks
+    int participant_base;                  // first participant of shard 0
+};
+
+SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool normalized);
+void prepare_snapshot(bsccs_state* st);
+void throw_device_error(int code, double value);
+
+} // namespace bsccs_b200

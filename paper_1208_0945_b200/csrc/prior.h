@@ -1,0 +1,105 @@
+// prior.h -- penalized Newton step and trust clamp, shared verbatim by the
+// host (C ABI bsccs_penalized_step) and the persistent sweep kernel, so the
+// step every CTA computes from the all-gathered (g, h) is the host's step.
+//
+// Restates prior.hpp:72-122 (penalized_step) and solver.hpp:131-150 (clamp,
+// trust update).  Branch structure and expression forms are kept exactly so
+// that fp64 results are bit-identical to the reference: -(g - beta/v)/(h - 1/v)
+// for Normal; the BBR two-sided rule with an exact -beta on a zero crossing
+// for Laplace; 0/0 -> 0 and g != 0, h == 0 -> numeric error for no prior.
+#pragma once
+
+#ifdef __CUDACC__
+#define BSCCS_HD __host__ __device__ __forceinline__
+#else
+#define BSCCS_HD inline
+#endif
+
+namespace bsccs_b200 {
+
+enum PriorCode { PRIOR_NONE = 0, PRIOR_NORMAL = 1, PRIOR_LAPLACE = 2 };
+
+// Device error codes; the host maps them to bsccs_status.
+enum DevError {
+    DERR_NONE = 0,
+    DERR_OVERFLOW = 1,          // numeric_error  engine.hpp:56-65
+    DERR_DEN_NONPOSITIVE = 2,   // internal_error engine.hpp:116-118
+    DERR_STEP_NONFINITE = 3,    // numeric_error  engine.hpp:210-212
+    DERR_FLAT_NO_PRIOR = 4,     // numeric_error  prior.hpp:77-86
+    DERR_POS_CURVATURE = 5,     // internal_error prior.hpp:73-75
+    DERR_LL_DEN_NONPOSITIVE = 6 // internal_error engine.hpp:418-420
+};
+
+struct PriorParams {
+    int kind;
+    double variance;
+    double laplace_b; // prior.hpp:22-24, computed once on the host
+};
+
+// Returns DERR_NONE or the error code; *out receives the unbounded step.
+BSCCS_HD int penalized_step(const PriorParams& p, double beta_j, double g, double h, double* out) {
+    if (h > 0.0) return DERR_POS_CURVATURE;
+    if (p.kind == PRIOR_NONE) {
+        if (h == 0.0) {
+            if (g == 0.0) {
+                *out = 0.0;
+                return DERR_NONE;
+            }
+            return DERR_FLAT_NO_PRIOR;
+        }
+        *out = -g / h;
+        return DERR_NONE;
+    }
+    if (p.kind == PRIOR_NORMAL) {
+        const double v = p.variance;
+        *out = -(g - beta_j / v) / (h - 1.0 / v);
+        return DERR_NONE;
+    }
+    const double b = p.laplace_b;
+    if (beta_j != 0.0) {
+        if (h == 0.0) {
+            *out = -beta_j;
+            return DERR_NONE;
+        }
+        const double sign = beta_j > 0.0 ? 1.0 : -1.0;
+        const double step = -(g - sign / b) / h;
+        const double landed = beta_j + step;
+        if ((beta_j > 0.0 && landed < 0.0) || (beta_j < 0.0 && landed > 0.0)) {
+            *out = -beta_j;
+            return DERR_NONE;
+        }
+        *out = step;
+        return DERR_NONE;
+    }
+    if (h == 0.0) {
+        *out = 0.0;
+        return DERR_NONE;
+    }
+    double step = -(g - 1.0 / b) / h;
+    if (step > 0.0) {
+        *out = step;
+        return DERR_NONE;
+    }
+    step = -(g + 1.0 / b) / h;
+    if (step < 0.0) {
+        *out = step;
+        return DERR_NONE;
+    }
+    *out = 0.0;
+    return DERR_NONE;
+}
+
+// std::clamp(v, -r, r) (solver.hpp:135): v < lo ? lo : (hi < v ? hi : v).
+BSCCS_HD double clamp_step(double v, double r) {
+    const double lo = -r;
+    return v < lo ? lo : (r < v ? r : v);
+}
+
+// std::max(2|delta|, r/2) (solver.hpp:150): (a < b) ? b : a.
+BSCCS_HD double next_trust(double delta, double r) {
+    const double a = 2.0 * (delta < 0.0 ? -delta : delta);
+    const double b = r / 2.0;
+    return a < b ? b : a;
+}
+
+} // namespace bsccs_b200

@@ -1,0 +1,177 @@
+"""Device engine vs the reference (test_engine.cpp restated, plus the
+golden engine cases generated from the reference).  Tolerances: x'beta is
+bit-exact (same per-row addition order); exp-derived values within 4 ulp
+(CUDA exp vs glibc exp, both <= 1 ulp); reductions within 1e-12 relative
+(the reference's own bound for re-partitioned sums, test_engine.cpp:103-125)."""
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from helpers import ds_from_json, fa, random_beta, random_dataset, rel_gap, toy_dataset
+from paper_1208_0945_b200 import bsccs as B
+
+pytestmark = pytest.mark.gpu
+
+ULP4 = 4 * np.finfo(np.float64).eps
+
+
+def close(a, b, rtol):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    return np.all(np.abs(a - b) <= rtol * np.maximum(1.0, np.maximum(np.abs(a), np.abs(b))))
+
+
+def test_toy_state_at_zero():
+    ds = toy_dataset()
+    st = B.init_state(ds)
+    assert list(st.beta) == [0.0]
+    assert list(st.xbeta) == [0.0, 0.0]
+    assert list(st.l_exp_xbeta) == [1.0, 1.0]
+    assert list(st.denominators) == [2.0]
+    assert B.log_likelihood(ds, st) == pytest.approx(-0.6931471805599453, rel=1e-12)
+
+
+def test_toy_gradient_and_curvature():
+    ds = toy_dataset()
+    st = B.init_state(ds)
+    gh = B.fused_grad_hess(ds, st, 0)
+    assert gh.gradient == pytest.approx(0.5, abs=1e-15)
+    assert gh.hessian == pytest.approx(-0.25, abs=1e-15)
+
+
+def test_unit_sparse_step():
+    ds = toy_dataset()
+    st = B.init_state(ds)
+    B.sparse_delta_update(ds, st, 0, 1.0)
+    assert list(st.beta) == [1.0]
+    assert list(st.xbeta) == [0.0, 1.0]
+    assert st.denominators[0] == pytest.approx(1.0 + np.exp(1.0), rel=1e-15)
+    assert B.log_likelihood(ds, st) == pytest.approx(1.0 - np.log(1.0 + np.exp(1.0)), rel=1e-12)
+    B.dense_recompute(ds, st, [np.log(2.0)])
+    assert B.log_likelihood(ds, st) == pytest.approx(np.log(2.0 / 3.0), rel=1e-12)
+
+
+def test_two_subject_dyadic_exact():
+    recs = [B.SubjectRecord("a", [B.Era(1, 0, [0]), B.Era(1, 1, [])]),
+            B.SubjectRecord("b", [B.Era(1, 0, [0]), B.Era(1, 2, []), B.Era(1, 0, []), B.Era(1, 0, [])])]
+    ds = B.build_dataset(recs, 1)
+    gh = B.fused_grad_hess(ds, B.init_state(ds), 0)
+    assert ds.y_dot_x[0] == 0
+    assert gh.gradient == -1.0
+    assert gh.hessian == -0.625
+
+
+def test_weights_in_unit_interval_and_no_negative_zero(port):
+    rng = B.Rng(31)
+    for trial in range(30):
+        J = rng.uniform_int(1, 8)
+        ds = random_dataset(rng, J, 40)
+        beta = random_beta(rng, J, 1.0)
+        st = B.init_state(ds, beta)
+        ost = port.init_state(ds, beta)
+        for j in range(J):
+            a = B.fused_grad_hess(ds, st, j)
+            assert a.hessian <= 0.0
+            if a.hessian == 0.0:
+                assert not np.signbit(a.hessian)
+            g, h = port.grad_hess(ds, ost, j)
+            assert rel_gap(a.gradient, g) < 1e-12
+            assert rel_gap(a.hessian, h) < 1e-12
+
+
+def test_incremental_drift_bounded():
+    rng = B.Rng(47)
+    ds = random_dataset(rng, 5, 80)
+    st = B.init_state(ds)
+    for _ in range(1000):
+        B.sparse_delta_update(ds, st, rng.uniform_int(0, 4), -0.05 + 0.1 * rng.uniform())
+    fresh = st.copy()
+    B.dense_recompute(ds, fresh)
+    assert np.array_equal(fresh.beta, st.beta)
+    assert close(st.xbeta, fresh.xbeta, 1e-9)
+    assert close(st.l_exp_xbeta, fresh.l_exp_xbeta, 1e-9)
+    assert close(st.denominators, fresh.denominators, 1e-9)
+
+
+def test_zero_step_noop_and_nonfinite_rejected():
+    ds = toy_dataset()
+    st = B.init_state(ds)
+    before = (st.beta, st.xbeta, st.l_exp_xbeta, st.denominators)
+    B.sparse_delta_update(ds, st, 0, 0.0)
+    after = (st.beta, st.xbeta, st.l_exp_xbeta, st.denominators)
+    assert all(np.array_equal(a, b) for a, b in zip(before, after))
+    with pytest.raises(B.NumericError):
+        B.sparse_delta_update(ds, st, 0, float("nan"))
+    with pytest.raises(B.NumericError):
+        B.sparse_delta_update(ds, st, 0, float("inf"))
+
+
+def test_overflow_guard():
+    ds = toy_dataset()
+    with pytest.raises(B.NumericError):
+        B.init_state(ds, [701.0])
+    st = B.init_state(ds, [699.0])
+    with pytest.raises(B.NumericError):
+        B.sparse_delta_update(ds, st, 0, 5.0)
+
+
+def test_covering_drug_exactly_uninformative():
+    recs = [B.SubjectRecord("a", [B.Era(3, 1, [0]), B.Era(2, 0, [0, 1])]),
+            B.SubjectRecord("b", [B.Era(5, 2, [0]), B.Era(1, 1, [0])])]
+    ds = B.build_dataset(recs, 2)
+    rng = B.Rng(59)
+    for _ in range(5):
+        st = B.init_state(ds, random_beta(rng, 2, 1.0))
+        gh = B.fused_grad_hess(ds, st, 0)
+        assert gh.gradient == 0.0 and gh.hessian == 0.0 and not np.signbit(gh.hessian)
+
+
+def test_log_likelihood_additive_over_subjects():
+    rng = B.Rng(61)
+    ds = random_dataset(rng, 3, 30)
+    twice = B.subset_dataset(ds, list(range(ds.num_subjects)) * 2)
+    beta = random_beta(rng, 3, 0.7)
+    a = B.log_likelihood(ds, B.init_state(ds, beta))
+    b = B.log_likelihood(twice, B.init_state(twice, beta))
+    assert rel_gap(2.0 * a, b) < 1e-12
+
+
+def test_golden_engine_cases():
+    for case in load_golden("engine_cases.json"):
+        ds = ds_from_json(case["dataset"])
+        st = B.init_state(ds, fa(case["beta"]))
+        assert np.array_equal(st.xbeta, fa(case["xbeta"]))  # same add order: bit-exact
+        assert close(st.l_exp_xbeta, fa(case["l_exp_xbeta"]), ULP4)
+        assert close(st.denominators, fa(case["denominators"]), ULP4 * 8)
+        for j, (g, h) in enumerate(case["grad_hess"]):
+            gh = B.fused_grad_hess(ds, st, j)
+            assert rel_gap(gh.gradient, float(g)) < 1e-12
+            assert rel_gap(gh.hessian, float(h)) < 1e-12
+        assert rel_gap(B.log_likelihood(ds, st), float(case["log_likelihood"])) < 1e-12
+        for j, d in case["updates"]:
+            B.sparse_delta_update(ds, st, j, float(d))
+        assert np.array_equal(st.beta, fa(case["after"]["beta"]))
+        assert close(st.xbeta, fa(case["after"]["xbeta"]), 1e-15)
+        assert close(st.l_exp_xbeta, fa(case["after"]["l_exp_xbeta"]), 1e-14)
+        assert close(st.denominators, fa(case["after"]["denominators"]), 1e-13)
+        assert rel_gap(B.log_likelihood(ds, st), float(case["ll_after"])) < 1e-12
+
+
+def test_slices_cover_many_ctas():
+    """A dataset with more subjects than CTAs, forcing every CTA to own a
+    slice and runs to cross register-cached tiles."""
+    rng = B.Rng(5)
+    ds = random_dataset(rng, 3, 3000, exposure_prob=0.8)
+    beta = random_beta(rng, 3, 0.8)
+    st = B.init_state(ds, beta)
+    import pyoracle
+    port = pyoracle.Port()
+    ost = port.init_state(ds, beta)
+    for j in range(3):
+        a = B.fused_grad_hess(ds, st, j)
+        g, h = port.grad_hess(ds, ost, j)
+        assert rel_gap(a.gradient, g) < 1e-12 and rel_gap(a.hessian, h) < 1e-12
+    for j, d in [(0, 0.3), (2, -0.2), (1, 0.11)]:
+        B.sparse_delta_update(ds, st, j, d)
+        port.sparse_update(ds, ost, j, d)
+    assert close(st.denominators, ost["denominators"], 1e-13)
+    assert close(st.xbeta, ost["xbeta"], 0.0)

@@ -1,0 +1,213 @@
+"""Device CCD fits vs the reference (test_solver.cpp restated) and vs the
+golden reference fits.  Parity bar (BASELINE.json north_star): beta within
+1e-6 relative (1e-9 absolute for Laplace zeros), log-posterior within 1e-8
+relative, identical cycle count."""
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, load_golden
+from helpers import fa, prior_from, random_dataset, rel_gap, toy_dataset
+from paper_1208_0945_b200 import bsccs as B
+from paper_1208_0945_b200 import datagen
+
+pytestmark = pytest.mark.gpu
+
+
+def assert_parity(res, beta_ref, lp_ref, cycles_ref):
+    beta_ref = np.asarray(beta_ref, float)
+    assert res.cycles_run == cycles_ref
+    zero = beta_ref == 0.0
+    assert np.all(np.abs(res.beta_map[zero]) <= 1e-9)
+    nz = ~zero
+    assert np.all(np.abs(res.beta_map[nz] - beta_ref[nz]) <= 1e-6 * np.abs(beta_ref[nz]))
+    assert abs(res.log_posterior - lp_ref) <= 1e-8 * abs(lp_ref)
+
+
+def toy_ridge_root():
+    lo, hi = 0.0, 1.0
+    for _ in range(200):
+        mid = 0.5 * (lo + hi)
+        if 1.0 / (np.exp(mid) + 1.0) - mid > 0:
+            lo = mid
+        else:
+            hi = mid
+    return 0.5 * (lo + hi)
+
+
+def test_toy_ridge_root():
+    res = B.fit(toy_dataset(), B.normal_prior(1.0), B.SolverConfig(epsilon=1e-6))
+    assert res.converged
+    assert abs(res.beta_map[0] - toy_ridge_root()) <= 1e-4
+
+
+def test_toy_lasso_zero_in_one_cycle():
+    res = B.fit(toy_dataset(), B.laplace_prior(2.0))
+    assert res.converged and res.cycles_run == 1
+    assert res.beta_map[0] == 0.0 and res.final_criterion == 0.0
+
+
+def test_first_unpenalized_cycle_clamped():
+    ds = toy_dataset()
+    cfg = B.SolverConfig()
+    st = B.init_state(ds)
+    solver = B.SolverState(ds, cfg)
+    crit = B.run_cycle(ds, st, solver, B.PriorSpec(), cfg)
+    assert list(st.beta) == [1.0]
+    assert crit == 1.0
+    assert solver.trust[0] == 2.0
+
+
+def test_normalized_criterion():
+    rng = B.Rng(83)
+    ds = random_dataset(rng, 3, 25)
+    raw, norm = B.SolverConfig(), B.SolverConfig(convergence=B.ConvergenceMode.normalized)
+    prior = B.normal_prior(0.5)
+    a, b = B.init_state(ds), B.init_state(ds)
+    r = B.run_cycle(ds, a, B.SolverState(ds, raw), prior, raw)
+    n = B.run_cycle(ds, b, B.SolverState(ds, norm), prior, norm)
+    assert np.array_equal(a.xbeta, b.xbeta)
+    assert n == pytest.approx(r / (1.0 + np.abs(a.xbeta).sum()), rel=1e-12)
+
+
+def test_warm_start_fixed_point():
+    rng = B.Rng(89)
+    for _ in range(5):
+        ds = random_dataset(rng, 4, 30)
+        cfg = B.SolverConfig(epsilon=1e-9, max_cycles=5000)
+        cold = B.fit(ds, B.normal_prior(0.8), cfg)
+        assert cold.converged
+        warm = B.fit(ds, B.normal_prior(0.8), cfg, cold.beta_map)
+        assert warm.converged and warm.cycles_run <= 2
+        assert np.max(np.abs(warm.beta_map - cold.beta_map)) <= 1e-8
+
+
+def test_matches_port_on_random_problems(port):
+    rng = B.Rng(103)
+    for trial in range(12):
+        J = rng.uniform_int(1, 6)
+        ds = random_dataset(rng, J, rng.uniform_int(10, 60))
+        for prior in (B.normal_prior(1.0), B.laplace_prior(0.5)):
+            cfg = B.SolverConfig(epsilon=1e-9, max_cycles=10000)
+            res = B.fit(ds, prior, cfg)
+            o = port.fit(ds, prior, cfg)
+            assert_parity(res, o["beta"], o["log_posterior"], o["cycles_run"])
+
+
+def test_lasso_zeros_are_bitwise():
+    rng = B.Rng(109)
+    zeros = 0
+    for _ in range(8):
+        J = rng.uniform_int(2, 6)
+        ds = random_dataset(rng, J, 25)
+        res = B.fit(ds, B.laplace_prior(0.05))
+        for b in res.beta_map:
+            if b == 0.0:
+                zeros += 1
+            else:
+                assert abs(b) > 1e-12
+    assert zeros > 0
+
+
+def test_missing_drug_skipped():
+    ds = B.build_dataset([B.SubjectRecord("s1", [B.Era(1, 0, []), B.Era(1, 1, [0])])], 2)
+    res = B.fit(ds, B.PriorSpec())
+    assert res.beta_map[1] == 0.0
+
+
+def test_cycle_cap_reports():
+    rng = B.Rng(113)
+    ds = random_dataset(rng, 4, 40)
+    res = B.fit(ds, B.normal_prior(1.0), B.SolverConfig(epsilon=1e-14, max_cycles=2))
+    assert not res.converged and res.cycles_run == 2
+    assert res.final_criterion > 1e-14 and np.isfinite(res.log_posterior)
+
+
+def test_unbounded_unpenalized_stalls():
+    res = B.fit(toy_dataset(), B.PriorSpec(), B.SolverConfig(max_cycles=10000))
+    assert res.converged and res.beta_map[0] > 30.0 and np.isfinite(res.log_posterior)
+    early = B.fit(toy_dataset(), B.PriorSpec(), B.SolverConfig(max_cycles=3))
+    assert not early.converged
+
+
+def test_shuffled_order_reproducible_and_matches_port(port):
+    rng = B.Rng(127)
+    ds = random_dataset(rng, 5, 40)
+    cfg = B.SolverConfig(epsilon=1e-8, max_cycles=5000, random_cycle=True, cycle_seed=22)
+    a = B.fit(ds, B.normal_prior(0.6), cfg)
+    b = B.fit(ds, B.normal_prior(0.6), cfg)
+    assert np.array_equal(a.beta_map, b.beta_map) and a.cycles_run == b.cycles_run
+    o = port.fit(ds, B.normal_prior(0.6), cfg)
+    assert_parity(a, o["beta"], o["log_posterior"], o["cycles_run"])
+
+
+def test_config_mistakes_rejected():
+    ds = toy_dataset()
+    for cfg in (B.SolverConfig(epsilon=0.0), B.SolverConfig(max_cycles=0), B.SolverConfig(trust_init=-1.0),
+                B.SolverConfig(partitions=0), B.SolverConfig(dense_refresh_interval=0)):
+        with pytest.raises(B.InputError):
+            B.fit(ds, B.PriorSpec(), cfg)
+    with pytest.raises(B.InputError):
+        B.fit(ds, B.normal_prior(0.0))
+    with pytest.raises(B.InputError):
+        B.fit(ds, B.normal_prior(1.0), B.SolverConfig(), [0.0, 0.0])
+
+
+def test_oracle_case_golden():
+    g = load_golden("oracle_case.json")
+    ds = datagen.simulate(datagen.oracle_case_config())
+    for fit in g["fits"]:
+        res = B.fit(ds, prior_from(fit["prior"]))
+        assert_parity(res, fa(fit["beta"]), float(fit["log_posterior"]), fit["cycles_run"])
+
+
+def test_oracle_case_first_cycle_trace():
+    g = load_golden("oracle_case.json")
+    ds = datagen.simulate(datagen.oracle_case_config())
+    st = B.init_state(ds)
+    prior = B.normal_prior(0.1)
+    trust = np.ones(ds.num_drugs)
+    for j, (gr, he, d) in enumerate(g["cycle1_trace_normal_0.1"]):
+        gh = B.fused_grad_hess(ds, st, j)
+        assert rel_gap(gh.gradient, float(gr)) < 1e-11
+        assert rel_gap(gh.hessian, float(he)) < 1e-11
+        beta_j = st.beta[j]
+        step = B.penalized_step(prior, beta_j, gh.gradient, gh.hessian)
+        delta = float(np.clip(step, -trust[j], trust[j]))
+        assert rel_gap(delta, float(d)) < 1e-10
+        B.sparse_delta_update(ds, st, j, delta)
+        trust[j] = max(2 * abs(delta), trust[j] / 2)
+
+
+def test_small_suite_golden():
+    for c in load_golden("small_suite.json"):
+        s = c["sim"]
+        cfg = datagen.SimConfig(subjects=s["subjects"], drugs=s["drugs"], min_eras=1, max_eras=6, min_era_length=5,
+                                max_era_length=30, prevalence=[float(s["prevalence"])] * s["drugs"],
+                                true_beta=fa(s["true_beta"]).tolist(), baseline_log_rate_mean=-3.0,
+                                baseline_log_rate_sd=0.4, seed=s["seed"])
+        ds = datagen.simulate(cfg)
+        for fit in c["fits"]:
+            res = B.fit(ds, prior_from(fit["prior"]), B.SolverConfig(epsilon=1e-8, max_cycles=10000))
+            assert_parity(res, fa(fit["beta"]), float(fit["log_posterior"]), fit["cycles_run"])
+
+
+def test_fast_10k_golden():
+    g = load_golden("fast_10k.json")
+    ds = datagen.config_dataset("10k")
+    res = B.fit(ds, prior_from(g["prior"]))
+    assert_parity(res, fa(g["beta"]), float(g["log_posterior"]), g["cycles_run"])
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name,fname", [("1M", "fit_1M_laplace.json"), ("10M", "fit_10M_laplace.json")])
+def test_full_size_golden(name, fname):
+    if not (GOLDEN / fname).exists():
+        pytest.skip(f"{fname} not generated")
+    g = load_golden(fname)
+    ds = datagen.config_dataset(name)
+    assert (ds.num_subjects, ds.num_eras, ds.nnz) == (g["sizes"]["N"], g["sizes"]["K"], g["sizes"]["nnz"])
+    res = B.fit(ds, prior_from(g["prior"]))
+    assert_parity(res, fa(g["beta"]), float(g["log_posterior"]), g["cycles_run"])
+    # repeat: bit-identical (fixed partition => fixed bits)
+    res2 = B.fit(ds, prior_from(g["prior"]))
+    assert np.array_equal(res.beta_map, res2.beta_map) and res.log_posterior == res2.log_posterior
