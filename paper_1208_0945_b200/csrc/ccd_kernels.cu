@@ -96,6 +96,8 @@ struct SweepArgs {
 };
 
 struct Smem {
+    double stage[kCached * kSweepThreads]; // per-pair l*exp (grad/hess) or l*exp delta (update)
+    int ssub[kCached * kSweepThreads];     // per-pair subject of the cached tiles
     double ra[kWarps], rb[kWarps];
     int re[kWarps];
     double pa[kMaxPollWarps], pb[kMaxPollWarps];
@@ -152,24 +154,27 @@ __device__ __forceinline__ void block_reduce(double& a, double& b, int& e, Smem&
 // tag + error bit), so a word is valid on its own and one L2 round trip
 // suffices.  Double-buffered by sequence parity.  Every CTA sums the P
 // records in the same fixed order, so all compute bit-identical totals.
-// (a, b, e) are read from thread 0; totals returned to every thread.
-__device__ __forceinline__ void exchange(const SweepArgs& A, int pid, unsigned long long seq, double a,
-                                         double b, int e, double& ta, double& tb, int& te, Smem& sm) {
+// publish(): thread 0 only.  gather(): all threads (polling warps + barrier).
+__device__ __forceinline__ void publish(const SweepArgs& A, int pid, unsigned long long seq, double a, double b,
+                                        int e) {
     const unsigned tag = tag_of(seq);
     const size_t slot_base = static_cast<size_t>(seq & 1ull) * static_cast<size_t>(A.P) * 4;
-    if (threadIdx.x == 0) {
-        const unsigned long long t =
-            static_cast<unsigned long long>(tag | (e ? 0x80000000u : 0u)) << 32;
-        const unsigned long long ab = static_cast<unsigned long long>(__double_as_longlong(a));
-        const unsigned long long bb = static_cast<unsigned long long>(__double_as_longlong(b));
-        const unsigned long long w0 = t | (ab & 0xffffffffull), w1 = t | (ab >> 32);
-        const unsigned long long w2 = t | (bb & 0xffffffffull), w3 = t | (bb >> 32);
-        const size_t off = slot_base + static_cast<size_t>(pid) * 4;
-        for (int d = 0; d < A.ndst; ++d) {
-            st_vol_v2(A.dst[d] + off, w0, w1);
-            st_vol_v2(A.dst[d] + off + 2, w2, w3);
-        }
+    const unsigned long long t = static_cast<unsigned long long>(tag | (e ? 0x80000000u : 0u)) << 32;
+    const unsigned long long ab = static_cast<unsigned long long>(__double_as_longlong(a));
+    const unsigned long long bb = static_cast<unsigned long long>(__double_as_longlong(b));
+    const unsigned long long w0 = t | (ab & 0xffffffffull), w1 = t | (ab >> 32);
+    const unsigned long long w2 = t | (bb & 0xffffffffull), w3 = t | (bb >> 32);
+    const size_t off = slot_base + static_cast<size_t>(pid) * 4;
+    for (int d = 0; d < A.ndst; ++d) {
+        st_vol_v2(A.dst[d] + off, w0, w1);
+        st_vol_v2(A.dst[d] + off + 2, w2, w3);
     }
+}
+
+__device__ __forceinline__ void gather(const SweepArgs& A, unsigned long long seq, double& ta, double& tb, int& te,
+                                       Smem& sm) {
+    const unsigned tag = tag_of(seq);
+    const size_t slot_base = static_cast<size_t>(seq & 1ull) * static_cast<size_t>(A.P) * 4;
     const int nwp = (A.P + 32 * kRecPerLane - 1) / (32 * kRecPerLane);
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     if (w < nwp) {
@@ -234,6 +239,12 @@ __device__ __forceinline__ void exchange(const SweepArgs& A, int pid, unsigned l
     ta = x;
     tb = y;
     te = z;
+}
+
+__device__ __forceinline__ void exchange(const SweepArgs& A, int pid, unsigned long long seq, double a, double b,
+                                         int e, double& ta, double& tb, int& te, Smem& sm) {
+    if (threadIdx.x == 0) publish(A, pid, seq, a, b, e);
+    gather(A, seq, ta, tb, te, sm);
 }
 
 // Index data of one pair slot: the pair, whether it starts a subject run
@@ -316,44 +327,62 @@ struct Cached {
     PairSlot slot[kCached];
 };
 
-// Grad/hess partial of this CTA's slice [p0, p1) of a column.  The first
-// kCached*T pairs come from prefetched slots and keep their era/subject data
-// in registers for the update; the rest stream tile by tile.
+// Per-lane data of the register-cached tiles (the first kCached*T pairs of
+// the CTA's slice).  Every lane gathers its own era record; run heads also
+// gather the subject record.  Runs are combined from shared memory in
+// ascending pair order, so the head never issues a dependent global load
+// unless its run spills past the cached tiles.
 struct HeadRegs {
     double xb[kCached], le[kCached], den[kCached];
-    int len[kCached];
+    int len[kCached], n[kCached];
 };
 
+__device__ __forceinline__ bool slot_valid(const PairSlot& s) { return s.pr.x >= 0; }
+
 __device__ __forceinline__ void gh_slice(const ShardArgs& S, const Cached& C, int64_t p0, int64_t p1, HeadRegs& H,
-                                         double& gs, double& hs, int& err) {
+                                         double& gs, double& hs, int& err, Smem& sm) {
     const int2* __restrict__ pairs = S.pairs;
     EraRec* era = S.era;
     SubjRec* subj = S.subj;
-    int n[kCached];
+    const int ncached = static_cast<int>(min(p1 - p0, static_cast<int64_t>(kCached) * kSweepThreads));
 #pragma unroll
     for (int v = 0; v < kCached; ++v) {
-        if (C.slot[v].head) {
+        if (slot_valid(C.slot[v])) {
             const double2 xl = *reinterpret_cast<const double2*>(era + C.slot[v].pr.x);
             H.xb[v] = xl.x;
             H.le[v] = xl.y;
             H.len[v] = era[C.slot[v].pr.x].len;
-            const SubjRec sr = subj[C.slot[v].pr.y];
-            H.den[v] = sr.den;
-            n[v] = sr.n;
+            if (C.slot[v].head) {
+                const SubjRec sr = subj[C.slot[v].pr.y];
+                H.den[v] = sr.den;
+                H.n[v] = sr.n;
+            }
         }
     }
+#pragma unroll
+    for (int v = 0; v < kCached; ++v) {
+        const int pos = v * kSweepThreads + static_cast<int>(threadIdx.x);
+        if (slot_valid(C.slot[v])) {
+            sm.stage[pos] = H.le[v];
+            sm.ssub[pos] = C.slot[v].pr.y;
+        }
+    }
+    __syncthreads();
 #pragma unroll
     for (int v = 0; v < kCached; ++v) {
         if (C.slot[v].head) {
             double num = H.le[v];
             if (C.slot[v].cont) {
-                const int64_t p = p0 + static_cast<int64_t>(v) * kSweepThreads + threadIdx.x;
-                num = run_tail_numerator(pairs, era, p + 1, p1, C.slot[v].pr.y, num);
+                const int s = C.slot[v].pr.y;
+                int q = v * kSweepThreads + static_cast<int>(threadIdx.x) + 1;
+                while (q < ncached && sm.ssub[q] == s) num = __dadd_rn(num, sm.stage[q++]);
+                if (q == ncached && p0 + q < p1 && ld_pair(pairs + p0 + q).y == s)
+                    num = run_tail_numerator(pairs, era, p0 + q, p1, s, num);
             }
-            run_terms(num, H.den[v], n[v], gs, hs, err);
+            run_terms(num, H.den[v], H.n[v], gs, hs, err);
         }
     }
-    // streamed remainder
+    // streamed remainder: head threads own their runs
     for (int64_t base = p0 + static_cast<int64_t>(kCached) * kSweepThreads; base < p1; base += kSweepThreads) {
         const int64_t p = base + threadIdx.x;
         const PairSlot s = load_slot(pairs, p, p0, p1);
@@ -368,17 +397,44 @@ __device__ __forceinline__ void gh_slice(const ShardArgs& S, const Cached& C, in
 }
 
 __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C, const HeadRegs& H, bool cached,
-                                             int64_t p0, int64_t p1, double d, int& err, double& errv) {
+                                             int64_t p0, int64_t p1, double d, int& err, double& errv, Smem& sm) {
     const int2* __restrict__ pairs = S.pairs;
     EraRec* era = S.era;
     SubjRec* subj = S.subj;
     if (cached) {
+        const int ncached = static_cast<int>(min(p1 - p0, static_cast<int64_t>(kCached) * kSweepThreads));
+        // every lane updates its own era (engine.hpp:219-229) and stages
+        // fresh - old for its run head
+#pragma unroll
+        for (int v = 0; v < kCached; ++v) {
+            const int pos = v * kSweepThreads + static_cast<int>(threadIdx.x);
+            if (slot_valid(C.slot[v])) {
+                const double updated = __dadd_rn(H.xb[v], d);
+                double diff = 0.0;
+                if (!(fabs(updated) <= kXbBound)) {
+                    err = DERR_OVERFLOW;
+                    errv = fabs(updated);
+                } else {
+                    const double fresh = __dmul_rn(static_cast<double>(H.len[v]), exp(updated));
+                    diff = __dsub_rn(fresh, H.le[v]);
+                    *reinterpret_cast<double2*>(era + C.slot[v].pr.x) = make_double2(updated, fresh);
+                }
+                sm.stage[pos] = diff;
+            }
+        }
+        __syncthreads();
+        // heads apply the run's differences to the denominator in order
 #pragma unroll
         for (int v = 0; v < kCached; ++v) {
             if (C.slot[v].head) {
-                const int64_t p = p0 + static_cast<int64_t>(v) * kSweepThreads + threadIdx.x;
-                double den = update_era(era, C.slot[v].pr.x, H.xb[v], H.le[v], H.len[v], d, H.den[v], err, errv);
-                if (C.slot[v].cont) den = run_tail_update(pairs, era, p + 1, p1, C.slot[v].pr.y, d, den, err, errv);
+                int q = v * kSweepThreads + static_cast<int>(threadIdx.x);
+                double den = __dadd_rn(H.den[v], sm.stage[q++]);
+                if (C.slot[v].cont) {
+                    const int s = C.slot[v].pr.y;
+                    while (q < ncached && sm.ssub[q] == s) den = __dadd_rn(den, sm.stage[q++]);
+                    if (q == ncached && p0 + q < p1 && ld_pair(pairs + p0 + q).y == s)
+                        den = run_tail_update(pairs, era, p0 + q, p1, s, d, den, err, errv);
+                }
                 subj[C.slot[v].pr.y].den = den;
             }
         }
@@ -430,7 +486,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
     if (A.mode == kModeUpdate) {
         const int j = A.single_j;
         const int64_t p0 = split_c[static_cast<int64_t>(j) * stride], p1 = split_c[static_cast<int64_t>(j) * stride + 1];
-        update_slice(S, C, H, false, p0, p1, A.single_delta, err, errv);
+        update_slice(S, C, H, false, p0, p1, A.single_delta, err, errv, sm);
         if (err) record_error(S.err, err, errv);
         if (c == 0 && threadIdx.x == 0) S.beta[j] = __dadd_rn(S.beta[j], A.single_delta);
         return;
@@ -441,7 +497,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         const int64_t p0 = split_c[static_cast<int64_t>(j) * stride], p1 = split_c[static_cast<int64_t>(j) * stride + 1];
         load_cached(S, p0, p1, C);
         double gs = 0.0, hs = 0.0;
-        gh_slice(S, C, p0, p1, H, gs, hs, err);
+        gh_slice(S, C, p0, p1, H, gs, hs, err, sm);
         if (err) record_error(S.err, err, 0.0);
         block_reduce(gs, hs, err, sm);
         double tg, th;
@@ -475,7 +531,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         const double rj = S.trust[j];
         const double ydx = A.y_dot_x[j];
         double gs = 0.0, hs = 0.0;
-        gh_slice(S, C, p0, p1, H, gs, hs, err);
+        gh_slice(S, C, p0, p1, H, gs, hs, err, sm);
         if (err) record_error(S.err, err, errv);
         // The publish below must not be observable before this coordinate's
         // beta/trust loads complete (CTA 0 overwrites them after the
@@ -483,8 +539,9 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         // record store data-dependent on the loads.
         int e = err | ((bj != bj) || (rj != rj) ? 1 : 0);
         block_reduce(gs, hs, e, sm);
-        // prefetch the next visited coordinate's index slice while the
-        // partials travel
+        if (threadIdx.x == 0) publish(A, pid, seq, gs, hs, e);
+        // while the partials travel: prefetch the next visited coordinate's
+        // index slice (read-only data, independent of this update)
         int nidx = idx + 1;
         while (nidx < A.J && !visited(A, S, coord_at(A, nidx))) ++nidx;
         const int nj = nidx < A.J ? coord_at(A, nidx) : 0;
@@ -494,10 +551,12 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             np0 = split_c[static_cast<int64_t>(nj) * stride];
             np1 = split_c[static_cast<int64_t>(nj) * stride + 1];
             load_cached(S, np0, np1, N);
+        } else {
+            load_cached(S, 0, 0, N);
         }
         double tg, th;
         int te;
-        exchange(A, pid, seq, gs, hs, e, tg, th, te, sm);
+        gather(A, seq, tg, th, te, sm);
         ++seq;
         if (te) { // an overflow or bad denominator somewhere: stop everywhere
             aborted = true;
@@ -527,7 +586,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                 break;
             }
             ++nmoved;
-            update_slice(S, C, H, true, p0, p1, delta, err, errv);
+            update_slice(S, C, H, true, p0, p1, delta, err, errv, sm);
             bnew = __dadd_rn(bj, delta);
         }
         if (c == 0 && threadIdx.x == 0) {
