@@ -104,6 +104,9 @@ bsccs_status bsccs_device_info(int32_t device, int32_t* sm_count, int32_t* ctas)
 /* Process-wide count of kernels this library has launched (evidence that
  * the device path ran; bench.py reports it as gpu_launches). */
 int64_t bsccs_launch_count(void);
+/* Profiling hook, not a reference entry point: sweep phases to skip (bit0
+ * grad/hess gathers, bit1 update, bit2 exchange).  0 = normal. */
+void bsccs_debug_set_sweep_flags(int32_t flags);
 
 /* ---- dataset (dataset.hpp:53-68 Dataset / SparseColumn) ---------------
  * Flat CSC form of bsccs::Dataset: column j's pairs are

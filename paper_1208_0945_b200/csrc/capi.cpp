@@ -252,6 +252,10 @@ const char* bsccs_last_error(void) { return g_last_error.c_str(); }
 
 int64_t bsccs_launch_count(void) { return launch_count(); }
 
+// Profiling hook (not part of the reference surface): phases of the sweep
+// kernel to skip -- bit0 grad/hess gathers, bit1 update, bit2 exchange.
+void bsccs_debug_set_sweep_flags(int32_t flags) { set_debug_flags(flags); }
+
 bsccs_status bsccs_device_info(int32_t device, int32_t* sms, int32_t* ctas) {
     return guard([&] {
         int n = 0;

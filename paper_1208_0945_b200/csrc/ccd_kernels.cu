@@ -93,6 +93,7 @@ struct SweepArgs {
     const unsigned long long* slots;
     int P;
     unsigned long long* counter;
+    int dbg; // profiling only: bit0 skip grad/hess loads, bit1 skip update, bit2 skip exchange
 };
 
 struct Smem {
@@ -531,7 +532,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         const double rj = S.trust[j];
         const double ydx = A.y_dot_x[j];
         double gs = 0.0, hs = 0.0;
-        gh_slice(S, C, p0, p1, H, gs, hs, err, sm);
+        if (!(A.dbg & 1)) gh_slice(S, C, p0, p1, H, gs, hs, err, sm);
         if (err) record_error(S.err, err, errv);
         // The publish below must not be observable before this coordinate's
         // beta/trust loads complete (CTA 0 overwrites them after the
@@ -539,7 +540,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         // record store data-dependent on the loads.
         int e = err | ((bj != bj) || (rj != rj) ? 1 : 0);
         block_reduce(gs, hs, e, sm);
-        if (threadIdx.x == 0) publish(A, pid, seq, gs, hs, e);
+        if (threadIdx.x == 0 && !(A.dbg & 4)) publish(A, pid, seq, gs, hs, e);
         // while the partials travel: prefetch the next visited coordinate's
         // index slice (read-only data, independent of this update)
         int nidx = idx + 1;
@@ -556,8 +557,19 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         }
         double tg, th;
         int te;
-        gather(A, seq, tg, th, te, sm);
-        ++seq;
+        if (A.dbg & 4) {
+            if (threadIdx.x == 0) {
+                sm.pa[0] = gs;
+                sm.pb[0] = hs;
+            }
+            __syncthreads();
+            tg = sm.pa[0];
+            th = sm.pb[0];
+            te = 0;
+        } else {
+            gather(A, seq, tg, th, te, sm);
+            ++seq;
+        }
         if (te) { // an overflow or bad denominator somewhere: stop everywhere
             aborted = true;
             if (c == 0 && threadIdx.x == 0) S.res->err_remote = 1;
@@ -586,7 +598,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                 break;
             }
             ++nmoved;
-            update_slice(S, C, H, true, p0, p1, delta, err, errv, sm);
+            if (!(A.dbg & 2)) update_slice(S, C, H, true, p0, p1, delta, err, errv, sm);
             bnew = __dadd_rn(bj, delta);
         }
         if (c == 0 && threadIdx.x == 0) {
@@ -1382,6 +1394,11 @@ void prepare_snapshot(bsccs_state* st) {
     st->snap_valid = true;
 }
 
+namespace {
+int g_debug_flags = 0;
+}
+void set_debug_flags(int f) { g_debug_flags = f; }
+
 SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool normalized) {
     bsccs_state* s0 = plan.shards[0];
     DeviceGuard dg(s0->ds->device);
@@ -1391,6 +1408,7 @@ SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool 
     }
     SweepArgs a = base_args(plan);
     a.mode = kModeSweep;
+    a.dbg = g_debug_flags;
     a.prior = prior;
     a.normalized = normalized ? 1 : 0;
     CUDA_TRY(cudaEventRecord(s0->ev0, s0->stream));

@@ -168,6 +168,7 @@ struct ExchangePlan {
 
 SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool normalized);
 void prepare_snapshot(bsccs_state* st);
+void set_debug_flags(int flags); // profiling only
 void throw_device_error(int code, double value);
 
 } // namespace bsccs_b200
