@@ -89,13 +89,8 @@ void fill_trust(FitContext& fc, double trust_init) {
     for (auto* st : fc.states) CUDA_TRY(cudaStreamSynchronize(st->stream));
 }
 
-void upload_order(FitContext& fc, const std::vector<int32_t>& order) {
-    const int32_t J = fc.states[0]->ds->J;
-    for (auto* st : fc.states) {
-        CUDA_TRY(cudaMemcpyAsync(st->order, order.data(), sizeof(int32_t) * J, cudaMemcpyHostToDevice, st->stream));
-        st->order_identity = false;
-    }
-    for (auto* st : fc.states) CUDA_TRY(cudaStreamSynchronize(st->stream));
+void set_order(FitContext& fc, const std::vector<int32_t>& order) {
+    for (auto* st : fc.states) st->order_h = order;
 }
 
 // fit_impl (solver.hpp:170-199) over bound shards.
@@ -110,7 +105,7 @@ void fit_loop(FitContext& fc, const PriorParams& prior, const bsccs_solver_confi
     std::vector<int32_t> order(static_cast<size_t>(J));
     std::iota(order.begin(), order.end(), 0);
     Xoshiro order_rng(cfg->cycle_seed);
-    for (auto* st : fc.states) st->order_identity = true;
+    set_order(fc, {});
 
     res->cycles_run = 0;
     res->converged = 0;
@@ -125,7 +120,7 @@ void fit_loop(FitContext& fc, const PriorParams& prior, const bsccs_solver_confi
                 const size_t r = static_cast<size_t>(order_rng.below(j));
                 std::swap(order[j - 1], order[r]);
             }
-            upload_order(fc, order);
+            set_order(fc, order);
         }
         const SweepOutcome o = run_sweep(fc.plan, prior, cfg->convergence != 0);
         res->final_criterion = o.criterion;
@@ -404,10 +399,9 @@ bsccs_status bsccs_run_cycle(bsccs_state* st, const bsccs_prior* prior, const bs
                     input_error("run_cycle: order must be a permutation of the coordinates");
                 seen[static_cast<size_t>(order[i])] = 1;
             }
-            CUDA_TRY(cudaMemcpyAsync(st->order, order, sizeof(int32_t) * J, cudaMemcpyHostToDevice, st->stream));
-            st->order_identity = false;
+            st->order_h.assign(order, order + J);
         } else {
-            st->order_identity = true;
+            st->order_h.clear();
         }
         CUDA_TRY(cudaMemcpyAsync(st->trust, trust, sizeof(double) * J, cudaMemcpyHostToDevice, st->stream));
         ExchangePlan plan;

@@ -52,7 +52,7 @@ constexpr int kModeGradHess = 1;
 constexpr int kModeUpdate = 2;
 constexpr int kCached = 2;          // register-cached tiles of the slice
 constexpr int kWarps = kSweepThreads / 32;
-constexpr int kRecPerLane = 4;      // exchange records polled per lane
+constexpr int kRecPerLane = 2;      // exchange records polled per lane
 constexpr int kMaxPollWarps = kWarps;
 constexpr int kLLBlocks = 592;      // fixed => deterministic LL reduction
 constexpr int kLLThreads = 256;
@@ -60,6 +60,7 @@ constexpr double kXbBound = 700.0;  // xbeta_bound<double> engine.hpp:20-23
 
 struct ShardArgs {
     const int2* pairs;
+    const longlong2* vsplit; // [ctas][nvisit] (p0, p1) of each CTA's slice in visit order
     const int64_t* col_ptr;
     const int32_t* col_runs;
     const int64_t* split;
@@ -79,7 +80,8 @@ struct ShardArgs {
 struct SweepArgs {
     ShardArgs sh[kMaxLocalShards];
     int nsh;
-    const int32_t* order; // nullptr: ascending
+    const int32_t* visit; // coordinates of this cycle in visit order (skip rule applied)
+    int nvisit;
     const double* y_dot_x;
     const uint8_t* col_nonempty;
     int J;
@@ -257,18 +259,44 @@ struct PairSlot {
     bool cont;
 };
 
-__device__ __forceinline__ PairSlot load_slot(const int2* __restrict__ pairs, int64_t p, int64_t p0, int64_t p1) {
-    PairSlot s;
+// Loads of one pair slot, issued ahead of use: the pair plus (lane 0 / lane
+// 31 only) the subjects just outside the warp.  finalize_slot() turns them
+// into head / continuation flags with warp shuffles; all lanes must call it.
+struct RawSlot {
+    int2 pr;
+    int edge; // lane 0: subject of pair p-1 ; lane 31: subject of pair p+1
+    bool first, last_valid;
+};
+
+__device__ __forceinline__ RawSlot issue_slot(const int2* __restrict__ pairs, int64_t p, int64_t p0, int64_t p1) {
+    RawSlot r;
     const bool valid = p < p1;
-    s.pr = valid ? ld_pair(pairs + p) : make_int2(-1, -1);
     const int l = threadIdx.x & 31;
-    int prev = __shfl_up_sync(0xffffffffu, s.pr.y, 1);
-    int next = __shfl_down_sync(0xffffffffu, s.pr.y, 1);
-    if (l == 0) prev = (valid && p > p0) ? ld_pair(pairs + p - 1).y : -1;
-    if (l == 31) next = (p + 1 < p1) ? ld_pair(pairs + p + 1).y : -1;
-    s.head = valid && (p == p0 || prev != s.pr.y);
-    s.cont = valid && (p + 1 < p1) && next == s.pr.y;
+    r.pr = valid ? ld_pair(pairs + p) : make_int2(-1, -1);
+    r.first = valid && p == p0;
+    r.last_valid = p + 1 < p1;
+    r.edge = -1;
+    if (l == 0 && valid && p > p0) r.edge = ld_pair(pairs + p - 1).y;
+    if (l == 31 && p + 1 < p1) r.edge = ld_pair(pairs + p + 1).y;
+    return r;
+}
+
+__device__ __forceinline__ PairSlot finalize_slot(const RawSlot& r) {
+    PairSlot s;
+    const int l = threadIdx.x & 31;
+    int prev = __shfl_up_sync(0xffffffffu, r.pr.y, 1);
+    int next = __shfl_down_sync(0xffffffffu, r.pr.y, 1);
+    if (l == 0) prev = r.edge;
+    if (l == 31) next = r.edge;
+    const bool valid = r.pr.x >= 0;
+    s.pr = r.pr;
+    s.head = valid && (r.first || prev != r.pr.y);
+    s.cont = valid && r.last_valid && next == r.pr.y;
     return s;
+}
+
+__device__ __forceinline__ PairSlot load_slot(const int2* __restrict__ pairs, int64_t p, int64_t p0, int64_t p1) {
+    return finalize_slot(issue_slot(pairs, p, p0, p1));
 }
 
 // Fused per-run reduction term (engine.hpp:108-129): numerator summed in
@@ -463,11 +491,22 @@ __device__ __forceinline__ void load_cached(const ShardArgs& S, int64_t p0, int6
     }
 }
 
-__device__ __forceinline__ bool visited(const SweepArgs& A, const ShardArgs& S, int j) {
-    return A.col_nonempty[j] != 0 || S.beta[j] != 0.0;
+struct RawCached {
+    RawSlot slot[kCached];
+};
+
+__device__ __forceinline__ void issue_cached(const ShardArgs& S, int64_t p0, int64_t p1, RawCached& R) {
+#pragma unroll
+    for (int v = 0; v < kCached; ++v) {
+        const int64_t p = p0 + static_cast<int64_t>(v) * kSweepThreads + threadIdx.x;
+        R.slot[v] = issue_slot(S.pairs, p, p0, p1);
+    }
 }
 
-__device__ __forceinline__ int coord_at(const SweepArgs& A, int idx) { return A.order ? A.order[idx] : idx; }
+__device__ __forceinline__ void finalize_cached(const RawCached& R, Cached& C) {
+#pragma unroll
+    for (int v = 0; v < kCached; ++v) C.slot[v] = finalize_slot(R.slot[v]);
+}
 
 __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant__ SweepArgs A) {
     __shared__ Smem sm;
@@ -515,102 +554,105 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
     }
 
     // ---- one full cycle -------------------------------------------------
+    // Software pipeline over the visit list: while coordinate idx runs, the
+    // pair slots of idx+1 are in flight (issued after the publish), and the
+    // slice bounds / coordinate ids of idx+2 are loading, so no dependent
+    // metadata load sits on the per-coordinate critical path.
     long long nvisit = 0, nmoved = 0;
     double abytes = 0.0; // SURVEY §8(d) byte model, tracked by CTA 0
-    int idx = 0;
-    while (idx < A.J && !visited(A, S, coord_at(A, idx))) ++idx;
-    int j = idx < A.J ? coord_at(A, idx) : 0;
-    int64_t p0 = 0, p1 = 0;
-    if (idx < A.J) {
-        p0 = split_c[static_cast<int64_t>(j) * stride];
-        p1 = split_c[static_cast<int64_t>(j) * stride + 1];
-        load_cached(S, p0, p1, C);
-    }
+    const int V = A.nvisit;
+    const longlong2* vs = S.vsplit + static_cast<size_t>(c) * static_cast<size_t>(V);
     bool aborted = false;
-    while (idx < A.J) {
-        const double bj = S.beta[j];
-        const double rj = S.trust[j];
-        const double ydx = A.y_dot_x[j];
-        double gs = 0.0, hs = 0.0;
-        if (!(A.dbg & 1)) gh_slice(S, C, p0, p1, H, gs, hs, err, sm);
-        if (err) record_error(S.err, err, errv);
-        // The publish below must not be observable before this coordinate's
-        // beta/trust loads complete (CTA 0 overwrites them after the
-        // exchange): folding them into the published error word makes the
-        // record store data-dependent on the loads.
-        int e = err | ((bj != bj) || (rj != rj) ? 1 : 0);
-        block_reduce(gs, hs, e, sm);
-        if (threadIdx.x == 0 && !(A.dbg & 4)) publish(A, pid, seq, gs, hs, e);
-        // while the partials travel: prefetch the next visited coordinate's
-        // index slice (read-only data, independent of this update)
-        int nidx = idx + 1;
-        while (nidx < A.J && !visited(A, S, coord_at(A, nidx))) ++nidx;
-        const int nj = nidx < A.J ? coord_at(A, nidx) : 0;
-        int64_t np0 = 0, np1 = 0;
-        Cached N;
-        if (nidx < A.J) {
-            np0 = split_c[static_cast<int64_t>(nj) * stride];
-            np1 = split_c[static_cast<int64_t>(nj) * stride + 1];
-            load_cached(S, np0, np1, N);
-        } else {
-            load_cached(S, 0, 0, N);
-        }
-        double tg, th;
-        int te;
-        if (A.dbg & 4) {
-            if (threadIdx.x == 0) {
-                sm.pa[0] = gs;
-                sm.pb[0] = hs;
+    if (V > 0) {
+        longlong2 cur = vs[0];
+        int j = A.visit[0];
+        double bj = S.beta[j], rj = S.trust[j], ydx = A.y_dot_x[j];
+        load_cached(S, cur.x, cur.y, C);
+        longlong2 nxt = V > 1 ? vs[1] : make_longlong2(0, 0);
+        int jn = V > 1 ? A.visit[1] : 0;
+        for (int idx = 0; idx < V; ++idx) {
+            const int64_t p0 = cur.x, p1 = cur.y;
+            double gs = 0.0, hs = 0.0;
+            if (!(A.dbg & 1)) gh_slice(S, C, p0, p1, H, gs, hs, err, sm);
+            if (err) record_error(S.err, err, errv);
+            // The publish below must not be observable before this
+            // coordinate's beta/trust loads complete (CTA 0 overwrites them
+            // after the exchange): folding them into the published error
+            // word makes the record store data-dependent on the loads.
+            int e = err | ((bj != bj) || (rj != rj) ? 1 : 0);
+            block_reduce(gs, hs, e, sm);
+            if (threadIdx.x == 0 && !(A.dbg & 4)) publish(A, pid, seq, gs, hs, e);
+            // while the partials travel: issue the next coordinate's loads
+            RawCached NR;
+            issue_cached(S, nxt.x, nxt.y, NR);
+            const bool more = idx + 1 < V;
+            const double bn = more ? S.beta[jn] : 0.0;
+            const double rn = more ? S.trust[jn] : 1.0;
+            const double yn = more ? A.y_dot_x[jn] : 0.0;
+            const longlong2 nxt2 = idx + 2 < V ? vs[idx + 2] : make_longlong2(0, 0);
+            const int jn2 = idx + 2 < V ? A.visit[idx + 2] : 0;
+            double tg, th;
+            int te;
+            if (A.dbg & 4) {
+                if (threadIdx.x == 0) {
+                    sm.pa[0] = gs;
+                    sm.pb[0] = hs;
+                }
+                __syncthreads();
+                tg = sm.pa[0];
+                th = sm.pb[0];
+                te = 0;
+            } else {
+                gather(A, seq, tg, th, te, sm);
+                ++seq;
             }
-            __syncthreads();
-            tg = sm.pa[0];
-            th = sm.pb[0];
-            te = 0;
-        } else {
-            gather(A, seq, tg, th, te, sm);
-            ++seq;
-        }
-        if (te) { // an overflow or bad denominator somewhere: stop everywhere
-            aborted = true;
-            if (c == 0 && threadIdx.x == 0) S.res->err_remote = 1;
-            break;
-        }
-        const double g = __dsub_rn(ydx, tg);
-        const double h = th == 0.0 ? 0.0 : -th;
-        double step = 0.0;
-        const int serr = penalized_step(A.prior, bj, g, h, &step);
-        if (serr) {
-            if (c == 0 && threadIdx.x == 0) record_error(S.err, serr, h);
-            aborted = true;
-            break;
-        }
-        const double delta = clamp_step(step, rj);
-        ++nvisit;
-        const double nnzj = static_cast<double>(S.col_ptr[j + 1] - S.col_ptr[j]);
-        const double runj = static_cast<double>(S.col_runs[j]);
-        abytes += 16.0 * nnzj + 12.0 * runj;
-        if (delta != 0.0) abytes += 28.0 * nnzj + 8.0 * runj;
-        double bnew = bj;
-        if (delta != 0.0) {
-            if (!isfinite(delta)) {
-                if (c == 0 && threadIdx.x == 0) record_error(S.err, DERR_STEP_NONFINITE, delta);
+            if (te) { // an overflow or bad denominator somewhere: stop everywhere
+                aborted = true;
+                if (c == 0 && threadIdx.x == 0) S.res->err_remote = 1;
+                break;
+            }
+            const double g = __dsub_rn(ydx, tg);
+            const double h = th == 0.0 ? 0.0 : -th;
+            double step = 0.0;
+            const int serr = penalized_step(A.prior, bj, g, h, &step);
+            if (serr) {
+                if (c == 0 && threadIdx.x == 0) record_error(S.err, serr, h);
                 aborted = true;
                 break;
             }
-            ++nmoved;
-            if (!(A.dbg & 2)) update_slice(S, C, H, true, p0, p1, delta, err, errv, sm);
-            bnew = __dadd_rn(bj, delta);
+            const double delta = clamp_step(step, rj);
+            ++nvisit;
+            if (c == 0 && threadIdx.x == 0) {
+                const double nnzj = static_cast<double>(S.col_ptr[j + 1] - S.col_ptr[j]);
+                const double runj = static_cast<double>(S.col_runs[j]);
+                abytes += 16.0 * nnzj + 12.0 * runj;
+                if (delta != 0.0) abytes += 28.0 * nnzj + 8.0 * runj;
+            }
+            double bnew = bj;
+            if (delta != 0.0) {
+                if (!isfinite(delta)) {
+                    if (c == 0 && threadIdx.x == 0) record_error(S.err, DERR_STEP_NONFINITE, delta);
+                    aborted = true;
+                    break;
+                }
+                ++nmoved;
+                if (!(A.dbg & 2)) update_slice(S, C, H, true, p0, p1, delta, err, errv, sm);
+                bnew = __dadd_rn(bj, delta);
+            }
+            if (c == 0 && threadIdx.x == 0) {
+                S.beta[j] = bnew;
+                S.trust[j] = next_trust(delta, rj);
+            }
+            __syncthreads(); // slice writes of this coordinate before the next reads
+            finalize_cached(NR, C);
+            cur = nxt;
+            j = jn;
+            bj = bn;
+            rj = rn;
+            ydx = yn;
+            nxt = nxt2;
+            jn = jn2;
         }
-        if (c == 0 && threadIdx.x == 0) {
-            S.beta[j] = bnew;
-            S.trust[j] = next_trust(delta, rj);
-        }
-        __syncthreads(); // slice writes of this coordinate before the next reads
-        idx = nidx;
-        j = nj;
-        p0 = np0;
-        p1 = np1;
-        C = N;
     }
 
     if (!aborted) {
@@ -838,6 +880,16 @@ __global__ void k_split(const int2* pairs, const int64_t* col_ptr, int32_t J, co
         else lo = mid + 1;
     }
     split[t] = lo;
+}
+
+// (p0, p1) of every CTA's slice, laid out per CTA in visit order
+__global__ void k_build_vsplit(const int64_t* __restrict__ split, const int32_t* __restrict__ visit, int V, int C,
+                               longlong2* vsplit) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t >= static_cast<int64_t>(V) * C) return;
+    const int c = static_cast<int>(t / V), idx = static_cast<int>(t % V);
+    const int64_t* row = split + static_cast<int64_t>(visit[idx]) * (C + 1) + c;
+    vsplit[t] = make_longlong2(row[0], row[1]);
 }
 
 // subject runs per column (heads of the CSC pair list)
@@ -1148,7 +1200,8 @@ void alloc_state(bsccs_state* st, const bsccs_dataset* ds) {
     st->subj = dalloc<SubjRec>(ds->N, b);
     st->beta = dalloc<double>(ds->J, b);
     st->trust = dalloc<double>(ds->J, b);
-    st->order = dalloc<int32_t>(ds->J, b);
+    st->visit = dalloc<int32_t>(ds->J, b);
+    st->vsplit = dalloc<longlong2>(static_cast<int64_t>(ds->J) * ds->ctas, b);
     st->slots = dalloc<unsigned long long>(static_cast<int64_t>(2) * ds->ctas * 4, b);
     st->counter = dalloc<unsigned long long>(1, b);
     st->err = dalloc<DevErr>(1, b);
@@ -1221,7 +1274,8 @@ void state_destroy(bsccs_state* st) {
     cudaFree(st->subj);
     cudaFree(st->beta);
     cudaFree(st->trust);
-    cudaFree(st->order);
+    cudaFree(st->visit);
+    cudaFree(st->vsplit);
     cudaFree(st->slots);
     cudaFree(st->counter);
     cudaFree(st->err);
@@ -1260,6 +1314,7 @@ SweepArgs base_args(const ExchangePlan& plan) {
         bsccs_state* st = plan.shards[i];
         ShardArgs& s = a.sh[i];
         s.pairs = st->ds->pairs;
+        s.vsplit = st->vsplit;
         s.col_ptr = st->ds->col_ptr;
         s.col_runs = st->ds->col_runs;
         s.K = st->ds->K;
@@ -1278,7 +1333,8 @@ SweepArgs base_args(const ExchangePlan& plan) {
     }
     a.nsh = static_cast<int>(plan.shards.size());
     const bsccs_state* s0 = plan.shards[0];
-    a.order = s0->order_identity ? nullptr : s0->order;
+    a.visit = s0->visit;
+    a.nvisit = static_cast<int>(s0->visit_h.size());
     a.y_dot_x = s0->ds->y_dot_x;
     a.col_nonempty = s0->ds->col_nonempty;
     a.J = s0->ds->J;
@@ -1402,10 +1458,43 @@ void set_debug_flags(int f) { g_debug_flags = f; }
 SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool normalized) {
     bsccs_state* s0 = plan.shards[0];
     DeviceGuard dg(s0->ds->device);
+    // visit list of this cycle: order filtered by the skip rule
+    // (solver.hpp:119-121: empty column and beta_j == 0)
+    const bsccs_dataset* ds0 = s0->ds;
+    const int32_t J = ds0->J;
+    bool any_empty = false;
+    for (int32_t j = 0; j < J; ++j) any_empty = any_empty || !ds0->col_nonempty_h[static_cast<size_t>(j)];
+    std::vector<double> beta_h;
+    if (any_empty) {
+        beta_h.resize(static_cast<size_t>(J));
+        CUDA_TRY(cudaMemcpyAsync(beta_h.data(), s0->beta, sizeof(double) * J, cudaMemcpyDeviceToHost, s0->stream));
+        CUDA_TRY(cudaStreamSynchronize(s0->stream));
+    }
+    std::vector<int32_t> visit;
+    visit.reserve(static_cast<size_t>(J));
+    for (int32_t i = 0; i < J; ++i) {
+        const int32_t j = s0->order_h.empty() ? i : s0->order_h[static_cast<size_t>(i)];
+        if (ds0->col_nonempty_h[static_cast<size_t>(j)] || (any_empty && beta_h[static_cast<size_t>(j)] != 0.0))
+            visit.push_back(j);
+    }
     for (auto* st : plan.shards) {
         prepare_snapshot(st);
+        if (!st->visit_valid || st->visit_h != visit) {
+            st->visit_h = visit;
+            st->visit_valid = true;
+            if (!visit.empty()) {
+                CUDA_TRY(cudaMemcpyAsync(st->visit, visit.data(), sizeof(int32_t) * visit.size(),
+                                         cudaMemcpyHostToDevice, st->stream));
+                const int64_t n = static_cast<int64_t>(visit.size()) * st->ds->ctas;
+                k_build_vsplit<<<static_cast<int>((n + 255) / 256), 256, 0, st->stream>>>(
+                    st->ds->split, st->visit, static_cast<int>(visit.size()), st->ds->ctas, st->vsplit);
+                CUDA_TRY(cudaGetLastError());
+                count_launches(1);
+            }
+        }
         if (st->stream != s0->stream) CUDA_TRY(cudaStreamSynchronize(st->stream));
     }
+    if (s0->visit_h.size() != visit.size()) internal_error("visit list mismatch across shards");
     SweepArgs a = base_args(plan);
     a.mode = kModeSweep;
     a.dbg = g_debug_flags;

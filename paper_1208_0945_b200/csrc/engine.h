@@ -105,7 +105,11 @@ struct bsccs_state {
     bsccs_b200::SubjRec* subj = nullptr;
     double* beta = nullptr;
     double* trust = nullptr;
-    int32_t* order = nullptr;
+    int32_t* visit = nullptr;            // [J] this cycle's visit list (device)
+    longlong2* vsplit = nullptr;         // [ctas][J] slice bounds in visit order
+    std::vector<int32_t> order_h;        // visit order (empty = ascending)
+    std::vector<int32_t> visit_h;        // visit list last uploaded
+    bool visit_valid = false;
     // exchange (own slot buffer; a group overrides it)
     unsigned long long* slots = nullptr; // [2][ctas][4]
     unsigned long long* counter = nullptr;
@@ -117,7 +121,6 @@ struct bsccs_state {
     double sweep_ms = 0.0;  // accumulated sweep-kernel time
     double alg_bytes = 0.0; // accumulated algorithmic bytes of the sweeps
     bool snap_valid = false;
-    bool order_identity = true;
 };
 
 namespace bsccs_b200 {
