@@ -52,8 +52,8 @@ constexpr int kModeGradHess = 1;
 constexpr int kModeUpdate = 2;
 constexpr int kCached = 2;          // register-cached tiles of the slice
 constexpr int kWarps = kSweepThreads / 32;
-constexpr int kRecPerLane = 2;      // exchange records polled per lane
-constexpr int kMaxPollWarps = kWarps;
+constexpr int kRecPerLane = 5;      // exchange records polled per lane (one warp covers 160 CTAs)
+constexpr int kMaxPollWarps = 8;
 constexpr int kLLBlocks = 592;      // fixed => deterministic LL reduction
 constexpr int kLLThreads = 256;
 constexpr double kXbBound = 700.0;  // xbeta_bound<double> engine.hpp:20-23
@@ -61,6 +61,7 @@ constexpr double kXbBound = 700.0;  // xbeta_bound<double> engine.hpp:20-23
 struct ShardArgs {
     const int2* pairs;
     const longlong2* vsplit; // [ctas][nvisit] (p0, p1) of each CTA's slice in visit order
+    uint8_t* moved;          // [nvisit] delta != 0 per visited coordinate (CTA 0 writes)
     const int64_t* col_ptr;
     const int32_t* col_runs;
     const int64_t* split;
@@ -107,11 +108,21 @@ struct Smem {
     int pe[kMaxPollWarps];
 };
 
+// Slot accesses: relaxed at GPU scope (the records are self-validating, so no
+// fences are needed; peers on other GPUs would need .sys).
 __device__ __forceinline__ void st_vol_v2(unsigned long long* p, unsigned long long a, unsigned long long b) {
-    asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
 }
 __device__ __forceinline__ void ld_vol_v2(const unsigned long long* p, unsigned long long& a, unsigned long long& b) {
-    asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+__device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
 }
 __device__ __forceinline__ int2 ld_pair(const int2* p) { return __ldg(p); }
 
@@ -171,6 +182,7 @@ __device__ __forceinline__ void publish(const SweepArgs& A, int pid, unsigned lo
     for (int d = 0; d < A.ndst; ++d) {
         st_vol_v2(A.dst[d] + off, w0, w1);
         st_vol_v2(A.dst[d] + off + 2, w2, w3);
+        if (A.dbg & 8) red_release_add(A.dst[d] + static_cast<size_t>(2) * A.P * 4, 1ull);
     }
 }
 
@@ -180,6 +192,14 @@ __device__ __forceinline__ void gather(const SweepArgs& A, unsigned long long se
     const size_t slot_base = static_cast<size_t>(seq & 1ull) * static_cast<size_t>(A.P) * 4;
     const int nwp = (A.P + 32 * kRecPerLane - 1) / (32 * kRecPerLane);
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (A.dbg & 8) { // variant: one thread waits on the arrival counter first
+        if (threadIdx.x == 0) {
+            const unsigned long long target = (seq + 1) * static_cast<unsigned long long>(A.P);
+            while (ld_acquire(A.slots + static_cast<size_t>(2) * A.P * 4) < target) {
+            }
+        }
+        __syncthreads();
+    }
     if (w < nwp) {
         unsigned long long r0[kRecPerLane], r1[kRecPerLane], r2[kRecPerLane], r3[kRecPerLane];
         bool ok[kRecPerLane];
@@ -559,7 +579,6 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
     // slice bounds / coordinate ids of idx+2 are loading, so no dependent
     // metadata load sits on the per-coordinate critical path.
     long long nvisit = 0, nmoved = 0;
-    double abytes = 0.0; // SURVEY §8(d) byte model, tracked by CTA 0
     const int V = A.nvisit;
     const longlong2* vs = S.vsplit + static_cast<size_t>(c) * static_cast<size_t>(V);
     bool aborted = false;
@@ -622,12 +641,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             }
             const double delta = clamp_step(step, rj);
             ++nvisit;
-            if (c == 0 && threadIdx.x == 0) {
-                const double nnzj = static_cast<double>(S.col_ptr[j + 1] - S.col_ptr[j]);
-                const double runj = static_cast<double>(S.col_runs[j]);
-                abytes += 16.0 * nnzj + 12.0 * runj;
-                if (delta != 0.0) abytes += 28.0 * nnzj + 8.0 * runj;
-            }
+            if (c == 0 && threadIdx.x == 0) S.moved[idx] = delta != 0.0 ? 1 : 0;
             double bnew = bj;
             if (delta != 0.0) {
                 if (!isfinite(delta)) {
@@ -685,7 +699,6 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
     }
     if (c == 0 && threadIdx.x == 0) {
         S.res->visited = nvisit;
-        S.res->alg_bytes = abytes + (aborted ? 0.0 : 32.0 * static_cast<double>(S.K));
         S.res->moved = nmoved;
         S.res->counter = seq;
         if (si == 0) *A.counter = seq;
@@ -1144,6 +1157,8 @@ bsccs_dataset* dataset_create(int32_t N, int32_t K, int32_t J, int64_t nnz, cons
                              "or rows not strictly ascending within a column)");
 
         ds->col_ptr_h.assign(col_ptr, col_ptr + J + 1);
+        ds->col_runs_h.resize(static_cast<size_t>(J));
+        CUDA_TRY(cudaMemcpy(ds->col_runs_h.data(), ds->col_runs, sizeof(int32_t) * J, cudaMemcpyDeviceToHost));
         ds->col_nonempty_h.resize(static_cast<size_t>(J));
         for (int32_t j = 0; j < J; ++j) {
             const int64_t cnt = col_nnz_global ? col_nnz_global[j] : (col_ptr[j + 1] - col_ptr[j]);
@@ -1202,7 +1217,8 @@ void alloc_state(bsccs_state* st, const bsccs_dataset* ds) {
     st->trust = dalloc<double>(ds->J, b);
     st->visit = dalloc<int32_t>(ds->J, b);
     st->vsplit = dalloc<longlong2>(static_cast<int64_t>(ds->J) * ds->ctas, b);
-    st->slots = dalloc<unsigned long long>(static_cast<int64_t>(2) * ds->ctas * 4, b);
+    st->slots = dalloc<unsigned long long>(static_cast<int64_t>(2) * ds->ctas * 4 + 16, b);
+    st->moved = dalloc<uint8_t>(ds->J, b);
     st->counter = dalloc<unsigned long long>(1, b);
     st->err = dalloc<DevErr>(1, b);
     st->res = dalloc<DevResult>(1, b);
@@ -1210,7 +1226,7 @@ void alloc_state(bsccs_state* st, const bsccs_dataset* ds) {
     CUDA_TRY(cudaMallocHost(&st->res_h, sizeof(DevResult)));
     CUDA_TRY(cudaEventCreate(&st->ev0));
     CUDA_TRY(cudaEventCreate(&st->ev1));
-    CUDA_TRY(cudaMemsetAsync(st->slots, 0, sizeof(unsigned long long) * 2 * ds->ctas * 4, st->stream));
+    CUDA_TRY(cudaMemsetAsync(st->slots, 0, sizeof(unsigned long long) * (2 * ds->ctas * 4 + 16), st->stream));
     CUDA_TRY(cudaMemsetAsync(st->counter, 0, sizeof(unsigned long long), st->stream));
     CUDA_TRY(cudaMemsetAsync(st->err, 0, sizeof(DevErr), st->stream));
     CUDA_TRY(cudaMemsetAsync(st->res, 0, sizeof(DevResult), st->stream));
@@ -1275,6 +1291,7 @@ void state_destroy(bsccs_state* st) {
     cudaFree(st->beta);
     cudaFree(st->trust);
     cudaFree(st->visit);
+    cudaFree(st->moved);
     cudaFree(st->vsplit);
     cudaFree(st->slots);
     cudaFree(st->counter);
@@ -1315,6 +1332,7 @@ SweepArgs base_args(const ExchangePlan& plan) {
         ShardArgs& s = a.sh[i];
         s.pairs = st->ds->pairs;
         s.vsplit = st->vsplit;
+        s.moved = st->moved;
         s.col_ptr = st->ds->col_ptr;
         s.col_runs = st->ds->col_runs;
         s.K = st->ds->K;
@@ -1508,6 +1526,9 @@ SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool 
         bsccs_state* st = plan.shards[i];
         CUDA_TRY(cudaMemcpyAsync(st->res_h, st->res, sizeof(DevResult), cudaMemcpyDeviceToHost, s0->stream));
     }
+    std::vector<uint8_t> moved(visit.size());
+    if (!visit.empty())
+        CUDA_TRY(cudaMemcpyAsync(moved.data(), s0->moved, visit.size(), cudaMemcpyDeviceToHost, s0->stream));
     CUDA_TRY(cudaStreamSynchronize(s0->stream));
     CUDA_TRY(cudaGetLastError());
     for (auto* st : plan.shards) {
@@ -1519,7 +1540,22 @@ SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool 
     float ms = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&ms, s0->ev0, s0->ev1));
     s0->sweep_ms += ms;
-    for (auto* st : plan.shards) s0->alg_bytes += st->res_h->alg_bytes;
+    // SURVEY §8(d) algorithmic bytes of this sweep, every shard: per visited
+    // coordinate 16*nnz_j + 12*u_j, per moved one + 28*nnz_j + 8*u_j, plus
+    // 32*K for the criterion / snapshot pass
+    const long long nv = s0->res_h->visited;
+    for (auto* st : plan.shards) {
+        const bsccs_dataset* d = st->ds;
+        double bytes = 32.0 * static_cast<double>(d->K);
+        for (long long i = 0; i < nv && i < static_cast<long long>(visit.size()); ++i) {
+            const size_t j = static_cast<size_t>(visit[static_cast<size_t>(i)]);
+            const double nnz = static_cast<double>(d->col_ptr_h[j + 1] - d->col_ptr_h[j]);
+            const double runs = static_cast<double>(d->col_runs_h[j]);
+            bytes += 16.0 * nnz + 12.0 * runs;
+            if (moved[static_cast<size_t>(i)]) bytes += 28.0 * nnz + 8.0 * runs;
+        }
+        s0->alg_bytes += bytes;
+    }
     out.criterion = s0->res_h->criterion;
     out.visited = s0->res_h->visited;
     out.moved = s0->res_h->moved;

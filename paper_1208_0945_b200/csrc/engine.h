@@ -49,7 +49,6 @@ struct DevResult {
     double change, magnitude; // criterion components
     double ll_linear, ll_logden;
     double err_value;
-    double alg_bytes; // SURVEY §8(d) bytes of this sweep (this shard)
     long long visited, moved;
     unsigned long long counter; // exchange sequence after the launch
     int err_code;
@@ -93,6 +92,7 @@ struct bsccs_dataset {
     // host copies of small metadata
     std::vector<int64_t> col_ptr_h;
     std::vector<uint8_t> col_nonempty_h;
+    std::vector<int32_t> col_runs_h;
     int64_t device_bytes = 0;
 };
 
@@ -107,6 +107,7 @@ struct bsccs_state {
     double* trust = nullptr;
     int32_t* visit = nullptr;            // [J] this cycle's visit list (device)
     longlong2* vsplit = nullptr;         // [ctas][J] slice bounds in visit order
+    uint8_t* moved = nullptr;            // [J] moved flag per visited coordinate
     std::vector<int32_t> order_h;        // visit order (empty = ascending)
     std::vector<int32_t> visit_h;        // visit list last uploaded
     bool visit_valid = false;
