@@ -107,6 +107,9 @@ int64_t bsccs_launch_count(void);
 /* Profiling hook, not a reference entry point: sweep phases to skip (bit0
  * grad/hess gathers, bit1 update, bit2 exchange).  0 = normal. */
 void bsccs_debug_set_sweep_flags(int32_t flags);
+/* Profiling hook: host_out == NULL arms per-CTA globaltimer stamps for the
+ * first ncoords coordinates of later sweeps; otherwise copies them out. */
+int32_t bsccs_debug_trace(int32_t ncoords, int32_t ctas, uint64_t* host_out, int64_t words);
 
 /* ---- dataset (dataset.hpp:53-68 Dataset / SparseColumn) ---------------
  * Flat CSC form of bsccs::Dataset: column j's pairs are

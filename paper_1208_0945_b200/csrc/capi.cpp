@@ -250,6 +250,14 @@ int64_t bsccs_launch_count(void) { return launch_count(); }
 // Profiling hook (not part of the reference surface): phases of the sweep
 // kernel to skip -- bit0 grad/hess gathers, bit1 update, bit2 exchange.
 void bsccs_debug_set_sweep_flags(int32_t flags) { set_debug_flags(flags); }
+// Profiling hook: globaltimer stamps (loop top, publish, gather done, update
+// done) of the first `ncoords` coordinates of each subsequent sweep, per CTA.
+int32_t bsccs_debug_trace(int32_t ncoords, int32_t ctas, uint64_t* host_out, int64_t words) {
+    return guard([&] {
+        if (host_out) read_debug_trace(reinterpret_cast<unsigned long long*>(host_out), static_cast<size_t>(words));
+        else set_debug_trace(ncoords, ctas);
+    });
+}
 
 bsccs_status bsccs_device_info(int32_t device, int32_t* sms, int32_t* ctas) {
     return guard([&] {

@@ -97,7 +97,15 @@ struct SweepArgs {
     int P;
     unsigned long long* counter;
     int dbg; // profiling only: bit0 skip grad/hess loads, bit1 skip update, bit2 skip exchange
+    unsigned long long* trace; // profiling only: [ntrace][gridDim][4] globaltimer stamps
+    int ntrace;
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 struct Smem {
     double stage[kCached * kSweepThreads]; // per-pair l*exp (grad/hess) or l*exp delta (update)
@@ -589,8 +597,12 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         load_cached(S, cur.x, cur.y, C);
         longlong2 nxt = V > 1 ? vs[1] : make_longlong2(0, 0);
         int jn = V > 1 ? A.visit[1] : 0;
+        const bool tr = A.trace != nullptr && threadIdx.x == 0;
+        unsigned long long* trb = tr ? A.trace + static_cast<size_t>(blockIdx.x) * 4 : nullptr;
+        const size_t trs = static_cast<size_t>(gridDim.x) * 4;
         for (int idx = 0; idx < V; ++idx) {
             const int64_t p0 = cur.x, p1 = cur.y;
+            if (tr && idx < A.ntrace) trb[idx * trs + 0] = gtimer();
             double gs = 0.0, hs = 0.0;
             if (!(A.dbg & 1)) gh_slice(S, C, p0, p1, H, gs, hs, err, sm);
             if (err) record_error(S.err, err, errv);
@@ -600,6 +612,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             // word makes the record store data-dependent on the loads.
             int e = err | ((bj != bj) || (rj != rj) ? 1 : 0);
             block_reduce(gs, hs, e, sm);
+            if (tr && idx < A.ntrace) trb[idx * trs + 1] = gtimer();
             if (threadIdx.x == 0 && !(A.dbg & 4)) publish(A, pid, seq, gs, hs, e);
             // while the partials travel: issue the next coordinate's loads
             RawCached NR;
@@ -625,6 +638,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                 gather(A, seq, tg, th, te, sm);
                 ++seq;
             }
+            if (tr && idx < A.ntrace) trb[idx * trs + 2] = gtimer();
             if (te) { // an overflow or bad denominator somewhere: stop everywhere
                 aborted = true;
                 if (c == 0 && threadIdx.x == 0) S.res->err_remote = 1;
@@ -658,6 +672,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                 S.trust[j] = next_trust(delta, rj);
             }
             __syncthreads(); // slice writes of this coordinate before the next reads
+            if (tr && idx < A.ntrace) trb[idx * trs + 3] = gtimer();
             finalize_cached(NR, C);
             cur = nxt;
             j = jn;
@@ -1470,8 +1485,26 @@ void prepare_snapshot(bsccs_state* st) {
 
 namespace {
 int g_debug_flags = 0;
+unsigned long long* g_trace = nullptr;
+int g_ntrace = 0;
+size_t g_trace_words = 0;
 }
 void set_debug_flags(int f) { g_debug_flags = f; }
+void set_debug_trace(int ncoords, int ctas) {
+    if (g_trace) cudaFree(g_trace);
+    g_trace = nullptr;
+    g_ntrace = ncoords;
+    g_trace_words = static_cast<size_t>(ncoords) * ctas * 4;
+    if (ncoords > 0) {
+        CUDA_TRY(cudaMalloc(&g_trace, g_trace_words * sizeof(unsigned long long)));
+        CUDA_TRY(cudaMemset(g_trace, 0, g_trace_words * sizeof(unsigned long long)));
+    }
+}
+void read_debug_trace(unsigned long long* host, size_t words) {
+    if (!g_trace) return;
+    CUDA_TRY(cudaMemcpy(host, g_trace, std::min(words, g_trace_words) * sizeof(unsigned long long),
+                        cudaMemcpyDeviceToHost));
+}
 
 SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool normalized) {
     bsccs_state* s0 = plan.shards[0];
@@ -1516,6 +1549,8 @@ SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool 
     SweepArgs a = base_args(plan);
     a.mode = kModeSweep;
     a.dbg = g_debug_flags;
+    a.trace = g_trace;
+    a.ntrace = g_ntrace;
     a.prior = prior;
     a.normalized = normalized ? 1 : 0;
     CUDA_TRY(cudaEventRecord(s0->ev0, s0->stream));

@@ -173,6 +173,8 @@ struct ExchangePlan {
 SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool normalized);
 void prepare_snapshot(bsccs_state* st);
 void set_debug_flags(int flags); // profiling only
+void set_debug_trace(int ncoords, int ctas);
+void read_debug_trace(unsigned long long* host, size_t words);
 void throw_device_error(int code, double value);
 
 } // namespace bsccs_b200

@@ -1,0 +1,53 @@
+"""Per-CTA timeline of the persistent sweep kernel (globaltimer stamps)."""
+import ctypes as C
+import sys
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_1208_0945_b200 import _native, bsccs as B, datagen  # noqa: E402
+
+wl = sys.argv[1] if len(sys.argv) > 1 else "1M"
+flags = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+NT = 300
+ds = datagen.config_dataset(wl)
+dds = B.DeviceDataset(ds, 0)
+ctas = dds.ctas
+lib = _native.lib()
+prior, cfg = B.laplace_prior(0.1), B.SolverConfig()
+st = B.init_state(dds)
+solver = B.SolverState(dds, cfg)
+B.run_cycle(dds, st, solver, prior, cfg)  # warm
+lib.bsccs_debug_set_sweep_flags(flags)
+lib.bsccs_debug_trace(NT, ctas, None, 0)
+B.run_cycle(dds, st, solver, prior, cfg)
+buf = np.zeros(NT * ctas * 4, dtype=np.uint64)
+lib.bsccs_debug_trace(NT, ctas, buf.ctypes.data_as(C.c_void_p), buf.size)
+lib.bsccs_debug_trace(0, ctas, None, 0)
+lib.bsccs_debug_set_sweep_flags(0)
+t = buf.reshape(NT, ctas, 4).astype(np.int64)
+t = t[20:NT - 1]  # skip the start
+t0 = t[:, :, 0]
+pub = t[:, :, 1]
+got = t[:, :, 2]
+done = t[:, :, 3]
+coord = np.diff(t[:, 0, 0])
+print(f"{wl} flags={flags} ctas={ctas}: per-coordinate period (CTA0 loop top) median {np.median(coord):.0f} ns")
+gh = pub - t0
+print(f"  gh+reduce (top->publish) per CTA: median {np.median(gh):.0f}  p90 {np.percentile(gh, 90):.0f}  "
+      f"max-over-CTAs median {np.median(gh.max(1)):.0f} ns")
+last_pub = pub.max(1)
+first_top = t0.min(1)
+print(f"  spread of loop-top across CTAs: median {np.median(t0.max(1) - t0.min(1)):.0f} ns")
+print(f"  last publish -> gather done: median over coords of (median over CTAs) "
+      f"{np.median(np.median(got, 1) - last_pub):.0f}  (max CTA) {np.median(got.max(1) - last_pub):.0f} ns")
+print(f"  first top -> last publish: {np.median(last_pub - first_top):.0f} ns")
+upd = done - got
+print(f"  gather done -> update done: median {np.median(upd):.0f}  max-over-CTAs median {np.median(upd.max(1)):.0f}")
+nxt = t[1:, :, 0] - done[:-1]
+print(f"  update done -> next top (finalize): median {np.median(nxt):.0f}")
+slow = np.argmax(pub, axis=1)
+vals, cnt = np.unique(slow, return_counts=True)
+order = np.argsort(-cnt)[:8]
+print("  most frequent last publisher CTAs:", [(int(vals[i]), int(cnt[i])) for i in order])
