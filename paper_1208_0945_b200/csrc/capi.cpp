@@ -469,8 +469,8 @@ bsccs_status bsccs_fit(const bsccs_dataset* ds, const bsccs_prior* prior, const 
 // ---- groups ----------------------------------------------------------------
 
 int64_t bsccs_group_slot_bytes(int32_t total_ctas) {
-    // [2 parities][P][4 words] records + arrival counter (+ padding)
-    return (static_cast<int64_t>(2) * total_ctas * 4 + 16) * static_cast<int64_t>(sizeof(unsigned long long));
+    (void)total_ctas; // the fixed-point exchange area does not grow with P
+    return static_cast<int64_t>(kXchgAreaWords) * static_cast<int64_t>(sizeof(unsigned long long));
 }
 
 bsccs_status bsccs_group_create_local(bsccs_dataset* const* shards, int32_t n, bsccs_group** out) {

@@ -52,8 +52,6 @@ constexpr int kModeGradHess = 1;
 constexpr int kModeUpdate = 2;
 constexpr int kCached = 2;          // register-cached tiles of the slice
 constexpr int kWarps = kSweepThreads / 32;
-constexpr int kRecPerLane = 5;      // exchange records polled per lane (one warp covers 160 CTAs)
-constexpr int kMaxPollWarps = 8;
 constexpr int kLLBlocks = 592;      // fixed => deterministic LL reduction
 constexpr int kLLThreads = 256;
 constexpr double kXbBound = 700.0;  // xbeta_bound<double> engine.hpp:20-23
@@ -112,24 +110,18 @@ struct Smem {
     int ssub[kCached * kSweepThreads];     // per-pair subject of the cached tiles
     double ra[kWarps], rb[kWarps];
     int re[kWarps];
-    double pa[kMaxPollWarps], pb[kMaxPollWarps];
-    int pe[kMaxPollWarps];
+    double pa[1], pb[1];
+    int pe[1];
 };
 
-// Slot accesses: relaxed at GPU scope (the records are self-validating, so no
-// fences are needed; peers on other GPUs would need .sys).
-__device__ __forceinline__ void st_vol_v2(unsigned long long* p, unsigned long long a, unsigned long long b) {
-    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+// Exchange words: relaxed at GPU scope (each word validates itself, so no
+// fences are needed; peers on other GPUs would use .sys).
+__device__ __forceinline__ void red_add(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ void ld_vol_v2(const unsigned long long* p, unsigned long long& a, unsigned long long& b) {
-    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
-}
-__device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned long long v) {
-    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
     unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
 __device__ __forceinline__ int2 ld_pair(const int2* p) { return __ldg(p); }
@@ -138,9 +130,6 @@ __device__ __forceinline__ void record_error(DevErr* e, int code, double value) 
     if (atomicCAS(&e->code, 0, code) == 0) e->value = value;
 }
 
-__device__ __forceinline__ unsigned tag_of(unsigned long long seq) {
-    return static_cast<unsigned>(1ull + seq % 0x7fffffffull);
-}
 
 // Reduce (a, b, e) over the CTA; result valid in thread 0.
 __device__ __forceinline__ void block_reduce(double& a, double& b, int& e, Smem& sm) {
@@ -171,116 +160,130 @@ __device__ __forceinline__ void block_reduce(double& a, double& b, int& e, Smem&
     }
 }
 
-// All-gather of one 2-double record per participant, LL-protocol style:
-// every 8-byte word carries 32 data bits and the 32-bit tag (31-bit sequence
-// tag + error bit), so a word is valid on its own and one L2 round trip
-// suffices.  Double-buffered by sequence parity.  Every CTA sums the P
-// records in the same fixed order, so all compute bit-identical totals.
-// publish(): thread 0 only.  gather(): all threads (polling warps + barrier).
-__device__ __forceinline__ void publish(const SweepArgs& A, int pid, unsigned long long seq, double a, double b,
-                                        int e) {
-    const unsigned tag = tag_of(seq);
-    const size_t slot_base = static_cast<size_t>(seq & 1ull) * static_cast<size_t>(A.P) * 4;
-    const unsigned long long t = static_cast<unsigned long long>(tag | (e ? 0x80000000u : 0u)) << 32;
-    const unsigned long long ab = static_cast<unsigned long long>(__double_as_longlong(a));
-    const unsigned long long bb = static_cast<unsigned long long>(__double_as_longlong(b));
-    const unsigned long long w0 = t | (ab & 0xffffffffull), w1 = t | (ab >> 32);
-    const unsigned long long w2 = t | (bb & 0xffffffffull), w3 = t | (bb >> 32);
-    const size_t off = slot_base + static_cast<size_t>(pid) * 4;
+// Order-independent all-reduce of two non-negative doubles per participant.
+//
+// Each participant splits its partial exactly into three 42-bit limbs of a
+// 2^-80 fixed-point number and issues seven relaxed red.add.u64 (six limbs
+// plus an error word) into the exchange area of every destination; each word
+// also gains 2^50 per arrival.  A poller knows a word is complete when its
+// growth since the previous use of that buffer carries P arrivals in the
+// bits above 2^50 -- every word validates itself, no fences or flags.  The
+// integer sum is associative, so every CTA reconstructs the bit-identical,
+// correctly rounded exact sum of the partials whatever the arrival order.
+// Words sit 256 B apart so the 148 adds per word land on distinct L2 slices;
+// two buffers alternate by sequence parity.
+constexpr int kXStride = 32; // u64 words between exchange words (256 B)
+constexpr int kXWords = 7;
+constexpr int kXBase = 2 * kXWords * kXStride; // running totals at launch end
+constexpr unsigned long long kXCnt = 1ull << 50;
+constexpr unsigned long long kXData = kXCnt - 1;
+constexpr unsigned long long kM42 = (1ull << 42) - 1;
+
+__device__ __forceinline__ bool to_limbs(double v, unsigned long long& l0, unsigned long long& l1,
+                                         unsigned long long& l2) {
+    if (!(v >= 0.0 && v < 0x1p46)) {
+        l0 = l1 = l2 = 0;
+        return false;
+    }
+    const double t2 = floor(__dmul_rn(v, 0x1p-4));
+    const double r = __dsub_rn(v, __dmul_rn(t2, 16.0)); // exact, [0, 16)
+    const double s1 = __dmul_rn(r, 0x1p38);
+    const double t1 = floor(s1);
+    const double r0 = __dsub_rn(s1, t1); // exact, [0, 1)
+    l2 = static_cast<unsigned long long>(t2);
+    l1 = static_cast<unsigned long long>(t1);
+    l0 = static_cast<unsigned long long>(floor(__dmul_rn(r0, 0x1p42)));
+    return true;
+}
+
+__device__ __forceinline__ double from_limbs(unsigned long long L0, unsigned long long L1, unsigned long long L2) {
+    L1 += L0 >> 42;
+    L0 &= kM42;
+    L2 += L1 >> 42;
+    L1 &= kM42;
+    const unsigned __int128 V = (static_cast<unsigned __int128>(L2) << 84) |
+                                (static_cast<unsigned __int128>(L1) << 42) | static_cast<unsigned __int128>(L0);
+    if (V == 0) return 0.0;
+    const unsigned long long hi = static_cast<unsigned long long>(V >> 64), lo = static_cast<unsigned long long>(V);
+    const int lz = hi ? __clzll(static_cast<long long>(hi)) : 64 + __clzll(static_cast<long long>(lo));
+    const unsigned __int128 W = V << lz;
+    unsigned long long m = static_cast<unsigned long long>(W >> 64);
+    m |= (static_cast<unsigned long long>(W) != 0ull) ? 1ull : 0ull; // sticky: correct rounding below
+    return ldexp(__ull2double_rn(m), 64 - lz - 80);
+}
+
+// thread 0 only
+__device__ __forceinline__ void publish(const SweepArgs& A, unsigned long long seq, double a, double b, int e) {
+    unsigned long long w[kXWords];
+    const bool ok = to_limbs(a, w[0], w[1], w[2]) && to_limbs(b, w[3], w[4], w[5]);
+    w[6] = (e || !ok) ? 1ull : 0ull;
+    const size_t off = static_cast<size_t>(seq & 1ull) * kXWords * kXStride;
+#pragma unroll
+    for (int i = 0; i < kXWords; ++i) w[i] += kXCnt;
     for (int d = 0; d < A.ndst; ++d) {
-        st_vol_v2(A.dst[d] + off, w0, w1);
-        st_vol_v2(A.dst[d] + off + 2, w2, w3);
-        if (A.dbg & 8) red_release_add(A.dst[d] + static_cast<size_t>(2) * A.P * 4, 1ull);
+#pragma unroll
+        for (int i = 0; i < kXWords; ++i) red_add(A.dst[d] + off + static_cast<size_t>(i) * kXStride, w[i]);
     }
 }
 
-__device__ __forceinline__ void gather(const SweepArgs& A, unsigned long long seq, double& ta, double& tb, int& te,
-                                       Smem& sm) {
-    const unsigned tag = tag_of(seq);
-    const size_t slot_base = static_cast<size_t>(seq & 1ull) * static_cast<size_t>(A.P) * 4;
-    const int nwp = (A.P + 32 * kRecPerLane - 1) / (32 * kRecPerLane);
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    if (A.dbg & 8) { // variant: one thread waits on the arrival counter first
-        if (threadIdx.x == 0) {
-            const unsigned long long target = (seq + 1) * static_cast<unsigned long long>(A.P);
-            while (ld_acquire(A.slots + static_cast<size_t>(2) * A.P * 4) < target) {
-            }
-        }
-        __syncthreads();
+// Per-lane running totals of the two buffers (lanes 0..6 of warp 0).
+struct XPrev {
+    unsigned long long b0, b1;
+};
+
+__device__ __forceinline__ void xprev_load(const SweepArgs& A, XPrev& pv) {
+    const int l = threadIdx.x & 31;
+    if (threadIdx.x < 32 && l < kXWords) {
+        pv.b0 = A.slots[kXBase + l];
+        pv.b1 = A.slots[kXBase + kXWords + l];
     }
-    if (w < nwp) {
-        unsigned long long r0[kRecPerLane], r1[kRecPerLane], r2[kRecPerLane], r3[kRecPerLane];
-        bool ok[kRecPerLane];
-#pragma unroll
-        for (int i = 0; i < kRecPerLane; ++i) ok[i] = (w * 32 * kRecPerLane + i * 32 + l) >= A.P;
-        for (;;) {
-#pragma unroll
-            for (int i = 0; i < kRecPerLane; ++i) {
-                if (!ok[i]) {
-                    const size_t off = slot_base + static_cast<size_t>(w * 32 * kRecPerLane + i * 32 + l) * 4;
-                    ld_vol_v2(A.slots + off, r0[i], r1[i]);
-                    ld_vol_v2(A.slots + off + 2, r2[i], r3[i]);
-                }
-            }
-            bool all = true;
-#pragma unroll
-            for (int i = 0; i < kRecPerLane; ++i) {
-                if (!ok[i]) {
-                    ok[i] = ((static_cast<unsigned>(r0[i] >> 32) & 0x7fffffffu) == tag) &&
-                            ((static_cast<unsigned>(r1[i] >> 32) & 0x7fffffffu) == tag) &&
-                            ((static_cast<unsigned>(r2[i] >> 32) & 0x7fffffffu) == tag) &&
-                            ((static_cast<unsigned>(r3[i] >> 32) & 0x7fffffffu) == tag);
-                    all = all && ok[i];
-                }
-            }
-            if (__all_sync(0xffffffffu, all)) break;
+}
+
+__device__ __forceinline__ void xprev_store(const SweepArgs& A, const XPrev& pv) {
+    const int l = threadIdx.x & 31;
+    if (threadIdx.x < 32 && l < kXWords) {
+        const_cast<unsigned long long*>(A.slots)[kXBase + l] = pv.b0;
+        const_cast<unsigned long long*>(A.slots)[kXBase + kXWords + l] = pv.b1;
+    }
+}
+
+// all threads; totals returned to every thread
+__device__ __forceinline__ void gather(const SweepArgs& A, unsigned long long seq, XPrev& pv, double& ta, double& tb,
+                                       int& te, Smem& sm) {
+    if (threadIdx.x < 32) {
+        const int l = threadIdx.x;
+        const unsigned buf = static_cast<unsigned>(seq & 1ull);
+        unsigned long long diff = 0;
+        if (l < kXWords) {
+            const unsigned long long* p = A.slots + static_cast<size_t>(buf) * kXWords * kXStride +
+                                          static_cast<size_t>(l) * kXStride;
+            const unsigned long long prev = buf ? pv.b1 : pv.b0;
+            unsigned long long v;
+            do {
+                v = ld_relaxed(p);
+                diff = v - prev;
+            } while ((diff >> 50) < static_cast<unsigned long long>(A.P));
+            if (buf) pv.b1 = v;
+            else pv.b0 = v;
         }
-        double sa = 0.0, sb = 0.0;
-        int se = 0;
+        const unsigned long long d = diff & kXData;
+        unsigned long long L[kXWords];
 #pragma unroll
-        for (int i = 0; i < kRecPerLane; ++i) {
-            if ((w * 32 * kRecPerLane + i * 32 + l) < A.P) {
-                const double va = __longlong_as_double(static_cast<long long>((r1[i] << 32) | (r0[i] & 0xffffffffull)));
-                const double vb = __longlong_as_double(static_cast<long long>((r3[i] << 32) | (r2[i] & 0xffffffffull)));
-                sa = __dadd_rn(sa, va);
-                sb = __dadd_rn(sb, vb);
-                se |= static_cast<int>(((r0[i] | r1[i] | r2[i] | r3[i]) >> 63) & 1ull);
-            }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            sa = __dadd_rn(sa, __shfl_xor_sync(0xffffffffu, sa, o));
-            sb = __dadd_rn(sb, __shfl_xor_sync(0xffffffffu, sb, o));
-        }
-        se = __reduce_or_sync(0xffffffffu, se);
+        for (int i = 0; i < kXWords; ++i) L[i] = __shfl_sync(0xffffffffu, d, i);
         if (l == 0) {
-            sm.pa[w] = sa;
-            sm.pb[w] = sb;
-            sm.pe[w] = se;
+            sm.pa[0] = from_limbs(L[0], L[1], L[2]);
+            sm.pb[0] = from_limbs(L[3], L[4], L[5]);
+            sm.pe[0] = L[6] != 0 ? 1 : 0;
         }
     }
     __syncthreads();
-    double x = 0.0, y = 0.0;
-    int z = 0;
-    for (int i = 0; i < nwp; ++i) {
-        x = __dadd_rn(x, sm.pa[i]);
-        y = __dadd_rn(y, sm.pb[i]);
-        z |= sm.pe[i];
-    }
-    ta = x;
-    tb = y;
-    te = z;
-}
-
-__device__ __forceinline__ void exchange(const SweepArgs& A, int pid, unsigned long long seq, double a, double b,
-                                         int e, double& ta, double& tb, int& te, Smem& sm) {
-    if (threadIdx.x == 0) publish(A, pid, seq, a, b, e);
-    gather(A, seq, ta, tb, te, sm);
+    ta = sm.pa[0];
+    tb = sm.pb[0];
+    te = sm.pe[0];
 }
 
 // Index data of one pair slot: the pair, whether it starts a subject run
-// (head) and whether the run continues past it.  Read-only; computed ahead
-// of the coordinate (prefetch) for the register-cached tiles.
+// (head) and whether the run continues past it.
 struct PairSlot {
     int2 pr;
     bool head;
@@ -542,7 +545,6 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
     while (si + 1 < A.nsh && static_cast<int>(blockIdx.x) >= A.sh[si + 1].cta_begin) ++si;
     const ShardArgs& S = A.sh[si];
     const int c = static_cast<int>(blockIdx.x) - S.cta_begin;
-    const int pid = S.pid_base + c;
     const int64_t* split_c = S.split + c;
     const int stride = S.ctas + 1;
     unsigned long long seq = *A.counter;
@@ -550,6 +552,8 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
     double errv = 0.0;
     Cached C;
     HeadRegs H;
+    XPrev pv{0ull, 0ull};
+    if (A.mode != kModeUpdate) xprev_load(A, pv);
 
     if (A.mode == kModeUpdate) {
         const int j = A.single_j;
@@ -570,7 +574,8 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         block_reduce(gs, hs, err, sm);
         double tg, th;
         int te;
-        exchange(A, pid, seq, gs, hs, err, tg, th, te, sm);
+        if (threadIdx.x == 0) publish(A, seq, gs, hs, err);
+        gather(A, seq, pv, tg, th, te, sm);
         ++seq;
         if (c == 0 && threadIdx.x == 0) {
             S.res->g = __dsub_rn(A.y_dot_x[j], tg);
@@ -578,6 +583,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             S.res->err_remote = te;
             if (si == 0) *A.counter = seq;
         }
+        if (c == 0 && si == 0) xprev_store(A, pv);
         return;
     }
 
@@ -613,7 +619,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             int e = err | ((bj != bj) || (rj != rj) ? 1 : 0);
             block_reduce(gs, hs, e, sm);
             if (tr && idx < A.ntrace) trb[idx * trs + 1] = gtimer();
-            if (threadIdx.x == 0 && !(A.dbg & 4)) publish(A, pid, seq, gs, hs, e);
+            if (threadIdx.x == 0 && !(A.dbg & 4)) publish(A, seq, gs, hs, e);
             // while the partials travel: issue the next coordinate's loads
             RawCached NR;
             issue_cached(S, nxt.x, nxt.y, NR);
@@ -635,7 +641,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                 th = sm.pb[0];
                 te = 0;
             } else {
-                gather(A, seq, tg, th, te, sm);
+                gather(A, seq, pv, tg, th, te, sm);
                 ++seq;
             }
             if (tr && idx < A.ntrace) trb[idx * trs + 2] = gtimer();
@@ -701,7 +707,8 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         block_reduce(ch, mg, e, sm);
         double tch, tmg;
         int te;
-        exchange(A, pid, seq, ch, mg, e, tch, tmg, te, sm);
+        if (threadIdx.x == 0) publish(A, seq, ch, mg, e);
+        gather(A, seq, pv, tch, tmg, te, sm);
         ++seq;
         if (c == 0 && threadIdx.x == 0) {
             S.res->change = tch;
@@ -718,6 +725,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         S.res->counter = seq;
         if (si == 0) *A.counter = seq;
     }
+    if (c == 0 && si == 0) xprev_store(A, pv);
 }
 
 // ---- dense kernels ---------------------------------------------------------
@@ -1232,7 +1240,7 @@ void alloc_state(bsccs_state* st, const bsccs_dataset* ds) {
     st->trust = dalloc<double>(ds->J, b);
     st->visit = dalloc<int32_t>(ds->J, b);
     st->vsplit = dalloc<longlong2>(static_cast<int64_t>(ds->J) * ds->ctas, b);
-    st->slots = dalloc<unsigned long long>(static_cast<int64_t>(2) * ds->ctas * 4 + 16, b);
+    st->slots = dalloc<unsigned long long>(kXchgAreaWords, b);
     st->moved = dalloc<uint8_t>(ds->J, b);
     st->counter = dalloc<unsigned long long>(1, b);
     st->err = dalloc<DevErr>(1, b);
@@ -1241,7 +1249,7 @@ void alloc_state(bsccs_state* st, const bsccs_dataset* ds) {
     CUDA_TRY(cudaMallocHost(&st->res_h, sizeof(DevResult)));
     CUDA_TRY(cudaEventCreate(&st->ev0));
     CUDA_TRY(cudaEventCreate(&st->ev1));
-    CUDA_TRY(cudaMemsetAsync(st->slots, 0, sizeof(unsigned long long) * (2 * ds->ctas * 4 + 16), st->stream));
+    CUDA_TRY(cudaMemsetAsync(st->slots, 0, sizeof(unsigned long long) * kXchgAreaWords, st->stream));
     CUDA_TRY(cudaMemsetAsync(st->counter, 0, sizeof(unsigned long long), st->stream));
     CUDA_TRY(cudaMemsetAsync(st->err, 0, sizeof(DevErr), st->stream));
     CUDA_TRY(cudaMemsetAsync(st->res, 0, sizeof(DevResult), st->stream));
@@ -1377,7 +1385,7 @@ SweepArgs base_args(const ExchangePlan& plan) {
     a.slots = plan.local_slots;
     a.P = plan.total_participants;
     a.counter = plan.counter;
-    if (a.P > kMaxPollWarps * 32 * kRecPerLane) internal_error("exchange plan: too many participants");
+    if (a.P >= (1 << 13)) internal_error("exchange plan: too many participants");
     return a;
 }
 

@@ -64,6 +64,7 @@ struct DevErr {
 constexpr int kSweepThreads = 512;
 constexpr int kMaxLocalShards = 8;
 constexpr int kMaxRanks = 8;
+constexpr int kXchgAreaWords = 512; // exchange words (2 x 7, 256 B apart) + running totals
 
 struct bsccs_dataset_impl;
 } // namespace bsccs_b200
