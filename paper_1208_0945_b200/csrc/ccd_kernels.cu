@@ -105,9 +105,18 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
+constexpr int kCap = kCached * kSweepThreads; // pairs a CTA keeps in registers per coordinate
+constexpr int kHtBits = 11;                     // subject hash table of the speculation repair
+constexpr int kHt = 1 << kHtBits;
+
 struct Smem {
-    double stage[kCached * kSweepThreads]; // per-pair l*exp (grad/hess) or l*exp delta (update)
-    int ssub[kCached * kSweepThreads];     // per-pair subject of the cached tiles
+    double stage[kCap]; // per-pair l*exp (grad/hess) or l*exp delta (update)
+    int ssub[kCap];     // per-pair subject of the cached tiles
+    // what the previous coordinate's update changed, for repairing the
+    // speculatively gathered records of the next coordinate
+    double jxb[kCap], jle[kCap], jden[kCap];
+    int jrow[kCap];
+    int htk[kHt], htv[kHt];
     double ra[kWarps], rb[kWarps];
     int re[kWarps];
     double pa[1], pb[1];
@@ -124,6 +133,11 @@ __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long lon
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ unsigned long long ld_poll(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ int2 ld_pair(const int2* p) { return __ldg(p); }
 
 __device__ __forceinline__ void record_error(DevErr* e, int code, double value) {
@@ -131,7 +145,8 @@ __device__ __forceinline__ void record_error(DevErr* e, int code, double value) 
 }
 
 
-// Reduce (a, b, e) over the CTA; result valid in thread 0.
+// Reduce (a, b, e) over the CTA; result valid in every lane of warp 0 (each
+// lane sums the warp partials in the same order, so the values agree).
 __device__ __forceinline__ void block_reduce(double& a, double& b, int& e, Smem& sm) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -146,7 +161,7 @@ __device__ __forceinline__ void block_reduce(double& a, double& b, int& e, Smem&
         sm.re[w] = e;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {
         double x = 0.0, y = 0.0;
         int z = 0;
         for (int i = 0; i < kWarps; ++i) {
@@ -212,18 +227,20 @@ __device__ __forceinline__ double from_limbs(unsigned long long L0, unsigned lon
     return ldexp(__ull2double_rn(m), 64 - lz - 80);
 }
 
-// thread 0 only
+// lanes 0..6 of warp 0 (all holding the same (a, b, e)): each converts and
+// adds one word, so the seven adds issue in parallel
 __device__ __forceinline__ void publish(const SweepArgs& A, unsigned long long seq, double a, double b, int e) {
-    unsigned long long w[kXWords];
-    const bool ok = to_limbs(a, w[0], w[1], w[2]) && to_limbs(b, w[3], w[4], w[5]);
-    w[6] = (e || !ok) ? 1ull : 0ull;
-    const size_t off = static_cast<size_t>(seq & 1ull) * kXWords * kXStride;
-#pragma unroll
-    for (int i = 0; i < kXWords; ++i) w[i] += kXCnt;
-    for (int d = 0; d < A.ndst; ++d) {
-#pragma unroll
-        for (int i = 0; i < kXWords; ++i) red_add(A.dst[d] + off + static_cast<size_t>(i) * kXStride, w[i]);
-    }
+    const int l = threadIdx.x & 31;
+    if (threadIdx.x >= 32 || l >= kXWords) return;
+    unsigned long long la[3], lb[3];
+    const bool ok = to_limbs(a, la[0], la[1], la[2]) && to_limbs(b, lb[0], lb[1], lb[2]);
+    unsigned long long w;
+    if (l < 3) w = la[l];
+    else if (l < 6) w = lb[l - 3];
+    else w = (e || !ok) ? 1ull : 0ull;
+    w += kXCnt;
+    const size_t off = static_cast<size_t>(seq & 1ull) * kXWords * kXStride + static_cast<size_t>(l) * kXStride;
+    for (int d = 0; d < A.ndst; ++d) red_add(A.dst[d] + off, w);
 }
 
 // Per-lane running totals of the two buffers (lanes 0..6 of warp 0).
@@ -260,7 +277,7 @@ __device__ __forceinline__ void gather(const SweepArgs& A, unsigned long long se
             const unsigned long long prev = buf ? pv.b1 : pv.b0;
             unsigned long long v;
             do {
-                v = ld_relaxed(p);
+                v = ld_poll(p);
                 diff = v - prev;
             } while ((diff >> 50) < static_cast<unsigned long long>(A.P));
             if (buf) pv.b1 = v;
@@ -399,12 +416,9 @@ struct HeadRegs {
 
 __device__ __forceinline__ bool slot_valid(const PairSlot& s) { return s.pr.x >= 0; }
 
-__device__ __forceinline__ void gh_slice(const ShardArgs& S, const Cached& C, int64_t p0, int64_t p1, HeadRegs& H,
-                                         double& gs, double& hs, int& err, Smem& sm) {
-    const int2* __restrict__ pairs = S.pairs;
+__device__ __forceinline__ void gather_records(const ShardArgs& S, const Cached& C, HeadRegs& H) {
     EraRec* era = S.era;
     SubjRec* subj = S.subj;
-    const int ncached = static_cast<int>(min(p1 - p0, static_cast<int64_t>(kCached) * kSweepThreads));
 #pragma unroll
     for (int v = 0; v < kCached; ++v) {
         if (slot_valid(C.slot[v])) {
@@ -419,6 +433,49 @@ __device__ __forceinline__ void gh_slice(const ShardArgs& S, const Cached& C, in
             }
         }
     }
+}
+
+__device__ __forceinline__ int ht_hash(int s) {
+    return static_cast<int>((static_cast<unsigned>(s) * 2654435761u) >> (32 - kHtBits));
+}
+
+// Patch speculatively gathered records with what the previous coordinate's
+// update wrote: a subject found in the table was touched, so its head takes
+// the new denominator and any of its eras among the updated rows takes the
+// new (x'beta, l*exp).  Shared-memory only.
+__device__ __forceinline__ void repair(const Cached& C, HeadRegs& H, const Smem& sm) {
+#pragma unroll
+    for (int v = 0; v < kCached; ++v) {
+        if (!slot_valid(C.slot[v])) continue;
+        const int s = C.slot[v].pr.y;
+        int h = ht_hash(s);
+        int k;
+        for (;;) {
+            k = sm.htk[h];
+            if (k == s || k == -1) break;
+            h = (h + 1) & (kHt - 1);
+        }
+        if (k != s) continue;
+        const int val = sm.htv[h];
+        const int posj = val & 0xffff, runj = val >> 16;
+        if (C.slot[v].head) H.den[v] = sm.jden[posj];
+        const int row = C.slot[v].pr.x;
+        for (int q = posj; q < posj + runj; ++q) {
+            if (sm.jrow[q] == row) {
+                H.xb[v] = sm.jxb[q];
+                H.le[v] = sm.jle[q];
+                break;
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void gh_compute(const ShardArgs& S, const Cached& C, int64_t p0, int64_t p1,
+                                           const HeadRegs& H, double& gs, double& hs, int& err, Smem& sm) {
+    const int2* __restrict__ pairs = S.pairs;
+    EraRec* era = S.era;
+    SubjRec* subj = S.subj;
+    const int ncached = static_cast<int>(min(p1 - p0, static_cast<int64_t>(kCap)));
 #pragma unroll
     for (int v = 0; v < kCached; ++v) {
         const int pos = v * kSweepThreads + static_cast<int>(threadIdx.x);
@@ -443,7 +500,7 @@ __device__ __forceinline__ void gh_slice(const ShardArgs& S, const Cached& C, in
         }
     }
     // streamed remainder: head threads own their runs
-    for (int64_t base = p0 + static_cast<int64_t>(kCached) * kSweepThreads; base < p1; base += kSweepThreads) {
+    for (int64_t base = p0 + static_cast<int64_t>(kCap); base < p1; base += kSweepThreads) {
         const int64_t p = base + threadIdx.x;
         const PairSlot s = load_slot(pairs, p, p0, p1);
         if (s.head) {
@@ -456,13 +513,20 @@ __device__ __forceinline__ void gh_slice(const ShardArgs& S, const Cached& C, in
     }
 }
 
+__device__ __forceinline__ void gh_slice(const ShardArgs& S, const Cached& C, int64_t p0, int64_t p1, HeadRegs& H,
+                                         double& gs, double& hs, int& err, Smem& sm) {
+    gather_records(S, C, H);
+    gh_compute(S, C, p0, p1, H, gs, hs, err, sm);
+}
+
 __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C, const HeadRegs& H, bool cached,
-                                             int64_t p0, int64_t p1, double d, int& err, double& errv, Smem& sm) {
+                                             int64_t p0, int64_t p1, double d, int& err, double& errv, Smem& sm,
+                                             bool record = false, int* myht = nullptr) {
     const int2* __restrict__ pairs = S.pairs;
     EraRec* era = S.era;
     SubjRec* subj = S.subj;
     if (cached) {
-        const int ncached = static_cast<int>(min(p1 - p0, static_cast<int64_t>(kCached) * kSweepThreads));
+        const int ncached = static_cast<int>(min(p1 - p0, static_cast<int64_t>(kCap)));
         // every lane updates its own era (engine.hpp:219-229) and stages
         // fresh - old for its run head
 #pragma unroll
@@ -478,7 +542,12 @@ __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C
                     const double fresh = __dmul_rn(static_cast<double>(H.len[v]), exp(updated));
                     diff = __dsub_rn(fresh, H.le[v]);
                     *reinterpret_cast<double2*>(era + C.slot[v].pr.x) = make_double2(updated, fresh);
+                    if (record) {
+                        sm.jxb[pos] = updated;
+                        sm.jle[pos] = fresh;
+                    }
                 }
+                if (record) sm.jrow[pos] = C.slot[v].pr.x;
                 sm.stage[pos] = diff;
             }
         }
@@ -487,7 +556,8 @@ __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C
 #pragma unroll
         for (int v = 0; v < kCached; ++v) {
             if (C.slot[v].head) {
-                int q = v * kSweepThreads + static_cast<int>(threadIdx.x);
+                const int pos = v * kSweepThreads + static_cast<int>(threadIdx.x);
+                int q = pos;
                 double den = __dadd_rn(H.den[v], sm.stage[q++]);
                 if (C.slot[v].cont) {
                     const int s = C.slot[v].pr.y;
@@ -496,6 +566,14 @@ __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C
                         den = run_tail_update(pairs, era, p0 + q, p1, s, d, den, err, errv);
                 }
                 subj[C.slot[v].pr.y].den = den;
+                if (record) { // publish (subject -> run) for the next coordinate's repair
+                    sm.jden[pos] = den;
+                    const int s = C.slot[v].pr.y;
+                    int h = ht_hash(s);
+                    while (atomicCAS(&sm.htk[h], -1, s) != -1) h = (h + 1) & (kHt - 1);
+                    sm.htv[h] = pos | ((q - pos) << 16);
+                    myht[v] = h;
+                }
             }
         }
     }
@@ -540,7 +618,8 @@ __device__ __forceinline__ void finalize_cached(const RawCached& R, Cached& C) {
 }
 
 __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant__ SweepArgs A) {
-    __shared__ Smem sm;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
     int si = 0;
     while (si + 1 < A.nsh && static_cast<int>(blockIdx.x) >= A.sh[si + 1].cta_begin) ++si;
     const ShardArgs& S = A.sh[si];
@@ -574,7 +653,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         block_reduce(gs, hs, err, sm);
         double tg, th;
         int te;
-        if (threadIdx.x == 0) publish(A, seq, gs, hs, err);
+        publish(A, seq, gs, hs, err);
         gather(A, seq, pv, tg, th, te, sm);
         ++seq;
         if (c == 0 && threadIdx.x == 0) {
@@ -588,21 +667,35 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
     }
 
     // ---- one full cycle -------------------------------------------------
-    // Software pipeline over the visit list: while coordinate idx runs, the
-    // pair slots of idx+1 are in flight (issued after the publish), and the
-    // slice bounds / coordinate ids of idx+2 are loading, so no dependent
-    // metadata load sits on the per-coordinate critical path.
+    // Software pipeline over the visit list.  While coordinate idx's
+    // partials travel: the pair slots of idx+2 load, and -- when both slices
+    // fit the register tiles -- the era / subject records of idx+1 are
+    // gathered speculatively.  The update of idx then records what it wrote
+    // (shared memory + subject hash table) and idx+1 repairs the few records
+    // it touched, so no HBM gather sits on the per-coordinate critical path.
     long long nvisit = 0, nmoved = 0;
     const int V = A.nvisit;
     const longlong2* vs = S.vsplit + static_cast<size_t>(c) * static_cast<size_t>(V);
     bool aborted = false;
     if (V > 0) {
+        for (int i = threadIdx.x; i < kHt; i += kSweepThreads) sm.htk[i] = -1;
+        const longlong2 z2 = make_longlong2(0, 0);
         longlong2 cur = vs[0];
         int j = A.visit[0];
         double bj = S.beta[j], rj = S.trust[j], ydx = A.y_dot_x[j];
         load_cached(S, cur.x, cur.y, C);
-        longlong2 nxt = V > 1 ? vs[1] : make_longlong2(0, 0);
+        longlong2 nxt = V > 1 ? vs[1] : z2;
         int jn = V > 1 ? A.visit[1] : 0;
+        Cached N;
+        load_cached(S, nxt.x, nxt.y, N);
+        longlong2 nxt2 = V > 2 ? vs[2] : z2;
+        int jn2 = V > 2 ? A.visit[2] : 0;
+        HeadRegs SH;
+        bool spec = false;
+        int myht[kCached];
+#pragma unroll
+        for (int v = 0; v < kCached; ++v) myht[v] = -1;
+        __syncthreads(); // hash table initialised
         const bool tr = A.trace != nullptr && threadIdx.x == 0;
         unsigned long long* trb = tr ? A.trace + static_cast<size_t>(blockIdx.x) * 4 : nullptr;
         const size_t trs = static_cast<size_t>(gridDim.x) * 4;
@@ -610,7 +703,11 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             const int64_t p0 = cur.x, p1 = cur.y;
             if (tr && idx < A.ntrace) trb[idx * trs + 0] = gtimer();
             double gs = 0.0, hs = 0.0;
-            if (!(A.dbg & 1)) gh_slice(S, C, p0, p1, H, gs, hs, err, sm);
+            if (!(A.dbg & 1)) {
+                if (spec) repair(C, H, sm);
+                else gather_records(S, C, H);
+                gh_compute(S, C, p0, p1, H, gs, hs, err, sm);
+            }
             if (err) record_error(S.err, err, errv);
             // The publish below must not be observable before this
             // coordinate's beta/trust loads complete (CTA 0 overwrites them
@@ -618,17 +715,27 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             // word makes the record store data-dependent on the loads.
             int e = err | ((bj != bj) || (rj != rj) ? 1 : 0);
             block_reduce(gs, hs, e, sm);
+            // every lookup of the previous coordinate's entries is done
+#pragma unroll
+            for (int v = 0; v < kCached; ++v) {
+                if (myht[v] >= 0) {
+                    sm.htk[myht[v]] = -1;
+                    myht[v] = -1;
+                }
+            }
             if (tr && idx < A.ntrace) trb[idx * trs + 1] = gtimer();
-            if (threadIdx.x == 0 && !(A.dbg & 4)) publish(A, seq, gs, hs, e);
-            // while the partials travel: issue the next coordinate's loads
+            if (!(A.dbg & 4)) publish(A, seq, gs, hs, e);
+            // while the partials travel
             RawCached NR;
-            issue_cached(S, nxt.x, nxt.y, NR);
+            issue_cached(S, nxt2.x, nxt2.y, NR);
             const bool more = idx + 1 < V;
+            const bool spec_next = more && !(A.dbg & 16) && (p1 - p0) <= kCap && (nxt.y - nxt.x) <= kCap;
+            if (spec_next) gather_records(S, N, SH);
             const double bn = more ? S.beta[jn] : 0.0;
             const double rn = more ? S.trust[jn] : 1.0;
             const double yn = more ? A.y_dot_x[jn] : 0.0;
-            const longlong2 nxt2 = idx + 2 < V ? vs[idx + 2] : make_longlong2(0, 0);
-            const int jn2 = idx + 2 < V ? A.visit[idx + 2] : 0;
+            const longlong2 nxt3 = idx + 3 < V ? vs[idx + 3] : z2;
+            const int jn3 = idx + 3 < V ? A.visit[idx + 3] : 0;
             double tg, th;
             int te;
             if (A.dbg & 4) {
@@ -670,7 +777,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                     break;
                 }
                 ++nmoved;
-                if (!(A.dbg & 2)) update_slice(S, C, H, true, p0, p1, delta, err, errv, sm);
+                if (!(A.dbg & 2)) update_slice(S, C, H, true, p0, p1, delta, err, errv, sm, spec_next, myht);
                 bnew = __dadd_rn(bj, delta);
             }
             if (c == 0 && threadIdx.x == 0) {
@@ -679,14 +786,19 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             }
             __syncthreads(); // slice writes of this coordinate before the next reads
             if (tr && idx < A.ntrace) trb[idx * trs + 3] = gtimer();
-            finalize_cached(NR, C);
+            C = N;
+            finalize_cached(NR, N);
+            H = SH;
+            spec = spec_next;
             cur = nxt;
+            nxt = nxt2;
+            nxt2 = nxt3;
             j = jn;
+            jn = jn2;
+            jn2 = jn3;
             bj = bn;
             rj = rn;
             ydx = yn;
-            nxt = nxt2;
-            jn = jn2;
         }
     }
 
@@ -707,7 +819,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         block_reduce(ch, mg, e, sm);
         double tch, tmg;
         int te;
-        if (threadIdx.x == 0) publish(A, seq, ch, mg, e);
+        publish(A, seq, ch, mg, e);
         gather(A, seq, pv, tch, tmg, te, sm);
         ++seq;
         if (c == 0 && threadIdx.x == 0) {
@@ -1036,10 +1148,18 @@ void throw_device_error(int code, double value) {
     }
 }
 
+void ensure_kernel_attrs(int device) {
+    static std::atomic<unsigned> done{0};
+    if (device < 32 && (done.load() & (1u << device))) return;
+    CUDA_TRY(cudaFuncSetAttribute(k_ccd, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(Smem))));
+    if (device < 32) done.fetch_or(1u << device);
+}
+
 int default_ctas(int device) {
     // one persistent CTA per SM (launch bounds force 1 resident CTA of 512)
+    ensure_kernel_attrs(device);
     int per_sm = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ccd, kSweepThreads, 0));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ccd, kSweepThreads, sizeof(Smem)));
     if (per_sm < 1) internal_error("sweep kernel cannot be resident");
     return sm_count(device);
 }
@@ -1397,9 +1517,10 @@ int plan_ctas(const ExchangePlan& plan) {
 
 void launch_ccd(const ExchangePlan& plan, SweepArgs& a) {
     bsccs_state* s0 = plan.shards[0];
+    ensure_kernel_attrs(s0->ds->device);
     void* params[] = {&a};
     CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_ccd), dim3(plan_ctas(plan)), dim3(kSweepThreads),
-                                         params, 0, s0->stream));
+                                         params, sizeof(Smem), s0->stream));
     count_launches(1);
 }
 
