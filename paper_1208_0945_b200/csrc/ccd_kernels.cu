@@ -730,7 +730,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             issue_cached(S, nxt2.x, nxt2.y, NR);
             const bool more = idx + 1 < V;
             const bool spec_next = more && !(A.dbg & 16) && (p1 - p0) <= kCap && (nxt.y - nxt.x) <= kCap;
-            if (spec_next) gather_records(S, N, SH);
+            if (spec_next && !(A.dbg & 32)) gather_records(S, N, SH);
             const double bn = more ? S.beta[jn] : 0.0;
             const double rn = more ? S.trust[jn] : 1.0;
             const double yn = more ? A.y_dot_x[jn] : 0.0;
@@ -752,6 +752,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                 ++seq;
             }
             if (tr && idx < A.ntrace) trb[idx * trs + 2] = gtimer();
+            if (spec_next && (A.dbg & 32)) gather_records(S, N, SH);
             if (te) { // an overflow or bad denominator somewhere: stop everywhere
                 aborted = true;
                 if (c == 0 && threadIdx.x == 0) S.res->err_remote = 1;
