@@ -95,10 +95,11 @@ struct SweepArgs {
     int P;
     unsigned long long* counter;
     int dbg; // profiling only: bit0 skip grad/hess loads, bit1 skip update, bit2 skip exchange
-    unsigned long long* trace; // profiling only: [ntrace][gridDim][4] globaltimer stamps
+    unsigned long long* trace; // profiling only: [ntrace][gridDim][kTr] globaltimer stamps
     int ntrace;
 };
 
+constexpr int kTr = 6; // stamps: top, pre-publish, gather done, update done, post-issue, poll done
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -266,7 +267,7 @@ __device__ __forceinline__ void xprev_store(const SweepArgs& A, const XPrev& pv)
 
 // all threads; totals returned to every thread
 __device__ __forceinline__ void gather(const SweepArgs& A, unsigned long long seq, XPrev& pv, double& ta, double& tb,
-                                       int& te, Smem& sm) {
+                                       int& te, Smem& sm, unsigned long long* stamp = nullptr) {
     if (threadIdx.x < 32) {
         const int l = threadIdx.x;
         const unsigned buf = static_cast<unsigned>(seq & 1ull);
@@ -283,6 +284,8 @@ __device__ __forceinline__ void gather(const SweepArgs& A, unsigned long long se
             if (buf) pv.b1 = v;
             else pv.b0 = v;
         }
+        __syncwarp();
+        if (stamp && l == 0) *stamp = gtimer();
         const unsigned long long d = diff & kXData;
         unsigned long long L[kXWords];
 #pragma unroll
@@ -697,8 +700,8 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         for (int v = 0; v < kCached; ++v) myht[v] = -1;
         __syncthreads(); // hash table initialised
         const bool tr = A.trace != nullptr && threadIdx.x == 0;
-        unsigned long long* trb = tr ? A.trace + static_cast<size_t>(blockIdx.x) * 4 : nullptr;
-        const size_t trs = static_cast<size_t>(gridDim.x) * 4;
+        unsigned long long* trb = tr ? A.trace + static_cast<size_t>(blockIdx.x) * kTr : nullptr;
+        const size_t trs = static_cast<size_t>(gridDim.x) * kTr;
         for (int idx = 0; idx < V; ++idx) {
             const int64_t p0 = cur.x, p1 = cur.y;
             if (tr && idx < A.ntrace) trb[idx * trs + 0] = gtimer();
@@ -736,6 +739,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             const double yn = more ? A.y_dot_x[jn] : 0.0;
             const longlong2 nxt3 = idx + 3 < V ? vs[idx + 3] : z2;
             const int jn3 = idx + 3 < V ? A.visit[idx + 3] : 0;
+            if (tr && idx < A.ntrace) trb[idx * trs + 4] = gtimer();
             double tg, th;
             int te;
             if (A.dbg & 4) {
@@ -748,7 +752,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                 th = sm.pb[0];
                 te = 0;
             } else {
-                gather(A, seq, pv, tg, th, te, sm);
+                gather(A, seq, pv, tg, th, te, sm, (tr && idx < A.ntrace) ? trb + idx * trs + 5 : nullptr);
                 ++seq;
             }
             if (tr && idx < A.ntrace) trb[idx * trs + 2] = gtimer();
@@ -1624,7 +1628,7 @@ void set_debug_trace(int ncoords, int ctas) {
     if (g_trace) cudaFree(g_trace);
     g_trace = nullptr;
     g_ntrace = ncoords;
-    g_trace_words = static_cast<size_t>(ncoords) * ctas * 4;
+    g_trace_words = static_cast<size_t>(ncoords) * ctas * kTr;
     if (ncoords > 0) {
         CUDA_TRY(cudaMalloc(&g_trace, g_trace_words * sizeof(unsigned long long)));
         CUDA_TRY(cudaMemset(g_trace, 0, g_trace_words * sizeof(unsigned long long)));

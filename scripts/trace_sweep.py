@@ -22,11 +22,11 @@ B.run_cycle(dds, st, solver, prior, cfg)  # warm
 lib.bsccs_debug_set_sweep_flags(flags)
 lib.bsccs_debug_trace(NT, ctas, None, 0)
 B.run_cycle(dds, st, solver, prior, cfg)
-buf = np.zeros(NT * ctas * 4, dtype=np.uint64)
+buf = np.zeros(NT * ctas * 6, dtype=np.uint64)
 lib.bsccs_debug_trace(NT, ctas, buf.ctypes.data_as(C.c_void_p), buf.size)
 lib.bsccs_debug_trace(0, ctas, None, 0)
 lib.bsccs_debug_set_sweep_flags(0)
-t = buf.reshape(NT, ctas, 4).astype(np.int64)
+t = buf.reshape(NT, ctas, 6).astype(np.int64)
 t = t[20:NT - 1]  # skip the start
 t0 = t[:, :, 0]
 pub = t[:, :, 1]
@@ -47,6 +47,13 @@ upd = done - got
 print(f"  gather done -> update done: median {np.median(upd):.0f}  max-over-CTAs median {np.median(upd.max(1)):.0f}")
 nxt = t[1:, :, 0] - done[:-1]
 print(f"  update done -> next top (finalize): median {np.median(nxt):.0f}")
+iss = t[:, :, 4]
+poll = t[:, :, 5]
+print(f"  publish -> prefetch issued: median {np.median(iss - pub):.0f}")
+print(f"  last publish -> poll done (lane 0, warp 0): median {np.median(np.median(poll, 1) - last_pub):.0f}  "
+      f"first CTA {np.median(poll.min(1) - last_pub):.0f}  last CTA {np.median(poll.max(1) - last_pub):.0f}")
+print(f"  poll done -> gather done: median {np.median(got - poll):.0f}")
+print(f"  own publish -> poll done: median {np.median(poll - pub):.0f}")
 slow = np.argmax(pub, axis=1)
 vals, cnt = np.unique(slow, return_counts=True)
 order = np.argsort(-cnt)[:8]
