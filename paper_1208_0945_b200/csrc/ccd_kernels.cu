@@ -50,11 +50,15 @@ namespace {
 constexpr int kModeSweep = 0;
 constexpr int kModeGradHess = 1;
 constexpr int kModeUpdate = 2;
-constexpr int kCached = 2;          // register-cached tiles of the slice
-constexpr int kWarps = kSweepThreads / 32;
+constexpr int kT = kSweepThreads;   // threads per CTA
+constexpr int kCached = 4;          // register tiles of the slice (pairs p0 + v*T + tid)
+constexpr int kWarps = kT / 32;
+constexpr int kCap = kCached * kT;  // pairs a CTA keeps in registers per coordinate
 constexpr int kLLBlocks = 592;      // fixed => deterministic LL reduction
 constexpr int kLLThreads = 256;
 constexpr double kXbBound = 700.0;  // xbeta_bound<double> engine.hpp:20-23
+constexpr int kHtBits = 11;         // subject hash table of the speculation repair
+constexpr int kHt = 1 << kHtBits;
 
 struct ShardArgs {
     const int2* pairs;
@@ -94,7 +98,7 @@ struct SweepArgs {
     const unsigned long long* slots;
     int P;
     unsigned long long* counter;
-    int dbg; // profiling only: bit0 skip grad/hess loads, bit1 skip update, bit2 skip exchange
+    int dbg; // profiling only: bit0 skip grad/hess, bit1 skip update, bit2 skip exchange, bit4 no speculation
     unsigned long long* trace; // profiling only: [ntrace][gridDim][kTr] globaltimer stamps
     int ntrace;
 };
@@ -106,10 +110,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
-constexpr int kCap = kCached * kSweepThreads; // pairs a CTA keeps in registers per coordinate
-constexpr int kHtBits = 11;                     // subject hash table of the speculation repair
-constexpr int kHt = 1 << kHtBits;
-
 struct Smem {
     double stage[kCap]; // per-pair l*exp (grad/hess) or l*exp delta (update)
     int ssub[kCap];     // per-pair subject of the cached tiles
@@ -120,19 +120,17 @@ struct Smem {
     int htk[kHt], htv[kHt];
     double ra[kWarps], rb[kWarps];
     int re[kWarps];
-    double pa[1], pb[1];
-    int pe[1];
+    // broadcast of the exchange result / step decision by warp 0
+    double ta, tb, delta;
+    int te, status;
 };
+
+// ---- memory helpers ----------------------------------------------------------
 
 // Exchange words: relaxed at GPU scope (each word validates itself, so no
 // fences are needed; peers on other GPUs would use .sys).
 __device__ __forceinline__ void red_add(unsigned long long* p, unsigned long long v) {
     asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
 }
 __device__ __forceinline__ unsigned long long ld_poll(const unsigned long long* p) {
     unsigned long long v;
@@ -145,26 +143,37 @@ __device__ __forceinline__ void record_error(DevErr* e, int code, double value) 
     if (atomicCAS(&e->code, 0, code) == 0) e->value = value;
 }
 
+__device__ __forceinline__ int warp_id() { return static_cast<int>(threadIdx.x) >> 5; }
+__device__ __forceinline__ int lane_id() { return static_cast<int>(threadIdx.x) & 31; }
+
+// ---- CTA reduction -------------------------------------------------------------
 
 // Reduce (a, b, e) over the CTA; result valid in every lane of warp 0 (each
 // lane sums the warp partials in the same order, so the values agree).
-__device__ __forceinline__ void block_reduce(double& a, double& b, int& e, Smem& sm) {
+// Warps with nothing to add (warp-uniform `idle`) skip the shuffle tree.
+__device__ __forceinline__ void block_reduce(double& a, double& b, int& e, bool idle, Smem& sm) {
+    if (!idle) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        a = __dadd_rn(a, __shfl_xor_sync(0xffffffffu, a, o));
-        b = __dadd_rn(b, __shfl_xor_sync(0xffffffffu, b, o));
+        for (int o = 16; o > 0; o >>= 1) {
+            a = __dadd_rn(a, __shfl_xor_sync(0xffffffffu, a, o));
+            b = __dadd_rn(b, __shfl_xor_sync(0xffffffffu, b, o));
+        }
+        e = __reduce_or_sync(0xffffffffu, e);
+    } else {
+        a = 0.0;
+        b = 0.0;
+        e = __reduce_or_sync(0xffffffffu, e);
     }
-    e = __reduce_or_sync(0xffffffffu, e);
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    if (l == 0) {
-        sm.ra[w] = a;
-        sm.rb[w] = b;
-        sm.re[w] = e;
+    if (lane_id() == 0) {
+        sm.ra[warp_id()] = a;
+        sm.rb[warp_id()] = b;
+        sm.re[warp_id()] = e;
     }
     __syncthreads();
     if (threadIdx.x < 32) {
         double x = 0.0, y = 0.0;
         int z = 0;
+#pragma unroll
         for (int i = 0; i < kWarps; ++i) {
             x = __dadd_rn(x, sm.ra[i]);
             y = __dadd_rn(y, sm.rb[i]);
@@ -176,7 +185,7 @@ __device__ __forceinline__ void block_reduce(double& a, double& b, int& e, Smem&
     }
 }
 
-// Order-independent all-reduce of two non-negative doubles per participant.
+// ---- order-independent exchange -------------------------------------------------
 //
 // Each participant splits its partial exactly into three 42-bit limbs of a
 // 2^-80 fixed-point number and issues seven relaxed red.add.u64 (six limbs
@@ -186,8 +195,8 @@ __device__ __forceinline__ void block_reduce(double& a, double& b, int& e, Smem&
 // bits above 2^50 -- every word validates itself, no fences or flags.  The
 // integer sum is associative, so every CTA reconstructs the bit-identical,
 // correctly rounded exact sum of the partials whatever the arrival order.
-// Words sit 256 B apart so the 148 adds per word land on distinct L2 slices;
-// two buffers alternate by sequence parity.
+// Words sit 256 B apart so the adds land on distinct L2 slices; two buffers
+// alternate by sequence parity.
 constexpr int kXStride = 32; // u64 words between exchange words (256 B)
 constexpr int kXWords = 7;
 constexpr int kXBase = 2 * kXWords * kXStride; // running totals at launch end
@@ -195,62 +204,80 @@ constexpr unsigned long long kXCnt = 1ull << 50;
 constexpr unsigned long long kXData = kXCnt - 1;
 constexpr unsigned long long kM42 = (1ull << 42) - 1;
 
-__device__ __forceinline__ bool to_limbs(double v, unsigned long long& l0, unsigned long long& l1,
-                                         unsigned long long& l2) {
+// limb i (0..2) of v in [0, 2^46) at 2^-80 resolution; false if out of range
+__device__ __forceinline__ bool limb_of(double v, int i, unsigned long long& out) {
     if (!(v >= 0.0 && v < 0x1p46)) {
-        l0 = l1 = l2 = 0;
+        out = 0;
         return false;
     }
     const double t2 = floor(__dmul_rn(v, 0x1p-4));
+    if (i == 2) {
+        out = static_cast<unsigned long long>(t2);
+        return true;
+    }
     const double r = __dsub_rn(v, __dmul_rn(t2, 16.0)); // exact, [0, 16)
     const double s1 = __dmul_rn(r, 0x1p38);
     const double t1 = floor(s1);
-    const double r0 = __dsub_rn(s1, t1); // exact, [0, 1)
-    l2 = static_cast<unsigned long long>(t2);
-    l1 = static_cast<unsigned long long>(t1);
-    l0 = static_cast<unsigned long long>(floor(__dmul_rn(r0, 0x1p42)));
+    if (i == 1) {
+        out = static_cast<unsigned long long>(t1);
+        return true;
+    }
+    out = static_cast<unsigned long long>(floor(__dmul_rn(__dsub_rn(s1, t1), 0x1p42))); // exact below 2^-80
     return true;
 }
 
+__device__ __forceinline__ double pow2(int e) { // 2^e for normal exponents
+    return __longlong_as_double(static_cast<long long>(1023 + e) << 52);
+}
+
+// correctly rounded double of (L2*2^84 + L1*2^42 + L0) * 2^-80
 __device__ __forceinline__ double from_limbs(unsigned long long L0, unsigned long long L1, unsigned long long L2) {
     L1 += L0 >> 42;
     L0 &= kM42;
     L2 += L1 >> 42;
     L1 &= kM42;
-    const unsigned __int128 V = (static_cast<unsigned __int128>(L2) << 84) |
-                                (static_cast<unsigned __int128>(L1) << 42) | static_cast<unsigned __int128>(L0);
-    if (V == 0) return 0.0;
-    const unsigned long long hi = static_cast<unsigned long long>(V >> 64), lo = static_cast<unsigned long long>(V);
-    const int lz = hi ? __clzll(static_cast<long long>(hi)) : 64 + __clzll(static_cast<long long>(lo));
-    const unsigned __int128 W = V << lz;
-    unsigned long long m = static_cast<unsigned long long>(W >> 64);
-    m |= (static_cast<unsigned long long>(W) != 0ull) ? 1ull : 0ull; // sticky: correct rounding below
-    return ldexp(__ull2double_rn(m), 64 - lz - 80);
+    // 128-bit V = hi:lo
+    const unsigned long long lo = L0 | (L1 << 42);
+    const unsigned long long hi = (L1 >> 22) | (L2 << 20);
+    if ((hi | lo) == 0) return 0.0;
+    int lz;
+    unsigned long long m, rest;
+    if (hi) {
+        lz = __clzll(static_cast<long long>(hi));
+        m = lz ? (hi << lz) | (lo >> (64 - lz)) : hi;
+        rest = lz ? lo << lz : lo;
+    } else {
+        lz = 64 + __clzll(static_cast<long long>(lo));
+        m = lo << (lz - 64);
+        rest = 0;
+    }
+    m |= rest != 0 ? 1ull : 0ull; // sticky bit for correct rounding
+    return __dmul_rn(__ull2double_rn(m), pow2(64 - lz - 80));
 }
 
-// lanes 0..6 of warp 0 (all holding the same (a, b, e)): each converts and
-// adds one word, so the seven adds issue in parallel
+// lanes 0..6 of warp 0 (all holding the same (a, b, e)) each add one word
 __device__ __forceinline__ void publish(const SweepArgs& A, unsigned long long seq, double a, double b, int e) {
-    const int l = threadIdx.x & 31;
+    const int l = lane_id();
     if (threadIdx.x >= 32 || l >= kXWords) return;
-    unsigned long long la[3], lb[3];
-    const bool ok = to_limbs(a, la[0], la[1], la[2]) && to_limbs(b, lb[0], lb[1], lb[2]);
     unsigned long long w;
-    if (l < 3) w = la[l];
-    else if (l < 6) w = lb[l - 3];
-    else w = (e || !ok) ? 1ull : 0ull;
+    bool ok = true;
+    if (l < 3) ok = limb_of(a, l, w);
+    else if (l < 6) ok = limb_of(b, l - 3, w);
+    else w = 0;
+    const bool okab = __all_sync(0x7fu, ok) && (0.0 <= a && a < 0x1p46 && 0.0 <= b && b < 0x1p46);
+    if (l == 6) w = (e || !okab) ? 1ull : 0ull;
     w += kXCnt;
     const size_t off = static_cast<size_t>(seq & 1ull) * kXWords * kXStride + static_cast<size_t>(l) * kXStride;
     for (int d = 0; d < A.ndst; ++d) red_add(A.dst[d] + off, w);
 }
 
-// Per-lane running totals of the two buffers (lanes 0..6 of warp 0).
+// Running totals of the two buffers (lanes 0..6 of warp 0).
 struct XPrev {
     unsigned long long b0, b1;
 };
 
 __device__ __forceinline__ void xprev_load(const SweepArgs& A, XPrev& pv) {
-    const int l = threadIdx.x & 31;
+    const int l = lane_id();
     if (threadIdx.x < 32 && l < kXWords) {
         pv.b0 = A.slots[kXBase + l];
         pv.b1 = A.slots[kXBase + kXWords + l];
@@ -258,49 +285,44 @@ __device__ __forceinline__ void xprev_load(const SweepArgs& A, XPrev& pv) {
 }
 
 __device__ __forceinline__ void xprev_store(const SweepArgs& A, const XPrev& pv) {
-    const int l = threadIdx.x & 31;
+    const int l = lane_id();
     if (threadIdx.x < 32 && l < kXWords) {
         const_cast<unsigned long long*>(A.slots)[kXBase + l] = pv.b0;
         const_cast<unsigned long long*>(A.slots)[kXBase + kXWords + l] = pv.b1;
     }
 }
 
-// all threads; totals returned to every thread
-__device__ __forceinline__ void gather(const SweepArgs& A, unsigned long long seq, XPrev& pv, double& ta, double& tb,
-                                       int& te, Smem& sm, unsigned long long* stamp = nullptr) {
-    if (threadIdx.x < 32) {
-        const int l = threadIdx.x;
-        const unsigned buf = static_cast<unsigned>(seq & 1ull);
-        unsigned long long diff = 0;
-        if (l < kXWords) {
-            const unsigned long long* p = A.slots + static_cast<size_t>(buf) * kXWords * kXStride +
-                                          static_cast<size_t>(l) * kXStride;
-            const unsigned long long prev = buf ? pv.b1 : pv.b0;
-            unsigned long long v;
-            do {
-                v = ld_poll(p);
-                diff = v - prev;
-            } while ((diff >> 50) < static_cast<unsigned long long>(A.P));
-            if (buf) pv.b1 = v;
-            else pv.b0 = v;
-        }
-        __syncwarp();
-        if (stamp && l == 0) *stamp = gtimer();
-        const unsigned long long d = diff & kXData;
-        unsigned long long L[kXWords];
-#pragma unroll
-        for (int i = 0; i < kXWords; ++i) L[i] = __shfl_sync(0xffffffffu, d, i);
-        if (l == 0) {
-            sm.pa[0] = from_limbs(L[0], L[1], L[2]);
-            sm.pb[0] = from_limbs(L[3], L[4], L[5]);
-            sm.pe[0] = L[6] != 0 ? 1 : 0;
-        }
+// warp 0 only: wait for the exchange `seq`, return the totals in every lane
+__device__ __forceinline__ void poll(const SweepArgs& A, unsigned long long seq, XPrev& pv, double& ta, double& tb,
+                                     int& te, unsigned long long* stamp) {
+    const int l = lane_id();
+    const unsigned buf = static_cast<unsigned>(seq & 1ull);
+    unsigned long long diff = 0;
+    if (l < kXWords) {
+        const unsigned long long* p =
+            A.slots + static_cast<size_t>(buf) * kXWords * kXStride + static_cast<size_t>(l) * kXStride;
+        const unsigned long long prev = buf ? pv.b1 : pv.b0;
+        unsigned long long v;
+        do {
+            v = ld_poll(p);
+            diff = v - prev;
+        } while ((diff >> 50) < static_cast<unsigned long long>(A.P));
+        if (buf) pv.b1 = v;
+        else pv.b0 = v;
     }
-    __syncthreads();
-    ta = sm.pa[0];
-    tb = sm.pb[0];
-    te = sm.pe[0];
+    __syncwarp();
+    if (stamp && l == 0) *stamp = gtimer();
+    const unsigned long long d = diff & kXData;
+    // lane 0 rebuilds a from lanes 0..2, lane 3 rebuilds b from lanes 3..5
+    const unsigned long long d1 = __shfl_down_sync(0xffffffffu, d, 1);
+    const unsigned long long d2 = __shfl_down_sync(0xffffffffu, d, 2);
+    const double v = from_limbs(d, d1, d2);
+    ta = __shfl_sync(0xffffffffu, v, 0);
+    tb = __shfl_sync(0xffffffffu, v, 3);
+    te = __shfl_sync(0xffffffffu, d, 6) != 0 ? 1 : 0;
 }
+
+// ---- pair slots -------------------------------------------------------------------
 
 // Index data of one pair slot: the pair, whether it starts a subject run
 // (head) and whether the run continues past it.
@@ -312,7 +334,7 @@ struct PairSlot {
 
 // Loads of one pair slot, issued ahead of use: the pair plus (lane 0 / lane
 // 31 only) the subjects just outside the warp.  finalize_slot() turns them
-// into head / continuation flags with warp shuffles; all lanes must call it.
+// into head / continuation flags with warp shuffles (all lanes of a warp).
 struct RawSlot {
     int2 pr;
     int edge; // lane 0: subject of pair p-1 ; lane 31: subject of pair p+1
@@ -322,7 +344,7 @@ struct RawSlot {
 __device__ __forceinline__ RawSlot issue_slot(const int2* __restrict__ pairs, int64_t p, int64_t p0, int64_t p1) {
     RawSlot r;
     const bool valid = p < p1;
-    const int l = threadIdx.x & 31;
+    const int l = lane_id();
     r.pr = valid ? ld_pair(pairs + p) : make_int2(-1, -1);
     r.first = valid && p == p0;
     r.last_valid = p + 1 < p1;
@@ -334,7 +356,7 @@ __device__ __forceinline__ RawSlot issue_slot(const int2* __restrict__ pairs, in
 
 __device__ __forceinline__ PairSlot finalize_slot(const RawSlot& r) {
     PairSlot s;
-    const int l = threadIdx.x & 31;
+    const int l = lane_id();
     int prev = __shfl_up_sync(0xffffffffu, r.pr.y, 1);
     int next = __shfl_down_sync(0xffffffffu, r.pr.y, 1);
     if (l == 0) prev = r.edge;
@@ -346,9 +368,65 @@ __device__ __forceinline__ PairSlot finalize_slot(const RawSlot& r) {
     return s;
 }
 
+__device__ __forceinline__ PairSlot invalid_slot() {
+    PairSlot s;
+    s.pr = make_int2(-1, -1);
+    s.head = false;
+    s.cont = false;
+    return s;
+}
+
 __device__ __forceinline__ PairSlot load_slot(const int2* __restrict__ pairs, int64_t p, int64_t p0, int64_t p1) {
     return finalize_slot(issue_slot(pairs, p, p0, p1));
 }
+
+__device__ __forceinline__ bool slot_valid(const PairSlot& s) { return s.pr.x >= 0; }
+
+// warp-uniform: does this warp hold any pair of tile v of [p0, p1)?
+__device__ __forceinline__ bool warp_active(int v, int64_t p0, int64_t p1) {
+    return p0 + static_cast<int64_t>(v) * kT + (static_cast<int>(threadIdx.x) & ~31) < p1;
+}
+
+struct Cached {
+    PairSlot slot[kCached];
+};
+
+struct RawCached {
+    RawSlot slot[kCached];
+};
+
+__device__ __forceinline__ void load_cached(const ShardArgs& S, int64_t p0, int64_t p1, Cached& C) {
+#pragma unroll
+    for (int v = 0; v < kCached; ++v) {
+        if (warp_active(v, p0, p1)) C.slot[v] = load_slot(S.pairs, p0 + static_cast<int64_t>(v) * kT + threadIdx.x, p0, p1);
+        else C.slot[v] = invalid_slot();
+    }
+}
+
+__device__ __forceinline__ void issue_cached(const ShardArgs& S, int64_t p0, int64_t p1, RawCached& R) {
+#pragma unroll
+    for (int v = 0; v < kCached; ++v) {
+        if (warp_active(v, p0, p1)) {
+            R.slot[v] = issue_slot(S.pairs, p0 + static_cast<int64_t>(v) * kT + threadIdx.x, p0, p1);
+        } else {
+            R.slot[v].pr = make_int2(-1, -1);
+            R.slot[v].edge = -1;
+            R.slot[v].first = false;
+            R.slot[v].last_valid = false;
+        }
+    }
+}
+
+__device__ __forceinline__ void finalize_cached(const RawCached& R, Cached& C) {
+#pragma unroll
+    for (int v = 0; v < kCached; ++v) {
+        // warp-uniform: a warp whose tile is empty has every lane invalid
+        if (__any_sync(0xffffffffu, R.slot[v].pr.x >= 0)) C.slot[v] = finalize_slot(R.slot[v]);
+        else C.slot[v] = invalid_slot();
+    }
+}
+
+// ---- fused grad/hess and sparse update ------------------------------------------
 
 // Fused per-run reduction term (engine.hpp:108-129): numerator summed in
 // ascending row order, w = min(num/den, 1), nw = n*w, (nw, nw*(1-w)).
@@ -403,21 +481,14 @@ __device__ __forceinline__ double run_tail_update(const int2* __restrict__ pairs
     return den;
 }
 
-struct Cached {
-    PairSlot slot[kCached];
-};
-
-// Per-lane data of the register-cached tiles (the first kCached*T pairs of
-// the CTA's slice).  Every lane gathers its own era record; run heads also
-// gather the subject record.  Runs are combined from shared memory in
-// ascending pair order, so the head never issues a dependent global load
-// unless its run spills past the cached tiles.
+// Per-lane records of the register tiles.  Every lane gathers its own era
+// record; run heads also gather the subject record.  Runs are combined from
+// shared memory in ascending pair order, so a head never issues a dependent
+// global load unless its run spills past the register tiles.
 struct HeadRegs {
     double xb[kCached], le[kCached], den[kCached];
     int len[kCached], n[kCached];
 };
-
-__device__ __forceinline__ bool slot_valid(const PairSlot& s) { return s.pr.x >= 0; }
 
 __device__ __forceinline__ void gather_records(const ShardArgs& S, const Cached& C, HeadRegs& H) {
     EraRec* era = S.era;
@@ -481,7 +552,7 @@ __device__ __forceinline__ void gh_compute(const ShardArgs& S, const Cached& C, 
     const int ncached = static_cast<int>(min(p1 - p0, static_cast<int64_t>(kCap)));
 #pragma unroll
     for (int v = 0; v < kCached; ++v) {
-        const int pos = v * kSweepThreads + static_cast<int>(threadIdx.x);
+        const int pos = v * kT + static_cast<int>(threadIdx.x);
         if (slot_valid(C.slot[v])) {
             sm.stage[pos] = H.le[v];
             sm.ssub[pos] = C.slot[v].pr.y;
@@ -494,7 +565,7 @@ __device__ __forceinline__ void gh_compute(const ShardArgs& S, const Cached& C, 
             double num = H.le[v];
             if (C.slot[v].cont) {
                 const int s = C.slot[v].pr.y;
-                int q = v * kSweepThreads + static_cast<int>(threadIdx.x) + 1;
+                int q = v * kT + static_cast<int>(threadIdx.x) + 1;
                 while (q < ncached && sm.ssub[q] == s) num = __dadd_rn(num, sm.stage[q++]);
                 if (q == ncached && p0 + q < p1 && ld_pair(pairs + p0 + q).y == s)
                     num = run_tail_numerator(pairs, era, p0 + q, p1, s, num);
@@ -503,7 +574,7 @@ __device__ __forceinline__ void gh_compute(const ShardArgs& S, const Cached& C, 
         }
     }
     // streamed remainder: head threads own their runs
-    for (int64_t base = p0 + static_cast<int64_t>(kCap); base < p1; base += kSweepThreads) {
+    for (int64_t base = p0 + static_cast<int64_t>(kCap); base < p1; base += kT) {
         const int64_t p = base + threadIdx.x;
         const PairSlot s = load_slot(pairs, p, p0, p1);
         if (s.head) {
@@ -514,12 +585,6 @@ __device__ __forceinline__ void gh_compute(const ShardArgs& S, const Cached& C, 
             run_terms(num, sr.den, sr.n, gs, hs, err);
         }
     }
-}
-
-__device__ __forceinline__ void gh_slice(const ShardArgs& S, const Cached& C, int64_t p0, int64_t p1, HeadRegs& H,
-                                         double& gs, double& hs, int& err, Smem& sm) {
-    gather_records(S, C, H);
-    gh_compute(S, C, p0, p1, H, gs, hs, err, sm);
 }
 
 __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C, const HeadRegs& H, bool cached,
@@ -534,7 +599,7 @@ __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C
         // fresh - old for its run head
 #pragma unroll
         for (int v = 0; v < kCached; ++v) {
-            const int pos = v * kSweepThreads + static_cast<int>(threadIdx.x);
+            const int pos = v * kT + static_cast<int>(threadIdx.x);
             if (slot_valid(C.slot[v])) {
                 const double updated = __dadd_rn(H.xb[v], d);
                 double diff = 0.0;
@@ -559,7 +624,7 @@ __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C
 #pragma unroll
         for (int v = 0; v < kCached; ++v) {
             if (C.slot[v].head) {
-                const int pos = v * kSweepThreads + static_cast<int>(threadIdx.x);
+                const int pos = v * kT + static_cast<int>(threadIdx.x);
                 int q = pos;
                 double den = __dadd_rn(H.den[v], sm.stage[q++]);
                 if (C.slot[v].cont) {
@@ -580,8 +645,8 @@ __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C
             }
         }
     }
-    const int64_t start = cached ? p0 + static_cast<int64_t>(kCached) * kSweepThreads : p0;
-    for (int64_t base = start; base < p1; base += kSweepThreads) {
+    const int64_t start = cached ? p0 + static_cast<int64_t>(kCap) : p0;
+    for (int64_t base = start; base < p1; base += kT) {
         const int64_t p = base + threadIdx.x;
         const PairSlot s = load_slot(pairs, p, p0, p1);
         if (s.head) {
@@ -595,30 +660,16 @@ __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C
     }
 }
 
-__device__ __forceinline__ void load_cached(const ShardArgs& S, int64_t p0, int64_t p1, Cached& C) {
+__device__ __forceinline__ bool any_slot(const Cached& C) {
+    bool a = false;
 #pragma unroll
-    for (int v = 0; v < kCached; ++v) {
-        const int64_t p = p0 + static_cast<int64_t>(v) * kSweepThreads + threadIdx.x;
-        C.slot[v] = load_slot(S.pairs, p, p0, p1);
-    }
+    for (int v = 0; v < kCached; ++v) a = a || slot_valid(C.slot[v]);
+    return a;
 }
 
-struct RawCached {
-    RawSlot slot[kCached];
-};
+// ---- the persistent kernel ------------------------------------------------------
 
-__device__ __forceinline__ void issue_cached(const ShardArgs& S, int64_t p0, int64_t p1, RawCached& R) {
-#pragma unroll
-    for (int v = 0; v < kCached; ++v) {
-        const int64_t p = p0 + static_cast<int64_t>(v) * kSweepThreads + threadIdx.x;
-        R.slot[v] = issue_slot(S.pairs, p, p0, p1);
-    }
-}
-
-__device__ __forceinline__ void finalize_cached(const RawCached& R, Cached& C) {
-#pragma unroll
-    for (int v = 0; v < kCached; ++v) C.slot[v] = finalize_slot(R.slot[v]);
-}
+enum StepStatus { ST_OK = 0, ST_REMOTE_ERR = 1, ST_STEP_ERR = 2, ST_NONFINITE = 3 };
 
 __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant__ SweepArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -651,21 +702,23 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         const int64_t p0 = split_c[static_cast<int64_t>(j) * stride], p1 = split_c[static_cast<int64_t>(j) * stride + 1];
         load_cached(S, p0, p1, C);
         double gs = 0.0, hs = 0.0;
-        gh_slice(S, C, p0, p1, H, gs, hs, err, sm);
+        gather_records(S, C, H);
+        gh_compute(S, C, p0, p1, H, gs, hs, err, sm);
         if (err) record_error(S.err, err, 0.0);
-        block_reduce(gs, hs, err, sm);
-        double tg, th;
-        int te;
+        block_reduce(gs, hs, err, false, sm);
         publish(A, seq, gs, hs, err);
-        gather(A, seq, pv, tg, th, te, sm);
-        ++seq;
-        if (c == 0 && threadIdx.x == 0) {
-            S.res->g = __dsub_rn(A.y_dot_x[j], tg);
-            S.res->h = th == 0.0 ? 0.0 : -th;
-            S.res->err_remote = te;
-            if (si == 0) *A.counter = seq;
+        if (threadIdx.x < 32) {
+            double tg, th;
+            int te;
+            poll(A, seq, pv, tg, th, te, nullptr);
+            if (c == 0 && threadIdx.x == 0) {
+                S.res->g = __dsub_rn(A.y_dot_x[j], tg);
+                S.res->h = th == 0.0 ? 0.0 : -th;
+                S.res->err_remote = te;
+                if (si == 0) *A.counter = seq + 1;
+            }
+            if (c == 0 && si == 0) xprev_store(A, pv);
         }
-        if (c == 0 && si == 0) xprev_store(A, pv);
         return;
     }
 
@@ -676,23 +729,30 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
     // gathered speculatively.  The update of idx then records what it wrote
     // (shared memory + subject hash table) and idx+1 repairs the few records
     // it touched, so no HBM gather sits on the per-coordinate critical path.
+    // Scalar work (exchange, penalized step, clamp) runs on warp 0 only and
+    // is broadcast through shared memory at the one barrier that follows.
     long long nvisit = 0, nmoved = 0;
     const int V = A.nvisit;
     const longlong2* vs = S.vsplit + static_cast<size_t>(c) * static_cast<size_t>(V);
     bool aborted = false;
+    const bool w0 = threadIdx.x < 32;
     if (V > 0) {
-        for (int i = threadIdx.x; i < kHt; i += kSweepThreads) sm.htk[i] = -1;
+        for (int i = threadIdx.x; i < kHt; i += kT) sm.htk[i] = -1;
         const longlong2 z2 = make_longlong2(0, 0);
         longlong2 cur = vs[0];
         int j = A.visit[0];
-        double bj = S.beta[j], rj = S.trust[j], ydx = A.y_dot_x[j];
+        double bj = 0.0, rj = 1.0, ydx = 0.0;
+        if (w0) {
+            bj = S.beta[j];
+            rj = S.trust[j];
+            ydx = A.y_dot_x[j];
+        }
         load_cached(S, cur.x, cur.y, C);
         longlong2 nxt = V > 1 ? vs[1] : z2;
         int jn = V > 1 ? A.visit[1] : 0;
         Cached N;
         load_cached(S, nxt.x, nxt.y, N);
         longlong2 nxt2 = V > 2 ? vs[2] : z2;
-        int jn2 = V > 2 ? A.visit[2] : 0;
         HeadRegs SH;
         bool spec = false;
         int myht[kCached];
@@ -706,18 +766,22 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             const int64_t p0 = cur.x, p1 = cur.y;
             if (tr && idx < A.ntrace) trb[idx * trs + 0] = gtimer();
             double gs = 0.0, hs = 0.0;
+            const bool active = any_slot(C) || (p1 - p0 > kCap);
+            const bool idle = !__any_sync(0xffffffffu, active);
             if (!(A.dbg & 1)) {
-                if (spec) repair(C, H, sm);
-                else gather_records(S, C, H);
+                if (!idle) {
+                    if (spec) repair(C, H, sm);
+                    else gather_records(S, C, H);
+                }
                 gh_compute(S, C, p0, p1, H, gs, hs, err, sm);
             }
             if (err) record_error(S.err, err, errv);
             // The publish below must not be observable before this
             // coordinate's beta/trust loads complete (CTA 0 overwrites them
             // after the exchange): folding them into the published error
-            // word makes the record store data-dependent on the loads.
+            // word makes the adds data-dependent on the loads.
             int e = err | ((bj != bj) || (rj != rj) ? 1 : 0);
-            block_reduce(gs, hs, e, sm);
+            block_reduce(gs, hs, e, idle && !(A.dbg & 1) ? true : idle, sm);
             // every lookup of the previous coordinate's entries is done
 #pragma unroll
             for (int v = 0; v < kCached; ++v) {
@@ -733,61 +797,72 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             issue_cached(S, nxt2.x, nxt2.y, NR);
             const bool more = idx + 1 < V;
             const bool spec_next = more && !(A.dbg & 16) && (p1 - p0) <= kCap && (nxt.y - nxt.x) <= kCap;
-            if (spec_next && !(A.dbg & 32)) gather_records(S, N, SH);
-            const double bn = more ? S.beta[jn] : 0.0;
-            const double rn = more ? S.trust[jn] : 1.0;
-            const double yn = more ? A.y_dot_x[jn] : 0.0;
+            if (spec_next) gather_records(S, N, SH);
             const longlong2 nxt3 = idx + 3 < V ? vs[idx + 3] : z2;
-            const int jn3 = idx + 3 < V ? A.visit[idx + 3] : 0;
-            if (tr && idx < A.ntrace) trb[idx * trs + 4] = gtimer();
-            double tg, th;
-            int te;
-            if (A.dbg & 4) {
+            int jn2 = 0;
+            double bn = 0.0, rn = 1.0, yn = 0.0;
+            if (w0) {
+                if (more) {
+                    bn = S.beta[jn];
+                    rn = S.trust[jn];
+                    yn = A.y_dot_x[jn];
+                }
+                jn2 = idx + 2 < V ? A.visit[idx + 2] : 0;
+                if (tr && idx < A.ntrace) trb[idx * trs + 4] = gtimer();
+                // exchange, then the scalar step (prior.hpp:72-122,
+                // solver.hpp:131-150), broadcast with the next barrier
+                double tg, th;
+                int te = 0;
+                if (A.dbg & 4) {
+                    tg = gs;
+                    th = hs;
+                } else {
+                    poll(A, seq, pv, tg, th, te, (tr && idx < A.ntrace) ? trb + idx * trs + 5 : nullptr);
+                }
+                int status = ST_OK;
+                double delta = 0.0;
+                if (te) {
+                    status = ST_REMOTE_ERR;
+                } else {
+                    const double g = __dsub_rn(ydx, tg);
+                    const double h = th == 0.0 ? 0.0 : -th;
+                    double step = 0.0;
+                    const int serr = penalized_step(A.prior, bj, g, h, &step);
+                    if (serr) {
+                        status = ST_STEP_ERR;
+                        if (c == 0 && threadIdx.x == 0) record_error(S.err, serr, h);
+                    } else {
+                        delta = clamp_step(step, rj);
+                        if (delta != 0.0 && !isfinite(delta)) {
+                            status = ST_NONFINITE;
+                            if (c == 0 && threadIdx.x == 0) record_error(S.err, DERR_STEP_NONFINITE, delta);
+                        }
+                    }
+                }
                 if (threadIdx.x == 0) {
-                    sm.pa[0] = gs;
-                    sm.pb[0] = hs;
+                    sm.delta = delta;
+                    sm.status = status;
+                    if (c == 0 && status == ST_OK) {
+                        S.moved[idx] = delta != 0.0 ? 1 : 0;
+                        S.beta[j] = __dadd_rn(bj, delta);
+                        S.trust[j] = next_trust(delta, rj);
+                    }
                 }
-                __syncthreads();
-                tg = sm.pa[0];
-                th = sm.pb[0];
-                te = 0;
-            } else {
-                gather(A, seq, pv, tg, th, te, sm, (tr && idx < A.ntrace) ? trb + idx * trs + 5 : nullptr);
-                ++seq;
             }
+            if (!(A.dbg & 4)) ++seq;
+            __syncthreads();
             if (tr && idx < A.ntrace) trb[idx * trs + 2] = gtimer();
-            if (spec_next && (A.dbg & 32)) gather_records(S, N, SH);
-            if (te) { // an overflow or bad denominator somewhere: stop everywhere
+            const int status = sm.status;
+            const double delta = sm.delta;
+            if (status != ST_OK) {
                 aborted = true;
-                if (c == 0 && threadIdx.x == 0) S.res->err_remote = 1;
+                if (status == ST_REMOTE_ERR && c == 0 && threadIdx.x == 0) S.res->err_remote = 1;
                 break;
             }
-            const double g = __dsub_rn(ydx, tg);
-            const double h = th == 0.0 ? 0.0 : -th;
-            double step = 0.0;
-            const int serr = penalized_step(A.prior, bj, g, h, &step);
-            if (serr) {
-                if (c == 0 && threadIdx.x == 0) record_error(S.err, serr, h);
-                aborted = true;
-                break;
-            }
-            const double delta = clamp_step(step, rj);
             ++nvisit;
-            if (c == 0 && threadIdx.x == 0) S.moved[idx] = delta != 0.0 ? 1 : 0;
-            double bnew = bj;
             if (delta != 0.0) {
-                if (!isfinite(delta)) {
-                    if (c == 0 && threadIdx.x == 0) record_error(S.err, DERR_STEP_NONFINITE, delta);
-                    aborted = true;
-                    break;
-                }
                 ++nmoved;
                 if (!(A.dbg & 2)) update_slice(S, C, H, true, p0, p1, delta, err, errv, sm, spec_next, myht);
-                bnew = __dadd_rn(bj, delta);
-            }
-            if (c == 0 && threadIdx.x == 0) {
-                S.beta[j] = bnew;
-                S.trust[j] = next_trust(delta, rj);
             }
             __syncthreads(); // slice writes of this coordinate before the next reads
             if (tr && idx < A.ntrace) trb[idx * trs + 3] = gtimer();
@@ -800,7 +875,6 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             nxt2 = nxt3;
             j = jn;
             jn = jn2;
-            jn2 = jn3;
             bj = bn;
             rj = rn;
             ydx = yn;
@@ -812,7 +886,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         // the next cycle taken in the same pass
         const int e0 = S.cta_era[c], e1 = S.cta_era[c + 1];
         double ch = 0.0, mg = 0.0;
-        for (int k = e0 + static_cast<int>(threadIdx.x); k < e1; k += kSweepThreads) {
+        for (int k = e0 + static_cast<int>(threadIdx.x); k < e1; k += kT) {
             EraRec* r = S.era + k;
             const double xb = r->xb;
             ch = __dadd_rn(ch, fabs(__dsub_rn(xb, r->snap)));
@@ -821,21 +895,24 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         }
         if (err) record_error(S.err, err, errv);
         int e = err;
-        block_reduce(ch, mg, e, sm);
-        double tch, tmg;
-        int te;
+        block_reduce(ch, mg, e, false, sm);
         publish(A, seq, ch, mg, e);
-        gather(A, seq, pv, tch, tmg, te, sm);
-        ++seq;
-        if (c == 0 && threadIdx.x == 0) {
-            S.res->change = tch;
-            S.res->magnitude = tmg;
-            S.res->criterion = A.normalized ? tch / (1.0 + tmg) : tch;
-            S.res->err_remote = te;
+        if (w0) {
+            double tch, tmg;
+            int te;
+            poll(A, seq, pv, tch, tmg, te, nullptr);
+            if (c == 0 && threadIdx.x == 0) {
+                S.res->change = tch;
+                S.res->magnitude = tmg;
+                S.res->criterion = A.normalized ? tch / (1.0 + tmg) : tch;
+                S.res->err_remote = te;
+            }
         }
+        ++seq;
     } else if (err) {
         record_error(S.err, err, errv);
     }
+    if (err) record_error(S.err, err, errv);
     if (c == 0 && threadIdx.x == 0) {
         S.res->visited = nvisit;
         S.res->moved = nmoved;

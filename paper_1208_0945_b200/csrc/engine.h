@@ -61,7 +61,7 @@ struct DevErr {
     double value;
 };
 
-constexpr int kSweepThreads = 512;
+constexpr int kSweepThreads = 256;
 constexpr int kMaxLocalShards = 8;
 constexpr int kMaxRanks = 8;
 constexpr int kXchgAreaWords = 512; // exchange words (2 x 7, 256 B apart) + running totals
