@@ -50,10 +50,11 @@ namespace {
 constexpr int kModeSweep = 0;
 constexpr int kModeGradHess = 1;
 constexpr int kModeUpdate = 2;
-constexpr int kT = kSweepThreads;   // threads per CTA
-constexpr int kCached = 4;          // register tiles of the slice (pairs p0 + v*T + tid)
+constexpr int kT = kSweepThreads;   // threads per CTA; warp 0 is the control warp
+constexpr int kD = kT - 32;         // data threads (warps 1..): tile v holds pairs p0 + v*kD + (tid - 32)
+constexpr int kCached = 5;          // register tiles per data thread
 constexpr int kWarps = kT / 32;
-constexpr int kCap = kCached * kT;  // pairs a CTA keeps in registers per coordinate
+constexpr int kCap = kCached * kD;  // pairs a CTA keeps in registers per coordinate
 constexpr int kLLBlocks = 592;      // fixed => deterministic LL reduction
 constexpr int kLLThreads = 256;
 constexpr double kXbBound = 700.0;  // xbeta_bound<double> engine.hpp:20-23
@@ -62,6 +63,7 @@ constexpr int kHt = 1 << kHtBits;
 
 struct ShardArgs {
     const int2* pairs;
+    double* snap;
     const longlong2* vsplit; // [ctas][nvisit] (p0, p1) of each CTA's slice in visit order
     uint8_t* moved;          // [nvisit] delta != 0 per visited coordinate (CTA 0 writes)
     const int64_t* col_ptr;
@@ -138,6 +140,33 @@ __device__ __forceinline__ unsigned long long ld_poll(const unsigned long long* 
     return v;
 }
 __device__ __forceinline__ int2 ld_pair(const int2* p) { return __ldg(p); }
+
+// one 16-byte load of an era record (read-write data: no read-only path)
+struct Rec {
+    double xb;
+    int len, y;
+};
+__device__ __forceinline__ Rec ld_rec(const EraRec* p) {
+    const int4 q = *reinterpret_cast<const int4*>(p);
+    Rec r;
+    r.xb = __hiloint2double(q.y, q.x);
+    r.len = q.z;
+    r.y = q.w;
+    return r;
+}
+// l * exp(x'beta), the reference's l_exp_xbeta expression (engine.hpp:77-78,224-225)
+__device__ __forceinline__ double lexp(int len, double xb) { return __dmul_rn(static_cast<double>(len), exp(xb)); }
+struct Subj {
+    double den;
+    int n;
+};
+__device__ __forceinline__ Subj ld_subj(const SubjRec* p) {
+    const int4 q = *reinterpret_cast<const int4*>(p);
+    Subj r;
+    r.den = __hiloint2double(q.y, q.x);
+    r.n = q.z;
+    return r;
+}
 
 __device__ __forceinline__ void record_error(DevErr* e, int code, double value) {
     if (atomicCAS(&e->code, 0, code) == 0) e->value = value;
@@ -382,9 +411,12 @@ __device__ __forceinline__ PairSlot load_slot(const int2* __restrict__ pairs, in
 
 __device__ __forceinline__ bool slot_valid(const PairSlot& s) { return s.pr.x >= 0; }
 
-// warp-uniform: does this warp hold any pair of tile v of [p0, p1)?
+__device__ __forceinline__ int data_tid() { return static_cast<int>(threadIdx.x) - 32; }
+__device__ __forceinline__ int slot_pos(int v) { return v * kD + data_tid(); }
+
+// warp-uniform: does this (data) warp hold any pair of tile v of [p0, p1)?
 __device__ __forceinline__ bool warp_active(int v, int64_t p0, int64_t p1) {
-    return p0 + static_cast<int64_t>(v) * kT + (static_cast<int>(threadIdx.x) & ~31) < p1;
+    return threadIdx.x >= 32 && p0 + static_cast<int64_t>(v) * kD + ((static_cast<int>(threadIdx.x) & ~31) - 32) < p1;
 }
 
 struct Cached {
@@ -398,7 +430,7 @@ struct RawCached {
 __device__ __forceinline__ void load_cached(const ShardArgs& S, int64_t p0, int64_t p1, Cached& C) {
 #pragma unroll
     for (int v = 0; v < kCached; ++v) {
-        if (warp_active(v, p0, p1)) C.slot[v] = load_slot(S.pairs, p0 + static_cast<int64_t>(v) * kT + threadIdx.x, p0, p1);
+        if (warp_active(v, p0, p1)) C.slot[v] = load_slot(S.pairs, p0 + slot_pos(v), p0, p1);
         else C.slot[v] = invalid_slot();
     }
 }
@@ -407,7 +439,7 @@ __device__ __forceinline__ void issue_cached(const ShardArgs& S, int64_t p0, int
 #pragma unroll
     for (int v = 0; v < kCached; ++v) {
         if (warp_active(v, p0, p1)) {
-            R.slot[v] = issue_slot(S.pairs, p0 + static_cast<int64_t>(v) * kT + threadIdx.x, p0, p1);
+            R.slot[v] = issue_slot(S.pairs, p0 + slot_pos(v), p0, p1);
         } else {
             R.slot[v].pr = make_int2(-1, -1);
             R.slot[v].edge = -1;
@@ -443,7 +475,8 @@ __device__ __forceinline__ void run_terms(double num, double den, int n, double&
 __device__ __forceinline__ double run_tail_numerator(const int2* __restrict__ pairs, const EraRec* era, int64_t q,
                                                      int64_t p1, int s, double num) {
     for (;;) {
-        num = __dadd_rn(num, era[ld_pair(pairs + q).x].le);
+        const Rec r = ld_rec(era + ld_pair(pairs + q).x);
+        num = __dadd_rn(num, lexp(r.len, r.xb));
         ++q;
         if (q >= p1 || ld_pair(pairs + q).y != s) break;
     }
@@ -460,10 +493,9 @@ __device__ __forceinline__ double update_era(EraRec* era, int row, double xb, do
         errv = fabs(updated);
         return den;
     }
-    const double fresh = __dmul_rn(static_cast<double>(len), exp(updated));
+    const double fresh = lexp(len, updated);
     den = __dadd_rn(den, __dsub_rn(fresh, le));
-    double2* rec = reinterpret_cast<double2*>(era + row);
-    *rec = make_double2(updated, fresh);
+    era[row].xb = updated;
     return den;
 }
 
@@ -472,9 +504,8 @@ __device__ __forceinline__ double run_tail_update(const int2* __restrict__ pairs
                                                   int s, double d, double den, int& err, double& errv) {
     for (;;) {
         const int row = ld_pair(pairs + q).x;
-        const double2 xl = *reinterpret_cast<const double2*>(era + row);
-        const int len = era[row].len;
-        den = update_era(era, row, xl.x, xl.y, len, d, den, err, errv);
+        const Rec r = ld_rec(era + row);
+        den = update_era(era, row, r.xb, lexp(r.len, r.xb), r.len, d, den, err, errv);
         ++q;
         if (q >= p1 || ld_pair(pairs + q).y != s) break;
     }
@@ -496,17 +527,19 @@ __device__ __forceinline__ void gather_records(const ShardArgs& S, const Cached&
 #pragma unroll
     for (int v = 0; v < kCached; ++v) {
         if (slot_valid(C.slot[v])) {
-            const double2 xl = *reinterpret_cast<const double2*>(era + C.slot[v].pr.x);
-            H.xb[v] = xl.x;
-            H.le[v] = xl.y;
-            H.len[v] = era[C.slot[v].pr.x].len;
+            const Rec r = ld_rec(era + C.slot[v].pr.x);
+            H.xb[v] = r.xb;
+            H.len[v] = r.len;
             if (C.slot[v].head) {
-                const SubjRec sr = subj[C.slot[v].pr.y];
+                const Subj sr = ld_subj(subj + C.slot[v].pr.y);
                 H.den[v] = sr.den;
                 H.n[v] = sr.n;
             }
         }
     }
+#pragma unroll
+    for (int v = 0; v < kCached; ++v)
+        if (slot_valid(C.slot[v])) H.le[v] = lexp(H.len[v], H.xb[v]);
 }
 
 __device__ __forceinline__ int ht_hash(int s) {
@@ -552,8 +585,8 @@ __device__ __forceinline__ void gh_compute(const ShardArgs& S, const Cached& C, 
     const int ncached = static_cast<int>(min(p1 - p0, static_cast<int64_t>(kCap)));
 #pragma unroll
     for (int v = 0; v < kCached; ++v) {
-        const int pos = v * kT + static_cast<int>(threadIdx.x);
         if (slot_valid(C.slot[v])) {
+            const int pos = slot_pos(v);
             sm.stage[pos] = H.le[v];
             sm.ssub[pos] = C.slot[v].pr.y;
         }
@@ -565,7 +598,7 @@ __device__ __forceinline__ void gh_compute(const ShardArgs& S, const Cached& C, 
             double num = H.le[v];
             if (C.slot[v].cont) {
                 const int s = C.slot[v].pr.y;
-                int q = v * kT + static_cast<int>(threadIdx.x) + 1;
+                int q = slot_pos(v) + 1;
                 while (q < ncached && sm.ssub[q] == s) num = __dadd_rn(num, sm.stage[q++]);
                 if (q == ncached && p0 + q < p1 && ld_pair(pairs + p0 + q).y == s)
                     num = run_tail_numerator(pairs, era, p0 + q, p1, s, num);
@@ -578,9 +611,9 @@ __device__ __forceinline__ void gh_compute(const ShardArgs& S, const Cached& C, 
         const int64_t p = base + threadIdx.x;
         const PairSlot s = load_slot(pairs, p, p0, p1);
         if (s.head) {
-            const double le = era[s.pr.x].le;
-            const SubjRec sr = subj[s.pr.y];
-            double num = le;
+            const Rec r = ld_rec(era + s.pr.x);
+            const Subj sr = ld_subj(subj + s.pr.y);
+            double num = lexp(r.len, r.xb);
             if (s.cont) num = run_tail_numerator(pairs, era, p + 1, p1, s.pr.y, num);
             run_terms(num, sr.den, sr.n, gs, hs, err);
         }
@@ -599,17 +632,17 @@ __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C
         // fresh - old for its run head
 #pragma unroll
         for (int v = 0; v < kCached; ++v) {
-            const int pos = v * kT + static_cast<int>(threadIdx.x);
             if (slot_valid(C.slot[v])) {
+                const int pos = slot_pos(v);
                 const double updated = __dadd_rn(H.xb[v], d);
                 double diff = 0.0;
                 if (!(fabs(updated) <= kXbBound)) {
                     err = DERR_OVERFLOW;
                     errv = fabs(updated);
                 } else {
-                    const double fresh = __dmul_rn(static_cast<double>(H.len[v]), exp(updated));
+                    const double fresh = lexp(H.len[v], updated);
                     diff = __dsub_rn(fresh, H.le[v]);
-                    *reinterpret_cast<double2*>(era + C.slot[v].pr.x) = make_double2(updated, fresh);
+                    era[C.slot[v].pr.x].xb = updated;
                     if (record) {
                         sm.jxb[pos] = updated;
                         sm.jle[pos] = fresh;
@@ -624,7 +657,7 @@ __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C
 #pragma unroll
         for (int v = 0; v < kCached; ++v) {
             if (C.slot[v].head) {
-                const int pos = v * kT + static_cast<int>(threadIdx.x);
+                const int pos = slot_pos(v);
                 int q = pos;
                 double den = __dadd_rn(H.den[v], sm.stage[q++]);
                 if (C.slot[v].cont) {
@@ -650,10 +683,9 @@ __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C
         const int64_t p = base + threadIdx.x;
         const PairSlot s = load_slot(pairs, p, p0, p1);
         if (s.head) {
-            const double2 xl = *reinterpret_cast<const double2*>(era + s.pr.x);
-            const int len = era[s.pr.x].len;
+            const Rec r = ld_rec(era + s.pr.x);
             double den = subj[s.pr.y].den;
-            den = update_era(era, s.pr.x, xl.x, xl.y, len, d, den, err, errv);
+            den = update_era(era, s.pr.x, r.xb, lexp(r.len, r.xb), r.len, d, den, err, errv);
             if (s.cont) den = run_tail_update(pairs, era, p + 1, p1, s.pr.y, d, den, err, errv);
             subj[s.pr.y].den = den;
         }
@@ -887,11 +919,10 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         const int e0 = S.cta_era[c], e1 = S.cta_era[c + 1];
         double ch = 0.0, mg = 0.0;
         for (int k = e0 + static_cast<int>(threadIdx.x); k < e1; k += kT) {
-            EraRec* r = S.era + k;
-            const double xb = r->xb;
-            ch = __dadd_rn(ch, fabs(__dsub_rn(xb, r->snap)));
+            const double xb = S.era[k].xb;
+            ch = __dadd_rn(ch, fabs(__dsub_rn(xb, S.snap[k])));
             if (A.normalized) mg = __dadd_rn(mg, fabs(xb));
-            r->snap = xb;
+            S.snap[k] = xb;
         }
         if (err) record_error(S.err, err, errv);
         int e = err;
@@ -930,8 +961,6 @@ __global__ void k_init_records(EraRec* era, SubjRec* subj, const int32_t* len, c
          k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         EraRec r;
         r.xb = 0.0;
-        r.le = 0.0;
-        r.snap = 0.0;
         r.len = len[k];
         r.y = y[k];
         era[k] = r;
@@ -947,10 +976,11 @@ __global__ void k_init_records(EraRec* era, SubjRec* subj, const int32_t* len, c
 }
 
 // xbeta_k = sum over drugs of row k in ascending j of beta_j, skipping
-// zeros (engine.hpp:173-181); then l*exp with the overflow guard
-// (engine.hpp:70-79).  snapshot := xbeta.
-__global__ void k_dense_xb(EraRec* era, const int64_t* __restrict__ csr_ptr, const int32_t* __restrict__ csr_col,
-                           const double* __restrict__ beta, int32_t K, DevErr* err) {
+// zeros (engine.hpp:173-181), with the overflow guard (engine.hpp:70-74).
+// snapshot := xbeta.
+__global__ void k_dense_xb(EraRec* era, double* snap, const int64_t* __restrict__ csr_ptr,
+                           const int32_t* __restrict__ csr_col, const double* __restrict__ beta, int32_t K,
+                           DevErr* err) {
     for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < K;
          k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         double xb = 0.0;
@@ -959,27 +989,36 @@ __global__ void k_dense_xb(EraRec* era, const int64_t* __restrict__ csr_ptr, con
             if (b != 0.0) xb = __dadd_rn(xb, b);
         }
         if (!(fabs(xb) <= kXbBound)) record_error(err, DERR_OVERFLOW, fabs(xb));
-        const int len = era[k].len;
-        const double le = __dmul_rn(static_cast<double>(len), exp(xb));
-        double2* rec = reinterpret_cast<double2*>(era + k);
-        rec[0] = make_double2(xb, le);
-        era[k].snap = xb;
+        era[k].xb = xb;
+        snap[k] = xb;
     }
 }
 
+// denominators: per subject, ascending sum of l*exp(x'beta) (engine.hpp:76-89)
 __global__ void k_dense_den(const EraRec* era, SubjRec* subj, const int32_t* __restrict__ off, int32_t N) {
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < N;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         double total = 0.0;
-        for (int32_t k = off[i]; k < off[i + 1]; ++k) total = __dadd_rn(total, era[k].le);
+        for (int32_t k = off[i]; k < off[i + 1]; ++k) {
+            const Rec r = ld_rec(era + k);
+            total = __dadd_rn(total, lexp(r.len, r.xb));
+        }
         subj[i].den = total;
     }
 }
 
-__global__ void k_snapshot(EraRec* era, int32_t K) {
+__global__ void k_snapshot(const EraRec* era, double* snap, int32_t K) {
     for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < K;
          k += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        era[k].snap = era[k].xb;
+        snap[k] = era[k].xb;
+}
+
+__global__ void k_lexp(const EraRec* era, double* out, int32_t K) {
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < K;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const Rec r = ld_rec(era + k);
+        out[k] = lexp(r.len, r.xb);
+    }
 }
 
 __global__ void k_ll_partial(const EraRec* era, const SubjRec* subj, int32_t K, int32_t N, double* partial,
@@ -1425,7 +1464,7 @@ namespace {
 void launch_dense(bsccs_state* st) {
     const bsccs_dataset* ds = st->ds;
     const int g = build_grid(ds->device);
-    k_dense_xb<<<g, 256, 0, st->stream>>>(st->era, ds->csr_ptr, ds->csr_col, st->beta, ds->K, st->err);
+    k_dense_xb<<<g, 256, 0, st->stream>>>(st->era, st->snap, ds->csr_ptr, ds->csr_col, st->beta, ds->K, st->err);
     k_dense_den<<<g, 256, 0, st->stream>>>(st->era, st->subj, ds->subject_offsets, ds->N);
     CUDA_TRY(cudaGetLastError());
     count_launches(2);
@@ -1437,6 +1476,7 @@ void alloc_state(bsccs_state* st, const bsccs_dataset* ds) {
     st->ds = ds;
     CUDA_TRY(cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking));
     st->era = dalloc<EraRec>(ds->K, b);
+    st->snap = dalloc<double>(ds->K, b);
     st->subj = dalloc<SubjRec>(ds->N, b);
     st->beta = dalloc<double>(ds->J, b);
     st->trust = dalloc<double>(ds->J, b);
@@ -1494,6 +1534,7 @@ bsccs_state* state_clone(const bsccs_state* src) {
         alloc_state(st, ds);
         CUDA_TRY(cudaStreamSynchronize(src->stream));
         CUDA_TRY(cudaMemcpyAsync(st->era, src->era, sizeof(EraRec) * ds->K, cudaMemcpyDeviceToDevice, st->stream));
+        CUDA_TRY(cudaMemcpyAsync(st->snap, src->snap, sizeof(double) * ds->K, cudaMemcpyDeviceToDevice, st->stream));
         CUDA_TRY(cudaMemcpyAsync(st->subj, src->subj, sizeof(SubjRec) * ds->N, cudaMemcpyDeviceToDevice, st->stream));
         CUDA_TRY(cudaMemcpyAsync(st->beta, src->beta, sizeof(double) * ds->J, cudaMemcpyDeviceToDevice, st->stream));
         st->snap_valid = src->snap_valid;
@@ -1512,6 +1553,8 @@ void state_destroy(bsccs_state* st) {
     if (st->ds) cudaSetDevice(st->ds->device);
     if (st->stream) cudaStreamSynchronize(st->stream);
     cudaFree(st->era);
+    cudaFree(st->snap);
+    cudaFree(st->le_tmp);
     cudaFree(st->subj);
     cudaFree(st->beta);
     cudaFree(st->trust);
@@ -1556,6 +1599,7 @@ SweepArgs base_args(const ExchangePlan& plan) {
         bsccs_state* st = plan.shards[i];
         ShardArgs& s = a.sh[i];
         s.pairs = st->ds->pairs;
+        s.snap = st->snap;
         s.vsplit = st->vsplit;
         s.moved = st->moved;
         s.col_ptr = st->ds->col_ptr;
@@ -1669,13 +1713,20 @@ void state_get(bsccs_state* st, double* beta, double* xbeta, double* le, double*
     DeviceGuard dg(ds->device);
     CUDA_TRY(cudaStreamSynchronize(st->stream));
     if (beta) CUDA_TRY(cudaMemcpy(beta, st->beta, sizeof(double) * ds->J, cudaMemcpyDeviceToHost));
-    if (xbeta || le) {
+    if (xbeta) {
         std::vector<EraRec> e(static_cast<size_t>(ds->K));
         CUDA_TRY(cudaMemcpy(e.data(), st->era, sizeof(EraRec) * ds->K, cudaMemcpyDeviceToHost));
-        for (int32_t k = 0; k < ds->K; ++k) {
-            if (xbeta) xbeta[k] = e[static_cast<size_t>(k)].xb;
-            if (le) le[k] = e[static_cast<size_t>(k)].le;
+        for (int32_t k = 0; k < ds->K; ++k) xbeta[k] = e[static_cast<size_t>(k)].xb;
+    }
+    if (le) { // recomputed on the device with the kernels' own expression
+        if (!st->le_tmp) {
+            int64_t b = 0;
+            st->le_tmp = dalloc<double>(ds->K, b);
         }
+        k_lexp<<<build_grid(ds->device), 256, 0, st->stream>>>(st->era, st->le_tmp, ds->K);
+        count_launches(1);
+        CUDA_TRY(cudaMemcpyAsync(le, st->le_tmp, sizeof(double) * ds->K, cudaMemcpyDeviceToHost, st->stream));
+        CUDA_TRY(cudaStreamSynchronize(st->stream));
     }
     if (den) {
         std::vector<SubjRec> s(static_cast<size_t>(ds->N));
@@ -1688,7 +1739,7 @@ void prepare_snapshot(bsccs_state* st) {
     if (st->snap_valid) return;
     const bsccs_dataset* ds = st->ds;
     DeviceGuard dg(ds->device);
-    k_snapshot<<<build_grid(ds->device), 256, 0, st->stream>>>(st->era, ds->K);
+    k_snapshot<<<build_grid(ds->device), 256, 0, st->stream>>>(st->era, st->snap, ds->K);
     CUDA_TRY(cudaGetLastError());
     count_launches(1);
     st->snap_valid = true;

@@ -10,8 +10,9 @@
 //   csr_ptr/  row -> drug list (ascending), built once by a stable radix sort;
 //   csr_col                  gives dense_recompute the reference's per-row
 //                            addition order (engine.hpp:173-181) w/o atomics
-//   EraRec    32 B / era     {x'beta, l*exp(x'beta), snapshot, len, y}: one
-//                            32-byte sector per scattered era access
+//   EraRec    16 B / era     {x'beta, len, y}: one 16-byte load per scattered
+//                            era access; l*exp(x'beta) recomputed, see below
+//   snap      8 B / era      criterion snapshot (streamed once per cycle)
 //   SubjRec   16 B / subject {denominator, n_i}
 #pragma once
 
@@ -26,14 +27,16 @@
 
 namespace bsccs_b200 {
 
-struct __align__(32) EraRec {
+// l*exp(x'beta) is not stored: the reference keeps l_exp_xbeta[k] ==
+// era_lengths[k] * exp(xbeta[k]) bit for bit at every write (init_state and
+// dense_recompute, engine.hpp:77-78; sparse_delta_update, engine.hpp:221-228),
+// so the device recomputes it from the 16-byte record instead of moving it.
+struct __align__(16) EraRec {
     double xb;   // x'_k beta                      (EngineState::xbeta)
-    double le;   // l_k exp(x'_k beta)             (EngineState::l_exp_xbeta)
-    double snap; // criterion snapshot             (SolverState::xbeta_snapshot)
     int32_t len; // era length l_k                 (Dataset::era_lengths)
     int32_t y;   // event count y_k                (Dataset::event_counts)
 };
-static_assert(sizeof(EraRec) == 32, "EraRec must be one sector");
+static_assert(sizeof(EraRec) == 16, "EraRec must be 16 bytes");
 
 struct __align__(16) SubjRec {
     double den; // sum of le over the subject's eras (EngineState::denominators)
@@ -103,6 +106,8 @@ struct bsccs_state {
     const bsccs_dataset* ds = nullptr;
     cudaStream_t stream = nullptr;
     bsccs_b200::EraRec* era = nullptr;
+    double* snap = nullptr;              // [K] criterion snapshot
+    double* le_tmp = nullptr;            // [K] scratch for state_get
     bsccs_b200::SubjRec* subj = nullptr;
     double* beta = nullptr;
     double* trust = nullptr;
