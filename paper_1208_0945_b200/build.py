@@ -78,11 +78,34 @@ def build_oracle(verbose: bool = False) -> None:
                    stdout=None if verbose else subprocess.DEVNULL)
 
 
+def build_cpp_tests(verbose: bool = False) -> None:
+    """Test infrastructure: the C++ drop-in check (tests/cpp/test_shim.cpp)
+    includes the untouched reference headers, so it is compiled here and the
+    binary travels with the snapshot (tests/cpp/_bin, git-ignored)."""
+    ref = Path(os.environ.get("REF_INCLUDE", "/root/reference/proj/include"))
+    if not ref.exists():
+        return
+    out = ROOT / "tests" / "cpp" / "_bin"
+    out.mkdir(exist_ok=True)
+    src = ROOT / "tests" / "cpp" / "test_shim.cpp"
+    exe = out / "test_shim"
+    deps = [src, LIB, ROOT / "include" / "bsccs_b200_solver.hpp", ROOT / "include" / "bsccs_b200.h"]
+    if exe.exists() and not _stale(exe, deps):
+        return
+    cmd = ["g++", "-std=c++20", "-O2", f"-I{ref}", f"-I{ROOT / 'include'}", str(src), "-o", str(exe),
+           f"-L{LIB_DIR}", "-lbsccs_b200", f"-Wl,-rpath,{LIB_DIR}", "-Wl,-rpath,$ORIGIN/../../../paper_1208_0945_b200/_lib",
+           "-lpthread"]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+
+
 def main(argv: list[str]) -> None:
     force = "--force" in argv
     verbose = "-v" in argv
     build_native(force=force, verbose=verbose)
     build_oracle(verbose=verbose)
+    build_cpp_tests(verbose=verbose)
     print(f"built {LIB}")
 
 
