@@ -22,6 +22,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <mutex>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -1097,10 +1099,18 @@ __global__ void k_pair_meta(const int2* pairs, const int64_t* __restrict__ col_p
         if (ok) ok = off[pr.y] <= pr.x && pr.x < off[pr.y + 1];
         if (ok && p > col_ptr[lo]) ok = pairs[p - 1].x < pr.x;
         if (!ok) {
-            atomicExch(bad, 1);
+            atomicOr(bad, 1);
         } else {
             atomicAdd(row_cnt + pr.x, 1ull);
         }
+    }
+}
+
+__global__ void k_validate_small(const int32_t* off, int32_t N, const int32_t* len, int32_t K, int* bad) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < N || i < K;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        if (i < N && off[i + 1] <= off[i]) atomicOr(bad, 2);
+        if (i < K && len[i] <= 0) atomicOr(bad, 4);
     }
 }
 
@@ -1198,13 +1208,112 @@ int grid_for(int64_t n, int threads, int dev_sms) {
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(g, static_cast<int64_t>(dev_sms) * 32)));
 }
 
+// Stream-ordered allocations from the device's default memory pool, which
+// is told to retain freed memory: re-creating datasets / fit workspaces
+// (bootstrap replicates, the e2e bench) then costs no cudaMalloc/cudaFree.
+void ensure_pool(int device) {
+    static std::atomic<unsigned> done{0};
+    if (device < 32 && (done.load() & (1u << device))) return;
+    cudaMemPool_t pool;
+    CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, device));
+    unsigned long long keep = ~0ull;
+    CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    if (device < 32) done.fetch_or(1u << device);
+}
+
 template <typename T>
-T* dalloc(int64_t count, int64_t& bytes) {
+T* dalloc(int64_t count, int64_t& bytes, cudaStream_t s) {
     T* p = nullptr;
     if (count <= 0) count = 1;
-    CUDA_TRY(cudaMalloc(&p, sizeof(T) * static_cast<size_t>(count)));
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * static_cast<size_t>(count), s));
     bytes += static_cast<int64_t>(sizeof(T)) * count;
     return p;
+}
+
+template <typename T>
+void dfree(T*& p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+}
+
+// Host -> device copy of pageable caller memory through two pinned staging
+// buffers: host threads fill one buffer while the DMA engine drains the other.
+struct Staging {
+    std::mutex m;
+    unsigned char* buf[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    int device = -1;
+    static constexpr size_t kChunk = size_t(64) << 20;
+};
+Staging g_staging;
+
+void parallel_memcpy(void* dst, const void* src, size_t n) {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const size_t T = std::min<size_t>(std::min<size_t>(hw, 16), std::max<size_t>(1, n >> 22));
+    if (T <= 1) {
+        std::memcpy(dst, src, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (size_t t = 0; t < T; ++t) {
+        const size_t a = n * t / T, b = n * (t + 1) / T;
+        th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a); });
+    }
+    for (auto& x : th) x.join();
+}
+
+void h2d(void* dst, const void* src, size_t bytes, cudaStream_t s, int device) {
+    if (bytes == 0) return;
+    if (bytes < (size_t(4) << 20)) { // small: a plain async copy
+        CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+        return;
+    }
+    std::lock_guard<std::mutex> lk(g_staging.m);
+    if (g_staging.device != device) {
+        for (int i = 0; i < 2; ++i) {
+            if (g_staging.buf[i]) cudaFreeHost(g_staging.buf[i]);
+            if (g_staging.ev[i]) cudaEventDestroy(g_staging.ev[i]);
+            CUDA_TRY(cudaMallocHost(&g_staging.buf[i], Staging::kChunk));
+            CUDA_TRY(cudaEventCreateWithFlags(&g_staging.ev[i], cudaEventDisableTiming));
+            CUDA_TRY(cudaEventRecord(g_staging.ev[i], s));
+        }
+        g_staging.device = device;
+    }
+    int k = 0;
+    for (size_t off = 0; off < bytes; off += Staging::kChunk, k ^= 1) {
+        const size_t n = std::min(Staging::kChunk, bytes - off);
+        CUDA_TRY(cudaEventSynchronize(g_staging.ev[k]));
+        parallel_memcpy(g_staging.buf[k], static_cast<const char*>(src) + off, n);
+        CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(dst) + off, g_staging.buf[k], n, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaEventRecord(g_staging.ev[k], s));
+    }
+    // the staging buffers are reused by the next call only after its events
+    CUDA_TRY(cudaEventSynchronize(g_staging.ev[k ^ 1]));
+}
+
+// Small pinned result blocks for the per-state D2H of kernel scalars.
+struct PinnedResults {
+    std::mutex m;
+    std::vector<DevResult*> free_list;
+};
+PinnedResults g_pinned;
+
+DevResult* pinned_result() {
+    std::lock_guard<std::mutex> lk(g_pinned.m);
+    if (g_pinned.free_list.empty()) {
+        DevResult* block = nullptr;
+        CUDA_TRY(cudaMallocHost(&block, sizeof(DevResult) * 64));
+        for (int i = 0; i < 64; ++i) g_pinned.free_list.push_back(block + i);
+    }
+    DevResult* r = g_pinned.free_list.back();
+    g_pinned.free_list.pop_back();
+    return r;
+}
+
+void release_pinned_result(DevResult* r) {
+    if (!r) return;
+    std::lock_guard<std::mutex> lk(g_pinned.m);
+    g_pinned.free_list.push_back(r);
 }
 
 int sm_count(int device) {
@@ -1298,15 +1407,13 @@ bsccs_dataset* dataset_create(int32_t N, int32_t K, int32_t J, int64_t nnz, cons
     if (nnz > 0 && (!rows || !subjects)) input_error("dataset: null pair arrays");
     // small-array invariants on the host (dataset.hpp:45-60)
     if (subject_offsets[0] != 0 || subject_offsets[N] != K) input_error("dataset: subject offsets must span [0, num_eras]");
-    for (int32_t i = 0; i < N; ++i)
-        if (subject_offsets[i + 1] <= subject_offsets[i]) input_error("dataset: every subject needs at least one era");
     if (col_ptr[0] != 0 || col_ptr[J] != nnz) input_error("dataset: column pointers must span [0, nnz]");
     for (int32_t j = 0; j < J; ++j)
         if (col_ptr[j + 1] < col_ptr[j]) input_error("dataset: column pointers must be non-decreasing");
-    for (int32_t k = 0; k < K; ++k)
-        if (era_lengths[k] <= 0) input_error("dataset: era length must be positive");
+    // per-subject and per-era checks run on the device after the upload
 
     DeviceGuard g(device);
+    ensure_pool(device);
     auto* ds = new bsccs_dataset();
     try {
         ds->device = device;
@@ -1318,45 +1425,47 @@ bsccs_dataset* dataset_create(int32_t N, int32_t K, int32_t J, int64_t nnz, cons
         const int C = ds->ctas;
         const int sms = sm_count(device);
         int64_t& B = ds->device_bytes;
-        cudaStream_t s;
-        CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamCreateWithFlags(&ds->stream, cudaStreamNonBlocking));
+        cudaStream_t s = ds->stream;
 
-        ds->pairs = dalloc<int2>(nnz, B);
-        ds->col_ptr = dalloc<int64_t>(J + 1, B);
-        ds->split = dalloc<int64_t>(static_cast<int64_t>(J) * (C + 1), B);
-        ds->cta_era = dalloc<int32_t>(C + 1, B);
-        ds->cta_subj = dalloc<int32_t>(C + 1, B);
-        ds->subject_offsets = dalloc<int32_t>(N + 1, B);
-        ds->events_per_subject = dalloc<int32_t>(N, B);
-        ds->era_lengths = dalloc<int32_t>(K, B);
-        ds->event_counts = dalloc<int32_t>(K, B);
-        ds->csr_ptr = dalloc<int64_t>(static_cast<int64_t>(K) + 1, B);
-        ds->csr_col = dalloc<int32_t>(nnz, B);
-        ds->y_dot_x = dalloc<double>(J, B);
-        ds->col_nonempty = dalloc<uint8_t>(J, B);
-        ds->col_runs = dalloc<int32_t>(J, B);
+        ds->pairs = dalloc<int2>(nnz, B, s);
+        ds->col_ptr = dalloc<int64_t>(J + 1, B, s);
+        ds->split = dalloc<int64_t>(static_cast<int64_t>(J) * (C + 1), B, s);
+        ds->cta_era = dalloc<int32_t>(C + 1, B, s);
+        ds->cta_subj = dalloc<int32_t>(C + 1, B, s);
+        ds->subject_offsets = dalloc<int32_t>(N + 1, B, s);
+        ds->events_per_subject = dalloc<int32_t>(N, B, s);
+        ds->era_lengths = dalloc<int32_t>(K, B, s);
+        ds->event_counts = dalloc<int32_t>(K, B, s);
+        ds->csr_ptr = dalloc<int64_t>(static_cast<int64_t>(K) + 1, B, s);
+        ds->csr_col = dalloc<int32_t>(nnz, B, s);
+        ds->y_dot_x = dalloc<double>(J, B, s);
+        ds->col_nonempty = dalloc<uint8_t>(J, B, s);
+        ds->col_runs = dalloc<int32_t>(J, B, s);
 
-        CUDA_TRY(cudaMemcpyAsync(ds->col_ptr, col_ptr, sizeof(int64_t) * (J + 1), cudaMemcpyHostToDevice, s));
-        CUDA_TRY(cudaMemcpyAsync(ds->subject_offsets, subject_offsets, sizeof(int32_t) * (N + 1), cudaMemcpyHostToDevice, s));
-        CUDA_TRY(cudaMemcpyAsync(ds->events_per_subject, events_per_subject, sizeof(int32_t) * N, cudaMemcpyHostToDevice, s));
-        CUDA_TRY(cudaMemcpyAsync(ds->era_lengths, era_lengths, sizeof(int32_t) * K, cudaMemcpyHostToDevice, s));
-        CUDA_TRY(cudaMemcpyAsync(ds->event_counts, event_counts, sizeof(int32_t) * K, cudaMemcpyHostToDevice, s));
+        h2d(ds->col_ptr, col_ptr, sizeof(int64_t) * (J + 1), s, device);
+        h2d(ds->subject_offsets, subject_offsets, sizeof(int32_t) * (N + 1), s, device);
+        h2d(ds->events_per_subject, events_per_subject, sizeof(int32_t) * N, s, device);
+        h2d(ds->era_lengths, era_lengths, sizeof(int32_t) * K, s, device);
+        h2d(ds->event_counts, event_counts, sizeof(int32_t) * K, s, device);
 
         // scratch for the build: rows, subjects, column ids, sort buffers
         int64_t scratch_bytes = 0;
-        int32_t* d_rows = dalloc<int32_t>(nnz, scratch_bytes);
-        int32_t* d_subj = dalloc<int32_t>(nnz, scratch_bytes);
-        int32_t* d_col = dalloc<int32_t>(nnz, scratch_bytes);
-        unsigned long long* d_cnt = dalloc<unsigned long long>(static_cast<int64_t>(K) + 1, scratch_bytes);
-        long long* d_w = dalloc<long long>(static_cast<int64_t>(N) + 1, scratch_bytes);
-        long long* d_excl = dalloc<long long>(static_cast<int64_t>(N) + 1, scratch_bytes);
-        int* d_bad = dalloc<int>(1, scratch_bytes);
+        int32_t* d_rows = dalloc<int32_t>(nnz, scratch_bytes, s);
+        int32_t* d_subj = dalloc<int32_t>(nnz, scratch_bytes, s);
+        int32_t* d_col = dalloc<int32_t>(nnz, scratch_bytes, s);
+        unsigned long long* d_cnt = dalloc<unsigned long long>(static_cast<int64_t>(K) + 1, scratch_bytes, s);
+        long long* d_w = dalloc<long long>(static_cast<int64_t>(N) + 1, scratch_bytes, s);
+        long long* d_excl = dalloc<long long>(static_cast<int64_t>(N) + 1, scratch_bytes, s);
+        int* d_bad = dalloc<int>(1, scratch_bytes, s);
         if (nnz > 0) {
-            CUDA_TRY(cudaMemcpyAsync(d_rows, rows, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, s));
-            CUDA_TRY(cudaMemcpyAsync(d_subj, subjects, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, s));
+            h2d(d_rows, rows, sizeof(int32_t) * nnz, s, device);
+            h2d(d_subj, subjects, sizeof(int32_t) * nnz, s, device);
         }
         CUDA_TRY(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * (static_cast<size_t>(K) + 1), s));
         CUDA_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
+        k_validate_small<<<grid_for(std::max<int64_t>(N, K), 256, sms), 256, 0, s>>>(ds->subject_offsets, N,
+                                                                                 ds->era_lengths, K, d_bad);
         if (nnz > 0) {
             k_interleave<<<grid_for(nnz, 256, sms), 256, 0, s>>>(d_rows, d_subj, ds->pairs, nnz);
             k_pair_meta<<<grid_for(nnz, 256, sms), 256, 0, s>>>(ds->pairs, ds->col_ptr, J, ds->subject_offsets, N, K,
@@ -1376,8 +1485,7 @@ bsccs_dataset* dataset_create(int32_t N, int32_t K, int32_t J, int64_t nnz, cons
             size_t scan2 = 0;
             CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, scan2, d_w, d_excl, N + 1, s));
             const size_t tb = std::max(std::max(tmp_bytes, sort_bytes), scan2);
-            void* tmp = nullptr;
-            CUDA_TRY(cudaMalloc(&tmp, std::max<size_t>(tb, 16)));
+            unsigned char* tmp = dalloc<unsigned char>(static_cast<int64_t>(std::max<size_t>(tb, 16)), scratch_bytes, s);
             CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, d_cnt,
                                                    reinterpret_cast<unsigned long long*>(ds->csr_ptr), K + 1, s));
             if (nnz > 0) {
@@ -1404,21 +1512,22 @@ bsccs_dataset* dataset_create(int32_t N, int32_t K, int32_t J, int64_t nnz, cons
             } else {
                 k_ydotx<<<J, 256, 0, s>>>(ds->pairs, ds->col_ptr, ds->event_counts, ds->y_dot_x, J);
             }
-            CUDA_TRY(cudaStreamSynchronize(s));
-            CUDA_TRY(cudaFree(tmp));
+            dfree(tmp, s);
         }
         int bad = 0;
-        CUDA_TRY(cudaMemcpy(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost));
-        cudaFree(d_rows);
-        cudaFree(d_subj);
-        cudaFree(d_col);
-        cudaFree(d_cnt);
-        cudaFree(d_w);
-        cudaFree(d_excl);
-        cudaFree(d_bad);
-        CUDA_TRY(cudaStreamDestroy(s));
-        if (bad) input_error("dataset: invalid pair (row/subject out of range, subject not owning its row, "
-                             "or rows not strictly ascending within a column)");
+        CUDA_TRY(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+        dfree(d_rows, s);
+        dfree(d_subj, s);
+        dfree(d_col, s);
+        dfree(d_cnt, s);
+        dfree(d_w, s);
+        dfree(d_excl, s);
+        dfree(d_bad, s);
+        CUDA_TRY(cudaStreamSynchronize(s));
+        if (bad & 2) input_error("dataset: every subject needs at least one era");
+        if (bad & 4) input_error("dataset: era length must be positive");
+        if (bad & 1) input_error("dataset: invalid pair (row/subject out of range, subject not owning its row, "
+                                 "or rows not strictly ascending within a column)");
 
         ds->col_ptr_h.assign(col_ptr, col_ptr + J + 1);
         ds->col_runs_h.resize(static_cast<size_t>(J));
@@ -1441,20 +1550,25 @@ void dataset_destroy(bsccs_dataset* ds) {
     int prev = -1;
     cudaGetDevice(&prev);
     cudaSetDevice(ds->device);
-    cudaFree(ds->pairs);
-    cudaFree(ds->col_ptr);
-    cudaFree(ds->split);
-    cudaFree(ds->cta_era);
-    cudaFree(ds->cta_subj);
-    cudaFree(ds->subject_offsets);
-    cudaFree(ds->events_per_subject);
-    cudaFree(ds->era_lengths);
-    cudaFree(ds->event_counts);
-    cudaFree(ds->csr_ptr);
-    cudaFree(ds->csr_col);
-    cudaFree(ds->y_dot_x);
-    cudaFree(ds->col_nonempty);
-    cudaFree(ds->col_runs);
+    cudaStream_t s = ds->stream;
+    dfree(ds->pairs, s);
+    dfree(ds->col_ptr, s);
+    dfree(ds->split, s);
+    dfree(ds->cta_era, s);
+    dfree(ds->cta_subj, s);
+    dfree(ds->subject_offsets, s);
+    dfree(ds->events_per_subject, s);
+    dfree(ds->era_lengths, s);
+    dfree(ds->event_counts, s);
+    dfree(ds->csr_ptr, s);
+    dfree(ds->csr_col, s);
+    dfree(ds->y_dot_x, s);
+    dfree(ds->col_nonempty, s);
+    dfree(ds->col_runs, s);
+    if (s) {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+    }
     if (prev >= 0) cudaSetDevice(prev);
     delete ds;
 }
@@ -1474,27 +1588,29 @@ void launch_dense(bsccs_state* st) {
 void alloc_state(bsccs_state* st, const bsccs_dataset* ds) {
     int64_t b = 0;
     st->ds = ds;
+    ensure_pool(ds->device);
     CUDA_TRY(cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking));
-    st->era = dalloc<EraRec>(ds->K, b);
-    st->snap = dalloc<double>(ds->K, b);
-    st->subj = dalloc<SubjRec>(ds->N, b);
-    st->beta = dalloc<double>(ds->J, b);
-    st->trust = dalloc<double>(ds->J, b);
-    st->visit = dalloc<int32_t>(ds->J, b);
-    st->vsplit = dalloc<longlong2>(static_cast<int64_t>(ds->J) * ds->ctas, b);
-    st->slots = dalloc<unsigned long long>(kXchgAreaWords, b);
-    st->moved = dalloc<uint8_t>(ds->J, b);
-    st->counter = dalloc<unsigned long long>(1, b);
-    st->err = dalloc<DevErr>(1, b);
-    st->res = dalloc<DevResult>(1, b);
-    st->scratch = dalloc<double>(2 * kLLBlocks, b);
-    CUDA_TRY(cudaMallocHost(&st->res_h, sizeof(DevResult)));
+    cudaStream_t s = st->stream;
+    st->era = dalloc<EraRec>(ds->K, b, s);
+    st->snap = dalloc<double>(ds->K, b, s);
+    st->subj = dalloc<SubjRec>(ds->N, b, s);
+    st->beta = dalloc<double>(ds->J, b, s);
+    st->trust = dalloc<double>(ds->J, b, s);
+    st->visit = dalloc<int32_t>(ds->J, b, s);
+    st->vsplit = dalloc<longlong2>(static_cast<int64_t>(ds->J) * ds->ctas, b, s);
+    st->slots = dalloc<unsigned long long>(kXchgAreaWords, b, s);
+    st->moved = dalloc<uint8_t>(ds->J, b, s);
+    st->counter = dalloc<unsigned long long>(1, b, s);
+    st->err = dalloc<DevErr>(1, b, s);
+    st->res = dalloc<DevResult>(1, b, s);
+    st->scratch = dalloc<double>(2 * kLLBlocks, b, s);
+    st->res_h = pinned_result();
     CUDA_TRY(cudaEventCreate(&st->ev0));
     CUDA_TRY(cudaEventCreate(&st->ev1));
-    CUDA_TRY(cudaMemsetAsync(st->slots, 0, sizeof(unsigned long long) * kXchgAreaWords, st->stream));
-    CUDA_TRY(cudaMemsetAsync(st->counter, 0, sizeof(unsigned long long), st->stream));
-    CUDA_TRY(cudaMemsetAsync(st->err, 0, sizeof(DevErr), st->stream));
-    CUDA_TRY(cudaMemsetAsync(st->res, 0, sizeof(DevResult), st->stream));
+    CUDA_TRY(cudaMemsetAsync(st->slots, 0, sizeof(unsigned long long) * kXchgAreaWords, s));
+    CUDA_TRY(cudaMemsetAsync(st->counter, 0, sizeof(unsigned long long), s));
+    CUDA_TRY(cudaMemsetAsync(st->err, 0, sizeof(DevErr), s));
+    CUDA_TRY(cudaMemsetAsync(st->res, 0, sizeof(DevResult), s));
 }
 
 } // namespace
@@ -1551,25 +1667,28 @@ void state_destroy(bsccs_state* st) {
     int prev = -1;
     cudaGetDevice(&prev);
     if (st->ds) cudaSetDevice(st->ds->device);
-    if (st->stream) cudaStreamSynchronize(st->stream);
-    cudaFree(st->era);
-    cudaFree(st->snap);
-    cudaFree(st->le_tmp);
-    cudaFree(st->subj);
-    cudaFree(st->beta);
-    cudaFree(st->trust);
-    cudaFree(st->visit);
-    cudaFree(st->moved);
-    cudaFree(st->vsplit);
-    cudaFree(st->slots);
-    cudaFree(st->counter);
-    cudaFree(st->err);
-    cudaFree(st->res);
-    cudaFree(st->scratch);
-    if (st->res_h) cudaFreeHost(st->res_h);
+    cudaStream_t s = st->stream;
+    if (s) {
+        dfree(st->era, s);
+        dfree(st->snap, s);
+        dfree(st->le_tmp, s);
+        dfree(st->subj, s);
+        dfree(st->beta, s);
+        dfree(st->trust, s);
+        dfree(st->visit, s);
+        dfree(st->moved, s);
+        dfree(st->vsplit, s);
+        dfree(st->slots, s);
+        dfree(st->counter, s);
+        dfree(st->err, s);
+        dfree(st->res, s);
+        dfree(st->scratch, s);
+        cudaStreamSynchronize(s);
+    }
+    release_pinned_result(st->res_h);
     if (st->ev0) cudaEventDestroy(st->ev0);
     if (st->ev1) cudaEventDestroy(st->ev1);
-    if (st->stream) cudaStreamDestroy(st->stream);
+    if (s) cudaStreamDestroy(s);
     if (prev >= 0) cudaSetDevice(prev);
     delete st;
 }
@@ -1721,7 +1840,7 @@ void state_get(bsccs_state* st, double* beta, double* xbeta, double* le, double*
     if (le) { // recomputed on the device with the kernels' own expression
         if (!st->le_tmp) {
             int64_t b = 0;
-            st->le_tmp = dalloc<double>(ds->K, b);
+            st->le_tmp = dalloc<double>(ds->K, b, st->stream);
         }
         k_lexp<<<build_grid(ds->device), 256, 0, st->stream>>>(st->era, st->le_tmp, ds->K);
         count_launches(1);

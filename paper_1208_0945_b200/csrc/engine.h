@@ -75,6 +75,7 @@ struct bsccs_dataset_impl;
 // Opaque handle types of the C ABI.
 struct bsccs_dataset {
     int device = 0;
+    cudaStream_t stream = nullptr; // allocation / build stream (pool frees are ordered on it)
     int32_t N = 0, K = 0, J = 0;
     int64_t nnz = 0;
     int ctas = 0;
