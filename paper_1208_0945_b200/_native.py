@@ -7,7 +7,9 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libbsccs_b200.so"
+import os
+
+LIB_PATH = Path(os.environ.get("BSCCS_B200_LIB", Path(__file__).resolve().parent / "_lib" / "libbsccs_b200.so"))
 
 i32, i64, u64, f64 = C.c_int32, C.c_int64, C.c_uint64, C.c_double
 P = C.POINTER

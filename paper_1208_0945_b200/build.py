@@ -41,15 +41,24 @@ def _stale(target: Path, deps: list[Path]) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build_native(force: bool = False, verbose: bool = False) -> Path:
+def build_native(force: bool = False, verbose: bool = False, variant: dict | None = None) -> Path:
+    """variant: compile-time overrides for kernel-shape experiments, e.g.
+    {"BSCCS_SWEEP_THREADS": 384, "BSCCS_CACHED_TILES": 3}; builds
+    _lib/libbsccs_b200_<tag>.so instead of the product library."""
     LIB_DIR.mkdir(exist_ok=True)
+    lib = LIB
+    extra = []
+    if variant:
+        tag = "_".join(f"{k.split('_')[-1].lower()}{v}" for k, v in sorted(variant.items()))
+        lib = LIB_DIR / f"libbsccs_b200_{tag}.so"
+        extra = [f"-D{k}={v}" for k, v in variant.items()]
     deps = [CSRC / s for s in SOURCES + HEADERS] + [ROOT / "include" / "bsccs_b200.h"]
-    if not force and not _stale(LIB, deps):
-        return LIB
+    if not force and not _stale(lib, deps):
+        return lib
     objs = []
     for src in SOURCES:
-        obj = LIB_DIR / (Path(src).stem + ".o")
-        cmd = [_nvcc(), *NVCC_FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+        obj = LIB_DIR / (Path(src).stem + (f"_{lib.stem}" if variant else "") + ".o")
+        cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-c", str(CSRC / src), "-o", str(obj)]
         if src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"] if verbose else []
         else:
@@ -58,14 +67,14 @@ def build_native(force: bool = False, verbose: bool = False) -> Path:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
         objs.append(str(obj))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp), *objs,
            "-lpthread", "-cudart", "static"]
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     for o in objs:
         Path(o).unlink(missing_ok=True)
-    return LIB
+    return lib
 
 
 def build_oracle(verbose: bool = False) -> None:

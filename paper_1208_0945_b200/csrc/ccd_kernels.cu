@@ -54,7 +54,10 @@ constexpr int kModeGradHess = 1;
 constexpr int kModeUpdate = 2;
 constexpr int kT = kSweepThreads;   // threads per CTA; warp 0 is the control warp
 constexpr int kD = kT - 32;         // data threads (warps 1..): tile v holds pairs p0 + v*kD + (tid - 32)
-constexpr int kCached = 5;          // register tiles per data thread
+#ifndef BSCCS_CACHED_TILES
+#define BSCCS_CACHED_TILES 5
+#endif
+constexpr int kCached = BSCCS_CACHED_TILES; // register tiles per data thread
 constexpr int kWarps = kT / 32;
 constexpr int kCap = kCached * kD;  // pairs a CTA keeps in registers per coordinate
 constexpr int kLLBlocks = 592;      // fixed => deterministic LL reduction

@@ -64,7 +64,10 @@ struct DevErr {
     double value;
 };
 
-constexpr int kSweepThreads = 256;
+#ifndef BSCCS_SWEEP_THREADS
+#define BSCCS_SWEEP_THREADS 256
+#endif
+constexpr int kSweepThreads = BSCCS_SWEEP_THREADS;
 constexpr int kMaxLocalShards = 8;
 constexpr int kMaxRanks = 8;
 constexpr int kXchgAreaWords = 512; // exchange words (2 x 7, 256 B apart) + running totals
