@@ -55,7 +55,7 @@ constexpr int kModeUpdate = 2;
 constexpr int kT = kSweepThreads;   // threads per CTA; warp 0 is the control warp
 constexpr int kD = kT - 32;         // data threads (warps 1..): tile v holds pairs p0 + v*kD + (tid - 32)
 #ifndef BSCCS_CACHED_TILES
-#define BSCCS_CACHED_TILES 5
+#define BSCCS_CACHED_TILES 3
 #endif
 constexpr int kCached = BSCCS_CACHED_TILES; // register tiles per data thread
 constexpr int kWarps = kT / 32;
@@ -526,6 +526,32 @@ struct HeadRegs {
     int len[kCached], n[kCached];
 };
 
+// loads only (the registers are consumed later): lets the speculative
+// gathers ride through the exchange without holding up the step broadcast
+__device__ __forceinline__ void issue_records(const ShardArgs& S, const Cached& C, HeadRegs& H) {
+    EraRec* era = S.era;
+    SubjRec* subj = S.subj;
+#pragma unroll
+    for (int v = 0; v < kCached; ++v) {
+        if (slot_valid(C.slot[v])) {
+            const Rec r = ld_rec(era + C.slot[v].pr.x);
+            H.xb[v] = r.xb;
+            H.len[v] = r.len;
+            if (C.slot[v].head) {
+                const Subj sr = ld_subj(subj + C.slot[v].pr.y);
+                H.den[v] = sr.den;
+                H.n[v] = sr.n;
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void finish_records(const Cached& C, HeadRegs& H) {
+#pragma unroll
+    for (int v = 0; v < kCached; ++v)
+        if (slot_valid(C.slot[v])) H.le[v] = lexp(H.len[v], H.xb[v]);
+}
+
 __device__ __forceinline__ void gather_records(const ShardArgs& S, const Cached& C, HeadRegs& H) {
     EraRec* era = S.era;
     SubjRec* subj = S.subj;
@@ -807,8 +833,12 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             const bool idle = !__any_sync(0xffffffffu, active);
             if (!(A.dbg & 1)) {
                 if (!idle) {
-                    if (spec) repair(C, H, sm);
-                    else gather_records(S, C, H);
+                    if (spec) {
+                        if (A.dbg & 64) finish_records(C, H);
+                        repair(C, H, sm);
+                    } else {
+                        gather_records(S, C, H);
+                    }
                 }
                 gh_compute(S, C, p0, p1, H, gs, hs, err, sm);
             }
@@ -834,7 +864,10 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             issue_cached(S, nxt2.x, nxt2.y, NR);
             const bool more = idx + 1 < V;
             const bool spec_next = more && !(A.dbg & 16) && (p1 - p0) <= kCap && (nxt.y - nxt.x) <= kCap;
-            if (spec_next) gather_records(S, N, SH);
+            if (spec_next) {
+                if (A.dbg & 64) issue_records(S, N, SH);
+                else gather_records(S, N, SH);
+            }
             const longlong2 nxt3 = idx + 3 < V ? vs[idx + 3] : z2;
             int jn2 = 0;
             double bn = 0.0, rn = 1.0, yn = 0.0;

@@ -65,7 +65,7 @@ struct DevErr {
 };
 
 #ifndef BSCCS_SWEEP_THREADS
-#define BSCCS_SWEEP_THREADS 256
+#define BSCCS_SWEEP_THREADS 384
 #endif
 constexpr int kSweepThreads = BSCCS_SWEEP_THREADS;
 constexpr int kMaxLocalShards = 8;

@@ -17,7 +17,7 @@ ds = datagen.config_dataset(wl)
 prior = B.laplace_prior(0.1)
 cfg = B.SolverConfig()
 lib = _native.lib()
-modes = {"full": 0, "nospec": 16, "no_update": 2, "no_xchg": 4, "xchg_only": 3}
+modes = {"full": 0, "late_lexp": 64, "nospec": 16, "no_update": 2, "no_xchg": 4, "xchg_only": 3}
 for ctas in ctas_list:
     dds = B.DeviceDataset(ds, 0, ctas)
     for name, f in modes.items():
