@@ -38,11 +38,7 @@ PriorParams to_params(const bsccs_prior* p) {
     // validate_prior (prior.hpp:27-32)
     if (p->kind != PRIOR_NONE && !(p->variance > 0.0 && std::isfinite(p->variance)))
         input_error("prior variance must be positive and finite");
-    PriorParams out;
-    out.kind = p->kind;
-    out.variance = p->variance;
-    out.laplace_b = p->variance_is_laplace_scale ? p->variance : std::sqrt(p->variance / 2.0);
-    return out;
+    return make_prior_params(p->kind, p->variance, p->variance_is_laplace_scale != 0);
 }
 
 // validate_config (solver.hpp:48-64) plus the knobs the device path pins.
@@ -380,8 +376,15 @@ bsccs_status bsccs_state_get(bsccs_state* st, double* beta, double* xbeta, doubl
 bsccs_status bsccs_penalized_step(const bsccs_prior* prior, double beta_j, double g, double h, double* step) {
     return guard([&] {
         const PriorParams p = to_params(prior);
-        const int e = penalized_step(p, beta_j, g, h, step);
+        // the sweep kernel's form (prior.h penalized_step_pre), checked
+        // against the reference expression form below
+        double a = 0.0, b = 0.0;
+        const int e = penalized_step_pre(p, beta_j, beta_over_v(p, beta_j), g, h, &a);
+        const int e2 = penalized_step(p, beta_j, g, h, &b);
+        if (e != e2 || (e == 0 && !(a == b || (a != a && b != b))))
+            internal_error("penalized_step: precomputed form disagrees with the reference form");
         if (e) throw_device_error(e, 0.0);
+        *step = a;
     });
 }
 

@@ -416,12 +416,21 @@ __device__ __forceinline__ PairSlot load_slot(const int2* __restrict__ pairs, in
 
 __device__ __forceinline__ bool slot_valid(const PairSlot& s) { return s.pr.x >= 0; }
 
-__device__ __forceinline__ int data_tid() { return static_cast<int>(threadIdx.x) - 32; }
+// Data-warp order: warps share schedulers by (warp % 4), so the control warp's
+// scheduler-mates (warps 4, 8, ...) take the highest data ranks -- on small
+// slices they hold no pairs and warp 0 issues without competition.
+__device__ __forceinline__ int data_warp() {
+    const int w = static_cast<int>(threadIdx.x) >> 5;
+    constexpr int kMates = (kWarps - 1) / 4; // warps 4, 8, ... below kWarps
+    if ((w & 3) == 0) return (kWarps - 1 - kMates) + (w >> 2) - 1;
+    return w - (w >> 2) - 1;
+}
+__device__ __forceinline__ int data_tid() { return data_warp() * 32 + (static_cast<int>(threadIdx.x) & 31); }
 __device__ __forceinline__ int slot_pos(int v) { return v * kD + data_tid(); }
 
 // warp-uniform: does this (data) warp hold any pair of tile v of [p0, p1)?
 __device__ __forceinline__ bool warp_active(int v, int64_t p0, int64_t p1) {
-    return threadIdx.x >= 32 && p0 + static_cast<int64_t>(v) * kD + ((static_cast<int>(threadIdx.x) & ~31) - 32) < p1;
+    return threadIdx.x >= 32 && p0 + static_cast<int64_t>(v) * kD + data_warp() * 32 < p1;
 }
 
 struct Cached {
@@ -881,6 +890,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                 if (tr && idx < A.ntrace) trb[idx * trs + 4] = gtimer();
                 // exchange, then the scalar step (prior.hpp:72-122,
                 // solver.hpp:131-150), broadcast with the next barrier
+                const double bv = beta_over_v(A.prior, bj); // while the partials travel
                 double tg, th;
                 int te = 0;
                 if (A.dbg & 4) {
@@ -897,7 +907,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                     const double g = __dsub_rn(ydx, tg);
                     const double h = th == 0.0 ? 0.0 : -th;
                     double step = 0.0;
-                    const int serr = penalized_step(A.prior, bj, g, h, &step);
+                    const int serr = penalized_step_pre(A.prior, bj, bv, g, h, &step);
                     if (serr) {
                         status = ST_STEP_ERR;
                         if (c == 0 && threadIdx.x == 0) record_error(S.err, serr, h);

@@ -9,6 +9,8 @@
 // for Laplace; 0/0 -> 0 and g != 0, h == 0 -> numeric error for no prior.
 #pragma once
 
+#include <cmath>
+
 #ifdef __CUDACC__
 #define BSCCS_HD __host__ __device__ __forceinline__
 #else
@@ -34,7 +36,78 @@ struct PriorParams {
     int kind;
     double variance;
     double laplace_b; // prior.hpp:22-24, computed once on the host
+    double inv_v;     // 1.0 / variance  (the reference's `1.0 / v`, prior.hpp:91)
+    double inv_b;     // 1.0 / b         (`1.0 / b`, prior.hpp:110-116; sign / b == +-inv_b exactly)
 };
+
+// Host-side construction of the constants (identical IEEE results to the
+// expressions they replace).
+inline PriorParams make_prior_params(int kind, double variance, bool variance_is_scale) {
+    PriorParams p;
+    p.kind = kind;
+    p.variance = variance;
+    p.laplace_b = variance_is_scale ? variance : std::sqrt(variance / 2.0);
+    p.inv_v = 1.0 / variance;
+    p.inv_b = 1.0 / p.laplace_b;
+    return p;
+}
+
+// beta_j / v, the only other division of the Normal step; it depends on
+// beta_j alone, so the sweep computes it while the exchange is in flight.
+BSCCS_HD double beta_over_v(const PriorParams& p, double beta_j) { return beta_j / p.variance; }
+
+// penalized_step with the beta/prior-only divisions precomputed: bitwise
+// the same branches and values as penalized_step (each replaced expression
+// is the identical IEEE operation; (-1)/b == -(1/b) exactly).
+BSCCS_HD int penalized_step_pre(const PriorParams& p, double beta_j, double bv, double g, double h, double* out) {
+    if (h > 0.0) return DERR_POS_CURVATURE;
+    if (p.kind == PRIOR_NONE) {
+        if (h == 0.0) {
+            if (g == 0.0) {
+                *out = 0.0;
+                return DERR_NONE;
+            }
+            return DERR_FLAT_NO_PRIOR;
+        }
+        *out = -g / h;
+        return DERR_NONE;
+    }
+    if (p.kind == PRIOR_NORMAL) {
+        *out = -(g - bv) / (h - p.inv_v);
+        return DERR_NONE;
+    }
+    if (beta_j != 0.0) {
+        if (h == 0.0) {
+            *out = -beta_j;
+            return DERR_NONE;
+        }
+        const double sb = beta_j > 0.0 ? p.inv_b : -p.inv_b;
+        const double step = -(g - sb) / h;
+        const double landed = beta_j + step;
+        if ((beta_j > 0.0 && landed < 0.0) || (beta_j < 0.0 && landed > 0.0)) {
+            *out = -beta_j;
+            return DERR_NONE;
+        }
+        *out = step;
+        return DERR_NONE;
+    }
+    if (h == 0.0) {
+        *out = 0.0;
+        return DERR_NONE;
+    }
+    const double up = -(g - p.inv_b) / h; // both one-sided trials, independent
+    const double dn = -(g + p.inv_b) / h;
+    if (up > 0.0) {
+        *out = up;
+        return DERR_NONE;
+    }
+    if (dn < 0.0) {
+        *out = dn;
+        return DERR_NONE;
+    }
+    *out = 0.0;
+    return DERR_NONE;
+}
 
 // Returns DERR_NONE or the error code; *out receives the unbounded step.
 BSCCS_HD int penalized_step(const PriorParams& p, double beta_j, double g, double h, double* out) {
