@@ -202,6 +202,11 @@ int64_t bsccs_group_slot_bytes(int32_t total_ctas);
 /* Local group over n shards of one device (one cooperative launch). */
 bsccs_status bsccs_group_create_local(bsccs_dataset* const* shards, int32_t n,
                                       bsccs_group** out);
+/* Virtual ranks: n shards of one device in one launch, each with its own
+ * exchange area that every CTA adds into (system-scope adds, per-shard
+ * polling) -- the multi-process protocol executed on a single GPU. */
+bsccs_status bsccs_group_create_virtual(bsccs_dataset* const* shards, int32_t n,
+                                        bsccs_group** out);
 /* Multi-process: rank r of world w with its one local shard. */
 bsccs_status bsccs_group_create_rank(bsccs_dataset* shard, int32_t rank,
                                      int32_t world, const int32_t* ctas_per_rank,

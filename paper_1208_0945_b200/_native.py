@@ -68,6 +68,7 @@ _SIGS = [
     ("bsccs_solver_config_default", None, [P(bsccs_solver_config)]),
     ("bsccs_group_slot_bytes", i64, [i32]),
     ("bsccs_group_create_local", C.c_int, [P(C.c_void_p), i32, P(C.c_void_p)]),
+    ("bsccs_group_create_virtual", C.c_int, [P(C.c_void_p), i32, P(C.c_void_p)]),
     ("bsccs_group_create_rank", C.c_int, [C.c_void_p, i32, i32, C.c_void_p, P(C.c_void_p)]),
     ("bsccs_group_ipc_handle", C.c_int, [C.c_void_p, C.c_void_p]),
     ("bsccs_group_open_peers", C.c_int, [C.c_void_p, C.c_void_p]),

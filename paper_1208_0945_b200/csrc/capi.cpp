@@ -228,6 +228,8 @@ struct bsccs_group {
     unsigned long long* slots = nullptr;   // local slot buffer
     unsigned long long* counter = nullptr; // local sequence word
     std::vector<unsigned long long*> peer; // per rank (own = slots)
+    // virtual ranks (one launch, one exchange area per shard)
+    std::vector<unsigned long long*> vslots, vcounters;
     int device = 0;
     int total = 0;
     int base = 0;
@@ -497,6 +499,33 @@ bsccs_status bsccs_group_create_local(bsccs_dataset* const* shards, int32_t n, b
     });
 }
 
+bsccs_status bsccs_group_create_virtual(bsccs_dataset* const* shards, int32_t n, bsccs_group** out) {
+    return guard([&] {
+        if (!shards || n < 1 || n > kMaxRanks) input_error("group: 1..8 virtual ranks");
+        auto g = std::make_unique<bsccs_group>();
+        g->device = shards[0]->device;
+        set_device(g->device);
+        for (int32_t i = 0; i < n; ++i) {
+            if (!shards[i] || shards[i]->device != g->device) input_error("group: shards must share one device");
+            if (shards[i]->J != shards[0]->J) input_error("group: shards must have the same drug count");
+            g->shards.push_back(shards[i]);
+            g->total += shards[i]->ctas;
+            unsigned long long* area = nullptr;
+            unsigned long long* ctr = nullptr;
+            CUDA_TRY(cudaMalloc(&area, static_cast<size_t>(bsccs_group_slot_bytes(0))));
+            CUDA_TRY(cudaMemset(area, 0, static_cast<size_t>(bsccs_group_slot_bytes(0))));
+            CUDA_TRY(cudaMalloc(&ctr, sizeof(unsigned long long)));
+            CUDA_TRY(cudaMemset(ctr, 0, sizeof(unsigned long long)));
+            g->vslots.push_back(area);
+            g->vcounters.push_back(ctr);
+        }
+        g->peer = g->vslots;
+        g->slots = g->vslots[0];
+        g->counter = g->vcounters[0];
+        *out = g.release();
+    });
+}
+
 bsccs_status bsccs_group_create_rank(bsccs_dataset* shard, int32_t rank, int32_t world,
                                      const int32_t* ctas_per_rank, bsccs_group** out) {
     return guard([&] {
@@ -554,6 +583,12 @@ bsccs_status bsccs_group_destroy(bsccs_group* g) {
     return guard([&] {
         if (!g) return;
         cudaSetDevice(g->device);
+        if (!g->vslots.empty()) {
+            for (auto* p : g->vslots) cudaFree(p);
+            for (auto* p : g->vcounters) cudaFree(p);
+            delete g;
+            return;
+        }
         for (int32_t r = 0; r < g->world; ++r)
             if (r != g->rank && g->peer.size() > static_cast<size_t>(r) && g->peer[static_cast<size_t>(r)])
                 cudaIpcCloseMemHandle(g->peer[static_cast<size_t>(r)]);
@@ -571,8 +606,6 @@ bsccs_status bsccs_group_fit(bsccs_group* g, const bsccs_prior* prior, const bsc
         const PriorParams p = to_params(prior);
         for (auto* pr : g->peer)
             if (!pr) input_error("group fit: peers not opened");
-        if (g->world > 1) input_error("group fit: multi-process groups need the host allreduce "
-                                      "(use paper_1208_0945_b200.sharding.fit_sharded)");
         set_device(g->device);
         std::memset(result, 0, sizeof *result);
         cudaEvent_t e0, e1;
@@ -588,7 +621,17 @@ bsccs_status bsccs_group_fit(bsccs_group* g, const bsccs_prior* prior, const bsc
             fc.plan.counter = g->counter;
             fc.plan.total_participants = g->total;
             fc.plan.participant_base = g->base;
-            fit_loop(fc, p, cfg, beta_out, result, [](double x) { return x; });
+            fc.plan.shard_slots = g->vslots;
+            fc.plan.shard_counters = g->vcounters;
+            // per-rank log-likelihood partials summed exactly in the exchange
+            // area (positive and negative parts: the words carry values >= 0)
+            auto allreduce = [&](double x) {
+                if (g->world == 1) return x;
+                double pos = 0.0, neg = 0.0;
+                plan_allreduce(fc.plan, x > 0.0 ? x : 0.0, x < 0.0 ? -x : 0.0, &pos, &neg);
+                return pos - neg;
+            };
+            fit_loop(fc, p, cfg, beta_out, result, allreduce);
         } catch (...) {
             for (auto* st : fc.states) release_state(st);
             cudaEventDestroy(e0);

@@ -52,6 +52,7 @@ namespace {
 constexpr int kModeSweep = 0;
 constexpr int kModeGradHess = 1;
 constexpr int kModeUpdate = 2;
+constexpr int kModeReduce = 3; // exact all-reduce of two host scalars over every participant
 constexpr int kT = kSweepThreads;   // threads per CTA; warp 0 is the control warp
 constexpr int kD = kT - 32;         // data threads (warps 1..): tile v holds pairs p0 + v*kD + (tid - 32)
 #ifndef BSCCS_CACHED_TILES
@@ -67,6 +68,9 @@ constexpr int kHtBits = 11;         // subject hash table of the speculation rep
 constexpr int kHt = 1 << kHtBits;
 
 struct ShardArgs {
+    const unsigned long long* xslots; // exchange area this shard polls (its rank's)
+    unsigned long long* xcounter;     // exchange sequence word of that area
+    int xowner;                       // this shard's CTA 0 stores the area's baseline / counter
     const int2* pairs;
     double* snap;
     const longlong2* vsplit; // [ctas][nvisit] (p0, p1) of each CTA's slice in visit order
@@ -105,6 +109,7 @@ struct SweepArgs {
     const unsigned long long* slots;
     int P;
     unsigned long long* counter;
+    double red_a, red_b; // kModeReduce inputs (this rank's values)
     int dbg; // profiling only: bit0 skip grad/hess, bit1 skip update, bit2 skip exchange, bit4 no speculation
     unsigned long long* trace; // profiling only: [ntrace][gridDim][kTr] globaltimer stamps
     int ntrace;
@@ -138,6 +143,10 @@ struct Smem {
 // fences are needed; peers on other GPUs would use .sys).
 __device__ __forceinline__ void red_add(unsigned long long* p, unsigned long long v) {
     asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// peer exchange areas (other GPUs, mapped through CUDA IPC over NVLink)
+__device__ __forceinline__ void red_add_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ unsigned long long ld_poll(const unsigned long long* p) {
     unsigned long long v;
@@ -302,7 +311,11 @@ __device__ __forceinline__ void publish(const SweepArgs& A, unsigned long long s
     if (l == 6) w = (e || !okab) ? 1ull : 0ull;
     w += kXCnt;
     const size_t off = static_cast<size_t>(seq & 1ull) * kXWords * kXStride + static_cast<size_t>(l) * kXStride;
-    for (int d = 0; d < A.ndst; ++d) red_add(A.dst[d] + off, w);
+    if (A.ndst == 1) {
+        red_add(A.dst[0] + off, w);
+    } else {
+        for (int d = 0; d < A.ndst; ++d) red_add_sys(A.dst[d] + off, w);
+    }
 }
 
 // Running totals of the two buffers (lanes 0..6 of warp 0).
@@ -310,31 +323,31 @@ struct XPrev {
     unsigned long long b0, b1;
 };
 
-__device__ __forceinline__ void xprev_load(const SweepArgs& A, XPrev& pv) {
+__device__ __forceinline__ void xprev_load(const unsigned long long* slots, XPrev& pv) {
     const int l = lane_id();
     if (threadIdx.x < 32 && l < kXWords) {
-        pv.b0 = A.slots[kXBase + l];
-        pv.b1 = A.slots[kXBase + kXWords + l];
+        pv.b0 = slots[kXBase + l];
+        pv.b1 = slots[kXBase + kXWords + l];
     }
 }
 
-__device__ __forceinline__ void xprev_store(const SweepArgs& A, const XPrev& pv) {
+__device__ __forceinline__ void xprev_store(const unsigned long long* slots, const XPrev& pv) {
     const int l = lane_id();
     if (threadIdx.x < 32 && l < kXWords) {
-        const_cast<unsigned long long*>(A.slots)[kXBase + l] = pv.b0;
-        const_cast<unsigned long long*>(A.slots)[kXBase + kXWords + l] = pv.b1;
+        const_cast<unsigned long long*>(slots)[kXBase + l] = pv.b0;
+        const_cast<unsigned long long*>(slots)[kXBase + kXWords + l] = pv.b1;
     }
 }
 
 // warp 0 only: wait for the exchange `seq`, return the totals in every lane
-__device__ __forceinline__ void poll(const SweepArgs& A, unsigned long long seq, XPrev& pv, double& ta, double& tb,
-                                     int& te, unsigned long long* stamp) {
+__device__ __forceinline__ void poll(const SweepArgs& A, const unsigned long long* slots, unsigned long long seq,
+                                     XPrev& pv, double& ta, double& tb, int& te, unsigned long long* stamp) {
     const int l = lane_id();
     const unsigned buf = static_cast<unsigned>(seq & 1ull);
     unsigned long long diff = 0;
     if (l < kXWords) {
         const unsigned long long* p =
-            A.slots + static_cast<size_t>(buf) * kXWords * kXStride + static_cast<size_t>(l) * kXStride;
+            slots + static_cast<size_t>(buf) * kXWords * kXStride + static_cast<size_t>(l) * kXStride;
         const unsigned long long prev = buf ? pv.b1 : pv.b0;
         unsigned long long v;
         do {
@@ -752,13 +765,13 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
     const int c = static_cast<int>(blockIdx.x) - S.cta_begin;
     const int64_t* split_c = S.split + c;
     const int stride = S.ctas + 1;
-    unsigned long long seq = *A.counter;
+    unsigned long long seq = *S.xcounter;
     int err = 0;
     double errv = 0.0;
     Cached C;
     HeadRegs H;
     XPrev pv{0ull, 0ull};
-    if (A.mode != kModeUpdate) xprev_load(A, pv);
+    if (A.mode != kModeUpdate) xprev_load(S.xslots, pv);
 
     if (A.mode == kModeUpdate) {
         const int j = A.single_j;
@@ -766,6 +779,26 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         update_slice(S, C, H, false, p0, p1, A.single_delta, err, errv, sm);
         if (err) record_error(S.err, err, errv);
         if (c == 0 && threadIdx.x == 0) S.beta[j] = __dadd_rn(S.beta[j], A.single_delta);
+        return;
+    }
+
+    if (A.mode == kModeReduce) {
+        // CTA 0 of the first local shard contributes this rank's values
+        const bool src = (c == 0 && si == 0);
+        const double a = src ? A.red_a : 0.0, b = src ? A.red_b : 0.0;
+        publish(A, seq, a, b, 0);
+        if (threadIdx.x < 32) {
+            double ta, tb;
+            int te;
+            poll(A, S.xslots, seq, pv, ta, tb, te, nullptr);
+            if (c == 0 && threadIdx.x == 0) {
+                S.res->change = ta;
+                S.res->magnitude = tb;
+                S.res->err_remote = te;
+                if (S.xowner) *S.xcounter = seq + 1;
+            }
+            if (c == 0 && S.xowner) xprev_store(S.xslots, pv);
+        }
         return;
     }
 
@@ -782,14 +815,14 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         if (threadIdx.x < 32) {
             double tg, th;
             int te;
-            poll(A, seq, pv, tg, th, te, nullptr);
+            poll(A, S.xslots, seq, pv, tg, th, te, nullptr);
             if (c == 0 && threadIdx.x == 0) {
                 S.res->g = __dsub_rn(A.y_dot_x[j], tg);
                 S.res->h = th == 0.0 ? 0.0 : -th;
                 S.res->err_remote = te;
-                if (si == 0) *A.counter = seq + 1;
+                if (S.xowner) *S.xcounter = seq + 1;
             }
-            if (c == 0 && si == 0) xprev_store(A, pv);
+            if (c == 0 && S.xowner) xprev_store(S.xslots, pv);
         }
         return;
     }
@@ -897,7 +930,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                     tg = gs;
                     th = hs;
                 } else {
-                    poll(A, seq, pv, tg, th, te, (tr && idx < A.ntrace) ? trb + idx * trs + 5 : nullptr);
+                    poll(A, S.xslots, seq, pv, tg, th, te, (tr && idx < A.ntrace) ? trb + idx * trs + 5 : nullptr);
                 }
                 int status = ST_OK;
                 double delta = 0.0;
@@ -979,7 +1012,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         if (w0) {
             double tch, tmg;
             int te;
-            poll(A, seq, pv, tch, tmg, te, nullptr);
+            poll(A, S.xslots, seq, pv, tch, tmg, te, nullptr);
             if (c == 0 && threadIdx.x == 0) {
                 S.res->change = tch;
                 S.res->magnitude = tmg;
@@ -996,9 +1029,9 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         S.res->visited = nvisit;
         S.res->moved = nmoved;
         S.res->counter = seq;
-        if (si == 0) *A.counter = seq;
+        if (S.xowner) *S.xcounter = seq;
     }
-    if (c == 0 && si == 0) xprev_store(A, pv);
+    if (c == 0 && S.xowner) xprev_store(S.xslots, pv);
 }
 
 // ---- dense kernels ---------------------------------------------------------
@@ -1763,6 +1796,9 @@ SweepArgs base_args(const ExchangePlan& plan) {
     for (size_t i = 0; i < plan.shards.size(); ++i) {
         bsccs_state* st = plan.shards[i];
         ShardArgs& s = a.sh[i];
+        s.xslots = plan.shard_slots.empty() ? plan.local_slots : plan.shard_slots[i];
+        s.xcounter = plan.shard_counters.empty() ? plan.counter : plan.shard_counters[i];
+        s.xowner = plan.shard_slots.empty() ? (i == 0) : 1;
         s.pairs = st->ds->pairs;
         s.snap = st->snap;
         s.vsplit = st->vsplit;
@@ -1931,6 +1967,26 @@ void read_debug_trace(unsigned long long* host, size_t words) {
     if (!g_trace) return;
     CUDA_TRY(cudaMemcpy(host, g_trace, std::min(words, g_trace_words) * sizeof(unsigned long long),
                         cudaMemcpyDeviceToHost));
+}
+
+// Exact, deterministic sum over every participant of the plan of two
+// non-negative host scalars (this rank contributes (a, b)).
+void plan_allreduce(const ExchangePlan& plan, double a, double b, double* ta, double* tb) {
+    bsccs_state* s0 = plan.shards[0];
+    DeviceGuard dg(s0->ds->device);
+    for (auto* st : plan.shards)
+        if (st->stream != s0->stream) CUDA_TRY(cudaStreamSynchronize(st->stream));
+    SweepArgs args = base_args(plan);
+    args.mode = kModeReduce;
+    args.red_a = a;
+    args.red_b = b;
+    launch_ccd(plan, args);
+    CUDA_TRY(cudaMemcpyAsync(s0->res_h, s0->res, sizeof(DevResult), cudaMemcpyDeviceToHost, s0->stream));
+    CUDA_TRY(cudaStreamSynchronize(s0->stream));
+    CUDA_TRY(cudaGetLastError());
+    if (s0->res_h->err_remote) numeric_error("all-reduce: invalid contribution");
+    *ta = s0->res_h->change;
+    *tb = s0->res_h->magnitude;
 }
 
 SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool normalized) {

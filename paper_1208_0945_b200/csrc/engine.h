@@ -176,11 +176,15 @@ struct ExchangePlan {
     std::vector<unsigned long long*> dst;  // slot buffers to publish into
     unsigned long long* local_slots;       // slot buffer to poll
     unsigned long long* counter;           // sequence word (local)
+    // virtual ranks inside one launch: per-shard poll area / counter (each
+    // shard is its own "rank"; every CTA adds into every area of `dst`)
+    std::vector<unsigned long long*> shard_slots, shard_counters;
     int total_participants;                // CTAs across all ranks
     int participant_base;                  // first participant of shard 0
 };
 
 SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool normalized);
+void plan_allreduce(const ExchangePlan& plan, double a, double b, double* ta, double* tb);
 void prepare_snapshot(bsccs_state* st);
 void set_debug_flags(int flags); // profiling only
 void set_debug_trace(int ncoords, int ctas);

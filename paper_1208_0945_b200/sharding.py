@@ -112,7 +112,8 @@ class LocalGroup:
     """All shards on one device, one cooperative launch per cycle: the
     single-GPU execution of the cross-shard exchange protocol."""
 
-    def __init__(self, shards: Sequence[Shard], device: int = 0, ctas_per_shard: Sequence[int] = None):
+    def __init__(self, shards: Sequence[Shard], device: int = 0, ctas_per_shard: Sequence[int] = None,
+                 virtual_ranks: bool = False):
         if ctas_per_shard is None:
             from .bsccs import device_info
             ctas_per_shard = split_ctas(device_info(device)["ctas"], len(shards))
@@ -121,7 +122,8 @@ class LocalGroup:
                      for sh, cc in zip(shards, ctas_per_shard)]
         arr = (C.c_void_p * len(self.devs))(*[d.handle for d in self.devs])
         h = C.c_void_p()
-        _check(lib().bsccs_group_create_local(arr, len(self.devs), C.byref(h)))
+        create = lib().bsccs_group_create_virtual if virtual_ranks else lib().bsccs_group_create_local
+        _check(create(arr, len(self.devs), C.byref(h)))
         self.handle = h
 
     def fit(self, prior: PriorSpec, cfg: SolverConfig = None, init_beta=None) -> FitResult:
@@ -148,3 +150,50 @@ class LocalGroup:
             self.close()
         except Exception:
             pass
+
+
+class RankGroup:
+    """One rank of a multi-process patient-sharded fit (one GPU per process,
+    launched by torchrun).  Ranks trade the CUDA IPC handle of their
+    exchange area through torch.distributed; afterwards the per-coordinate
+    partials travel as `red.add` into every peer's area over NVLink, inside
+    the sweep kernel -- no host collective on the per-coordinate path.  The
+    per-fit log-likelihood is summed exactly through the same words."""
+
+    def __init__(self, shard: Shard, device: int, ctas: int = 0):
+        import torch.distributed as dist
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        self.dds = DeviceDataset(shard.dataset, device, ctas, (shard.y_dot_x_global, shard.col_nnz_global))
+        self.J = shard.dataset.num_drugs
+        all_ctas = [None] * self.world
+        dist.all_gather_object(all_ctas, self.dds.ctas)
+        h = C.c_void_p()
+        arr = (C.c_int32 * self.world)(*all_ctas)
+        _check(lib().bsccs_group_create_rank(self.dds.handle, self.rank, self.world, arr, C.byref(h)))
+        self.handle = h
+        blob = (C.c_uint8 * 64)()
+        _check(lib().bsccs_group_ipc_handle(h, blob))
+        blobs = [None] * self.world
+        dist.all_gather_object(blobs, bytes(blob))
+        allb = (C.c_uint8 * (64 * self.world)).from_buffer_copy(b"".join(blobs))
+        _check(lib().bsccs_group_open_peers(h, allb))
+        dist.barrier()  # every exchange area zeroed and mapped before any add
+
+    def fit(self, prior: PriorSpec, cfg: SolverConfig = None, init_beta=None) -> FitResult:
+        cfg = cfg or SolverConfig()
+        b = None if init_beta is None else np.ascontiguousarray(init_beta, dtype=np.float64)
+        beta = np.empty(self.J, dtype=np.float64)
+        res = bsccs_fit_result()
+        p, c = prior._c(), cfg._c()
+        _check(lib().bsccs_group_fit(self.handle, C.byref(p), C.byref(c), _ptr(b), _ptr(beta), C.byref(res)))
+        return FitResult(beta, res.log_posterior, res.cycles_run, bool(res.converged), res.final_criterion,
+                         res.coordinates_visited, res.coordinates_moved, res.dense_refreshes, res.device_seconds,
+                         res.sweep_seconds, res.algorithmic_bytes, res.kernel_launches)
+
+    def close(self):
+        import torch.distributed as dist
+        if self.handle:
+            dist.barrier()  # nobody still adds into our area
+            _check(lib().bsccs_group_destroy(self.handle))
+            self.handle = None
+        self.dds.close()

@@ -135,12 +135,15 @@ def test_gloo_world2_sharded_ccd_matches_unsharded():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("nshards", [2, 3])
-def test_local_group_matches_single_fit(nshards):
+@pytest.mark.parametrize("nshards,virtual", [(2, False), (3, False), (2, True), (4, True)])
+def test_local_group_matches_single_fit(nshards, virtual):
+    """virtual=True: each shard is a separate 'rank' with its own exchange
+    area, every CTA adds into all areas with system-scope adds -- the
+    multi-GPU protocol on one device."""
     ds = datagen.config_dataset("10k")
     prior = B.laplace_prior(0.1)
     single = B.fit(ds, prior)
-    grp = sharding.LocalGroup(sharding.shard_dataset(ds, nshards))
+    grp = sharding.LocalGroup(sharding.shard_dataset(ds, nshards), virtual_ranks=virtual)
     res = grp.fit(prior)
     grp.close()
     assert res.cycles_run == single.cycles_run
