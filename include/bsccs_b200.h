@@ -149,6 +149,32 @@ bsccs_status bsccs_dataset_destroy(bsccs_dataset* ds);
 /* sizes: N, K, J, nnz, ctas, device bytes resident */
 bsccs_status bsccs_dataset_info(const bsccs_dataset* ds, int64_t out[6]);
 
+/* subset_dataset (dataset.hpp:157-217), built on the device from a resident
+ * dataset: subjects in the given order, repeats allowed (each occurrence an
+ * independent copy).  Bit-identical layout to the reference's subset.
+ * Empty selection or an index out of range: BSCCS_INPUT_ERROR. */
+bsccs_status bsccs_dataset_subset(const bsccs_dataset* ds,
+                                  const int32_t* subject_indices, int64_t n,
+                                  int32_t num_ctas_override,
+                                  bsccs_dataset** out);
+/* Copies the flat CSC arrays of a resident dataset back to host (sizes from
+ * bsccs_dataset_info); any pointer may be NULL. */
+bsccs_status bsccs_dataset_export(const bsccs_dataset* ds,
+                                  int32_t* subject_offsets,
+                                  int32_t* events_per_subject,
+                                  int32_t* era_lengths, int32_t* event_counts,
+                                  int64_t* col_ptr, int32_t* rows,
+                                  int32_t* subjects, int64_t* y_dot_x);
+/* kfold_split (cross_validation.hpp:58-80): fold lists back to back in
+ * subjects_out[num_subjects], their sizes in fold_sizes[folds]. */
+bsccs_status bsccs_kfold_split(int32_t num_subjects, int32_t folds,
+                               uint64_t seed, int32_t* subjects_out,
+                               int32_t* fold_sizes);
+/* resample (bootstrap.hpp:43-52) drawn from Rng(seed, stream); replicate r
+ * of run_bootstrap uses stream r + 1 (bootstrap.hpp:104). */
+bsccs_status bsccs_resample(int32_t num_subjects, uint64_t seed,
+                            uint64_t stream, int32_t* out);
+
 /* ---- tier 1: engine (engine.hpp) --------------------------------------- */
 /* init_state (engine.hpp:137-166); beta may be NULL (zeros). */
 bsccs_status bsccs_state_create(const bsccs_dataset* ds, const double* beta,
@@ -190,6 +216,131 @@ bsccs_status bsccs_fit(const bsccs_dataset* ds, const bsccs_prior* prior,
                        double* beta_out, bsccs_fit_result* result);
 /* Defaults of SolverConfig{} (solver.hpp:21-46). */
 void bsccs_solver_config_default(bsccs_solver_config* cfg);
+
+/* ---- callers of fit: cross-validation and bootstrap -------------------- */
+/* Engines for the many-fit drivers.
+ *   BSCCS_ENGINE_SUBSET   the reference's route: every fold / replicate
+ *                         dataset is materialised (bsccs_dataset_subset, on
+ *                         the device) and fitted by the single-fit kernel.
+ *   BSCCS_ENGINE_BATCHED  R fits share the parent dataset and every
+ *                         per-coordinate exchange: a subject taken m times
+ *                         carries weight m (0 when left out).  Same model and
+ *                         visit order; sums differ from the materialised
+ *                         dataset's by rounding only. */
+#define BSCCS_ENGINE_SUBSET 0
+#define BSCCS_ENGINE_BATCHED 1
+
+/* CVConfig (cross_validation.hpp:29-41); the grid is passed separately. */
+typedef struct bsccs_cv_config {
+    int32_t folds;
+    int32_t prior_kind;
+    int32_t variance_is_laplace_scale;
+    int32_t warm_start;
+    uint64_t seed;
+    bsccs_solver_config solver;
+    int32_t engine;     /* BSCCS_ENGINE_* */
+    int32_t batch;      /* batched engine: max fits per launch (<= 0: auto) */
+} bsccs_cv_config;
+
+/* CVCell (cross_validation.hpp:43-48). */
+typedef struct bsccs_cv_cell {
+    double predictive_ll;
+    int32_t cycles;
+    int32_t converged;
+    int32_t valid;
+    int32_t reserved;
+} bsccs_cv_cell;
+
+/* CVResult scalars (cross_validation.hpp:50-57); the vectors go to caller
+ * buffers. */
+typedef struct bsccs_cv_result {
+    int32_t selected_index;
+    int32_t points;
+    double selected_variance;
+    int64_t total_cycles;
+    double device_seconds;      /* instrumentation */
+    int64_t fits;               /* fits run */
+    int64_t coordinates_visited;
+} bsccs_cv_result;
+
+/* Defaults of CVConfig{} (cross_validation.hpp:29-41): 10 folds, laplace,
+ * seed 0, warm start, default SolverConfig; engine SUBSET. */
+void bsccs_cv_config_default(bsccs_cv_config* cfg);
+/* The 13-point default grid (cross_validation.hpp:19-27). */
+void bsccs_default_variance_grid(double out[13]);
+
+/* grid_search_cv (cross_validation.hpp:100-215).  grid_out[points] receives
+ * the sorted grid, cells[points * folds] the cells ([grid point][fold]),
+ * mean_predictive_ll[points] the fold means (NaN where a fold failed).  A
+ * fit failing with a numeric/internal error marks its cell invalid; input
+ * errors propagate; no usable grid point -> BSCCS_CONVERGENCE_ERROR. */
+bsccs_status bsccs_grid_search_cv(const bsccs_dataset* ds,
+                                  const bsccs_cv_config* cfg,
+                                  const double* variance_grid, int32_t points,
+                                  double* grid_out, bsccs_cv_cell* cells,
+                                  double* mean_predictive_ll,
+                                  bsccs_cv_result* result);
+/* The fold loop of grid_search_cv for folds [fold_begin, fold_end) only
+ * (ranks of a multi-GPU job each run a range); cells as above, only the
+ * range's columns written. */
+bsccs_status bsccs_cv_run_folds(const bsccs_dataset* ds,
+                                const bsccs_cv_config* cfg,
+                                const double* variance_grid, int32_t points,
+                                int32_t fold_begin, int32_t fold_end,
+                                bsccs_cv_cell* cells, bsccs_cv_result* result);
+/* The selection step of grid_search_cv over complete cells. */
+bsccs_status bsccs_cv_select(const double* sorted_grid, int32_t points,
+                             int32_t folds, const bsccs_cv_cell* cells,
+                             double* mean_predictive_ll,
+                             bsccs_cv_result* result);
+
+/* BootstrapConfig (bootstrap.hpp:17-28). */
+typedef struct bsccs_bootstrap_config {
+    int32_t replicates;
+    int32_t warm_start;
+    double level;
+    uint64_t seed;
+    bsccs_prior prior;
+    bsccs_solver_config solver;
+    int32_t engine;     /* BSCCS_ENGINE_* */
+    int32_t batch;      /* batched engine: max fits per launch (<= 0: auto) */
+} bsccs_bootstrap_config;
+
+/* BootstrapResult scalars (bootstrap.hpp:30-41). */
+typedef struct bsccs_bootstrap_result {
+    int32_t replicates;
+    int32_t used;
+    int32_t non_converged;
+    int32_t full_converged;
+    double device_seconds;      /* instrumentation */
+    int64_t total_cycles;
+    int64_t coordinates_visited;
+} bsccs_bootstrap_result;
+
+void bsccs_bootstrap_config_default(bsccs_bootstrap_config* cfg);
+/* run_bootstrap (bootstrap.hpp:79-158); every output has num_drugs
+ * entries. */
+bsccs_status bsccs_run_bootstrap(const bsccs_dataset* ds,
+                                 const bsccs_bootstrap_config* cfg,
+                                 double* beta_full, double* lower,
+                                 double* upper, double* p_hat,
+                                 bsccs_bootstrap_result* result);
+/* Replicates [r_begin, r_end) of run_bootstrap (replicate r is a pure
+ * function of (seed, r), bootstrap.hpp:103-106): estimates row-major
+ * [(r_end - r_begin) x num_drugs], converged flags per replicate.
+ * beta_full is the warm start (NULL: cold). */
+bsccs_status bsccs_bootstrap_replicates(const bsccs_dataset* ds,
+                                        const bsccs_bootstrap_config* cfg,
+                                        const double* beta_full,
+                                        int32_t r_begin, int32_t r_end,
+                                        double* estimates, int32_t* converged,
+                                        bsccs_bootstrap_result* result);
+/* The summary step of run_bootstrap (bootstrap.hpp:120-156). */
+bsccs_status bsccs_bootstrap_summarize(int32_t num_drugs, int32_t replicates,
+                                       double level, const double* estimates,
+                                       const int32_t* converged, double* lower,
+                                       double* upper, double* p_hat,
+                                       bsccs_bootstrap_result* result);
 
 /* ---- multi-GPU patient sharding ------------------------ */
 /* A group binds the shards that exchange (gradient, hessian) partials each

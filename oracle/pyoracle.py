@@ -242,6 +242,52 @@ class RefDataset:
         self.ref._chk(self.ref.lib.ref_subset(self.h, _p(sel), i64(sel.size), C.byref(h)))
         return RefDataset(self.ref, h)
 
+    def kfold_split(self, folds, seed):
+        n = self.sizes()["N"]
+        out = np.zeros(n, np.int32)
+        sizes = np.zeros(folds, np.int32)
+        self.ref._chk(self.ref.lib.ref_kfold_split(self.h, i32(folds), u64(seed), _p(out), _p(sizes)))
+        return np.split(out, np.cumsum(sizes)[:-1])
+
+    def resample(self, seed, stream):
+        out = np.zeros(self.sizes()["N"], np.int32)
+        self.ref._chk(self.ref.lib.ref_resample(self.h, u64(seed), u64(stream), _p(out)))
+        return out
+
+    def predictive_ll(self, beta):
+        b = np.ascontiguousarray(beta, dtype=np.float64)
+        out = f64()
+        self.ref._chk(self.ref.lib.ref_predictive_ll(self.h, _p(b), C.byref(out)))
+        return out.value
+
+    def grid_search_cv(self, folds, grid, prior_kind, seed, cfg, warm_start=True, scale=False, threads=1):
+        g = np.ascontiguousarray(grid, dtype=np.float64)
+        P = g.size
+        grid_out, mean = np.zeros(P), np.zeros(P)
+        cell_ll = np.zeros(P * folds)
+        cell_int = np.zeros(3 * P * folds, np.int32)
+        sel, selv, tot = i32(), f64(), i64()
+        c = _ccfg(cfg)
+        self.ref._chk(self.ref.lib.ref_grid_search_cv(
+            self.h, i32(folds), i32(int(prior_kind)), i32(int(scale)), i32(int(warm_start)), u64(seed),
+            C.byref(c), _p(g), i32(P), i32(threads), _p(grid_out), _p(cell_ll), _p(cell_int), _p(mean),
+            C.byref(sel), C.byref(selv), C.byref(tot)))
+        ci = cell_int.reshape(P, folds, 3)
+        return dict(variance_grid=grid_out, predictive_ll=cell_ll.reshape(P, folds), cycles=ci[..., 0],
+                    converged=ci[..., 1], valid=ci[..., 2], mean_predictive_ll=mean, selected_index=sel.value,
+                    selected_variance=selv.value, total_cycles=tot.value)
+
+    def run_bootstrap(self, replicates, level, seed, prior, cfg, warm_start=True, threads=1):
+        J = self._J()
+        a = [np.zeros(J) for _ in range(4)]
+        ints = np.zeros(3, np.int32)
+        p, c = _cprior(prior), _ccfg(cfg)
+        self.ref._chk(self.ref.lib.ref_run_bootstrap(
+            self.h, i32(replicates), f64(level), u64(seed), C.byref(p), C.byref(c), i32(int(warm_start)),
+            i32(threads), *[_p(x) for x in a], _p(ints)))
+        return dict(beta_full=a[0], lower=a[1], upper=a[2], p_hat=a[3], used=int(ints[0]),
+                    non_converged=int(ints[1]), full_converged=bool(ints[2]))
+
     def fit(self, prior, cfg, init_beta=None, threads=1):
         J = self._J()
         beta = np.zeros(J)

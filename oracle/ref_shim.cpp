@@ -205,6 +205,100 @@ int ref_fit(void* dsp, const bsccs_prior* prior, const bsccs_solver_config* cfg,
     });
 }
 
+// kfold_split (cross_validation.hpp:58-80): fold lists back to back
+int ref_kfold_split(void* dsp, int32_t folds, uint64_t seed, int32_t* out, int32_t* sizes) {
+    return guard([&] {
+        auto lists = bsccs::kfold_split(*static_cast<bsccs::Dataset*>(dsp), folds, seed);
+        size_t p = 0;
+        for (size_t f = 0; f < lists.size(); ++f) {
+            sizes[f] = static_cast<int32_t>(lists[f].size());
+            for (auto s : lists[f]) out[p++] = s;
+        }
+    });
+}
+
+// resample (bootstrap.hpp:43-52) from Rng(seed, stream)
+int ref_resample(void* dsp, uint64_t seed, uint64_t stream, int32_t* out) {
+    return guard([&] {
+        bsccs::Rng rng(seed, stream);
+        auto idx = bsccs::resample(*static_cast<bsccs::Dataset*>(dsp), rng);
+        std::memcpy(out, idx.data(), sizeof(int32_t) * idx.size());
+    });
+}
+
+// predictive_log_likelihood (cross_validation.hpp:89-93)
+int ref_predictive_ll(void* dsp, const double* beta, double* out) {
+    return guard([&] {
+        auto* ds = static_cast<bsccs::Dataset*>(dsp);
+        std::vector<double> b(beta, beta + ds->num_drugs);
+        *out = bsccs::predictive_log_likelihood(b, *ds);
+    });
+}
+
+// grid_search_cv (cross_validation.hpp:100-215).  cells: [points][folds] x
+// {predictive_ll, cycles, converged, valid}; threads > 1 supplies a pool.
+int ref_grid_search_cv(void* dsp, int32_t folds, int32_t prior_kind, int32_t scale, int32_t warm,
+                       uint64_t seed, const bsccs_solver_config* cfg, const double* grid, int32_t points,
+                       int32_t threads, double* grid_out, double* cell_ll, int32_t* cell_int,
+                       double* mean_ll, int32_t* selected_index, double* selected_variance,
+                       int64_t* total_cycles) {
+    return guard([&] {
+        bsccs::CVConfig c;
+        c.folds = folds;
+        c.variance_grid.assign(grid, grid + points);
+        c.prior_kind = static_cast<bsccs::PriorKind>(prior_kind);
+        c.variance_is_laplace_scale = scale != 0;
+        c.seed = seed;
+        c.solver = to_cfg(cfg);
+        c.warm_start = warm != 0;
+        std::unique_ptr<bsccs::ThreadPool> pool;
+        if (threads > 1) pool = std::make_unique<bsccs::ThreadPool>(threads - 1);
+        auto r = bsccs::grid_search_cv(*static_cast<bsccs::Dataset*>(dsp), c, pool.get());
+        for (int32_t g = 0; g < points; ++g) {
+            grid_out[g] = r.variance_grid[static_cast<size_t>(g)];
+            mean_ll[g] = r.mean_predictive_ll[static_cast<size_t>(g)];
+            for (int32_t f = 0; f < folds; ++f) {
+                const auto& cell = r.cells[static_cast<size_t>(g)][static_cast<size_t>(f)];
+                const size_t k = static_cast<size_t>(g) * folds + f;
+                cell_ll[k] = cell.predictive_ll;
+                cell_int[3 * k] = cell.cycles;
+                cell_int[3 * k + 1] = cell.converged ? 1 : 0;
+                cell_int[3 * k + 2] = cell.valid ? 1 : 0;
+            }
+        }
+        *selected_index = r.selected_index;
+        *selected_variance = r.selected_variance;
+        *total_cycles = r.total_cycles;
+    });
+}
+
+// run_bootstrap (bootstrap.hpp:79-158); ints = {used, non_converged, full_converged}
+int ref_run_bootstrap(void* dsp, int32_t replicates, double level, uint64_t seed,
+                      const bsccs_prior* prior, const bsccs_solver_config* cfg, int32_t warm,
+                      int32_t threads, double* beta_full, double* lower, double* upper,
+                      double* p_hat, int32_t* ints) {
+    return guard([&] {
+        bsccs::BootstrapConfig c;
+        c.replicates = replicates;
+        c.level = level;
+        c.seed = seed;
+        c.prior = to_prior(prior);
+        c.solver = to_cfg(cfg);
+        c.warm_start = warm != 0;
+        std::unique_ptr<bsccs::ThreadPool> pool;
+        if (threads > 1) pool = std::make_unique<bsccs::ThreadPool>(threads - 1);
+        auto r = bsccs::run_bootstrap(*static_cast<bsccs::Dataset*>(dsp), c, pool.get());
+        const size_t J = r.beta_full.size();
+        std::memcpy(beta_full, r.beta_full.data(), sizeof(double) * J);
+        std::memcpy(lower, r.lower.data(), sizeof(double) * J);
+        std::memcpy(upper, r.upper.data(), sizeof(double) * J);
+        std::memcpy(p_hat, r.p_hat.data(), sizeof(double) * J);
+        ints[0] = r.used;
+        ints[1] = r.non_converged;
+        ints[2] = r.full_converged ? 1 : 0;
+    });
+}
+
 // ---- engine-level handles --------------------------------------------------
 int ref_state_create(void* dsp, const double* beta, const bsccs_solver_config* cfg, void** out) {
     return guard([&] {

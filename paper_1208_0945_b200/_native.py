@@ -35,6 +35,30 @@ class bsccs_fit_result(C.Structure):
     ]
 
 
+class bsccs_cv_config(C.Structure):
+    _fields_ = [("folds", i32), ("prior_kind", i32), ("variance_is_laplace_scale", i32), ("warm_start", i32),
+                ("seed", u64), ("solver", bsccs_solver_config), ("engine", i32), ("batch", i32)]
+
+
+class bsccs_cv_cell(C.Structure):
+    _fields_ = [("predictive_ll", f64), ("cycles", i32), ("converged", i32), ("valid", i32), ("reserved", i32)]
+
+
+class bsccs_cv_result(C.Structure):
+    _fields_ = [("selected_index", i32), ("points", i32), ("selected_variance", f64), ("total_cycles", i64),
+                ("device_seconds", f64), ("fits", i64), ("coordinates_visited", i64)]
+
+
+class bsccs_bootstrap_config(C.Structure):
+    _fields_ = [("replicates", i32), ("warm_start", i32), ("level", f64), ("seed", u64), ("prior", bsccs_prior),
+                ("solver", bsccs_solver_config), ("engine", i32), ("batch", i32)]
+
+
+class bsccs_bootstrap_result(C.Structure):
+    _fields_ = [("replicates", i32), ("used", i32), ("non_converged", i32), ("full_converged", i32),
+                ("device_seconds", f64), ("total_cycles", i64), ("coordinates_visited", i64)]
+
+
 # (name, restype, argtypes); restype int = bsccs_status
 _SIGS = [
     ("bsccs_abi_version", i32, []),
@@ -51,6 +75,10 @@ _SIGS = [
                                               C.c_void_p, i32, i32, P(C.c_void_p)]),
     ("bsccs_dataset_destroy", C.c_int, [C.c_void_p]),
     ("bsccs_dataset_info", C.c_int, [C.c_void_p, P(i64)]),
+    ("bsccs_dataset_subset", C.c_int, [C.c_void_p, C.c_void_p, i64, i32, P(C.c_void_p)]),
+    ("bsccs_dataset_export", C.c_int, [C.c_void_p] + [C.c_void_p] * 8),
+    ("bsccs_kfold_split", C.c_int, [i32, i32, u64, C.c_void_p, C.c_void_p]),
+    ("bsccs_resample", C.c_int, [i32, u64, u64, C.c_void_p]),
     ("bsccs_state_create", C.c_int, [C.c_void_p, C.c_void_p, P(C.c_void_p)]),
     ("bsccs_state_clone", C.c_int, [C.c_void_p, P(C.c_void_p)]),
     ("bsccs_state_destroy", C.c_int, [C.c_void_p]),
@@ -66,6 +94,20 @@ _SIGS = [
     ("bsccs_fit", C.c_int, [C.c_void_p, P(bsccs_prior), P(bsccs_solver_config), C.c_void_p, C.c_void_p,
                              P(bsccs_fit_result)]),
     ("bsccs_solver_config_default", None, [P(bsccs_solver_config)]),
+    ("bsccs_cv_config_default", None, [P(bsccs_cv_config)]),
+    ("bsccs_default_variance_grid", None, [C.c_void_p]),
+    ("bsccs_grid_search_cv", C.c_int, [C.c_void_p, P(bsccs_cv_config), C.c_void_p, i32, C.c_void_p,
+                                        C.c_void_p, C.c_void_p, P(bsccs_cv_result)]),
+    ("bsccs_cv_run_folds", C.c_int, [C.c_void_p, P(bsccs_cv_config), C.c_void_p, i32, i32, i32, C.c_void_p,
+                                      P(bsccs_cv_result)]),
+    ("bsccs_cv_select", C.c_int, [C.c_void_p, i32, i32, C.c_void_p, C.c_void_p, P(bsccs_cv_result)]),
+    ("bsccs_bootstrap_config_default", None, [P(bsccs_bootstrap_config)]),
+    ("bsccs_run_bootstrap", C.c_int, [C.c_void_p, P(bsccs_bootstrap_config), C.c_void_p, C.c_void_p,
+                                       C.c_void_p, C.c_void_p, P(bsccs_bootstrap_result)]),
+    ("bsccs_bootstrap_replicates", C.c_int, [C.c_void_p, P(bsccs_bootstrap_config), C.c_void_p, i32, i32,
+                                              C.c_void_p, C.c_void_p, P(bsccs_bootstrap_result)]),
+    ("bsccs_bootstrap_summarize", C.c_int, [i32, i32, f64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                             C.c_void_p, P(bsccs_bootstrap_result)]),
     ("bsccs_group_slot_bytes", i64, [i32]),
     ("bsccs_group_create_local", C.c_int, [P(C.c_void_p), i32, P(C.c_void_p)]),
     ("bsccs_group_create_virtual", C.c_int, [P(C.c_void_p), i32, P(C.c_void_p)]),

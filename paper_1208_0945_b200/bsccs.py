@@ -15,7 +15,7 @@ from __future__ import annotations
 import ctypes as C
 import enum
 from dataclasses import dataclass, field
-from typing import Optional, Sequence
+from typing import List, Optional, Sequence
 
 import numpy as np
 
@@ -385,15 +385,37 @@ def subset_dataset(ds: Dataset, subject_indices: Sequence[int]) -> Dataset:
                    new_row, out_sub[new_row], ydx, ds.drug_ids)
 
 
+def kfold_split(ds, folds: int, seed: int) -> List[np.ndarray]:
+    """cross_validation.hpp:58-80: seeded Fisher-Yates over subject ids,
+    dealt round-robin into `folds` lists (the reference's order)."""
+    n = ds.num_subjects
+    out = np.empty(n, dtype=np.int32)
+    sizes = np.empty(max(int(folds), 0), dtype=np.int32)
+    _check(lib().bsccs_kfold_split(n, int(folds), int(seed) & (2**64 - 1), _ptr(out), _ptr(sizes)))
+    return np.split(out, np.cumsum(sizes)[:-1])
+
+
+def resample(ds, seed: int, stream: int = 0) -> np.ndarray:
+    """bootstrap.hpp:43-52 with the generator Rng(seed, stream)."""
+    n = ds.num_subjects
+    out = np.empty(n, dtype=np.int32)
+    _check(lib().bsccs_resample(n, int(seed) & (2**64 - 1), int(stream) & (2**64 - 1), _ptr(out)))
+    return out
+
+
 # ---------------------------------------------------------------- device
 
 
 class DeviceDataset:
     """Device-resident dataset handle (bsccs_dataset_create)."""
 
-    def __init__(self, ds: Dataset, device: int = 0, ctas: int = 0, shard_globals=None):
+    def __init__(self, ds: Optional[Dataset], device: int = 0, ctas: int = 0, shard_globals=None, handle=None):
         self.host = ds
         self.device = device
+        if handle is not None:  # built on the device (subset)
+            self.handle = handle
+            self._sizes = None
+            return
         h = C.c_void_p()
         a = ds.arrays()
         if shard_globals is None:
@@ -405,6 +427,7 @@ class DeviceDataset:
                                                     *[_ptr(x) for x in a[:7]], _ptr(ydx), _ptr(cnnz), device, ctas,
                                                     C.byref(h)))
         self.handle = h
+        self._sizes = None
 
     def info(self):
         out = (C.c_int64 * 6)()
@@ -414,6 +437,32 @@ class DeviceDataset:
     @property
     def ctas(self) -> int:
         return self.info()["ctas"]
+
+    def _size(self, k):
+        if self._sizes is None:
+            self._sizes = self.info()
+        return int(self._sizes[k])
+
+    num_subjects = property(lambda s: s._size("N"))
+    num_eras = property(lambda s: s._size("K"))
+    num_drugs = property(lambda s: s._size("J"))
+    nnz = property(lambda s: s._size("nnz"))
+
+    def subset(self, subject_indices: Sequence[int], ctas: int = 0) -> "DeviceDataset":
+        """subset_dataset (dataset.hpp:157-217) built on the device."""
+        sel = np.ascontiguousarray(subject_indices, dtype=np.int32)
+        h = C.c_void_p()
+        _check(lib().bsccs_dataset_subset(self.handle, _ptr(sel), sel.size, ctas, C.byref(h)))
+        return DeviceDataset(None, self.device, ctas, handle=h)
+
+    def to_host(self) -> Dataset:
+        """Flat CSC arrays copied back from the device."""
+        n = self.info()
+        N, K, J, nnz = n["N"], n["K"], n["J"], n["nnz"]
+        arr = [np.empty(N + 1, np.int32), np.empty(N, np.int32), np.empty(K, np.int32), np.empty(K, np.int32),
+               np.empty(J + 1, np.int64), np.empty(nnz, np.int32), np.empty(nnz, np.int32), np.empty(J, np.int64)]
+        _check(lib().bsccs_dataset_export(self.handle, *[_ptr(a) for a in arr]))
+        return Dataset(*arr)
 
     def close(self):
         if self.handle:
@@ -443,7 +492,7 @@ class EngineState:
         self.handle = handle
 
     def _get(self, which):
-        ds = self.dds.host
+        ds = self.dds
         n = {"beta": ds.num_drugs, "xbeta": ds.num_eras, "l_exp_xbeta": ds.num_eras,
              "denominators": ds.num_subjects}[which]
         out = np.empty(n, dtype=np.float64)
@@ -480,7 +529,7 @@ def init_state(ds, beta: Optional[Sequence[float]] = None) -> EngineState:
     b = None
     if beta is not None and len(beta) > 0:
         b = np.ascontiguousarray(beta, dtype=np.float64)
-        if b.size != dds.host.num_drugs:
+        if b.size != dds.num_drugs:
             raise InputError("init_state: coefficient count does not match drug count")
     h = C.c_void_p()
     _check(lib().bsccs_state_create(dds.handle, _ptr(b), C.byref(h)))
@@ -492,7 +541,7 @@ def dense_recompute(ds, state: EngineState, beta: Optional[Sequence[float]] = No
     b = None
     if beta is not None:
         b = np.ascontiguousarray(beta, dtype=np.float64)
-        if b.size != state.dds.host.num_drugs:
+        if b.size != state.dds.num_drugs:
             raise InputError("dense_recompute: coefficient count does not match state")
     _check(lib().bsccs_dense_recompute(state.handle, _ptr(b)))
 
@@ -547,7 +596,7 @@ class SolverState:
     """solver.hpp:76-93: trust radii, visit order, cycle count, order RNG."""
 
     def __init__(self, ds, cfg: SolverConfig):
-        J = _dev(ds).host.num_drugs
+        J = _dev(ds).num_drugs
         self.trust = np.full(J, cfg.trust_init, dtype=np.float64)
         self.order = np.arange(J, dtype=np.int32)
         self.order_rng = Rng(cfg.cycle_seed)
@@ -576,7 +625,7 @@ def fit(ds, prior: PriorSpec, cfg: Optional[SolverConfig] = None, init_beta: Opt
     """solver.hpp:206-220 on the device (dataset uploaded once and cached)."""
     cfg = cfg or SolverConfig()
     dds = _dev(ds)
-    J = dds.host.num_drugs
+    J = dds.num_drugs
     b = None
     if init_beta is not None and len(init_beta) > 0:
         b = np.ascontiguousarray(init_beta, dtype=np.float64)

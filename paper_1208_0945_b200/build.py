@@ -18,8 +18,8 @@ CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libbsccs_b200.so"
 
-SOURCES = ["ccd_kernels.cu", "capi.cpp", "datagen.cpp"]
-HEADERS = ["engine.h", "prior.h", "rng.h", "status.h"]
+SOURCES = ["ccd_kernels.cu", "subset.cu", "batch.cu", "capi.cpp", "drivers.cpp", "datagen.cpp"]
+HEADERS = ["engine.h", "devutil.h", "prior.h", "rng.h", "status.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -30,8 +30,6 @@ thread_local std::string g_last_error;
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 
-namespace {
-
 PriorParams to_params(const bsccs_prior* p) {
     if (!p) input_error("null prior");
     if (p->kind < 0 || p->kind > 2) input_error("unknown prior kind");
@@ -68,6 +66,8 @@ double log_density(const PriorParams& p, const double* beta, int32_t n) {
     for (int32_t j = 0; j < n; ++j) abs_sum += std::abs(beta[j]);
     return -abs_sum / b - static_cast<double>(n) * std::log(2.0 * b);
 }
+
+namespace {
 
 void set_device(int dev) { CUDA_TRY(cudaSetDevice(dev)); }
 
@@ -218,6 +218,46 @@ void drop_workspaces(const bsccs_dataset* ds) {
 }
 
 } // namespace
+
+// fit (solver.hpp:206-220) on a resident dataset, validated arguments.
+void fit_resident(const bsccs_dataset* ds, const PriorParams& p, const bsccs_solver_config* cfg,
+                  const double* init_beta, double* beta_out, bsccs_fit_result* result) {
+    if (ds->N == 0) input_error("fit: dataset has no subjects");
+    set_device(ds->device);
+    std::memset(result, 0, sizeof *result);
+    cudaEvent_t e0, e1;
+    CUDA_TRY(cudaEventCreate(&e0));
+    CUDA_TRY(cudaEventCreate(&e1));
+    CUDA_TRY(cudaEventRecord(e0, nullptr));
+    bsccs_state* st = acquire_state(ds, init_beta);
+    try {
+        FitContext fc;
+        fc.states = {st};
+        fc.plan.shards = {st};
+        fc.plan.dst = {st->slots};
+        fc.plan.local_slots = st->slots;
+        fc.plan.counter = st->counter;
+        fc.plan.total_participants = ds->ctas;
+        fc.plan.participant_base = 0;
+        fit_loop(fc, p, cfg, beta_out, result, [](double x) { return x; });
+    } catch (...) {
+        release_state(st);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        throw;
+    }
+    release_state(st);
+    CUDA_TRY(cudaEventRecord(e1, nullptr));
+    CUDA_TRY(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+    result->device_seconds = ms * 1e-3;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+}
+
+void release_dataset_workspaces(const bsccs_dataset* ds) { drop_workspaces(ds); }
+
 } // namespace bsccs_b200
 
 // ---------------------------------------------------------------------------
@@ -332,6 +372,35 @@ bsccs_status bsccs_dataset_info(const bsccs_dataset* ds, int64_t out[6]) {
     });
 }
 
+bsccs_status bsccs_dataset_subset(const bsccs_dataset* ds, const int32_t* subject_indices, int64_t n,
+                                  int32_t num_ctas_override, bsccs_dataset** out) {
+    return guard([&] {
+        if (!out) input_error("null output handle");
+        *out = dataset_subset(ds, subject_indices, n, num_ctas_override);
+    });
+}
+
+bsccs_status bsccs_dataset_export(const bsccs_dataset* ds, int32_t* subject_offsets, int32_t* events_per_subject,
+                                  int32_t* era_lengths, int32_t* event_counts, int64_t* col_ptr, int32_t* rows,
+                                  int32_t* subjects, int64_t* y_dot_x) {
+    return guard([&] {
+        dataset_export(ds, subject_offsets, events_per_subject, era_lengths, event_counts, col_ptr, rows, subjects,
+                       y_dot_x);
+    });
+}
+
+bsccs_status bsccs_kfold_split(int32_t num_subjects, int32_t folds, uint64_t seed, int32_t* subjects_out,
+                               int32_t* fold_sizes) {
+    return guard([&] { kfold_split(num_subjects, folds, seed, subjects_out, fold_sizes); });
+}
+
+bsccs_status bsccs_resample(int32_t num_subjects, uint64_t seed, uint64_t stream, int32_t* out) {
+    return guard([&] {
+        if (!out) input_error("null output");
+        resample(num_subjects, seed, stream, out);
+    });
+}
+
 bsccs_status bsccs_state_create(const bsccs_dataset* ds, const double* beta, bsccs_state** out) {
     return guard([&] { *out = state_create(ds, beta); });
 }
@@ -436,38 +505,7 @@ bsccs_status bsccs_fit(const bsccs_dataset* ds, const bsccs_prior* prior, const 
         if (!ds || !beta_out || !result) input_error("fit: null argument");
         validate_config(cfg);
         const PriorParams p = to_params(prior);
-        if (ds->N == 0) input_error("fit: dataset has no subjects");
-        set_device(ds->device);
-        std::memset(result, 0, sizeof *result);
-        cudaEvent_t e0, e1;
-        CUDA_TRY(cudaEventCreate(&e0));
-        CUDA_TRY(cudaEventCreate(&e1));
-        CUDA_TRY(cudaEventRecord(e0, nullptr));
-        bsccs_state* st = acquire_state(ds, init_beta);
-        try {
-            FitContext fc;
-            fc.states = {st};
-            fc.plan.shards = {st};
-            fc.plan.dst = {st->slots};
-            fc.plan.local_slots = st->slots;
-            fc.plan.counter = st->counter;
-            fc.plan.total_participants = ds->ctas;
-            fc.plan.participant_base = 0;
-            fit_loop(fc, p, cfg, beta_out, result, [](double x) { return x; });
-        } catch (...) {
-            release_state(st);
-            cudaEventDestroy(e0);
-            cudaEventDestroy(e1);
-            throw;
-        }
-        release_state(st);
-        CUDA_TRY(cudaEventRecord(e1, nullptr));
-        CUDA_TRY(cudaEventSynchronize(e1));
-        float ms = 0.f;
-        CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
-        result->device_seconds = ms * 1e-3;
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
+        fit_resident(ds, p, cfg, init_beta, beta_out, result);
     });
 }
 

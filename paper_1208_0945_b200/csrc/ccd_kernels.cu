@@ -32,6 +32,7 @@
 #include <vector>
 
 #include "engine.h"
+#include "devutil.h"
 
 namespace bsccs_b200 {
 
@@ -1282,94 +1283,6 @@ __global__ void k_ydotx(const int2* pairs, const int64_t* col_ptr, const int32_t
     }
 }
 
-int grid_for(int64_t n, int threads, int dev_sms) {
-    const int64_t g = (n + threads - 1) / threads;
-    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(g, static_cast<int64_t>(dev_sms) * 32)));
-}
-
-// Stream-ordered allocations from the device's default memory pool, which
-// is told to retain freed memory: re-creating datasets / fit workspaces
-// (bootstrap replicates, the e2e bench) then costs no cudaMalloc/cudaFree.
-void ensure_pool(int device) {
-    static std::atomic<unsigned> done{0};
-    if (device < 32 && (done.load() & (1u << device))) return;
-    cudaMemPool_t pool;
-    CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, device));
-    unsigned long long keep = ~0ull;
-    CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-    if (device < 32) done.fetch_or(1u << device);
-}
-
-template <typename T>
-T* dalloc(int64_t count, int64_t& bytes, cudaStream_t s) {
-    T* p = nullptr;
-    if (count <= 0) count = 1;
-    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * static_cast<size_t>(count), s));
-    bytes += static_cast<int64_t>(sizeof(T)) * count;
-    return p;
-}
-
-template <typename T>
-void dfree(T*& p, cudaStream_t s) {
-    if (p) cudaFreeAsync(p, s);
-    p = nullptr;
-}
-
-// Host -> device copy of pageable caller memory through two pinned staging
-// buffers: host threads fill one buffer while the DMA engine drains the other.
-struct Staging {
-    std::mutex m;
-    unsigned char* buf[2] = {nullptr, nullptr};
-    cudaEvent_t ev[2] = {nullptr, nullptr};
-    int device = -1;
-    static constexpr size_t kChunk = size_t(64) << 20;
-};
-Staging g_staging;
-
-void parallel_memcpy(void* dst, const void* src, size_t n) {
-    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    const size_t T = std::min<size_t>(std::min<size_t>(hw, 16), std::max<size_t>(1, n >> 22));
-    if (T <= 1) {
-        std::memcpy(dst, src, n);
-        return;
-    }
-    std::vector<std::thread> th;
-    for (size_t t = 0; t < T; ++t) {
-        const size_t a = n * t / T, b = n * (t + 1) / T;
-        th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a); });
-    }
-    for (auto& x : th) x.join();
-}
-
-void h2d(void* dst, const void* src, size_t bytes, cudaStream_t s, int device) {
-    if (bytes == 0) return;
-    if (bytes < (size_t(4) << 20)) { // small: a plain async copy
-        CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
-        return;
-    }
-    std::lock_guard<std::mutex> lk(g_staging.m);
-    if (g_staging.device != device) {
-        for (int i = 0; i < 2; ++i) {
-            if (g_staging.buf[i]) cudaFreeHost(g_staging.buf[i]);
-            if (g_staging.ev[i]) cudaEventDestroy(g_staging.ev[i]);
-            CUDA_TRY(cudaMallocHost(&g_staging.buf[i], Staging::kChunk));
-            CUDA_TRY(cudaEventCreateWithFlags(&g_staging.ev[i], cudaEventDisableTiming));
-            CUDA_TRY(cudaEventRecord(g_staging.ev[i], s));
-        }
-        g_staging.device = device;
-    }
-    int k = 0;
-    for (size_t off = 0; off < bytes; off += Staging::kChunk, k ^= 1) {
-        const size_t n = std::min(Staging::kChunk, bytes - off);
-        CUDA_TRY(cudaEventSynchronize(g_staging.ev[k]));
-        parallel_memcpy(g_staging.buf[k], static_cast<const char*>(src) + off, n);
-        CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(dst) + off, g_staging.buf[k], n, cudaMemcpyHostToDevice, s));
-        CUDA_TRY(cudaEventRecord(g_staging.ev[k], s));
-    }
-    // the staging buffers are reused by the next call only after its events
-    CUDA_TRY(cudaEventSynchronize(g_staging.ev[k ^ 1]));
-}
-
 // Small pinned result blocks for the per-state D2H of kernel scalars.
 struct PinnedResults {
     std::mutex m;
@@ -1395,24 +1308,6 @@ void release_pinned_result(DevResult* r) {
     g_pinned.free_list.push_back(r);
 }
 
-int sm_count(int device) {
-    int n = 0;
-    CUDA_TRY(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device));
-    return n;
-}
-
-struct DeviceGuard {
-    int prev = -1;
-    explicit DeviceGuard(int dev) {
-        CUDA_TRY(cudaGetDevice(&prev));
-        if (prev != dev) CUDA_TRY(cudaSetDevice(dev));
-    }
-    ~DeviceGuard() {
-        int cur = -1;
-        if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
-    }
-};
-
 void sync_and_check(bsccs_state* st) {
     CUDA_TRY(cudaStreamSynchronize(st->stream));
     CUDA_TRY(cudaGetLastError());
@@ -1429,7 +1324,6 @@ void check_err_block(bsccs_state* st) {
     }
 }
 
-int build_grid(int device) { return sm_count(device) * 8; }
 
 } // namespace
 
@@ -1474,6 +1368,151 @@ int default_ctas(int device) {
 }
 
 // ---------------------------------------------------------------------------
+namespace {
+
+// Allocates the dataset's device arrays (sizes and CTA count already set).
+void alloc_dataset(bsccs_dataset* ds) {
+    const int C = ds->ctas;
+    const int32_t N = ds->N, K = ds->K, J = ds->J;
+    const int64_t nnz = ds->nnz;
+    int64_t& B = ds->device_bytes;
+    CUDA_TRY(cudaStreamCreateWithFlags(&ds->stream, cudaStreamNonBlocking));
+    cudaStream_t s = ds->stream;
+    ds->pairs = dalloc<int2>(nnz, B, s);
+    ds->col_ptr = dalloc<int64_t>(J + 1, B, s);
+    ds->split = dalloc<int64_t>(static_cast<int64_t>(J) * (C + 1), B, s);
+    ds->cta_era = dalloc<int32_t>(C + 1, B, s);
+    ds->cta_subj = dalloc<int32_t>(C + 1, B, s);
+    ds->subject_offsets = dalloc<int32_t>(N + 1, B, s);
+    ds->events_per_subject = dalloc<int32_t>(N, B, s);
+    ds->era_lengths = dalloc<int32_t>(K, B, s);
+    ds->event_counts = dalloc<int32_t>(K, B, s);
+    ds->csr_ptr = dalloc<int64_t>(static_cast<int64_t>(K) + 1, B, s);
+    ds->csr_col = dalloc<int32_t>(nnz, B, s);
+    ds->y_dot_x = dalloc<double>(J, B, s);
+    ds->col_nonempty = dalloc<uint8_t>(J, B, s);
+    ds->col_runs = dalloc<int32_t>(J, B, s);
+}
+
+} // namespace
+
+// Device half of the dataset build.  On entry the small arrays (col_ptr,
+// subject_offsets, events_per_subject, era_lengths, event_counts) are on the
+// device, ds->col_ptr_h holds the column pointers, and d_rows / d_subj (owned
+// here, freed on return) hold the CSC pair arrays.  Validates the
+// build_dataset invariants (dataset.hpp:135-175), builds the interleaved
+// pairs, the row-major copy, the CTA ranges and the per-column splits.
+void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const int64_t* y_dot_x_global,
+                    const int64_t* col_nnz_global) {
+    const int C = ds->ctas;
+    const int32_t N = ds->N, K = ds->K, J = ds->J;
+    const int64_t nnz = ds->nnz;
+    const int sms = sm_count(ds->device);
+    cudaStream_t s = ds->stream;
+    int64_t scratch_bytes = 0;
+    int32_t* d_col = dalloc<int32_t>(nnz, scratch_bytes, s);
+    unsigned long long* d_cnt = dalloc<unsigned long long>(static_cast<int64_t>(K) + 1, scratch_bytes, s);
+    long long* d_w = dalloc<long long>(static_cast<int64_t>(N) + 1, scratch_bytes, s);
+    long long* d_excl = dalloc<long long>(static_cast<int64_t>(N) + 1, scratch_bytes, s);
+    int* d_bad = dalloc<int>(1, scratch_bytes, s);
+    CUDA_TRY(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * (static_cast<size_t>(K) + 1), s));
+    CUDA_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
+    k_validate_small<<<grid_for(std::max<int64_t>(N, K), 256, sms), 256, 0, s>>>(ds->subject_offsets, N,
+                                                                             ds->era_lengths, K, d_bad);
+    if (nnz > 0) {
+        k_interleave<<<grid_for(nnz, 256, sms), 256, 0, s>>>(d_rows, d_subj, ds->pairs, nnz);
+        k_pair_meta<<<grid_for(nnz, 256, sms), 256, 0, s>>>(ds->pairs, ds->col_ptr, J, ds->subject_offsets, N, K,
+                                                           nnz, d_col, d_cnt, d_bad);
+    }
+    // CSR: exclusive scan of the row histogram, stable sort by row
+    {
+        size_t tmp_bytes = 0;
+        CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_cnt,
+                                               reinterpret_cast<unsigned long long*>(ds->csr_ptr), K + 1, s));
+        size_t sort_bytes = 0;
+        int end_bit = 1;
+        while ((1ll << end_bit) < static_cast<long long>(K)) ++end_bit;
+        if (nnz > 0)
+            CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, d_rows, d_subj, d_col, ds->csr_col, nnz, 0,
+                                                     end_bit, s));
+        size_t scan2 = 0;
+        CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, scan2, d_w, d_excl, N + 1, s));
+        const size_t tb = std::max(std::max(tmp_bytes, sort_bytes), scan2);
+        unsigned char* tmp = dalloc<unsigned char>(static_cast<int64_t>(std::max<size_t>(tb, 16)), scratch_bytes, s);
+        CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, d_cnt,
+                                               reinterpret_cast<unsigned long long*>(ds->csr_ptr), K + 1, s));
+        if (nnz > 0) {
+            // keys: rows (consumed); d_subj is free after interleave and
+            // receives the sorted keys
+            CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, d_rows, d_subj, d_col, ds->csr_col, nnz, 0,
+                                                     end_bit, s));
+        }
+        // nnz-balanced CTA subject ranges
+        k_subject_weight<<<grid_for(N, 256, sms), 256, 0, s>>>(ds->subject_offsets, ds->csr_ptr, N, d_w);
+        CUDA_TRY(cudaMemsetAsync(d_w + N, 0, sizeof(long long), s));
+        CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, scan2, d_w, d_excl, N + 1, s));
+        k_cta_bounds<<<(C + 1 + 127) / 128, 128, 0, s>>>(d_excl, N, C, ds->subject_offsets, ds->cta_subj,
+                                                         ds->cta_era);
+        k_col_runs<<<J, 256, 0, s>>>(ds->pairs, ds->col_ptr, ds->col_runs, J);
+        const int64_t nsplit = static_cast<int64_t>(J) * (C + 1);
+        k_split<<<static_cast<int>((nsplit + 255) / 256), 256, 0, s>>>(ds->pairs, ds->col_ptr, J, ds->cta_subj, C,
+                                                                        ds->split);
+        if (y_dot_x_global) {
+            std::vector<double> yd(static_cast<size_t>(J));
+            for (int32_t j = 0; j < J; ++j) yd[static_cast<size_t>(j)] = static_cast<double>(y_dot_x_global[j]);
+            CUDA_TRY(cudaMemcpyAsync(ds->y_dot_x, yd.data(), sizeof(double) * J, cudaMemcpyHostToDevice, s));
+            CUDA_TRY(cudaStreamSynchronize(s)); // yd is stack-owned
+        } else {
+            k_ydotx<<<J, 256, 0, s>>>(ds->pairs, ds->col_ptr, ds->event_counts, ds->y_dot_x, J);
+        }
+        count_launches(5 + (nnz > 0 ? 2 : 0) + (y_dot_x_global ? 0 : 1));
+        dfree(tmp, s);
+    }
+    int bad = 0;
+    CUDA_TRY(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+    dfree(d_rows, s);
+    dfree(d_subj, s);
+    dfree(d_col, s);
+    dfree(d_cnt, s);
+    dfree(d_w, s);
+    dfree(d_excl, s);
+    dfree(d_bad, s);
+    CUDA_TRY(cudaStreamSynchronize(s));
+    CUDA_TRY(cudaGetLastError());
+    if (bad & 2) input_error("dataset: every subject needs at least one era");
+    if (bad & 4) input_error("dataset: era length must be positive");
+    if (bad & 1) input_error("dataset: invalid pair (row/subject out of range, subject not owning its row, "
+                             "or rows not strictly ascending within a column)");
+
+    ds->col_runs_h.resize(static_cast<size_t>(J));
+    CUDA_TRY(cudaMemcpy(ds->col_runs_h.data(), ds->col_runs, sizeof(int32_t) * J, cudaMemcpyDeviceToHost));
+    ds->col_nonempty_h.resize(static_cast<size_t>(J));
+    for (int32_t j = 0; j < J; ++j) {
+        const int64_t cnt =
+            col_nnz_global ? col_nnz_global[j] : (ds->col_ptr_h[static_cast<size_t>(j) + 1] - ds->col_ptr_h[j]);
+        ds->col_nonempty_h[static_cast<size_t>(j)] = cnt > 0 ? 1 : 0;
+    }
+    CUDA_TRY(cudaMemcpy(ds->col_nonempty, ds->col_nonempty_h.data(), J, cudaMemcpyHostToDevice));
+}
+
+bsccs_dataset* dataset_new(int32_t N, int32_t K, int32_t J, int64_t nnz, int device, int ctas_override) {
+    ensure_pool(device);
+    auto* ds = new bsccs_dataset();
+    try {
+        ds->device = device;
+        ds->N = N;
+        ds->K = K;
+        ds->J = J;
+        ds->nnz = nnz;
+        ds->ctas = ctas_override > 0 ? ctas_override : default_ctas(device);
+        alloc_dataset(ds);
+    } catch (...) {
+        dataset_destroy(ds);
+        throw;
+    }
+    return ds;
+}
+
 bsccs_dataset* dataset_create(int32_t N, int32_t K, int32_t J, int64_t nnz, const int32_t* subject_offsets,
                               const int32_t* events_per_subject, const int32_t* era_lengths,
                               const int32_t* event_counts, const int64_t* col_ptr, const int32_t* rows,
@@ -1492,131 +1531,23 @@ bsccs_dataset* dataset_create(int32_t N, int32_t K, int32_t J, int64_t nnz, cons
     // per-subject and per-era checks run on the device after the upload
 
     DeviceGuard g(device);
-    ensure_pool(device);
-    auto* ds = new bsccs_dataset();
+    bsccs_dataset* ds = dataset_new(N, K, J, nnz, device, ctas_override);
     try {
-        ds->device = device;
-        ds->N = N;
-        ds->K = K;
-        ds->J = J;
-        ds->nnz = nnz;
-        ds->ctas = ctas_override > 0 ? ctas_override : default_ctas(device);
-        const int C = ds->ctas;
-        const int sms = sm_count(device);
-        int64_t& B = ds->device_bytes;
-        CUDA_TRY(cudaStreamCreateWithFlags(&ds->stream, cudaStreamNonBlocking));
         cudaStream_t s = ds->stream;
-
-        ds->pairs = dalloc<int2>(nnz, B, s);
-        ds->col_ptr = dalloc<int64_t>(J + 1, B, s);
-        ds->split = dalloc<int64_t>(static_cast<int64_t>(J) * (C + 1), B, s);
-        ds->cta_era = dalloc<int32_t>(C + 1, B, s);
-        ds->cta_subj = dalloc<int32_t>(C + 1, B, s);
-        ds->subject_offsets = dalloc<int32_t>(N + 1, B, s);
-        ds->events_per_subject = dalloc<int32_t>(N, B, s);
-        ds->era_lengths = dalloc<int32_t>(K, B, s);
-        ds->event_counts = dalloc<int32_t>(K, B, s);
-        ds->csr_ptr = dalloc<int64_t>(static_cast<int64_t>(K) + 1, B, s);
-        ds->csr_col = dalloc<int32_t>(nnz, B, s);
-        ds->y_dot_x = dalloc<double>(J, B, s);
-        ds->col_nonempty = dalloc<uint8_t>(J, B, s);
-        ds->col_runs = dalloc<int32_t>(J, B, s);
-
         h2d(ds->col_ptr, col_ptr, sizeof(int64_t) * (J + 1), s, device);
         h2d(ds->subject_offsets, subject_offsets, sizeof(int32_t) * (N + 1), s, device);
         h2d(ds->events_per_subject, events_per_subject, sizeof(int32_t) * N, s, device);
         h2d(ds->era_lengths, era_lengths, sizeof(int32_t) * K, s, device);
         h2d(ds->event_counts, event_counts, sizeof(int32_t) * K, s, device);
-
-        // scratch for the build: rows, subjects, column ids, sort buffers
         int64_t scratch_bytes = 0;
         int32_t* d_rows = dalloc<int32_t>(nnz, scratch_bytes, s);
         int32_t* d_subj = dalloc<int32_t>(nnz, scratch_bytes, s);
-        int32_t* d_col = dalloc<int32_t>(nnz, scratch_bytes, s);
-        unsigned long long* d_cnt = dalloc<unsigned long long>(static_cast<int64_t>(K) + 1, scratch_bytes, s);
-        long long* d_w = dalloc<long long>(static_cast<int64_t>(N) + 1, scratch_bytes, s);
-        long long* d_excl = dalloc<long long>(static_cast<int64_t>(N) + 1, scratch_bytes, s);
-        int* d_bad = dalloc<int>(1, scratch_bytes, s);
         if (nnz > 0) {
             h2d(d_rows, rows, sizeof(int32_t) * nnz, s, device);
             h2d(d_subj, subjects, sizeof(int32_t) * nnz, s, device);
         }
-        CUDA_TRY(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * (static_cast<size_t>(K) + 1), s));
-        CUDA_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
-        k_validate_small<<<grid_for(std::max<int64_t>(N, K), 256, sms), 256, 0, s>>>(ds->subject_offsets, N,
-                                                                                 ds->era_lengths, K, d_bad);
-        if (nnz > 0) {
-            k_interleave<<<grid_for(nnz, 256, sms), 256, 0, s>>>(d_rows, d_subj, ds->pairs, nnz);
-            k_pair_meta<<<grid_for(nnz, 256, sms), 256, 0, s>>>(ds->pairs, ds->col_ptr, J, ds->subject_offsets, N, K,
-                                                               nnz, d_col, d_cnt, d_bad);
-        }
-        // CSR: exclusive scan of the row histogram, stable sort by row
-        {
-            size_t tmp_bytes = 0;
-            CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_cnt,
-                                                   reinterpret_cast<unsigned long long*>(ds->csr_ptr), K + 1, s));
-            size_t sort_bytes = 0;
-            int end_bit = 1;
-            while ((1ll << end_bit) < static_cast<long long>(K)) ++end_bit;
-            if (nnz > 0)
-                CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, d_rows, d_subj, d_col, ds->csr_col,
-                                                         nnz, 0, end_bit, s));
-            size_t scan2 = 0;
-            CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, scan2, d_w, d_excl, N + 1, s));
-            const size_t tb = std::max(std::max(tmp_bytes, sort_bytes), scan2);
-            unsigned char* tmp = dalloc<unsigned char>(static_cast<int64_t>(std::max<size_t>(tb, 16)), scratch_bytes, s);
-            CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, d_cnt,
-                                                   reinterpret_cast<unsigned long long*>(ds->csr_ptr), K + 1, s));
-            if (nnz > 0) {
-                // keys: copy of rows (d_rows is consumed as the key input;
-                // d_subj is free after interleave and receives sorted keys)
-                CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, d_rows, d_subj, d_col, ds->csr_col, nnz, 0,
-                                                         end_bit, s));
-            }
-            // nnz-balanced CTA subject ranges
-            k_subject_weight<<<grid_for(N, 256, sms), 256, 0, s>>>(ds->subject_offsets, ds->csr_ptr, N, d_w);
-            CUDA_TRY(cudaMemsetAsync(d_w + N, 0, sizeof(long long), s));
-            CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, scan2, d_w, d_excl, N + 1, s));
-            k_cta_bounds<<<(C + 1 + 127) / 128, 128, 0, s>>>(d_excl, N, C, ds->subject_offsets, ds->cta_subj,
-                                                             ds->cta_era);
-            k_col_runs<<<J, 256, 0, s>>>(ds->pairs, ds->col_ptr, ds->col_runs, J);
-            const int64_t nsplit = static_cast<int64_t>(J) * (C + 1);
-            k_split<<<static_cast<int>((nsplit + 255) / 256), 256, 0, s>>>(ds->pairs, ds->col_ptr, J, ds->cta_subj,
-                                                                            C, ds->split);
-            if (y_dot_x_global) {
-                std::vector<double> yd(static_cast<size_t>(J));
-                for (int32_t j = 0; j < J; ++j) yd[static_cast<size_t>(j)] = static_cast<double>(y_dot_x_global[j]);
-                CUDA_TRY(cudaMemcpyAsync(ds->y_dot_x, yd.data(), sizeof(double) * J, cudaMemcpyHostToDevice, s));
-                CUDA_TRY(cudaStreamSynchronize(s)); // yd is stack-owned
-            } else {
-                k_ydotx<<<J, 256, 0, s>>>(ds->pairs, ds->col_ptr, ds->event_counts, ds->y_dot_x, J);
-            }
-            dfree(tmp, s);
-        }
-        int bad = 0;
-        CUDA_TRY(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
-        dfree(d_rows, s);
-        dfree(d_subj, s);
-        dfree(d_col, s);
-        dfree(d_cnt, s);
-        dfree(d_w, s);
-        dfree(d_excl, s);
-        dfree(d_bad, s);
-        CUDA_TRY(cudaStreamSynchronize(s));
-        if (bad & 2) input_error("dataset: every subject needs at least one era");
-        if (bad & 4) input_error("dataset: era length must be positive");
-        if (bad & 1) input_error("dataset: invalid pair (row/subject out of range, subject not owning its row, "
-                                 "or rows not strictly ascending within a column)");
-
         ds->col_ptr_h.assign(col_ptr, col_ptr + J + 1);
-        ds->col_runs_h.resize(static_cast<size_t>(J));
-        CUDA_TRY(cudaMemcpy(ds->col_runs_h.data(), ds->col_runs, sizeof(int32_t) * J, cudaMemcpyDeviceToHost));
-        ds->col_nonempty_h.resize(static_cast<size_t>(J));
-        for (int32_t j = 0; j < J; ++j) {
-            const int64_t cnt = col_nnz_global ? col_nnz_global[j] : (col_ptr[j + 1] - col_ptr[j]);
-            ds->col_nonempty_h[static_cast<size_t>(j)] = cnt > 0 ? 1 : 0;
-        }
-        CUDA_TRY(cudaMemcpy(ds->col_nonempty, ds->col_nonempty_h.data(), J, cudaMemcpyHostToDevice));
+        finish_dataset(ds, d_rows, d_subj, y_dot_x_global, col_nnz_global);
     } catch (...) {
         dataset_destroy(ds);
         throw;

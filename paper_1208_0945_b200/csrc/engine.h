@@ -151,6 +151,18 @@ bsccs_dataset* dataset_create(int32_t N, int32_t K, int32_t J, int64_t nnz,
                               const int64_t* y_dot_x_global, const int64_t* col_nnz_global,
                               int device, int ctas_override);
 void dataset_destroy(bsccs_dataset* ds);
+// building blocks of dataset_create, shared with the device-side subset
+bsccs_dataset* dataset_new(int32_t N, int32_t K, int32_t J, int64_t nnz, int device, int ctas_override);
+void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const int64_t* y_dot_x_global,
+                    const int64_t* col_nnz_global);
+// subset_dataset (dataset.hpp:157-217) built on the device (subset.cu)
+bsccs_dataset* dataset_subset(const bsccs_dataset* parent, const int32_t* subject_indices, int64_t n,
+                              int ctas_override);
+void dataset_export(const bsccs_dataset* ds, int32_t* subject_offsets, int32_t* events_per_subject,
+                    int32_t* era_lengths, int32_t* event_counts, int64_t* col_ptr, int32_t* rows, int32_t* subjects,
+                    int64_t* y_dot_x);
+void kfold_split(int32_t N, int32_t folds, uint64_t seed, int32_t* subjects_out, int32_t* fold_sizes);
+void resample(int32_t N, uint64_t seed, uint64_t stream, int32_t* out);
 
 bsccs_state* state_create(const bsccs_dataset* ds, const double* beta_host);
 bsccs_state* state_clone(const bsccs_state* src);
@@ -190,5 +202,20 @@ void set_debug_flags(int flags); // profiling only
 void set_debug_trace(int ncoords, int ctas);
 void read_debug_trace(unsigned long long* host, size_t words);
 void throw_device_error(int code, double value);
+
+// ---- host driver (capi.cpp) ---------------------------------------------
+PriorParams to_params(const bsccs_prior* p);                // validate_prior + constants
+void validate_config(const bsccs_solver_config* c);         // validate_config + device knobs
+double log_density(const PriorParams& p, const double* beta, int32_t n);
+void fit_resident(const bsccs_dataset* ds, const PriorParams& p, const bsccs_solver_config* cfg,
+                  const double* init_beta, double* beta_out, bsccs_fit_result* result);
+void release_dataset_workspaces(const bsccs_dataset* ds);
+
+// ---- batched weighted engine (batch.cu) ---------------------------------
+void cv_folds_batched(const bsccs_dataset* ds, const bsccs_cv_config* cfg, const std::vector<double>& grid,
+                      const std::vector<int32_t>& fold_subjects, const std::vector<int32_t>& fold_sizes, int32_t f0,
+                      int32_t f1, bsccs_cv_cell* cells, bsccs_cv_result* res);
+void boot_replicates_batched(const bsccs_dataset* ds, const bsccs_bootstrap_config* cfg, const double* beta_full,
+                             int32_t r0, int32_t r1, double* est, int32_t* conv, bsccs_bootstrap_result* res);
 
 } // namespace bsccs_b200

@@ -189,6 +189,32 @@ def fast_case(ref: po.Reference, name, attempts, drugs, lam, prior, zipf=False):
             **fit_dict(r)}
 
 
+def drivers_case(ref: po.Reference):
+    """grid_search_cv (config 4's shape, scaled to the oracle case) and
+    run_bootstrap (config 5's shape, 16 replicates) by the reference."""
+    cfg = datagen.oracle_case_config()
+    rds = ref.simulate(cfg)
+    ds = rds.to_host()
+    lo, hi = np.log(0.001), np.log(10.0)
+    grid = [float(np.exp(lo + (hi - lo) * i / 7.0)) for i in range(8)]  # SURVEY §8(d) config 4: 8 points
+    cv = {"folds": 8, "grid": grid,
+          "prior": "laplace", "seed": 17, "warm_start": True}
+    r = rds.grid_search_cv(cv["folds"], cv["grid"], B.PriorKind.laplace, cv["seed"], B.SolverConfig(),
+                           warm_start=True, threads=8)
+    cv["expected"] = {"variance_grid": r["variance_grid"].tolist(),
+                      "predictive_ll": [[repr(float(x)) for x in row] for row in r["predictive_ll"]],
+                      "cycles": r["cycles"].tolist(), "converged": r["converged"].tolist(),
+                      "valid": r["valid"].tolist(),
+                      "mean_predictive_ll": [repr(float(x)) for x in r["mean_predictive_ll"]],
+                      "selected_index": r["selected_index"], "selected_variance": r["selected_variance"],
+                      "total_cycles": r["total_cycles"]}
+    boot = {"replicates": 16, "level": 0.95, "seed": 77, "prior": "normal", "variance": 0.1, "warm_start": True}
+    b = rds.run_bootstrap(16, 0.95, 77, B.normal_prior(0.1), B.SolverConfig(), warm_start=True, threads=8)
+    boot["expected"] = {k: ([repr(float(x)) for x in v] if isinstance(v, np.ndarray) else v) for k, v in b.items()}
+    return {"config": "oracle case (simulate 10300 x 100, seed 12080945)", "digest": digest(ds),
+            "resample_77_1_head": rds.resample(77, 1)[:32].tolist(), "cv": cv, "bootstrap": boot}
+
+
 def main():
     ref = po.Reference()
     large = "--large" in sys.argv
@@ -200,6 +226,9 @@ def main():
     if want("oracle_case"):
         (OUT / "oracle_case.json").write_text(json.dumps(oracle_case(ref), indent=1))
         print("oracle_case.json")
+    if want("drivers"):
+        (OUT / "drivers_oracle_case.json").write_text(json.dumps(drivers_case(ref), indent=1))
+        print("drivers_oracle_case.json")
     if want("engine_cases"):
         (OUT / "engine_cases.json").write_text(json.dumps(engine_cases(ref)))
         print("engine_cases.json")
