@@ -230,6 +230,19 @@ void bsccs_solver_config_default(bsccs_solver_config* cfg);
 #define BSCCS_ENGINE_SUBSET 0
 #define BSCCS_ENGINE_BATCHED 1
 
+/* R independent fits (1 <= R <= 16) on one resident dataset in one batched
+ * launch per cycle: fit r weights subject i by weights[r * num_subjects + i]
+ * (its multiplicity in the selection: 0 leaves it out, m > 1 repeats it;
+ * NULL = every subject once), with its own prior and start (init_beta
+ * [R x num_drugs] or NULL).  Equivalent to fit() on the materialised
+ * selection (subset_dataset) up to summation order.  status[r] receives the
+ * fit's own outcome (a failed fit does not stop the others). */
+bsccs_status bsccs_fit_batch(const bsccs_dataset* ds, int32_t R,
+                             const bsccs_prior* priors,
+                             const int32_t* weights, const double* init_beta,
+                             const bsccs_solver_config* cfg, double* beta_out,
+                             bsccs_fit_result* results, int32_t* status);
+
 /* CVConfig (cross_validation.hpp:29-41); the grid is passed separately. */
 typedef struct bsccs_cv_config {
     int32_t folds;

@@ -94,6 +94,8 @@ _SIGS = [
     ("bsccs_fit", C.c_int, [C.c_void_p, P(bsccs_prior), P(bsccs_solver_config), C.c_void_p, C.c_void_p,
                              P(bsccs_fit_result)]),
     ("bsccs_solver_config_default", None, [P(bsccs_solver_config)]),
+    ("bsccs_fit_batch", C.c_int, [C.c_void_p, i32, P(bsccs_prior), C.c_void_p, C.c_void_p, P(bsccs_solver_config),
+                                   C.c_void_p, P(bsccs_fit_result), C.c_void_p]),
     ("bsccs_cv_config_default", None, [P(bsccs_cv_config)]),
     ("bsccs_default_variance_grid", None, [C.c_void_p]),
     ("bsccs_grid_search_cv", C.c_int, [C.c_void_p, P(bsccs_cv_config), C.c_void_p, i32, C.c_void_p,

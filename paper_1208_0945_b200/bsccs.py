@@ -640,6 +640,32 @@ def fit(ds, prior: PriorSpec, cfg: Optional[SolverConfig] = None, init_beta: Opt
                      res.sweep_seconds, res.algorithmic_bytes, res.kernel_launches)
 
 
+def fit_batch(ds, priors: Sequence[PriorSpec], weights=None, init_betas=None,
+              cfg: Optional[SolverConfig] = None):
+    """R <= 16 fits in one batched launch per cycle (bsccs_fit_batch): fit r
+    weights subject i by weights[r][i] (its multiplicity in a selection; 0
+    leaves it out).  Returns (list of FitResult, list of per-fit status) --
+    a failed fit carries its exception class instead of stopping the batch."""
+    cfg = cfg or SolverConfig()
+    dds = _dev(ds)
+    R, J, N = len(priors), dds.num_drugs, dds.num_subjects
+    pr = (bsccs_prior * max(R, 1))(*[p._c() for p in priors])
+    w = None if weights is None else np.ascontiguousarray(weights, dtype=np.int32).reshape(R, N)
+    b0 = None if init_betas is None else np.ascontiguousarray(init_betas, dtype=np.float64).reshape(R, J)
+    beta = np.zeros((max(R, 1), J))
+    res = (bsccs_fit_result * max(R, 1))()
+    st = np.zeros(max(R, 1), dtype=np.int32)
+    c = cfg._c()
+    _check(lib().bsccs_fit_batch(dds.handle, R, pr, _ptr(w), _ptr(b0), C.byref(c), _ptr(beta), res, _ptr(st)))
+    out = []
+    for r in range(R):
+        x = res[r]
+        out.append(FitResult(beta[r].copy(), x.log_posterior, x.cycles_run, bool(x.converged), x.final_criterion,
+                             x.coordinates_visited, x.coordinates_moved, x.dense_refreshes, x.device_seconds,
+                             x.sweep_seconds, x.algorithmic_bytes, x.kernel_launches))
+    return out, [None if s == 0 else _STATUS.get(int(s), InternalError) for s in st[:R]]
+
+
 def launch_count() -> int:
     return int(lib().bsccs_launch_count())
 

@@ -336,6 +336,48 @@ bsccs_status bsccs_bootstrap_summarize(int32_t num_drugs, int32_t replicates, do
     });
 }
 
+bsccs_status bsccs_fit_batch(const bsccs_dataset* ds, int32_t R, const bsccs_prior* priors, const int32_t* weights,
+                             const double* init_beta, const bsccs_solver_config* cfg, double* beta_out,
+                             bsccs_fit_result* results, int32_t* status) {
+    return guard([&] {
+        if (!ds || !priors || !beta_out || !results || !status) input_error("fit_batch: null argument");
+        if (R < 1 || R > 16) input_error("fit_batch: 1..16 fits per batch");
+        validate_config(cfg);
+        const int32_t N = ds->N, J = ds->J;
+        std::vector<PriorParams> p(static_cast<size_t>(R));
+        for (int32_t r = 0; r < R; ++r) p[r] = to_params(&priors[r]);
+        const int RB = R <= 8 ? 8 : 16;
+        std::vector<int32_t> m(static_cast<size_t>(N) * RB, 0);
+        for (int32_t r = 0; r < R; ++r)
+            for (int32_t i = 0; i < N; ++i) {
+                const int32_t w = weights ? weights[static_cast<size_t>(r) * N + i] : 1;
+                if (w < 0) input_error("fit_batch: negative subject weight");
+                m[static_cast<size_t>(i) * RB + r] = w;
+            }
+        std::vector<const double*> init(static_cast<size_t>(R), nullptr);
+        if (init_beta)
+            for (int32_t r = 0; r < R; ++r) init[r] = init_beta + static_cast<size_t>(r) * J;
+        std::vector<int> err(static_cast<size_t>(R));
+        DeviceGuard g(ds->device);
+        Batch* b = batch_create(ds, RB);
+        try {
+            batch_set_weights(b, m.data(), nullptr);
+            batch_fit(b, R, p.data(), init.data(), cfg, beta_out, results, err.data(), nullptr);
+        } catch (...) {
+            batch_destroy(b);
+            throw;
+        }
+        batch_destroy(b);
+        for (int32_t r = 0; r < R; ++r) {
+            status[r] = BSCCS_OK;
+            if (err[r] == DERR_OVERFLOW || err[r] == DERR_STEP_NONFINITE || err[r] == DERR_FLAT_NO_PRIOR)
+                status[r] = BSCCS_NUMERIC_ERROR;
+            else if (err[r] != 0)
+                status[r] = BSCCS_INTERNAL_ERROR;
+        }
+    });
+}
+
 bsccs_status bsccs_run_bootstrap(const bsccs_dataset* ds, const bsccs_bootstrap_config* cfg, double* beta_full,
                                  double* lower, double* upper, double* p_hat, bsccs_bootstrap_result* result) {
     return guard([&] {

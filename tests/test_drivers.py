@@ -208,17 +208,18 @@ def _check_cv(res, exp):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("engine", ["subset"])
+@pytest.mark.parametrize("engine", ["subset", "batched"])
 def test_grid_search_cv_matches_reference(oracle_ds, golden, engine):
     res = CV.grid_search_cv(oracle_ds, _cv_cfg(golden, engine))
     _check_cv(res, golden["cv"]["expected"])
 
 
 @pytest.mark.gpu
-def test_grid_search_cv_live_reference_cold(oracle_ds, ref):
+@pytest.mark.parametrize("engine", ["subset", "batched"])
+def test_grid_search_cv_live_reference_cold(oracle_ds, ref, engine):
     """cold starts, normal prior, 3 folds -- against the live reference"""
     cfg = CV.CVConfig(folds=3, variance_grid=[0.5, 0.02, 0.1], prior_kind=B.PriorKind.normal, seed=5,
-                      warm_start=False)
+                      warm_start=False, engine=engine)
     res = CV.grid_search_cv(oracle_ds, cfg)
     exp = ref.dataset(oracle_ds).grid_search_cv(3, [0.5, 0.02, 0.1], B.PriorKind.normal, 5, B.SolverConfig(),
                                                 warm_start=False)
@@ -243,17 +244,18 @@ def _check_boot(res, exp):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("engine", ["subset"])
+@pytest.mark.parametrize("engine", ["subset", "batched"])
 def test_run_bootstrap_matches_reference(oracle_ds, golden, engine):
     res = BT.run_bootstrap(oracle_ds, _boot_cfg(golden, engine))
     _check_boot(res, golden["bootstrap"]["expected"])
 
 
 @pytest.mark.gpu
-def test_run_bootstrap_laplace_live_reference(oracle_ds, ref):
+@pytest.mark.parametrize("engine", ["subset", "batched"])
+def test_run_bootstrap_laplace_live_reference(oracle_ds, ref, engine):
     """laplace prior (zeros and p_hat < 1), cold starts, 6 replicates"""
     prior = B.laplace_prior(0.05)
-    cfg = BT.BootstrapConfig(replicates=6, level=0.8, seed=123, prior=prior, warm_start=False)
+    cfg = BT.BootstrapConfig(replicates=6, level=0.8, seed=123, prior=prior, warm_start=False, engine=engine)
     res = BT.run_bootstrap(oracle_ds, cfg)
     exp = ref.dataset(oracle_ds).run_bootstrap(6, 0.8, 123, prior, B.SolverConfig(), warm_start=False)
     _check_boot(res, exp)
@@ -272,3 +274,62 @@ def test_driver_input_errors(oracle_ds):
         BT.run_bootstrap(oracle_ds, BT.BootstrapConfig(replicates=0))
     with pytest.raises(B.InputError):
         BT.run_bootstrap(oracle_ds, BT.BootstrapConfig(level=1.0))
+
+
+@pytest.mark.gpu
+def test_fit_batch_matches_reference_fits(oracle_ds, ref):
+    """one batched launch, five fits of different selections / priors /
+    starts, each against the reference fit on the materialised selection"""
+    rds = ref.dataset(oracle_ds)
+    N = oracle_ds.num_subjects
+    res_idx = B.resample(oracle_ds, 77, 4)
+    held = np.sort(B.kfold_split(oracle_ds, 5, 9)[2])
+    rest = np.setdiff1d(np.arange(N), held).astype(np.int32)
+    w = np.ones((5, N), np.int32)
+    w[1] = np.bincount(res_idx, minlength=N)
+    w[2] = 0
+    w[2][rest] = 1
+    w[4] = np.bincount(res_idx, minlength=N)
+    priors = [B.normal_prior(0.1), B.normal_prior(0.1), B.laplace_prior(0.1), B.laplace_prior(1.0),
+              B.laplace_prior(0.05)]
+    start = rds.fit(B.normal_prior(0.1), B.SolverConfig())["beta"]
+    init = np.zeros((5, oracle_ds.num_drugs))
+    init[4] = start
+    fits, status = B.fit_batch(oracle_ds, priors, w, init)
+    sel = [None, res_idx, rest, None, res_idx]
+    for r in range(5):
+        assert status[r] is None
+        src = rds if sel[r] is None else rds.subset(sel[r])
+        t = src.fit(priors[r], B.SolverConfig(), init_beta=init[r] if r == 4 else None)
+        assert fits[r].cycles_run == t["cycles_run"], r
+        assert fits[r].converged == t["converged"]
+        assert close(fits[r].beta_map, t["beta"]), r
+        assert abs(fits[r].log_posterior - t["log_posterior"]) <= LL_REL * abs(t["log_posterior"]), r
+
+
+@pytest.mark.gpu
+def test_fit_batch_sixteen_and_errors(oracle_ds, ref):
+    """a full 16-fit block; a diverging fit (no prior, x'beta past 700) fails
+    alone with the reference's error class while the others finish"""
+    rds = ref.dataset(oracle_ds)
+    N = oracle_ds.num_subjects
+    w = np.stack([np.bincount(B.resample(oracle_ds, 5, r + 1), minlength=N) for r in range(16)]).astype(np.int32)
+    priors = [B.normal_prior(0.1)] * 16
+    fits, status = B.fit_batch(oracle_ds, priors, w)
+    for r in (0, 7, 15):
+        t = rds.subset(B.resample(oracle_ds, 5, r + 1)).fit(priors[r], B.SolverConfig())
+        assert fits[r].cycles_run == t["cycles_run"]
+        assert close(fits[r].beta_map, t["beta"])
+    # a start with |x'beta| > 700 fails alone (init_state's overflow guard,
+    # engine.hpp:56-74 -> numeric_error) while its batch mates finish
+    init = np.zeros((3, oracle_ds.num_drugs))
+    init[1, :] = 701.0
+    fits, status = B.fit_batch(oracle_ds, [B.normal_prior(0.1)] * 3, None, init)
+    with pytest.raises(Exception) as ei:
+        rds.fit(B.normal_prior(0.1), B.SolverConfig(), init_beta=init[1])
+    assert getattr(ei.value, "code", None) == 2  # BSCCS_NUMERIC_ERROR <- bsccs::numeric_error
+    assert status[1] is B.NumericError
+    assert status[0] is None and status[2] is None
+    t = rds.fit(B.normal_prior(0.1), B.SolverConfig())
+    for r in (0, 2):
+        assert fits[r].cycles_run == t["cycles_run"] and close(fits[r].beta_map, t["beta"])
