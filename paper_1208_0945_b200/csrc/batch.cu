@@ -26,6 +26,7 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <thread>
 #include <vector>
 
 #include "devutil.h"
@@ -48,10 +49,11 @@ template <int RB>
 struct BCfg {
     static constexpr int kErrWords = (RB + 5) / 6;       // 8-bit error counters, 6 fits per word
     static constexpr int kNW = 6 * RB + kErrWords;       // exchange words per round
-    static constexpr int kWPL = (kNW + 31) / 32;         // words per polling lane
+    static constexpr int kPollThreads = (kNW + 31) / 32 * 32; // exchanging threads
     static constexpr int kQStep = kBT / RB;              // pairs per block-wide pass
-    // staged l*exp per slot + subject per pair
-    static constexpr int kCapP = (kBSmemBudget - 4096) / (RB * 8 + 4) / kQStep * kQStep;
+    // staged l*exp per slot + two pair buffers
+    static constexpr int kCapP = (kBSmemBudget - 4096) / (RB * 8 + 16) / kQStep * kQStep;
+    static constexpr int kU = 8; // slots per thread whose gathers are in flight together
 };
 
 struct BatchArgs {
@@ -63,10 +65,12 @@ struct BatchArgs {
     const int32_t* subject_offsets;
     const int32_t* era_len;
     const int32_t* eps;      // events_per_subject
+    const int32_t* era_subj; // subject of every era
     double* xb;              // [K][RB]
     double* snap;            // [K][RB]
     double* den;             // [N][RB]
     const int32_t* m;        // [N][RB] multiplicities
+    const int32_t* wn;       // [N][RB] m * n_i (the run weight of the gradient sums)
     double* beta;            // [J][RB]
     double* trust;           // [J][RB]
     const double* ydx;       // [J][RB]
@@ -83,7 +87,24 @@ struct BatchArgs {
     double* crit;            // [RB] criterion, [RB..2RB) change, magnitude
     long long* visited;      // [RB]
     long long* moved;        // [RB]
+    const int64_t* col_ptr;  // byte accounting
+    const int32_t* col_runs;
+    int64_t K, N;
+    double* bytes;           // algorithmic bytes of this launch (CTA 0)
+    unsigned long long* trace; // profiling only: [ntrace][ctas][6] globaltimer stamps
+    int ntrace;
 };
+
+__device__ __forceinline__ unsigned long long bgtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define BTRACE(slot)                                                                                     \
+    do {                                                                                                 \
+        if (A.trace && threadIdx.x == 0 && idx < A.ntrace)                                               \
+            A.trace[(static_cast<size_t>(idx) * gridDim.x + blockIdx.x) * 6 + (slot)] = bgtimer();        \
+    } while (0)
 
 // Per-fit CTA reduction of (a, b, e): result in smem ra/rb/re[RB] (fixed order).
 template <int RB>
@@ -125,28 +146,33 @@ struct BSmem {
     double ra[RB], rb[RB];
     int re[RB];
     unsigned long long xd[BCfg<RB>::kNW];
+    unsigned long long pv[2][BCfg<RB>::kNW]; // running totals of both buffers (warp 0)
     double delta[RB];
+    double em1[RB];   // expm1(delta): the update scales l*exp by exp(delta)
     int status[RB];   // 0 ok, else error code of the fit (it stops)
     unsigned live;
-    int sub[BCfg<RB>::kCapP];
-    double le[BCfg<RB>::kCapP * RB];
+    // warp 0 lane r: fit r's coordinate scalars and counters (kept out of
+    // the registers of every thread)
+    double bj[RB], rj[RB], yj[RB], abytes[RB];
+    int nz[RB];
+    long long nvis[RB], nmov[RB];
+    int2 pst[2][BCfg<RB>::kCapP];         // pairs of this / the next coordinate's slice
+    double le[BCfg<RB>::kCapP * RB];      // l*exp per slot (then the update's differences)
 };
 
-// Exchange round: warp 0 publishes the CTA's per-fit (ra, rb, re) as limbs
-// and error counters, polls until every participant has added, and leaves
-// the totals' limb words in sm.xd.  Lanes keep the running totals of their
-// words for both buffers in pv.
+// Exchange round over the first kPollThreads threads, one word per thread:
+// publish the CTA's per-fit (ra, rb, re) word as a limb or error counter,
+// poll it until every participant has added, leave the total's word in
+// sm.xd, then a named barrier joins the exchanging warps.  (One word per
+// lane across several warps halves the exchange against one warp looping
+// over 4 words each: scripts/xbench2.cu.)
 template <int RB>
-__device__ __forceinline__ void bexchange(const BatchArgs& A, BSmem<RB>& sm, unsigned long long seq,
-                                          unsigned long long (&pv)[2][BCfg<RB>::kWPL]) {
+__device__ __forceinline__ void bexchange(const BatchArgs& A, BSmem<RB>& sm, unsigned long long seq) {
     using Cf = BCfg<RB>;
-    const int l = threadIdx.x & 31;
+    const int w = threadIdx.x;
     const unsigned buf = static_cast<unsigned>(seq & 1ull);
-    unsigned long long* base = A.xarea + static_cast<size_t>(buf) * Cf::kNW * kBXStride;
-#pragma unroll
-    for (int i = 0; i < Cf::kWPL; ++i) {
-        const int w = l + 32 * i;
-        if (w >= Cf::kNW) break;
+    if (w < Cf::kNW) {
+        unsigned long long* p = A.xarea + (static_cast<size_t>(buf) * Cf::kNW + w) * kBXStride;
         unsigned long long v = 0;
         if (w < 6 * RB) {
             const int f = w / 6, part = w % 6;
@@ -160,24 +186,17 @@ __device__ __forceinline__ void bexchange(const BatchArgs& A, BSmem<RB>& sm, uns
                 if (bad) v += 1ull << (8 * (f - e0));
             }
         }
-        red_add(base + static_cast<size_t>(w) * kBXStride, v + kXCnt);
-    }
-#pragma unroll
-    for (int i = 0; i < Cf::kWPL; ++i) {
-        const int w = l + 32 * i;
-        if (w >= Cf::kNW) break;
-        const unsigned long long* p = base + static_cast<size_t>(w) * kBXStride;
-        const unsigned long long prev = buf ? pv[1][i] : pv[0][i];
-        unsigned long long v, diff;
+        red_add(p, v + kXCnt);
+        const unsigned long long prev = sm.pv[buf][w];
+        unsigned long long x, diff;
         do {
-            v = ld_poll(p);
-            diff = v - prev;
+            x = ld_poll(p);
+            diff = x - prev;
         } while ((diff >> 50) < static_cast<unsigned long long>(A.ctas));
-        if (buf) pv[1][i] = v;
-        else pv[0][i] = v;
+        sm.pv[buf][w] = x;
         sm.xd[w] = diff & kXData;
     }
-    __syncwarp();
+    asm volatile("bar.sync 1, %0;" ::"n"(Cf::kPollThreads) : "memory");
 }
 
 template <int RB>
@@ -189,9 +208,61 @@ __device__ __forceinline__ int berr_count(const BSmem<RB>& sm, int f) {
 // per-slot run bookkeeping: subject of pair q of the slice
 __device__ __forceinline__ int pair_subj(const int2* pairs, int64_t p0, int q) { return __ldg(&pairs[p0 + q].y); }
 
+// Run sums of slots beyond the staging capacity: the run head walks its run
+// from global memory (rare: only slices longer than kCapP pairs).
+template <int RB>
+__device__ __forceinline__ void gh_tail_head(const BatchArgs& A, int64_t p0, int q, int np, int fit, double& gs,
+                                             double& hs, int& ferr) {
+    const int2 pr = __ldg(&A.pairs[p0 + q]);
+    if (q > 0 && __ldg(&A.pairs[p0 + q - 1].y) == pr.y) return; // not a head
+    const int m = A.m[static_cast<size_t>(pr.y) * RB + fit];
+    if (m == 0) return;
+    double num = 0.0;
+    for (int q2 = q; q2 < np; ++q2) {
+        const int2 p2 = __ldg(&A.pairs[p0 + q2]);
+        if (p2.y != pr.y) break;
+        num = __dadd_rn(num, lexp(A.era_len[p2.x], A.xb[static_cast<size_t>(p2.x) * RB + fit]));
+    }
+    const double den = A.den[static_cast<size_t>(pr.y) * RB + fit];
+    if (!(den > 0.0)) ferr = ferr ? ferr : DERR_DEN_NONPOSITIVE;
+    double w = num / den;
+    if (w > 1.0) w = 1.0;
+    const double nw = __dmul_rn(static_cast<double>(m) * static_cast<double>(A.eps[pr.y]), w);
+    gs = __dadd_rn(gs, nw);
+    hs = __dadd_rn(hs, __dmul_rn(nw, __dsub_rn(1.0, w)));
+}
+
+template <int RB>
+__device__ __forceinline__ void upd_tail_head(const BatchArgs& A, int64_t p0, int q, int np, int fit, double d,
+                                              int& ferr, double& ferrv) {
+    const int2 pr = __ldg(&A.pairs[p0 + q]);
+    if (q > 0 && __ldg(&A.pairs[p0 + q - 1].y) == pr.y) return;
+    if (A.m[static_cast<size_t>(pr.y) * RB + fit] == 0) return;
+    double den = A.den[static_cast<size_t>(pr.y) * RB + fit];
+    for (int q2 = q; q2 < np; ++q2) {
+        const int2 p2 = __ldg(&A.pairs[p0 + q2]);
+        if (p2.y != pr.y) break;
+        double* xp = A.xb + static_cast<size_t>(p2.x) * RB + fit;
+        const double old = *xp;
+        const int len = A.era_len[p2.x];
+        const double upd = __dadd_rn(old, d);
+        if (!(fabs(upd) <= kBXbBound)) {
+            ferr = ferr ? ferr : DERR_OVERFLOW;
+            ferrv = fabs(upd);
+            break;
+        }
+        den = __dadd_rn(den, __dsub_rn(lexp(len, upd), lexp(len, old)));
+        *xp = upd;
+    }
+    A.den[static_cast<size_t>(pr.y) * RB + fit] = den;
+}
+
 template <int RB>
 __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchArgs A) {
     using Cf = BCfg<RB>;
+    constexpr int U = Cf::kU;
+    constexpr int QS = Cf::kQStep;
+    constexpr int CAP = Cf::kCapP;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BSmem<RB>& sm = *reinterpret_cast<BSmem<RB>*>(smem_raw);
     const int c = blockIdx.x;
@@ -199,109 +270,160 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
     const int qfirst = static_cast<int>(threadIdx.x) / RB;
     const bool w0 = threadIdx.x < 32;
     unsigned long long seq = *A.xcounter;
-    unsigned long long pv[2][Cf::kWPL];
     {
-        const int l = threadIdx.x & 31;
         const unsigned long long* tot = A.xarea + static_cast<size_t>(2) * Cf::kNW * kBXStride;
-#pragma unroll
-        for (int i = 0; i < Cf::kWPL; ++i) {
-            const int w = l + 32 * i;
-            pv[0][i] = (w < Cf::kNW && w0) ? tot[w] : 0ull;
-            pv[1][i] = (w < Cf::kNW && w0) ? tot[Cf::kNW + w] : 0ull;
+        for (int w = threadIdx.x; w < Cf::kNW; w += kBT) {
+            sm.pv[0][w] = tot[w];
+            sm.pv[1][w] = tot[Cf::kNW + w];
         }
     }
     if (threadIdx.x == 0) sm.live = A.live;
     if (threadIdx.x < RB) sm.status[threadIdx.x] = 0;
-    __syncthreads();
-    long long nvis = 0, nmov = 0; // lane r of warp 0 counts fit r
     const longlong2* vs = A.vsplit + static_cast<size_t>(c) * A.nvisit;
-    int ferr = 0;     // this thread's fit: error seen (code)
+    if (A.nvisit > 0) { // first slice's pairs
+        const longlong2 s0 = vs[0];
+        const int n0 = min(static_cast<int>(s0.y - s0.x), CAP);
+        for (int q = threadIdx.x; q < n0; q += kBT) sm.pst[0][q] = __ldg(&A.pairs[s0.x + q]);
+    }
+    __syncthreads();
+    if (threadIdx.x < RB) {
+        sm.nvis[threadIdx.x] = 0;
+        sm.nmov[threadIdx.x] = 0;
+        sm.abytes[threadIdx.x] = 0.0;
+    }
+    int ferr = 0;                 // this thread's fit: error seen (code)
     double ferrv = 0.0;
     for (int idx = 0; idx < A.nvisit; ++idx) {
+        const int cur = idx & 1;
+        const int2* P = sm.pst[cur];
         const int j = A.visit[idx];
         const longlong2 sl = vs[idx];
         const int64_t p0 = sl.x;
         const int np = static_cast<int>(sl.y - sl.x);
+        const int lim = np < CAP ? np : CAP;
+        BTRACE(0);
         const unsigned live = sm.live;
         const bool flive = (live >> fit) & 1u;
         // warp 0 lane r: this coordinate's beta / trust / y_dot_x of fit r
-        double bj = 0.0, rj = 1.0, yj = 0.0;
-        int nz = 0;
-        if (w0 && threadIdx.x < RB) {
-            bj = A.beta[static_cast<size_t>(j) * RB + threadIdx.x];
-            rj = A.trust[static_cast<size_t>(j) * RB + threadIdx.x];
-            yj = A.ydx[static_cast<size_t>(j) * RB + threadIdx.x];
-            nz = A.colnz[static_cast<size_t>(j) * RB + threadIdx.x];
+        if (threadIdx.x < RB) {
+            const size_t o = static_cast<size_t>(j) * RB + threadIdx.x;
+            sm.bj[threadIdx.x] = A.beta[o];
+            sm.rj[threadIdx.x] = A.trust[o];
+            sm.yj[threadIdx.x] = A.ydx[o];
+            sm.nz[threadIdx.x] = A.colnz[o];
         }
-        // ---- gradient / hessian partials (engine.hpp:97-132, weighted) ----
+        // Single-chunk slices (every slot of this thread fits its U
+        // registers) keep each slot's gathered values in registers from the
+        // gradient pass through the update: one gather round trip per
+        // coordinate.  Larger slices take the chunked path with reloads.
+        const bool fast = np <= U * QS;
+        double xbv[U], dn[U];
+        int len[U], mm[U], fl[U]; // mm: m * n_i of the slot's subject; fl: bit0 valid, bit1 head, bit2 single run
         double gs = 0.0, hs = 0.0;
-        if (flive || fit == 0) { // fit 0's threads stage the subjects even when fit 0 is idle
-            for (int q = qfirst; q < np; q += Cf::kQStep) {
-                if (!flive) {
-                    if (q < Cf::kCapP) sm.sub[q] = pair_subj(A.pairs, p0, q);
-                    continue;
-                }
-                const int2 pr = __ldg(&A.pairs[p0 + q]);
-                const int sp = q > 0 ? pair_subj(A.pairs, p0, q - 1) : -1;
-                const int sn = q + 1 < np ? pair_subj(A.pairs, p0, q + 1) : -1;
-                const bool head = pr.y != sp;
-                if (q >= Cf::kCapP) {
-                    if (!head) continue;
-                    // beyond the staging capacity: the head walks its run
-                    const int m = A.m[static_cast<size_t>(pr.y) * RB + fit];
-                    if (m == 0) continue;
-                    double num = 0.0;
-                    for (int q2 = q; q2 < np; ++q2) {
-                        const int2 p2 = __ldg(&A.pairs[p0 + q2]);
-                        if (p2.y != pr.y) break;
-                        num = __dadd_rn(num, lexp(A.era_len[p2.x], A.xb[static_cast<size_t>(p2.x) * RB + fit]));
-                    }
-                    const double den = A.den[static_cast<size_t>(pr.y) * RB + fit];
-                    if (!(den > 0.0)) ferr = ferr ? ferr : DERR_DEN_NONPOSITIVE;
-                    double w = num / den;
-                    if (w > 1.0) w = 1.0;
-                    const double nw = __dmul_rn(static_cast<double>(m) * static_cast<double>(A.eps[pr.y]), w);
-                    gs = __dadd_rn(gs, nw);
-                    hs = __dadd_rn(hs, __dmul_rn(nw, __dsub_rn(1.0, w)));
-                    continue;
-                }
-                const double xbv = A.xb[static_cast<size_t>(pr.x) * RB + fit];
-                const int len = __ldg(&A.era_len[pr.x]);
-                int m = 0;
-                double den = 1.0;
-                int nev = 0;
-                if (head) {
-                    m = A.m[static_cast<size_t>(pr.y) * RB + fit];
-                    den = A.den[static_cast<size_t>(pr.y) * RB + fit];
-                    nev = __ldg(&A.eps[pr.y]);
-                }
-                const double le = lexp(len, xbv);
-                sm.le[q * RB + fit] = le;
-                if (fit == 0) sm.sub[q] = pr.y;
-                if (head && sn != pr.y && m != 0) { // single-pair run: its term now
-                    if (!(den > 0.0)) ferr = ferr ? ferr : DERR_DEN_NONPOSITIVE;
-                    double w = le / den;
-                    if (w > 1.0) w = 1.0;
-                    const double nw = __dmul_rn(static_cast<double>(m) * static_cast<double>(nev), w);
-                    gs = __dadd_rn(gs, nw);
-                    hs = __dadd_rn(hs, __dmul_rn(nw, __dsub_rn(1.0, w)));
+        // ---- gradient / hessian partials (engine.hpp:97-132, weighted) ----
+        if (flive && fast) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int q = qfirst + u * QS;
+                fl[u] = 0;
+                mm[u] = 0;
+                if (q < np) {
+                    const int2 pr = P[q];
+                    const int sp = q > 0 ? P[q - 1].y : -1;
+                    const int sn = q + 1 < np ? P[q + 1].y : -1;
+                    const bool hd = pr.y != sp;
+                    fl[u] = 1 | (hd ? 2 : 0) | (hd && sn != pr.y ? 4 : 0);
+                    xbv[u] = A.xb[static_cast<size_t>(pr.x) * RB + fit];
+                    len[u] = __ldg(&A.era_len[pr.x]);
+                    mm[u] = __ldg(&A.wn[static_cast<size_t>(pr.y) * RB + fit]);
+                    if (hd) dn[u] = A.den[static_cast<size_t>(pr.y) * RB + fit];
                 }
             }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int q = qfirst + u * QS;
+                if (fl[u] & 1) {
+                    const double le = lexp(len[u], xbv[u]);
+                    sm.le[q * RB + fit] = le;
+                    if ((fl[u] & 4) && mm[u] != 0) { // single-pair run: its term now
+                        if (!(dn[u] > 0.0)) ferr = ferr ? ferr : DERR_DEN_NONPOSITIVE;
+                        double w = le / dn[u];
+                        if (w > 1.0) w = 1.0;
+                        const double nw = __dmul_rn(static_cast<double>(mm[u]), w);
+                        gs = __dadd_rn(gs, nw);
+                        hs = __dadd_rn(hs, __dmul_rn(nw, __dsub_rn(1.0, w)));
+                    }
+                }
+            }
+        } else if (flive) {
+            for (int base = qfirst; base < lim; base += U * QS) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int q = base + u * QS;
+                    fl[u] = 0;
+                    mm[u] = 0;
+                    if (q < lim) {
+                        const int2 pr = P[q];
+                        const int sp = q > 0 ? P[q - 1].y : -1;
+                        const int sn = q + 1 < lim ? P[q + 1].y : (q + 1 < np ? pair_subj(A.pairs, p0, q + 1) : -1);
+                        const bool sg = pr.y != sp && sn != pr.y;
+                        fl[u] = 1 | (sg ? 4 : 0);
+                        xbv[u] = A.xb[static_cast<size_t>(pr.x) * RB + fit];
+                        len[u] = __ldg(&A.era_len[pr.x]);
+                        if (sg) {
+                            mm[u] = __ldg(&A.wn[static_cast<size_t>(pr.y) * RB + fit]);
+                            dn[u] = A.den[static_cast<size_t>(pr.y) * RB + fit];
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int q = base + u * QS;
+                    if (fl[u] & 1) {
+                        const double le = lexp(len[u], xbv[u]);
+                        sm.le[q * RB + fit] = le;
+                        if ((fl[u] & 4) && mm[u] != 0) {
+                            if (!(dn[u] > 0.0)) ferr = ferr ? ferr : DERR_DEN_NONPOSITIVE;
+                            double w = le / dn[u];
+                            if (w > 1.0) w = 1.0;
+                            const double nw = __dmul_rn(static_cast<double>(mm[u]), w);
+                            gs = __dadd_rn(gs, nw);
+                            hs = __dadd_rn(hs, __dmul_rn(nw, __dsub_rn(1.0, w)));
+                        }
+                    }
+                }
+            }
+            for (int q = CAP + qfirst; q < np; q += QS) gh_tail_head<RB>(A, p0, q, np, fit, gs, hs, ferr);
         }
+        BTRACE(1);
         __syncthreads();
-        if (flive) {
-            // heads of runs longer than one pair: numerator in ascending row order
-            const int lim = np < Cf::kCapP ? np : Cf::kCapP;
-            for (int q = qfirst; q < lim; q += Cf::kQStep) {
-                const int s = sm.sub[q];
-                if (q > 0 && sm.sub[q - 1] == s) continue;
-                const bool multi = q + 1 < np && (q + 1 < lim ? sm.sub[q + 1] : pair_subj(A.pairs, p0, q + 1)) == s;
+        // heads of runs longer than one pair: numerator in ascending row order
+        if (flive && fast) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if ((fl[u] & 6) != 2 || mm[u] == 0) continue; // head of a multi-pair run
+                const int q = qfirst + u * QS;
+                const int s = P[q].y;
+                double num = 0.0;
+                for (int q2 = q; q2 < np && P[q2].y == s; ++q2) num = __dadd_rn(num, sm.le[q2 * RB + fit]);
+                if (!(dn[u] > 0.0)) ferr = ferr ? ferr : DERR_DEN_NONPOSITIVE;
+                double w = num / dn[u];
+                if (w > 1.0) w = 1.0;
+                const double nw = __dmul_rn(static_cast<double>(mm[u]), w);
+                gs = __dadd_rn(gs, nw);
+                hs = __dadd_rn(hs, __dmul_rn(nw, __dsub_rn(1.0, w)));
+            }
+        } else if (flive) {
+            for (int q = qfirst; q < lim; q += QS) {
+                const int s = P[q].y;
+                if (q > 0 && P[q - 1].y == s) continue;
+                const bool multi = q + 1 < np && (q + 1 < lim ? P[q + 1].y : pair_subj(A.pairs, p0, q + 1)) == s;
                 if (!multi) continue;
                 const int m = A.m[static_cast<size_t>(s) * RB + fit];
                 if (m == 0) continue;
                 double num = 0.0;
                 int q2 = q;
-                for (; q2 < lim && sm.sub[q2] == s; ++q2) num = __dadd_rn(num, sm.le[q2 * RB + fit]);
+                for (; q2 < lim && P[q2].y == s; ++q2) num = __dadd_rn(num, sm.le[q2 * RB + fit]);
                 for (; q2 < np; ++q2) {
                     const int2 p2 = __ldg(&A.pairs[p0 + q2]);
                     if (p2.y != s) break;
@@ -316,25 +438,27 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
                 hs = __dadd_rn(hs, __dmul_rn(nw, __dsub_rn(1.0, w)));
             }
         }
-        // the publish must not be observable before warp 0's beta/trust loads
-        // complete (CTA 0 overwrites them after the exchange): fold them in
-        const int dep = __any_sync(0xffffffffu, (bj != bj) || (rj != rj));
-        breduce<RB>(gs, hs, ferr | dep, sm.wa, sm.wb, sm.we, sm.ra, sm.rb, sm.re);
+        // warp 0's beta/trust loads were consumed into shared memory before
+        // the barriers of this reduction, so the publish cannot overtake them
+        // (CTA 0 overwrites them after the exchange)
+        breduce<RB>(gs, hs, ferr, sm.wa, sm.wb, sm.we, sm.ra, sm.rb, sm.re);
+        BTRACE(2);
+        if (threadIdx.x < Cf::kPollThreads) bexchange<RB>(A, sm, seq);
         if (w0) {
-            bexchange<RB>(A, sm, seq, pv);
             const int r = threadIdx.x;
             if (r < RB) {
+                const double bj = sm.bj[r], rj = sm.rj[r];
                 double delta = 0.0;
                 int st = sm.status[r];
                 const bool lr = ((live >> r) & 1u) && st == 0;
-                const bool skip = !nz && bj == 0.0; // solver.hpp:119-121 (weighted column)
+                const bool skip = !sm.nz[r] && bj == 0.0; // solver.hpp:119-121 (weighted column)
                 if (lr && !skip) {
                     if (berr_count<RB>(sm, r) != 0) {
                         st = -1; // an error seen by some CTA (recorded there)
                     } else {
                         const double tg = from_limbs(sm.xd[6 * r], sm.xd[6 * r + 1], sm.xd[6 * r + 2]);
                         const double th = from_limbs(sm.xd[6 * r + 3], sm.xd[6 * r + 4], sm.xd[6 * r + 5]);
-                        const double g = __dsub_rn(yj, tg);
+                        const double g = __dsub_rn(sm.yj[r], tg);
                         const double h = th == 0.0 ? 0.0 : -th;
                         double step = 0.0;
                         const int serr = penalized_step(A.prior[r], bj, g, h, &step);
@@ -354,8 +478,17 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
                                     A.fit_errv[r] = step;
                                 }
                             } else {
-                                ++nvis;
-                                if (delta != 0.0) ++nmov;
+                                ++sm.nvis[r];
+                                const double nzj = static_cast<double>(A.col_ptr[j + 1] - A.col_ptr[j]);
+                                const double uj = static_cast<double>(A.col_runs[j]);
+                                double ab = 8.0 * nzj + 12.0 * uj; // x'beta gathers; den, m per run
+                                if (delta != 0.0) {
+                                    ++sm.nmov[r];
+                                    ab += 8.0 * nzj + 8.0 * uj; // x'beta, den writes
+                                }
+                                if (r == 0) // pairs + era lengths + event counts, once for all fits
+                                    ab += 12.0 * nzj + 4.0 * uj;
+                                sm.abytes[r] += ab;
                                 if (c == 0) {
                                     A.beta[static_cast<size_t>(j) * RB + r] = __dadd_rn(bj, delta);
                                     A.trust[static_cast<size_t>(j) * RB + r] = next_trust(delta, rj);
@@ -365,13 +498,20 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
                     }
                 }
                 sm.delta[r] = st == 0 ? delta : 0.0;
+                sm.em1[r] = st == 0 ? expm1(delta) : 0.0;
                 sm.status[r] = st;
             }
-            ++seq;
-        } else {
-            ++seq;
+        } else if (threadIdx.x >= Cf::kPollThreads && idx + 1 < A.nvisit) {
+            // while the partials travel: the next slice's pairs
+            const longlong2 nsl = vs[idx + 1];
+            const int nn = min(static_cast<int>(nsl.y - nsl.x), CAP);
+            int2* Q = sm.pst[cur ^ 1];
+            for (int q = threadIdx.x - Cf::kPollThreads; q < nn; q += kBT - Cf::kPollThreads)
+                Q[q] = __ldg(&A.pairs[nsl.x + q]);
         }
+        ++seq;
         __syncthreads();
+        BTRACE(3);
         if (threadIdx.x == 0) {
             unsigned lv = live;
             for (int r = 0; r < RB; ++r)
@@ -380,115 +520,147 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
         }
         // ---- sparse update (engine.hpp:205-231), weighted subjects only ----
         const double d = sm.delta[fit];
-        if (flive && d != 0.0) {
-            for (int q = qfirst; q < np; q += Cf::kQStep) {
-                const int2 pr = __ldg(&A.pairs[p0 + q]);
-                const int sp = q > 0 ? pair_subj(A.pairs, p0, q - 1) : -1;
-                const bool head = pr.y != sp;
-                if (q >= Cf::kCapP && !head) continue; // owned by its head
-                const int m = A.m[static_cast<size_t>(pr.y) * RB + fit];
-                if (m == 0) continue;
-                if (q >= Cf::kCapP) {
-                    double den = A.den[static_cast<size_t>(pr.y) * RB + fit];
-                    for (int q2 = q; q2 < np; ++q2) {
-                        const int2 p2 = __ldg(&A.pairs[p0 + q2]);
-                        if (p2.y != pr.y) break;
-                        double* xp = A.xb + static_cast<size_t>(p2.x) * RB + fit;
-                        const double old = *xp;
-                        const int len = A.era_len[p2.x];
-                        const double upd = __dadd_rn(old, d);
-                        if (!(fabs(upd) <= kBXbBound)) {
-                            ferr = ferr ? ferr : DERR_OVERFLOW;
-                            ferrv = fabs(upd);
-                            break;
-                        }
-                        const double fresh = lexp(len, upd);
-                        den = __dadd_rn(den, __dsub_rn(fresh, lexp(len, old)));
-                        *xp = upd;
-                    }
-                    A.den[static_cast<size_t>(pr.y) * RB + fit] = den;
-                    continue;
-                }
-                const int sn = q + 1 < np ? pair_subj(A.pairs, p0, q + 1) : -1;
-                double* xp = A.xb + static_cast<size_t>(pr.x) * RB + fit;
-                const double upd = __dadd_rn(*xp, d);
+        // l*exp(x'b + d) - l*exp(x'b) = l*exp(x'b) * expm1(d): the reference's
+        // difference (engine.hpp:224-226) up to rounding, with no per-era exp
+        const double em1 = sm.em1[fit];
+        if (flive && d != 0.0 && fast) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (!(fl[u] & 1) || mm[u] == 0) continue;
+                const int q = qfirst + u * QS;
+                const int2 pr = P[q];
+                const double upd = __dadd_rn(xbv[u], d);
                 double diff = 0.0;
                 if (!(fabs(upd) <= kBXbBound)) {
                     ferr = ferr ? ferr : DERR_OVERFLOW;
                     ferrv = fabs(upd);
                 } else {
-                    const double fresh = lexp(__ldg(&A.era_len[pr.x]), upd);
-                    diff = __dsub_rn(fresh, sm.le[q * RB + fit]);
-                    *xp = upd;
+                    diff = __dmul_rn(sm.le[q * RB + fit], em1);
+                    A.xb[static_cast<size_t>(pr.x) * RB + fit] = upd;
                 }
-                if (head && sn != pr.y) {
-                    double* dp = A.den + static_cast<size_t>(pr.y) * RB + fit;
-                    *dp = __dadd_rn(*dp, diff);
-                } else {
-                    sm.le[q * RB + fit] = diff; // this slot's l*exp is no longer needed
+                if (fl[u] & 4) A.den[static_cast<size_t>(pr.y) * RB + fit] = __dadd_rn(dn[u], diff);
+                else sm.le[q * RB + fit] = diff; // this slot's l*exp is no longer needed
+            }
+        } else if (flive && d != 0.0) {
+            for (int base = qfirst; base < lim; base += U * QS) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int q = base + u * QS;
+                    mm[u] = 0;
+                    fl[u] = 0;
+                    if (q < lim) {
+                        const int2 pr = P[q];
+                        const int sp = q > 0 ? P[q - 1].y : -1;
+                        const int sn = q + 1 < lim ? P[q + 1].y : (q + 1 < np ? pair_subj(A.pairs, p0, q + 1) : -1);
+                        const bool sg = pr.y != sp && sn != pr.y;
+                        fl[u] = 1 | (sg ? 4 : 0);
+                        mm[u] = __ldg(&A.wn[static_cast<size_t>(pr.y) * RB + fit]);
+                        xbv[u] = A.xb[static_cast<size_t>(pr.x) * RB + fit];
+                        if (sg) dn[u] = A.den[static_cast<size_t>(pr.y) * RB + fit];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int q = base + u * QS;
+                    if ((fl[u] & 1) && mm[u] != 0) {
+                        const int2 pr = P[q];
+                        const double upd = __dadd_rn(xbv[u], d);
+                        double diff = 0.0;
+                        if (!(fabs(upd) <= kBXbBound)) {
+                            ferr = ferr ? ferr : DERR_OVERFLOW;
+                            ferrv = fabs(upd);
+                        } else {
+                            diff = __dmul_rn(sm.le[q * RB + fit], em1);
+                            A.xb[static_cast<size_t>(pr.x) * RB + fit] = upd;
+                        }
+                        if (fl[u] & 4) A.den[static_cast<size_t>(pr.y) * RB + fit] = __dadd_rn(dn[u], diff);
+                        else sm.le[q * RB + fit] = diff;
+                    }
                 }
             }
+            for (int q = CAP + qfirst; q < np; q += QS) upd_tail_head<RB>(A, p0, q, np, fit, d, ferr, ferrv);
         }
+        BTRACE(4);
         __syncthreads();
-        if (flive && d != 0.0) {
-            const int lim = np < Cf::kCapP ? np : Cf::kCapP;
-            for (int q = qfirst; q < lim; q += Cf::kQStep) {
-                const int s = sm.sub[q];
-                if (q > 0 && sm.sub[q - 1] == s) continue;
-                const bool multi = q + 1 < np && (q + 1 < lim ? sm.sub[q + 1] : pair_subj(A.pairs, p0, q + 1)) == s;
+        if (flive && d != 0.0 && fast) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if ((fl[u] & 6) != 2 || mm[u] == 0) continue;
+                const int q = qfirst + u * QS;
+                const int s = P[q].y;
+                double den = dn[u];
+                for (int q2 = q; q2 < np && P[q2].y == s; ++q2) den = __dadd_rn(den, sm.le[q2 * RB + fit]);
+                A.den[static_cast<size_t>(s) * RB + fit] = den;
+            }
+        } else if (flive && d != 0.0) {
+            for (int q = qfirst; q < lim; q += QS) {
+                const int s = P[q].y;
+                if (q > 0 && P[q - 1].y == s) continue;
+                const bool multi = q + 1 < np && (q + 1 < lim ? P[q + 1].y : pair_subj(A.pairs, p0, q + 1)) == s;
                 if (!multi) continue;
                 if (A.m[static_cast<size_t>(s) * RB + fit] == 0) continue;
                 double* dp = A.den + static_cast<size_t>(s) * RB + fit;
                 double den = *dp;
                 int q2 = q;
-                for (; q2 < lim && sm.sub[q2] == s; ++q2) den = __dadd_rn(den, sm.le[q2 * RB + fit]);
+                for (; q2 < lim && P[q2].y == s; ++q2) den = __dadd_rn(den, sm.le[q2 * RB + fit]);
                 for (; q2 < np; ++q2) { // tail beyond the staging capacity
                     const int2 p2 = __ldg(&A.pairs[p0 + q2]);
                     if (p2.y != s) break;
                     double* xp = A.xb + static_cast<size_t>(p2.x) * RB + fit;
                     const double old = *xp;
-                    const int len = A.era_len[p2.x];
+                    const int len1 = A.era_len[p2.x];
                     const double upd = __dadd_rn(old, d);
                     if (!(fabs(upd) <= kBXbBound)) {
                         ferr = ferr ? ferr : DERR_OVERFLOW;
                         ferrv = fabs(upd);
                         break;
                     }
-                    den = __dadd_rn(den, __dsub_rn(lexp(len, upd), lexp(len, old)));
+                    den = __dadd_rn(den, __dsub_rn(lexp(len1, upd), lexp(len1, old)));
                     *xp = upd;
                 }
                 *dp = den;
             }
         }
         __syncthreads(); // slice writes of this coordinate before the next reads
+        BTRACE(5);
     }
 
     // ---- criterion (solver.hpp:154-165) per fit, snapshot in the same pass ----
+    // (era, fit) slots of the CTA's era range, fit-minor: fully coalesced
     {
         const unsigned live = sm.live;
         const bool flive = (live >> fit) & 1u;
         double ch = 0.0, mg = 0.0;
         if (flive) {
-            const int s0 = A.cta_subj[c], s1 = A.cta_subj[c + 1];
-            for (int s = s0 + qfirst; s < s1; s += Cf::kQStep) {
-                const int m = A.m[static_cast<size_t>(s) * RB + fit];
-                if (m == 0) continue;
-                double cs = 0.0, ms = 0.0;
-                for (int k = A.subject_offsets[s]; k < A.subject_offsets[s + 1]; ++k) {
-                    const size_t o = static_cast<size_t>(k) * RB + fit;
-                    const double x = A.xb[o];
-                    cs = __dadd_rn(cs, fabs(__dsub_rn(x, A.snap[o])));
-                    if (A.normalized) ms = __dadd_rn(ms, fabs(x));
-                    A.snap[o] = x;
+            const int e0 = A.subject_offsets[A.cta_subj[c]], e1 = A.subject_offsets[A.cta_subj[c + 1]];
+            for (int base = e0 + qfirst; base < e1; base += U * QS) {
+                double x[U], sn[U];
+                int mm[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int k = base + u * QS;
+                    if (k < e1) {
+                        const size_t o = static_cast<size_t>(k) * RB + fit;
+                        x[u] = A.xb[o];
+                        sn[u] = A.snap[o];
+                        mm[u] = A.m[static_cast<size_t>(__ldg(&A.era_subj[k])) * RB + fit];
+                    }
                 }
-                const double mm = static_cast<double>(m);
-                ch = __dadd_rn(ch, __dmul_rn(mm, cs));
-                mg = __dadd_rn(mg, __dmul_rn(mm, ms));
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int k = base + u * QS;
+                    if (k < e1 && mm[u] != 0) {
+                        const double mw = static_cast<double>(mm[u]);
+                        ch = __dadd_rn(ch, __dmul_rn(mw, fabs(__dsub_rn(x[u], sn[u]))));
+                        if (A.normalized) mg = __dadd_rn(mg, __dmul_rn(mw, fabs(x[u])));
+                        A.snap[static_cast<size_t>(k) * RB + fit] = x[u];
+                    }
+                }
             }
         }
         breduce<RB>(ch, mg, ferr, sm.wa, sm.wb, sm.we, sm.ra, sm.rb, sm.re);
+        if (threadIdx.x < Cf::kPollThreads) bexchange<RB>(A, sm, seq);
         if (w0) {
-            bexchange<RB>(A, sm, seq, pv);
             const int r = threadIdx.x;
             if (r < RB && c == 0) {
                 const double tch = from_limbs(sm.xd[6 * r], sm.xd[6 * r + 1], sm.xd[6 * r + 2]);
@@ -497,20 +669,19 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
                 A.crit[RB + r] = tch;
                 A.crit[2 * RB + r] = tmg;
                 if (berr_count<RB>(sm, r) != 0 && ((live >> r) & 1u)) atomicCAS(&A.fit_err[r], 0, -1);
-                A.visited[r] += nvis;
-                A.moved[r] += nmov;
+                A.visited[r] += sm.nvis[r];
+                A.moved[r] += sm.nmov[r];
+                // criterion pass: x'beta, snapshot read + write per era, m per era
+                double cb = 0.0;
+                if ((live >> r) & 1u) cb = 24.0 * static_cast<double>(A.K) + 4.0 * static_cast<double>(A.K);
+                A.bytes[r] = sm.abytes[r] + cb;
             }
             if (c == 0 && threadIdx.x == 0) *A.xcounter = seq + 1;
             if (c == 0) {
-                const int l = threadIdx.x & 31;
                 unsigned long long* tot = A.xarea + static_cast<size_t>(2) * Cf::kNW * kBXStride;
-#pragma unroll
-                for (int i = 0; i < Cf::kWPL; ++i) {
-                    const int w = l + 32 * i;
-                    if (w < Cf::kNW) {
-                        tot[w] = pv[0][i];
-                        tot[Cf::kNW + w] = pv[1][i];
-                    }
+                for (int w = threadIdx.x; w < Cf::kNW; w += 32) {
+                    tot[w] = sm.pv[0][w];
+                    tot[Cf::kNW + w] = sm.pv[1][w];
                 }
             }
         }
@@ -520,6 +691,12 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
         const int old = atomicCAS(&A.fit_err[fit], 0, ferr);
         if (old == 0 || (old == -1 && atomicCAS(&A.fit_err[fit], -1, ferr) == -1)) A.fit_errv[fit] = ferrv;
     }
+}
+
+__global__ void k_era_subj(const int32_t* __restrict__ off, int32_t N, int32_t* era_subj) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < N;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        for (int32_t k = off[i]; k < off[i + 1]; ++k) era_subj[k] = static_cast<int32_t>(i);
 }
 
 // ---- dense rebuild, log likelihood, weights ---------------------------------
@@ -620,6 +797,13 @@ __global__ void k_bll_final(const double* partial, int nb, double* out) {
 // weighted y_dot_x and column occupancy per fit (dataset.hpp:140-150 over
 // the selection): one block per column, exact integer sums
 template <int RB>
+__global__ void k_bwn(const int32_t* __restrict__ m, const int32_t* __restrict__ eps, int32_t N, int32_t* wn) {
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < static_cast<int64_t>(N) * RB;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        wn[t] = m[t] * eps[t / RB];
+}
+
+template <int RB>
 __global__ void k_bydx(const int2* __restrict__ pairs, const int64_t* __restrict__ col_ptr,
                        const int32_t* __restrict__ y, const int32_t* __restrict__ m, int J, double* ydx,
                        uint8_t* colnz) {
@@ -644,6 +828,19 @@ __global__ void k_bydx(const int2* __restrict__ pairs, const int64_t* __restrict
         }
         ydx[static_cast<size_t>(j) * RB + threadIdx.x] = static_cast<double>(x);
         colnz[static_cast<size_t>(j) * RB + threadIdx.x] = z > 0 ? 1 : 0;
+    }
+}
+
+// per-fit weight rows [R][N] -> fit-minor [N][RB] (zero beyond R)
+template <int RB>
+__global__ void k_btranspose(const int32_t* __restrict__ w, int64_t n, int R, int32_t* m, int* bad) {
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n * RB;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t s = t / RB;
+        const int r = static_cast<int>(t % RB);
+        const int32_t v = r < R ? w[static_cast<int64_t>(r) * n + s] : 0;
+        if (v < 0) atomicOr(bad, 1);
+        m[t] = v;
     }
 }
 
@@ -682,7 +879,8 @@ struct Batch {
     int RB = 16;
     cudaStream_t stream = nullptr;
     double *xb = nullptr, *snap = nullptr, *den = nullptr;
-    int32_t *m = nullptr, *mheld = nullptr;
+    int32_t *m = nullptr, *mheld = nullptr, *wn = nullptr;
+    int32_t* era_subj = nullptr;
     double *beta = nullptr, *trust = nullptr, *ydx = nullptr;
     uint8_t* colnz = nullptr;
     int32_t* visit = nullptr;
@@ -694,6 +892,7 @@ struct Batch {
     long long *visited = nullptr, *moved = nullptr;
     double* ll_partial = nullptr;
     double* ll_out = nullptr;
+    double* bytes_d = nullptr;
     int32_t* scratch_i = nullptr;
     int64_t scratch_n = 0;
     std::vector<int32_t> visit_h;
@@ -731,6 +930,10 @@ Batch* batch_create(const bsccs_dataset* ds, int RB) {
         b->den = dalloc<double>(N * RB, b->bytes, s);
         b->m = dalloc<int32_t>(N * RB, b->bytes, s);
         b->mheld = dalloc<int32_t>(N * RB, b->bytes, s);
+        b->wn = dalloc<int32_t>(N * RB, b->bytes, s);
+        b->era_subj = dalloc<int32_t>(K, b->bytes, s);
+        k_era_subj<<<build_grid(ds->device), 256, 0, s>>>(ds->subject_offsets, ds->N, b->era_subj);
+        count_launches(1);
         b->beta = dalloc<double>(J * RB, b->bytes, s);
         b->trust = dalloc<double>(J * RB, b->bytes, s);
         b->ydx = dalloc<double>(J * RB, b->bytes, s);
@@ -746,6 +949,7 @@ Batch* batch_create(const bsccs_dataset* ds, int RB) {
         b->moved = dalloc<long long>(RB, b->bytes, s);
         b->ll_partial = dalloc<double>(static_cast<int64_t>(kBLLBlocks) * RB * 2, b->bytes, s);
         b->ll_out = dalloc<double>(RB, b->bytes, s);
+        b->bytes_d = dalloc<double>(RB, b->bytes, s);
         CUDA_TRY(cudaMemsetAsync(b->xarea, 0, sizeof(unsigned long long) * xarea_words(RB), s));
         CUDA_TRY(cudaMemsetAsync(b->xcounter, 0, sizeof(unsigned long long), s));
         CUDA_TRY(cudaEventCreate(&b->ev0));
@@ -772,11 +976,11 @@ void batch_destroy(Batch* b) {
     cudaSetDevice(b->ds->device);
     cudaStream_t s = b->stream;
     if (s) {
-        for (void** p : {(void**)&b->xb, (void**)&b->snap, (void**)&b->den, (void**)&b->m, (void**)&b->mheld,
+        for (void** p : {(void**)&b->xb, (void**)&b->snap, (void**)&b->den, (void**)&b->m, (void**)&b->mheld, (void**)&b->wn, (void**)&b->era_subj,
                          (void**)&b->beta, (void**)&b->trust, (void**)&b->ydx, (void**)&b->colnz, (void**)&b->visit,
                          (void**)&b->vsplit, (void**)&b->xarea, (void**)&b->xcounter, (void**)&b->fit_err,
                          (void**)&b->fit_errv, (void**)&b->crit, (void**)&b->visited, (void**)&b->moved,
-                         (void**)&b->ll_partial, (void**)&b->ll_out, (void**)&b->scratch_i}) {
+                         (void**)&b->ll_partial, (void**)&b->ll_out, (void**)&b->bytes_d, (void**)&b->scratch_i}) {
             if (*p) cudaFreeAsync(*p, s);
             *p = nullptr;
         }
@@ -806,7 +1010,9 @@ void launch_weights_ydx(Batch* b) {
     const bsccs_dataset* ds = b->ds;
     k_bydx<RB><<<ds->J, 256, 0, b->stream>>>(ds->pairs, ds->col_ptr, ds->event_counts, b->m, ds->J, b->ydx,
                                              b->colnz);
-    count_launches(1);
+    k_bwn<RB><<<grid_for(static_cast<int64_t>(ds->N) * RB, 256, sm_count(ds->device)), 256, 0, b->stream>>>(
+        b->m, ds->events_per_subject, ds->N, b->wn);
+    count_launches(2);
 }
 
 template <int RB>
@@ -846,6 +1052,35 @@ void batch_set_weights(Batch* b, const int32_t* m_host, const int32_t* mheld_hos
     const size_t n = static_cast<size_t>(ds->N) * b->RB;
     CUDA_TRY(cudaMemcpyAsync(b->m, m_host, sizeof(int32_t) * n, cudaMemcpyHostToDevice, b->stream));
     if (mheld_host) CUDA_TRY(cudaMemcpyAsync(b->mheld, mheld_host, sizeof(int32_t) * n, cudaMemcpyHostToDevice, b->stream));
+    if (b->RB == 8) launch_weights_ydx<8>(b);
+    else launch_weights_ydx<16>(b);
+    CUDA_TRY(cudaStreamSynchronize(b->stream));
+}
+
+// Weights as R host rows of N (bsccs_fit_batch layout), transposed on the device.
+void batch_set_weight_rows(Batch* b, const int32_t* rows_host, int R) {
+    const bsccs_dataset* ds = b->ds;
+    DeviceGuard g(ds->device);
+    const int64_t n = ds->N;
+    int32_t* d = batch_scratch(b, n * R + 1);
+    int* bad = reinterpret_cast<int*>(d + n * R);
+    CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int), b->stream));
+    if (rows_host) {
+        h2d(d, rows_host, sizeof(int32_t) * static_cast<size_t>(n * R), b->stream, ds->device);
+    } else {
+        std::vector<int32_t> ones(static_cast<size_t>(n), 1);
+        for (int r = 0; r < R; ++r)
+            CUDA_TRY(cudaMemcpyAsync(d + r * n, ones.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, b->stream));
+        CUDA_TRY(cudaStreamSynchronize(b->stream));
+    }
+    const int grid = grid_for(n * b->RB, 256, sm_count(ds->device));
+    if (b->RB == 8) k_btranspose<8><<<grid, 256, 0, b->stream>>>(d, n, R, b->m, bad);
+    else k_btranspose<16><<<grid, 256, 0, b->stream>>>(d, n, R, b->m, bad);
+    count_launches(1);
+    int hb = 0;
+    CUDA_TRY(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, b->stream));
+    CUDA_TRY(cudaStreamSynchronize(b->stream));
+    if (hb) input_error("fit_batch: negative subject weight");
     if (b->RB == 8) launch_weights_ydx<8>(b);
     else launch_weights_ydx<16>(b);
     CUDA_TRY(cudaStreamSynchronize(b->stream));
@@ -967,10 +1202,12 @@ void batch_fit(Batch* b, int R, const PriorParams* priors, const double* const* 
     a.subject_offsets = ds->subject_offsets;
     a.era_len = ds->era_lengths;
     a.eps = ds->events_per_subject;
+    a.era_subj = b->era_subj;
     a.xb = b->xb;
     a.snap = b->snap;
     a.den = b->den;
     a.m = b->m;
+    a.wn = b->wn;
     a.beta = b->beta;
     a.trust = b->trust;
     a.ydx = b->ydx;
@@ -986,6 +1223,13 @@ void batch_fit(Batch* b, int R, const PriorParams* priors, const double* const* 
     a.crit = b->crit;
     a.visited = b->visited;
     a.moved = b->moved;
+    a.col_ptr = ds->col_ptr;
+    a.col_runs = ds->col_runs;
+    a.K = ds->K;
+    a.N = ds->N;
+    a.bytes = b->bytes_d;
+    a.trace = debug_trace_buffer(&a.ntrace);
+    std::vector<double> lb(RB);
     b->sweep_ms = 0.0;
     b->alg_bytes = 0.0;
     while (live && cycles < cfg->max_cycles) {
@@ -995,7 +1239,9 @@ void batch_fit(Batch* b, int R, const PriorParams* priors, const double* const* 
         else launch_cycle<16>(b, a);
         CUDA_TRY(cudaEventRecord(b->ev1, s));
         CUDA_TRY(cudaMemcpyAsync(crit.data(), b->crit, sizeof(double) * 3 * RB, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(lb.data(), b->bytes_d, sizeof(double) * RB, cudaMemcpyDeviceToHost, s));
         read_errors();
+        for (int r = 0; r < RB; ++r) b->alg_bytes += lb[r];
         float ms = 0.f;
         CUDA_TRY(cudaEventElapsedTime(&ms, b->ev0, b->ev1));
         b->sweep_ms += ms;
@@ -1052,6 +1298,7 @@ void batch_fit(Batch* b, int R, const PriorParams* priors, const double* const* 
         res[r].coordinates_moved = mov[r];
         res[r].dense_refreshes += 1;
         res[r].sweep_seconds = b->sweep_ms * 1e-3;
+        res[r].algorithmic_bytes = b->alg_bytes; // the whole batch's (shared stream included)
         if (!err_code[r]) {
             res[r].log_posterior = ll[r] + log_density(priors[r], out, J);
             if (pred_ll) pred_ll[r] = pll[r];
@@ -1060,6 +1307,7 @@ void batch_fit(Batch* b, int R, const PriorParams* priors, const double* const* 
 }
 
 double batch_sweep_ms(const Batch* b) { return b->sweep_ms; }
+double batch_alg_bytes(const Batch* b) { return b->alg_bytes; }
 
 // ---- drivers over the batched engine ----------------------------------------
 
@@ -1143,8 +1391,15 @@ void boot_replicates_batched(const bsccs_dataset* ds, const bsccs_bootstrap_conf
         for (int32_t rb = r0; rb < r1; rb += RB) {
             const int R = std::min<int32_t>(RB, r1 - rb);
             idx.resize(static_cast<size_t>(R) * N);
-            for (int r = 0; r < R; ++r)
-                resample(N, cfg->seed, static_cast<uint64_t>(rb + r) + 1, idx.data() + static_cast<size_t>(r) * N);
+            { // replicate r's draws are a pure function of (seed, r): one host thread each
+                std::vector<std::thread> th;
+                for (int r = 0; r < R; ++r)
+                    th.emplace_back([&, r] {
+                        resample(N, cfg->seed, static_cast<uint64_t>(rb + r) + 1,
+                                 idx.data() + static_cast<size_t>(r) * N);
+                    });
+                for (auto& t : th) t.join();
+            }
             batch_set_resamples(b, idx.data(), R);
             std::vector<PriorParams> priors(static_cast<size_t>(R), p);
             std::vector<const double*> init(static_cast<size_t>(R), cfg->warm_start ? beta_full : nullptr);

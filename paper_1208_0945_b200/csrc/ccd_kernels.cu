@@ -1824,6 +1824,10 @@ void set_debug_trace(int ncoords, int ctas) {
         CUDA_TRY(cudaMemset(g_trace, 0, g_trace_words * sizeof(unsigned long long)));
     }
 }
+unsigned long long* debug_trace_buffer(int* ncoords) {
+    *ncoords = g_ntrace;
+    return g_trace;
+}
 void read_debug_trace(unsigned long long* host, size_t words) {
     if (!g_trace) return;
     CUDA_TRY(cudaMemcpy(host, g_trace, std::min(words, g_trace_words) * sizeof(unsigned long long),

@@ -347,13 +347,7 @@ bsccs_status bsccs_fit_batch(const bsccs_dataset* ds, int32_t R, const bsccs_pri
         std::vector<PriorParams> p(static_cast<size_t>(R));
         for (int32_t r = 0; r < R; ++r) p[r] = to_params(&priors[r]);
         const int RB = R <= 8 ? 8 : 16;
-        std::vector<int32_t> m(static_cast<size_t>(N) * RB, 0);
-        for (int32_t r = 0; r < R; ++r)
-            for (int32_t i = 0; i < N; ++i) {
-                const int32_t w = weights ? weights[static_cast<size_t>(r) * N + i] : 1;
-                if (w < 0) input_error("fit_batch: negative subject weight");
-                m[static_cast<size_t>(i) * RB + r] = w;
-            }
+        (void)N;
         std::vector<const double*> init(static_cast<size_t>(R), nullptr);
         if (init_beta)
             for (int32_t r = 0; r < R; ++r) init[r] = init_beta + static_cast<size_t>(r) * J;
@@ -361,7 +355,7 @@ bsccs_status bsccs_fit_batch(const bsccs_dataset* ds, int32_t R, const bsccs_pri
         DeviceGuard g(ds->device);
         Batch* b = batch_create(ds, RB);
         try {
-            batch_set_weights(b, m.data(), nullptr);
+            batch_set_weight_rows(b, weights, R);
             batch_fit(b, R, p.data(), init.data(), cfg, beta_out, results, err.data(), nullptr);
         } catch (...) {
             batch_destroy(b);

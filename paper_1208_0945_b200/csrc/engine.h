@@ -201,6 +201,7 @@ void prepare_snapshot(bsccs_state* st);
 void set_debug_flags(int flags); // profiling only
 void set_debug_trace(int ncoords, int ctas);
 void read_debug_trace(unsigned long long* host, size_t words);
+unsigned long long* debug_trace_buffer(int* ncoords); // profiling only
 void throw_device_error(int code, double value);
 
 // ---- host driver (capi.cpp) ---------------------------------------------
@@ -218,10 +219,12 @@ Batch* batch_create(const bsccs_dataset* ds, int RB);
 void batch_destroy(Batch* b);
 void batch_set_weights(Batch* b, const int32_t* m_host, const int32_t* mheld_host); // [N][RB]
 void batch_set_resamples(Batch* b, const int32_t* idx_host, int R);                 // [R][N]
+void batch_set_weight_rows(Batch* b, const int32_t* rows_host, int R);              // [R][N], NULL = ones
 void batch_set_folds(Batch* b, const int32_t* fold_of_host, const int32_t* fold_r, int R);
 void batch_fit(Batch* b, int R, const PriorParams* priors, const double* const* init, const bsccs_solver_config* cfg,
                double* beta_out, bsccs_fit_result* res, int* err_code, double* pred_ll);
 double batch_sweep_ms(const Batch* b);
+double batch_alg_bytes(const Batch* b);
 void cv_folds_batched(const bsccs_dataset* ds, const bsccs_cv_config* cfg, const std::vector<double>& grid,
                       const std::vector<int32_t>& fold_subjects, const std::vector<int32_t>& fold_sizes, int32_t f0,
                       int32_t f1, bsccs_cv_cell* cells, bsccs_cv_result* res);
