@@ -80,6 +80,9 @@ __device__ __forceinline__ double from_limbs(unsigned long long L0, unsigned lon
 
 
 // l * exp(x'beta), the reference's l_exp_xbeta expression (engine.hpp:77-78,224-225)
-__device__ __forceinline__ double lexp(int len, double xb) { return __dmul_rn(static_cast<double>(len), exp(xb)); }
+#ifndef EXPFN
+#define EXPFN exp // profiling variants may substitute a cheaper function
+#endif
+__device__ __forceinline__ double lexp(int len, double xb) { return __dmul_rn(static_cast<double>(len), EXPFN(xb)); }
 
 } // namespace bsccs_b200
