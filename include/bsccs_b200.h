@@ -149,6 +149,25 @@ bsccs_status bsccs_dataset_destroy(bsccs_dataset* ds);
 /* sizes: N, K, J, nnz, ctas, device bytes resident */
 bsccs_status bsccs_dataset_info(const bsccs_dataset* ds, int64_t out[6]);
 
+/* read_long_format (io.hpp:88-174) + build_dataset (dataset.hpp:74-152):
+ * the era-level long format (subject_id TAB length_days TAB event_count
+ * [TAB space-separated drug labels]) parsed by `threads` host threads (<= 0:
+ * all) and laid out as CSC on the device.  Labels are numbered in
+ * first-appearance order, or by `dictionary` when dict_size > 0.  Errors
+ * (BSCCS_INPUT_ERROR) carry the reference's "path:line: ..." messages; with
+ * several errors in a file the earliest line's is reported. */
+bsccs_status bsccs_dataset_read_long_format(const char* path,
+                                           const char* const* dictionary,
+                                           int32_t dict_size, int32_t device,
+                                           int32_t num_ctas_override,
+                                           int32_t threads,
+                                           bsccs_dataset** out);
+/* Dataset::drug_ids (dataset.hpp:66): set (n == num_drugs, or 0 to clear)
+ * and read back newline-separated (needed = bytes including the NUL). */
+bsccs_status bsccs_dataset_set_drug_ids(bsccs_dataset* ds,
+                                        const char* const* labels, int32_t n);
+bsccs_status bsccs_dataset_drug_ids(const bsccs_dataset* ds, char* buf,
+                                    int64_t capacity, int64_t* needed);
 /* subset_dataset (dataset.hpp:157-217), built on the device from a resident
  * dataset: subjects in the given order, repeats allowed (each occurrence an
  * independent copy).  Bit-identical layout to the reference's subset.

@@ -202,6 +202,19 @@ class Reference:
                                         u64(cfg.seed), C.byref(h)))
         return RefDataset(self, h)
 
+    def read_long_format(self, path, dictionary=None):
+        """reference read_long_format + build_dataset -> (RefDataset, labels)"""
+        d = None
+        n = 0
+        if dictionary:
+            d = (C.c_char_p * len(dictionary))(*[x.encode() for x in dictionary])
+            n = len(dictionary)
+        h = VP()
+        buf = C.create_string_buffer(1 << 20)
+        self._chk(self.lib.ref_read_long_format(str(path).encode(), d, i32(n), C.byref(h), buf, i64(len(buf))))
+        txt = buf.value.decode()
+        return RefDataset(self, h), (txt.split("\n") if txt else [])
+
     def penalized_step(self, prior, beta_j, g, h):
         out = f64()
         p = _cprior(prior)

@@ -205,6 +205,30 @@ int ref_fit(void* dsp, const bsccs_prior* prior, const bsccs_solver_config* cfg,
     });
 }
 
+// read_long_format (io.hpp:88-174) + build_dataset (dataset.hpp:74-152);
+// labels: newline-joined into a caller buffer
+int ref_read_long_format(const char* path, const char* const* dict, int32_t dict_n, void** out, char* labels,
+                         int64_t cap) {
+    return guard([&] {
+        std::vector<std::string> d;
+        for (int32_t j = 0; j < dict_n; ++j) d.emplace_back(dict[j]);
+        auto data = bsccs::read_long_format(path, d);
+        auto* ds = new bsccs::Dataset(bsccs::build_dataset(
+            data.records, static_cast<bsccs::index_t>(data.drug_ids.size()), data.drug_ids));
+        std::string joined;
+        for (size_t j = 0; j < ds->drug_ids.size(); ++j) {
+            if (j) joined += '\n';
+            joined += ds->drug_ids[j];
+        }
+        if (labels && cap > 0) {
+            const size_t n = std::min<size_t>(joined.size(), static_cast<size_t>(cap - 1));
+            std::memcpy(labels, joined.data(), n);
+            labels[n] = '\0';
+        }
+        *out = ds;
+    });
+}
+
 // kfold_split (cross_validation.hpp:58-80): fold lists back to back
 int ref_kfold_split(void* dsp, int32_t folds, uint64_t seed, int32_t* out, int32_t* sizes) {
     return guard([&] {

@@ -76,6 +76,9 @@ _SIGS = [
     ("bsccs_dataset_destroy", C.c_int, [C.c_void_p]),
     ("bsccs_dataset_info", C.c_int, [C.c_void_p, P(i64)]),
     ("bsccs_dataset_subset", C.c_int, [C.c_void_p, C.c_void_p, i64, i32, P(C.c_void_p)]),
+    ("bsccs_dataset_read_long_format", C.c_int, [C.c_char_p, C.c_void_p, i32, i32, i32, i32, P(C.c_void_p)]),
+    ("bsccs_dataset_set_drug_ids", C.c_int, [C.c_void_p, C.c_void_p, i32]),
+    ("bsccs_dataset_drug_ids", C.c_int, [C.c_void_p, C.c_char_p, i64, P(i64)]),
     ("bsccs_dataset_export", C.c_int, [C.c_void_p] + [C.c_void_p] * 8),
     ("bsccs_kfold_split", C.c_int, [i32, i32, u64, C.c_void_p, C.c_void_p]),
     ("bsccs_resample", C.c_int, [i32, u64, u64, C.c_void_p]),

@@ -403,6 +403,29 @@ def resample(ds, seed: int, stream: int = 0) -> np.ndarray:
     return out
 
 
+def read_long_format(path: str, dictionary: Optional[Sequence[str]] = None, device: int = 0, ctas: int = 0,
+                     threads: int = 0) -> "DeviceDataset":
+    """io.hpp:88-174 + dataset.hpp:74-152: the era-level long format parsed
+    by native host threads and laid out as CSC on the device."""
+    h = C.c_void_p()
+    d = None
+    n = 0
+    if dictionary:
+        d = (C.c_char_p * len(dictionary))(*[x.encode() for x in dictionary])
+        n = len(dictionary)
+    _check(lib().bsccs_dataset_read_long_format(str(path).encode(), d, n, device, ctas, threads, C.byref(h)))
+    return DeviceDataset(None, device, ctas, handle=h)
+
+
+def write_long_format(path: str, records: Sequence[SubjectRecord], drug_ids: Sequence[str]) -> None:
+    """io.hpp:176-196: one era per line, subject, length, events, labels."""
+    with open(path, "w") as out:
+        for rec in records:
+            for era in rec.eras:
+                out.write(f"{rec.subject_id}\t{era.length_days}\t{era.event_count}\t"
+                          + " ".join(drug_ids[j] for j in era.exposures) + "\n")
+
+
 # ---------------------------------------------------------------- device
 
 
@@ -428,6 +451,9 @@ class DeviceDataset:
                                                     C.byref(h)))
         self.handle = h
         self._sizes = None
+        if ds.drug_ids:
+            labels = (C.c_char_p * len(ds.drug_ids))(*[x.encode() for x in ds.drug_ids])
+            _check(lib().bsccs_dataset_set_drug_ids(h, labels, len(ds.drug_ids)))
 
     def info(self):
         out = (C.c_int64 * 6)()
@@ -448,6 +474,16 @@ class DeviceDataset:
     num_drugs = property(lambda s: s._size("J"))
     nnz = property(lambda s: s._size("nnz"))
 
+    @property
+    def drug_ids(self) -> List[str]:
+        """Dataset::drug_ids (dataset.hpp:66) held with the device copy."""
+        need = C.c_int64()
+        _check(lib().bsccs_dataset_drug_ids(self.handle, None, 0, C.byref(need)))
+        buf = C.create_string_buffer(max(int(need.value), 1))
+        _check(lib().bsccs_dataset_drug_ids(self.handle, buf, len(buf), None))
+        txt = buf.value.decode()
+        return txt.split("\n") if txt else []
+
     def subset(self, subject_indices: Sequence[int], ctas: int = 0) -> "DeviceDataset":
         """subset_dataset (dataset.hpp:157-217) built on the device."""
         sel = np.ascontiguousarray(subject_indices, dtype=np.int32)
@@ -462,7 +498,7 @@ class DeviceDataset:
         arr = [np.empty(N + 1, np.int32), np.empty(N, np.int32), np.empty(K, np.int32), np.empty(K, np.int32),
                np.empty(J + 1, np.int64), np.empty(nnz, np.int32), np.empty(nnz, np.int32), np.empty(J, np.int64)]
         _check(lib().bsccs_dataset_export(self.handle, *[_ptr(a) for a in arr]))
-        return Dataset(*arr)
+        return Dataset(*arr, drug_ids=self.drug_ids)
 
     def close(self):
         if self.handle:

@@ -18,7 +18,7 @@ CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libbsccs_b200.so"
 
-SOURCES = ["ccd_kernels.cu", "subset.cu", "batch.cu", "capi.cpp", "drivers.cpp", "datagen.cpp"]
+SOURCES = ["ccd_kernels.cu", "subset.cu", "batch.cu", "capi.cpp", "drivers.cpp", "loader.cpp", "datagen.cpp"]
 HEADERS = ["engine.h", "devutil.h", "prior.h", "rng.h", "status.h", "xchg.cuh"]
 
 NVCC_FLAGS = [

@@ -372,6 +372,41 @@ bsccs_status bsccs_dataset_info(const bsccs_dataset* ds, int64_t out[6]) {
     });
 }
 
+bsccs_status bsccs_dataset_read_long_format(const char* path, const char* const* dictionary, int32_t dict_size,
+                                           int32_t device, int32_t num_ctas_override, int32_t threads,
+                                           bsccs_dataset** out) {
+    return guard([&] {
+        if (!out) input_error("null output handle");
+        *out = load_long_format(path, dictionary, dict_size, device, num_ctas_override, threads);
+    });
+}
+
+bsccs_status bsccs_dataset_set_drug_ids(bsccs_dataset* ds, const char* const* labels, int32_t n) {
+    return guard([&] {
+        if (!ds) input_error("null dataset");
+        if (n != 0 && n != ds->J) input_error("build_dataset: drug label count does not match drug count");
+        ds->drug_ids.clear();
+        for (int32_t j = 0; j < n; ++j) ds->drug_ids.emplace_back(labels[j] ? labels[j] : "");
+    });
+}
+
+bsccs_status bsccs_dataset_drug_ids(const bsccs_dataset* ds, char* buf, int64_t capacity, int64_t* needed) {
+    return guard([&] {
+        if (!ds) input_error("null dataset");
+        std::string joined;
+        for (size_t j = 0; j < ds->drug_ids.size(); ++j) {
+            if (j) joined += '\n';
+            joined += ds->drug_ids[j];
+        }
+        if (needed) *needed = static_cast<int64_t>(joined.size()) + 1;
+        if (buf && capacity > 0) {
+            const size_t n = std::min<size_t>(joined.size(), static_cast<size_t>(capacity - 1));
+            std::memcpy(buf, joined.data(), n);
+            buf[n] = '\0';
+        }
+    });
+}
+
 bsccs_status bsccs_dataset_subset(const bsccs_dataset* ds, const int32_t* subject_indices, int64_t n,
                                   int32_t num_ctas_override, bsccs_dataset** out) {
     return guard([&] {

@@ -101,6 +101,7 @@ struct bsccs_dataset {
     std::vector<int64_t> col_ptr_h;
     std::vector<uint8_t> col_nonempty_h;
     std::vector<int32_t> col_runs_h;
+    std::vector<std::string> drug_ids; // labels (Dataset::drug_ids), may be empty
     int64_t device_bytes = 0;
 };
 
@@ -162,6 +163,17 @@ void dataset_export(const bsccs_dataset* ds, int32_t* subject_offsets, int32_t* 
                     int32_t* era_lengths, int32_t* event_counts, int64_t* col_ptr, int32_t* rows, int32_t* subjects,
                     int64_t* y_dot_x);
 void kfold_split(int32_t N, int32_t folds, uint64_t seed, int32_t* subjects_out, int32_t* fold_sizes);
+// Dataset from host arrays whose pairs come in row order (drug ascending
+// within a row): (drug, row, subject) triples; the CSC is built on the
+// device by a stable sort on the drug (subset.cu).
+bsccs_dataset* dataset_from_row_pairs(int32_t N, int32_t K, int32_t J, int64_t nnz, const int32_t* subject_offsets,
+                                      const int32_t* events_per_subject, const int32_t* era_lengths,
+                                      const int32_t* event_counts, const uint32_t* drug, const int2* row_subj,
+                                      int device, int ctas_override);
+// read_long_format (io.hpp:88-174) + build_dataset (dataset.hpp:74-152) into a
+// resident dataset (loader.cpp)
+bsccs_dataset* load_long_format(const char* path, const char* const* dictionary, int32_t dict_size, int device,
+                                int ctas_override, int threads);
 void resample(int32_t N, uint64_t seed, uint64_t stream, int32_t* out);
 
 bsccs_state* state_create(const bsccs_dataset* ds, const double* beta_host);

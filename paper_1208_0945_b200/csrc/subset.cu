@@ -219,8 +219,61 @@ bsccs_dataset* dataset_subset(const bsccs_dataset* parent, const int32_t* subjec
         free_tmp();
         CUDA_TRY(cudaStreamSynchronize(ps));
         finish_dataset(ds, d_rows, d_subj, nullptr, nullptr);
+        ds->drug_ids = parent->drug_ids; // labels carried over unchanged (dataset.hpp:160-162)
     } catch (...) {
         if (ds) dataset_destroy(ds);
+        throw;
+    }
+    return ds;
+}
+
+bsccs_dataset* dataset_from_row_pairs(int32_t N, int32_t K, int32_t J, int64_t nnz, const int32_t* subject_offsets,
+                                      const int32_t* events_per_subject, const int32_t* era_lengths,
+                                      const int32_t* event_counts, const uint32_t* drug, const int2* row_subj,
+                                      int device, int ctas_override) {
+    DeviceGuard g(device);
+    const int sms = sm_count(device);
+    bsccs_dataset* ds = dataset_new(N, K, J, nnz, device, ctas_override);
+    try {
+        cudaStream_t s = ds->stream;
+        h2d(ds->subject_offsets, subject_offsets, sizeof(int32_t) * (static_cast<size_t>(N) + 1), s, device);
+        h2d(ds->events_per_subject, events_per_subject, sizeof(int32_t) * N, s, device);
+        h2d(ds->era_lengths, era_lengths, sizeof(int32_t) * K, s, device);
+        h2d(ds->event_counts, event_counts, sizeof(int32_t) * K, s, device);
+        int64_t sb = 0;
+        uint32_t* keys[2] = {dalloc<uint32_t>(nnz, sb, s), dalloc<uint32_t>(nnz, sb, s)};
+        int2* vals[2] = {dalloc<int2>(nnz, sb, s), dalloc<int2>(nnz, sb, s)};
+        int sel = 0;
+        if (nnz > 0) {
+            h2d(keys[0], drug, sizeof(uint32_t) * static_cast<size_t>(nnz), s, device);
+            h2d(vals[0], row_subj, sizeof(int2) * static_cast<size_t>(nnz), s, device);
+            int end_bit = 1;
+            while ((1ll << end_bit) < static_cast<long long>(J)) ++end_bit;
+            cub::DoubleBuffer<uint32_t> dk(keys[0], keys[1]);
+            cub::DoubleBuffer<int2> dv(vals[0], vals[1]);
+            size_t tb = 0;
+            CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, nnz, 0, end_bit, s));
+            unsigned char* tmp = dalloc<unsigned char>(static_cast<int64_t>(std::max<size_t>(tb, 16)), sb, s);
+            CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, nnz, 0, end_bit, s));
+            dfree(tmp, s);
+            sel = dk.selector;
+        }
+        k_sub_colptr<<<(J + 1 + 255) / 256, 256, 0, s>>>(keys[sel], nnz, J, ds->col_ptr);
+        int32_t* d_rows = dalloc<int32_t>(nnz, sb, s);
+        int32_t* d_subj = dalloc<int32_t>(nnz, sb, s);
+        k_sub_split<<<grid_for(nnz, 256, sms), 256, 0, s>>>(vals[sel], nnz, d_rows, d_subj);
+        count_launches(2);
+        ds->col_ptr_h.resize(static_cast<size_t>(J) + 1);
+        CUDA_TRY(cudaMemcpyAsync(ds->col_ptr_h.data(), ds->col_ptr, sizeof(int64_t) * (J + 1), cudaMemcpyDeviceToHost,
+                                 s));
+        for (int b = 0; b < 2; ++b) {
+            dfree(keys[b], s);
+            dfree(vals[b], s);
+        }
+        CUDA_TRY(cudaStreamSynchronize(s));
+        finish_dataset(ds, d_rows, d_subj, nullptr, nullptr);
+    } catch (...) {
+        dataset_destroy(ds);
         throw;
     }
     return ds;
