@@ -49,7 +49,7 @@ void validate_config(const bsccs_solver_config* c) {
     if (c->partitions < 1) input_error("solver: partitions must be at least 1");
     if (c->dense_refresh_interval < 1) input_error("solver: dense refresh interval must be at least 1");
     if (c->precision != 1) input_error("solver: the B200 path computes in double precision only");
-    if (c->path != 0) input_error("solver: the B200 path implements the sparse update path only");
+    if (c->path != 0 && c->path != 1) input_error("solver: unknown update path");
 }
 
 // prior.hpp:36-61
@@ -118,7 +118,7 @@ void fit_loop(FitContext& fc, const PriorParams& prior, const bsccs_solver_confi
             }
             set_order(fc, order);
         }
-        const SweepOutcome o = run_sweep(fc.plan, prior, cfg->convergence != 0);
+        const SweepOutcome o = run_sweep(fc.plan, prior, cfg->convergence != 0, cfg->path == 1);
         res->final_criterion = o.criterion;
         res->coordinates_visited += o.visited;
         res->coordinates_moved += o.moved;
@@ -528,7 +528,7 @@ bsccs_status bsccs_run_cycle(bsccs_state* st, const bsccs_prior* prior, const bs
         plan.counter = st->counter;
         plan.total_participants = st->ds->ctas;
         plan.participant_base = 0;
-        const SweepOutcome o = run_sweep(plan, p, cfg->convergence != 0);
+        const SweepOutcome o = run_sweep(plan, p, cfg->convergence != 0, cfg->path == 1);
         CUDA_TRY(cudaMemcpy(trust, st->trust, sizeof(double) * J, cudaMemcpyDeviceToHost));
         *criterion = o.criterion;
     });

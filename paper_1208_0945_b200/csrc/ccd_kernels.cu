@@ -81,6 +81,9 @@ struct ShardArgs {
     const int32_t* col_runs;
     const int64_t* split;
     const int32_t* cta_era;
+    const int32_t* cta_subj;  // [ctas+1] first subject of each CTA (dense path)
+    const int32_t* subject_offsets;
+    double* num;              // [N] run numerators of the dense path (zero between uses)
     EraRec* era;
     SubjRec* subj;
     double* beta;
@@ -965,6 +968,208 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
     if (c == 0 && S.xowner) xprev_store(S.xslots, pv);
 }
 
+// ---- the dense update path (UpdatePath::dense) ---------------------------------
+//
+// The reference's benchmark route (engine.hpp:368-401, solver.hpp:124-146):
+// per coordinate, the column's run numerators are scattered into a
+// per-subject array, a full sweep over every subject forms (g, h), and an
+// accepted step is applied to the column's rows followed by a full rebuild
+// of every denominator from x'beta (refresh_from_xbeta, engine.hpp:68-90).
+// Subjects and their eras are CTA-owned, so each CTA does all of that for
+// its own subject range; only the (g, h) sum crosses CTAs (the exact
+// exchange of §4.2).  Results equal the sparse path up to addition order.
+constexpr int kDT = 256;
+struct DSmem {
+    double ra[kDT / 32], rb[kDT / 32];
+    int re[kDT / 32];
+    double delta;
+    int status;
+};
+
+__device__ __forceinline__ void dblock_reduce(double& a, double& b, int& e, DSmem& sm) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a = __dadd_rn(a, __shfl_xor_sync(0xffffffffu, a, o));
+        b = __dadd_rn(b, __shfl_xor_sync(0xffffffffu, b, o));
+    }
+    e = __reduce_or_sync(0xffffffffu, e);
+    if (lane_id() == 0) {
+        sm.ra[warp_id()] = a;
+        sm.rb[warp_id()] = b;
+        sm.re[warp_id()] = e;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double x = 0.0, y = 0.0;
+        int z = 0;
+        for (int i = 0; i < kDT / 32; ++i) {
+            x = __dadd_rn(x, sm.ra[i]);
+            y = __dadd_rn(y, sm.rb[i]);
+            z |= sm.re[i];
+        }
+        a = x;
+        b = y;
+        e = z;
+    }
+}
+
+__global__ void __launch_bounds__(kDT) k_ccd_dense(const __grid_constant__ SweepArgs A) {
+    __shared__ DSmem sm;
+    const ShardArgs& S = A.sh[0];
+    const int c = static_cast<int>(blockIdx.x);
+    const bool w0 = threadIdx.x < 32;
+    unsigned long long seq = *S.xcounter;
+    XPrev pv{0ull, 0ull};
+    xprev_load(S.xslots, pv);
+    int err = 0;
+    double errv = 0.0;
+    long long nvisit = 0, nmoved = 0;
+    const int V = A.nvisit;
+    const longlong2* vs = S.vsplit + static_cast<size_t>(c) * static_cast<size_t>(V);
+    const int s0 = S.cta_subj[c], s1 = S.cta_subj[c + 1];
+    bool aborted = false;
+    for (int idx = 0; idx < V; ++idx) {
+        const int j = A.visit[idx];
+        const longlong2 sl = vs[idx];
+        double bj = 0.0, rj = 1.0;
+        if (w0) {
+            bj = S.beta[j];
+            rj = S.trust[j];
+        }
+        // run numerators of the column into num[subject] (engine.hpp:376-380)
+        for (int64_t p = sl.x + threadIdx.x; p < sl.y; p += kDT) {
+            const int2 pr = ld_pair(S.pairs + p);
+            if (p > sl.x && ld_pair(S.pairs + p - 1).y == pr.y) continue;
+            double numv = 0.0;
+            for (int64_t q = p; q < sl.y; ++q) {
+                const int2 p2 = ld_pair(S.pairs + q);
+                if (p2.y != pr.y) break;
+                const Rec r = ld_rec(S.era + p2.x);
+                numv = __dadd_rn(numv, lexp(r.len, r.xb));
+            }
+            S.num[pr.y] = numv;
+        }
+        __syncthreads();
+        // full sweep over the CTA's subjects (engine.hpp:381-395)
+        double gs = 0.0, hs = 0.0;
+        for (int s = s0 + static_cast<int>(threadIdx.x); s < s1; s += kDT) {
+            const Subj sr = ld_subj(S.subj + s);
+            if (!(sr.den > 0.0)) err = DERR_DEN_NONPOSITIVE;
+            double w = S.num[s] / sr.den;
+            if (w > 1.0) w = 1.0;
+            const double nw = __dmul_rn(static_cast<double>(sr.n), w);
+            gs = __dadd_rn(gs, nw);
+            hs = __dadd_rn(hs, __dmul_rn(nw, __dsub_rn(1.0, w)));
+        }
+        int e = err | ((bj != bj) || (rj != rj) ? 1 : 0);
+        dblock_reduce(gs, hs, e, sm);
+        publish(A, seq, gs, hs, e);
+        if (w0) {
+            double tg, th;
+            int te = 0;
+            poll(A, S.xslots, seq, pv, tg, th, te, nullptr);
+            int status = ST_OK;
+            double delta = 0.0;
+            if (te) {
+                status = ST_REMOTE_ERR;
+            } else {
+                const double g = __dsub_rn(A.y_dot_x[j], tg);
+                const double h = th == 0.0 ? 0.0 : -th;
+                double step = 0.0;
+                const int serr = penalized_step(A.prior, bj, g, h, &step);
+                if (serr) {
+                    status = ST_STEP_ERR;
+                    if (c == 0 && threadIdx.x == 0) record_error(S.err, serr, h);
+                } else {
+                    delta = clamp_step(step, rj);
+                    if (delta != 0.0 && !isfinite(delta)) {
+                        status = ST_NONFINITE;
+                        if (c == 0 && threadIdx.x == 0) record_error(S.err, DERR_STEP_NONFINITE, delta);
+                    }
+                }
+            }
+            if (threadIdx.x == 0) {
+                sm.delta = delta;
+                sm.status = status;
+                if (c == 0 && status == ST_OK) {
+                    S.moved[idx] = delta != 0.0 ? 1 : 0;
+                    S.beta[j] = __dadd_rn(bj, delta);
+                    S.trust[j] = next_trust(delta, rj);
+                }
+            }
+        }
+        ++seq;
+        __syncthreads();
+        const int status = sm.status;
+        const double delta = sm.delta;
+        // the numerators are consumed: back to zero for the next column
+        for (int64_t p = sl.x + threadIdx.x; p < sl.y; p += kDT) S.num[ld_pair(S.pairs + p).y] = 0.0;
+        if (status != ST_OK) {
+            aborted = true;
+            if (status == ST_REMOTE_ERR && c == 0 && threadIdx.x == 0) S.res->err_remote = 1;
+            break;
+        }
+        ++nvisit;
+        if (delta != 0.0) {
+            ++nmoved;
+            // x'beta of the column's rows (solver.hpp:138-143) ...
+            for (int64_t p = sl.x + threadIdx.x; p < sl.y; p += kDT) {
+                const int row = ld_pair(S.pairs + p).x;
+                S.era[row].xb = __dadd_rn(S.era[row].xb, delta);
+            }
+            __syncthreads();
+            // ... then every denominator rebuilt from x'beta (engine.hpp:68-90)
+            for (int s = s0 + static_cast<int>(threadIdx.x); s < s1; s += kDT) {
+                double total = 0.0;
+                for (int k = S.subject_offsets[s]; k < S.subject_offsets[s + 1]; ++k) {
+                    const Rec r = ld_rec(S.era + k);
+                    if (!(fabs(r.xb) <= kXbBound)) {
+                        err = DERR_OVERFLOW;
+                        errv = fabs(r.xb);
+                    }
+                    total = __dadd_rn(total, lexp(r.len, r.xb));
+                }
+                S.subj[s].den = total;
+            }
+        }
+        __syncthreads();
+    }
+    if (!aborted) {
+        // criterion (solver.hpp:154-165), snapshot for the next cycle
+        const int e0 = S.cta_era[c], e1 = S.cta_era[c + 1];
+        double ch = 0.0, mg = 0.0;
+        for (int k = e0 + static_cast<int>(threadIdx.x); k < e1; k += kDT) {
+            const double xb = S.era[k].xb;
+            ch = __dadd_rn(ch, fabs(__dsub_rn(xb, S.snap[k])));
+            if (A.normalized) mg = __dadd_rn(mg, fabs(xb));
+            S.snap[k] = xb;
+        }
+        int e = err;
+        dblock_reduce(ch, mg, e, sm);
+        publish(A, seq, ch, mg, e);
+        if (w0) {
+            double tch, tmg;
+            int te;
+            poll(A, S.xslots, seq, pv, tch, tmg, te, nullptr);
+            if (c == 0 && threadIdx.x == 0) {
+                S.res->change = tch;
+                S.res->magnitude = tmg;
+                S.res->criterion = A.normalized ? tch / (1.0 + tmg) : tch;
+                S.res->err_remote = te;
+            }
+        }
+        ++seq;
+    }
+    if (err) record_error(S.err, err, errv);
+    if (c == 0 && threadIdx.x == 0) {
+        S.res->visited = nvisit;
+        S.res->moved = nmoved;
+        S.res->counter = seq;
+        if (S.xowner) *S.xcounter = seq;
+    }
+    if (c == 0 && S.xowner) xprev_store(S.xslots, pv);
+}
+
 // ---- dense kernels ---------------------------------------------------------
 
 __global__ void k_init_records(EraRec* era, SubjRec* subj, const int32_t* len, const int32_t* y, const int32_t* n,
@@ -1612,6 +1817,7 @@ void state_destroy(bsccs_state* st) {
         dfree(st->era, s);
         dfree(st->snap, s);
         dfree(st->le_tmp, s);
+        dfree(st->num, s);
         dfree(st->subj, s);
         dfree(st->beta, s);
         dfree(st->trust, s);
@@ -1669,6 +1875,9 @@ SweepArgs base_args(const ExchangePlan& plan) {
         s.K = st->ds->K;
         s.split = st->ds->split;
         s.cta_era = st->ds->cta_era;
+        s.cta_subj = st->ds->cta_subj;
+        s.subject_offsets = st->ds->subject_offsets;
+        s.num = st->num;
         s.era = st->era;
         s.subj = st->subj;
         s.beta = st->beta;
@@ -1862,8 +2071,15 @@ void build_vsplit(const bsccs_dataset* ds, const int32_t* d_visit, int V, longlo
     count_launches(1);
 }
 
-SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool normalized) {
+SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool normalized, bool dense) {
     bsccs_state* s0 = plan.shards[0];
+    if (dense && (plan.shards.size() != 1 || plan.dst.size() != 1))
+        input_error("solver: the dense update path runs on an unsharded dataset");
+    if (dense && !s0->num) {
+        int64_t b = 0;
+        s0->num = dalloc<double>(s0->ds->N, b, s0->stream);
+        CUDA_TRY(cudaMemsetAsync(s0->num, 0, sizeof(double) * s0->ds->N, s0->stream));
+    }
     DeviceGuard dg(s0->ds->device);
     // visit list of this cycle: order filtered by the skip rule
     // (solver.hpp:119-121: empty column and beta_j == 0)
@@ -1910,7 +2126,14 @@ SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool 
     a.prior = prior;
     a.normalized = normalized ? 1 : 0;
     CUDA_TRY(cudaEventRecord(s0->ev0, s0->stream));
-    launch_ccd(plan, a);
+    if (dense) {
+        void* params[] = {&a};
+        CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_ccd_dense), dim3(s0->ds->ctas), dim3(kDT),
+                                             params, 0, s0->stream));
+        count_launches(1);
+    } else {
+        launch_ccd(plan, a);
+    }
     CUDA_TRY(cudaEventRecord(s0->ev1, s0->stream));
     SweepOutcome out{0.0, 0, 0};
     for (size_t i = 0; i < plan.shards.size(); ++i) {
@@ -1943,7 +2166,12 @@ SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool 
             const double nnz = static_cast<double>(d->col_ptr_h[j + 1] - d->col_ptr_h[j]);
             const double runs = static_cast<double>(d->col_runs_h[j]);
             bytes += 16.0 * nnz + 12.0 * runs;
-            if (moved[static_cast<size_t>(i)]) bytes += 28.0 * nnz + 8.0 * runs;
+            if (dense) { // the subject sweep; on a step the full rebuild (engine.hpp:68-90)
+                bytes += 24.0 * static_cast<double>(d->N);
+                if (moved[static_cast<size_t>(i)]) bytes += 16.0 * nnz + 16.0 * d->K + 8.0 * d->N;
+            } else if (moved[static_cast<size_t>(i)]) {
+                bytes += 28.0 * nnz + 8.0 * runs;
+            }
         }
         s0->alg_bytes += bytes;
     }

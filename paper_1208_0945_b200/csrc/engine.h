@@ -113,6 +113,7 @@ struct bsccs_state {
     bsccs_b200::EraRec* era = nullptr;
     double* snap = nullptr;              // [K] criterion snapshot
     double* le_tmp = nullptr;            // [K] scratch for state_get
+    double* num = nullptr;               // [N] run numerators of the dense path (lazy)
     bsccs_b200::SubjRec* subj = nullptr;
     double* beta = nullptr;
     double* trust = nullptr;
@@ -207,7 +208,7 @@ struct ExchangePlan {
     int participant_base;                  // first participant of shard 0
 };
 
-SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool normalized);
+SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool normalized, bool dense = false);
 void plan_allreduce(const ExchangePlan& plan, double a, double b, double* ta, double* tb);
 void prepare_snapshot(bsccs_state* st);
 void set_debug_flags(int flags); // profiling only
