@@ -76,9 +76,18 @@ inline void parallel_memcpy(void* dst, const void* src, size_t n) {
     for (auto& x : th) x.join();
 }
 
+inline bool is_pinned(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError(); // clear: unregistered pageable memory
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
 inline void h2d(void* dst, const void* src, size_t bytes, cudaStream_t s, int device) {
     if (bytes == 0) return;
-    if (bytes < (size_t(4) << 20)) { // small: a plain async copy
+    if (bytes < (size_t(4) << 20) || is_pinned(src)) { // small, or already page-locked: DMA directly
         CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
         return;
     }
