@@ -36,6 +36,11 @@
 #include <bsccs/solver.hpp> // reference types: Dataset, PriorSpec, SolverConfig, FitResult, exceptions
 #define BSCCS_B200_HAVE_REFERENCE 1
 #endif
+#if __has_include(<bsccs/cross_validation.hpp>) && __has_include(<bsccs/bootstrap.hpp>)
+#include <bsccs/bootstrap.hpp>        // BootstrapConfig / BootstrapResult
+#include <bsccs/cross_validation.hpp> // CVConfig / CVCell / CVResult
+#define BSCCS_B200_HAVE_REFERENCE_DRIVERS 1
+#endif
 
 namespace bsccs_b200 {
 
@@ -92,6 +97,8 @@ public:
         handle_.reset(h);
         num_drugs_ = static_cast<int32_t>(J);
     }
+    // adopt a handle built by the library (read_long_format, subset)
+    DeviceDataset(bsccs_dataset* h, int32_t num_drugs) : handle_(h), num_drugs_(num_drugs) {}
     bsccs_dataset* get() const { return handle_.get(); }
     int32_t num_drugs() const { return num_drugs_; }
 
@@ -151,7 +158,126 @@ FitResult fit(const DeviceDataset& dds, const PriorSpec& prior, const SolverConf
     return out;
 }
 
+// read_long_format (io.hpp:88-174) + build_dataset (dataset.hpp:74-152)
+// straight into a device-resident dataset; labels via drug_ids().
+inline DeviceDataset read_long_format(const std::string& path, const std::vector<std::string>& dictionary = {},
+                                      int device = 0, int threads = 0) {
+    std::vector<const char*> d;
+    for (const auto& x : dictionary) d.push_back(x.c_str());
+    bsccs_dataset* h = nullptr;
+    detail::check(bsccs_dataset_read_long_format(path.c_str(), d.empty() ? nullptr : d.data(),
+                                                 static_cast<int32_t>(d.size()), device, 0, threads, &h));
+    int64_t info[6];
+    bsccs_dataset_info(h, info);
+    return DeviceDataset(h, static_cast<int32_t>(info[2]));
+}
+
+inline std::vector<std::string> drug_ids(const DeviceDataset& dds) {
+    int64_t need = 0;
+    detail::check(bsccs_dataset_drug_ids(dds.get(), nullptr, 0, &need));
+    std::string buf(static_cast<std::size_t>(need), '\0');
+    detail::check(bsccs_dataset_drug_ids(dds.get(), buf.data(), need, nullptr));
+    buf.resize(buf.size() - 1);
+    std::vector<std::string> out;
+    if (buf.empty()) return out;
+    std::size_t a = 0;
+    for (std::size_t b = 0; b <= buf.size(); ++b)
+        if (b == buf.size() || buf[b] == '\n') {
+            out.push_back(buf.substr(a, b - a));
+            a = b + 1;
+        }
+    return out;
+}
+
 } // namespace bsccs_b200
+
+#if defined(BSCCS_B200_HAVE_REFERENCE_DRIVERS)
+namespace bsccs_b200 {
+// Signature of bsccs::grid_search_cv (cross_validation.hpp:100-104) with the
+// device engine as an extra trailing argument; returns the reference's
+// CVResult (cells [grid point][fold]).
+inline ::bsccs::CVResult grid_search_cv(const DeviceDataset& dds, const ::bsccs::CVConfig& cfg,
+                                        int engine = BSCCS_ENGINE_SUBSET) {
+    bsccs_cv_config c;
+    bsccs_cv_config_default(&c);
+    c.folds = cfg.folds;
+    c.prior_kind = static_cast<int32_t>(cfg.prior_kind);
+    c.variance_is_laplace_scale = cfg.variance_is_laplace_scale ? 1 : 0;
+    c.warm_start = cfg.warm_start ? 1 : 0;
+    c.seed = cfg.seed;
+    c.solver = to_c_config(cfg.solver);
+    c.engine = engine;
+    const int32_t P = static_cast<int32_t>(cfg.variance_grid.size());
+    const std::size_t F = static_cast<std::size_t>(cfg.folds > 0 ? cfg.folds : 1);
+    std::vector<double> grid(static_cast<std::size_t>(P > 0 ? P : 1)), mean(grid.size());
+    std::vector<bsccs_cv_cell> cells(grid.size() * F);
+    bsccs_cv_result r;
+    detail::check(bsccs_grid_search_cv(dds.get(), &c, cfg.variance_grid.data(), P, grid.data(), cells.data(),
+                                       mean.data(), &r));
+    ::bsccs::CVResult out;
+    out.variance_grid.assign(grid.begin(), grid.begin() + P);
+    out.cells.assign(static_cast<std::size_t>(P), std::vector<::bsccs::CVCell>(F));
+    for (int32_t g = 0; g < P; ++g)
+        for (std::size_t f = 0; f < F; ++f) {
+            const bsccs_cv_cell& x = cells[static_cast<std::size_t>(g) * F + f];
+            ::bsccs::CVCell& y = out.cells[static_cast<std::size_t>(g)][f];
+            y.predictive_ll = x.predictive_ll;
+            y.cycles = x.cycles;
+            y.converged = x.converged != 0;
+            y.valid = x.valid != 0;
+        }
+    out.mean_predictive_ll.assign(mean.begin(), mean.begin() + P);
+    out.selected_index = r.selected_index;
+    out.selected_variance = r.selected_variance;
+    out.total_cycles = r.total_cycles;
+    return out;
+}
+
+inline ::bsccs::CVResult grid_search_cv(const ::bsccs::Dataset& ds, const ::bsccs::CVConfig& cfg,
+                                        ::bsccs::ThreadPool* pool = nullptr, int device = 0,
+                                        int engine = BSCCS_ENGINE_SUBSET) {
+    (void)pool;
+    DeviceDataset dds(ds, device);
+    return grid_search_cv(dds, cfg, engine);
+}
+
+// Signature of bsccs::run_bootstrap (bootstrap.hpp:79-81) plus the engine.
+inline ::bsccs::BootstrapResult run_bootstrap(const DeviceDataset& dds, const ::bsccs::BootstrapConfig& cfg,
+                                              int engine = BSCCS_ENGINE_SUBSET) {
+    bsccs_bootstrap_config c;
+    bsccs_bootstrap_config_default(&c);
+    c.replicates = cfg.replicates;
+    c.warm_start = cfg.warm_start ? 1 : 0;
+    c.level = cfg.level;
+    c.seed = cfg.seed;
+    c.prior = to_c_prior(cfg.prior);
+    c.solver = to_c_config(cfg.solver);
+    c.engine = engine;
+    const std::size_t J = static_cast<std::size_t>(dds.num_drugs());
+    ::bsccs::BootstrapResult out;
+    out.beta_full.assign(J, 0.0);
+    out.lower.assign(J, 0.0);
+    out.upper.assign(J, 0.0);
+    out.p_hat.assign(J, 0.0);
+    bsccs_bootstrap_result r;
+    detail::check(bsccs_run_bootstrap(dds.get(), &c, out.beta_full.data(), out.lower.data(), out.upper.data(),
+                                      out.p_hat.data(), &r));
+    out.full_converged = r.full_converged != 0;
+    out.replicates = r.replicates;
+    out.used = r.used;
+    out.non_converged = r.non_converged;
+    return out;
+}
+
+inline ::bsccs::BootstrapResult run_bootstrap(const ::bsccs::Dataset& ds, const ::bsccs::BootstrapConfig& cfg,
+                                              ::bsccs::ThreadPool* pool = nullptr, int device = 0,
+                                              int engine = BSCCS_ENGINE_SUBSET) {
+    (void)pool;
+    DeviceDataset dds(ds, device);
+    return run_bootstrap(dds, cfg, engine);
+}
+} // namespace bsccs_b200
+#endif
 
 #if defined(BSCCS_B200_HAVE_REFERENCE)
 namespace bsccs_b200 {

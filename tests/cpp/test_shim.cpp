@@ -5,6 +5,7 @@
 #include <bsccs/bsccs.hpp>
 #include <bsccs_b200_solver.hpp>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 
@@ -39,6 +40,37 @@ int main() {
         bsccs_b200::fit(ds, prior, badc);
     } catch (const bsccs::input_error&) {
         threw = true;
+    }
+    // the many-fit callers: same call with the namespace switched, both engines
+    bsccs::CVConfig cv;
+    cv.folds = 4;
+    cv.variance_grid = {0.01, 0.1, 1.0};
+    cv.seed = 5;
+    const bsccs::CVResult rcv = bsccs::grid_search_cv(ds, cv);
+    bsccs::BootstrapConfig bc;
+    bc.replicates = 5;
+    bc.seed = 9;
+    bc.prior.kind = bsccs::PriorKind::normal;
+    bc.prior.variance = 0.1;
+    const bsccs::BootstrapResult rbt = bsccs::run_bootstrap(ds, bc);
+    const bsccs_b200::DeviceDataset dds(ds);
+    for (int engine : {BSCCS_ENGINE_SUBSET, BSCCS_ENGINE_BATCHED}) {
+        const bsccs::CVResult dcv = bsccs_b200::grid_search_cv(dds, cv, engine);
+        if (dcv.selected_index != rcv.selected_index || dcv.total_cycles != rcv.total_cycles) bad = 1;
+        for (std::size_t g = 0; g < rcv.cells.size(); ++g)
+            for (std::size_t f = 0; f < rcv.cells[g].size(); ++f) {
+                const double a = dcv.cells[g][f].predictive_ll, b = rcv.cells[g][f].predictive_ll;
+                if (dcv.cells[g][f].cycles != rcv.cells[g][f].cycles || std::abs(a - b) > 1e-8 * std::abs(b)) bad = 1;
+            }
+        const bsccs::BootstrapResult dbt = bsccs_b200::run_bootstrap(dds, bc, engine);
+        if (dbt.used != rbt.used || dbt.p_hat != rbt.p_hat) bad = 1;
+        for (std::size_t j = 0; j < rbt.lower.size(); ++j) {
+            const double lo = rbt.lower[j], up = rbt.upper[j];
+            if (std::abs(dbt.lower[j] - lo) > std::max(1e-6 * std::abs(lo), 1e-9)) bad = 1;
+            if (std::abs(dbt.upper[j] - up) > std::max(1e-6 * std::abs(up), 1e-9)) bad = 1;
+        }
+        std::printf("shim engine %d: cv selected %d/%d, bootstrap used %d/%d\n", engine, dcv.selected_index,
+                    rcv.selected_index, dbt.used, rbt.used);
     }
     std::printf("shim: cycles %d/%d lp %.17g/%.17g threw=%d -> %s\n", dev.cycles_run, ref.cycles_run,
                 dev.log_posterior, ref.log_posterior, threw, (!bad && threw) ? "OK" : "FAIL");
