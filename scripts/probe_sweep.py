@@ -17,7 +17,10 @@ ds = datagen.config_dataset(wl)
 prior = B.laplace_prior(0.1)
 cfg = B.SolverConfig()
 lib = _native.lib()
-modes = {"full": 0, "late_lexp": 64, "nospec": 16, "no_update": 2, "no_xchg": 4, "xchg_only": 3}
+modes = {"full": 0, "early_spec": 128, "late_lexp": 64, "nospec": 16, "no_update": 2, "no_xchg": 4,
+         "xchg_only": 3}
+if len(sys.argv) > 3:
+    modes = {k: v for k, v in modes.items() if k in sys.argv[3].split(",")}
 for ctas in ctas_list:
     dds = B.DeviceDataset(ds, 0, ctas)
     for name, f in modes.items():
