@@ -77,7 +77,6 @@ struct BatchArgs {
     const uint8_t* colnz;    // [J][RB]
     PriorParams prior[kBMaxRB];
     unsigned live;           // fits taking part in this cycle
-    int R;
     int normalized;
     int ctas;
     unsigned long long* xarea; // exchange area
@@ -89,7 +88,7 @@ struct BatchArgs {
     long long* moved;        // [RB]
     const int64_t* col_ptr;  // byte accounting
     const int32_t* col_runs;
-    int64_t K, N;
+    int64_t K;
     double* bytes;           // algorithmic bytes of this launch (CTA 0)
     unsigned long long* trace; // profiling only: [ntrace][ctas][6] globaltimer stamps
     int ntrace;
@@ -1213,7 +1212,6 @@ void batch_fit(Batch* b, int R, const PriorParams* priors, const double* const* 
     a.ydx = b->ydx;
     a.colnz = b->colnz;
     for (int r = 0; r < R; ++r) a.prior[r] = priors[r];
-    a.R = R;
     a.normalized = cfg->convergence != 0;
     a.ctas = ds->ctas;
     a.xarea = b->xarea;
@@ -1226,7 +1224,6 @@ void batch_fit(Batch* b, int R, const PriorParams* priors, const double* const* 
     a.col_ptr = ds->col_ptr;
     a.col_runs = ds->col_runs;
     a.K = ds->K;
-    a.N = ds->N;
     a.bytes = b->bytes_d;
     a.trace = debug_trace_buffer(&a.ntrace);
     std::vector<double> lb(RB);
