@@ -32,6 +32,7 @@
 #include "devutil.h"
 #include "engine.h"
 #include "prior.h"
+#include "rng.h"
 #include "xchg.cuh"
 
 namespace bsccs_b200 {
@@ -1176,27 +1177,41 @@ void batch_fit(Batch* b, int R, const PriorParams* priors, const double* const* 
     read_errors(); // init_state overflow
     // visit list: every column non-empty in the parent (an empty parent column
     // is empty for every selection; its beta stays at its start value and the
-    // skip rule holds unless a warm start made it non-zero -- then visit it)
-    std::vector<int32_t> visit;
+    // skip rule holds unless a warm start made it non-zero -- then visit it);
+    // the per-fit skip rule (solver.hpp:119-121) runs in the kernel
+    std::vector<uint8_t> keep(static_cast<size_t>(J), 0);
     for (int32_t j = 0; j < J; ++j) {
         bool any_nz = false;
         for (int r = 0; r < R && !any_nz; ++r) any_nz = bh[static_cast<size_t>(j) * RB + r] != 0.0;
-        if (ds->col_nonempty_h[static_cast<size_t>(j)] || any_nz) visit.push_back(j);
+        keep[static_cast<size_t>(j)] = ds->col_nonempty_h[static_cast<size_t>(j)] || any_nz;
     }
-    if (visit != b->visit_h) {
-        b->visit_h = visit;
-        if (!visit.empty()) {
-            CUDA_TRY(cudaMemcpyAsync(b->visit, visit.data(), sizeof(int32_t) * visit.size(), cudaMemcpyHostToDevice, s));
-            // reuse the single-fit vsplit builder through a tiny kernel launch on this stream
-            build_vsplit(ds, b->visit, static_cast<int>(visit.size()), b->vsplit, s);
+    // visit order: ascending, or reshuffled every cycle (solver.hpp:109-114)
+    // by the generator every fit of the batch shares (same seed, same cycle)
+    std::vector<int32_t> order(static_cast<size_t>(J));
+    for (int32_t j = 0; j < J; ++j) order[static_cast<size_t>(j)] = j;
+    Xoshiro order_rng(cfg->cycle_seed);
+    std::vector<int32_t> visit;
+    auto upload_visit = [&]() {
+        visit.clear();
+        for (int32_t j : order)
+            if (keep[static_cast<size_t>(j)]) visit.push_back(j);
+        if (visit != b->visit_h) {
+            b->visit_h = visit;
+            if (!visit.empty()) {
+                CUDA_TRY(
+                    cudaMemcpyAsync(b->visit, visit.data(), sizeof(int32_t) * visit.size(), cudaMemcpyHostToDevice, s));
+                build_vsplit(ds, b->visit, static_cast<int>(visit.size()), b->vsplit, s);
+                CUDA_TRY(cudaStreamSynchronize(s)); // `visit` is reused by the next cycle
+            }
         }
-    }
+    };
+    if (!cfg->random_cycle) upload_visit();
     BatchArgs a;
     std::memset(&a, 0, sizeof a);
     a.pairs = ds->pairs;
     a.vsplit = b->vsplit;
     a.visit = b->visit;
-    a.nvisit = static_cast<int>(visit.size());
+    a.nvisit = static_cast<int>(std::count(keep.begin(), keep.end(), static_cast<uint8_t>(1)));
     a.cta_subj = ds->cta_subj;
     a.subject_offsets = ds->subject_offsets;
     a.era_len = ds->era_lengths;
@@ -1230,6 +1245,13 @@ void batch_fit(Batch* b, int R, const PriorParams* priors, const double* const* 
     b->sweep_ms = 0.0;
     b->alg_bytes = 0.0;
     while (live && cycles < cfg->max_cycles) {
+        if (cfg->random_cycle) {
+            for (size_t jj = order.size(); jj > 1; --jj) {
+                const size_t rr = static_cast<size_t>(order_rng.below(jj));
+                std::swap(order[jj - 1], order[rr]);
+            }
+            upload_visit();
+        }
         a.live = live;
         CUDA_TRY(cudaEventRecord(b->ev0, s));
         if (RB == 8) launch_cycle<8>(b, a);

@@ -96,7 +96,9 @@ void cv_folds(const bsccs_dataset* ds, const bsccs_cv_config* cfg, const std::ve
     std::vector<int32_t> all(static_cast<size_t>(ds->N)), sizes(static_cast<size_t>(std::max(folds, 0)));
     kfold_split(ds->N, folds, cfg->seed, all.data(), sizes.data());
     if (f0 < 0 || f1 > folds || f0 > f1) input_error("cross-validation: fold range out of bounds");
-    if (cfg->engine == BSCCS_ENGINE_BATCHED) {
+    // the batched engine runs the sparse update path; dense-route configs
+    // (UpdatePath::dense) take the materialised route
+    if (cfg->engine == BSCCS_ENGINE_BATCHED && cfg->solver.path == 0) {
         cv_folds_batched(ds, cfg, grid, all, sizes, f0, f1, cells, res);
         return;
     }
@@ -178,7 +180,7 @@ void validate_bootstrap(const bsccs_bootstrap_config* cfg) {
 void boot_replicates(const bsccs_dataset* ds, const bsccs_bootstrap_config* cfg, const double* beta_full, int32_t r0,
                      int32_t r1, double* est, int32_t* conv, bsccs_bootstrap_result* res) {
     if (r0 < 0 || r1 < r0) input_error("bootstrap: replicate range out of bounds");
-    if (cfg->engine == BSCCS_ENGINE_BATCHED) {
+    if (cfg->engine == BSCCS_ENGINE_BATCHED && cfg->solver.path == 0) {
         boot_replicates_batched(ds, cfg, beta_full, r0, r1, est, conv, res);
         return;
     }
@@ -343,6 +345,7 @@ bsccs_status bsccs_fit_batch(const bsccs_dataset* ds, int32_t R, const bsccs_pri
         if (!ds || !priors || !beta_out || !results || !status) input_error("fit_batch: null argument");
         if (R < 1 || R > 16) input_error("fit_batch: 1..16 fits per batch");
         validate_config(cfg);
+        if (cfg->path != 0) input_error("fit_batch: the batched engine runs the sparse update path");
         const int32_t N = ds->N, J = ds->J;
         std::vector<PriorParams> p(static_cast<size_t>(R));
         for (int32_t r = 0; r < R; ++r) p[r] = to_params(&priors[r]);

@@ -333,3 +333,33 @@ def test_fit_batch_sixteen_and_errors(oracle_ds, ref):
     t = rds.fit(B.normal_prior(0.1), B.SolverConfig())
     for r in (0, 2):
         assert fits[r].cycles_run == t["cycles_run"] and close(fits[r].beta_map, t["beta"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("engine", ["subset", "batched"])
+def test_cv_shuffled_order_normalized_criterion(oracle_ds, ref, engine):
+    """random_cycle (a fresh Fisher-Yates order every cycle, solver.hpp:109-114)
+    and the normalized criterion through both engines, against the reference"""
+    solver = B.SolverConfig(random_cycle=True, cycle_seed=31, convergence=B.ConvergenceMode.normalized,
+                            epsilon=1e-6)
+    cfg = CV.CVConfig(folds=3, variance_grid=[0.05, 0.5], prior_kind=B.PriorKind.laplace, seed=2, solver=solver,
+                      engine=engine)
+    res = CV.grid_search_cv(oracle_ds, cfg)
+    exp = ref.dataset(oracle_ds).grid_search_cv(3, [0.05, 0.5], B.PriorKind.laplace, 2, solver)
+    exp = {k: (v.tolist() if hasattr(v, "tolist") else v) for k, v in exp.items()}
+    _check_cv(res, exp)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("engine", ["subset", "batched"])
+def test_bootstrap_dense_route(oracle_ds, ref, engine):
+    """UpdatePath::dense replicates (the batched request takes the
+    materialised route) against the reference"""
+    solver = B.SolverConfig(path=B.UpdatePath.dense)
+    prior = B.normal_prior(0.1)
+    res = BT.run_bootstrap(oracle_ds, BT.BootstrapConfig(replicates=3, seed=4, prior=prior, solver=solver,
+                                                         engine=engine))
+    exp = ref.dataset(oracle_ds).run_bootstrap(3, 0.95, 4, prior, solver)
+    _check_boot(res, exp)
+    with pytest.raises(B.InputError):
+        B.fit_batch(oracle_ds, [prior], None, None, solver)
