@@ -363,3 +363,22 @@ def test_bootstrap_dense_route(oracle_ds, ref, engine):
     _check_boot(res, exp)
     with pytest.raises(B.InputError):
         B.fit_batch(oracle_ds, [prior], None, None, solver)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("engine", ["subset", "batched"])
+def test_bootstrap_cycle_cap_and_refresh(oracle_ds, ref, engine):
+    """a cycle cap that stops some replicates short (counted as non-converged,
+    excluded from the summaries, bootstrap.hpp:118-127) and a dense refresh
+    every 2 cycles (solver.hpp:187-189), cold starts"""
+    solver = B.SolverConfig(max_cycles=7, dense_refresh_interval=2, epsilon=3e-4)  # 2 of 9 converge
+    prior = B.laplace_prior(0.2)
+    cfg = BT.BootstrapConfig(replicates=9, seed=11, prior=prior, solver=solver, warm_start=False, engine=engine)
+    exp = ref.dataset(oracle_ds).run_bootstrap(9, 0.95, 11, prior, solver, warm_start=False)
+    if exp["used"] == 0:
+        with pytest.raises(B.ConvergenceError):
+            BT.run_bootstrap(oracle_ds, cfg)
+        return
+    res = BT.run_bootstrap(oracle_ds, cfg)
+    _check_boot(res, exp)
+    assert res.non_converged == exp["non_converged"]
