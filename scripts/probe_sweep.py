@@ -17,8 +17,8 @@ ds = datagen.config_dataset(wl)
 prior = B.laplace_prior(0.1)
 cfg = B.SolverConfig()
 lib = _native.lib()
-modes = {"full": 0, "early_spec": 128, "late_lexp": 64, "nospec": 16, "no_update": 2, "no_xchg": 4,
-         "xchg_only": 3}
+modes = {"full": 0, "late_lexp": 64, "nospec": 16, "no_update": 2, "no_xchg": 4, "xchg_only": 3,
+         "no_gh": 1, "xchg_only_late": 67, "xchg_only_nospec": 19, "nothing": 7, "nothing_nospec": 23}
 if len(sys.argv) > 3:
     modes = {k: v for k, v in modes.items() if k in sys.argv[3].split(",")}
 for ctas in ctas_list:
