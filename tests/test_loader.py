@@ -4,7 +4,8 @@ the reference's own reader and builder on the same files -- every array
 bit-for-bit, the labels, and the exact error messages (cases restated from
 test_io.cpp:48-116).  Files larger than 1 MB are parsed in several host
 chunks; the multi-chunk cases pin that the result and the reported error do
-not depend on the chunking."""
+not depend on the chunking.  Every error is raised before the device is
+touched, so the error cases run in the CPU suite."""
 import numpy as np
 import pytest
 
@@ -110,7 +111,6 @@ def test_dictionary_pins_order(ref, tmp_path):
         assert str(ei.value) == msg
 
 
-@pytest.mark.gpu
 @pytest.mark.parametrize("text", [
     "p1\t5\t0\na b c\n",              # field count, line 2
     "p1\tfive\t0\n",                  # not an integer
@@ -131,7 +131,6 @@ def test_errors_match_reference_messages(ref, tmp_path, text):
     assert str(ei.value) == msg
 
 
-@pytest.mark.gpu
 def test_earliest_error_wins_across_chunks(ref, tmp_path):
     """a non-contiguous subject early in the file and a malformed line in a
     later chunk: the reference stops at the first; so must every chunking"""
@@ -160,7 +159,6 @@ def test_earliest_error_wins_across_chunks(ref, tmp_path):
         assert str(ei.value) == msg
 
 
-@pytest.mark.gpu
 def test_missing_file(tmp_path):
     with pytest.raises(B.InputError, match="cannot open"):
         B.read_long_format(str(tmp_path / "missing_file.tsv"))
