@@ -35,6 +35,13 @@
 #include "rng.h"
 #include "xchg.cuh"
 
+#ifndef BSCCS_DIAG_NOLOAD
+#define BSCCS_DIAG_NOLOAD 0
+#endif
+#ifndef BSCCS_DIAG_NOCOMPUTE
+#define BSCCS_DIAG_NOCOMPUTE 0
+#endif
+
 namespace bsccs_b200 {
 
 namespace {
@@ -69,9 +76,9 @@ struct BatchArgs {
     const int32_t* era_subj; // subject of every era
     double* xb;              // [K][RB]
     double* snap;            // [K][RB]
-    double* den;             // [N][RB]
+    double* den;             // subject blocks: [N][2*RB] doubles = den[RB] | m*n[RB] (int32) | pad
     const int32_t* m;        // [N][RB] multiplicities
-    const int32_t* wn;       // [N][RB] m * n_i (the run weight of the gradient sums)
+    const int32_t* wn;       // m * n_i inside the subject blocks: int index s*4*RB + f from (int*)den + 2*RB
     double* beta;            // [J][RB]
     double* trust;           // [J][RB]
     const double* ydx;       // [J][RB]
@@ -153,8 +160,8 @@ struct BSmem {
     unsigned live;
     // warp 0 lane r: fit r's coordinate scalars and counters (kept out of
     // the registers of every thread)
-    double bj[RB], rj[RB], yj[RB], abytes[RB];
-    int nz[RB];
+    double bj[2][RB], rj[2][RB], yj[2][RB], abytes[RB]; // [coordinate parity][fit]
+    int nz[2][RB];
     long long nvis[RB], nmov[RB];
     int2 pst[2][BCfg<RB>::kCapP];         // pairs of this / the next coordinate's slice
     double le[BCfg<RB>::kCapP * RB];      // l*exp per slot (then the update's differences)
@@ -223,7 +230,7 @@ __device__ __forceinline__ void gh_tail_head(const BatchArgs& A, int64_t p0, int
         if (p2.y != pr.y) break;
         num = __dadd_rn(num, lexp(A.era_len[p2.x], A.xb[static_cast<size_t>(p2.x) * RB + fit]));
     }
-    const double den = A.den[static_cast<size_t>(pr.y) * RB + fit];
+    const double den = A.den[static_cast<size_t>(pr.y) * (2 * RB) + fit];
     if (!(den > 0.0)) ferr = ferr ? ferr : DERR_DEN_NONPOSITIVE;
     double w = num / den;
     if (w > 1.0) w = 1.0;
@@ -238,7 +245,7 @@ __device__ __forceinline__ void upd_tail_head(const BatchArgs& A, int64_t p0, in
     const int2 pr = __ldg(&A.pairs[p0 + q]);
     if (q > 0 && __ldg(&A.pairs[p0 + q - 1].y) == pr.y) return;
     if (A.m[static_cast<size_t>(pr.y) * RB + fit] == 0) return;
-    double den = A.den[static_cast<size_t>(pr.y) * RB + fit];
+    double den = A.den[static_cast<size_t>(pr.y) * (2 * RB) + fit];
     for (int q2 = q; q2 < np; ++q2) {
         const int2 p2 = __ldg(&A.pairs[p0 + q2]);
         if (p2.y != pr.y) break;
@@ -254,7 +261,7 @@ __device__ __forceinline__ void upd_tail_head(const BatchArgs& A, int64_t p0, in
         den = __dadd_rn(den, __dsub_rn(lexp(len, upd), lexp(len, old)));
         *xp = upd;
     }
-    A.den[static_cast<size_t>(pr.y) * RB + fit] = den;
+    A.den[static_cast<size_t>(pr.y) * (2 * RB) + fit] = den;
 }
 
 template <int RB>
@@ -280,10 +287,17 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
     if (threadIdx.x == 0) sm.live = A.live;
     if (threadIdx.x < RB) sm.status[threadIdx.x] = 0;
     const longlong2* vs = A.vsplit + static_cast<size_t>(c) * A.nvisit;
-    if (A.nvisit > 0) { // first slice's pairs
+    if (A.nvisit > 0) { // first slice's pairs and per-fit scalars
         const longlong2 s0 = vs[0];
         const int n0 = min(static_cast<int>(s0.y - s0.x), CAP);
         for (int q = threadIdx.x; q < n0; q += kBT) sm.pst[0][q] = __ldg(&A.pairs[s0.x + q]);
+        if (threadIdx.x < RB) {
+            const size_t o = static_cast<size_t>(A.visit[0]) * RB + threadIdx.x;
+            sm.bj[0][threadIdx.x] = A.beta[o];
+            sm.rj[0][threadIdx.x] = A.trust[o];
+            sm.yj[0][threadIdx.x] = A.ydx[o];
+            sm.nz[0][threadIdx.x] = A.colnz[o];
+        }
     }
     __syncthreads();
     if (threadIdx.x < RB) {
@@ -304,14 +318,6 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
         BTRACE(0);
         const unsigned live = sm.live;
         const bool flive = (live >> fit) & 1u;
-        // warp 0 lane r: this coordinate's beta / trust / y_dot_x of fit r
-        if (threadIdx.x < RB) {
-            const size_t o = static_cast<size_t>(j) * RB + threadIdx.x;
-            sm.bj[threadIdx.x] = A.beta[o];
-            sm.rj[threadIdx.x] = A.trust[o];
-            sm.yj[threadIdx.x] = A.ydx[o];
-            sm.nz[threadIdx.x] = A.colnz[o];
-        }
         // Single-chunk slices (every slot of this thread fits its U
         // registers) keep each slot's gathered values in registers from the
         // gradient pass through the update: one gather round trip per
@@ -333,19 +339,38 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
                     const int sn = q + 1 < np ? P[q + 1].y : -1;
                     const bool hd = pr.y != sp;
                     fl[u] = 1 | (hd ? 2 : 0) | (hd && sn != pr.y ? 4 : 0);
+#if BSCCS_DIAG_NOLOAD // profiling variant: no gathers (compute on stand-in values)
+                    xbv[u] = -1e-3 * q;
+                    len[u] = 10;
+                    mm[u] = 1;
+                    dn[u] = 50.0;
+#else
                     xbv[u] = A.xb[static_cast<size_t>(pr.x) * RB + fit];
                     len[u] = __ldg(&A.era_len[pr.x]);
-                    mm[u] = __ldg(&A.wn[static_cast<size_t>(pr.y) * RB + fit]);
-                    if (hd) dn[u] = A.den[static_cast<size_t>(pr.y) * RB + fit];
+                    mm[u] = __ldg(&A.wn[static_cast<size_t>(pr.y) * (4 * RB) + fit]);
+                    if (hd) dn[u] = A.den[static_cast<size_t>(pr.y) * (2 * RB) + fit];
+#endif
                 }
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int q = qfirst + u * QS;
                 if (fl[u] & 1) {
+#if BSCCS_DIAG_NOCOMPUTE // profiling variant: gathers consumed without exp / divide
+                    {
+                        const double lz = xbv[u] + len[u];
+                        if ((fl[u] & 4) && mm[u] != 0) {
+                            gs = __dadd_rn(gs, lz + dn[u]);
+                            hs = __dadd_rn(hs, lz);
+                        }
+                        sm.le[q * RB + fit] = lz;
+                        continue;
+                    }
+#endif
+                    if (mm[u] == 0) continue; // a left-out subject: no term, no update (engine work skipped)
                     const double le = lexp(len[u], xbv[u]);
                     sm.le[q * RB + fit] = le;
-                    if ((fl[u] & 4) && mm[u] != 0) { // single-pair run: its term now
+                    if (fl[u] & 4) { // single-pair run: its term now
                         if (!(dn[u] > 0.0)) ferr = ferr ? ferr : DERR_DEN_NONPOSITIVE;
                         double w = le / dn[u];
                         if (w > 1.0) w = 1.0;
@@ -371,8 +396,8 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
                         xbv[u] = A.xb[static_cast<size_t>(pr.x) * RB + fit];
                         len[u] = __ldg(&A.era_len[pr.x]);
                         if (sg) {
-                            mm[u] = __ldg(&A.wn[static_cast<size_t>(pr.y) * RB + fit]);
-                            dn[u] = A.den[static_cast<size_t>(pr.y) * RB + fit];
+                            mm[u] = __ldg(&A.wn[static_cast<size_t>(pr.y) * (4 * RB) + fit]);
+                            dn[u] = A.den[static_cast<size_t>(pr.y) * (2 * RB) + fit];
                         }
                     }
                 }
@@ -429,7 +454,7 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
                     if (p2.y != s) break;
                     num = __dadd_rn(num, lexp(A.era_len[p2.x], A.xb[static_cast<size_t>(p2.x) * RB + fit]));
                 }
-                const double den = A.den[static_cast<size_t>(s) * RB + fit];
+                const double den = A.den[static_cast<size_t>(s) * (2 * RB) + fit];
                 if (!(den > 0.0)) ferr = ferr ? ferr : DERR_DEN_NONPOSITIVE;
                 double w = num / den;
                 if (w > 1.0) w = 1.0;
@@ -447,18 +472,21 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
         if (w0) {
             const int r = threadIdx.x;
             if (r < RB) {
-                const double bj = sm.bj[r], rj = sm.rj[r];
+                // this coordinate's beta / trust / y_dot_x, prefetched during
+                // the previous exchange (CTA 0 writes column j only after
+                // this coordinate's exchange, which needs this CTA's publish)
+                const double bj = sm.bj[cur][r], rj = sm.rj[cur][r];
                 double delta = 0.0;
                 int st = sm.status[r];
                 const bool lr = ((live >> r) & 1u) && st == 0;
-                const bool skip = !sm.nz[r] && bj == 0.0; // solver.hpp:119-121 (weighted column)
+                const bool skip = !sm.nz[cur][r] && bj == 0.0; // solver.hpp:119-121 (weighted column)
                 if (lr && !skip) {
                     if (berr_count<RB>(sm, r) != 0) {
                         st = -1; // an error seen by some CTA (recorded there)
                     } else {
                         const double tg = from_limbs(sm.xd[6 * r], sm.xd[6 * r + 1], sm.xd[6 * r + 2]);
                         const double th = from_limbs(sm.xd[6 * r + 3], sm.xd[6 * r + 4], sm.xd[6 * r + 5]);
-                        const double g = __dsub_rn(sm.yj[r], tg);
+                        const double g = __dsub_rn(sm.yj[cur][r], tg);
                         const double h = th == 0.0 ? 0.0 : -th;
                         double step = 0.0;
                         const int serr = penalized_step(A.prior[r], bj, g, h, &step);
@@ -502,7 +530,16 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
                 sm.status[r] = st;
             }
         } else if (threadIdx.x >= Cf::kPollThreads && idx + 1 < A.nvisit) {
-            // while the partials travel: the next slice's pairs
+            // while the partials travel: the next coordinate's per-fit scalars ...
+            const int tt = static_cast<int>(threadIdx.x) - Cf::kPollThreads;
+            if (tt < RB) {
+                const size_t o = static_cast<size_t>(A.visit[idx + 1]) * RB + tt;
+                sm.bj[cur ^ 1][tt] = A.beta[o];
+                sm.rj[cur ^ 1][tt] = A.trust[o];
+                sm.yj[cur ^ 1][tt] = A.ydx[o];
+                sm.nz[cur ^ 1][tt] = A.colnz[o];
+            }
+            // ... and the next slice's pairs
             const longlong2 nsl = vs[idx + 1];
             const int nn = min(static_cast<int>(nsl.y - nsl.x), CAP);
             int2* Q = sm.pst[cur ^ 1];
@@ -538,7 +575,7 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
                     diff = __dmul_rn(sm.le[q * RB + fit], em1);
                     A.xb[static_cast<size_t>(pr.x) * RB + fit] = upd;
                 }
-                if (fl[u] & 4) A.den[static_cast<size_t>(pr.y) * RB + fit] = __dadd_rn(dn[u], diff);
+                if (fl[u] & 4) A.den[static_cast<size_t>(pr.y) * (2 * RB) + fit] = __dadd_rn(dn[u], diff);
                 else sm.le[q * RB + fit] = diff; // this slot's l*exp is no longer needed
             }
         } else if (flive && d != 0.0) {
@@ -554,9 +591,9 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
                         const int sn = q + 1 < lim ? P[q + 1].y : (q + 1 < np ? pair_subj(A.pairs, p0, q + 1) : -1);
                         const bool sg = pr.y != sp && sn != pr.y;
                         fl[u] = 1 | (sg ? 4 : 0);
-                        mm[u] = __ldg(&A.wn[static_cast<size_t>(pr.y) * RB + fit]);
+                        mm[u] = __ldg(&A.wn[static_cast<size_t>(pr.y) * (4 * RB) + fit]);
                         xbv[u] = A.xb[static_cast<size_t>(pr.x) * RB + fit];
-                        if (sg) dn[u] = A.den[static_cast<size_t>(pr.y) * RB + fit];
+                        if (sg) dn[u] = A.den[static_cast<size_t>(pr.y) * (2 * RB) + fit];
                     }
                 }
 #pragma unroll
@@ -573,7 +610,7 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
                             diff = __dmul_rn(sm.le[q * RB + fit], em1);
                             A.xb[static_cast<size_t>(pr.x) * RB + fit] = upd;
                         }
-                        if (fl[u] & 4) A.den[static_cast<size_t>(pr.y) * RB + fit] = __dadd_rn(dn[u], diff);
+                        if (fl[u] & 4) A.den[static_cast<size_t>(pr.y) * (2 * RB) + fit] = __dadd_rn(dn[u], diff);
                         else sm.le[q * RB + fit] = diff;
                     }
                 }
@@ -590,7 +627,7 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
                 const int s = P[q].y;
                 double den = dn[u];
                 for (int q2 = q; q2 < np && P[q2].y == s; ++q2) den = __dadd_rn(den, sm.le[q2 * RB + fit]);
-                A.den[static_cast<size_t>(s) * RB + fit] = den;
+                A.den[static_cast<size_t>(s) * (2 * RB) + fit] = den;
             }
         } else if (flive && d != 0.0) {
             for (int q = qfirst; q < lim; q += QS) {
@@ -599,7 +636,7 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
                 const bool multi = q + 1 < np && (q + 1 < lim ? P[q + 1].y : pair_subj(A.pairs, p0, q + 1)) == s;
                 if (!multi) continue;
                 if (A.m[static_cast<size_t>(s) * RB + fit] == 0) continue;
-                double* dp = A.den + static_cast<size_t>(s) * RB + fit;
+                double* dp = A.den + static_cast<size_t>(s) * (2 * RB) + fit;
                 double den = *dp;
                 int q2 = q;
                 for (; q2 < lim && P[q2].y == s; ++q2) den = __dadd_rn(den, sm.le[q2 * RB + fit]);
@@ -733,7 +770,7 @@ __global__ void k_bdense_den(const int32_t* __restrict__ off, const int32_t* __r
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x / RB) + threadIdx.x / RB; i < N; i += step) {
         double t = 0.0;
         for (int32_t k = off[i]; k < off[i + 1]; ++k) t = __dadd_rn(t, lexp(len[k], xb[static_cast<size_t>(k) * RB + fit]));
-        den[static_cast<size_t>(i) * RB + fit] = t;
+        den[static_cast<size_t>(i) * (2 * RB) + fit] = t; // subject block layout
     }
 }
 
@@ -758,7 +795,7 @@ __global__ void k_bll_partial(const int32_t* __restrict__ off, const int32_t* __
                 const int yk = y[k];
                 if (yk != 0) a = __dadd_rn(a, __dmul_rn(static_cast<double>(yk), xb[static_cast<size_t>(k) * RB + fit]));
             }
-            const double d = den[static_cast<size_t>(i) * RB + fit];
+            const double d = den[static_cast<size_t>(i) * (2 * RB) + fit];
             if (!(d > 0.0)) {
                 if (atomicCAS(&fit_err[fit], 0, DERR_LL_DEN_NONPOSITIVE) == 0) fit_errv[fit] = d;
             }
@@ -800,7 +837,7 @@ template <int RB>
 __global__ void k_bwn(const int32_t* __restrict__ m, const int32_t* __restrict__ eps, int32_t N, int32_t* wn) {
     for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < static_cast<int64_t>(N) * RB;
          t += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        wn[t] = m[t] * eps[t / RB];
+        wn[(t / RB) * (4 * RB) + 2 * RB + t % RB] = m[t] * eps[t / RB]; // into the subject block
 }
 
 template <int RB>
@@ -879,7 +916,7 @@ struct Batch {
     int RB = 16;
     cudaStream_t stream = nullptr;
     double *xb = nullptr, *snap = nullptr, *den = nullptr;
-    int32_t *m = nullptr, *mheld = nullptr, *wn = nullptr;
+    int32_t *m = nullptr, *mheld = nullptr;
     int32_t* era_subj = nullptr;
     double *beta = nullptr, *trust = nullptr, *ydx = nullptr;
     uint8_t* colnz = nullptr;
@@ -927,10 +964,11 @@ Batch* batch_create(const bsccs_dataset* ds, int RB) {
         const int64_t K = ds->K, N = ds->N, J = ds->J;
         b->xb = dalloc<double>(K * RB, b->bytes, s);
         b->snap = dalloc<double>(K * RB, b->bytes, s);
-        b->den = dalloc<double>(N * RB, b->bytes, s);
+        // per subject one 2*RB-double block: the denominators and, right
+        // after them, the m*n weights -- one DRAM page per subject gather
+        b->den = dalloc<double>(N * 2 * RB, b->bytes, s);
         b->m = dalloc<int32_t>(N * RB, b->bytes, s);
         b->mheld = dalloc<int32_t>(N * RB, b->bytes, s);
-        b->wn = dalloc<int32_t>(N * RB, b->bytes, s);
         b->era_subj = dalloc<int32_t>(K, b->bytes, s);
         k_era_subj<<<build_grid(ds->device), 256, 0, s>>>(ds->subject_offsets, ds->N, b->era_subj);
         count_launches(1);
@@ -976,7 +1014,7 @@ void batch_destroy(Batch* b) {
     cudaSetDevice(b->ds->device);
     cudaStream_t s = b->stream;
     if (s) {
-        for (void** p : {(void**)&b->xb, (void**)&b->snap, (void**)&b->den, (void**)&b->m, (void**)&b->mheld, (void**)&b->wn, (void**)&b->era_subj,
+        for (void** p : {(void**)&b->xb, (void**)&b->snap, (void**)&b->den, (void**)&b->m, (void**)&b->mheld, (void**)&b->era_subj,
                          (void**)&b->beta, (void**)&b->trust, (void**)&b->ydx, (void**)&b->colnz, (void**)&b->visit,
                          (void**)&b->vsplit, (void**)&b->xarea, (void**)&b->xcounter, (void**)&b->fit_err,
                          (void**)&b->fit_errv, (void**)&b->crit, (void**)&b->visited, (void**)&b->moved,
@@ -1011,7 +1049,7 @@ void launch_weights_ydx(Batch* b) {
     k_bydx<RB><<<ds->J, 256, 0, b->stream>>>(ds->pairs, ds->col_ptr, ds->event_counts, b->m, ds->J, b->ydx,
                                              b->colnz);
     k_bwn<RB><<<grid_for(static_cast<int64_t>(ds->N) * RB, 256, sm_count(ds->device)), 256, 0, b->stream>>>(
-        b->m, ds->events_per_subject, ds->N, b->wn);
+        b->m, ds->events_per_subject, ds->N, reinterpret_cast<int32_t*>(b->den));
     count_launches(2);
 }
 
@@ -1221,7 +1259,7 @@ void batch_fit(Batch* b, int R, const PriorParams* priors, const double* const* 
     a.snap = b->snap;
     a.den = b->den;
     a.m = b->m;
-    a.wn = b->wn;
+    a.wn = reinterpret_cast<const int32_t*>(b->den) + 2 * RB;
     a.beta = b->beta;
     a.trust = b->trust;
     a.ydx = b->ydx;
