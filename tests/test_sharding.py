@@ -168,3 +168,53 @@ def test_local_group_oracle_case_golden():
         lp = float(fit["log_posterior"])
         assert abs(res.log_posterior - lp) <= 1e-8 * abs(lp)
     grp.close()
+
+
+def _rank_worker(port_no, q):
+    import os
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    sys.path[:0] = [str(root), str(root / "oracle")]
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_no)
+    import numpy as np
+    import torch.distributed as dist
+
+    from paper_1208_0945_b200 import bsccs as Bw
+    from paper_1208_0945_b200 import datagen as dg
+    from paper_1208_0945_b200 import sharding as sh
+
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        ds = dg.fast_sccs(6000, 30, 3.0)
+        prior = Bw.laplace_prior(0.1)
+        shard = sh.shard_dataset(ds, 1)[0]
+        g = sh.RankGroup(shard, 0)
+        r = g.fit(prior)
+        g.close()
+        s = Bw.fit(ds, prior)
+        q.put(("ok", r.cycles_run, s.cycles_run, bool(np.array_equal(r.beta_map, s.beta_map)),
+               r.log_posterior, s.log_posterior))
+    except Exception as e:  # pragma: no cover
+        q.put(("error", repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_rank_group_world1_matches_single_fit():
+    """The multi-process entry points end to end on one device: exchange-area
+    IPC handle export, peer open (own entry skipped), group fit through the
+    rank's area -- bit for bit the single fit (same kernel and partition)"""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_rank_worker, args=(_free_port(), q))
+    p.start()
+    got = q.get(timeout=300)
+    p.join(timeout=120)
+    assert got[0] == "ok", got
+    _, c1, c2, same, lp1, lp2 = got
+    assert c1 == c2 and same and lp1 == lp2
