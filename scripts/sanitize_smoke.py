@@ -1,0 +1,27 @@
+"""Small runs of every kernel family for compute-sanitizer (memcheck /
+racecheck / synccheck): dataset build, subset, single fit (sparse + dense
+route), tier-1 ops, batched fits, CV and bootstrap drivers, loader."""
+import sys
+import tempfile
+sys.path[:0] = ['.', 'oracle']
+import numpy as np
+from paper_1208_0945_b200 import bootstrap as BT, bsccs as B, cross_validation as CV, datagen
+
+ds = datagen.fast_sccs(3000, 20, 3.0)
+dds = ds.on_device()
+r = B.fit(dds, B.laplace_prior(0.1))
+B.fit(dds, B.normal_prior(0.1), B.SolverConfig(path=B.UpdatePath.dense))
+st = B.init_state(dds)
+B.fused_grad_hess(dds, st, 3)
+B.sparse_delta_update(dds, st, 3, 0.1)
+B.log_likelihood(dds, st)
+sub = dds.subset(B.resample(ds, 7, 1))
+B.fit(sub, B.normal_prior(0.1))
+w = np.stack([np.bincount(B.resample(ds, 5, k + 1), minlength=ds.num_subjects) for k in range(3)]).astype(np.int32)
+B.fit_batch(dds, [B.normal_prior(0.1)] * 3, w)
+CV.grid_search_cv(ds, CV.CVConfig(folds=3, variance_grid=[0.1, 1.0], engine="batched"))
+BT.run_bootstrap(ds, BT.BootstrapConfig(replicates=3, prior=B.normal_prior(0.1), engine="batched"))
+with tempfile.NamedTemporaryFile("w", suffix=".tsv", delete=False) as f:
+    f.write("p1\t5\t0\ta\np1\t5\t1\tb a\np2\t7\t1\tb\n")
+B.read_long_format(f.name)
+print("sanitize smoke done", r.cycles_run)
