@@ -49,7 +49,7 @@ def build_native(force: bool = False, verbose: bool = False, variant: dict | Non
     lib = LIB
     extra = []
     if variant:
-        tag = "_".join(f"{k.split('_')[-1].lower()}{v}" for k, v in sorted(variant.items()))
+        tag = "_".join(f"{k.replace('BSCCS_', '').replace('_', '').lower()}{v}" for k, v in sorted(variant.items()))
         lib = LIB_DIR / f"libbsccs_b200_{tag}.so"
         extra = [f"-D{k}={v}" for k, v in variant.items()]
     deps = [CSRC / s for s in SOURCES + HEADERS] + [ROOT / "include" / "bsccs_b200.h"]

@@ -102,6 +102,11 @@ struct BatchArgs {
     int ntrace;
 };
 
+#ifndef BSCCS_BPREFETCH
+#define BSCCS_BPREFETCH 1
+#endif
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 __device__ __forceinline__ unsigned long long bgtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -543,8 +548,24 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
             const longlong2 nsl = vs[idx + 1];
             const int nn = min(static_cast<int>(nsl.y - nsl.x), CAP);
             int2* Q = sm.pst[cur ^ 1];
-            for (int q = threadIdx.x - Cf::kPollThreads; q < nn; q += kBT - Cf::kPollThreads)
-                Q[q] = __ldg(&A.pairs[nsl.x + q]);
+            // single-chunk slices only: measured -14% sweep time at config 2
+            // (1M), +10% at config 3 (10M, chunked slices) where the extra
+            // line fetches compete with the gathers
+            const bool pf = BSCCS_BPREFETCH && nsl.y - nsl.x <= U * QS;
+            for (int q = threadIdx.x - Cf::kPollThreads; q < nn; q += kBT - Cf::kPollThreads) {
+                const int2 pr = __ldg(&A.pairs[nsl.x + q]);
+                Q[q] = pr;
+#if BSCCS_BPREFETCH
+                // ... and their gathers, into L2: the next gradient pass then
+                // hits L2 instead of HBM (the update below writes through L2,
+                // so nothing prefetched can go stale)
+                if (!pf) continue;
+                prefetch_l2(A.xb + static_cast<size_t>(pr.x) * RB);
+                prefetch_l2(A.era_len + pr.x);
+                prefetch_l2(A.den + static_cast<size_t>(pr.y) * (2 * RB));
+                if (RB * 8 >= 128) prefetch_l2(A.den + static_cast<size_t>(pr.y) * (2 * RB) + RB);
+#endif
+            }
         }
         ++seq;
         __syncthreads();

@@ -26,6 +26,7 @@
 #include <thread>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -115,6 +116,8 @@ struct SweepArgs {
     int P;
     unsigned long long* counter;
     double red_a, red_b; // kModeReduce inputs (this rank's values)
+    int prefetch; // L2 prefetch of the records two coordinates ahead (small slices only)
+    int ss_cap; // capacity of the shared-memory subject tile (0: subjects stay in HBM)
     int dbg; // profiling only: bit0 skip grad/hess, bit1 skip update, bit2 skip exchange, bit4 no speculation
     unsigned long long* trace; // profiling only: [ntrace][gridDim][kTr] globaltimer stamps
     int ntrace;
@@ -303,6 +306,20 @@ __device__ __forceinline__ void poll(const SweepArgs& A, const unsigned long lon
     te = __shfl_sync(0xffffffffu, d, 6) != 0 ? 1 : 0;
 }
 
+// ---- shared-memory subject tile -----------------------------------------------------
+//
+// When a CTA's subject range fits in shared memory, a sweep launch keeps the
+// range's (den, n) there for the whole cycle: loaded once at the start,
+// written back once at the end.  Heads then read and write denominators
+// in shared memory -- no subject gathers in the speculative window, and the
+// denominator a head reads is always current (no repair).  Subjects are
+// CTA-owned (nnz-balanced subject ranges), so no other CTA touches them.
+struct SubjTile {
+    double* den;
+    int* n;
+    int base;
+};
+
 // ---- pair slots -------------------------------------------------------------------
 
 // Index data of one pair slot: the pair, whether it starts a subject run
@@ -484,6 +501,7 @@ struct HeadRegs {
 
 // loads only (the registers are consumed later): lets the speculative
 // gathers ride through the exchange without holding up the step broadcast
+template <bool kSS>
 __device__ __forceinline__ void issue_records(const ShardArgs& S, const Cached& C, HeadRegs& H) {
     EraRec* era = S.era;
     SubjRec* subj = S.subj;
@@ -493,7 +511,7 @@ __device__ __forceinline__ void issue_records(const ShardArgs& S, const Cached& 
             const Rec r = ld_rec(era + C.slot[v].pr.x);
             H.xb[v] = r.xb;
             H.len[v] = r.len;
-            if (C.slot[v].head) {
+            if (!kSS && C.slot[v].head) {
                 const Subj sr = ld_subj(subj + C.slot[v].pr.y);
                 H.den[v] = sr.den;
                 H.n[v] = sr.n;
@@ -508,6 +526,7 @@ __device__ __forceinline__ void finish_records(const Cached& C, HeadRegs& H) {
         if (slot_valid(C.slot[v])) H.le[v] = lexp(H.len[v], H.xb[v]);
 }
 
+template <bool kSS>
 __device__ __forceinline__ void gather_records(const ShardArgs& S, const Cached& C, HeadRegs& H) {
     EraRec* era = S.era;
     SubjRec* subj = S.subj;
@@ -517,7 +536,7 @@ __device__ __forceinline__ void gather_records(const ShardArgs& S, const Cached&
             const Rec r = ld_rec(era + C.slot[v].pr.x);
             H.xb[v] = r.xb;
             H.len[v] = r.len;
-            if (C.slot[v].head) {
+            if (!kSS && C.slot[v].head) {
                 const Subj sr = ld_subj(subj + C.slot[v].pr.y);
                 H.den[v] = sr.den;
                 H.n[v] = sr.n;
@@ -529,6 +548,19 @@ __device__ __forceinline__ void gather_records(const ShardArgs& S, const Cached&
         if (slot_valid(C.slot[v])) H.le[v] = lexp(H.len[v], H.xb[v]);
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+template <bool kSS>
+__device__ __forceinline__ void prefetch_records(const ShardArgs& S, const RawCached& R) {
+#pragma unroll
+    for (int v = 0; v < kCached; ++v) {
+        if (R.slot[v].pr.x >= 0) {
+            prefetch_l2(S.era + R.slot[v].pr.x);
+            if (!kSS) prefetch_l2(S.subj + R.slot[v].pr.y);
+        }
+    }
+}
+
 __device__ __forceinline__ int ht_hash(int s) {
     return static_cast<int>((static_cast<unsigned>(s) * 2654435761u) >> (32 - kHtBits));
 }
@@ -537,6 +569,7 @@ __device__ __forceinline__ int ht_hash(int s) {
 // update wrote: a subject found in the table was touched, so its head takes
 // the new denominator and any of its eras among the updated rows takes the
 // new (x'beta, l*exp).  Shared-memory only.
+template <bool kSS>
 __device__ __forceinline__ void repair(const Cached& C, HeadRegs& H, const Smem& sm) {
 #pragma unroll
     for (int v = 0; v < kCached; ++v) {
@@ -552,7 +585,7 @@ __device__ __forceinline__ void repair(const Cached& C, HeadRegs& H, const Smem&
         if (k != s) continue;
         const int val = sm.htv[h];
         const int posj = val & 0xffff, runj = val >> 16;
-        if (C.slot[v].head) H.den[v] = sm.jden[posj];
+        if (!kSS && C.slot[v].head) H.den[v] = sm.jden[posj];
         const int row = C.slot[v].pr.x;
         for (int q = posj; q < posj + runj; ++q) {
             if (sm.jrow[q] == row) {
@@ -564,8 +597,10 @@ __device__ __forceinline__ void repair(const Cached& C, HeadRegs& H, const Smem&
     }
 }
 
+template <bool kSS>
 __device__ __forceinline__ void gh_compute(const ShardArgs& S, const Cached& C, int64_t p0, int64_t p1,
-                                           const HeadRegs& H, double& gs, double& hs, int& err, Smem& sm) {
+                                           const HeadRegs& H, double& gs, double& hs, int& err, Smem& sm,
+                                           const SubjTile& T) {
     const int2* __restrict__ pairs = S.pairs;
     EraRec* era = S.era;
     SubjRec* subj = S.subj;
@@ -590,7 +625,12 @@ __device__ __forceinline__ void gh_compute(const ShardArgs& S, const Cached& C, 
                 if (q == ncached && p0 + q < p1 && ld_pair(pairs + p0 + q).y == s)
                     num = run_tail_numerator(pairs, era, p0 + q, p1, s, num);
             }
-            run_terms(num, H.den[v], H.n[v], gs, hs, err);
+            if constexpr (kSS) {
+                const int t = C.slot[v].pr.y - T.base;
+                run_terms(num, T.den[t], T.n[t], gs, hs, err);
+            } else {
+                run_terms(num, H.den[v], H.n[v], gs, hs, err);
+            }
         }
     }
     // streamed remainder: head threads own their runs
@@ -599,7 +639,13 @@ __device__ __forceinline__ void gh_compute(const ShardArgs& S, const Cached& C, 
         const PairSlot s = load_slot(pairs, p, p0, p1);
         if (s.head) {
             const Rec r = ld_rec(era + s.pr.x);
-            const Subj sr = ld_subj(subj + s.pr.y);
+            Subj sr;
+            if constexpr (kSS) {
+                sr.den = T.den[s.pr.y - T.base];
+                sr.n = T.n[s.pr.y - T.base];
+            } else {
+                sr = ld_subj(subj + s.pr.y);
+            }
             double num = lexp(r.len, r.xb);
             if (s.cont) num = run_tail_numerator(pairs, era, p + 1, p1, s.pr.y, num);
             run_terms(num, sr.den, sr.n, gs, hs, err);
@@ -607,9 +653,10 @@ __device__ __forceinline__ void gh_compute(const ShardArgs& S, const Cached& C, 
     }
 }
 
+template <bool kSS>
 __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C, const HeadRegs& H, bool cached,
                                              int64_t p0, int64_t p1, double d, int& err, double& errv, Smem& sm,
-                                             bool record = false, int* myht = nullptr) {
+                                             const SubjTile& T, bool record = false, int* myht = nullptr) {
     const int2* __restrict__ pairs = S.pairs;
     EraRec* era = S.era;
     SubjRec* subj = S.subj;
@@ -646,16 +693,17 @@ __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C
             if (C.slot[v].head) {
                 const int pos = slot_pos(v);
                 int q = pos;
-                double den = __dadd_rn(H.den[v], sm.stage[q++]);
+                double den = __dadd_rn(kSS ? T.den[C.slot[v].pr.y - T.base] : H.den[v], sm.stage[q++]);
                 if (C.slot[v].cont) {
                     const int s = C.slot[v].pr.y;
                     while (q < ncached && sm.ssub[q] == s) den = __dadd_rn(den, sm.stage[q++]);
                     if (q == ncached && p0 + q < p1 && ld_pair(pairs + p0 + q).y == s)
                         den = run_tail_update(pairs, era, p0 + q, p1, s, d, den, err, errv);
                 }
-                subj[C.slot[v].pr.y].den = den;
+                if constexpr (kSS) T.den[C.slot[v].pr.y - T.base] = den;
+                else subj[C.slot[v].pr.y].den = den;
                 if (record) { // publish (subject -> run) for the next coordinate's repair
-                    sm.jden[pos] = den;
+                    if constexpr (!kSS) sm.jden[pos] = den;
                     const int s = C.slot[v].pr.y;
                     int h = ht_hash(s);
                     while (atomicCAS(&sm.htk[h], -1, s) != -1) h = (h + 1) & (kHt - 1);
@@ -671,10 +719,11 @@ __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C
         const PairSlot s = load_slot(pairs, p, p0, p1);
         if (s.head) {
             const Rec r = ld_rec(era + s.pr.x);
-            double den = subj[s.pr.y].den;
+            double den = kSS ? T.den[s.pr.y - T.base] : subj[s.pr.y].den;
             den = update_era(era, s.pr.x, r.xb, lexp(r.len, r.xb), r.len, d, den, err, errv);
             if (s.cont) den = run_tail_update(pairs, era, p + 1, p1, s.pr.y, d, den, err, errv);
-            subj[s.pr.y].den = den;
+            if constexpr (kSS) T.den[s.pr.y - T.base] = den;
+            else subj[s.pr.y].den = den;
         }
     }
 }
@@ -690,9 +739,13 @@ __device__ __forceinline__ bool any_slot(const Cached& C) {
 
 enum StepStatus { ST_OK = 0, ST_REMOTE_ERR = 1, ST_STEP_ERR = 2, ST_NONFINITE = 3 };
 
+constexpr size_t kSmemSubjOffset = (sizeof(Smem) + 15) / 16 * 16;
+
+template <bool kSS>
 __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant__ SweepArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+    SubjTile T{nullptr, nullptr, 0};
     int si = 0;
     while (si + 1 < A.nsh && static_cast<int>(blockIdx.x) >= A.sh[si + 1].cta_begin) ++si;
     const ShardArgs& S = A.sh[si];
@@ -710,7 +763,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
     if (A.mode == kModeUpdate) {
         const int j = A.single_j;
         const int64_t p0 = split_c[static_cast<int64_t>(j) * stride], p1 = split_c[static_cast<int64_t>(j) * stride + 1];
-        update_slice(S, C, H, false, p0, p1, A.single_delta, err, errv, sm);
+        update_slice<false>(S, C, H, false, p0, p1, A.single_delta, err, errv, sm, T);
         if (err) record_error(S.err, err, errv);
         if (c == 0 && threadIdx.x == 0) S.beta[j] = __dadd_rn(S.beta[j], A.single_delta);
         return;
@@ -741,8 +794,8 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         const int64_t p0 = split_c[static_cast<int64_t>(j) * stride], p1 = split_c[static_cast<int64_t>(j) * stride + 1];
         load_cached(S, p0, p1, C);
         double gs = 0.0, hs = 0.0;
-        gather_records(S, C, H);
-        gh_compute(S, C, p0, p1, H, gs, hs, err, sm);
+        gather_records<false>(S, C, H);
+        gh_compute<false>(S, C, p0, p1, H, gs, hs, err, sm, T);
         if (err) record_error(S.err, err, 0.0);
         block_reduce(gs, hs, err, false, sm);
         publish(A, seq, gs, hs, err);
@@ -777,6 +830,17 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
     const bool w0 = threadIdx.x < 32;
     if (V > 0) {
         for (int i = threadIdx.x; i < kHt; i += kT) sm.htk[i] = -1;
+        if constexpr (kSS) {
+            T.base = S.cta_subj[c];
+            const int ns = S.cta_subj[c + 1] - T.base;
+            T.den = reinterpret_cast<double*>(smem_raw + kSmemSubjOffset);
+            T.n = reinterpret_cast<int*>(T.den + A.ss_cap);
+            for (int t = threadIdx.x; t < ns; t += kT) {
+                const Subj sr = ld_subj(S.subj + T.base + t);
+                T.den[t] = sr.den;
+                T.n[t] = sr.n;
+            }
+        }
         const longlong2 z2 = make_longlong2(0, 0);
         longlong2 cur = vs[0];
         int j = A.visit[0];
@@ -811,12 +875,12 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                 if (!idle) {
                     if (spec) {
                         if (A.dbg & 64) finish_records(C, H);
-                        repair(C, H, sm);
+                        repair<kSS>(C, H, sm);
                     } else {
-                        gather_records(S, C, H);
+                        gather_records<kSS>(S, C, H);
                     }
                 }
-                gh_compute(S, C, p0, p1, H, gs, hs, err, sm);
+                gh_compute<kSS>(S, C, p0, p1, H, gs, hs, err, sm, T);
             }
             if (err) record_error(S.err, err, errv);
             // The publish below must not be observable before this
@@ -841,9 +905,13 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             const bool more = idx + 1 < V;
             const bool spec_next = more && !(A.dbg & 16) && (p1 - p0) <= kCap && (nxt.y - nxt.x) <= kCap;
             if (spec_next) {
-                if (A.dbg & 64) issue_records(S, N, SH);
-                else gather_records(S, N, SH);
+                if (A.dbg & 64) issue_records<kSS>(S, N, SH);
+                else gather_records<kSS>(S, N, SH);
             }
+            // ... and, once idx+2's pairs have landed, its records into L2, so
+            // the speculative gathers of the next window hit L2, not HBM
+            if (A.prefetch && more && (nxt.y - nxt.x) <= kCap && (nxt2.y - nxt2.x) <= kCap)
+                prefetch_records<kSS>(S, NR);
             const longlong2 nxt3 = idx + 3 < V ? vs[idx + 3] : z2;
             int jn2 = 0;
             double bn = 0.0, rn = 1.0, yn = 0.0;
@@ -909,7 +977,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             ++nvisit;
             if (delta != 0.0) {
                 ++nmoved;
-                if (!(A.dbg & 2)) update_slice(S, C, H, true, p0, p1, delta, err, errv, sm, spec_next, myht);
+                if (!(A.dbg & 2)) update_slice<kSS>(S, C, H, true, p0, p1, delta, err, errv, sm, T, spec_next, myht);
             }
             __syncthreads(); // slice writes of this coordinate before the next reads
             if (tr && idx < A.ntrace) trb[idx * trs + 3] = gtimer();
@@ -925,6 +993,10 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             bj = bn;
             rj = rn;
             ydx = yn;
+        }
+        if constexpr (kSS) { // the cycle's denominators back to HBM (ordered by the loop's last barrier)
+            const int ns = S.cta_subj[c + 1] - T.base;
+            for (int t = threadIdx.x; t < ns; t += kT) S.subj[T.base + t].den = T.den[t];
         }
     }
 
@@ -1486,10 +1558,14 @@ void throw_device_error(int code, double value) {
     }
 }
 
+constexpr int kMaxSweepSmem = 225 * 1024; // opt-in dynamic shared memory per CTA (227 KB less static use)
+
 void ensure_kernel_attrs(int device) {
     static std::atomic<unsigned> done{0};
     if (device < 32 && (done.load() & (1u << device))) return;
-    CUDA_TRY(cudaFuncSetAttribute(k_ccd, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(Smem))));
+    CUDA_TRY(cudaFuncSetAttribute(k_ccd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sizeof(Smem))));
+    CUDA_TRY(cudaFuncSetAttribute(k_ccd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSweepSmem));
     if (device < 32) done.fetch_or(1u << device);
 }
 
@@ -1497,7 +1573,7 @@ int default_ctas(int device) {
     // one persistent CTA per SM (launch bounds force 1 resident CTA of 512)
     ensure_kernel_attrs(device);
     int per_sm = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ccd, kSweepThreads, sizeof(Smem)));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ccd<false>, kSweepThreads, sizeof(Smem)));
     if (per_sm < 1) internal_error("sweep kernel cannot be resident");
     return sm_count(device);
 }
@@ -1621,6 +1697,12 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
 
     ds->col_runs_h.resize(static_cast<size_t>(J));
     CUDA_TRY(cudaMemcpy(ds->col_runs_h.data(), ds->col_runs, sizeof(int32_t) * J, cudaMemcpyDeviceToHost));
+    {
+        std::vector<int32_t> cs(static_cast<size_t>(C) + 1);
+        CUDA_TRY(cudaMemcpy(cs.data(), ds->cta_subj, sizeof(int32_t) * (C + 1), cudaMemcpyDeviceToHost));
+        ds->max_cta_subjects = 0;
+        for (int c = 0; c < C; ++c) ds->max_cta_subjects = std::max(ds->max_cta_subjects, cs[c + 1] - cs[c]);
+    }
     ds->col_nonempty_h.resize(static_cast<size_t>(J));
     for (int32_t j = 0; j < J; ++j) {
         const int64_t cnt =
@@ -1912,12 +1994,58 @@ int plan_ctas(const ExchangePlan& plan) {
     return n;
 }
 
+// Sweeps keep each CTA's subject records in shared memory when every
+// shard's largest CTA subject range fits (BSCCS_SUBJ_SMEM=0 disables it).
+int subject_tile_cap(const ExchangePlan& plan) {
+    static const bool enabled = [] {
+        const char* e = std::getenv("BSCCS_SUBJ_SMEM");
+        return !(e && e[0] == '0');
+    }();
+    if (!enabled) return 0;
+    int m = 0;
+    for (auto* st : plan.shards) m = std::max(m, st->ds->max_cta_subjects);
+    const int cap = (m + 1) / 2 * 2; // keeps the int array 8-byte aligned
+    const size_t bytes = kSmemSubjOffset + static_cast<size_t>(cap) * (sizeof(double) + sizeof(int));
+    return bytes <= static_cast<size_t>(kMaxSweepSmem) ? std::max(cap, 2) : 0;
+}
+
+// The L2 prefetch of the records two coordinates ahead pays while the
+// slices are small: measured -3% fit time at ~200 pairs per CTA per
+// coordinate (config 2), +4% at ~740 (config 3), where the extra line
+// fetches compete with the gathers.  BSCCS_PREFETCH=0/1 forces it.
+int prefetch_enabled(const ExchangePlan& plan) {
+    static const int forced = [] {
+        const char* e = std::getenv("BSCCS_PREFETCH");
+        return e ? (e[0] == '0' ? 0 : 1) : -1;
+    }();
+    if (forced >= 0) return forced;
+    int64_t nnz = 0, ctas = 0;
+    for (auto* st : plan.shards) {
+        nnz += st->ds->nnz;
+        ctas += st->ds->ctas;
+    }
+    const bsccs_dataset* ds = plan.shards[0]->ds;
+    int64_t cols = 0;
+    for (uint8_t nz : ds->col_nonempty_h) cols += nz ? 1 : 0;
+    if (cols == 0 || ctas == 0) return 0;
+    const double per_cta = static_cast<double>(nnz) / static_cast<double>(cols) / static_cast<double>(ctas);
+    return per_cta <= 384.0 ? 1 : 0;
+}
+
 void launch_ccd(const ExchangePlan& plan, SweepArgs& a) {
     bsccs_state* s0 = plan.shards[0];
     ensure_kernel_attrs(s0->ds->device);
+    a.ss_cap = a.mode == kModeSweep ? subject_tile_cap(plan) : 0;
+    a.prefetch = a.mode == kModeSweep ? prefetch_enabled(plan) : 0;
     void* params[] = {&a};
-    CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_ccd), dim3(plan_ctas(plan)), dim3(kSweepThreads),
-                                         params, sizeof(Smem), s0->stream));
+    if (a.ss_cap > 0) {
+        const size_t bytes = kSmemSubjOffset + static_cast<size_t>(a.ss_cap) * (sizeof(double) + sizeof(int));
+        CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_ccd<true>), dim3(plan_ctas(plan)),
+                                             dim3(kSweepThreads), params, bytes, s0->stream));
+    } else {
+        CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_ccd<false>), dim3(plan_ctas(plan)),
+                                             dim3(kSweepThreads), params, sizeof(Smem), s0->stream));
+    }
     count_launches(1);
 }
 

@@ -97,6 +97,7 @@ struct bsccs_dataset {
     double* y_dot_x = nullptr;        // [J] global y_dot_x as double
     uint8_t* col_nonempty = nullptr;  // [J] global
     int32_t* col_runs = nullptr;      // [J] subject runs per column (this shard)
+    int32_t max_cta_subjects = 0;     // largest CTA subject range (sizes the shared-memory subject tile)
     // host copies of small metadata
     std::vector<int64_t> col_ptr_h;
     std::vector<uint8_t> col_nonempty_h;
