@@ -165,8 +165,9 @@ struct BSmem {
     unsigned live;
     // warp 0 lane r: fit r's coordinate scalars and counters (kept out of
     // the registers of every thread)
-    double bj[2][RB], rj[2][RB], yj[2][RB], abytes[RB]; // [coordinate parity][fit]
+    double bj[2][RB], rj[2][RB], yj[2][RB], bv[2][RB], abytes[RB]; // [coordinate parity][fit]
     int nz[2][RB];
+    double nzj[2], uj[2]; // column nnz and subject runs (byte accounting)
     long long nvis[RB], nmov[RB];
     int2 pst[2][BCfg<RB>::kCapP];         // pairs of this / the next coordinate's slice
     double le[BCfg<RB>::kCapP * RB];      // l*exp per slot (then the update's differences)
@@ -299,9 +300,14 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
         if (threadIdx.x < RB) {
             const size_t o = static_cast<size_t>(A.visit[0]) * RB + threadIdx.x;
             sm.bj[0][threadIdx.x] = A.beta[o];
+            sm.bv[0][threadIdx.x] = beta_over_v(A.prior[threadIdx.x], sm.bj[0][threadIdx.x]);
             sm.rj[0][threadIdx.x] = A.trust[o];
             sm.yj[0][threadIdx.x] = A.ydx[o];
             sm.nz[0][threadIdx.x] = A.colnz[o];
+        } else if (threadIdx.x == RB) {
+            const int j0 = A.visit[0];
+            sm.nzj[0] = static_cast<double>(A.col_ptr[j0 + 1] - A.col_ptr[j0]);
+            sm.uj[0] = static_cast<double>(A.col_runs[j0]);
         }
     }
     __syncthreads();
@@ -494,7 +500,7 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
                         const double g = __dsub_rn(sm.yj[cur][r], tg);
                         const double h = th == 0.0 ? 0.0 : -th;
                         double step = 0.0;
-                        const int serr = penalized_step(A.prior[r], bj, g, h, &step);
+                        const int serr = penalized_step_pre(A.prior[r], bj, sm.bv[cur][r], g, h, &step);
                         if (serr) {
                             st = serr;
                             if (c == 0) {
@@ -512,8 +518,7 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
                                 }
                             } else {
                                 ++sm.nvis[r];
-                                const double nzj = static_cast<double>(A.col_ptr[j + 1] - A.col_ptr[j]);
-                                const double uj = static_cast<double>(A.col_runs[j]);
+                                const double nzj = sm.nzj[cur], uj = sm.uj[cur];
                                 double ab = 8.0 * nzj + 12.0 * uj; // x'beta gathers; den, m per run
                                 if (delta != 0.0) {
                                     ++sm.nmov[r];
@@ -539,10 +544,16 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
             const int tt = static_cast<int>(threadIdx.x) - Cf::kPollThreads;
             if (tt < RB) {
                 const size_t o = static_cast<size_t>(A.visit[idx + 1]) * RB + tt;
-                sm.bj[cur ^ 1][tt] = A.beta[o];
+                const double b1 = A.beta[o];
+                sm.bj[cur ^ 1][tt] = b1;
+                sm.bv[cur ^ 1][tt] = beta_over_v(A.prior[tt], b1);
                 sm.rj[cur ^ 1][tt] = A.trust[o];
                 sm.yj[cur ^ 1][tt] = A.ydx[o];
                 sm.nz[cur ^ 1][tt] = A.colnz[o];
+            } else if (tt == RB) {
+                const int j1 = A.visit[idx + 1];
+                sm.nzj[cur ^ 1] = static_cast<double>(A.col_ptr[j1 + 1] - A.col_ptr[j1]);
+                sm.uj[cur ^ 1] = static_cast<double>(A.col_runs[j1]);
             }
             // ... and the next slice's pairs
             const longlong2 nsl = vs[idx + 1];
