@@ -123,7 +123,8 @@ struct SweepArgs {
     int ntrace;
 };
 
-constexpr int kTr = 6; // stamps: top, pre-publish, gather done, update done, post-issue, poll done
+constexpr int kTr = 8; // stamps: top, pre-publish, gather done, update done, post-issue, poll done,
+                       // data warp at the step barrier, step computed (warp 0)
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -346,9 +347,11 @@ __device__ __forceinline__ RawSlot issue_slot(const int2* __restrict__ pairs, in
     r.pr = valid ? ld_pair(pairs + p) : make_int2(-1, -1);
     r.first = valid && p == p0;
     r.last_valid = p + 1 < p1;
+    // one load instruction for both edge lanes (two would serialise the
+    // warp on the shared destination register)
     r.edge = -1;
-    if (l == 0 && valid && p > p0) r.edge = ld_pair(pairs + p - 1).y;
-    if (l == 31 && p + 1 < p1) r.edge = ld_pair(pairs + p + 1).y;
+    const bool lo = l == 0 && valid && p > p0, hi = l == 31 && p + 1 < p1;
+    if (lo || hi) r.edge = ld_pair(pairs + (lo ? p - 1 : p + 1)).y;
     return r;
 }
 
@@ -863,6 +866,8 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         for (int v = 0; v < kCached; ++v) myht[v] = -1;
         __syncthreads(); // hash table initialised
         const bool tr = A.trace != nullptr && threadIdx.x == 0;
+        const bool trd = A.trace != nullptr && threadIdx.x == 32;
+        unsigned long long* trbd = trd ? A.trace + static_cast<size_t>(blockIdx.x) * kTr : nullptr;
         unsigned long long* trb = tr ? A.trace + static_cast<size_t>(blockIdx.x) * kTr : nullptr;
         const size_t trs = static_cast<size_t>(gridDim.x) * kTr;
         for (int idx = 0; idx < V; ++idx) {
@@ -901,13 +906,13 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             if (!(A.dbg & 4)) publish(A, seq, gs, hs, e);
             // while the partials travel
             RawCached NR;
-            issue_cached(S, nxt2.x, nxt2.y, NR);
+            // the speculative gathers go out first (they are on the critical
+            // path), then idx+2's pairs, then the gathers are consumed
             const bool more = idx + 1 < V;
             const bool spec_next = more && !(A.dbg & 16) && (p1 - p0) <= kCap && (nxt.y - nxt.x) <= kCap;
-            if (spec_next) {
-                if (A.dbg & 64) issue_records<kSS>(S, N, SH);
-                else gather_records<kSS>(S, N, SH);
-            }
+            if (spec_next) issue_records<kSS>(S, N, SH);
+            issue_cached(S, nxt2.x, nxt2.y, NR);
+            if (spec_next && !(A.dbg & 64)) finish_records(N, SH);
             // ... and, once idx+2's pairs have landed, its records into L2, so
             // the speculative gathers of the next window hit L2, not HBM
             if (A.prefetch && more && (nxt.y - nxt.x) <= kCap && (nxt2.y - nxt2.x) <= kCap)
@@ -965,6 +970,14 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                 }
             }
             if (!(A.dbg & 4)) ++seq;
+            if (tr && idx < A.ntrace) trb[idx * trs + 7] = gtimer();
+            if (trd && idx < A.ntrace) {
+                // the stamp waits for the window's speculative gathers
+                double dep = 0.0;
+#pragma unroll
+                for (int v = 0; v < kCached; ++v) dep += slot_valid(N.slot[v]) ? SH.le[v] : 0.0;
+                trbd[idx * trs + 6] = gtimer() + (dep == 1.2345 ? 1 : 0);
+            }
             __syncthreads();
             if (tr && idx < A.ntrace) trb[idx * trs + 2] = gtimer();
             const int status = sm.status;

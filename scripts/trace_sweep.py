@@ -22,11 +22,11 @@ B.run_cycle(dds, st, solver, prior, cfg)  # warm
 lib.bsccs_debug_set_sweep_flags(flags)
 lib.bsccs_debug_trace(NT, ctas, None, 0)
 B.run_cycle(dds, st, solver, prior, cfg)
-buf = np.zeros(NT * ctas * 6, dtype=np.uint64)
+buf = np.zeros(NT * ctas * 8, dtype=np.uint64)
 lib.bsccs_debug_trace(NT, ctas, buf.ctypes.data_as(C.c_void_p), buf.size)
 lib.bsccs_debug_trace(0, ctas, None, 0)
 lib.bsccs_debug_set_sweep_flags(0)
-t = buf.reshape(NT, ctas, 6).astype(np.int64)
+t = buf.reshape(NT, ctas, 8).astype(np.int64)
 t = t[20:NT - 1]  # skip the start
 t0 = t[:, :, 0]
 pub = t[:, :, 1]
@@ -58,3 +58,9 @@ slow = np.argmax(pub, axis=1)
 vals, cnt = np.unique(slow, return_counts=True)
 order = np.argsort(-cnt)[:8]
 print("  most frequent last publisher CTAs:", [(int(vals[i]), int(cnt[i])) for i in order])
+dat = t[:, :, 6]
+stp = t[:, :, 7]
+print(f"  poll done -> step computed (warp 0): median {np.median(stp - poll):.0f}")
+print(f"  poll done -> data warp 1 at barrier: median {np.median(dat - poll):.0f}  "
+      f"(publish -> data warp at barrier {np.median(dat - pub):.0f})")
+print(f"  data warp at barrier -> released: median {np.median(got - dat):.0f}")
