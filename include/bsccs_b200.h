@@ -110,6 +110,14 @@ void bsccs_debug_set_sweep_flags(int32_t flags);
 /* Profiling hook: host_out == NULL arms per-CTA globaltimer stamps for the
  * first ncoords coordinates of later sweeps; otherwise copies them out. */
 int32_t bsccs_debug_trace(int32_t ncoords, int32_t ctas, uint64_t* host_out, int64_t words);
+/* Self-test of the exact all-reduce encoding, not a
+ * reference entry point: n (<= 2048) partials in [0, 2^43) are split into
+ * limbs and added into one set of exchange words on `device` exactly as n
+ * participants would; *sum receives the reconstructed total and *status
+ * 0 = ok, 1 = a partial out of range, 2 = total out of range, 3 = the
+ * arrival count did not read n. */
+bsccs_status bsccs_debug_exchange_sum(int32_t device, const double* partials, int32_t n, double* sum,
+                                      int32_t* status);
 
 /* ---- dataset (dataset.hpp:53-68 Dataset / SparseColumn) ---------------
  * Flat CSC form of bsccs::Dataset: column j's pairs are

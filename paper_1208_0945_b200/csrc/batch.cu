@@ -194,8 +194,8 @@ __device__ __forceinline__ void bexchange(const BatchArgs& A, BSmem<RB>& sm, uns
         } else {
             const int e0 = (w - 6 * RB) * 6;
             for (int f = e0; f < e0 + 6 && f < RB; ++f) {
-                const bool bad = sm.re[f] != 0 || !(sm.ra[f] >= 0.0 && sm.ra[f] < 0x1p46) ||
-                                 !(sm.rb[f] >= 0.0 && sm.rb[f] < 0x1p46);
+                const bool bad = sm.re[f] != 0 || !(sm.ra[f] >= 0.0 && sm.ra[f] < kXMaxValue) ||
+                                 !(sm.rb[f] >= 0.0 && sm.rb[f] < kXMaxValue);
                 if (bad) v += 1ull << (8 * (f - e0));
             }
         }
@@ -205,7 +205,7 @@ __device__ __forceinline__ void bexchange(const BatchArgs& A, BSmem<RB>& sm, uns
         do {
             x = ld_poll(p);
             diff = x - prev;
-        } while ((diff >> 50) < static_cast<unsigned long long>(A.ctas));
+        } while ((diff >> kXCntShift) < static_cast<unsigned long long>(A.ctas));
         sm.pv[buf][w] = x;
         sm.xd[w] = diff & kXData;
     }
@@ -495,12 +495,14 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
                     if (berr_count<RB>(sm, r) != 0) {
                         st = -1; // an error seen by some CTA (recorded there)
                     } else {
-                        const double tg = from_limbs(sm.xd[6 * r], sm.xd[6 * r + 1], sm.xd[6 * r + 2]);
-                        const double th = from_limbs(sm.xd[6 * r + 3], sm.xd[6 * r + 4], sm.xd[6 * r + 5]);
+                        bool o1, o2;
+                        const double tg = from_limbs(sm.xd[6 * r], sm.xd[6 * r + 1], sm.xd[6 * r + 2], o1);
+                        const double th = from_limbs(sm.xd[6 * r + 3], sm.xd[6 * r + 4], sm.xd[6 * r + 5], o2);
                         const double g = __dsub_rn(sm.yj[cur][r], tg);
                         const double h = th == 0.0 ? 0.0 : -th;
                         double step = 0.0;
-                        const int serr = penalized_step_pre(A.prior[r], bj, sm.bv[cur][r], g, h, &step);
+                        const int serr = (o1 || o2) ? DERR_SUM_RANGE
+                                                    : penalized_step_pre(A.prior[r], bj, sm.bv[cur][r], g, h, &step);
                         if (serr) {
                             st = serr;
                             if (c == 0) {
@@ -732,8 +734,10 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
         if (w0) {
             const int r = threadIdx.x;
             if (r < RB && c == 0) {
-                const double tch = from_limbs(sm.xd[6 * r], sm.xd[6 * r + 1], sm.xd[6 * r + 2]);
-                const double tmg = from_limbs(sm.xd[6 * r + 3], sm.xd[6 * r + 4], sm.xd[6 * r + 5]);
+                bool o1, o2;
+                const double tch = from_limbs(sm.xd[6 * r], sm.xd[6 * r + 1], sm.xd[6 * r + 2], o1);
+                const double tmg = from_limbs(sm.xd[6 * r + 3], sm.xd[6 * r + 4], sm.xd[6 * r + 5], o2);
+                if ((o1 || o2) && ((live >> r) & 1u)) atomicCAS(&A.fit_err[r], 0, DERR_SUM_RANGE);
                 A.crit[r] = A.normalized ? tch / (1.0 + tmg) : tch;
                 A.crit[RB + r] = tch;
                 A.crit[2 * RB + r] = tmg;

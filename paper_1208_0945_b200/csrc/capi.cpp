@@ -297,6 +297,14 @@ int32_t bsccs_debug_trace(int32_t ncoords, int32_t ctas, uint64_t* host_out, int
     });
 }
 
+bsccs_status bsccs_debug_exchange_sum(int32_t device, const double* partials, int32_t n, double* sum,
+                                      int32_t* status) {
+    return guard([&] {
+        if (!partials || !sum || !status || n < 1 || n > 2048) input_error("debug_exchange_sum: bad arguments");
+        debug_exchange_sum(device, partials, n, sum, status);
+    });
+}
+
 bsccs_status bsccs_device_info(int32_t device, int32_t* sms, int32_t* ctas) {
     return guard([&] {
         int n = 0;

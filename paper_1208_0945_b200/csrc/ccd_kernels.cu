@@ -223,12 +223,12 @@ __device__ __forceinline__ void block_reduce(double& a, double& b, int& e, bool 
 
 // ---- order-independent exchange -------------------------------------------------
 //
-// Each participant splits its partial exactly into three 42-bit limbs of a
+// Each participant splits its partial exactly into three 41-bit limbs of a
 // 2^-80 fixed-point number and issues seven relaxed red.add.u64 (six limbs
 // plus an error word) into the exchange area of every destination; each word
-// also gains 2^50 per arrival.  A poller knows a word is complete when its
+// also gains 2^52 per arrival.  A poller knows a word is complete when its
 // growth since the previous use of that buffer carries P arrivals in the
-// bits above 2^50 -- every word validates itself, no fences or flags.  The
+// bits above 2^52 -- every word validates itself, no fences or flags.  The
 // integer sum is associative, so every CTA reconstructs the bit-identical,
 // correctly rounded exact sum of the partials whatever the arrival order.
 // Words sit 256 B apart so the adds land on distinct L2 slices; two buffers
@@ -245,7 +245,7 @@ __device__ __forceinline__ void publish(const SweepArgs& A, unsigned long long s
     if (l < 3) ok = limb_of(a, l, w);
     else if (l < 6) ok = limb_of(b, l - 3, w);
     else w = 0;
-    const bool okab = __all_sync(0x7fu, ok) && (0.0 <= a && a < 0x1p46 && 0.0 <= b && b < 0x1p46);
+    const bool okab = __all_sync(0x7fu, ok) && (0.0 <= a && a < kXMaxValue && 0.0 <= b && b < kXMaxValue);
     if (l == 6) w = (e || !okab) ? 1ull : 0ull;
     w += kXCnt;
     const size_t off = static_cast<size_t>(seq & 1ull) * kXWords * kXStride + static_cast<size_t>(l) * kXStride;
@@ -291,7 +291,7 @@ __device__ __forceinline__ void poll(const SweepArgs& A, const unsigned long lon
         do {
             v = ld_poll(p);
             diff = v - prev;
-        } while ((diff >> 50) < static_cast<unsigned long long>(A.P));
+        } while ((diff >> kXCntShift) < static_cast<unsigned long long>(A.P));
         if (buf) pv.b1 = v;
         else pv.b0 = v;
     }
@@ -301,10 +301,13 @@ __device__ __forceinline__ void poll(const SweepArgs& A, const unsigned long lon
     // lane 0 rebuilds a from lanes 0..2, lane 3 rebuilds b from lanes 3..5
     const unsigned long long d1 = __shfl_down_sync(0xffffffffu, d, 1);
     const unsigned long long d2 = __shfl_down_sync(0xffffffffu, d, 2);
-    const double v = from_limbs(d, d1, d2);
+    bool ovf;
+    const double v = from_limbs(d, d1, d2, ovf);
     ta = __shfl_sync(0xffffffffu, v, 0);
     tb = __shfl_sync(0xffffffffu, v, 3);
-    te = __shfl_sync(0xffffffffu, d, 6) != 0 ? 1 : 0;
+    const unsigned bad = __ballot_sync(0xffffffffu, ovf) & 0x9u; // lanes 0 (a) and 3 (b)
+    te = (__shfl_sync(0xffffffffu, d, 6) != 0 || bad) ? 1 : 0;
+    if (bad && l == 0) record_error(A.sh[0].err, DERR_SUM_RANGE, 0.0);
 }
 
 // ---- shared-memory subject tile -----------------------------------------------------
@@ -1565,6 +1568,8 @@ void throw_device_error(int code, double value) {
         internal_error("penalized_step: positive likelihood curvature");
     case DERR_LL_DEN_NONPOSITIVE:
         internal_error("log_likelihood: nonpositive subject denominator");
+    case DERR_SUM_RANGE:
+        numeric_error("exact all-reduce: a partial sum outside [0, 2^43) or a total at or above 2^48");
     default:
         std::snprintf(buf, sizeof buf, "device error code %d", code);
         internal_error(buf);
@@ -1997,7 +2002,7 @@ SweepArgs base_args(const ExchangePlan& plan) {
     a.slots = plan.local_slots;
     a.P = plan.total_participants;
     a.counter = plan.counter;
-    if (a.P >= (1 << 13)) internal_error("exchange plan: too many participants");
+    if (a.P > kMaxParticipants) internal_error("exchange plan: too many participants (limit 2048 CTAs over all ranks)");
     return a;
 }
 
@@ -2163,6 +2168,62 @@ unsigned long long* g_trace = nullptr;
 int g_ntrace = 0;
 size_t g_trace_words = 0;
 }
+namespace {
+// n participants, one per thread: limbs + one arrival each into three words
+// (the publish of §4.2), then thread 0 checks the count and reconstructs
+__global__ void k_xsum_test(const double* v, int n, unsigned long long* words, double* out, int* status) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        bool ok = true;
+        for (int l = 0; l < 3; ++l) {
+            unsigned long long w;
+            ok = limb_of(v[i], l, w) && ok;
+            red_add(words + l, w + kXCnt);
+        }
+        if (!ok) atomicOr(status, 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned long long w0 = ld_poll(words), w1 = ld_poll(words + 1), w2 = ld_poll(words + 2);
+        if ((w0 >> kXCntShift) != static_cast<unsigned long long>(n) || (w1 >> kXCntShift) != (w0 >> kXCntShift) ||
+            (w2 >> kXCntShift) != (w0 >> kXCntShift))
+            atomicOr(status, 4);
+        bool ovf;
+        *out = from_limbs(w0 & kXData, w1 & kXData, w2 & kXData, ovf);
+        if (ovf) atomicOr(status, 2);
+    }
+}
+} // namespace
+
+void debug_exchange_sum(int device, const double* partials, int n, double* sum, int* status) {
+    DeviceGuard g(device);
+    cudaStream_t s = nullptr;
+    CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    double* dv = nullptr;
+    unsigned long long* dw = nullptr;
+    double* dout = nullptr;
+    int* dst = nullptr;
+    CUDA_TRY(cudaMalloc(&dv, sizeof(double) * n));
+    CUDA_TRY(cudaMalloc(&dw, sizeof(unsigned long long) * 3));
+    CUDA_TRY(cudaMalloc(&dout, sizeof(double)));
+    CUDA_TRY(cudaMalloc(&dst, sizeof(int)));
+    CUDA_TRY(cudaMemcpyAsync(dv, partials, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemsetAsync(dw, 0, sizeof(unsigned long long) * 3, s));
+    CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(int), s));
+    k_xsum_test<<<1, 1024, 0, s>>>(dv, n, dw, dout, dst);
+    count_launches(1);
+    int st = 0;
+    CUDA_TRY(cudaMemcpyAsync(sum, dout, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(&st, dst, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    CUDA_TRY(cudaGetLastError());
+    cudaFree(dv);
+    cudaFree(dw);
+    cudaFree(dout);
+    cudaFree(dst);
+    cudaStreamDestroy(s);
+    *status = (st & 1) ? 1 : (st & 2) ? 2 : (st & 4) ? 3 : 0;
+}
+
 void set_debug_flags(int f) { g_debug_flags = f; }
 void set_debug_trace(int ncoords, int ctas) {
     if (g_trace) cudaFree(g_trace);

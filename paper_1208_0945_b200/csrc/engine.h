@@ -215,6 +215,7 @@ void prepare_snapshot(bsccs_state* st);
 void set_debug_flags(int flags); // profiling only
 void set_debug_trace(int ncoords, int ctas);
 void read_debug_trace(unsigned long long* host, size_t words);
+void debug_exchange_sum(int device, const double* partials, int n, double* sum, int* status);
 unsigned long long* debug_trace_buffer(int* ncoords); // profiling only
 void throw_device_error(int code, double value);
 

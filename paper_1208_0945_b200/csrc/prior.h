@@ -29,7 +29,8 @@ enum DevError {
     DERR_STEP_NONFINITE = 3,    // numeric_error  engine.hpp:210-212
     DERR_FLAT_NO_PRIOR = 4,     // numeric_error  prior.hpp:77-86
     DERR_POS_CURVATURE = 5,     // internal_error prior.hpp:73-75
-    DERR_LL_DEN_NONPOSITIVE = 6 // internal_error engine.hpp:418-420
+    DERR_LL_DEN_NONPOSITIVE = 6, // internal_error engine.hpp:418-420
+    DERR_SUM_RANGE = 7           // exact exchange: a partial >= 2^43 or a total >= 2^48 (xchg.cuh)
 };
 
 struct PriorParams {

@@ -1,8 +1,13 @@
 // xchg.cuh -- device helpers of the order-independent exact all-reduce
 // shared by the single-fit sweep (ccd_kernels.cu) and the batched engine
 // (batch.cu): relaxed red.add / volatile poll words and the exact split of
-// a non-negative double into three 42-bit limbs of a 2^-80 fixed-point
+// a non-negative double into three 41-bit limbs of a 2^-80 fixed-point
 // number (and the correctly rounded reconstruction).  See DESIGN.md §4.2.
+//
+// Word layout: bits 0..51 carry the sum of the participants' limbs, bits
+// 52..63 count arrivals.  A limb is < 2^41, so up to kMaxParticipants =
+// 2^11 arrivals can never carry into the count (2^11 * (2^41 - 1) < 2^52),
+// and the 12-bit count holds 2^11 arrivals per use of a buffer.
 #pragma once
 
 #include <cstdint>
@@ -23,29 +28,36 @@ __device__ __forceinline__ unsigned long long ld_poll(const unsigned long long* 
     asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-constexpr unsigned long long kXCnt = 1ull << 50;
+constexpr int kXCntShift = 52;
+constexpr unsigned long long kXCnt = 1ull << kXCntShift;
 constexpr unsigned long long kXData = kXCnt - 1;
-constexpr unsigned long long kM42 = (1ull << 42) - 1;
+constexpr int kLimbBits = 41;
+constexpr unsigned long long kMLimb = (1ull << kLimbBits) - 1;
+constexpr int kMaxParticipants = 1 << 11;
+constexpr double kXMaxValue = 0x1p43; // partials must lie in [0, 2^43): 3 x 41 bits from 2^-80
+static_assert(static_cast<unsigned long long>(kMaxParticipants) * kMLimb < kXCnt, "limb sums must not reach the count");
+static_assert(kMaxParticipants < (1 << (64 - kXCntShift)), "the count field must hold kMaxParticipants arrivals");
 
-// limb i (0..2) of v in [0, 2^46) at 2^-80 resolution; false if out of range
+// limb i (0..2) of v in [0, 2^43) at 2^-80 resolution: v = L2*2^2 + L1*2^-39
+// + L0*2^-80 (bits below 2^-80 dropped); false if out of range
 __device__ __forceinline__ bool limb_of(double v, int i, unsigned long long& out) {
-    if (!(v >= 0.0 && v < 0x1p46)) {
+    if (!(v >= 0.0 && v < kXMaxValue)) {
         out = 0;
         return false;
     }
-    const double t2 = floor(__dmul_rn(v, 0x1p-4));
+    const double t2 = floor(__dmul_rn(v, 0x1p-2));
     if (i == 2) {
         out = static_cast<unsigned long long>(t2);
         return true;
     }
-    const double r = __dsub_rn(v, __dmul_rn(t2, 16.0)); // exact, [0, 16)
-    const double s1 = __dmul_rn(r, 0x1p38);
+    const double r = __dsub_rn(v, __dmul_rn(t2, 4.0)); // exact, [0, 4)
+    const double s1 = __dmul_rn(r, 0x1p39);
     const double t1 = floor(s1);
     if (i == 1) {
         out = static_cast<unsigned long long>(t1);
         return true;
     }
-    out = static_cast<unsigned long long>(floor(__dmul_rn(__dsub_rn(s1, t1), 0x1p42))); // exact below 2^-80
+    out = static_cast<unsigned long long>(floor(__dmul_rn(__dsub_rn(s1, t1), 0x1p41))); // exact below 2^-80
     return true;
 }
 
@@ -53,15 +65,20 @@ __device__ __forceinline__ double pow2(int e) { // 2^e for normal exponents
     return __longlong_as_double(static_cast<long long>(1023 + e) << 52);
 }
 
-// correctly rounded double of (L2*2^84 + L1*2^42 + L0) * 2^-80
-__device__ __forceinline__ double from_limbs(unsigned long long L0, unsigned long long L1, unsigned long long L2) {
-    L1 += L0 >> 42;
-    L0 &= kM42;
-    L2 += L1 >> 42;
-    L1 &= kM42;
+// correctly rounded double of (L2*2^82 + L1*2^41 + L0) * 2^-80, the limb
+// sums of up to kMaxParticipants partials; `ovf` is set (and 0 returned)
+// when the total reaches 2^48, beyond the 128-bit reconstruction
+__device__ __forceinline__ double from_limbs(unsigned long long L0, unsigned long long L1, unsigned long long L2,
+                                             bool& ovf) {
+    L1 += L0 >> kLimbBits;
+    L0 &= kMLimb;
+    L2 += L1 >> kLimbBits;
+    L1 &= kMLimb;
+    ovf = (L2 >> 46) != 0;
+    if (ovf) return 0.0;
     // 128-bit V = hi:lo
-    const unsigned long long lo = L0 | (L1 << 42);
-    const unsigned long long hi = (L1 >> 22) | (L2 << 20);
+    const unsigned long long lo = L0 | (L1 << kLimbBits);
+    const unsigned long long hi = (L1 >> (64 - kLimbBits)) | (L2 << (2 * kLimbBits - 64));
     if ((hi | lo) == 0) return 0.0;
     int lz;
     unsigned long long m, rest;
