@@ -5,7 +5,8 @@ import sys
 import tempfile
 sys.path[:0] = ['.', 'oracle']
 import numpy as np
-from paper_1208_0945_b200 import bootstrap as BT, bsccs as B, cross_validation as CV, datagen
+import ctypes as C
+from paper_1208_0945_b200 import _native, bootstrap as BT, bsccs as B, cross_validation as CV, datagen, sharding
 
 ds = datagen.fast_sccs(3000, 20, 3.0)
 dds = ds.on_device()
@@ -24,4 +25,11 @@ BT.run_bootstrap(ds, BT.BootstrapConfig(replicates=3, prior=B.normal_prior(0.1),
 with tempfile.NamedTemporaryFile("w", suffix=".tsv", delete=False) as f:
     f.write("p1\t5\t0\ta\np1\t5\t1\tb a\np2\t7\t1\tb\n")
 B.read_long_format(f.name)
+for virtual in (False, True):  # multi-shard launches: local and virtual-rank exchange
+    grp = sharding.LocalGroup(sharding.shard_dataset(ds, 3), virtual_ranks=virtual)
+    grp.fit(B.laplace_prior(0.1))
+    grp.close()
+vals = np.random.default_rng(1).uniform(0, 1e6, 1500)
+out, stc = C.c_double(), C.c_int32()
+_native.lib().bsccs_debug_exchange_sum(0, vals.ctypes.data_as(C.c_void_p), len(vals), C.byref(out), C.byref(stc))
 print("sanitize smoke done", r.cycles_run)
