@@ -144,6 +144,10 @@ struct Smem {
     // broadcast of the exchange result / step decision by warp 0
     double ta, tb, delta;
     int te, status;
+    // a subject run crossing a chunk edge of a streamed slice: its partial
+    // numerator (grad/hess) or denominator (update), carried to the next chunk
+    double cr_num, cr_den;
+    int cr_on, cr_subj, cr_n;
 };
 
 // ---- memory helpers ----------------------------------------------------------
@@ -455,47 +459,6 @@ __device__ __forceinline__ void run_terms(double num, double den, int n, double&
     hs = __dadd_rn(hs, __dmul_rn(nw, __dsub_rn(1.0, w)));
 }
 
-// Continuation of a run past its head pair: numerator terms in order.
-__device__ __forceinline__ double run_tail_numerator(const int2* __restrict__ pairs, const EraRec* era, int64_t q,
-                                                     int64_t p1, int s, double num) {
-    for (;;) {
-        const Rec r = ld_rec(era + ld_pair(pairs + q).x);
-        num = __dadd_rn(num, lexp(r.len, r.xb));
-        ++q;
-        if (q >= p1 || ld_pair(pairs + q).y != s) break;
-    }
-    return num;
-}
-
-// Sparse update of one era in the reference's statement order
-// (engine.hpp:219-229); returns the new denominator.
-__device__ __forceinline__ double update_era(EraRec* era, int row, double xb, double le, int len, double d,
-                                             double den, int& err, double& errv) {
-    const double updated = __dadd_rn(xb, d);
-    if (!(fabs(updated) <= kXbBound)) {
-        err = DERR_OVERFLOW;
-        errv = fabs(updated);
-        return den;
-    }
-    const double fresh = lexp(len, updated);
-    den = __dadd_rn(den, __dsub_rn(fresh, le));
-    era[row].xb = updated;
-    return den;
-}
-
-// Update of the rest of a run after its head (pairs q.. of subject s).
-__device__ __forceinline__ double run_tail_update(const int2* __restrict__ pairs, EraRec* era, int64_t q, int64_t p1,
-                                                  int s, double d, double den, int& err, double& errv) {
-    for (;;) {
-        const int row = ld_pair(pairs + q).x;
-        const Rec r = ld_rec(era + row);
-        den = update_era(era, row, r.xb, lexp(r.len, r.xb), r.len, d, den, err, errv);
-        ++q;
-        if (q >= p1 || ld_pair(pairs + q).y != s) break;
-    }
-    return den;
-}
-
 // Per-lane records of the register tiles.  Every lane gathers its own era
 // record; run heads also gather the subject record.  Runs are combined from
 // shared memory in ascending pair order, so a head never issues a dependent
@@ -603,14 +566,244 @@ __device__ __forceinline__ void repair(const Cached& C, HeadRegs& H, const Smem&
     }
 }
 
+// ---- slices beyond the register tiles (skewed columns) ----------------------
+//
+// Pairs [b0, p1) are processed in chunks of kCH (kSP per thread, every
+// thread of the CTA): each lane gathers its own era record, so a chunk's
+// gathers are all in flight together; run sums are then taken in ascending
+// pair order from shared memory, and a run crossing a chunk edge is carried
+// to the next chunk in shared memory (thread 0 finishes it there).  A run
+// that starts in the register tiles and continues is carried in the same way.
+constexpr int kSP = kCap / kT;
+constexpr int kCH = kSP * kT;
+static_assert(kSP >= 1, "a streamed chunk must fit the staging arrays");
+
+// (out of line, with the accumulators passed by value, so the register
+// tiles' fast path keeps its allocation)
+struct GhAcc {
+    double gs, hs;
+    int err;
+};
+
+#ifndef BSCCS_STREAM_NOINLINE
+#define BSCCS_STREAM_NOINLINE 0
+#endif
+#if BSCCS_STREAM_NOINLINE
+#define STREAM_FN __noinline__
+#else
+#define STREAM_FN __forceinline__
+#endif
 template <bool kSS>
+__device__ STREAM_FN GhAcc gh_streamed(const ShardArgs& S, int64_t p0, int64_t b0, int64_t p1, GhAcc acc,
+                                          Smem& sm, const SubjTile T) {
+    double gs = acc.gs, hs = acc.hs;
+    int err = acc.err;
+    const int2* __restrict__ pairs = S.pairs;
+    const EraRec* era = S.era;
+    const SubjRec* subj = S.subj;
+    for (int64_t b = b0; b < p1; b += kCH) {
+        const int ne = static_cast<int>(min(p1 - b, static_cast<int64_t>(kCH)));
+        __syncthreads(); // the previous chunk's readers of stage / carry are done
+        int cr_on = 0, cr_subj = -1, cr_n = 0;
+        double cr_num = 0.0, cr_den = 0.0;
+        if (threadIdx.x == 0) {
+            cr_on = sm.cr_on;
+            cr_subj = sm.cr_subj;
+            cr_num = sm.cr_num;
+            cr_den = sm.cr_den;
+            cr_n = sm.cr_n;
+            sm.cr_on = 0;
+        }
+        int sj[kSP];
+        bool hd[kSP];
+        Rec rr[kSP];
+        double dn[kSP];
+        int nn[kSP];
+#pragma unroll
+        for (int i = 0; i < kSP; ++i) {
+            const int q = i * kT + static_cast<int>(threadIdx.x);
+            sj[i] = -1;
+            hd[i] = false;
+            if (q < ne) {
+                const int64_t p = b + q;
+                const int2 pr = ld_pair(pairs + p);
+                const int prev = p > p0 ? ld_pair(pairs + p - 1).y : -1;
+                sj[i] = pr.y;
+                hd[i] = prev != pr.y;
+                rr[i] = ld_rec(era + pr.x);
+                if (!kSS && hd[i]) {
+                    const Subj sr = ld_subj(subj + pr.y);
+                    dn[i] = sr.den;
+                    nn[i] = sr.n;
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < kSP; ++i) {
+            const int q = i * kT + static_cast<int>(threadIdx.x);
+            if (q < ne) {
+                sm.stage[q] = lexp(rr[i].len, rr[i].xb);
+                sm.ssub[q] = sj[i];
+            }
+        }
+        __syncthreads();
+        const bool more = b + ne < p1;
+        const int after = more ? ld_pair(pairs + b + ne).y : -1; // subject just past the chunk
+#pragma unroll
+        for (int i = 0; i < kSP; ++i) {
+            const int q = i * kT + static_cast<int>(threadIdx.x);
+            if (!hd[i]) continue;
+            const int s = sj[i];
+            double num = 0.0;
+            int e = q;
+            while (e < ne && sm.ssub[e] == s) num = __dadd_rn(num, sm.stage[e++]);
+            double den;
+            int n;
+            if constexpr (kSS) {
+                den = T.den[s - T.base];
+                n = T.n[s - T.base];
+            } else {
+                den = dn[i];
+                n = nn[i];
+            }
+            if (e == ne && after == s) {
+                sm.cr_num = num;
+                sm.cr_den = den;
+                sm.cr_n = n;
+                sm.cr_subj = s;
+                sm.cr_on = 1;
+            } else {
+                run_terms(num, den, n, gs, hs, err);
+            }
+        }
+        if (cr_on) { // thread 0: the run carried into this chunk
+            double num = cr_num;
+            int e = 0;
+            while (e < ne && sm.ssub[e] == cr_subj) num = __dadd_rn(num, sm.stage[e++]);
+            if (e == ne && after == cr_subj) {
+                sm.cr_num = num;
+                sm.cr_den = cr_den;
+                sm.cr_n = cr_n;
+                sm.cr_subj = cr_subj;
+                sm.cr_on = 1;
+            } else {
+                run_terms(num, cr_den, cr_n, gs, hs, err);
+            }
+        }
+    }
+    return GhAcc{gs, hs, err};
+}
+
+// The sparse update of a streamed slice, same chunking: every lane updates
+// its own era (engine.hpp:219-229) and stages fresh - old; heads (and the
+// carried run) apply the differences to the denominator in pair order.
+struct UpdErr {
+    int err;
+    double errv;
+};
+
+template <bool kSS>
+__device__ STREAM_FN UpdErr update_streamed(const ShardArgs& S, int64_t p0, int64_t b0, int64_t p1, double d,
+                                               UpdErr ue, Smem& sm, const SubjTile T) {
+    int err = ue.err;
+    double errv = ue.errv;
+    const int2* __restrict__ pairs = S.pairs;
+    EraRec* era = S.era;
+    SubjRec* subj = S.subj;
+    for (int64_t b = b0; b < p1; b += kCH) {
+        const int ne = static_cast<int>(min(p1 - b, static_cast<int64_t>(kCH)));
+        __syncthreads();
+        int cr_on = 0, cr_subj = -1;
+        double cr_den = 0.0;
+        if (threadIdx.x == 0) {
+            cr_on = sm.cr_on;
+            cr_subj = sm.cr_subj;
+            cr_den = sm.cr_den;
+            sm.cr_on = 0;
+        }
+        int sj[kSP], row[kSP];
+        bool hd[kSP];
+        Rec rr[kSP];
+        double dn[kSP];
+#pragma unroll
+        for (int i = 0; i < kSP; ++i) {
+            const int q = i * kT + static_cast<int>(threadIdx.x);
+            sj[i] = -1;
+            hd[i] = false;
+            if (q < ne) {
+                const int64_t p = b + q;
+                const int2 pr = ld_pair(pairs + p);
+                const int prev = p > p0 ? ld_pair(pairs + p - 1).y : -1;
+                sj[i] = pr.y;
+                row[i] = pr.x;
+                hd[i] = prev != pr.y;
+                rr[i] = ld_rec(era + pr.x);
+                if (!kSS && hd[i]) dn[i] = subj[pr.y].den;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < kSP; ++i) {
+            const int q = i * kT + static_cast<int>(threadIdx.x);
+            if (q < ne) {
+                const double updated = __dadd_rn(rr[i].xb, d);
+                double diff = 0.0;
+                if (!(fabs(updated) <= kXbBound)) {
+                    err = DERR_OVERFLOW;
+                    errv = fabs(updated);
+                } else {
+                    diff = __dsub_rn(lexp(rr[i].len, updated), lexp(rr[i].len, rr[i].xb));
+                    era[row[i]].xb = updated;
+                }
+                sm.stage[q] = diff;
+                sm.ssub[q] = sj[i];
+            }
+        }
+        __syncthreads();
+        const bool more = b + ne < p1;
+        const int after = more ? ld_pair(pairs + b + ne).y : -1;
+#pragma unroll
+        for (int i = 0; i < kSP; ++i) {
+            const int q = i * kT + static_cast<int>(threadIdx.x);
+            if (!hd[i]) continue;
+            const int s = sj[i];
+            double den = kSS ? T.den[s - T.base] : dn[i];
+            int e = q;
+            while (e < ne && sm.ssub[e] == s) den = __dadd_rn(den, sm.stage[e++]);
+            if (e == ne && after == s) {
+                sm.cr_den = den;
+                sm.cr_subj = s;
+                sm.cr_on = 1;
+            } else if constexpr (kSS) {
+                T.den[s - T.base] = den;
+            } else {
+                subj[s].den = den;
+            }
+        }
+        if (cr_on) {
+            double den = cr_den;
+            int e = 0;
+            while (e < ne && sm.ssub[e] == cr_subj) den = __dadd_rn(den, sm.stage[e++]);
+            if (e == ne && after == cr_subj) {
+                sm.cr_den = den;
+                sm.cr_subj = cr_subj;
+                sm.cr_on = 1;
+            } else if constexpr (kSS) {
+                T.den[cr_subj - T.base] = den;
+            } else {
+                subj[cr_subj].den = den;
+            }
+        }
+    }
+    return UpdErr{err, errv};
+}
+
+template <bool kSS, bool kST>
 __device__ __forceinline__ void gh_compute(const ShardArgs& S, const Cached& C, int64_t p0, int64_t p1,
                                            const HeadRegs& H, double& gs, double& hs, int& err, Smem& sm,
                                            const SubjTile& T) {
     const int2* __restrict__ pairs = S.pairs;
-    EraRec* era = S.era;
-    SubjRec* subj = S.subj;
     const int ncached = static_cast<int>(min(p1 - p0, static_cast<int64_t>(kCap)));
+    if (threadIdx.x == 0) sm.cr_on = 0;
 #pragma unroll
     for (int v = 0; v < kCached; ++v) {
         if (slot_valid(C.slot[v])) {
@@ -624,48 +817,52 @@ __device__ __forceinline__ void gh_compute(const ShardArgs& S, const Cached& C, 
     for (int v = 0; v < kCached; ++v) {
         if (C.slot[v].head) {
             double num = H.le[v];
+            const int s = C.slot[v].pr.y;
+            double den;
+            int n;
+            if constexpr (kSS) {
+                den = T.den[s - T.base];
+                n = T.n[s - T.base];
+            } else {
+                den = H.den[v];
+                n = H.n[v];
+            }
             if (C.slot[v].cont) {
-                const int s = C.slot[v].pr.y;
                 int q = slot_pos(v) + 1;
                 while (q < ncached && sm.ssub[q] == s) num = __dadd_rn(num, sm.stage[q++]);
-                if (q == ncached && p0 + q < p1 && ld_pair(pairs + p0 + q).y == s)
-                    num = run_tail_numerator(pairs, era, p0 + q, p1, s, num);
+                if constexpr (kST) {
+                    if (q == ncached && p0 + q < p1 && ld_pair(pairs + p0 + q).y == s) {
+                        // the run continues into the streamed part: carried there
+                        sm.cr_num = num;
+                        sm.cr_den = den;
+                        sm.cr_n = n;
+                        sm.cr_subj = s;
+                        sm.cr_on = 1;
+                        continue;
+                    }
+                }
             }
-            if constexpr (kSS) {
-                const int t = C.slot[v].pr.y - T.base;
-                run_terms(num, T.den[t], T.n[t], gs, hs, err);
-            } else {
-                run_terms(num, H.den[v], H.n[v], gs, hs, err);
-            }
+            run_terms(num, den, n, gs, hs, err);
         }
     }
-    // streamed remainder: head threads own their runs
-    for (int64_t base = p0 + static_cast<int64_t>(kCap); base < p1; base += kT) {
-        const int64_t p = base + threadIdx.x;
-        const PairSlot s = load_slot(pairs, p, p0, p1);
-        if (s.head) {
-            const Rec r = ld_rec(era + s.pr.x);
-            Subj sr;
-            if constexpr (kSS) {
-                sr.den = T.den[s.pr.y - T.base];
-                sr.n = T.n[s.pr.y - T.base];
-            } else {
-                sr = ld_subj(subj + s.pr.y);
-            }
-            double num = lexp(r.len, r.xb);
-            if (s.cont) num = run_tail_numerator(pairs, era, p + 1, p1, s.pr.y, num);
-            run_terms(num, sr.den, sr.n, gs, hs, err);
+    if constexpr (kST) {
+        if (p1 - p0 > kCap) {
+            const GhAcc a = gh_streamed<kSS>(S, p0, p0 + kCap, p1, GhAcc{gs, hs, err}, sm, T);
+            gs = a.gs;
+            hs = a.hs;
+            err = a.err;
         }
     }
 }
 
-template <bool kSS>
+template <bool kSS, bool kST>
 __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C, const HeadRegs& H, bool cached,
                                              int64_t p0, int64_t p1, double d, int& err, double& errv, Smem& sm,
                                              const SubjTile& T, bool record = false, int* myht = nullptr) {
     const int2* __restrict__ pairs = S.pairs;
     EraRec* era = S.era;
     SubjRec* subj = S.subj;
+    if (threadIdx.x == 0) sm.cr_on = 0;
     if (cached) {
         const int ncached = static_cast<int>(min(p1 - p0, static_cast<int64_t>(kCap)));
         // every lane updates its own era (engine.hpp:219-229) and stages
@@ -690,6 +887,7 @@ __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C
                 }
                 if (record) sm.jrow[pos] = C.slot[v].pr.x;
                 sm.stage[pos] = diff;
+                sm.ssub[pos] = C.slot[v].pr.y; // (a streamed grad/hess pass reused ssub)
             }
         }
         __syncthreads();
@@ -703,8 +901,15 @@ __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C
                 if (C.slot[v].cont) {
                     const int s = C.slot[v].pr.y;
                     while (q < ncached && sm.ssub[q] == s) den = __dadd_rn(den, sm.stage[q++]);
-                    if (q == ncached && p0 + q < p1 && ld_pair(pairs + p0 + q).y == s)
-                        den = run_tail_update(pairs, era, p0 + q, p1, s, d, den, err, errv);
+                    if constexpr (kST) {
+                        if (q == ncached && p0 + q < p1 && ld_pair(pairs + p0 + q).y == s) {
+                            // continues into the streamed part: carried there
+                            sm.cr_den = den;
+                            sm.cr_subj = s;
+                            sm.cr_on = 1;
+                            continue;
+                        }
+                    }
                 }
                 if constexpr (kSS) T.den[C.slot[v].pr.y - T.base] = den;
                 else subj[C.slot[v].pr.y].den = den;
@@ -719,17 +924,12 @@ __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C
             }
         }
     }
-    const int64_t start = cached ? p0 + static_cast<int64_t>(kCap) : p0;
-    for (int64_t base = start; base < p1; base += kT) {
-        const int64_t p = base + threadIdx.x;
-        const PairSlot s = load_slot(pairs, p, p0, p1);
-        if (s.head) {
-            const Rec r = ld_rec(era + s.pr.x);
-            double den = kSS ? T.den[s.pr.y - T.base] : subj[s.pr.y].den;
-            den = update_era(era, s.pr.x, r.xb, lexp(r.len, r.xb), r.len, d, den, err, errv);
-            if (s.cont) den = run_tail_update(pairs, era, p + 1, p1, s.pr.y, d, den, err, errv);
-            if constexpr (kSS) T.den[s.pr.y - T.base] = den;
-            else subj[s.pr.y].den = den;
+    if constexpr (kST) {
+        const int64_t start = cached ? p0 + static_cast<int64_t>(kCap) : p0;
+        if (start < p1) {
+            const UpdErr u = update_streamed<kSS>(S, p0, start, p1, d, UpdErr{err, errv}, sm, T);
+            err = u.err;
+            errv = u.errv;
         }
     }
 }
@@ -747,7 +947,11 @@ enum StepStatus { ST_OK = 0, ST_REMOTE_ERR = 1, ST_STEP_ERR = 2, ST_NONFINITE = 
 
 constexpr size_t kSmemSubjOffset = (sizeof(Smem) + 15) / 16 * 16;
 
-template <bool kSS>
+// kSS: subject records in shared memory for the cycle.  kST: slices may
+// exceed the register tiles (the streamed path is compiled in); the host
+// picks kST = false when no slice of the dataset does, so the common case
+// carries none of the streamed path's register pressure.
+template <bool kSS, bool kST>
 __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant__ SweepArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
@@ -769,7 +973,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
     if (A.mode == kModeUpdate) {
         const int j = A.single_j;
         const int64_t p0 = split_c[static_cast<int64_t>(j) * stride], p1 = split_c[static_cast<int64_t>(j) * stride + 1];
-        update_slice<false>(S, C, H, false, p0, p1, A.single_delta, err, errv, sm, T);
+        if constexpr (kST) update_slice<false, true>(S, C, H, false, p0, p1, A.single_delta, err, errv, sm, T);
         if (err) record_error(S.err, err, errv);
         if (c == 0 && threadIdx.x == 0) S.beta[j] = __dadd_rn(S.beta[j], A.single_delta);
         return;
@@ -801,7 +1005,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         load_cached(S, p0, p1, C);
         double gs = 0.0, hs = 0.0;
         gather_records<false>(S, C, H);
-        gh_compute<false>(S, C, p0, p1, H, gs, hs, err, sm, T);
+        gh_compute<false, kST>(S, C, p0, p1, H, gs, hs, err, sm, T);
         if (err) record_error(S.err, err, 0.0);
         block_reduce(gs, hs, err, false, sm);
         publish(A, seq, gs, hs, err);
@@ -888,7 +1092,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                         gather_records<kSS>(S, C, H);
                     }
                 }
-                gh_compute<kSS>(S, C, p0, p1, H, gs, hs, err, sm, T);
+                gh_compute<kSS, kST>(S, C, p0, p1, H, gs, hs, err, sm, T);
             }
             if (err) record_error(S.err, err, errv);
             // The publish below must not be observable before this
@@ -993,7 +1197,8 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             ++nvisit;
             if (delta != 0.0) {
                 ++nmoved;
-                if (!(A.dbg & 2)) update_slice<kSS>(S, C, H, true, p0, p1, delta, err, errv, sm, T, spec_next, myht);
+                if (!(A.dbg & 2))
+                    update_slice<kSS, kST>(S, C, H, true, p0, p1, delta, err, errv, sm, T, spec_next, myht);
             }
             __syncthreads(); // slice writes of this coordinate before the next reads
             if (tr && idx < A.ntrace) trb[idx * trs + 3] = gtimer();
@@ -1475,6 +1680,20 @@ __global__ void k_build_vsplit(const int64_t* __restrict__ split, const int32_t*
 }
 
 // subject runs per column (heads of the CSC pair list)
+// largest per-CTA slice of any column (decides whether sweeps need the
+// streamed path)
+__global__ void k_max_slice(const int64_t* __restrict__ split, int32_t J, int C, int* out) {
+    const int64_t n = static_cast<int64_t>(J) * C;
+    int m = 0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t j = i / C, c = i % C;
+        const int64_t a = split[j * (C + 1) + c], b = split[j * (C + 1) + c + 1];
+        m = max(m, static_cast<int>(min(b - a, static_cast<int64_t>(1 << 30))));
+    }
+    atomicMax(out, m);
+}
+
 __global__ void k_col_runs(const int2* pairs, const int64_t* col_ptr, int32_t* runs, int J) {
     const int j = blockIdx.x;
     if (j >= J) return;
@@ -1581,9 +1800,12 @@ constexpr int kMaxSweepSmem = 225 * 1024; // opt-in dynamic shared memory per CT
 void ensure_kernel_attrs(int device) {
     static std::atomic<unsigned> done{0};
     if (device < 32 && (done.load() & (1u << device))) return;
-    CUDA_TRY(cudaFuncSetAttribute(k_ccd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CUDA_TRY(cudaFuncSetAttribute(k_ccd<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(sizeof(Smem))));
-    CUDA_TRY(cudaFuncSetAttribute(k_ccd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSweepSmem));
+    CUDA_TRY(cudaFuncSetAttribute(k_ccd<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sizeof(Smem))));
+    CUDA_TRY(cudaFuncSetAttribute(k_ccd<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSweepSmem));
+    CUDA_TRY(cudaFuncSetAttribute(k_ccd<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSweepSmem));
     if (device < 32) done.fetch_or(1u << device);
 }
 
@@ -1591,7 +1813,7 @@ int default_ctas(int device) {
     // one persistent CTA per SM (launch bounds force 1 resident CTA of 512)
     ensure_kernel_attrs(device);
     int per_sm = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ccd<false>, kSweepThreads, sizeof(Smem)));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ccd<false, true>, kSweepThreads, sizeof(Smem)));
     if (per_sm < 1) internal_error("sweep kernel cannot be resident");
     return sm_count(device);
 }
@@ -1715,6 +1937,17 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
 
     ds->col_runs_h.resize(static_cast<size_t>(J));
     CUDA_TRY(cudaMemcpy(ds->col_runs_h.data(), ds->col_runs, sizeof(int32_t) * J, cudaMemcpyDeviceToHost));
+    {
+        int* d_mx = nullptr;
+        int64_t b2 = 0;
+        d_mx = dalloc<int>(1, b2, s);
+        CUDA_TRY(cudaMemsetAsync(d_mx, 0, sizeof(int), s));
+        const int64_t nsl = static_cast<int64_t>(J) * C;
+        if (nsl > 0) k_max_slice<<<grid_for(nsl, 256, sms), 256, 0, s>>>(ds->split, J, C, d_mx);
+        CUDA_TRY(cudaMemcpyAsync(&ds->max_slice, d_mx, sizeof(int), cudaMemcpyDeviceToHost, s));
+        dfree(d_mx, s);
+        CUDA_TRY(cudaStreamSynchronize(s));
+    }
     {
         std::vector<int32_t> cs(static_cast<size_t>(C) + 1);
         CUDA_TRY(cudaMemcpy(cs.data(), ds->cta_subj, sizeof(int32_t) * (C + 1), cudaMemcpyDeviceToHost));
@@ -2055,15 +2288,20 @@ void launch_ccd(const ExchangePlan& plan, SweepArgs& a) {
     ensure_kernel_attrs(s0->ds->device);
     a.ss_cap = a.mode == kModeSweep ? subject_tile_cap(plan) : 0;
     a.prefetch = a.mode == kModeSweep ? prefetch_enabled(plan) : 0;
+    // the streamed path only when some slice exceeds the register tiles
+    // (and always for the single-coordinate ops, whose update streams)
+    bool streamed = a.mode != kModeSweep;
+    for (auto* st : plan.shards) streamed = streamed || st->ds->max_slice > kCap;
     void* params[] = {&a};
+    void* fn;
+    size_t bytes = sizeof(Smem);
     if (a.ss_cap > 0) {
-        const size_t bytes = kSmemSubjOffset + static_cast<size_t>(a.ss_cap) * (sizeof(double) + sizeof(int));
-        CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_ccd<true>), dim3(plan_ctas(plan)),
-                                             dim3(kSweepThreads), params, bytes, s0->stream));
+        bytes = kSmemSubjOffset + static_cast<size_t>(a.ss_cap) * (sizeof(double) + sizeof(int));
+        fn = streamed ? reinterpret_cast<void*>(k_ccd<true, true>) : reinterpret_cast<void*>(k_ccd<true, false>);
     } else {
-        CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_ccd<false>), dim3(plan_ctas(plan)),
-                                             dim3(kSweepThreads), params, sizeof(Smem), s0->stream));
+        fn = streamed ? reinterpret_cast<void*>(k_ccd<false, true>) : reinterpret_cast<void*>(k_ccd<false, false>);
     }
+    CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(plan_ctas(plan)), dim3(kSweepThreads), params, bytes, s0->stream));
     count_launches(1);
 }
 

@@ -98,6 +98,7 @@ struct bsccs_dataset {
     uint8_t* col_nonempty = nullptr;  // [J] global
     int32_t* col_runs = nullptr;      // [J] subject runs per column (this shard)
     int32_t max_cta_subjects = 0;     // largest CTA subject range (sizes the shared-memory subject tile)
+    int32_t max_slice = 0;            // largest per-CTA slice of any column (streamed path needed above kCap)
     // host copies of small metadata
     std::vector<int64_t> col_ptr_h;
     std::vector<uint8_t> col_nonempty_h;

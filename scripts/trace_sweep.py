@@ -10,8 +10,10 @@ from paper_1208_0945_b200 import _native, bsccs as B, datagen  # noqa: E402
 
 wl = sys.argv[1] if len(sys.argv) > 1 else "1M"
 flags = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+zipf = "zipf" in sys.argv[3:]
+per_coord = "per-coord" in sys.argv[3:]
 NT = 300
-ds = datagen.config_dataset(wl)
+ds = datagen.config_dataset(wl, zipf)
 dds = B.DeviceDataset(ds, 0)
 ctas = dds.ctas
 lib = _native.lib()
@@ -27,6 +29,13 @@ lib.bsccs_debug_trace(NT, ctas, buf.ctypes.data_as(C.c_void_p), buf.size)
 lib.bsccs_debug_trace(0, ctas, None, 0)
 lib.bsccs_debug_set_sweep_flags(0)
 t = buf.reshape(NT, ctas, 8).astype(np.int64)
+if per_coord:  # first coordinates in visit order (fixed order: j = 0, 1, ...): the head columns of a skewed set
+    full = t[:NT - 1, 0, 0]
+    nnz = np.diff(ds.col_ptr)
+    per = np.diff(t[:NT, 0, 0])
+    for i in range(0, 40):
+        print(f"  coord {i:3d} nnz {nnz[i]:8d}  period {per[i]:8d} ns")
+    print(f"  coords 0-39 total {per[:40].sum() / 1e3:.1f} us, coords 40-298 median {np.median(per[40:]):.0f} ns")
 t = t[20:NT - 1]  # skip the start
 t0 = t[:, :, 0]
 pub = t[:, :, 1]

@@ -243,6 +243,10 @@ def main():
         (OUT / "fit_1M_laplace.json").write_text(json.dumps(
             fast_case(ref, "1M", 1_030_000, 1500, 3.0, B.laplace_prior(0.1)), indent=1))
         print("fit_1M_laplace.json")
+    if large and want("fit_1M_zipf"):  # the skewed variant, reported beside the uniform one
+        (OUT / "fit_1M_zipf_laplace.json").write_text(json.dumps(
+            fast_case(ref, "1M", 1_030_000, 1500, 3.0, B.laplace_prior(0.1), zipf=True), indent=1))
+        print("fit_1M_zipf_laplace.json")
     if large and want("fit_10M"):
         (OUT / "fit_10M_laplace.json").write_text(json.dumps(
             fast_case(ref, "10M", 10_300_000, 4000, 3.0, B.laplace_prior(0.1)), indent=1))

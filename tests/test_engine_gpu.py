@@ -175,3 +175,35 @@ def test_slices_cover_many_ctas():
         port.sparse_update(ds, ost, j, d)
     assert close(st.denominators, ost["denominators"], 1e-13)
     assert close(st.xbeta, ost["xbeta"], 0.0)
+
+
+@pytest.mark.parametrize("ctas", [1, 2, 3])
+def test_streamed_slices_beyond_register_tiles(ctas):
+    """Few CTAs, so every column's slice is far larger than the register
+    tiles: the chunked streamed path, with runs crossing chunk edges and the
+    tile/stream boundary, in the tier-1 ops and in whole sweeps, against the
+    oracle (the skewed-column case of SURVEY §8(d))."""
+    import pyoracle
+    rng = B.Rng(77 + ctas)
+    ds = random_dataset(rng, 4, 2500, exposure_prob=0.85)
+    beta = random_beta(rng, 4, 0.6)
+    dds = B.DeviceDataset(ds, 0, ctas)
+    assert max(np.diff(ds.col_ptr)) > 1200 * ctas  # beyond the register tiles of every CTA
+    st = B.init_state(dds, beta)
+    port = pyoracle.Port()
+    ost = port.init_state(ds, beta)
+    for j in range(4):
+        a = B.fused_grad_hess(dds, st, j)
+        g, h = port.grad_hess(ds, ost, j)
+        assert rel_gap(a.gradient, g) < 1e-12 and rel_gap(a.hessian, h) < 1e-12
+    for j, d in [(0, 0.3), (2, -0.2), (1, 0.11), (3, 0.05)]:
+        B.sparse_delta_update(dds, st, j, d)
+        port.sparse_update(ds, ost, j, d)
+    assert close(st.denominators, ost["denominators"], 1e-12)
+    assert close(st.xbeta, ost["xbeta"], 0.0)
+    for prior in (B.laplace_prior(0.1), B.normal_prior(1.0)):
+        res = B.fit(dds, prior)
+        exp = port.fit(ds, prior, B.SolverConfig())
+        assert res.cycles_run == exp["cycles_run"]
+        assert np.all(np.abs(res.beta_map - exp["beta"]) <= np.maximum(1e-8 * np.abs(exp["beta"]), 1e-11))
+        assert rel_gap(res.log_posterior, exp["log_posterior"]) < 1e-10

@@ -199,12 +199,17 @@ def test_fast_10k_golden():
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("name,fname", [("1M", "fit_1M_laplace.json"), ("10M", "fit_10M_laplace.json")])
-def test_full_size_golden(name, fname):
+@pytest.mark.parametrize("name,fname,zipf", [("1M", "fit_1M_laplace.json", False), ("10M", "fit_10M_laplace.json", False),
+                                             ("1M", "fit_1M_zipf_laplace.json", True)])
+def test_full_size_golden(name, fname, zipf):
+    """configs 2 and 3 (uniform prevalence) and the skewed (Zipf) variant of
+    config 2 that SURVEY §8(d) asks to report beside it: its head columns
+    hold ~30% of the eras, so their slices take the streamed path"""
     if not (GOLDEN / fname).exists():
         pytest.skip(f"{fname} not generated")
     g = load_golden(fname)
-    ds = datagen.config_dataset(name)
+    assert bool(g.get("zipf", False)) == zipf
+    ds = datagen.config_dataset(name, zipf)
     assert (ds.num_subjects, ds.num_eras, ds.nnz) == (g["sizes"]["N"], g["sizes"]["K"], g["sizes"]["nnz"])
     res = B.fit(ds, prior_from(g["prior"]))
     assert_parity(res, fa(g["beta"]), float(g["log_posterior"]), g["cycles_run"])
