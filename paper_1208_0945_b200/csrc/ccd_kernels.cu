@@ -117,6 +117,7 @@ struct SweepArgs {
     unsigned long long* counter;
     double red_a, red_b; // kModeReduce inputs (this rank's values)
     int prefetch; // L2 prefetch of the records two coordinates ahead (small slices only)
+    int stream_off, stream_cap; // streamed-slice staging buffer in dynamic shared memory (bytes offset, pairs)
     int ss_cap; // capacity of the shared-memory subject tile (0: subjects stay in HBM)
     int dbg; // profiling only: bit0 skip grad/hess, bit1 skip update, bit2 skip exchange, bit4 no speculation
     unsigned long long* trace; // profiling only: [ntrace][gridDim][kTr] globaltimer stamps
@@ -568,23 +569,19 @@ __device__ __forceinline__ void repair(const Cached& C, HeadRegs& H, const Smem&
 
 // ---- slices beyond the register tiles (skewed columns) ----------------------
 //
-// Pairs [b0, p1) are processed in chunks of kCH (kSP per thread, every
-// thread of the CTA): each lane gathers its own era record, so a chunk's
-// gathers are all in flight together; run sums are then taken in ascending
-// pair order from shared memory, and a run crossing a chunk edge is carried
-// to the next chunk in shared memory (thread 0 finishes it there).  A run
-// that starts in the register tiles and continues is carried in the same way.
-constexpr int kSP = kCap / kT;
-constexpr int kCH = kSP * kT;
-static_assert(kSP >= 1, "a streamed chunk must fit the staging arrays");
-
-// (out of line, with the accumulators passed by value, so the register
-// tiles' fast path keeps its allocation)
-struct GhAcc {
-    double gs, hs;
-    int err;
-};
-
+// Pairs [b0, p1) are processed in chunks of up to `cap` pairs staged in a
+// dynamic shared-memory buffer (l*exp or the update's differences, and the
+// subject of every pair).  Every thread stages its pairs in groups of kSU
+// with all their loads in flight together (no per-pair state survives the
+// staging, so the path adds little register pressure); run sums are then
+// taken in ascending pair order from shared memory, and a run crossing a
+// chunk edge is carried to the next chunk in shared memory (thread 0
+// finishes it there).  A run that starts in the register tiles and
+// continues is carried in the same way.
+#ifndef BSCCS_STREAM_UNROLL
+#define BSCCS_STREAM_UNROLL 2
+#endif
+constexpr int kSU = BSCCS_STREAM_UNROLL;
 #ifndef BSCCS_STREAM_NOINLINE
 #define BSCCS_STREAM_NOINLINE 0
 #endif
@@ -593,20 +590,39 @@ struct GhAcc {
 #else
 #define STREAM_FN __forceinline__
 #endif
+
+struct StreamBuf {
+    double* x; // [cap] l*exp (grad/hess) or fresh - old (update)
+    int* sub;  // [cap] subject of each staged pair
+    int cap;   // a multiple of kT
+};
+
+// (the accumulators travel by value, so the fast path's allocation is not
+// disturbed by references into it)
+struct GhAcc {
+    double gs, hs;
+    int err;
+};
+struct UpdErr {
+    int err;
+    double errv;
+};
+
 template <bool kSS>
 __device__ STREAM_FN GhAcc gh_streamed(const ShardArgs& S, int64_t p0, int64_t b0, int64_t p1, GhAcc acc,
-                                          Smem& sm, const SubjTile T) {
-    double gs = acc.gs, hs = acc.hs;
-    int err = acc.err;
+                                             Smem& sm, const SubjTile T, const StreamBuf X) {
     const int2* __restrict__ pairs = S.pairs;
     const EraRec* era = S.era;
     const SubjRec* subj = S.subj;
-    for (int64_t b = b0; b < p1; b += kCH) {
-        const int ne = static_cast<int>(min(p1 - b, static_cast<int64_t>(kCH)));
-        __syncthreads(); // the previous chunk's readers of stage / carry are done
+    double gs = acc.gs, hs = acc.hs;
+    int err = acc.err;
+    const int tid = static_cast<int>(threadIdx.x);
+    for (int64_t b = b0; b < p1; b += X.cap) {
+        const int ne = static_cast<int>(min(p1 - b, static_cast<int64_t>(X.cap)));
+        __syncthreads(); // the previous chunk's readers of the buffer / carry are done
         int cr_on = 0, cr_subj = -1, cr_n = 0;
         double cr_num = 0.0, cr_den = 0.0;
-        if (threadIdx.x == 0) {
+        if (tid == 0) {
             cr_on = sm.cr_on;
             cr_subj = sm.cr_subj;
             cr_num = sm.cr_num;
@@ -614,57 +630,42 @@ __device__ STREAM_FN GhAcc gh_streamed(const ShardArgs& S, int64_t p0, int64_t b
             cr_n = sm.cr_n;
             sm.cr_on = 0;
         }
-        int sj[kSP];
-        bool hd[kSP];
-        Rec rr[kSP];
-        double dn[kSP];
-        int nn[kSP];
+        for (int q0 = tid; q0 < ne; q0 += kSU * kT) {
+            int2 pr[kSU];
 #pragma unroll
-        for (int i = 0; i < kSP; ++i) {
-            const int q = i * kT + static_cast<int>(threadIdx.x);
-            sj[i] = -1;
-            hd[i] = false;
-            if (q < ne) {
-                const int64_t p = b + q;
-                const int2 pr = ld_pair(pairs + p);
-                const int prev = p > p0 ? ld_pair(pairs + p - 1).y : -1;
-                sj[i] = pr.y;
-                hd[i] = prev != pr.y;
-                rr[i] = ld_rec(era + pr.x);
-                if (!kSS && hd[i]) {
-                    const Subj sr = ld_subj(subj + pr.y);
-                    dn[i] = sr.den;
-                    nn[i] = sr.n;
+            for (int u = 0; u < kSU; ++u)
+                if (q0 + u * kT < ne) pr[u] = ld_pair(pairs + b + q0 + u * kT);
+            Rec rr[kSU];
+#pragma unroll
+            for (int u = 0; u < kSU; ++u)
+                if (q0 + u * kT < ne) rr[u] = ld_rec(era + pr[u].x);
+#pragma unroll
+            for (int u = 0; u < kSU; ++u) {
+                const int q = q0 + u * kT;
+                if (q < ne) {
+                    X.x[q] = lexp(rr[u].len, rr[u].xb);
+                    X.sub[q] = pr[u].y;
                 }
             }
         }
-#pragma unroll
-        for (int i = 0; i < kSP; ++i) {
-            const int q = i * kT + static_cast<int>(threadIdx.x);
-            if (q < ne) {
-                sm.stage[q] = lexp(rr[i].len, rr[i].xb);
-                sm.ssub[q] = sj[i];
-            }
-        }
         __syncthreads();
-        const bool more = b + ne < p1;
-        const int after = more ? ld_pair(pairs + b + ne).y : -1; // subject just past the chunk
-#pragma unroll
-        for (int i = 0; i < kSP; ++i) {
-            const int q = i * kT + static_cast<int>(threadIdx.x);
-            if (!hd[i]) continue;
-            const int s = sj[i];
+        const int before = b > p0 ? ld_pair(pairs + b - 1).y : -1; // subject just before the chunk
+        const int after = b + ne < p1 ? ld_pair(pairs + b + ne).y : -1; // ... and just past it
+        for (int q = tid; q < ne; q += kT) {
+            const int s = X.sub[q];
+            if ((q > 0 ? X.sub[q - 1] : before) == s) continue; // not a run head
             double num = 0.0;
             int e = q;
-            while (e < ne && sm.ssub[e] == s) num = __dadd_rn(num, sm.stage[e++]);
+            while (e < ne && X.sub[e] == s) num = __dadd_rn(num, X.x[e++]);
             double den;
             int n;
             if constexpr (kSS) {
                 den = T.den[s - T.base];
                 n = T.n[s - T.base];
             } else {
-                den = dn[i];
-                n = nn[i];
+                const Subj sr = ld_subj(subj + s);
+                den = sr.den;
+                n = sr.n;
             }
             if (e == ne && after == s) {
                 sm.cr_num = num;
@@ -679,7 +680,7 @@ __device__ STREAM_FN GhAcc gh_streamed(const ShardArgs& S, int64_t p0, int64_t b
         if (cr_on) { // thread 0: the run carried into this chunk
             double num = cr_num;
             int e = 0;
-            while (e < ne && sm.ssub[e] == cr_subj) num = __dadd_rn(num, sm.stage[e++]);
+            while (e < ne && X.sub[e] == cr_subj) num = __dadd_rn(num, X.x[e++]);
             if (e == ne && after == cr_subj) {
                 sm.cr_num = num;
                 sm.cr_den = cr_den;
@@ -697,78 +698,62 @@ __device__ STREAM_FN GhAcc gh_streamed(const ShardArgs& S, int64_t p0, int64_t b
 // The sparse update of a streamed slice, same chunking: every lane updates
 // its own era (engine.hpp:219-229) and stages fresh - old; heads (and the
 // carried run) apply the differences to the denominator in pair order.
-struct UpdErr {
-    int err;
-    double errv;
-};
-
 template <bool kSS>
 __device__ STREAM_FN UpdErr update_streamed(const ShardArgs& S, int64_t p0, int64_t b0, int64_t p1, double d,
-                                               UpdErr ue, Smem& sm, const SubjTile T) {
-    int err = ue.err;
-    double errv = ue.errv;
+                                                  UpdErr ue, Smem& sm, const SubjTile T, const StreamBuf X) {
     const int2* __restrict__ pairs = S.pairs;
     EraRec* era = S.era;
     SubjRec* subj = S.subj;
-    for (int64_t b = b0; b < p1; b += kCH) {
-        const int ne = static_cast<int>(min(p1 - b, static_cast<int64_t>(kCH)));
+    int err = ue.err;
+    double errv = ue.errv;
+    const int tid = static_cast<int>(threadIdx.x);
+    for (int64_t b = b0; b < p1; b += X.cap) {
+        const int ne = static_cast<int>(min(p1 - b, static_cast<int64_t>(X.cap)));
         __syncthreads();
         int cr_on = 0, cr_subj = -1;
         double cr_den = 0.0;
-        if (threadIdx.x == 0) {
+        if (tid == 0) {
             cr_on = sm.cr_on;
             cr_subj = sm.cr_subj;
             cr_den = sm.cr_den;
             sm.cr_on = 0;
         }
-        int sj[kSP], row[kSP];
-        bool hd[kSP];
-        Rec rr[kSP];
-        double dn[kSP];
+        for (int q0 = tid; q0 < ne; q0 += kSU * kT) {
+            int2 pr[kSU];
 #pragma unroll
-        for (int i = 0; i < kSP; ++i) {
-            const int q = i * kT + static_cast<int>(threadIdx.x);
-            sj[i] = -1;
-            hd[i] = false;
-            if (q < ne) {
-                const int64_t p = b + q;
-                const int2 pr = ld_pair(pairs + p);
-                const int prev = p > p0 ? ld_pair(pairs + p - 1).y : -1;
-                sj[i] = pr.y;
-                row[i] = pr.x;
-                hd[i] = prev != pr.y;
-                rr[i] = ld_rec(era + pr.x);
-                if (!kSS && hd[i]) dn[i] = subj[pr.y].den;
-            }
-        }
+            for (int u = 0; u < kSU; ++u)
+                if (q0 + u * kT < ne) pr[u] = ld_pair(pairs + b + q0 + u * kT);
+            Rec rr[kSU];
 #pragma unroll
-        for (int i = 0; i < kSP; ++i) {
-            const int q = i * kT + static_cast<int>(threadIdx.x);
-            if (q < ne) {
-                const double updated = __dadd_rn(rr[i].xb, d);
-                double diff = 0.0;
-                if (!(fabs(updated) <= kXbBound)) {
-                    err = DERR_OVERFLOW;
-                    errv = fabs(updated);
-                } else {
-                    diff = __dsub_rn(lexp(rr[i].len, updated), lexp(rr[i].len, rr[i].xb));
-                    era[row[i]].xb = updated;
+            for (int u = 0; u < kSU; ++u)
+                if (q0 + u * kT < ne) rr[u] = ld_rec(era + pr[u].x);
+#pragma unroll
+            for (int u = 0; u < kSU; ++u) {
+                const int q = q0 + u * kT;
+                if (q < ne) {
+                    const double updated = __dadd_rn(rr[u].xb, d);
+                    double diff = 0.0;
+                    if (!(fabs(updated) <= kXbBound)) {
+                        err = DERR_OVERFLOW;
+                        errv = fabs(updated);
+                    } else {
+                        diff = __dsub_rn(lexp(rr[u].len, updated), lexp(rr[u].len, rr[u].xb));
+                        era[pr[u].x].xb = updated;
+                    }
+                    X.x[q] = diff;
+                    X.sub[q] = pr[u].y;
                 }
-                sm.stage[q] = diff;
-                sm.ssub[q] = sj[i];
             }
         }
         __syncthreads();
-        const bool more = b + ne < p1;
-        const int after = more ? ld_pair(pairs + b + ne).y : -1;
-#pragma unroll
-        for (int i = 0; i < kSP; ++i) {
-            const int q = i * kT + static_cast<int>(threadIdx.x);
-            if (!hd[i]) continue;
-            const int s = sj[i];
-            double den = kSS ? T.den[s - T.base] : dn[i];
+        const int before = b > p0 ? ld_pair(pairs + b - 1).y : -1;
+        const int after = b + ne < p1 ? ld_pair(pairs + b + ne).y : -1;
+        for (int q = tid; q < ne; q += kT) {
+            const int s = X.sub[q];
+            if ((q > 0 ? X.sub[q - 1] : before) == s) continue;
+            double den = kSS ? T.den[s - T.base] : subj[s].den;
             int e = q;
-            while (e < ne && sm.ssub[e] == s) den = __dadd_rn(den, sm.stage[e++]);
+            while (e < ne && X.sub[e] == s) den = __dadd_rn(den, X.x[e++]);
             if (e == ne && after == s) {
                 sm.cr_den = den;
                 sm.cr_subj = s;
@@ -782,7 +767,7 @@ __device__ STREAM_FN UpdErr update_streamed(const ShardArgs& S, int64_t p0, int6
         if (cr_on) {
             double den = cr_den;
             int e = 0;
-            while (e < ne && sm.ssub[e] == cr_subj) den = __dadd_rn(den, sm.stage[e++]);
+            while (e < ne && X.sub[e] == cr_subj) den = __dadd_rn(den, X.x[e++]);
             if (e == ne && after == cr_subj) {
                 sm.cr_den = den;
                 sm.cr_subj = cr_subj;
@@ -800,7 +785,7 @@ __device__ STREAM_FN UpdErr update_streamed(const ShardArgs& S, int64_t p0, int6
 template <bool kSS, bool kST>
 __device__ __forceinline__ void gh_compute(const ShardArgs& S, const Cached& C, int64_t p0, int64_t p1,
                                            const HeadRegs& H, double& gs, double& hs, int& err, Smem& sm,
-                                           const SubjTile& T) {
+                                           const SubjTile& T, const StreamBuf X) {
     const int2* __restrict__ pairs = S.pairs;
     const int ncached = static_cast<int>(min(p1 - p0, static_cast<int64_t>(kCap)));
     if (threadIdx.x == 0) sm.cr_on = 0;
@@ -847,7 +832,7 @@ __device__ __forceinline__ void gh_compute(const ShardArgs& S, const Cached& C, 
     }
     if constexpr (kST) {
         if (p1 - p0 > kCap) {
-            const GhAcc a = gh_streamed<kSS>(S, p0, p0 + kCap, p1, GhAcc{gs, hs, err}, sm, T);
+            const GhAcc a = gh_streamed<kSS>(S, p0, p0 + kCap, p1, GhAcc{gs, hs, err}, sm, T, X);
             gs = a.gs;
             hs = a.hs;
             err = a.err;
@@ -858,7 +843,8 @@ __device__ __forceinline__ void gh_compute(const ShardArgs& S, const Cached& C, 
 template <bool kSS, bool kST>
 __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C, const HeadRegs& H, bool cached,
                                              int64_t p0, int64_t p1, double d, int& err, double& errv, Smem& sm,
-                                             const SubjTile& T, bool record = false, int* myht = nullptr) {
+                                             const SubjTile& T, const StreamBuf X, bool record = false,
+                                             int* myht = nullptr) {
     const int2* __restrict__ pairs = S.pairs;
     EraRec* era = S.era;
     SubjRec* subj = S.subj;
@@ -887,7 +873,6 @@ __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C
                 }
                 if (record) sm.jrow[pos] = C.slot[v].pr.x;
                 sm.stage[pos] = diff;
-                sm.ssub[pos] = C.slot[v].pr.y; // (a streamed grad/hess pass reused ssub)
             }
         }
         __syncthreads();
@@ -927,7 +912,7 @@ __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C
     if constexpr (kST) {
         const int64_t start = cached ? p0 + static_cast<int64_t>(kCap) : p0;
         if (start < p1) {
-            const UpdErr u = update_streamed<kSS>(S, p0, start, p1, d, UpdErr{err, errv}, sm, T);
+            const UpdErr u = update_streamed<kSS>(S, p0, start, p1, d, UpdErr{err, errv}, sm, T, X);
             err = u.err;
             errv = u.errv;
         }
@@ -956,6 +941,8 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
     SubjTile T{nullptr, nullptr, 0};
+    const StreamBuf X{reinterpret_cast<double*>(smem_raw + A.stream_off),
+                      reinterpret_cast<int*>(smem_raw + A.stream_off + sizeof(double) * A.stream_cap), A.stream_cap};
     int si = 0;
     while (si + 1 < A.nsh && static_cast<int>(blockIdx.x) >= A.sh[si + 1].cta_begin) ++si;
     const ShardArgs& S = A.sh[si];
@@ -973,7 +960,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
     if (A.mode == kModeUpdate) {
         const int j = A.single_j;
         const int64_t p0 = split_c[static_cast<int64_t>(j) * stride], p1 = split_c[static_cast<int64_t>(j) * stride + 1];
-        if constexpr (kST) update_slice<false, true>(S, C, H, false, p0, p1, A.single_delta, err, errv, sm, T);
+        if constexpr (kST) update_slice<false, true>(S, C, H, false, p0, p1, A.single_delta, err, errv, sm, T, X);
         if (err) record_error(S.err, err, errv);
         if (c == 0 && threadIdx.x == 0) S.beta[j] = __dadd_rn(S.beta[j], A.single_delta);
         return;
@@ -1005,7 +992,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         load_cached(S, p0, p1, C);
         double gs = 0.0, hs = 0.0;
         gather_records<false>(S, C, H);
-        gh_compute<false, kST>(S, C, p0, p1, H, gs, hs, err, sm, T);
+        gh_compute<false, kST>(S, C, p0, p1, H, gs, hs, err, sm, T, X);
         if (err) record_error(S.err, err, 0.0);
         block_reduce(gs, hs, err, false, sm);
         publish(A, seq, gs, hs, err);
@@ -1092,7 +1079,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                         gather_records<kSS>(S, C, H);
                     }
                 }
-                gh_compute<kSS, kST>(S, C, p0, p1, H, gs, hs, err, sm, T);
+                gh_compute<kSS, kST>(S, C, p0, p1, H, gs, hs, err, sm, T, X);
             }
             if (err) record_error(S.err, err, errv);
             // The publish below must not be observable before this
@@ -1198,7 +1185,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             if (delta != 0.0) {
                 ++nmoved;
                 if (!(A.dbg & 2))
-                    update_slice<kSS, kST>(S, C, H, true, p0, p1, delta, err, errv, sm, T, spec_next, myht);
+                    update_slice<kSS, kST>(S, C, H, true, p0, p1, delta, err, errv, sm, T, X, spec_next, myht);
             }
             __syncthreads(); // slice writes of this coordinate before the next reads
             if (tr && idx < A.ntrace) trb[idx * trs + 3] = gtimer();
@@ -1802,8 +1789,7 @@ void ensure_kernel_attrs(int device) {
     if (device < 32 && (done.load() & (1u << device))) return;
     CUDA_TRY(cudaFuncSetAttribute(k_ccd<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(sizeof(Smem))));
-    CUDA_TRY(cudaFuncSetAttribute(k_ccd<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(sizeof(Smem))));
+    CUDA_TRY(cudaFuncSetAttribute(k_ccd<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSweepSmem));
     CUDA_TRY(cudaFuncSetAttribute(k_ccd<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSweepSmem));
     CUDA_TRY(cudaFuncSetAttribute(k_ccd<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSweepSmem));
     if (device < 32) done.fetch_or(1u << device);
@@ -2289,18 +2275,38 @@ void launch_ccd(const ExchangePlan& plan, SweepArgs& a) {
     a.ss_cap = a.mode == kModeSweep ? subject_tile_cap(plan) : 0;
     a.prefetch = a.mode == kModeSweep ? prefetch_enabled(plan) : 0;
     // the streamed path only when some slice exceeds the register tiles
-    // (and always for the single-coordinate ops, whose update streams)
+    // (and always for the single-coordinate ops, whose update streams); its
+    // staging buffer takes the shared memory left beside the subject tile
+    // (up to kStreamMax pairs; the tile is dropped if that leaves too little)
     bool streamed = a.mode != kModeSweep;
     for (auto* st : plan.shards) streamed = streamed || st->ds->max_slice > kCap;
+    constexpr size_t kPairBytes = sizeof(double) + sizeof(int);
+    static const int kStreamMax = [] {
+        const char* e = std::getenv("BSCCS_STREAM_MAX"); // experiment hook
+        return e ? std::atoi(e) : 1536;
+    }();
+    auto base_bytes = [&] {
+        return a.ss_cap > 0 ? kSmemSubjOffset + static_cast<size_t>(a.ss_cap) * kPairBytes : sizeof(Smem);
+    };
+    size_t bytes = base_bytes();
+    a.stream_off = 0;
+    a.stream_cap = 0;
+    if (streamed) {
+        auto room = [&] { return (static_cast<size_t>(kMaxSweepSmem) - (base_bytes() + 15) / 16 * 16) / kPairBytes; };
+        if (a.ss_cap > 0 && room() < static_cast<size_t>(2 * kT)) a.ss_cap = 0;
+        const size_t off = (base_bytes() + 15) / 16 * 16;
+        const int cap = static_cast<int>(std::min<size_t>(room(), kStreamMax)) / kT * kT;
+        if (cap < kT) internal_error("sweep: no shared memory for the streamed-slice buffer");
+        a.stream_off = static_cast<int>(off);
+        a.stream_cap = cap;
+        bytes = off + static_cast<size_t>(cap) * kPairBytes;
+    }
     void* params[] = {&a};
     void* fn;
-    size_t bytes = sizeof(Smem);
-    if (a.ss_cap > 0) {
-        bytes = kSmemSubjOffset + static_cast<size_t>(a.ss_cap) * (sizeof(double) + sizeof(int));
+    if (a.ss_cap > 0)
         fn = streamed ? reinterpret_cast<void*>(k_ccd<true, true>) : reinterpret_cast<void*>(k_ccd<true, false>);
-    } else {
+    else
         fn = streamed ? reinterpret_cast<void*>(k_ccd<false, true>) : reinterpret_cast<void*>(k_ccd<false, false>);
-    }
     CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(plan_ctas(plan)), dim3(kSweepThreads), params, bytes, s0->stream));
     count_launches(1);
 }
