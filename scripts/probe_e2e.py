@@ -1,4 +1,6 @@
-"""Where the end-to-end step goes: dataset upload + device build, fit, free."""
+"""Where the end-to-end step goes (bench.py's e2e leg): dataset upload +
+device build from pinned host arrays, fit (state create, cycles, final
+rebuild), free -- wall time of each C-ABI call."""
 import sys
 import time
 sys.path[:0] = ['.', 'oracle']
@@ -6,32 +8,39 @@ import numpy as np
 import torch
 from paper_1208_0945_b200 import bsccs as B, datagen
 
-ds = datagen.config_dataset("1M")
+wl = sys.argv[1] if len(sys.argv) > 1 else "1M"
+ds = datagen.config_dataset(wl)
 prior = B.laplace_prior(0.1)
-nbytes = sum(a.nbytes for a in ds.arrays())
-for it in range(4):
+
+
+def pinned(a):
+    t = torch.empty(a.size, dtype={np.int32: torch.int32, np.int64: torch.int64}[a.dtype.type], pin_memory=True)
+    v = t.numpy()
+    v[:] = a
+    return t, v
+
+
+held = [pinned(a) for a in ds.arrays()]
+ds_host = B.Dataset(*[v for _, v in held])
+nbytes = sum(a.nbytes for a in ds_host.arrays())
+for it in range(5):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    d = B.DeviceDataset(ds, 0)
+    d = B.DeviceDataset(ds_host, 0)
     t1 = time.perf_counter()
     r = B.fit(d, prior)
     t2 = time.perf_counter()
     d.close()
     t3 = time.perf_counter()
-    print(f"create {1e3*(t1-t0):7.2f} ms ({nbytes/(t1-t0)/1e9:5.1f} GB/s)  fit {1e3*(t2-t1):7.2f} ms  "
-          f"destroy {1e3*(t3-t2):6.2f} ms", flush=True)
-# raw copy rates for the same bytes
-a = np.concatenate([x.view(np.uint8) for x in ds.arrays()])
-dev = torch.empty(a.size, dtype=torch.uint8, device="cuda")
-pin = torch.empty(a.size, dtype=torch.uint8, pin_memory=True)
-pin.numpy()[:] = a
-for name, src in [("pageable", torch.from_numpy(a)), ("pinned", pin)]:
-    for _ in range(2):
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        dev.copy_(src, non_blocking=False)
-        torch.cuda.synchronize()
-        t = time.perf_counter() - t0
-    print(f"H2D {name}: {a.size/t/1e9:.1f} GB/s", flush=True)
-import os
-print("host cpus", os.cpu_count(), len(os.sched_getaffinity(0)))
+    print(f"create {1e3*(t1-t0):7.2f} ms ({nbytes/(t1-t0)/1e9:5.1f} GB/s)  fit {1e3*(t2-t1):7.2f} ms "
+          f"(device {1e3*r.device_seconds:6.2f}, sweeps {1e3*r.sweep_seconds:6.2f})  destroy {1e3*(t3-t2):6.2f} ms",
+          flush=True)
+dev = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+pin = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+for _ in range(3):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    dev.copy_(pin, non_blocking=False)
+    torch.cuda.synchronize()
+    t = time.perf_counter() - t0
+print(f"raw pinned H2D of the same bytes: {1e3*t:.2f} ms ({nbytes/t/1e9:.1f} GB/s)", flush=True)
