@@ -2,6 +2,7 @@
 # Bench lines and many-fit logs kept under profiles/ (one B200).
 mkdir -p gpurun_out/r
 python bench.py > gpurun_out/r/bench_1M.json 2> gpurun_out/r/bench_1M.err
+python bench.py --zipf --no-many-fit > gpurun_out/r/bench_1M_zipf.json 2> gpurun_out/r/bench_1M_zipf.err
 python bench.py --workload 10M --steps 3 --warmup 3 --no-cpu-baseline --no-many-fit > gpurun_out/r/bench_10M.json 2> gpurun_out/r/bench_10M.err
 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/r/bench_reference_1M.json 2> gpurun_out/r/bench_reference_1M.err
 python scripts/bench_batch.py --cv --subset > gpurun_out/r/bench_batch_1M.log 2>&1

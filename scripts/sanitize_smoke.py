@@ -11,6 +11,12 @@ from paper_1208_0945_b200 import _native, bootstrap as BT, bsccs as B, cross_val
 ds = datagen.fast_sccs(3000, 20, 3.0)
 dds = ds.on_device()
 r = B.fit(dds, B.laplace_prior(0.1))
+few = B.DeviceDataset(ds, 0, 2)  # two CTAs: slices beyond the register tiles take the streamed path
+B.fit(few, B.laplace_prior(0.1))
+stf = B.init_state(few)
+B.fused_grad_hess(few, stf, 1)
+B.sparse_delta_update(few, stf, 1, 0.05)
+few.close()
 B.fit(dds, B.normal_prior(0.1), B.SolverConfig(path=B.UpdatePath.dense))
 st = B.init_state(dds)
 B.fused_grad_hess(dds, st, 3)
