@@ -207,3 +207,21 @@ def test_streamed_slices_beyond_register_tiles(ctas):
         assert res.cycles_run == exp["cycles_run"]
         assert np.all(np.abs(res.beta_map - exp["beta"]) <= np.maximum(1e-8 * np.abs(exp["beta"]), 1e-11))
         assert rel_gap(res.log_posterior, exp["log_posterior"]) < 1e-10
+
+
+def test_streamed_sweep_without_subject_tile():
+    """One CTA owning ~25k subjects: too many for the shared-memory subject
+    tile, so the sweep runs the instantiation with subject records in HBM and
+    the streamed path (k_ccd<0,1>), against the oracle."""
+    import pyoracle
+    from paper_1208_0945_b200 import datagen
+    ds = datagen.fast_sccs(26_000, 6, 3.0)
+    assert ds.num_subjects > 20_000
+    dds = B.DeviceDataset(ds, 0, 1)
+    port = pyoracle.Port()
+    for prior in (B.laplace_prior(0.1), B.normal_prior(0.5)):
+        res = B.fit(dds, prior)
+        exp = port.fit(ds, prior, B.SolverConfig())
+        assert res.cycles_run == exp["cycles_run"]
+        assert np.all(np.abs(res.beta_map - exp["beta"]) <= np.maximum(1e-8 * np.abs(exp["beta"]), 1e-11))
+        assert rel_gap(res.log_posterior, exp["log_posterior"]) < 1e-10
