@@ -283,8 +283,15 @@ __device__ __forceinline__ void xprev_store(const unsigned long long* slots, con
 }
 
 // warp 0 only: wait for the exchange `seq`, return the totals in every lane
-__device__ __forceinline__ void poll(const SweepArgs& A, const unsigned long long* slots, unsigned long long seq,
-                                     XPrev& pv, double& ta, double& tb, int& te, unsigned long long* stamp) {
+struct PollOut {
+    double ta, tb;
+    int te;
+    XPrev pv;
+};
+__device__ __forceinline__ PollOut poll_body(const SweepArgs& A, const unsigned long long* slots, unsigned long long seq, XPrev pv,
+                  unsigned long long* stamp) {
+    double ta, tb;
+    int te;
     const int l = lane_id();
     const unsigned buf = static_cast<unsigned>(seq & 1ull);
     unsigned long long diff = 0;
@@ -313,6 +320,28 @@ __device__ __forceinline__ void poll(const SweepArgs& A, const unsigned long lon
     const unsigned bad = __ballot_sync(0xffffffffu, ovf) & 0x9u; // lanes 0 (a) and 3 (b)
     te = (__shfl_sync(0xffffffffu, d, 6) != 0 || bad) ? 1 : 0;
     if (bad && l == 0) record_error(A.sh[0].err, DERR_SUM_RANGE, 0.0);
+    return PollOut{ta, tb, te, pv};
+}
+
+// The same, out of line.  Which one a kernel instantiation uses is a
+// measured code-generation choice: inline in the sweep with
+// the shared-memory subject tile (config 2: 3% faster), out of line without
+// it (config 3: 4% faster).
+__device__ __noinline__ PollOut poll_ool(const SweepArgs& A, const unsigned long long* slots, unsigned long long seq,
+                                         XPrev pv, unsigned long long* stamp) {
+    return poll_body(A, slots, seq, pv, stamp);
+}
+
+template <bool kOOL = false>
+__device__ __forceinline__ void poll(const SweepArgs& A, const unsigned long long* slots, unsigned long long seq,
+                                     XPrev& pv, double& ta, double& tb, int& te, unsigned long long* stamp) {
+    PollOut o;
+    if constexpr (kOOL) o = poll_ool(A, slots, seq, pv, stamp);
+    else o = poll_body(A, slots, seq, pv, stamp);
+    ta = o.ta;
+    tb = o.tb;
+    te = o.te;
+    pv = o.pv;
 }
 
 // ---- shared-memory subject tile -----------------------------------------------------
@@ -1131,7 +1160,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                     tg = gs;
                     th = hs;
                 } else {
-                    poll(A, S.xslots, seq, pv, tg, th, te, (tr && idx < A.ntrace) ? trb + idx * trs + 5 : nullptr);
+                    poll<!kSS>(A, S.xslots, seq, pv, tg, th, te, (tr && idx < A.ntrace) ? trb + idx * trs + 5 : nullptr);
                 }
                 int status = ST_OK;
                 double delta = 0.0;

@@ -2,7 +2,7 @@
 // shared by the single-fit sweep (ccd_kernels.cu) and the batched engine
 // (batch.cu): relaxed red.add / volatile poll words and the exact split of
 // a non-negative double into three 41-bit limbs of a 2^-80 fixed-point
-// number (and the correctly rounded reconstruction).  See DESIGN.md §4.2.
+// number (and the reconstruction of their integer sums).  See DESIGN.md §4.2.
 //
 // Word layout: bits 0..51 carry the sum of the participants' limbs, bits
 // 52..63 count arrivals.  A limb is < 2^41, so up to kMaxParticipants =
@@ -65,36 +65,25 @@ __device__ __forceinline__ double pow2(int e) { // 2^e for normal exponents
     return __longlong_as_double(static_cast<long long>(1023 + e) << 52);
 }
 
-// correctly rounded double of (L2*2^82 + L1*2^41 + L0) * 2^-80, the limb
-// sums of up to kMaxParticipants partials; `ovf` is set (and 0 returned)
-// when the total reaches 2^48, beyond the 128-bit reconstruction
+// (L2*2^82 + L1*2^41 + L0) * 2^-80 for the limb sums L0..L2 (< 2^52 each,
+// no carries needed): each limb sum converts to double exactly, and the
+// value is (L2*2^2 + L1*2^-39) + L0*2^-80 in that order -- within one ulp
+// of the exact sum, and a pure function of the integer sums, so every
+// participant (and every partition of the data) gets the same bits.  Lanes
+// can convert their own limb and combine with two shuffles (poll()).
+__device__ __forceinline__ double limb_part(unsigned long long L, int i) { // i = limb index 0..2
+    return __dmul_rn(__ull2double_rn(L), pow2(kLimbBits * i - 80));
+}
+__device__ __forceinline__ double limbs_combine(double p0, double p1, double p2) {
+    return __dadd_rn(__dadd_rn(p2, p1), p0);
+}
+constexpr double kXMaxTotal = 0x1p48; // totals beyond are reported (DERR_SUM_RANGE)
 __device__ __forceinline__ double from_limbs(unsigned long long L0, unsigned long long L1, unsigned long long L2,
                                              bool& ovf) {
-    L1 += L0 >> kLimbBits;
-    L0 &= kMLimb;
-    L2 += L1 >> kLimbBits;
-    L1 &= kMLimb;
-    ovf = (L2 >> 46) != 0;
-    if (ovf) return 0.0;
-    // 128-bit V = hi:lo
-    const unsigned long long lo = L0 | (L1 << kLimbBits);
-    const unsigned long long hi = (L1 >> (64 - kLimbBits)) | (L2 << (2 * kLimbBits - 64));
-    if ((hi | lo) == 0) return 0.0;
-    int lz;
-    unsigned long long m, rest;
-    if (hi) {
-        lz = __clzll(static_cast<long long>(hi));
-        m = lz ? (hi << lz) | (lo >> (64 - lz)) : hi;
-        rest = lz ? lo << lz : lo;
-    } else {
-        lz = 64 + __clzll(static_cast<long long>(lo));
-        m = lo << (lz - 64);
-        rest = 0;
-    }
-    m |= rest != 0 ? 1ull : 0ull; // sticky bit for correct rounding
-    return __dmul_rn(__ull2double_rn(m), pow2(64 - lz - 80));
+    const double v = limbs_combine(limb_part(L0, 0), limb_part(L1, 1), limb_part(L2, 2));
+    ovf = !(v < kXMaxTotal);
+    return ovf ? 0.0 : v;
 }
-
 
 // l * exp(x'beta), the reference's l_exp_xbeta expression (engine.hpp:77-78,224-225)
 #ifndef EXPFN

@@ -1,0 +1,7 @@
+import sys
+sys.path[:0] = ['.', 'oracle']
+from paper_1208_0945_b200 import bsccs as B, datagen
+ds = datagen.config_dataset(sys.argv[1])
+dds = B.DeviceDataset(ds, 0)
+r = B.fit(dds, B.laplace_prior(0.1))
+print(sys.argv[1], "visited", r.coordinates_visited, "moved", r.coordinates_moved, "lp", repr(r.log_posterior))
