@@ -354,9 +354,13 @@ __device__ __forceinline__ void poll(const SweepArgs& A, const unsigned long lon
 // CTA-owned (nnz-balanced subject ranges), so no other CTA touches them.
 struct SubjTile {
     double* den;
+    int2* touch; // per subject: {stamp of the coordinate whose update touched it, run pos | len << 16}
     int* n;
     int base;
 };
+// bytes per subject of the tile: den, n, and (instantiations without the
+// streamed path) the touch entry that replaces the repair hash table
+constexpr size_t subj_tile_bytes(bool touch) { return sizeof(double) + sizeof(int) + (touch ? sizeof(int2) : 0); }
 
 // ---- pair slots -------------------------------------------------------------------
 
@@ -568,21 +572,29 @@ __device__ __forceinline__ int ht_hash(int s) {
 // update wrote: a subject found in the table was touched, so its head takes
 // the new denominator and any of its eras among the updated rows takes the
 // new (x'beta, l*exp).  Shared-memory only.
-template <bool kSS>
-__device__ __forceinline__ void repair(const Cached& C, HeadRegs& H, const Smem& sm) {
+template <bool kSS, bool kTouch>
+__device__ __forceinline__ void repair(const Cached& C, HeadRegs& H, const Smem& sm, const SubjTile& T,
+                                       int stamp_prev) {
 #pragma unroll
     for (int v = 0; v < kCached; ++v) {
         if (!slot_valid(C.slot[v])) continue;
         const int s = C.slot[v].pr.y;
-        int h = ht_hash(s);
-        int k;
-        for (;;) {
-            k = sm.htk[h];
-            if (k == s || k == -1) break;
-            h = (h + 1) & (kHt - 1);
+        int val;
+        if constexpr (kTouch) { // direct-mapped: the subject's entry carries the stamp of its last update
+            const int2 tc = T.touch[s - T.base];
+            if (tc.x != stamp_prev) continue;
+            val = tc.y;
+        } else {
+            int h = ht_hash(s);
+            int k;
+            for (;;) {
+                k = sm.htk[h];
+                if (k == s || k == -1) break;
+                h = (h + 1) & (kHt - 1);
+            }
+            if (k != s) continue;
+            val = sm.htv[h];
         }
-        if (k != s) continue;
-        const int val = sm.htv[h];
         const int posj = val & 0xffff, runj = val >> 16;
         if (!kSS && C.slot[v].head) H.den[v] = sm.jden[posj];
         const int row = C.slot[v].pr.x;
@@ -873,7 +885,7 @@ template <bool kSS, bool kST>
 __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C, const HeadRegs& H, bool cached,
                                              int64_t p0, int64_t p1, double d, int& err, double& errv, Smem& sm,
                                              const SubjTile& T, const StreamBuf X, bool record = false,
-                                             int* myht = nullptr) {
+                                             int* myht = nullptr, int stamp = 0) {
     const int2* __restrict__ pairs = S.pairs;
     EraRec* era = S.era;
     SubjRec* subj = S.subj;
@@ -928,12 +940,16 @@ __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C
                 if constexpr (kSS) T.den[C.slot[v].pr.y - T.base] = den;
                 else subj[C.slot[v].pr.y].den = den;
                 if (record) { // publish (subject -> run) for the next coordinate's repair
-                    if constexpr (!kSS) sm.jden[pos] = den;
                     const int s = C.slot[v].pr.y;
-                    int h = ht_hash(s);
-                    while (atomicCAS(&sm.htk[h], -1, s) != -1) h = (h + 1) & (kHt - 1);
-                    sm.htv[h] = pos | ((q - pos) << 16);
-                    myht[v] = h;
+                    if constexpr (kSS && !kST) {
+                        T.touch[s - T.base] = make_int2(stamp, pos | ((q - pos) << 16));
+                    } else {
+                        if constexpr (!kSS) sm.jden[pos] = den;
+                        int h = ht_hash(s);
+                        while (atomicCAS(&sm.htk[h], -1, s) != -1) h = (h + 1) & (kHt - 1);
+                        sm.htv[h] = pos | ((q - pos) << 16);
+                        myht[v] = h;
+                    }
                 }
             }
         }
@@ -1060,11 +1076,13 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             T.base = S.cta_subj[c];
             const int ns = S.cta_subj[c + 1] - T.base;
             T.den = reinterpret_cast<double*>(smem_raw + kSmemSubjOffset);
-            T.n = reinterpret_cast<int*>(T.den + A.ss_cap);
+            T.touch = kST ? nullptr : reinterpret_cast<int2*>(T.den + A.ss_cap);
+            T.n = kST ? reinterpret_cast<int*>(T.den + A.ss_cap) : reinterpret_cast<int*>(T.touch + A.ss_cap);
             for (int t = threadIdx.x; t < ns; t += kT) {
                 const Subj sr = ld_subj(S.subj + T.base + t);
                 T.den[t] = sr.den;
                 T.n[t] = sr.n;
+                if constexpr (!kST) T.touch[t] = make_int2(0, 0);
             }
         }
         const longlong2 z2 = make_longlong2(0, 0);
@@ -1103,7 +1121,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                 if (!idle) {
                     if (spec) {
                         if (A.dbg & 64) finish_records(C, H);
-                        repair<kSS>(C, H, sm);
+                        repair<kSS, kSS && !kST>(C, H, sm, T, idx); // stamps: coordinate idx-1 wrote idx
                     } else {
                         gather_records<kSS>(S, C, H);
                     }
@@ -1214,7 +1232,8 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             if (delta != 0.0) {
                 ++nmoved;
                 if (!(A.dbg & 2))
-                    update_slice<kSS, kST>(S, C, H, true, p0, p1, delta, err, errv, sm, T, X, spec_next, myht);
+                    update_slice<kSS, kST>(S, C, H, true, p0, p1, delta, err, errv, sm, T, X, spec_next, myht,
+                                           idx + 1);
             }
             __syncthreads(); // slice writes of this coordinate before the next reads
             if (tr && idx < A.ntrace) trb[idx * trs + 3] = gtimer();
@@ -2262,7 +2281,7 @@ int plan_ctas(const ExchangePlan& plan) {
 
 // Sweeps keep each CTA's subject records in shared memory when every
 // shard's largest CTA subject range fits (BSCCS_SUBJ_SMEM=0 disables it).
-int subject_tile_cap(const ExchangePlan& plan) {
+int subject_tile_cap(const ExchangePlan& plan, bool streamed) {
     static const bool enabled = [] {
         const char* e = std::getenv("BSCCS_SUBJ_SMEM");
         return !(e && e[0] == '0');
@@ -2270,8 +2289,8 @@ int subject_tile_cap(const ExchangePlan& plan) {
     if (!enabled) return 0;
     int m = 0;
     for (auto* st : plan.shards) m = std::max(m, st->ds->max_cta_subjects);
-    const int cap = (m + 1) / 2 * 2; // keeps the int array 8-byte aligned
-    const size_t bytes = kSmemSubjOffset + static_cast<size_t>(cap) * (sizeof(double) + sizeof(int));
+    const int cap = (m + 1) / 2 * 2; // keeps the arrays 8-byte aligned
+    const size_t bytes = kSmemSubjOffset + static_cast<size_t>(cap) * subj_tile_bytes(!streamed);
     return bytes <= static_cast<size_t>(kMaxSweepSmem) ? std::max(cap, 2) : 0;
 }
 
@@ -2301,21 +2320,22 @@ int prefetch_enabled(const ExchangePlan& plan) {
 void launch_ccd(const ExchangePlan& plan, SweepArgs& a) {
     bsccs_state* s0 = plan.shards[0];
     ensure_kernel_attrs(s0->ds->device);
-    a.ss_cap = a.mode == kModeSweep ? subject_tile_cap(plan) : 0;
-    a.prefetch = a.mode == kModeSweep ? prefetch_enabled(plan) : 0;
     // the streamed path only when some slice exceeds the register tiles
     // (and always for the single-coordinate ops, whose update streams); its
     // staging buffer takes the shared memory left beside the subject tile
     // (up to kStreamMax pairs; the tile is dropped if that leaves too little)
     bool streamed = a.mode != kModeSweep;
     for (auto* st : plan.shards) streamed = streamed || st->ds->max_slice > kCap;
+    a.ss_cap = a.mode == kModeSweep ? subject_tile_cap(plan, streamed) : 0;
+    a.prefetch = a.mode == kModeSweep ? prefetch_enabled(plan) : 0;
     constexpr size_t kPairBytes = sizeof(double) + sizeof(int);
     static const int kStreamMax = [] {
         const char* e = std::getenv("BSCCS_STREAM_MAX"); // experiment hook
         return e ? std::atoi(e) : 1536;
     }();
     auto base_bytes = [&] {
-        return a.ss_cap > 0 ? kSmemSubjOffset + static_cast<size_t>(a.ss_cap) * kPairBytes : sizeof(Smem);
+        return a.ss_cap > 0 ? kSmemSubjOffset + static_cast<size_t>(a.ss_cap) * subj_tile_bytes(!streamed)
+                            : sizeof(Smem);
     };
     size_t bytes = base_bytes();
     a.stream_off = 0;
