@@ -704,6 +704,14 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
         double ch = 0.0, mg = 0.0;
         if (flive) {
             const int e0 = A.subject_offsets[A.cta_subj[c]], e1 = A.subject_offsets[A.cta_subj[c + 1]];
+            // software-pipelined: the next block's era -> subject map loads
+            // while this block's multiplicities (which depend on it) load
+            int es[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int k = e0 + qfirst + u * QS;
+                es[u] = k < e1 ? __ldg(&A.era_subj[k]) : 0;
+            }
             for (int base = e0 + qfirst; base < e1; base += U * QS) {
                 double x[U], sn[U];
                 int mm[U];
@@ -714,8 +722,13 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
                         const size_t o = static_cast<size_t>(k) * RB + fit;
                         x[u] = A.xb[o];
                         sn[u] = A.snap[o];
-                        mm[u] = A.m[static_cast<size_t>(__ldg(&A.era_subj[k])) * RB + fit];
+                        mm[u] = A.m[static_cast<size_t>(es[u]) * RB + fit];
                     }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int k = base + U * QS + u * QS;
+                    es[u] = k < e1 ? __ldg(&A.era_subj[k]) : 0;
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
