@@ -118,6 +118,7 @@ struct SweepArgs {
     double red_a, red_b; // kModeReduce inputs (this rank's values)
     int prefetch; // L2 prefetch of the records two coordinates ahead (small slices only)
     int stream_off, stream_cap; // streamed-slice staging buffer in dynamic shared memory (bytes offset, pairs)
+    int bm_words; // touched-subject bitmaps (words each) instead of the hash table (no subject tile)
     int ss_cap; // capacity of the shared-memory subject tile (0: subjects stay in HBM)
     int dbg; // profiling only: bit0 skip grad/hess, bit1 skip update, bit2 skip exchange, bit4 no speculation
     unsigned long long* trace; // profiling only: [ntrace][gridDim][kTr] globaltimer stamps
@@ -138,7 +139,7 @@ struct Smem {
     // what the previous coordinate's update changed, for repairing the
     // speculatively gathered records of the next coordinate
     double jxb[kCap], jle[kCap], jden[kCap];
-    int jrow[kCap];
+    int jrow[kCap], jsub[kCap];
     int htk[kHt], htv[kHt];
     double ra[kWarps], rb[kWarps];
     int re[kWarps];
@@ -572,9 +573,22 @@ __device__ __forceinline__ int ht_hash(int s) {
 // update wrote: a subject found in the table was touched, so its head takes
 // the new denominator and any of its eras among the updated rows takes the
 // new (x'beta, l*exp).  Shared-memory only.
+// Touched-subject bitmaps (one bit per subject of the CTA's range, two
+// alternating by coordinate parity): the update sets its heads' bits with one
+// atomicOr each; the repair tests a bit and, for the few touched subjects,
+// finds the run by binary search in the previous slice's subjects (a slice
+// is in ascending subject order).  Used when the subject tile does not fit.
+struct TouchBits {
+    unsigned* b0; // even coordinates' marks
+    unsigned* b1; // odd
+    int base;
+    __device__ __forceinline__ unsigned* of(int parity) const { return parity ? b1 : b0; }
+};
+
 template <bool kSS, bool kTouch>
 __device__ __forceinline__ void repair(const Cached& C, HeadRegs& H, const Smem& sm, const SubjTile& T,
-                                       int stamp_prev) {
+                                       int stamp_prev, const unsigned* bmprev = nullptr, int bbase = 0,
+                                       int nprev = 0) {
 #pragma unroll
     for (int v = 0; v < kCached; ++v) {
         if (!slot_valid(C.slot[v])) continue;
@@ -584,6 +598,18 @@ __device__ __forceinline__ void repair(const Cached& C, HeadRegs& H, const Smem&
             const int2 tc = T.touch[s - T.base];
             if (tc.x != stamp_prev) continue;
             val = tc.y;
+        } else if (bmprev) {
+            const int t = s - bbase;
+            if (!((bmprev[t >> 5] >> (t & 31)) & 1u)) continue;
+            int lo = 0, hi = nprev; // first position of subject s in the previous slice
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (sm.jsub[mid] < s) lo = mid + 1;
+                else hi = mid;
+            }
+            int e = lo;
+            while (e < nprev && sm.jsub[e] == s) ++e;
+            val = lo | ((e - lo) << 16);
         } else {
             int h = ht_hash(s);
             int k;
@@ -885,7 +911,8 @@ template <bool kSS, bool kST>
 __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C, const HeadRegs& H, bool cached,
                                              int64_t p0, int64_t p1, double d, int& err, double& errv, Smem& sm,
                                              const SubjTile& T, const StreamBuf X, bool record = false,
-                                             int* myht = nullptr, int stamp = 0) {
+                                             int* myht = nullptr, int stamp = 0, unsigned* bmcur = nullptr,
+                                             int bbase = 0) {
     const int2* __restrict__ pairs = S.pairs;
     EraRec* era = S.era;
     SubjRec* subj = S.subj;
@@ -912,7 +939,10 @@ __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C
                         sm.jle[pos] = fresh;
                     }
                 }
-                if (record) sm.jrow[pos] = C.slot[v].pr.x;
+                if (record) {
+                    sm.jrow[pos] = C.slot[v].pr.x;
+                    if constexpr (!kSS) sm.jsub[pos] = C.slot[v].pr.y;
+                }
                 sm.stage[pos] = diff;
             }
         }
@@ -945,10 +975,15 @@ __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C
                         T.touch[s - T.base] = make_int2(stamp, pos | ((q - pos) << 16));
                     } else {
                         if constexpr (!kSS) sm.jden[pos] = den;
-                        int h = ht_hash(s);
-                        while (atomicCAS(&sm.htk[h], -1, s) != -1) h = (h + 1) & (kHt - 1);
-                        sm.htv[h] = pos | ((q - pos) << 16);
-                        myht[v] = h;
+                        if (!kSS && bmcur) {
+                            const int t = s - bbase;
+                            atomicOr(&bmcur[t >> 5], 1u << (t & 31));
+                        } else {
+                            int h = ht_hash(s);
+                            while (atomicCAS(&sm.htk[h], -1, s) != -1) h = (h + 1) & (kHt - 1);
+                            sm.htv[h] = pos | ((q - pos) << 16);
+                            myht[v] = h;
+                        }
                     }
                 }
             }
@@ -1072,6 +1107,14 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
     const bool w0 = threadIdx.x < 32;
     if (V > 0) {
         for (int i = threadIdx.x; i < kHt; i += kT) sm.htk[i] = -1;
+        TouchBits TB{nullptr, nullptr, 0};
+        if (!kSS && A.bm_words > 0) {
+            TB.base = S.cta_subj[c];
+            TB.b0 = reinterpret_cast<unsigned*>(smem_raw + kSmemSubjOffset);
+            TB.b1 = TB.b0 + A.bm_words;
+            for (int i = threadIdx.x; i < 2 * A.bm_words; i += kT) TB.b0[i] = 0u;
+        }
+        int nprev = 0; // slice length of the previous coordinate (its record's extent)
         if constexpr (kSS) {
             T.base = S.cta_subj[c];
             const int ns = S.cta_subj[c + 1] - T.base;
@@ -1121,7 +1164,8 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                 if (!idle) {
                     if (spec) {
                         if (A.dbg & 64) finish_records(C, H);
-                        repair<kSS, kSS && !kST>(C, H, sm, T, idx); // stamps: coordinate idx-1 wrote idx
+                        repair<kSS, kSS && !kST>(C, H, sm, T, idx, // stamps: coordinate idx-1 wrote idx
+                                                 TB.b0 ? TB.of((idx + 1) & 1) : nullptr, TB.base, nprev);
                     } else {
                         gather_records<kSS>(S, C, H);
                     }
@@ -1145,6 +1189,10 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             }
             if (tr && idx < A.ntrace) trb[idx * trs + 1] = gtimer();
             if (!(A.dbg & 4)) publish(A, seq, gs, hs, e);
+            if (TB.b0) { // the previous coordinate's marks were read above: clear them for the next update
+                unsigned* b = TB.of((idx + 1) & 1);
+                for (int i = threadIdx.x; i < A.bm_words; i += kT) b[i] = 0u;
+            }
             // while the partials travel
             RawCached NR;
             // the speculative gathers go out first (they are on the critical
@@ -1233,7 +1281,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                 ++nmoved;
                 if (!(A.dbg & 2))
                     update_slice<kSS, kST>(S, C, H, true, p0, p1, delta, err, errv, sm, T, X, spec_next, myht,
-                                           idx + 1);
+                                           idx + 1, TB.b0 ? TB.of(idx & 1) : nullptr, TB.base);
             }
             __syncthreads(); // slice writes of this coordinate before the next reads
             if (tr && idx < A.ntrace) trb[idx * trs + 3] = gtimer();
@@ -1241,6 +1289,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             finalize_cached(NR, N);
             H = SH;
             spec = spec_next;
+            nprev = static_cast<int>(p1 - p0);
             cur = nxt;
             nxt = nxt2;
             nxt2 = nxt3;
@@ -1835,8 +1884,7 @@ constexpr int kMaxSweepSmem = 225 * 1024; // opt-in dynamic shared memory per CT
 void ensure_kernel_attrs(int device) {
     static std::atomic<unsigned> done{0};
     if (device < 32 && (done.load() & (1u << device))) return;
-    CUDA_TRY(cudaFuncSetAttribute(k_ccd<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(sizeof(Smem))));
+    CUDA_TRY(cudaFuncSetAttribute(k_ccd<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSweepSmem));
     CUDA_TRY(cudaFuncSetAttribute(k_ccd<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSweepSmem));
     CUDA_TRY(cudaFuncSetAttribute(k_ccd<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSweepSmem));
     CUDA_TRY(cudaFuncSetAttribute(k_ccd<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSweepSmem));
@@ -2327,6 +2375,17 @@ void launch_ccd(const ExchangePlan& plan, SweepArgs& a) {
     bool streamed = a.mode != kModeSweep;
     for (auto* st : plan.shards) streamed = streamed || st->ds->max_slice > kCap;
     a.ss_cap = a.mode == kModeSweep ? subject_tile_cap(plan, streamed) : 0;
+    a.bm_words = 0;
+    if (a.mode == kModeSweep && a.ss_cap == 0) { // touched-subject bitmaps instead of the hash table
+        int m = 0;
+        for (auto* st : plan.shards) m = std::max(m, st->ds->max_cta_subjects);
+        const int words = (m + 31) / 32 + 1;
+        static const bool bm_on = [] {
+            const char* e = std::getenv("BSCCS_TOUCH_BITS"); // experiment hook
+            return !(e && e[0] == '0');
+        }();
+        if (bm_on && 2 * static_cast<size_t>(words) * sizeof(unsigned) <= 64 * 1024) a.bm_words = words;
+    }
     a.prefetch = a.mode == kModeSweep ? prefetch_enabled(plan) : 0;
     constexpr size_t kPairBytes = sizeof(double) + sizeof(int);
     static const int kStreamMax = [] {
@@ -2335,7 +2394,8 @@ void launch_ccd(const ExchangePlan& plan, SweepArgs& a) {
     }();
     auto base_bytes = [&] {
         return a.ss_cap > 0 ? kSmemSubjOffset + static_cast<size_t>(a.ss_cap) * subj_tile_bytes(!streamed)
-                            : sizeof(Smem);
+               : a.bm_words > 0 ? kSmemSubjOffset + 2 * static_cast<size_t>(a.bm_words) * sizeof(unsigned)
+                                : sizeof(Smem);
     };
     size_t bytes = base_bytes();
     a.stream_off = 0;

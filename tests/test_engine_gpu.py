@@ -225,3 +225,21 @@ def test_streamed_sweep_without_subject_tile():
         assert res.cycles_run == exp["cycles_run"]
         assert np.all(np.abs(res.beta_map - exp["beta"]) <= np.maximum(1e-8 * np.abs(exp["beta"]), 1e-11))
         assert rel_gap(res.log_posterior, exp["log_posterior"]) < 1e-10
+
+
+def test_speculative_sweep_without_subject_tile():
+    """Eight CTAs owning ~12k subjects each (too many for the shared-memory
+    subject tile) with slices inside the register tiles: the speculative
+    sweep with the touched-subject bitmaps (k_ccd<0,0>), against the oracle."""
+    import pyoracle
+    from paper_1208_0945_b200 import datagen
+    ds = datagen.fast_sccs(100_000, 200, 0.5)
+    dds = B.DeviceDataset(ds, 0, 8)
+    assert max(np.diff(ds.col_ptr)) < 8 * 900  # slices fit the register tiles
+    port = pyoracle.Port()
+    for prior in (B.laplace_prior(0.1), B.normal_prior(0.5)):
+        res = B.fit(dds, prior)
+        exp = port.fit(ds, prior, B.SolverConfig())
+        assert res.cycles_run == exp["cycles_run"]
+        assert np.all(np.abs(res.beta_map - exp["beta"]) <= np.maximum(1e-8 * np.abs(exp["beta"]), 1e-11))
+        assert rel_gap(res.log_posterior, exp["log_posterior"]) < 1e-10
