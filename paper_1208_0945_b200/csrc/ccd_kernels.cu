@@ -1674,27 +1674,51 @@ __global__ void k_interleave(const int32_t* rows, const int32_t* subjects, int2*
 // column of every pair (upper_bound on col_ptr), row histogram, and the
 // structural checks of build_dataset (dataset.hpp:135-175): row in range,
 // subject in range and owning the row, rows strictly ascending in a column.
+// Per pair: its column (for the row-major copy), and the build_dataset
+// checks (dataset.hpp:135-175): row / subject in range, the subject owns
+// the row, rows strictly ascending within the column.  Each block walks a
+// contiguous pair range and finds the column of its first pair once; the
+// threads then advance their column monotonically (no per-pair search, no
+// atomics -- the CSR row pointers come from the sorted keys afterwards).
 __global__ void k_pair_meta(const int2* pairs, const int64_t* __restrict__ col_ptr, int32_t J,
                             const int32_t* __restrict__ off, int32_t N, int32_t K, int64_t nnz, int32_t* col_of,
-                            unsigned long long* row_cnt, int* bad) {
-    for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < nnz;
-         p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        int lo = 0, hi = J; // first j with col_ptr[j+1] > p
+                            int* bad) {
+    const int64_t per = (nnz + gridDim.x - 1) / gridDim.x;
+    const int64_t b0 = static_cast<int64_t>(blockIdx.x) * per, b1 = min(nnz, b0 + per);
+    if (b0 >= b1) return;
+    __shared__ int jc0;
+    if (threadIdx.x == 0) {
+        int lo = 0, hi = J; // first j with col_ptr[j+1] > b0
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
-            if (col_ptr[mid + 1] > p) hi = mid;
+            if (col_ptr[mid + 1] > b0) hi = mid;
             else lo = mid + 1;
         }
-        col_of[p] = lo;
+        jc0 = lo;
+    }
+    __syncthreads();
+    int jc = jc0;
+    int nbad = 0;
+    for (int64_t p = b0 + threadIdx.x; p < b1; p += blockDim.x) {
+        while (col_ptr[jc + 1] <= p) ++jc;
+        col_of[p] = jc;
         const int2 pr = pairs[p];
         bool ok = pr.x >= 0 && pr.x < K && pr.y >= 0 && pr.y < N;
         if (ok) ok = off[pr.y] <= pr.x && pr.x < off[pr.y + 1];
-        if (ok && p > col_ptr[lo]) ok = pairs[p - 1].x < pr.x;
-        if (!ok) {
-            atomicOr(bad, 1);
-        } else {
-            atomicAdd(row_cnt + pr.x, 1ull);
-        }
+        if (ok && p > col_ptr[jc]) ok = pairs[p - 1].x < pr.x;
+        nbad |= ok ? 0 : 1;
+    }
+    if (__syncthreads_or(nbad) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+
+// CSR row pointers from the row-sorted keys: csr_ptr[k] = first sorted
+// position with row >= k (= the exclusive scan of the row counts).
+__global__ void k_csr_ptr(const int32_t* __restrict__ sorted_rows, int64_t nnz, int32_t K, int64_t* csr_ptr) {
+    for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p <= nnz;
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int r = p < nnz ? sorted_rows[p] : K;
+        const int rp = p > 0 ? sorted_rows[p - 1] : -1;
+        for (int k = rp + 1; k <= r; ++k) csr_ptr[k] = p;
     }
 }
 
@@ -1944,24 +1968,20 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
     cudaStream_t s = ds->stream;
     int64_t scratch_bytes = 0;
     int32_t* d_col = dalloc<int32_t>(nnz, scratch_bytes, s);
-    unsigned long long* d_cnt = dalloc<unsigned long long>(static_cast<int64_t>(K) + 1, scratch_bytes, s);
     long long* d_w = dalloc<long long>(static_cast<int64_t>(N) + 1, scratch_bytes, s);
     long long* d_excl = dalloc<long long>(static_cast<int64_t>(N) + 1, scratch_bytes, s);
     int* d_bad = dalloc<int>(1, scratch_bytes, s);
-    CUDA_TRY(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * (static_cast<size_t>(K) + 1), s));
     CUDA_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
     k_validate_small<<<grid_for(std::max<int64_t>(N, K), 256, sms), 256, 0, s>>>(ds->subject_offsets, N,
                                                                              ds->era_lengths, K, d_bad);
     if (nnz > 0) {
         k_interleave<<<grid_for(nnz, 256, sms), 256, 0, s>>>(d_rows, d_subj, ds->pairs, nnz);
         k_pair_meta<<<grid_for(nnz, 256, sms), 256, 0, s>>>(ds->pairs, ds->col_ptr, J, ds->subject_offsets, N, K,
-                                                           nnz, d_col, d_cnt, d_bad);
+                                                           nnz, d_col, d_bad);
     }
-    // CSR: exclusive scan of the row histogram, stable sort by row
+    // CSR: stable sort by row, row pointers from the sorted keys
     {
         size_t tmp_bytes = 0;
-        CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_cnt,
-                                               reinterpret_cast<unsigned long long*>(ds->csr_ptr), K + 1, s));
         size_t sort_bytes = 0;
         int end_bit = 1;
         while ((1ll << end_bit) < static_cast<long long>(K)) ++end_bit;
@@ -1972,14 +1992,13 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
         CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, scan2, d_w, d_excl, N + 1, s));
         const size_t tb = std::max(std::max(tmp_bytes, sort_bytes), scan2);
         unsigned char* tmp = dalloc<unsigned char>(static_cast<int64_t>(std::max<size_t>(tb, 16)), scratch_bytes, s);
-        CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, d_cnt,
-                                               reinterpret_cast<unsigned long long*>(ds->csr_ptr), K + 1, s));
         if (nnz > 0) {
             // keys: rows (consumed); d_subj is free after interleave and
             // receives the sorted keys
             CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, d_rows, d_subj, d_col, ds->csr_col, nnz, 0,
                                                      end_bit, s));
         }
+        k_csr_ptr<<<grid_for(nnz + 1, 256, sms), 256, 0, s>>>(d_subj, nnz, K, ds->csr_ptr);
         // nnz-balanced CTA subject ranges
         k_subject_weight<<<grid_for(N, 256, sms), 256, 0, s>>>(ds->subject_offsets, ds->csr_ptr, N, d_w);
         CUDA_TRY(cudaMemsetAsync(d_w + N, 0, sizeof(long long), s));
@@ -1998,7 +2017,7 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
         } else {
             k_ydotx<<<J, 256, 0, s>>>(ds->pairs, ds->col_ptr, ds->event_counts, ds->y_dot_x, J);
         }
-        count_launches(5 + (nnz > 0 ? 2 : 0) + (y_dot_x_global ? 0 : 1));
+        count_launches(6 + (nnz > 0 ? 2 : 0) + (y_dot_x_global ? 0 : 1));
         dfree(tmp, s);
     }
     int bad = 0;
@@ -2006,7 +2025,6 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
     dfree(d_rows, s);
     dfree(d_subj, s);
     dfree(d_col, s);
-    dfree(d_cnt, s);
     dfree(d_w, s);
     dfree(d_excl, s);
     dfree(d_bad, s);
