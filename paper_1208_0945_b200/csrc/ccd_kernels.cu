@@ -27,6 +27,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <exception>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -1960,7 +1961,7 @@ void alloc_dataset(bsccs_dataset* ds) {
 // build_dataset invariants (dataset.hpp:135-175), builds the interleaved
 // pairs, the row-major copy, the CTA ranges and the per-column splits.
 void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const int64_t* y_dot_x_global,
-                    const int64_t* col_nnz_global) {
+                    const int64_t* col_nnz_global, cudaEvent_t era_ready) {
     const int C = ds->ctas;
     const int32_t N = ds->N, K = ds->K, J = ds->J;
     const int64_t nnz = ds->nnz;
@@ -1972,8 +1973,6 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
     long long* d_excl = dalloc<long long>(static_cast<int64_t>(N) + 1, scratch_bytes, s);
     int* d_bad = dalloc<int>(1, scratch_bytes, s);
     CUDA_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
-    k_validate_small<<<grid_for(std::max<int64_t>(N, K), 256, sms), 256, 0, s>>>(ds->subject_offsets, N,
-                                                                             ds->era_lengths, K, d_bad);
     if (nnz > 0) {
         k_interleave<<<grid_for(nnz, 256, sms), 256, 0, s>>>(d_rows, d_subj, ds->pairs, nnz);
         k_pair_meta<<<grid_for(nnz, 256, sms), 256, 0, s>>>(ds->pairs, ds->col_ptr, J, ds->subject_offsets, N, K,
@@ -1999,6 +1998,11 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
                                                      end_bit, s));
         }
         k_csr_ptr<<<grid_for(nnz + 1, 256, sms), 256, 0, s>>>(d_subj, nnz, K, ds->csr_ptr);
+        // the era arrays may still be arriving on a side stream: the pair-side
+        // build above overlapped their upload
+        if (era_ready) CUDA_TRY(cudaStreamWaitEvent(s, era_ready, 0));
+        k_validate_small<<<grid_for(std::max<int64_t>(N, K), 256, sms), 256, 0, s>>>(ds->subject_offsets, N,
+                                                                                 ds->era_lengths, K, d_bad);
         // nnz-balanced CTA subject ranges
         k_subject_weight<<<grid_for(N, 256, sms), 256, 0, s>>>(ds->subject_offsets, ds->csr_ptr, N, d_w);
         CUDA_TRY(cudaMemsetAsync(d_w + N, 0, sizeof(long long), s));
@@ -2100,25 +2104,45 @@ bsccs_dataset* dataset_create(int32_t N, int32_t K, int32_t J, int64_t nnz, cons
 
     DeviceGuard g(device);
     bsccs_dataset* ds = dataset_new(N, K, J, nnz, device, ctas_override);
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t ev_alloc = nullptr, ev_era = nullptr;
+    std::exception_ptr failure;
     try {
         cudaStream_t s = ds->stream;
         h2d(ds->col_ptr, col_ptr, sizeof(int64_t) * (J + 1), s, device);
         h2d(ds->subject_offsets, subject_offsets, sizeof(int32_t) * (N + 1), s, device);
         h2d(ds->events_per_subject, events_per_subject, sizeof(int32_t) * N, s, device);
-        h2d(ds->era_lengths, era_lengths, sizeof(int32_t) * K, s, device);
-        h2d(ds->event_counts, event_counts, sizeof(int32_t) * K, s, device);
         int64_t scratch_bytes = 0;
         int32_t* d_rows = dalloc<int32_t>(nnz, scratch_bytes, s);
         int32_t* d_subj = dalloc<int32_t>(nnz, scratch_bytes, s);
+        // the pair arrays first: the build starts on them while the era
+        // arrays upload on a side stream (copy and compute overlap)
         if (nnz > 0) {
             h2d(d_rows, rows, sizeof(int32_t) * nnz, s, device);
             h2d(d_subj, subjects, sizeof(int32_t) * nnz, s, device);
         }
+        CUDA_TRY(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&ev_alloc, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&ev_era, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventRecord(ev_alloc, s)); // the era arrays were allocated on s
+        CUDA_TRY(cudaStreamWaitEvent(s2, ev_alloc, 0));
+        h2d(ds->era_lengths, era_lengths, sizeof(int32_t) * K, s2, device);
+        h2d(ds->event_counts, event_counts, sizeof(int32_t) * K, s2, device);
+        CUDA_TRY(cudaEventRecord(ev_era, s2));
         ds->col_ptr_h.assign(col_ptr, col_ptr + J + 1);
-        finish_dataset(ds, d_rows, d_subj, y_dot_x_global, col_nnz_global);
+        finish_dataset(ds, d_rows, d_subj, y_dot_x_global, col_nnz_global, ev_era);
     } catch (...) {
+        failure = std::current_exception();
+    }
+    if (s2) {
+        cudaStreamSynchronize(s2);
+        cudaStreamDestroy(s2);
+    }
+    if (ev_alloc) cudaEventDestroy(ev_alloc);
+    if (ev_era) cudaEventDestroy(ev_era);
+    if (failure) {
         dataset_destroy(ds);
-        throw;
+        std::rethrow_exception(failure);
     }
     return ds;
 }

@@ -158,7 +158,7 @@ void dataset_destroy(bsccs_dataset* ds);
 // building blocks of dataset_create, shared with the device-side subset
 bsccs_dataset* dataset_new(int32_t N, int32_t K, int32_t J, int64_t nnz, int device, int ctas_override);
 void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const int64_t* y_dot_x_global,
-                    const int64_t* col_nnz_global);
+                    const int64_t* col_nnz_global, cudaEvent_t era_ready = nullptr);
 // subset_dataset (dataset.hpp:157-217) built on the device (subset.cu)
 bsccs_dataset* dataset_subset(const bsccs_dataset* parent, const int32_t* subject_indices, int64_t n,
                               int ctas_override);

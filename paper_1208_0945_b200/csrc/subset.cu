@@ -218,7 +218,7 @@ bsccs_dataset* dataset_subset(const bsccs_dataset* parent, const int32_t* subjec
         CUDA_TRY(cudaStreamSynchronize(s));
         free_tmp();
         CUDA_TRY(cudaStreamSynchronize(ps));
-        finish_dataset(ds, d_rows, d_subj, nullptr, nullptr);
+        finish_dataset(ds, d_rows, d_subj, nullptr, nullptr, nullptr);
         ds->drug_ids = parent->drug_ids; // labels carried over unchanged (dataset.hpp:160-162)
     } catch (...) {
         if (ds) dataset_destroy(ds);
@@ -271,7 +271,7 @@ bsccs_dataset* dataset_from_row_pairs(int32_t N, int32_t K, int32_t J, int64_t n
             dfree(vals[b], s);
         }
         CUDA_TRY(cudaStreamSynchronize(s));
-        finish_dataset(ds, d_rows, d_subj, nullptr, nullptr);
+        finish_dataset(ds, d_rows, d_subj, nullptr, nullptr, nullptr);
     } catch (...) {
         dataset_destroy(ds);
         throw;
