@@ -243,3 +243,36 @@ def test_speculative_sweep_without_subject_tile():
         assert res.cycles_run == exp["cycles_run"]
         assert np.all(np.abs(res.beta_map - exp["beta"]) <= np.maximum(1e-8 * np.abs(exp["beta"]), 1e-11))
         assert rel_gap(res.log_posterior, exp["log_posterior"]) < 1e-10
+
+
+@pytest.mark.parametrize("corrupt,message", [
+    ("row_out_of_range", "invalid pair"),
+    ("foreign_subject", "invalid pair"),
+    ("rows_not_ascending", "invalid pair"),
+    ("era_length_zero", "era length must be positive"),
+    ("subject_without_eras", "every subject needs at least one era"),
+])
+def test_device_build_validation(corrupt, message):
+    """build_dataset's invariants (dataset.hpp:135-175) checked by the device
+    build (k_validate_small, k_pair_meta) on a dataset large enough for many
+    build blocks, each corruption planted mid-array."""
+    from paper_1208_0945_b200 import datagen
+    ds = datagen.fast_sccs(20_000, 30, 3.0)
+    a = [x.copy() for x in ds.arrays()]
+    off, eps, lens, cnts, cptr, rows, subs, ydx = a
+    p = int(cptr[17]) + 5  # inside column 17
+    if corrupt == "row_out_of_range":
+        rows[p] = lens.size
+    elif corrupt == "foreign_subject":
+        subs[p] = (subs[p] + 7) % (off.size - 1)
+    elif corrupt == "rows_not_ascending":
+        rows[p], rows[p + 1] = rows[p + 1], rows[p]
+        subs[p], subs[p + 1] = subs[p + 1], subs[p]
+    elif corrupt == "era_length_zero":
+        lens[lens.size // 2] = 0
+    elif corrupt == "subject_without_eras":
+        i = (off.size - 1) // 2
+        off[i + 1] = off[i]
+    bad = B.Dataset(off, eps, lens, cnts, cptr, rows, subs, ydx)
+    with pytest.raises(B.InputError, match=message):
+        B.DeviceDataset(bad, 0)
