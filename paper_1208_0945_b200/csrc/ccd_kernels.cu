@@ -5,18 +5,24 @@
 //                    runs one full cycle (run_cycle, solver.hpp:101-166) or a
 //                    single tier-1 op.  Per coordinate: fused grad/hess over
 //                    the CTA's subject-aligned slice of the column
-//                    (engine.hpp:97-132), a 32-byte all-gather of the
-//                    per-CTA partials through self-validating slots, the
-//                    penalized step evaluated redundantly by every CTA
+//                    (engine.hpp:97-132), an exact order-independent
+//                    all-reduce of the per-CTA partials (fixed-point limbs
+//                    added with red.add into self-validating words, §4.2),
+//                    the penalized step evaluated redundantly by every CTA
 //                    (prior.hpp:72-122), and the sparse update of the
-//                    slice's runs (engine.hpp:205-231) -- no atomics, no
-//                    grid barrier, one exchange per coordinate.
+//                    slice's runs (engine.hpp:205-231) -- no grid barrier,
+//                    one exchange per coordinate.  The next coordinate's
+//                    records are gathered speculatively while the partials
+//                    travel and repaired from the update's record.  Four
+//                    instantiations: subject tile in shared memory or not,
+//                    streamed path for large slices compiled in or not.
 //   k_dense_xb       dense_recompute xbeta / l*exp rebuild (engine.hpp:68-90,
 //                    170-183) from the row-major copy, reference add order
 //   k_dense_den      per-subject ascending sum of l*exp (engine.hpp:81-89)
 //   k_ll_partial/    log_likelihood (engine.hpp:404-425), fixed-order
 //   k_ll_final       two-level reduction
-//   dataset build    interleave, row histogram, stable radix sort (CUB) to
+//   k_ccd_dense      the reference's dense update route (UpdatePath::dense)
+//   dataset build    interleave + validation, stable radix sort (CUB) to
 //                    build the CSR, nnz-balanced CTA subject ranges, split.
 #include <cub/cub.cuh>
 
