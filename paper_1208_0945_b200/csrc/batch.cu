@@ -61,7 +61,10 @@ struct BCfg {
     static constexpr int kQStep = kBT / RB;              // pairs per block-wide pass
     // staged l*exp per slot + two pair buffers
     static constexpr int kCapP = (kBSmemBudget - 4096) / (RB * 8 + 16) / kQStep * kQStep;
-    static constexpr int kU = 8; // slots per thread whose gathers are in flight together
+#ifndef BSCCS_BSLOTS
+#define BSCCS_BSLOTS 8
+#endif
+    static constexpr int kU = BSCCS_BSLOTS; // slots per thread whose gathers are in flight together
 };
 
 struct BatchArgs {
@@ -270,7 +273,10 @@ __device__ __forceinline__ void upd_tail_head(const BatchArgs& A, int64_t p0, in
     A.den[static_cast<size_t>(pr.y) * (2 * RB) + fit] = den;
 }
 
-template <int RB>
+// kChunk: the chunked path for slices beyond the register slots is compiled
+// in; the host launches the instantiation without it when every slice fits
+// (its register pressure slows the common single-chunk path).
+template <int RB, bool kChunk>
 __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchArgs A) {
     using Cf = BCfg<RB>;
     constexpr int U = Cf::kU;
@@ -333,7 +339,7 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
         // registers) keep each slot's gathered values in registers from the
         // gradient pass through the update: one gather round trip per
         // coordinate.  Larger slices take the chunked path with reloads.
-        const bool fast = np <= U * QS;
+        const bool fast = !kChunk || np <= U * QS;
         double xbv[U], dn[U];
         int len[U], mm[U], fl[U]; // mm: m * n_i of the slot's subject; fl: bit0 valid, bit1 head, bit2 single run
         double gs = 0.0, hs = 0.0;
@@ -391,7 +397,7 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
                     }
                 }
             }
-        } else if (flive) {
+        } else if (kChunk && flive) {
             for (int base = qfirst; base < lim; base += U * QS) {
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
@@ -449,7 +455,7 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
                 gs = __dadd_rn(gs, nw);
                 hs = __dadd_rn(hs, __dmul_rn(nw, __dsub_rn(1.0, w)));
             }
-        } else if (flive) {
+        } else if (kChunk && flive) {
             for (int q = qfirst; q < lim; q += QS) {
                 const int s = P[q].y;
                 if (q > 0 && P[q - 1].y == s) continue;
@@ -612,7 +618,7 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
                 if (fl[u] & 4) A.den[static_cast<size_t>(pr.y) * (2 * RB) + fit] = __dadd_rn(dn[u], diff);
                 else sm.le[q * RB + fit] = diff; // this slot's l*exp is no longer needed
             }
-        } else if (flive && d != 0.0) {
+        } else if (kChunk && flive && d != 0.0) {
             for (int base = qfirst; base < lim; base += U * QS) {
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
@@ -663,7 +669,7 @@ __global__ void __launch_bounds__(kBT, 1) k_bccd(const __grid_constant__ BatchAr
                 for (int q2 = q; q2 < np && P[q2].y == s; ++q2) den = __dadd_rn(den, sm.le[q2 * RB + fit]);
                 A.den[static_cast<size_t>(s) * (2 * RB) + fit] = den;
             }
-        } else if (flive && d != 0.0) {
+        } else if (kChunk && flive && d != 0.0) {
             for (int q = qfirst; q < lim; q += QS) {
                 const int s = P[q].y;
                 if (q > 0 && P[q - 1].y == s) continue;
@@ -1042,10 +1048,14 @@ Batch* batch_create(const bsccs_dataset* ds, int RB) {
         CUDA_TRY(cudaEventCreate(&b->ev0));
         CUDA_TRY(cudaEventCreate(&b->ev1));
         if (RB == 8) {
-            CUDA_TRY(cudaFuncSetAttribute(k_bccd<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            CUDA_TRY(cudaFuncSetAttribute(k_bccd<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(smem_bytes<8>())));
+            CUDA_TRY(cudaFuncSetAttribute(k_bccd<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(smem_bytes<8>())));
         } else {
-            CUDA_TRY(cudaFuncSetAttribute(k_bccd<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            CUDA_TRY(cudaFuncSetAttribute(k_bccd<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(smem_bytes<16>())));
+            CUDA_TRY(cudaFuncSetAttribute(k_bccd<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(smem_bytes<16>())));
         }
         CUDA_TRY(cudaStreamSynchronize(s));
@@ -1125,8 +1135,10 @@ void launch_ll(Batch* b, const int32_t* w, unsigned mask) {
 template <int RB>
 void launch_cycle(Batch* b, BatchArgs& a) {
     void* params[] = {&a};
-    CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_bccd<RB>), dim3(b->ds->ctas), dim3(kBT), params,
-                                         smem_bytes<RB>(), b->stream));
+    // the single-chunk instantiation when every slice fits the register slots
+    const bool chunk = b->ds->max_slice > BCfg<RB>::kU * BCfg<RB>::kQStep;
+    void* fn = chunk ? reinterpret_cast<void*>(k_bccd<RB, true>) : reinterpret_cast<void*>(k_bccd<RB, false>);
+    CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(b->ds->ctas), dim3(kBT), params, smem_bytes<RB>(), b->stream));
     count_launches(1);
 }
 
