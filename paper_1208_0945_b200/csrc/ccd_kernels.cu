@@ -1028,7 +1028,8 @@ void ensure_kernel_attrs(int device) {
     if (device < 32 && (done.load() & (1u << device))) return;
     for (void* fn : {reinterpret_cast<void*>(t3::k_ccd<false, false>), reinterpret_cast<void*>(t3::k_ccd<false, true>),
                      reinterpret_cast<void*>(t3::k_ccd<true, false>), reinterpret_cast<void*>(t3::k_ccd<true, true>),
-                     reinterpret_cast<void*>(t1::k_ccd<false, false>), reinterpret_cast<void*>(t1::k_ccd<true, false>)})
+                     reinterpret_cast<void*>(t1::k_ccd<false, false>), reinterpret_cast<void*>(t1::k_ccd<true, false>),
+                     reinterpret_cast<void*>(t1::k_ccd<false, true>), reinterpret_cast<void*>(t1::k_ccd<true, true>)})
         CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSweepSmem));
     if (device < 32) done.fetch_or(1u << device);
 }
@@ -1506,12 +1507,8 @@ int subject_tile_cap(const ExchangePlan& plan, bool streamed, size_t tile_offset
 // slices are small: measured -3% fit time at ~200 pairs per CTA per
 // coordinate (config 2), +4% at ~740 (config 3), where the extra line
 // fetches compete with the gathers.  BSCCS_PREFETCH=0/1 forces it.
-int prefetch_enabled(const ExchangePlan& plan) {
-    static const int forced = [] {
-        const char* e = std::getenv("BSCCS_PREFETCH");
-        return e ? (e[0] == '0' ? 0 : 1) : -1;
-    }();
-    if (forced >= 0) return forced;
+// mean pairs per CTA per (non-empty) coordinate
+double mean_slice(const ExchangePlan& plan) {
     int64_t nnz = 0, ctas = 0;
     for (auto* st : plan.shards) {
         nnz += st->ds->nnz;
@@ -1520,9 +1517,18 @@ int prefetch_enabled(const ExchangePlan& plan) {
     const bsccs_dataset* ds = plan.shards[0]->ds;
     int64_t cols = 0;
     for (uint8_t nz : ds->col_nonempty_h) cols += nz ? 1 : 0;
-    if (cols == 0 || ctas == 0) return 0;
-    const double per_cta = static_cast<double>(nnz) / static_cast<double>(cols) / static_cast<double>(ctas);
-    return per_cta <= 384.0 ? 1 : 0;
+    if (cols == 0 || ctas == 0) return 0.0;
+    return static_cast<double>(nnz) / static_cast<double>(cols) / static_cast<double>(ctas);
+}
+
+int prefetch_enabled(const ExchangePlan& plan) {
+    static const int forced = [] {
+        const char* e = std::getenv("BSCCS_PREFETCH");
+        return e ? (e[0] == '0' ? 0 : 1) : -1;
+    }();
+    if (forced >= 0) return forced;
+    const double per_cta = mean_slice(plan);
+    return per_cta > 0.0 && per_cta <= 384.0 ? 1 : 0;
 }
 
 void launch_ccd(const ExchangePlan& plan, SweepArgs& a) {
@@ -1534,15 +1540,20 @@ void launch_ccd(const ExchangePlan& plan, SweepArgs& a) {
     // (up to kStreamMax pairs; the tile is dropped if that leaves too little)
     // one register tile when every slice fits it (1 tile = 352 pairs per
     // CTA and coordinate; config 2's slices are ~200): fewer registers and
-    // less shared memory, measured 10% faster than 3 tiles at config 2
+    // less shared memory, measured 10% faster than 3 tiles at config 2.
+    // Also when the typical slice is well inside it and only some columns
+    // exceed it (skewed prevalence): those stream, the rest run lighter --
+    // Zipf 1M 54.7 -> 47.5 ms; config 3 (mean ~740) stays on 3 tiles.
     static const int tiles_forced = [] {
         const char* e = std::getenv("BSCCS_TILES"); // experiment hook: 1 or 3
         return e ? std::atoi(e) : 0;
     }();
     bool one_tile = a.mode == kModeSweep && tiles_forced != 3;
     for (auto* st : plan.shards) one_tile = one_tile && st->ds->max_slice <= t1::kCap;
+    if (a.mode == kModeSweep && tiles_forced != 3 && mean_slice(plan) <= 0.75 * t1::kCap) one_tile = true;
+    if (a.mode == kModeSweep && tiles_forced == 1) one_tile = true;
     bool streamed = a.mode != kModeSweep;
-    for (auto* st : plan.shards) streamed = streamed || st->ds->max_slice > t3::kCap;
+    for (auto* st : plan.shards) streamed = streamed || st->ds->max_slice > (one_tile ? t1::kCap : t3::kCap);
     const size_t smem_size = one_tile ? sizeof(t1::Smem) : sizeof(t3::Smem);
     const size_t tile_off = one_tile ? t1::kSmemSubjOffset : t3::kSmemSubjOffset;
     a.ss_cap = a.mode == kModeSweep ? subject_tile_cap(plan, streamed, tile_off) : 0;
@@ -1583,7 +1594,9 @@ void launch_ccd(const ExchangePlan& plan, SweepArgs& a) {
     }
     void* params[] = {&a};
     void* fn;
-    if (one_tile)
+    if (one_tile && streamed)
+        fn = a.ss_cap > 0 ? reinterpret_cast<void*>(t1::k_ccd<true, true>) : reinterpret_cast<void*>(t1::k_ccd<false, true>);
+    else if (one_tile)
         fn = a.ss_cap > 0 ? reinterpret_cast<void*>(t1::k_ccd<true, false>) : reinterpret_cast<void*>(t1::k_ccd<false, false>);
     else if (a.ss_cap > 0)
         fn = streamed ? reinterpret_cast<void*>(t3::k_ccd<true, true>) : reinterpret_cast<void*>(t3::k_ccd<true, false>);
