@@ -276,3 +276,22 @@ def test_device_build_validation(corrupt, message):
     bad = B.Dataset(off, eps, lens, cnts, cptr, rows, subs, ydx)
     with pytest.raises(B.InputError, match=message):
         B.DeviceDataset(bad, 0)
+
+
+def test_three_tile_sweep_with_subject_tile():
+    """Mean slices of ~500 pairs per CTA (beyond the one-tile kernel's 352,
+    inside the three-tile kernel's 1,056) with the subject tile: the
+    t3::k_ccd<1,0> instantiation, against the oracle."""
+    import pyoracle
+    rng = B.Rng(31)
+    ds = random_dataset(rng, 8, 4000, exposure_prob=0.3)
+    dds = B.DeviceDataset(ds, 0, 8)
+    nnz_col = np.diff(ds.col_ptr)
+    assert nnz_col.mean() / 8 > 300 and nnz_col.max() / 8 < 900
+    port = pyoracle.Port()
+    for prior in (B.laplace_prior(0.1), B.normal_prior(0.5)):
+        res = B.fit(dds, prior)
+        exp = port.fit(ds, prior, B.SolverConfig())
+        assert res.cycles_run == exp["cycles_run"]
+        assert np.all(np.abs(res.beta_map - exp["beta"]) <= np.maximum(1e-8 * np.abs(exp["beta"]), 1e-11))
+        assert rel_gap(res.log_posterior, exp["log_posterior"]) < 1e-10
