@@ -73,6 +73,16 @@ inline void check(bsccs_status st) {
     throw Error(st, msg);
 }
 
+// An input error raised on this side of the C ABI, with its own message
+// (bsccs_last_error() would still hold an earlier call's text).
+[[noreturn]] inline void input_error(const std::string& msg) {
+#if defined(BSCCS_B200_HAVE_REFERENCE)
+    raise_as<::bsccs::input_error>(msg);
+#else
+    throw Error(BSCCS_INPUT_ERROR, msg);
+#endif
+}
+
 } // namespace detail
 
 // Device-resident copy of a reference-layout Dataset (one upload).
@@ -145,7 +155,7 @@ FitResult fit(const DeviceDataset& dds, const PriorSpec& prior, const SolverConf
     const bsccs_prior p = to_c_prior(prior);
     const bsccs_solver_config c = to_c_config(cfg);
     if (!init_beta.empty() && static_cast<int32_t>(init_beta.size()) != dds.num_drugs())
-        detail::check((bsccs_status)BSCCS_INPUT_ERROR);
+        detail::input_error("init_state: coefficient count does not match drug count"); // engine.hpp:142-144
     FitResult out;
     out.beta_map.assign(static_cast<std::size_t>(dds.num_drugs()), 0.0);
     bsccs_fit_result r;

@@ -215,6 +215,15 @@ class Reference:
         txt = buf.value.decode()
         return RefDataset(self, h), (txt.split("\n") if txt else [])
 
+    def fast_sccs(self, attempts, drugs, lambda_x=3.0, zipf=False, seed=20261017, threads=None):
+        """SURVEY §8(d) fast generator on the reference's own Rng (ref_shim.cpp):
+        the same arrays as the product generator, without loading it."""
+        h = VP()
+        self._chk(self.lib.ref_fast_sccs(i64(int(attempts)), i32(int(drugs)), f64(lambda_x), i32(int(bool(zipf))),
+                                         u64(int(seed) & 0xFFFFFFFFFFFFFFFF), i32(threads or host_cores()),
+                                         C.byref(h)))
+        return RefDataset(self, h)
+
     def penalized_step(self, prior, beta_j, g, h):
         out = f64()
         p = _cprior(prior)
@@ -241,19 +250,42 @@ class RefDataset:
 
     def to_host(self):
         from paper_1208_0945_b200.bsccs import Dataset
-        sz = (i64 * 4)()
-        self.ref.lib.ref_dataset_sizes(self.h, sz)
-        N, K, J, nnz = list(sz)
-        a = [np.zeros(N + 1, np.int32), np.zeros(N, np.int32), np.zeros(K, np.int32), np.zeros(K, np.int32),
-             np.zeros(J + 1, np.int64), np.zeros(nnz, np.int32), np.zeros(nnz, np.int32), np.zeros(J, np.int64)]
-        self.ref.lib.ref_dataset_flatten(self.h, *[_p(x) for x in a])
-        return Dataset(*a)
+        return Dataset(*self.arrays())
 
     def subset(self, idx):
         sel = np.ascontiguousarray(idx, dtype=np.int32)
         h = VP()
         self.ref._chk(self.ref.lib.ref_subset(self.h, _p(sel), i64(sel.size), C.byref(h)))
         return RefDataset(self.ref, h)
+
+    def columns(self, cols):
+        """column sample: same subjects and eras, only `cols` (ref_dataset_columns)"""
+        c = np.ascontiguousarray(cols, dtype=np.int32)
+        h = VP()
+        self.ref._chk(self.ref.lib.ref_dataset_columns(self.h, _p(c), i32(c.size), C.byref(h)))
+        return RefDataset(self.ref, h)
+
+    def arrays(self):
+        """flat CSC arrays (numpy), in Dataset.arrays() order"""
+        sz = (i64 * 4)()
+        self.ref.lib.ref_dataset_sizes(self.h, sz)
+        N, K, J, nnz = list(sz)
+        a = [np.zeros(N + 1, np.int32), np.zeros(N, np.int32), np.zeros(K, np.int32), np.zeros(K, np.int32),
+             np.zeros(J + 1, np.int64), np.zeros(nnz, np.int32), np.zeros(nnz, np.int32), np.zeros(J, np.int64)]
+        self.ref.lib.ref_dataset_flatten(self.h, *[_p(x) for x in a])
+        return a
+
+    def bootstrap_replicate(self, seed, r, prior, cfg, init_beta=None):
+        """run_bootstrap's replicate r (bootstrap.hpp:103-112): beta and fit summary"""
+        J = self._J()
+        beta = np.zeros(J)
+        b = None if init_beta is None else np.ascontiguousarray(init_beta, dtype=np.float64)
+        res = _CRes()
+        p, c = _cprior(prior), _ccfg(cfg)
+        self.ref._chk(self.ref.lib.ref_bootstrap_replicate(self.h, u64(seed), i32(r), C.byref(p), C.byref(c), _p(b),
+                                                           _p(beta), C.byref(res)))
+        return dict(beta=beta, log_posterior=res.log_posterior, cycles_run=res.cycles_run,
+                    converged=bool(res.converged), final_criterion=res.final_criterion)
 
     def kfold_split(self, folds, seed):
         n = self.sizes()["N"]

@@ -8,7 +8,10 @@
 // restatement oracle/ccd_oracle.c bit for bit, (b) to generate the golden
 // fixtures in tests/golden/, and (c) as bench.py's CPU baseline
 // (cpu_baseline.kind = "reference").
+#include <algorithm>
 #include <chrono>
+#include <cmath>
+#include <thread>
 #include <cstdint>
 #include <cstring>
 #include <memory>
@@ -387,6 +390,182 @@ int ref_run_cycle(void* dsp, void* sp, const bsccs_prior* prior, const bsccs_sol
 }
 int ref_penalized_step(const bsccs_prior* prior, double beta_j, double g, double h, double* out) {
     return guard([&] { *out = bsccs::penalized_step(to_prior(prior), beta_j, g, h); });
+}
+
+// One bootstrap replicate exactly as run_bootstrap's run_replicate does it
+// (bootstrap.hpp:103-112): indices from Rng(seed, r + 1), subset_dataset,
+// fit warm from init_beta (nullable = cold).  Exposes the per-replicate
+// estimate that run_bootstrap keeps internal.
+int ref_bootstrap_replicate(void* dsp, uint64_t seed, int32_t r, const bsccs_prior* prior,
+                            const bsccs_solver_config* cfg, const double* init_beta, double* beta_out,
+                            bsccs_fit_result* res) {
+    return guard([&] {
+        auto* ds = static_cast<bsccs::Dataset*>(dsp);
+        bsccs::Rng rng(seed, static_cast<std::uint64_t>(r) + 1);
+        const bsccs::Dataset resampled = bsccs::subset_dataset(*ds, bsccs::resample(*ds, rng));
+        std::vector<double> init;
+        if (init_beta) init.assign(init_beta, init_beta + ds->num_drugs);
+        const bsccs::FitResult f = bsccs::fit(resampled, to_prior(prior), to_cfg(cfg), init);
+        std::memcpy(beta_out, f.beta_map.data(), sizeof(double) * f.beta_map.size());
+        std::memset(res, 0, sizeof *res);
+        res->log_posterior = f.log_posterior;
+        res->final_criterion = f.final_criterion;
+        res->cycles_run = f.cycles_run;
+        res->converged = f.converged ? 1 : 0;
+    });
+}
+
+// The fast SCCS generator of SURVEY §8(d), written here on the reference's
+// own Rng so the bench's reference arm can build its dataset without the
+// product library in its process.  Attempted subject s draws from
+// Rng(seed, s + 1): phi ~ N(-5, 0.5), E ~ U{10..20} eras; per era
+// L ~ U{10..60}, m = min(Poisson(lambda_x), J) distinct drugs (below(J) with
+// rejection, or the 1/(j+1) inverse CDF for the Zipf variant) sorted
+// ascending, y ~ Poisson(L exp(phi + sum beta_true)); subjects with no
+// events are dropped and the rest laid out as build_dataset does
+// (dataset.hpp:74-152).  tests/test_oracle.py checks it produces the same
+// arrays as the product generator.
+int ref_fast_sccs(int64_t attempts, int32_t drugs, double lambda_x, int32_t zipf, uint64_t seed, int32_t threads,
+                  void** out) {
+    return guard([&] {
+        if (attempts < 1 || drugs < 1 || !(lambda_x >= 0.0)) throw bsccs::input_error("fast_sccs: bad arguments");
+        std::vector<double> truth(static_cast<size_t>(drugs), 0.0);
+        const int32_t stride = drugs >= 10 ? drugs / 10 : 1;
+        for (int p = 0; p < 10; ++p) {
+            const int64_t j = static_cast<int64_t>(p) * stride;
+            if (j < drugs) truth[static_cast<size_t>(j)] = (p % 2 == 0) ? 0.7 : -0.5;
+        }
+        std::vector<double> cum;
+        if (zipf) {
+            double acc = 0.0;
+            for (int32_t j = 0; j < drugs; ++j) cum.push_back(acc += 1.0 / static_cast<double>(j + 1));
+        }
+        struct Part {
+            std::vector<int32_t> nera, nev, len, y, m, drug;
+        };
+        const int T = std::max(1, threads);
+        const int64_t P = std::min<int64_t>(attempts, 64LL * T);
+        std::vector<Part> parts(static_cast<size_t>(P));
+        auto make = [&](int64_t b) {
+            Part& pt = parts[static_cast<size_t>(b)];
+            std::vector<int32_t> picked;
+            for (int64_t s = attempts * b / P; s < attempts * (b + 1) / P; ++s) {
+                bsccs::Rng rng(seed, static_cast<std::uint64_t>(s) + 1);
+                const double phi = rng.normal(-5.0, 0.5);
+                const int eras = rng.uniform_int(10, 20);
+                const size_t e0 = pt.len.size(), d0 = pt.drug.size();
+                int32_t events = 0;
+                for (int e = 0; e < eras; ++e) {
+                    const int32_t L = rng.uniform_int(10, 60);
+                    const int32_t m = std::min<int32_t>(rng.poisson(lambda_x), drugs);
+                    picked.clear();
+                    while (static_cast<int32_t>(picked.size()) < m) {
+                        int32_t d;
+                        if (zipf) {
+                            const double u = rng.uniform() * cum.back();
+                            d = static_cast<int32_t>(std::upper_bound(cum.begin(), cum.end(), u) - cum.begin());
+                            d = std::min(d, drugs - 1);
+                        } else {
+                            d = static_cast<int32_t>(rng.below(static_cast<std::uint64_t>(drugs)));
+                        }
+                        if (std::find(picked.begin(), picked.end(), d) == picked.end()) picked.push_back(d);
+                    }
+                    std::sort(picked.begin(), picked.end());
+                    double xb = 0.0;
+                    for (int32_t d : picked) xb += truth[static_cast<size_t>(d)];
+                    const int32_t y = rng.poisson(static_cast<double>(L) * std::exp(phi + xb));
+                    events += y;
+                    pt.len.push_back(L);
+                    pt.y.push_back(y);
+                    pt.m.push_back(m);
+                    pt.drug.insert(pt.drug.end(), picked.begin(), picked.end());
+                }
+                if (events == 0) {
+                    pt.len.resize(e0);
+                    pt.y.resize(e0);
+                    pt.m.resize(e0);
+                    pt.drug.resize(d0);
+                    continue;
+                }
+                pt.nera.push_back(eras);
+                pt.nev.push_back(events);
+            }
+        };
+        {
+            std::vector<std::thread> pool;
+            for (int t = 0; t < T; ++t)
+                pool.emplace_back([&, t] {
+                    for (int64_t b = t; b < P; b += T) make(b);
+                });
+            for (auto& th : pool) th.join();
+        }
+        auto* ds = new bsccs::Dataset();
+        std::unique_ptr<bsccs::Dataset> keep(ds);
+        ds->num_drugs = drugs;
+        std::vector<int64_t> cnt(static_cast<size_t>(drugs), 0);
+        for (const Part& pt : parts)
+            for (int32_t d : pt.drug) ++cnt[static_cast<size_t>(d)];
+        ds->columns.resize(static_cast<size_t>(drugs));
+        for (int32_t j = 0; j < drugs; ++j) {
+            ds->columns[static_cast<size_t>(j)].rows.reserve(static_cast<size_t>(cnt[static_cast<size_t>(j)]));
+            ds->columns[static_cast<size_t>(j)].subjects.reserve(static_cast<size_t>(cnt[static_cast<size_t>(j)]));
+        }
+        ds->y_dot_x.assign(static_cast<size_t>(drugs), 0);
+        ds->subject_offsets.push_back(0);
+        bsccs::index_t row = 0, subj = 0;
+        for (const Part& pt : parts) {
+            size_t e = 0, d = 0;
+            for (size_t s = 0; s < pt.nera.size(); ++s, ++subj) {
+                for (int32_t q = 0; q < pt.nera[s]; ++q, ++e, ++row) {
+                    ds->era_lengths.push_back(pt.len[e]);
+                    ds->event_counts.push_back(pt.y[e]);
+                    for (int32_t k = 0; k < pt.m[e]; ++k, ++d) {
+                        auto& col = ds->columns[static_cast<size_t>(pt.drug[d])];
+                        col.rows.push_back(row);
+                        col.subjects.push_back(subj);
+                        ds->y_dot_x[static_cast<size_t>(pt.drug[d])] += pt.y[e];
+                    }
+                }
+                ds->subject_offsets.push_back(row);
+                ds->events_per_subject.push_back(pt.nev[s]);
+            }
+        }
+        if (subj == 0) throw bsccs::input_error("fast_sccs: no subject drew an event");
+        ds->num_subjects = subj;
+        ds->num_eras = row;
+        for (const auto& c : ds->columns)
+            ds->max_column_nnz = std::max<bsccs::index_t>(ds->max_column_nnz, static_cast<bsccs::index_t>(c.rows.size()));
+        *out = keep.release();
+    });
+}
+
+// A column sample of a dataset: the same subjects and eras, only the listed
+// columns (in the listed order).  The reference's own run_cycle on it does
+// exactly the per-coordinate work of those columns against the full-size
+// state -- the bounded CPU sample the bench times.
+int ref_dataset_columns(void* dsp, const int32_t* cols, int32_t n, void** out) {
+    return guard([&] {
+        const auto* src = static_cast<bsccs::Dataset*>(dsp);
+        auto* ds = new bsccs::Dataset();
+        ds->num_drugs = n;
+        ds->num_subjects = src->num_subjects;
+        ds->num_eras = src->num_eras;
+        ds->event_counts = src->event_counts;
+        ds->era_lengths = src->era_lengths;
+        ds->subject_offsets = src->subject_offsets;
+        ds->events_per_subject = src->events_per_subject;
+        for (int32_t i = 0; i < n; ++i) {
+            if (cols[i] < 0 || cols[i] >= src->num_drugs) {
+                delete ds;
+                throw bsccs::input_error("dataset_columns: column out of range");
+            }
+            ds->columns.push_back(src->columns[static_cast<size_t>(cols[i])]);
+            ds->y_dot_x.push_back(src->y_dot_x[static_cast<size_t>(cols[i])]);
+            ds->max_column_nnz =
+                std::max<bsccs::index_t>(ds->max_column_nnz, static_cast<bsccs::index_t>(ds->columns.back().rows.size()));
+        }
+        *out = ds;
+    });
 }
 int ref_log_density(const bsccs_prior* prior, const double* beta, int32_t n, double* out) {
     return guard([&] { *out = bsccs::log_density(to_prior(prior), std::vector<double>(beta, beta + n)); });

@@ -10,6 +10,7 @@
 // stream (SolverState::order_rng, solver.hpp:81,109-114).
 #include <cmath>
 #include <cstring>
+#include <exception>
 #include <functional>
 #include <memory>
 #include <mutex>
@@ -89,9 +90,33 @@ void set_order(FitContext& fc, const std::vector<int32_t>& order) {
     for (auto* st : fc.states) st->order_h = order;
 }
 
+// Error agreement.  In a multi-rank group every host step that can fail on
+// one rank only (a dense rebuild that overflows, a nonpositive denominator in
+// the log-likelihood) runs through agreed(): each rank then learns, by an
+// exact all-reduce of the status, whether any rank failed, and all of them
+// throw -- a rank that threw alone would stop launching and leave its peers
+// polling in the next exchange.  Errors inside a sweep already travel in the
+// exchange's error word.  One process: the error is rethrown as is.
+using Agree = std::function<void(std::exception_ptr)>;
+
+void rethrow_local(std::exception_ptr e) {
+    if (e) std::rethrow_exception(e);
+}
+
+void agreed(const Agree& agree, const std::function<void()>& body) {
+    std::exception_ptr e;
+    try {
+        body();
+    } catch (...) {
+        e = std::current_exception();
+    }
+    agree(e);
+}
+
 // fit_impl (solver.hpp:170-199) over bound shards.
 void fit_loop(FitContext& fc, const PriorParams& prior, const bsccs_solver_config* cfg, double* beta_out,
-              bsccs_fit_result* res, const std::function<double(double)>& allreduce_sum) {
+              bsccs_fit_result* res, const std::function<double(double)>& allreduce_sum,
+              const Agree& agree = rethrow_local) {
     bsccs_state* s0 = fc.states[0];
     const int32_t J = s0->ds->J;
     const long long launches0 = launch_count();
@@ -128,15 +153,21 @@ void fit_loop(FitContext& fc, const PriorParams& prior, const bsccs_solver_confi
             break;
         }
         if (res->cycles_run % cfg->dense_refresh_interval == 0) {
-            for (auto* st : fc.states) dense_recompute(st, nullptr);
+            agreed(agree, [&] {
+                for (auto* st : fc.states) dense_recompute(st, nullptr);
+            });
             ++res->dense_refreshes;
         }
     }
-    for (auto* st : fc.states) dense_recompute(st, nullptr); // report from a clean rebuild
+    agreed(agree, [&] {
+        for (auto* st : fc.states) dense_recompute(st, nullptr); // report from a clean rebuild
+    });
     ++res->dense_refreshes;
     CUDA_TRY(cudaMemcpy(beta_out, s0->beta, sizeof(double) * J, cudaMemcpyDeviceToHost));
     double ll = 0.0;
-    for (auto* st : fc.states) ll += log_likelihood(st);
+    agreed(agree, [&] {
+        for (auto* st : fc.states) ll += log_likelihood(st);
+    });
     ll = allreduce_sum(ll);
     res->log_posterior = ll + log_density(prior, beta_out, J);
     res->sweep_seconds = s0->sweep_ms * 1e-3;
@@ -695,7 +726,12 @@ bsccs_status bsccs_group_fit(bsccs_group* g, const bsccs_prior* prior, const bsc
         CUDA_TRY(cudaEventRecord(e0, nullptr));
         FitContext fc;
         try {
-            for (auto* ds : g->shards) fc.states.push_back(acquire_state(ds, init_beta));
+            if (init_beta)
+                for (int32_t j = 0; j < g->shards[0]->J; ++j)
+                    if (!std::isfinite(init_beta[j])) input_error("init_state: non-finite coefficient");
+            // states start from beta = 0 (cannot fail on one rank alone); the
+            // caller's start is applied under agreement below
+            for (auto* ds : g->shards) fc.states.push_back(acquire_state(ds, g->world > 1 ? nullptr : init_beta));
             fc.plan.shards = fc.states;
             fc.plan.dst = g->peer;
             fc.plan.local_slots = g->slots;
@@ -712,7 +748,35 @@ bsccs_status bsccs_group_fit(bsccs_group* g, const bsccs_prior* prior, const bsc
                 plan_allreduce(fc.plan, x > 0.0 ? x : 0.0, x < 0.0 ? -x : 0.0, &pos, &neg);
                 return pos - neg;
             };
-            fit_loop(fc, p, cfg, beta_out, result, allreduce);
+            // every rank's status, one base-16 digit per status code (at
+            // most 8 ranks per digit, so digits never carry)
+            Agree agree = rethrow_local;
+            if (g->world > 1)
+                agree = [&](std::exception_ptr e) {
+                    int code = 0;
+                    if (e) {
+                        try {
+                            std::rethrow_exception(e);
+                        } catch (const Error& x) {
+                            code = static_cast<int>(x.code);
+                        } catch (...) {
+                            code = BSCCS_INTERNAL_ERROR;
+                        }
+                    }
+                    double tot = 0.0, unused = 0.0;
+                    plan_allreduce(fc.plan, code > 0 && code < 8 ? std::ldexp(1.0, 4 * code) : 0.0, 0.0, &tot,
+                                   &unused);
+                    if (e) std::rethrow_exception(e);
+                    for (int c = 1; c < 8; ++c)
+                        if (std::fmod(std::floor(std::ldexp(tot, -4 * c)), 16.0) != 0.0)
+                            fail(static_cast<bsccs_status>(c), "group fit: another rank of the group failed (status " +
+                                                                   std::to_string(c) + "); see that rank's error");
+                };
+            if (g->world > 1 && init_beta)
+                agreed(agree, [&] {
+                    for (auto* st : fc.states) dense_recompute(st, init_beta);
+                });
+            fit_loop(fc, p, cfg, beta_out, result, allreduce, agree);
         } catch (...) {
             for (auto* st : fc.states) release_state(st);
             cudaEventDestroy(e0);

@@ -128,6 +128,7 @@ struct SweepArgs {
     int dbg; // profiling only: bit0 skip grad/hess, bit1 skip update, bit2 skip exchange, bit4 no speculation
     unsigned long long* trace; // profiling only: [ntrace][gridDim][kTr] globaltimer stamps
     int ntrace;
+    unsigned long long poll_timeout_ns; // bounded exchange spin (DERR_XCHG_TIMEOUT)
 };
 
 constexpr int kTr = 8; // stamps: top, pre-publish, gather done, update done, post-issue, poll done,
@@ -182,24 +183,29 @@ __device__ __forceinline__ int lane_id() { return static_cast<int>(threadIdx.x) 
 // also gains 2^52 per arrival.  A poller knows a word is complete when its
 // growth since the previous use of that buffer carries P arrivals in the
 // bits above 2^52 -- every word validates itself, no fences or flags.  The
-// integer sum is associative, so every CTA reconstructs the bit-identical,
-// correctly rounded exact sum of the partials whatever the arrival order.
+// integer sum is associative, so every CTA reconstructs bit-identical totals
+// whatever the arrival order: the exact sum of the partials truncated to
+// 2^-80, converted within one ulp (xchg.cuh from_limbs).
 // Words sit 256 B apart so the adds land on distinct L2 slices; two buffers
 // alternate by sequence parity.
 constexpr int kXStride = 32; // u64 words between exchange words (256 B)
 constexpr int kXWords = 7;
 constexpr int kXBase = 2 * kXWords * kXStride; // running totals at launch end
-// lanes 0..6 of warp 0 (all holding the same (a, b, e)) each add one word
+// lanes 0..6 of warp 0 (all holding the same (a, b, e)) each add one word;
+// the error word also counts the partials that lost bits below 2^-80
 __device__ __forceinline__ void publish(const SweepArgs& A, unsigned long long seq, double a, double b, int e) {
     const int l = lane_id();
     if (threadIdx.x >= 32 || l >= kXWords) return;
     unsigned long long w;
-    bool ok = true;
-    if (l < 3) ok = limb_of(a, l, w);
-    else if (l < 6) ok = limb_of(b, l - 3, w);
+    bool ok = true, inex = false;
+    if (l < 3) ok = limb_of(a, l, w, &inex);
+    else if (l < 6) ok = limb_of(b, l - 3, w, &inex);
     else w = 0;
+    const unsigned lost = __ballot_sync(0x7fu, inex);
     const bool okab = __all_sync(0x7fu, ok) && (0.0 <= a && a < kXMaxValue && 0.0 <= b && b < kXMaxValue);
-    if (l == 6) w = (e || !okab) ? 1ull : 0ull;
+    if (l == 6)
+        w = ((e || !okab) ? 1ull : 0ull) | ((lost & 1u) ? 1ull << kXInexA : 0ull) |
+            ((lost & 8u) ? 1ull << kXInexB : 0ull);
     w += kXCnt;
     const size_t off = static_cast<size_t>(seq & 1ull) * kXWords * kXStride + static_cast<size_t>(l) * kXStride;
     if (A.ndst == 1) {
@@ -230,10 +236,14 @@ __device__ __forceinline__ void xprev_store(const unsigned long long* slots, con
     }
 }
 
-// warp 0 only: wait for the exchange `seq`, return the totals in every lane
+// warp 0 only: wait for the exchange `seq`, return the totals in every lane.
+// The spin is bounded (A.poll_timeout_ns of globaltimer): a participant that
+// never publishes -- a peer rank that failed on the host or died -- turns
+// into DERR_XCHG_TIMEOUT instead of a hang.
 struct PollOut {
     double ta, tb;
     int te;
+    unsigned ia, ib; // participants whose partial a / b lost bits below 2^-80
     XPrev pv;
 };
 __device__ __forceinline__ PollOut poll_body(const SweepArgs& A, const unsigned long long* slots, unsigned long long seq, XPrev pv,
@@ -243,14 +253,24 @@ __device__ __forceinline__ PollOut poll_body(const SweepArgs& A, const unsigned 
     const int l = lane_id();
     const unsigned buf = static_cast<unsigned>(seq & 1ull);
     unsigned long long diff = 0;
+    bool timed_out = false;
     if (l < kXWords) {
         const unsigned long long* p =
             slots + static_cast<size_t>(buf) * kXWords * kXStride + static_cast<size_t>(l) * kXStride;
         const unsigned long long prev = buf ? pv.b1 : pv.b0;
-        unsigned long long v;
+        unsigned long long v, t_first = 0;
+        unsigned spins = 0;
         do {
             v = ld_poll(p);
             diff = v - prev;
+            if ((++spins & 4095u) == 0u) {
+                const unsigned long long now = gtimer();
+                if (t_first == 0) t_first = now;
+                else if (now - t_first > A.poll_timeout_ns) {
+                    timed_out = true;
+                    break;
+                }
+            }
         } while ((diff >> kXCntShift) < static_cast<unsigned long long>(A.P));
         if (buf) pv.b1 = v;
         else pv.b0 = v;
@@ -266,9 +286,15 @@ __device__ __forceinline__ PollOut poll_body(const SweepArgs& A, const unsigned 
     ta = __shfl_sync(0xffffffffu, v, 0);
     tb = __shfl_sync(0xffffffffu, v, 3);
     const unsigned bad = __ballot_sync(0xffffffffu, ovf) & 0x9u; // lanes 0 (a) and 3 (b)
-    te = (__shfl_sync(0xffffffffu, d, 6) != 0 || bad) ? 1 : 0;
-    if (bad && l == 0) record_error(A.sh[0].err, DERR_SUM_RANGE, 0.0);
-    return PollOut{ta, tb, te, pv};
+    const bool to = __any_sync(0xffffffffu, timed_out);
+    const unsigned long long ew = __shfl_sync(0xffffffffu, d, 6);
+    te = ((ew & kXCountMask) != 0 || bad || to) ? 1 : 0;
+    if (l == 0) {
+        if (to) record_error(A.sh[0].err, DERR_XCHG_TIMEOUT, 0.0);
+        else if (bad) record_error(A.sh[0].err, DERR_SUM_RANGE, 0.0);
+    }
+    return PollOut{ta, tb, te, static_cast<unsigned>((ew >> kXInexA) & kXCountMask),
+                   static_cast<unsigned>((ew >> kXInexB) & kXCountMask), pv};
 }
 
 // The same, out of line.  Which one a kernel instantiation uses is a
@@ -282,7 +308,8 @@ __device__ __noinline__ PollOut poll_ool(const SweepArgs& A, const unsigned long
 
 template <bool kOOL = false>
 __device__ __forceinline__ void poll(const SweepArgs& A, const unsigned long long* slots, unsigned long long seq,
-                                     XPrev& pv, double& ta, double& tb, int& te, unsigned long long* stamp) {
+                                     XPrev& pv, double& ta, double& tb, int& te, unsigned long long* stamp,
+                                     unsigned* inexact = nullptr) {
     PollOut o;
     if constexpr (kOOL) o = poll_ool(A, slots, seq, pv, stamp);
     else o = poll_body(A, slots, seq, pv, stamp);
@@ -290,6 +317,22 @@ __device__ __forceinline__ void poll(const SweepArgs& A, const unsigned long lon
     tb = o.tb;
     te = o.te;
     pv = o.pv;
+    if (inexact) {
+        inexact[0] = o.ia;
+        inexact[1] = o.ib;
+    }
+}
+
+// (g, h) from the exchanged sums (engine.hpp:294-296), or DERR_SUM_PRECISION
+// when a partial lost bits below the exchange's 2^-80 resolution and the
+// result is too small for that loss to be negligible (|g| or |h| below
+// P * 2^-40): the reference would step on a gradient / curvature this
+// exchange cannot reproduce, so the fit stops instead of reading h == 0.
+__device__ __forceinline__ int grad_hess_of(double ydx, double tg, double th, const unsigned* inexact, int P,
+                                            double& g, double& h) {
+    g = __dsub_rn(ydx, tg);
+    h = th == 0.0 ? 0.0 : -th;
+    return (precision_lost(fabs(g), inexact[0], P) || precision_lost(th, inexact[1], P)) ? DERR_SUM_PRECISION : 0;
 }
 
 // ---- shared-memory subject tile -----------------------------------------------------
@@ -562,14 +605,18 @@ __global__ void __launch_bounds__(kDT) k_ccd_dense(const __grid_constant__ Sweep
         if (w0) {
             double tg, th;
             int te = 0;
-            poll(A, S.xslots, seq, pv, tg, th, te, nullptr);
+            unsigned inexact[2];
+            poll(A, S.xslots, seq, pv, tg, th, te, nullptr, inexact);
             int status = ST_OK;
             double delta = 0.0;
+            double g, h;
+            const int perr = te ? 0 : grad_hess_of(A.y_dot_x[j], tg, th, inexact, A.P, g, h);
             if (te) {
                 status = ST_REMOTE_ERR;
+            } else if (perr) {
+                status = ST_STEP_ERR;
+                if (c == 0 && threadIdx.x == 0) record_error(S.err, perr, th);
             } else {
-                const double g = __dsub_rn(A.y_dot_x[j], tg);
-                const double h = th == 0.0 ? 0.0 : -th;
                 double step = 0.0;
                 const int serr = penalized_step(A.prior, bj, g, h, &step);
                 if (serr) {
@@ -1015,6 +1062,14 @@ void throw_device_error(int code, double value) {
         internal_error("log_likelihood: nonpositive subject denominator");
     case DERR_SUM_RANGE:
         numeric_error("exact all-reduce: a partial sum outside [0, 2^43) or a total at or above 2^48");
+    case DERR_XCHG_TIMEOUT:
+        internal_error("exact all-reduce: a participant stopped publishing (a peer rank failed or exited); "
+                       "the group must be recreated");
+    case DERR_SUM_PRECISION:
+        std::snprintf(buf, sizeof buf,
+                      "exact all-reduce: a gradient/hessian sum (%g) lies below the exchange's 2^-80 "
+                      "resolution; the fit has drifted to a degenerate coordinate", value);
+        numeric_error(buf);
     default:
         std::snprintf(buf, sizeof buf, "device error code %d", code);
         internal_error(buf);
@@ -1478,6 +1533,12 @@ SweepArgs base_args(const ExchangePlan& plan) {
     a.slots = plan.local_slots;
     a.P = plan.total_participants;
     a.counter = plan.counter;
+    static const unsigned long long timeout_ns = [] {
+        const char* e = std::getenv("BSCCS_XCHG_TIMEOUT_S");
+        const double sec = e ? std::atof(e) : 120.0;
+        return static_cast<unsigned long long>((sec > 0.0 ? sec : 120.0) * 1e9);
+    }();
+    a.poll_timeout_ns = timeout_ns;
     if (a.P > kMaxParticipants) internal_error("exchange plan: too many participants (limit 2048 CTAs over all ranks)");
     return a;
 }

@@ -45,6 +45,10 @@ struct Chunk {
     std::vector<std::string_view> labels;     // local labels in first-appearance order
     long err_line = -1;                       // first error within the chunk (local line number)
     std::string err_msg;                      // message without the "path:line: " prefix
+    // subject of the failing line when its error comes after the reference's
+    // contiguity check (io.hpp:123-132 runs before parse_day and the labels):
+    // that check still has precedence on the same line
+    std::string_view err_subject;
 };
 
 bool parse_int(std::string_view f, int32_t& v) {
@@ -59,9 +63,10 @@ void parse_chunk(Chunk& ch, const std::unordered_map<std::string_view, int32_t>*
     std::vector<int32_t> era;
     const char* p = ch.begin;
     long line_no = 0;
-    auto fail_at = [&](long ln, std::string msg) {
+    auto fail_at = [&](long ln, std::string msg, std::string_view subject = {}) {
         ch.err_line = ln;
         ch.err_msg = std::move(msg);
+        ch.err_subject = subject;
         // count the remaining lines: later chunks number theirs after these
         long n = ln;
         const char* q = p;
@@ -94,9 +99,9 @@ void parse_chunk(Chunk& ch, const std::unordered_map<std::string_view, int32_t>*
         r.subject = fields[0];
         r.line = line_no;
         if (!parse_int(fields[1], r.length))
-            return fail_at(line_no, "expected an integer, got '" + std::string(fields[1]) + "'");
+            return fail_at(line_no, "expected an integer, got '" + std::string(fields[1]) + "'", r.subject);
         if (!parse_int(fields[2], r.events))
-            return fail_at(line_no, "expected an integer, got '" + std::string(fields[2]) + "'");
+            return fail_at(line_no, "expected an integer, got '" + std::string(fields[2]) + "'", r.subject);
         r.first_label = static_cast<uint32_t>(ch.occ.size());
         era.clear();
         if (fields.size() == 4 && !fields[3].empty()) {
@@ -109,7 +114,8 @@ void parse_chunk(Chunk& ch, const std::unordered_map<std::string_view, int32_t>*
                 if (dict) {
                     const auto f = dict->find(label);
                     if (f == dict->end())
-                        return fail_at(line_no, "drug '" + std::string(label) + "' is not in the dictionary");
+                        return fail_at(line_no, "drug '" + std::string(label) + "' is not in the dictionary",
+                                       r.subject);
                     era.push_back(f->second);
                 } else {
                     auto f = local.find(label);
@@ -124,7 +130,7 @@ void parse_chunk(Chunk& ch, const std::unordered_map<std::string_view, int32_t>*
             std::vector<int32_t> sorted(era);
             std::sort(sorted.begin(), sorted.end());
             for (size_t k = 1; k < sorted.size(); ++k)
-                if (sorted[k] == sorted[k - 1]) return fail_at(line_no, "drug listed twice in one era");
+                if (sorted[k] == sorted[k - 1]) return fail_at(line_no, "drug listed twice in one era", r.subject);
         }
         ch.occ.insert(ch.occ.end(), era.begin(), era.end());
         r.nlabels = static_cast<uint32_t>(era.size());
@@ -194,10 +200,12 @@ bsccs_dataset* load_long_format(const char* path, const char* const* dictionary,
     // the earliest line-local error (parse, field count, dictionary, duplicate)
     long first_err = -1;
     std::string first_msg;
+    std::string_view first_subject;
     for (unsigned t = 0; t < T && first_err < 0; ++t)
         if (chunks[t].err_line >= 0) {
             first_err = line_base[t] + chunks[t].err_line;
             first_msg = chunks[t].err_msg;
+            first_subject = chunks[t].err_subject;
         }
     // labels numbered in first-appearance order (chunk order = file order)
     std::vector<std::vector<int32_t>> remap(T);
@@ -246,6 +254,10 @@ bsccs_dataset* load_long_format(const char* path, const char* const* dictionary,
                 line_order.emplace_back(t, i);
             }
         }
+        // the failing line itself: the contiguity check precedes its error
+        if (!stop && first_err >= 0 && !first_subject.empty() && (!have || first_subject != last) &&
+            seen.count(first_subject))
+            first_msg = "rows of subject '" + std::string(first_subject) + "' are not contiguous";
     }
     if (first_err >= 0) input_error(spath + ":" + std::to_string(first_err) + ": " + first_msg);
     rec_start.push_back(static_cast<int64_t>(line_order.size()));

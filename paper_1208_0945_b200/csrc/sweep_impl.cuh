@@ -9,6 +9,9 @@
 
 constexpr int kCached = SWEEP_TILES; // register tiles per data thread
 constexpr int kCap = kCached * kD;   // pairs a CTA keeps in registers per coordinate
+// the repair hash table holds every run head of a cached slice (at most kCap);
+// a full table would make the insert probe spin forever
+static_assert(kCap <= kHt, "repair hash table smaller than the register tiles (raise kHtBits)");
 
 struct Smem {
     double stage[kCap]; // per-pair l*exp (grad/hess) or l*exp delta (update)
@@ -644,10 +647,14 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         if (threadIdx.x < 32) {
             double tg, th;
             int te;
-            poll(A, S.xslots, seq, pv, tg, th, te, nullptr);
+            unsigned inexact[2];
+            poll(A, S.xslots, seq, pv, tg, th, te, nullptr, inexact);
             if (c == 0 && threadIdx.x == 0) {
-                S.res->g = __dsub_rn(A.y_dot_x[j], tg);
-                S.res->h = th == 0.0 ? 0.0 : -th;
+                double g, h;
+                const int perr = grad_hess_of(A.y_dot_x[j], tg, th, inexact, A.P, g, h);
+                if (perr && !te) record_error(S.err, perr, th);
+                S.res->g = g;
+                S.res->h = h;
                 S.res->err_remote = te;
                 if (S.xowner) *S.xcounter = seq + 1;
             }
@@ -787,19 +794,24 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                 const double bv = beta_over_v(A.prior, bj); // while the partials travel
                 double tg, th;
                 int te = 0;
+                unsigned inexact[2] = {0u, 0u};
                 if (A.dbg & 4) {
                     tg = gs;
                     th = hs;
                 } else {
-                    poll<!kSS>(A, S.xslots, seq, pv, tg, th, te, (tr && idx < A.ntrace) ? trb + idx * trs + 5 : nullptr);
+                    poll<!kSS>(A, S.xslots, seq, pv, tg, th, te, (tr && idx < A.ntrace) ? trb + idx * trs + 5 : nullptr,
+                               inexact);
                 }
                 int status = ST_OK;
                 double delta = 0.0;
+                double g, h;
+                const int perr = grad_hess_of(ydx, tg, th, inexact, A.P, g, h);
                 if (te) {
                     status = ST_REMOTE_ERR;
+                } else if (perr) {
+                    status = ST_STEP_ERR;
+                    if (c == 0 && threadIdx.x == 0) record_error(S.err, perr, th);
                 } else {
-                    const double g = __dsub_rn(ydx, tg);
-                    const double h = th == 0.0 ? 0.0 : -th;
                     double step = 0.0;
                     const int serr = penalized_step_pre(A.prior, bj, bv, g, h, &step);
                     if (serr) {

@@ -39,8 +39,9 @@ static_assert(static_cast<unsigned long long>(kMaxParticipants) * kMLimb < kXCnt
 static_assert(kMaxParticipants < (1 << (64 - kXCntShift)), "the count field must hold kMaxParticipants arrivals");
 
 // limb i (0..2) of v in [0, 2^43) at 2^-80 resolution: v = L2*2^2 + L1*2^-39
-// + L0*2^-80 (bits below 2^-80 dropped); false if out of range
-__device__ __forceinline__ bool limb_of(double v, int i, unsigned long long& out) {
+// + L0*2^-80 (bits below 2^-80 dropped: *inexact, limb 0 only); false if out
+// of range
+__device__ __forceinline__ bool limb_of(double v, int i, unsigned long long& out, bool* inexact = nullptr) {
     if (!(v >= 0.0 && v < kXMaxValue)) {
         out = 0;
         return false;
@@ -57,8 +58,23 @@ __device__ __forceinline__ bool limb_of(double v, int i, unsigned long long& out
         out = static_cast<unsigned long long>(t1);
         return true;
     }
-    out = static_cast<unsigned long long>(floor(__dmul_rn(__dsub_rn(s1, t1), 0x1p41))); // exact below 2^-80
+    const double s0 = __dmul_rn(__dsub_rn(s1, t1), 0x1p41); // exact
+    const double t0 = floor(s0);
+    if (inexact) *inexact = s0 != t0; // nonzero bits below 2^-80
+    out = static_cast<unsigned long long>(t0);
     return true;
+}
+
+// Error-word layout (data bits): participants reporting an error in bits
+// 0..11, participants whose first / second partial lost bits below 2^-80 in
+// bits 12..23 / 24..35 (each count <= 2^11).
+constexpr int kXInexA = 12, kXInexB = 24;
+constexpr unsigned long long kXCountMask = 0xfffull;
+// A total T of partials that lost bits is trusted to 2^-40 relative when
+// T >= P * 2^-40 (each of the P partials is short by less than 2^-80);
+// below that the gradient / hessian would be a truncation artefact.
+__device__ __forceinline__ bool precision_lost(double total, unsigned long long inexact, int P) {
+    return inexact != 0 && total < static_cast<double>(P) * 0x1p-40;
 }
 
 __device__ __forceinline__ double pow2(int e) { // 2^e for normal exponents

@@ -16,7 +16,7 @@ from __future__ import annotations
 
 import ctypes as C
 from dataclasses import dataclass
-from typing import List, Sequence
+from typing import List, Optional, Sequence
 
 import numpy as np
 
@@ -56,26 +56,36 @@ def balanced_subject_bounds(ds: Dataset, nshards: int) -> np.ndarray:
     return bounds
 
 
-def shard_dataset(ds: Dataset, nshards: int) -> List[Shard]:
-    """Split `ds` into `nshards` contiguous patient shards."""
+def shard_dataset(ds: Dataset, nshards: int, only: Optional[int] = None) -> List[Shard]:
+    """Split `ds` into `nshards` contiguous patient shards (all of them, or
+    just shard `only`, as one rank of a multi-process fit needs).  A column's
+    pairs are in ascending row -- hence subject -- order, so each shard's
+    part of a column is one contiguous range, found by binary search."""
     bounds = balanced_subject_bounds(ds, nshards)
     J = ds.num_drugs
-    col_nnz = np.diff(ds.col_ptr).astype(np.int64)
-    pair_col = np.repeat(np.arange(J), col_nnz)
+    cp = ds.col_ptr.astype(np.int64)
+    col_nnz = np.diff(cp)
     out = []
-    for r in range(nshards):
+    for r in (range(nshards) if only is None else [int(only)]):
         s0, s1 = int(bounds[r]), int(bounds[r + 1])
         e0, e1 = int(ds.subject_offsets[s0]), int(ds.subject_offsets[s1])
-        sel = (ds.subjects >= s0) & (ds.subjects < s1)
-        # CSC order is (column, row) ascending, so the masked pairs stay in order
-        rows = ds.rows[sel] - e0
-        subs = ds.subjects[sel] - s0
-        cnt = np.bincount(pair_col[sel], minlength=J)
+        lo = np.empty(J, np.int64)
+        hi = np.empty(J, np.int64)
+        for j in range(J):
+            seg = ds.subjects[cp[j]:cp[j + 1]]
+            lo[j] = cp[j] + np.searchsorted(seg, s0, side="left")
+            hi[j] = cp[j] + np.searchsorted(seg, s1, side="left")
+        cnt = hi - lo
+        take = np.concatenate([np.arange(a, b, dtype=np.int64) for a, b in zip(lo, hi)]) if cnt.sum() else \
+            np.zeros(0, np.int64)
+        rows = ds.rows[take] - e0
+        subs = ds.subjects[take] - s0
         col_ptr = np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64)
+        ev = ds.event_counts[ds.rows[take]].astype(np.int64)
+        ydx = np.add.reduceat(ev, np.minimum(col_ptr[:-1], ev.size - 1)) if ev.size else np.zeros(J, np.int64)
+        ydx = np.where(cnt > 0, ydx, 0).astype(np.int64)
         sub_ds = Dataset(ds.subject_offsets[s0:s1 + 1] - e0, ds.events_per_subject[s0:s1],
-                         ds.era_lengths[e0:e1], ds.event_counts[e0:e1], col_ptr, rows, subs,
-                         y_dot_x=np.bincount(pair_col[sel], weights=ds.event_counts[ds.rows[sel]],
-                                             minlength=J).astype(np.int64))
+                         ds.era_lengths[e0:e1], ds.event_counts[e0:e1], col_ptr, rows, subs, y_dot_x=ydx)
         out.append(Shard(sub_ds, s0, s1, e0, ds.y_dot_x.copy(), col_nnz.copy()))
     return out
 

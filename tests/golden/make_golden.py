@@ -215,6 +215,50 @@ def drivers_case(ref: po.Reference):
             "resample_77_1_head": rds.resample(77, 1)[:32].tolist(), "cv": cv, "bootstrap": boot}
 
 
+def drivers_1M(ref: po.Reference):
+    """Configs 4 and 5 at their named size (1M x 1500) by the reference:
+    the full config-4 grid_search_cv (8 folds x 8 points, Laplace, seed 17,
+    warm), a 16-replicate prefix of config 5's run_bootstrap (Normal 0.1,
+    seed 77, warm; replicate r depends only on (seed, r), so the prefix is
+    an exact sub-run) and the per-replicate estimates of r = 0..3
+    (bootstrap.hpp:103-112).  About 30 min on 8 cores."""
+    from concurrent.futures import ThreadPoolExecutor
+    t0 = time.time()
+    ds = datagen.fast_sccs(1_030_000, 1500, 3.0)
+    rds = ref.fast_sccs(1_030_000, 1500, 3.0, threads=8)
+    out = {"workload": "1M", "attempts": 1_030_000, "drugs": 1500, "lambda_x": 3.0, "seed": datagen.FAST_SEED,
+           "digest": digest(ds), "sizes": {"N": ds.num_subjects, "K": ds.num_eras, "J": ds.num_drugs,
+                                            "nnz": ds.nnz}}
+    lo, hi = np.log(0.001), np.log(10.0)
+    grid = [float(np.exp(lo + (hi - lo) * i / 7.0)) for i in range(8)]
+    cv = {"folds": 8, "grid": grid, "prior": "laplace", "seed": 17, "warm_start": True}
+    r = rds.grid_search_cv(8, grid, B.PriorKind.laplace, 17, B.SolverConfig(), warm_start=True, threads=8)
+    cv["expected"] = {"variance_grid": r["variance_grid"].tolist(),
+                      "predictive_ll": [[repr(float(x)) for x in row] for row in r["predictive_ll"]],
+                      "cycles": r["cycles"].tolist(), "converged": r["converged"].tolist(),
+                      "valid": r["valid"].tolist(),
+                      "mean_predictive_ll": [repr(float(x)) for x in r["mean_predictive_ll"]],
+                      "selected_index": r["selected_index"], "selected_variance": r["selected_variance"],
+                      "total_cycles": r["total_cycles"]}
+    cv["reference_seconds_8_threads"] = time.time() - t0
+    out["cv"] = cv
+    print(f"  cv done {time.time() - t0:.0f}s", flush=True)
+    t1 = time.time()
+    boot = {"replicates": 16, "level": 0.95, "seed": 77, "prior": "normal", "variance": 0.1, "warm_start": True}
+    b = rds.run_bootstrap(16, 0.95, 77, B.normal_prior(0.1), B.SolverConfig(), warm_start=True, threads=8)
+    boot["expected"] = {k: ([repr(float(x)) for x in v] if isinstance(v, np.ndarray) else v) for k, v in b.items()}
+    boot["reference_seconds_8_threads"] = time.time() - t1
+    out["bootstrap"] = boot
+    print(f"  bootstrap done {time.time() - t0:.0f}s", flush=True)
+    beta_full = b["beta_full"]
+    with ThreadPoolExecutor(4) as ex:
+        reps = list(ex.map(lambda rr: rds.bootstrap_replicate(77, rr, B.normal_prior(0.1), B.SolverConfig(),
+                                                                beta_full), range(4)))
+    out["replicates"] = [{"r": i, **fit_dict(x)} for i, x in enumerate(reps)]
+    print(f"  replicates done {time.time() - t0:.0f}s", flush=True)
+    return out
+
+
 def main():
     ref = po.Reference()
     large = "--large" in sys.argv
@@ -251,6 +295,9 @@ def main():
         (OUT / "fit_10M_laplace.json").write_text(json.dumps(
             fast_case(ref, "10M", 10_300_000, 4000, 3.0, B.laplace_prior(0.1)), indent=1))
         print("fit_10M_laplace.json")
+    if large and want("drivers_1M"):
+        (OUT / "drivers_1M.json").write_text(json.dumps(drivers_1M(ref), indent=1))
+        print("drivers_1M.json")
 
 
 if __name__ == "__main__":

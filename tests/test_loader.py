@@ -117,6 +117,8 @@ def test_dictionary_pins_order(ref, tmp_path):
     "p1\t5\t0\ta a\n",                # a drug twice in one era
     "\t5\t0\n",                       # empty subject id
     "p1\t5\t0\np2\t5\t0\np1\t5\t0\n",  # rows of a subject not contiguous
+    "p1\t5\t0\np2\t5\t0\np1\tfive\t0\n",  # ... on a line that also has a bad integer
+    "p1\t5\t0\ta\np2\t5\t0\np1\t5\t0\ta a\n",  # ... and a drug twice
     "p1\t0\t1\ta\n",                  # build_dataset: era length must be positive
     "p1\t5\t-1\ta\np1\t5\t2\tb\n",    # build_dataset: negative event count
     "p1\t5\t0\ta\n",                  # no subject with events
