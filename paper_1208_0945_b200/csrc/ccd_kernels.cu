@@ -323,16 +323,39 @@ __device__ __forceinline__ void poll(const SweepArgs& A, const unsigned long lon
     }
 }
 
-// (g, h) from the exchanged sums (engine.hpp:294-296), or DERR_SUM_PRECISION
-// when a partial lost bits below the exchange's 2^-80 resolution and the
-// result is too small for that loss to be negligible (|g| or |h| below
-// P * 2^-40): the reference would step on a gradient / curvature this
-// exchange cannot reproduce, so the fit stops instead of reading h == 0.
-__device__ __forceinline__ int grad_hess_of(double ydx, double tg, double th, const unsigned* inexact, int P,
-                                            double& g, double& h) {
-    g = __dsub_rn(ydx, tg);
-    h = th == 0.0 ? 0.0 : -th;
-    return (precision_lost(fabs(g), inexact[0], P) || precision_lost(th, inexact[1], P)) ? DERR_SUM_PRECISION : 0;
+// Warp 0, after the first poll of a (gs, hs) exchange: when a total came out
+// with fewer than 53 significant bits (partials that lost bits below 2^-80;
+// xchg.cuh needs_refine), exchange the same partials again scaled by powers
+// of two until it does -- the reference forms gs and hs in full double
+// precision however small (engine.hpp:108-129), so tiny gradients and
+// curvatures must not read as 0.  Degenerate fits only (a coordinate driven
+// to w ~ 0); every participant takes the same rounds.  `seq` advances by one
+// per extra round.  Out of line: the common path only tests the counts.
+__device__ __noinline__ void refine_sums(const SweepArgs& A, const unsigned long long* slots, unsigned long long& seq,
+                                         XPrev& pv, double a, double b, int e, double& ta, double& tb, int& te,
+                                         unsigned ia, unsigned ib) {
+    int sa = 0, sb = 0;
+    double va = ta, vb = tb;
+    for (;;) {
+        const bool na = needs_refine(va, ia, sa), nb = needs_refine(vb, ib, sb);
+        if (!na && !nb) break;
+        if (na) sa = next_scale(va, ia, sa);
+        if (nb) sb = next_scale(vb, ib, sb);
+        ++seq;
+        publish(A, seq, ldexp(a, sa), ldexp(b, sb), e);
+        const PollOut o = poll_body(A, slots, seq, pv, nullptr);
+        pv = o.pv;
+        if (o.te) {
+            te = 1;
+            return;
+        }
+        va = ldexp(o.ta, -sa); // exact power-of-two rescale
+        vb = ldexp(o.tb, -sb);
+        ia = o.ia;
+        ib = o.ib;
+    }
+    ta = va;
+    tb = vb;
 }
 
 // ---- shared-memory subject tile -----------------------------------------------------
@@ -607,16 +630,14 @@ __global__ void __launch_bounds__(kDT) k_ccd_dense(const __grid_constant__ Sweep
             int te = 0;
             unsigned inexact[2];
             poll(A, S.xslots, seq, pv, tg, th, te, nullptr, inexact);
+            if (!te && (inexact[0] | inexact[1])) refine_sums(A, S.xslots, seq, pv, gs, hs, e, tg, th, te, inexact[0], inexact[1]);
             int status = ST_OK;
             double delta = 0.0;
-            double g, h;
-            const int perr = te ? 0 : grad_hess_of(A.y_dot_x[j], tg, th, inexact, A.P, g, h);
             if (te) {
                 status = ST_REMOTE_ERR;
-            } else if (perr) {
-                status = ST_STEP_ERR;
-                if (c == 0 && threadIdx.x == 0) record_error(S.err, perr, th);
             } else {
+                const double g = __dsub_rn(A.y_dot_x[j], tg);
+                const double h = th == 0.0 ? 0.0 : -th;
                 double step = 0.0;
                 const int serr = penalized_step(A.prior, bj, g, h, &step);
                 if (serr) {
@@ -1065,11 +1086,7 @@ void throw_device_error(int code, double value) {
     case DERR_XCHG_TIMEOUT:
         internal_error("exact all-reduce: a participant stopped publishing (a peer rank failed or exited); "
                        "the group must be recreated");
-    case DERR_SUM_PRECISION:
-        std::snprintf(buf, sizeof buf,
-                      "exact all-reduce: a gradient/hessian sum (%g) lies below the exchange's 2^-80 "
-                      "resolution; the fit has drifted to a degenerate coordinate", value);
-        numeric_error(buf);
+
     default:
         std::snprintf(buf, sizeof buf, "device error code %d", code);
         internal_error(buf);

@@ -31,8 +31,7 @@ enum DevError {
     DERR_POS_CURVATURE = 5,     // internal_error prior.hpp:73-75
     DERR_LL_DEN_NONPOSITIVE = 6, // internal_error engine.hpp:418-420
     DERR_SUM_RANGE = 7,          // exact exchange: a partial >= 2^43 or a total >= 2^48 (xchg.cuh)
-    DERR_XCHG_TIMEOUT = 8,       // exact exchange: a participant stopped publishing (peer rank gone)
-    DERR_SUM_PRECISION = 9       // exact exchange: a gradient/hessian sum below its 2^-80 resolution
+    DERR_XCHG_TIMEOUT = 8        // exact exchange: a participant stopped publishing (peer rank gone)
 };
 
 struct PriorParams {

@@ -649,12 +649,10 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             int te;
             unsigned inexact[2];
             poll(A, S.xslots, seq, pv, tg, th, te, nullptr, inexact);
+            if (!te && (inexact[0] | inexact[1])) refine_sums(A, S.xslots, seq, pv, gs, hs, err, tg, th, te, inexact[0], inexact[1]);
             if (c == 0 && threadIdx.x == 0) {
-                double g, h;
-                const int perr = grad_hess_of(A.y_dot_x[j], tg, th, inexact, A.P, g, h);
-                if (perr && !te) record_error(S.err, perr, th);
-                S.res->g = g;
-                S.res->h = h;
+                S.res->g = __dsub_rn(A.y_dot_x[j], tg);
+                S.res->h = th == 0.0 ? 0.0 : -th;
                 S.res->err_remote = te;
                 if (S.xowner) *S.xcounter = seq + 1;
             }
@@ -802,16 +800,15 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                     poll<!kSS>(A, S.xslots, seq, pv, tg, th, te, (tr && idx < A.ntrace) ? trb + idx * trs + 5 : nullptr,
                                inexact);
                 }
+                if (!te && (inexact[0] | inexact[1]))
+                    refine_sums(A, S.xslots, seq, pv, gs, hs, e, tg, th, te, inexact[0], inexact[1]);
                 int status = ST_OK;
                 double delta = 0.0;
-                double g, h;
-                const int perr = grad_hess_of(ydx, tg, th, inexact, A.P, g, h);
                 if (te) {
                     status = ST_REMOTE_ERR;
-                } else if (perr) {
-                    status = ST_STEP_ERR;
-                    if (c == 0 && threadIdx.x == 0) record_error(S.err, perr, th);
                 } else {
+                    const double g = __dsub_rn(ydx, tg);
+                    const double h = th == 0.0 ? 0.0 : -th;
                     double step = 0.0;
                     const int serr = penalized_step_pre(A.prior, bj, bv, g, h, &step);
                     if (serr) {

@@ -70,11 +70,22 @@ __device__ __forceinline__ bool limb_of(double v, int i, unsigned long long& out
 // bits 12..23 / 24..35 (each count <= 2^11).
 constexpr int kXInexA = 12, kXInexB = 24;
 constexpr unsigned long long kXCountMask = 0xfffull;
-// A total T of partials that lost bits is trusted to 2^-40 relative when
-// T >= P * 2^-40 (each of the P partials is short by less than 2^-80);
-// below that the gradient / hessian would be a truncation artefact.
-__device__ __forceinline__ bool precision_lost(double total, unsigned long long inexact, int P) {
-    return inexact != 0 && total < static_cast<double>(P) * 0x1p-40;
+// Refinement of small totals.  A partial below 2^-28 can carry bits below
+// the 2^-80 resolution; the total then has fewer than 53 significant bits
+// when it is below (inexact partials) * 2^-80 * 2^53.  Every participant sees
+// the same totals and counts, so all of them decide alike to exchange the
+// same partials again scaled by 2^s, with s chosen from an upper bound U of
+// every partial (U = total + loss bound; partials are >= 0) so that the
+// scaled partials stay below 2^42.  Each round gains >= 57 bits of
+// resolution; at s = kXMaxScale the resolution is 2^-1074 (every double is
+// representable) and the sum is exact.
+constexpr int kXMaxScale = 994;
+__device__ __forceinline__ bool needs_refine(double total, unsigned inexact, int s) {
+    return inexact != 0 && s < kXMaxScale && total < ldexp(static_cast<double>(inexact), 53 - 80 - s);
+}
+__device__ __forceinline__ int next_scale(double total, unsigned inexact, int s) {
+    const double U = total + ldexp(static_cast<double>(inexact), -80 - s);
+    return min(kXMaxScale, max(s + 1, 41 - ilogb(U)));
 }
 
 __device__ __forceinline__ double pow2(int e) { // 2^e for normal exponents

@@ -60,6 +60,26 @@ def test_two_subject_dyadic_exact():
     assert gh.hessian == -0.625
 
 
+@pytest.mark.parametrize("b", [-40.0, -60.0, -200.0, -600.0])
+def test_tiny_weights_keep_full_precision(ref, b):
+    """Hessian terms far below the exchange's 2^-80 resolution (w ~ e^b, a
+    coordinate driven towards -inf): the scaled refinement rounds of the
+    exchange (xchg.cuh needs_refine) reproduce the reference's (g, h) to
+    1e-12 relative -- not h == 0, which would take the reference's h == 0
+    branches (prior.hpp:95-98,107-109) where the reference does not"""
+    rng = B.Rng(5151)
+    ds = random_dataset(rng, 3, 60)
+    beta = [b, 0.3, -0.2]
+    st = B.init_state(ds, beta)
+    rs = ref.dataset(ds).state(beta)
+    for j in range(3):
+        a = B.fused_grad_hess(ds, st, j)
+        g, h = rs.grad_hess(j)
+        assert h < 0.0 and a.hessian < 0.0
+        assert abs(a.hessian - h) <= 1e-12 * abs(h), (j, a.hessian, h)
+        assert abs(a.gradient - g) <= 1e-12 * abs(g) if g != 0.0 else a.gradient == 0.0
+
+
 def test_weights_in_unit_interval_and_no_negative_zero(port):
     rng = B.Rng(31)
     for trial in range(30):

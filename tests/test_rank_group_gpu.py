@@ -99,6 +99,8 @@ def _worker(rank, world, port_no, mode, q, go):
             else:  # joins the group, then never fits; stays alive until told
                 q.put((rank, "idle"))
                 go.wait(300)
+            q.close()
+            q.join_thread()  # flush the queue's feeder thread before the hard exit
             os._exit(0)  # no collective close: the peer is gone from the protocol
     except Exception as e:  # pragma: no cover
         q.put((rank, "error", repr(e)))
