@@ -331,7 +331,7 @@ __device__ __forceinline__ void poll(const SweepArgs& A, const unsigned long lon
 // curvatures must not read as 0.  Degenerate fits only (a coordinate driven
 // to w ~ 0); every participant takes the same rounds.  `seq` advances by one
 // per extra round.  Out of line: the common path only tests the counts.
-__device__ __noinline__ void refine_sums(const SweepArgs& A, const unsigned long long* slots, unsigned long long& seq,
+__device__ __forceinline__ void refine_sums(const SweepArgs& A, const unsigned long long* slots, unsigned long long& seq,
                                          XPrev& pv, double a, double b, int e, double& ta, double& tb, int& te,
                                          unsigned ia, unsigned ib) {
     int sa = 0, sb = 0;
