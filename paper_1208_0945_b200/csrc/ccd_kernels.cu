@@ -79,7 +79,7 @@ struct ShardArgs {
     const unsigned long long* xslots; // exchange area this shard polls (its rank's)
     unsigned long long* xcounter;     // exchange sequence word of that area
     int xowner;                       // this shard's CTA 0 stores the area's baseline / counter
-    const int2* pairs;
+    const int4* pq;                   // {era slot, block slot, era length, subject - cta_subj[c]} per pair
     double* snap;
     const longlong2* vsplit; // [ctas][nvisit] (p0, p1) of each CTA's slice in visit order
     uint8_t* moved;          // [nvisit] delta != 0 per visited coordinate (CTA 0 writes)
@@ -90,8 +90,10 @@ struct ShardArgs {
     const int32_t* cta_subj;  // [ctas+1] first subject of each CTA (dense path)
     const int32_t* subject_offsets;
     double* num;              // [N] run numerators of the dense path (zero between uses)
-    EraRec* era;
-    SubjRec* subj;
+    double* X;                // subject blocks {den, n, x'beta of each era}
+    const int32_t* row_slot;  // [K] slot of each era
+    const int32_t* bstart;    // [N] block of each subject
+    const int32_t* era_len;   // [K] era lengths (dense path)
     double* beta;
     double* trust;
     DevErr* err;
@@ -112,6 +114,7 @@ struct SweepArgs {
     int J;
     PriorParams prior;
     int mode;
+    int visit_begin; // kModeSweep: first visit-list entry of this launch
     int single_j;
     double single_delta;
     int normalized;
@@ -141,30 +144,23 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 // ---- memory helpers ----------------------------------------------------------
 
-__device__ __forceinline__ int2 ld_pair(const int2* p) { return __ldg(p); }
+// one 16-byte load of the sweep's pair record (read-only for the launch)
+__device__ __forceinline__ int4 ld_pq(const int4* p) { return __ldg(p); }
+// the subject index field alone (run-edge tests of neighbouring pairs)
+__device__ __forceinline__ int ld_pq_sub(const int4* p) { return __ldg(&p->w); }
 
-// one 16-byte load of an era record (read-write data: no read-only path)
-struct Rec {
-    double xb;
-    int len, y;
-};
-__device__ __forceinline__ Rec ld_rec(const EraRec* p) {
-    const int4 q = *reinterpret_cast<const int4*>(p);
-    Rec r;
-    r.xb = __hiloint2double(q.y, q.x);
-    r.len = q.z;
-    r.y = q.w;
-    return r;
-}
+// x'beta of an era / the header {den, n} of a subject block (read-write
+// data: no read-only path; the header is 16-B aligned, bstart is even)
+__device__ __forceinline__ double ld_x(const double* X, int slot) { return X[slot]; }
 struct Subj {
     double den;
     int n;
 };
-__device__ __forceinline__ Subj ld_subj(const SubjRec* p) {
-    const int4 q = *reinterpret_cast<const int4*>(p);
+__device__ __forceinline__ Subj ld_hdr(const double* X, int slot) {
+    const double2 h = *reinterpret_cast<const double2*>(X + slot);
     Subj r;
-    r.den = __hiloint2double(q.y, q.x);
-    r.n = q.z;
+    r.den = h.x;
+    r.n = static_cast<int>(h.y);
     return r;
 }
 
@@ -329,11 +325,21 @@ __device__ __forceinline__ void poll(const SweepArgs& A, const unsigned long lon
 // of two until it does -- the reference forms gs and hs in full double
 // precision however small (engine.hpp:108-129), so tiny gradients and
 // curvatures must not read as 0.  Degenerate fits only (a coordinate driven
-// to w ~ 0); every participant takes the same rounds.  `seq` advances by one
-// per extra round.  Out of line: the common path only tests the counts.
-__device__ __forceinline__ void refine_sums(const SweepArgs& A, const unsigned long long* slots, unsigned long long& seq,
-                                         XPrev& pv, double a, double b, int e, double& ta, double& tb, int& te,
-                                         unsigned ia, unsigned ib) {
+// to w ~ 0); every participant takes the same rounds, `seq` advances by one
+// per extra round.  Used by the single-coordinate grad/hess launch and the
+// dense route; the sweep loop only detects the need and stops (ST_REFINE),
+// and the host finishes that coordinate through the single-coordinate
+// launches (run_sweep): compiled into the loop, even never taken, these
+// rounds slowed the config-2 fit by half (code size and register pressure).
+struct Refined {
+    double sum_a, sum_b;
+    int err;
+    unsigned long long next_seq;
+    XPrev prev;
+};
+__device__ __forceinline__ Refined refine_sums(const SweepArgs& A, const unsigned long long* slots, unsigned long long seq,
+                                            XPrev pv, double a, double b, int e, double ta, double tb, unsigned ia,
+                                            unsigned ib) {
     int sa = 0, sb = 0;
     double va = ta, vb = tb;
     for (;;) {
@@ -345,18 +351,27 @@ __device__ __forceinline__ void refine_sums(const SweepArgs& A, const unsigned l
         publish(A, seq, ldexp(a, sa), ldexp(b, sb), e);
         const PollOut o = poll_body(A, slots, seq, pv, nullptr);
         pv = o.pv;
-        if (o.te) {
-            te = 1;
-            return;
-        }
+        if (o.te) return Refined{va, vb, 1, seq, pv};
         va = ldexp(o.ta, -sa); // exact power-of-two rescale
         vb = ldexp(o.tb, -sb);
         ia = o.ia;
         ib = o.ib;
     }
-    ta = va;
-    tb = vb;
+    return Refined{va, vb, 0, seq, pv};
 }
+
+// the call site: the common path only tests the two counts
+#define BSCCS_REFINE(A, slots, seq, pv, a, b, e, ta, tb, te, inexact)                                \
+    do {                                                                                              \
+        if (!(te) && ((inexact)[0] | (inexact)[1])) {                                                 \
+            const Refined r_ = refine_sums(A, slots, seq, pv, a, b, e, ta, tb, (inexact)[0], (inexact)[1]); \
+            ta = r_.sum_a;                                                                            \
+            tb = r_.sum_b;                                                                            \
+            te = r_.err;                                                                              \
+            seq = r_.next_seq;                                                                        \
+            pv = r_.prev;                                                                             \
+        }                                                                                             \
+    } while (0)
 
 // ---- shared-memory subject tile -----------------------------------------------------
 //
@@ -378,65 +393,74 @@ constexpr size_t subj_tile_bytes(bool touch) { return sizeof(double) + sizeof(in
 
 // ---- pair slots -------------------------------------------------------------------
 
-// Index data of one pair slot: the pair, whether it starts a subject run
-// (head) and whether the run continues past it.
+// Index data of one pair slot: the pair record, whether it starts a subject
+// run (head) and whether the run continues past it.
 struct PairSlot {
-    int2 pr;
+    int xs;  // era slot (-1: no pair)
+    int ds;  // subject block slot
+    int len; // era length
+    int ls;  // subject index within the CTA's range (run identity, tile index)
     bool head;
     bool cont;
 };
 
-// Loads of one pair slot, issued ahead of use: the pair plus (lane 0 / lane
-// 31 only) the subjects just outside the warp.  finalize_slot() turns them
-// into head / continuation flags with warp shuffles (all lanes of a warp).
+// Loads of one pair slot, issued ahead of use: the pair record plus (lane 0
+// / lane 31 only) the subjects just outside the warp.  finalize_slot() turns
+// them into head / continuation flags with warp shuffles (all lanes of a warp).
 struct RawSlot {
-    int2 pr;
+    int4 q;
     int edge; // lane 0: subject of pair p-1 ; lane 31: subject of pair p+1
     bool first, last_valid;
 };
 
-__device__ __forceinline__ RawSlot issue_slot(const int2* __restrict__ pairs, int64_t p, int64_t p0, int64_t p1) {
+__device__ __forceinline__ RawSlot issue_slot(const int4* __restrict__ pq, int64_t p, int64_t p0, int64_t p1) {
     RawSlot r;
     const bool valid = p < p1;
     const int l = lane_id();
-    r.pr = valid ? ld_pair(pairs + p) : make_int2(-1, -1);
+    r.q = valid ? ld_pq(pq + p) : make_int4(-1, -1, 0, -1);
     r.first = valid && p == p0;
     r.last_valid = p + 1 < p1;
     // one load instruction for both edge lanes (two would serialise the
     // warp on the shared destination register)
     r.edge = -1;
     const bool lo = l == 0 && valid && p > p0, hi = l == 31 && p + 1 < p1;
-    if (lo || hi) r.edge = ld_pair(pairs + (lo ? p - 1 : p + 1)).y;
+    if (lo || hi) r.edge = ld_pq_sub(pq + (lo ? p - 1 : p + 1));
     return r;
 }
 
 __device__ __forceinline__ PairSlot finalize_slot(const RawSlot& r) {
     PairSlot s;
     const int l = lane_id();
-    int prev = __shfl_up_sync(0xffffffffu, r.pr.y, 1);
-    int next = __shfl_down_sync(0xffffffffu, r.pr.y, 1);
+    int prev = __shfl_up_sync(0xffffffffu, r.q.w, 1);
+    int next = __shfl_down_sync(0xffffffffu, r.q.w, 1);
     if (l == 0) prev = r.edge;
     if (l == 31) next = r.edge;
-    const bool valid = r.pr.x >= 0;
-    s.pr = r.pr;
-    s.head = valid && (r.first || prev != r.pr.y);
-    s.cont = valid && r.last_valid && next == r.pr.y;
+    const bool valid = r.q.x >= 0;
+    s.xs = r.q.x;
+    s.ds = r.q.y;
+    s.len = r.q.z;
+    s.ls = r.q.w;
+    s.head = valid && (r.first || prev != r.q.w);
+    s.cont = valid && r.last_valid && next == r.q.w;
     return s;
 }
 
 __device__ __forceinline__ PairSlot invalid_slot() {
     PairSlot s;
-    s.pr = make_int2(-1, -1);
+    s.xs = -1;
+    s.ds = -1;
+    s.len = 0;
+    s.ls = -1;
     s.head = false;
     s.cont = false;
     return s;
 }
 
-__device__ __forceinline__ PairSlot load_slot(const int2* __restrict__ pairs, int64_t p, int64_t p0, int64_t p1) {
-    return finalize_slot(issue_slot(pairs, p, p0, p1));
+__device__ __forceinline__ PairSlot load_slot(const int4* __restrict__ pq, int64_t p, int64_t p0, int64_t p1) {
+    return finalize_slot(issue_slot(pq, p, p0, p1));
 }
 
-__device__ __forceinline__ bool slot_valid(const PairSlot& s) { return s.pr.x >= 0; }
+__device__ __forceinline__ bool slot_valid(const PairSlot& s) { return s.xs >= 0; }
 
 // Data-warp order: warps share schedulers by (warp % 4), so the control warp's
 // scheduler-mates (warps 4, 8, ...) take the highest data ranks -- on small
@@ -515,7 +539,7 @@ struct UpdErr {
     double errv;
 };
 
-enum StepStatus { ST_OK = 0, ST_REMOTE_ERR = 1, ST_STEP_ERR = 2, ST_NONFINITE = 3 };
+enum StepStatus { ST_OK = 0, ST_REMOTE_ERR = 1, ST_STEP_ERR = 2, ST_NONFINITE = 3, ST_REFINE = 4 };
 
 // ---- the sweep kernel, per register-tile count -------------------------------
 namespace t3 {
@@ -599,22 +623,21 @@ __global__ void __launch_bounds__(kDT) k_ccd_dense(const __grid_constant__ Sweep
         }
         // run numerators of the column into num[subject] (engine.hpp:376-380)
         for (int64_t p = sl.x + threadIdx.x; p < sl.y; p += kDT) {
-            const int2 pr = ld_pair(S.pairs + p);
-            if (p > sl.x && ld_pair(S.pairs + p - 1).y == pr.y) continue;
+            const int4 pr = ld_pq(S.pq + p);
+            if (p > sl.x && ld_pq_sub(S.pq + p - 1) == pr.w) continue;
             double numv = 0.0;
             for (int64_t q = p; q < sl.y; ++q) {
-                const int2 p2 = ld_pair(S.pairs + q);
-                if (p2.y != pr.y) break;
-                const Rec r = ld_rec(S.era + p2.x);
-                numv = __dadd_rn(numv, lexp(r.len, r.xb));
+                const int4 p2 = ld_pq(S.pq + q);
+                if (p2.w != pr.w) break;
+                numv = __dadd_rn(numv, lexp(p2.z, ld_x(S.X, p2.x)));
             }
-            S.num[pr.y] = numv;
+            S.num[s0 + pr.w] = numv;
         }
         __syncthreads();
         // full sweep over the CTA's subjects (engine.hpp:381-395)
         double gs = 0.0, hs = 0.0;
         for (int s = s0 + static_cast<int>(threadIdx.x); s < s1; s += kDT) {
-            const Subj sr = ld_subj(S.subj + s);
+            const Subj sr = ld_hdr(S.X, S.bstart[s]);
             if (!(sr.den > 0.0)) err = DERR_DEN_NONPOSITIVE;
             double w = S.num[s] / sr.den;
             if (w > 1.0) w = 1.0;
@@ -630,7 +653,7 @@ __global__ void __launch_bounds__(kDT) k_ccd_dense(const __grid_constant__ Sweep
             int te = 0;
             unsigned inexact[2];
             poll(A, S.xslots, seq, pv, tg, th, te, nullptr, inexact);
-            if (!te && (inexact[0] | inexact[1])) refine_sums(A, S.xslots, seq, pv, gs, hs, e, tg, th, te, inexact[0], inexact[1]);
+            BSCCS_REFINE(A, S.xslots, seq, pv, gs, hs, e, tg, th, te, inexact);
             int status = ST_OK;
             double delta = 0.0;
             if (te) {
@@ -666,7 +689,7 @@ __global__ void __launch_bounds__(kDT) k_ccd_dense(const __grid_constant__ Sweep
         const int status = sm.status;
         const double delta = sm.delta;
         // the numerators are consumed: back to zero for the next column
-        for (int64_t p = sl.x + threadIdx.x; p < sl.y; p += kDT) S.num[ld_pair(S.pairs + p).y] = 0.0;
+        for (int64_t p = sl.x + threadIdx.x; p < sl.y; p += kDT) S.num[s0 + ld_pq_sub(S.pq + p)] = 0.0;
         if (status != ST_OK) {
             aborted = true;
             if (status == ST_REMOTE_ERR && c == 0 && threadIdx.x == 0) S.res->err_remote = 1;
@@ -677,22 +700,23 @@ __global__ void __launch_bounds__(kDT) k_ccd_dense(const __grid_constant__ Sweep
             ++nmoved;
             // x'beta of the column's rows (solver.hpp:138-143) ...
             for (int64_t p = sl.x + threadIdx.x; p < sl.y; p += kDT) {
-                const int row = ld_pair(S.pairs + p).x;
-                S.era[row].xb = __dadd_rn(S.era[row].xb, delta);
+                const int xs = ld_pq(S.pq + p).x;
+                S.X[xs] = __dadd_rn(S.X[xs], delta);
             }
             __syncthreads();
             // ... then every denominator rebuilt from x'beta (engine.hpp:68-90)
             for (int s = s0 + static_cast<int>(threadIdx.x); s < s1; s += kDT) {
                 double total = 0.0;
-                for (int k = S.subject_offsets[s]; k < S.subject_offsets[s + 1]; ++k) {
-                    const Rec r = ld_rec(S.era + k);
-                    if (!(fabs(r.xb) <= kXbBound)) {
+                const int b = S.bstart[s] + kBlockHeader, k0 = S.subject_offsets[s];
+                for (int k = k0; k < S.subject_offsets[s + 1]; ++k) {
+                    const double xb = S.X[b + (k - k0)];
+                    if (!(fabs(xb) <= kXbBound)) {
                         err = DERR_OVERFLOW;
-                        errv = fabs(r.xb);
+                        errv = fabs(xb);
                     }
-                    total = __dadd_rn(total, lexp(r.len, r.xb));
+                    total = __dadd_rn(total, lexp(S.era_len[k], xb));
                 }
-                S.subj[s].den = total;
+                S.X[S.bstart[s]] = total;
             }
         }
         __syncthreads();
@@ -702,7 +726,7 @@ __global__ void __launch_bounds__(kDT) k_ccd_dense(const __grid_constant__ Sweep
         const int e0 = S.cta_era[c], e1 = S.cta_era[c + 1];
         double ch = 0.0, mg = 0.0;
         for (int k = e0 + static_cast<int>(threadIdx.x); k < e1; k += kDT) {
-            const double xb = S.era[k].xb;
+            const double xb = S.X[S.row_slot[k]];
             ch = __dadd_rn(ch, fabs(__dsub_rn(xb, S.snap[k])));
             if (A.normalized) mg = __dadd_rn(mg, fabs(xb));
             S.snap[k] = xb;
@@ -728,6 +752,7 @@ __global__ void __launch_bounds__(kDT) k_ccd_dense(const __grid_constant__ Sweep
         S.res->visited = nvisit;
         S.res->moved = nmoved;
         S.res->counter = seq;
+        S.res->refine_at = -1; // refines in place
         if (S.xowner) *S.xcounter = seq;
     }
     if (c == 0 && S.xowner) xprev_store(S.xslots, pv);
@@ -735,32 +760,25 @@ __global__ void __launch_bounds__(kDT) k_ccd_dense(const __grid_constant__ Sweep
 
 // ---- dense kernels ---------------------------------------------------------
 
-__global__ void k_init_records(EraRec* era, SubjRec* subj, const int32_t* len, const int32_t* y, const int32_t* n,
-                               int32_t K, int32_t N) {
-    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < K;
-         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        EraRec r;
-        r.xb = 0.0;
-        r.len = len[k];
-        r.y = y[k];
-        era[k] = r;
-    }
+// zero state: every block's header {den 0, n_i} and x'beta 0 for its eras
+__global__ void k_init_blocks(double* X, const int32_t* __restrict__ bstart, const int32_t* __restrict__ off,
+                              const int32_t* __restrict__ n, int32_t N) {
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < N;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        SubjRec s;
-        s.den = 0.0;
-        s.n = n[i];
-        s.pad = 0;
-        subj[i] = s;
+        const int b = bstart[i];
+        X[b] = 0.0;
+        X[b + 1] = static_cast<double>(n[i]);
+        const int E = off[i + 1] - off[i];
+        for (int q = 0; q < E; ++q) X[b + kBlockHeader + q] = 0.0;
     }
 }
 
 // xbeta_k = sum over drugs of row k in ascending j of beta_j, skipping
 // zeros (engine.hpp:173-181), with the overflow guard (engine.hpp:70-74).
 // snapshot := xbeta.
-__global__ void k_dense_xb(EraRec* era, double* snap, const int64_t* __restrict__ csr_ptr,
-                           const int32_t* __restrict__ csr_col, const double* __restrict__ beta, int32_t K,
-                           DevErr* err) {
+__global__ void k_dense_xb(double* X, double* snap, const int64_t* __restrict__ csr_ptr,
+                           const int32_t* __restrict__ csr_col, const double* __restrict__ beta,
+                           const int32_t* __restrict__ row_slot, int32_t K, DevErr* err) {
     for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < K;
          k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         double xb = 0.0;
@@ -769,51 +787,52 @@ __global__ void k_dense_xb(EraRec* era, double* snap, const int64_t* __restrict_
             if (b != 0.0) xb = __dadd_rn(xb, b);
         }
         if (!(fabs(xb) <= kXbBound)) record_error(err, DERR_OVERFLOW, fabs(xb));
-        era[k].xb = xb;
+        X[row_slot[k]] = xb;
         snap[k] = xb;
     }
 }
 
 // denominators: per subject, ascending sum of l*exp(x'beta) (engine.hpp:76-89)
-__global__ void k_dense_den(const EraRec* era, SubjRec* subj, const int32_t* __restrict__ off, int32_t N) {
+__global__ void k_dense_den(double* X, const int32_t* __restrict__ len, const int32_t* __restrict__ off,
+                            const int32_t* __restrict__ bstart, int32_t N) {
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < N;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int b = bstart[i], k0 = off[i], k1 = off[i + 1];
         double total = 0.0;
-        for (int32_t k = off[i]; k < off[i + 1]; ++k) {
-            const Rec r = ld_rec(era + k);
-            total = __dadd_rn(total, lexp(r.len, r.xb));
-        }
-        subj[i].den = total;
+        for (int k = k0; k < k1; ++k) total = __dadd_rn(total, lexp(len[k], X[b + kBlockHeader + (k - k0)]));
+        X[b] = total;
     }
 }
 
-__global__ void k_snapshot(const EraRec* era, double* snap, int32_t K) {
+__global__ void k_snapshot(const double* X, const int32_t* __restrict__ row_slot, double* snap, int32_t K) {
     for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < K;
          k += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        snap[k] = era[k].xb;
+        snap[k] = X[row_slot[k]];
 }
 
-__global__ void k_lexp(const EraRec* era, double* out, int32_t K) {
-    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < K;
-         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const Rec r = ld_rec(era + k);
-        out[k] = lexp(r.len, r.xb);
+// out[i] = X[idx[i]] (+ l*exp when len != nullptr): state_get's gathers
+__global__ void k_gather_slots(const double* X, const int32_t* __restrict__ idx, const int32_t* __restrict__ len,
+                               double* out, int64_t n) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double x = X[idx[i]];
+        out[i] = len ? lexp(len[i], x) : x;
     }
 }
 
-__global__ void k_ll_partial(const EraRec* era, const SubjRec* subj, int32_t K, int32_t N, double* partial,
-                             DevErr* err) {
+__global__ void k_ll_partial(const double* X, const int32_t* __restrict__ row_slot, const int32_t* __restrict__ y,
+                             const int32_t* __restrict__ bstart, int32_t K, int32_t N, double* partial, DevErr* err) {
     double lin = 0.0, lg = 0.0;
     for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < K;
          k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int y = era[k].y;
-        if (y != 0) lin = __dadd_rn(lin, __dmul_rn(static_cast<double>(y), era[k].xb));
+        const int yk = y[k];
+        if (yk != 0) lin = __dadd_rn(lin, __dmul_rn(static_cast<double>(yk), X[row_slot[k]]));
     }
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < N;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const SubjRec s = subj[i];
-        if (!(s.den > 0.0)) record_error(err, DERR_LL_DEN_NONPOSITIVE, s.den);
-        lg = __dadd_rn(lg, __dmul_rn(static_cast<double>(s.n), log(s.den)));
+        const Subj sr = ld_hdr(X, bstart[i]);
+        if (!(sr.den > 0.0)) record_error(err, DERR_LL_DEN_NONPOSITIVE, sr.den);
+        lg = __dadd_rn(lg, __dmul_rn(static_cast<double>(sr.n), log(sr.den)));
     }
     __shared__ double sa[kLLThreads / 32], sb[kLLThreads / 32];
 #pragma unroll
@@ -827,13 +846,13 @@ __global__ void k_ll_partial(const EraRec* era, const SubjRec* subj, int32_t K, 
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        double x = 0.0, y = 0.0;
+        double x = 0.0, y2 = 0.0;
         for (int w = 0; w < kLLThreads / 32; ++w) {
             x = __dadd_rn(x, sa[w]);
-            y = __dadd_rn(y, sb[w]);
+            y2 = __dadd_rn(y2, sb[w]);
         }
         partial[2 * blockIdx.x] = x;
-        partial[2 * blockIdx.x + 1] = y;
+        partial[2 * blockIdx.x + 1] = y2;
     }
 }
 
@@ -1019,6 +1038,67 @@ __global__ void k_ydotx(const int2* pairs, const int64_t* col_ptr, const int32_t
     }
 }
 
+// ---- subject blocks (engine.h) --------------------------------------------
+// Blocks are packed per chunk of kBlockChunk subjects, each chunk from a line
+// boundary (chunks pack in parallel; the gaps cost < 2%).  A block of
+// z = 2 + E slots starts on an even slot (its 16-B header load); if z <= 16
+// it never straddles a 16-slot (128-B) line, a longer one starts on a line.
+__device__ __forceinline__ long long pack_at(long long c, int z) {
+    c = (c + 1) & ~1ll;
+    const long long in_line = c & (kLineSlots - 1);
+    if (z > kLineSlots ? in_line != 0 : in_line + z > kLineSlots) c = (c + kLineSlots - 1) & ~(kLineSlots - 1ll);
+    return c;
+}
+
+__global__ void k_block_chunks(const int32_t* __restrict__ off, int32_t N, long long* chunk_slots, int64_t nchunks) {
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < nchunks;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t s1 = min(static_cast<int64_t>(N), (t + 1) * kBlockChunk);
+        long long c = 0;
+        for (int64_t i = t * kBlockChunk; i < s1; ++i) {
+            const int z = kBlockHeader + (off[i + 1] - off[i]);
+            c = pack_at(c, z) + z;
+        }
+        chunk_slots[t] = (c + kLineSlots - 1) & ~(kLineSlots - 1ll);
+    }
+}
+
+__global__ void k_block_place(const int32_t* __restrict__ off, int32_t N, const long long* __restrict__ chunk_base,
+                              int64_t nchunks, int32_t* bstart, int32_t* row_slot) {
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < nchunks;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t s1 = min(static_cast<int64_t>(N), (t + 1) * kBlockChunk);
+        const long long base = chunk_base[t];
+        long long c = 0;
+        for (int64_t i = t * kBlockChunk; i < s1; ++i) {
+            const int k0 = off[i], E = off[i + 1] - k0, z = kBlockHeader + E;
+            c = pack_at(c, z);
+            bstart[i] = static_cast<int32_t>(base + c);
+            for (int q = 0; q < E; ++q) row_slot[k0 + q] = static_cast<int32_t>(base + c + kBlockHeader + q);
+            c += z;
+        }
+    }
+}
+
+// The sweep's pair records: {era slot, block slot, era length, subject index
+// within the owning CTA's range} (the CTA that owns the subject owns the
+// pair's slice: splits are subject-aligned).
+__global__ void k_build_pq(const int2* __restrict__ pairs, int64_t nnz, const int32_t* __restrict__ row_slot,
+                           const int32_t* __restrict__ bstart, const int32_t* __restrict__ len,
+                           const int32_t* __restrict__ cta_subj, int C, int4* pq) {
+    for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < nnz;
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int2 pr = pairs[p];
+        int lo = 0, hi = C + 1; // first c with cta_subj[c] > subject
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (cta_subj[mid] > pr.y) hi = mid;
+            else lo = mid + 1;
+        }
+        pq[p] = make_int4(row_slot[pr.x], bstart[pr.y], len[pr.x], pr.y - cta_subj[lo - 1]);
+    }
+}
+
 // Small pinned result blocks for the per-state D2H of kernel scalars.
 struct PinnedResults {
     std::mutex m;
@@ -1128,6 +1208,9 @@ void alloc_dataset(bsccs_dataset* ds) {
     CUDA_TRY(cudaStreamCreateWithFlags(&ds->stream, cudaStreamNonBlocking));
     cudaStream_t s = ds->stream;
     ds->pairs = dalloc<int2>(nnz, B, s);
+    ds->pq = dalloc<int4>(nnz, B, s);
+    ds->row_slot = dalloc<int32_t>(K, B, s);
+    ds->bstart = dalloc<int32_t>(N, B, s);
     ds->col_ptr = dalloc<int64_t>(J + 1, B, s);
     ds->split = dalloc<int64_t>(static_cast<int64_t>(J) * (C + 1), B, s);
     ds->cta_era = dalloc<int32_t>(C + 1, B, s);
@@ -1204,6 +1287,34 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
         const int64_t nsplit = static_cast<int64_t>(J) * (C + 1);
         k_split<<<static_cast<int>((nsplit + 255) / 256), 256, 0, s>>>(ds->pairs, ds->col_ptr, J, ds->cta_subj, C,
                                                                         ds->split);
+        // subject blocks and the sweep's pair records (engine.h)
+        {
+            const int64_t nch = (static_cast<int64_t>(N) + kBlockChunk - 1) / kBlockChunk;
+            int64_t b3 = 0;
+            long long* d_cs = dalloc<long long>(nch + 1, b3, s);
+            long long* d_cb = dalloc<long long>(nch + 1, b3, s);
+            CUDA_TRY(cudaMemsetAsync(d_cs + nch, 0, sizeof(long long), s));
+            k_block_chunks<<<grid_for(nch, 128, sms), 128, 0, s>>>(ds->subject_offsets, N, d_cs, nch);
+            size_t sb = 0;
+            CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, sb, d_cs, d_cb, nch + 1, s));
+            unsigned char* tmp2 = dalloc<unsigned char>(static_cast<int64_t>(std::max<size_t>(sb, 16)), b3, s);
+            CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp2, sb, d_cs, d_cb, nch + 1, s));
+            long long total = 0;
+            CUDA_TRY(cudaMemcpyAsync(&total, d_cb + nch, sizeof(long long), cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+            if (total >= (1ll << 31) - kLineSlots)
+                input_error("dataset: eras plus subject headers exceed the 32-bit slot range");
+            ds->nslots = total;
+            k_block_place<<<grid_for(nch, 128, sms), 128, 0, s>>>(ds->subject_offsets, N, d_cb, nch, ds->bstart,
+                                                                  ds->row_slot);
+            if (nnz > 0)
+                k_build_pq<<<grid_for(nnz, 256, sms), 256, 0, s>>>(ds->pairs, nnz, ds->row_slot, ds->bstart,
+                                                                   ds->era_lengths, ds->cta_subj, C, ds->pq);
+            count_launches(3 + (nnz > 0 ? 1 : 0));
+            dfree(tmp2, s);
+            dfree(d_cs, s);
+            dfree(d_cb, s);
+        }
         if (y_dot_x_global) {
             std::vector<double> yd(static_cast<size_t>(J));
             for (int32_t j = 0; j < J; ++j) yd[static_cast<size_t>(j)] = static_cast<double>(y_dot_x_global[j]);
@@ -1345,6 +1456,9 @@ void dataset_destroy(bsccs_dataset* ds) {
     cudaSetDevice(ds->device);
     cudaStream_t s = ds->stream;
     dfree(ds->pairs, s);
+    dfree(ds->pq, s);
+    dfree(ds->row_slot, s);
+    dfree(ds->bstart, s);
     dfree(ds->col_ptr, s);
     dfree(ds->split, s);
     dfree(ds->cta_era, s);
@@ -1371,8 +1485,9 @@ namespace {
 void launch_dense(bsccs_state* st) {
     const bsccs_dataset* ds = st->ds;
     const int g = build_grid(ds->device);
-    k_dense_xb<<<g, 256, 0, st->stream>>>(st->era, st->snap, ds->csr_ptr, ds->csr_col, st->beta, ds->K, st->err);
-    k_dense_den<<<g, 256, 0, st->stream>>>(st->era, st->subj, ds->subject_offsets, ds->N);
+    k_dense_xb<<<g, 256, 0, st->stream>>>(st->X, st->snap, ds->csr_ptr, ds->csr_col, st->beta, ds->row_slot, ds->K,
+                                          st->err);
+    k_dense_den<<<g, 256, 0, st->stream>>>(st->X, ds->era_lengths, ds->subject_offsets, ds->bstart, ds->N);
     CUDA_TRY(cudaGetLastError());
     count_launches(2);
     st->snap_valid = true;
@@ -1384,9 +1499,8 @@ void alloc_state(bsccs_state* st, const bsccs_dataset* ds) {
     ensure_pool(ds->device);
     CUDA_TRY(cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking));
     cudaStream_t s = st->stream;
-    st->era = dalloc<EraRec>(ds->K, b, s);
+    st->X = dalloc<double>(ds->nslots, b, s);
     st->snap = dalloc<double>(ds->K, b, s);
-    st->subj = dalloc<SubjRec>(ds->N, b, s);
     st->beta = dalloc<double>(ds->J, b, s);
     st->trust = dalloc<double>(ds->J, b, s);
     st->visit = dalloc<int32_t>(ds->J, b, s);
@@ -1418,8 +1532,8 @@ bsccs_state* state_create(const bsccs_dataset* ds, const double* beta_host) {
     try {
         alloc_state(st, ds);
         const int grid = build_grid(ds->device);
-        k_init_records<<<grid, 256, 0, st->stream>>>(st->era, st->subj, ds->era_lengths, ds->event_counts,
-                                                     ds->events_per_subject, ds->K, ds->N);
+        k_init_blocks<<<grid, 256, 0, st->stream>>>(st->X, ds->bstart, ds->subject_offsets, ds->events_per_subject,
+                                                    ds->N);
         count_launches(1);
         if (beta_host)
             CUDA_TRY(cudaMemcpyAsync(st->beta, beta_host, sizeof(double) * ds->J, cudaMemcpyHostToDevice, st->stream));
@@ -1442,9 +1556,8 @@ bsccs_state* state_clone(const bsccs_state* src) {
     try {
         alloc_state(st, ds);
         CUDA_TRY(cudaStreamSynchronize(src->stream));
-        CUDA_TRY(cudaMemcpyAsync(st->era, src->era, sizeof(EraRec) * ds->K, cudaMemcpyDeviceToDevice, st->stream));
+        CUDA_TRY(cudaMemcpyAsync(st->X, src->X, sizeof(double) * ds->nslots, cudaMemcpyDeviceToDevice, st->stream));
         CUDA_TRY(cudaMemcpyAsync(st->snap, src->snap, sizeof(double) * ds->K, cudaMemcpyDeviceToDevice, st->stream));
-        CUDA_TRY(cudaMemcpyAsync(st->subj, src->subj, sizeof(SubjRec) * ds->N, cudaMemcpyDeviceToDevice, st->stream));
         CUDA_TRY(cudaMemcpyAsync(st->beta, src->beta, sizeof(double) * ds->J, cudaMemcpyDeviceToDevice, st->stream));
         st->snap_valid = src->snap_valid;
         sync_and_check(st);
@@ -1462,11 +1575,10 @@ void state_destroy(bsccs_state* st) {
     if (st->ds) cudaSetDevice(st->ds->device);
     cudaStream_t s = st->stream;
     if (s) {
-        dfree(st->era, s);
+        dfree(st->X, s);
         dfree(st->snap, s);
         dfree(st->le_tmp, s);
         dfree(st->num, s);
-        dfree(st->subj, s);
         dfree(st->beta, s);
         dfree(st->trust, s);
         dfree(st->visit, s);
@@ -1514,7 +1626,7 @@ SweepArgs base_args(const ExchangePlan& plan) {
         s.xslots = plan.shard_slots.empty() ? plan.local_slots : plan.shard_slots[i];
         s.xcounter = plan.shard_counters.empty() ? plan.counter : plan.shard_counters[i];
         s.xowner = plan.shard_slots.empty() ? (i == 0) : 1;
-        s.pairs = st->ds->pairs;
+        s.pq = st->ds->pq;
         s.snap = st->snap;
         s.vsplit = st->vsplit;
         s.moved = st->moved;
@@ -1526,8 +1638,10 @@ SweepArgs base_args(const ExchangePlan& plan) {
         s.cta_subj = st->ds->cta_subj;
         s.subject_offsets = st->ds->subject_offsets;
         s.num = st->num;
-        s.era = st->era;
-        s.subj = st->subj;
+        s.X = st->X;
+        s.row_slot = st->ds->row_slot;
+        s.bstart = st->ds->bstart;
+        s.era_len = st->ds->era_lengths;
         s.beta = st->beta;
         s.trust = st->trust;
         s.err = st->err;
@@ -1733,7 +1847,8 @@ void sparse_update(bsccs_state* st, int32_t j, double delta) {
 double log_likelihood(bsccs_state* st) {
     const bsccs_dataset* ds = st->ds;
     DeviceGuard dg(ds->device);
-    k_ll_partial<<<kLLBlocks, kLLThreads, 0, st->stream>>>(st->era, st->subj, ds->K, ds->N, st->scratch, st->err);
+    k_ll_partial<<<kLLBlocks, kLLThreads, 0, st->stream>>>(st->X, ds->row_slot, ds->event_counts, ds->bstart, ds->K,
+                                                           ds->N, st->scratch, st->err);
     k_ll_final<<<1, 32, 0, st->stream>>>(st->scratch, kLLBlocks, st->res);
     count_launches(2);
     CUDA_TRY(cudaMemcpyAsync(st->res_h, st->res, sizeof(DevResult), cudaMemcpyDeviceToHost, st->stream));
@@ -1747,33 +1862,28 @@ void state_get(bsccs_state* st, double* beta, double* xbeta, double* le, double*
     DeviceGuard dg(ds->device);
     CUDA_TRY(cudaStreamSynchronize(st->stream));
     if (beta) CUDA_TRY(cudaMemcpy(beta, st->beta, sizeof(double) * ds->J, cudaMemcpyDeviceToHost));
-    if (xbeta) {
-        std::vector<EraRec> e(static_cast<size_t>(ds->K));
-        CUDA_TRY(cudaMemcpy(e.data(), st->era, sizeof(EraRec) * ds->K, cudaMemcpyDeviceToHost));
-        for (int32_t k = 0; k < ds->K; ++k) xbeta[k] = e[static_cast<size_t>(k)].xb;
+    if (!st->le_tmp) {
+        int64_t b = 0;
+        st->le_tmp = dalloc<double>(std::max(ds->K, ds->N), b, st->stream);
     }
-    if (le) { // recomputed on the device with the kernels' own expression
-        if (!st->le_tmp) {
-            int64_t b = 0;
-            st->le_tmp = dalloc<double>(ds->K, b, st->stream);
-        }
-        k_lexp<<<build_grid(ds->device), 256, 0, st->stream>>>(st->era, st->le_tmp, ds->K);
+    // gathered out of the subject blocks on the device (l*exp with the
+    // kernels' own expression)
+    auto gather = [&](const int32_t* idx, const int32_t* len, int64_t n, double* out) {
+        k_gather_slots<<<build_grid(ds->device), 256, 0, st->stream>>>(st->X, idx, len, st->le_tmp, n);
         count_launches(1);
-        CUDA_TRY(cudaMemcpyAsync(le, st->le_tmp, sizeof(double) * ds->K, cudaMemcpyDeviceToHost, st->stream));
+        CUDA_TRY(cudaMemcpyAsync(out, st->le_tmp, sizeof(double) * n, cudaMemcpyDeviceToHost, st->stream));
         CUDA_TRY(cudaStreamSynchronize(st->stream));
-    }
-    if (den) {
-        std::vector<SubjRec> s(static_cast<size_t>(ds->N));
-        CUDA_TRY(cudaMemcpy(s.data(), st->subj, sizeof(SubjRec) * ds->N, cudaMemcpyDeviceToHost));
-        for (int32_t i = 0; i < ds->N; ++i) den[i] = s[static_cast<size_t>(i)].den;
-    }
+    };
+    if (xbeta) gather(ds->row_slot, nullptr, ds->K, xbeta);
+    if (le) gather(ds->row_slot, ds->era_lengths, ds->K, le);
+    if (den) gather(ds->bstart, nullptr, ds->N, den);
 }
 
 void prepare_snapshot(bsccs_state* st) {
     if (st->snap_valid) return;
     const bsccs_dataset* ds = st->ds;
     DeviceGuard dg(ds->device);
-    k_snapshot<<<build_grid(ds->device), 256, 0, st->stream>>>(st->era, st->snap, ds->K);
+    k_snapshot<<<build_grid(ds->device), 256, 0, st->stream>>>(st->X, ds->row_slot, st->snap, ds->K);
     CUDA_TRY(cudaGetLastError());
     count_launches(1);
     st->snap_valid = true;
@@ -1890,6 +2000,60 @@ void build_vsplit(const bsccs_dataset* ds, const int32_t* d_visit, int V, longlo
     count_launches(1);
 }
 
+namespace {
+
+void check_plan_errors(const ExchangePlan& plan) {
+    for (auto* st : plan.shards) check_err_block(st);
+    for (auto* st : plan.shards)
+        if (st->res_h->err_remote) numeric_error("sweep aborted: a device error was raised on another shard");
+}
+
+// One coordinate finished on the host's side of the C ABI after the sweep
+// stopped before it (ST_REFINE): the single-coordinate grad/hess launch
+// (exact exchange with refinement rounds), the reference step on the host
+// (the same prior.h code the kernel runs, solver.hpp:131-150), and the
+// single-coordinate update launch.  Every rank of a group takes the same
+// path (the stop is decided from identical exchange results).  Returns
+// whether the coordinate moved.
+bool refine_coordinate(const ExchangePlan& plan, const PriorParams& prior, int32_t j) {
+    bsccs_state* s0 = plan.shards[0];
+    SweepArgs g = base_args(plan);
+    g.mode = kModeGradHess;
+    g.single_j = j;
+    launch_ccd(plan, g);
+    for (auto* st : plan.shards)
+        CUDA_TRY(cudaMemcpyAsync(st->res_h, st->res, sizeof(DevResult), cudaMemcpyDeviceToHost, s0->stream));
+    double bj = 0.0, rj = 0.0;
+    CUDA_TRY(cudaMemcpyAsync(&bj, s0->beta + j, sizeof(double), cudaMemcpyDeviceToHost, s0->stream));
+    CUDA_TRY(cudaMemcpyAsync(&rj, s0->trust + j, sizeof(double), cudaMemcpyDeviceToHost, s0->stream));
+    CUDA_TRY(cudaStreamSynchronize(s0->stream));
+    CUDA_TRY(cudaGetLastError());
+    check_plan_errors(plan);
+    const double gv = s0->res_h->g, hv = s0->res_h->h;
+    double step = 0.0;
+    const int serr = penalized_step_pre(prior, bj, beta_over_v(prior, bj), gv, hv, &step);
+    if (serr) throw_device_error(serr, hv);
+    const double delta = clamp_step(step, rj);
+    if (delta != 0.0 && !std::isfinite(delta)) throw_device_error(DERR_STEP_NONFINITE, delta);
+    if (delta != 0.0) {
+        SweepArgs u = base_args(plan);
+        u.mode = kModeUpdate;
+        u.single_j = j;
+        u.single_delta = delta;
+        launch_ccd(plan, u);
+        CUDA_TRY(cudaStreamSynchronize(s0->stream));
+        CUDA_TRY(cudaGetLastError());
+        for (auto* st : plan.shards) check_err_block(st);
+    }
+    const double rn = next_trust(delta, rj);
+    for (auto* st : plan.shards)
+        CUDA_TRY(cudaMemcpyAsync(st->trust + j, &rn, sizeof(double), cudaMemcpyHostToDevice, s0->stream));
+    CUDA_TRY(cudaStreamSynchronize(s0->stream));
+    return delta != 0.0;
+}
+
+} // namespace
+
 SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool normalized, bool dense) {
     bsccs_state* s0 = plan.shards[0];
     if (dense && (plan.shards.size() != 1 || plan.dst.size() != 1))
@@ -1937,46 +2101,61 @@ SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool 
         if (st->stream != s0->stream) CUDA_TRY(cudaStreamSynchronize(st->stream));
     }
     if (s0->visit_h.size() != visit.size()) internal_error("visit list mismatch across shards");
-    SweepArgs a = base_args(plan);
-    a.mode = kModeSweep;
-    a.dbg = g_debug_flags;
-    a.trace = g_trace;
-    a.ntrace = g_ntrace;
-    a.prior = prior;
-    a.normalized = normalized ? 1 : 0;
     CUDA_TRY(cudaEventRecord(s0->ev0, s0->stream));
-    if (dense) {
-        void* params[] = {&a};
-        CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_ccd_dense), dim3(s0->ds->ctas), dim3(kDT),
-                                             params, 0, s0->stream));
-        count_launches(1);
-    } else {
-        launch_ccd(plan, a);
+    // Launch from `begin`; a launch that stops before a coordinate whose sums
+    // need refinement (res->refine_at) is followed by that coordinate on the
+    // single-coordinate path and a relaunch after it.
+    long long visited = 0, nmoved = 0;
+    std::vector<std::pair<int, uint8_t>> refined; // (visit index, moved)
+    int begin = 0;
+    for (;;) {
+        SweepArgs a = base_args(plan);
+        a.mode = kModeSweep;
+        a.visit_begin = begin;
+        a.dbg = g_debug_flags;
+        a.trace = g_trace;
+        a.ntrace = g_ntrace;
+        a.prior = prior;
+        a.normalized = normalized ? 1 : 0;
+        if (dense) {
+            void* params[] = {&a};
+            CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_ccd_dense), dim3(s0->ds->ctas), dim3(kDT),
+                                                 params, 0, s0->stream));
+            count_launches(1);
+        } else {
+            launch_ccd(plan, a);
+        }
+        for (size_t i = 0; i < plan.shards.size(); ++i) {
+            bsccs_state* st = plan.shards[i];
+            CUDA_TRY(cudaMemcpyAsync(st->res_h, st->res, sizeof(DevResult), cudaMemcpyDeviceToHost, s0->stream));
+        }
+        CUDA_TRY(cudaStreamSynchronize(s0->stream));
+        CUDA_TRY(cudaGetLastError());
+        check_plan_errors(plan);
+        visited += s0->res_h->visited;
+        nmoved += s0->res_h->moved;
+        const int ra = s0->res_h->refine_at;
+        if (ra < 0) break;
+        const bool mv = refine_coordinate(plan, prior, visit[static_cast<size_t>(ra)]);
+        refined.emplace_back(ra, mv ? 1 : 0);
+        ++visited;
+        nmoved += mv ? 1 : 0;
+        begin = ra + 1;
     }
     CUDA_TRY(cudaEventRecord(s0->ev1, s0->stream));
-    SweepOutcome out{0.0, 0, 0};
-    for (size_t i = 0; i < plan.shards.size(); ++i) {
-        bsccs_state* st = plan.shards[i];
-        CUDA_TRY(cudaMemcpyAsync(st->res_h, st->res, sizeof(DevResult), cudaMemcpyDeviceToHost, s0->stream));
-    }
     std::vector<uint8_t> moved(visit.size());
     if (!visit.empty())
         CUDA_TRY(cudaMemcpyAsync(moved.data(), s0->moved, visit.size(), cudaMemcpyDeviceToHost, s0->stream));
     CUDA_TRY(cudaStreamSynchronize(s0->stream));
-    CUDA_TRY(cudaGetLastError());
-    for (auto* st : plan.shards) {
-        st->snap_valid = true;
-        check_err_block(st);
-    }
-    for (auto* st : plan.shards)
-        if (st->res_h->err_remote) numeric_error("sweep aborted: a device error was raised on another shard");
+    for (const auto& r : refined) moved[static_cast<size_t>(r.first)] = r.second;
+    for (auto* st : plan.shards) st->snap_valid = true;
     float ms = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&ms, s0->ev0, s0->ev1));
     s0->sweep_ms += ms;
     // SURVEY §8(d) algorithmic bytes of this sweep, every shard: per visited
     // coordinate 16*nnz_j + 12*u_j, per moved one + 28*nnz_j + 8*u_j, plus
     // 32*K for the criterion / snapshot pass
-    const long long nv = s0->res_h->visited;
+    const long long nv = visited;
     for (auto* st : plan.shards) {
         const bsccs_dataset* d = st->ds;
         double bytes = 32.0 * static_cast<double>(d->K);
@@ -1994,9 +2173,10 @@ SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool 
         }
         s0->alg_bytes += bytes;
     }
+    SweepOutcome out{0.0, 0, 0};
     out.criterion = s0->res_h->criterion;
-    out.visited = s0->res_h->visited;
-    out.moved = s0->res_h->moved;
+    out.visited = visited;
+    out.moved = nmoved;
     return out;
 }
 

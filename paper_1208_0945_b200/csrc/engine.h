@@ -3,17 +3,25 @@
 // HBM layout:
 //   pairs     int2[nnz]      {row, subject} of every nonzero, CSC order
 //                            (SparseColumn::rows/::subjects interleaved,
-//                            dataset.hpp:38-43) -> one 8-byte load per pair
+//                            dataset.hpp:38-43): dataset build, batched
+//                            engine, subset builder, export
+//   pq        int4[nnz]      the sweep's view of the same pairs:
+//                            {era slot, subject block slot, era length,
+//                            subject index within its CTA's range}
 //   split     int64[J][C+1]  first pair of column j owned by CTA c; CTAs own
 //                            contiguous subject ranges, so a column's pairs
 //                            split into C contiguous, subject-aligned slices
 //   csr_ptr/  row -> drug list (ascending), built once by a stable radix sort;
 //   csr_col                  gives dense_recompute the reference's per-row
 //                            addition order (engine.hpp:173-181) w/o atomics
-//   EraRec    16 B / era     {x'beta, len, y}: one 16-byte load per scattered
-//                            era access; l*exp(x'beta) recomputed, see below
+//   X         f64 slots      per subject one block [den, n, x'beta of each
+//                            era]: a block of <= 16 slots never straddles a
+//                            128-B line, so a scattered pair visit reads ONE
+//                            line for its era's x'beta and its subject's
+//                            denominator (the L2 fills whole 128-B lines:
+//                            scripts/gbench4.cu).  l*exp(x'beta) recomputed.
+//   row_slot  int32[K]       slot of era k; bstart int32[N]: block of subject i
 //   snap      8 B / era      criterion snapshot (streamed once per cycle)
-//   SubjRec   16 B / subject {denominator, n_i}
 #pragma once
 
 #include <cuda_runtime.h>
@@ -30,20 +38,14 @@ namespace bsccs_b200 {
 // l*exp(x'beta) is not stored: the reference keeps l_exp_xbeta[k] ==
 // era_lengths[k] * exp(xbeta[k]) bit for bit at every write (init_state and
 // dense_recompute, engine.hpp:77-78; sparse_delta_update, engine.hpp:221-228),
-// so the device recomputes it from the 16-byte record instead of moving it.
-struct __align__(16) EraRec {
-    double xb;   // x'_k beta                      (EngineState::xbeta)
-    int32_t len; // era length l_k                 (Dataset::era_lengths)
-    int32_t y;   // event count y_k                (Dataset::event_counts)
-};
-static_assert(sizeof(EraRec) == 16, "EraRec must be 16 bytes");
-
-struct __align__(16) SubjRec {
-    double den; // sum of le over the subject's eras (EngineState::denominators)
-    int32_t n;  // events_per_subject
-    int32_t pad;
-};
-static_assert(sizeof(SubjRec) == 16, "SubjRec must be 16 bytes");
+// so the device recomputes it from x'beta and the length in the pair stream.
+//
+// Subject blocks: slot bstart[i] = denominator (EngineState::denominators),
+// bstart[i] + 1 = n_i as a double (events_per_subject, exact), then one slot
+// of x'beta (EngineState::xbeta) per era of the subject in row order.
+constexpr int kBlockHeader = 2;
+constexpr int kLineSlots = 16;    // 128-B line / 8-B slot
+constexpr int kBlockChunk = 64;   // subjects packed per build thread (each chunk starts on a line)
 
 // Per-state device scalars written by kernels, mirrored to pinned host.
 struct DevResult {
@@ -56,6 +58,7 @@ struct DevResult {
     unsigned long long counter; // exchange sequence after the launch
     int err_code;
     int err_remote; // error seen in the exchange (possibly another shard)
+    int refine_at;  // sweep stopped before this visit-list entry: its sums need refinement (run_sweep)
 };
 
 struct DevErr {
@@ -84,6 +87,10 @@ struct bsccs_dataset {
     int ctas = 0;
     // device arrays
     int2* pairs = nullptr;
+    int4* pq = nullptr;               // [nnz] {era slot, block slot, era length, subject - cta_subj[c]}
+    int32_t* row_slot = nullptr;      // [K]
+    int32_t* bstart = nullptr;        // [N]
+    int64_t nslots = 0;               // slots of the per-subject blocks
     int64_t* col_ptr = nullptr;
     int64_t* split = nullptr;         // [J*(ctas+1)]
     int32_t* cta_era = nullptr;       // [ctas+1]
@@ -112,11 +119,10 @@ struct bsccs_group;
 struct bsccs_state {
     const bsccs_dataset* ds = nullptr;
     cudaStream_t stream = nullptr;
-    bsccs_b200::EraRec* era = nullptr;
+    double* X = nullptr;                 // [ds->nslots] subject blocks {den, n, x'beta...}
     double* snap = nullptr;              // [K] criterion snapshot
     double* le_tmp = nullptr;            // [K] scratch for state_get
     double* num = nullptr;               // [N] run numerators of the dense path (lazy)
-    bsccs_b200::SubjRec* subj = nullptr;
     double* beta = nullptr;
     double* trust = nullptr;
     int32_t* visit = nullptr;            // [J] this cycle's visit list (device)

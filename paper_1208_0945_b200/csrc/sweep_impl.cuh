@@ -29,7 +29,7 @@ struct Smem {
     // a subject run crossing a chunk edge of a streamed slice: its partial
     // numerator (grad/hess) or denominator (update), carried to the next chunk
     double cr_num, cr_den;
-    int cr_on, cr_subj, cr_n;
+    int cr_on, cr_subj, cr_n, cr_ds;
 };
 
 // ---- CTA reduction -------------------------------------------------------------
@@ -82,7 +82,7 @@ struct RawCached {
 __device__ __forceinline__ void load_cached(const ShardArgs& S, int64_t p0, int64_t p1, Cached& C) {
 #pragma unroll
     for (int v = 0; v < kCached; ++v) {
-        if (warp_active(v, p0, p1)) C.slot[v] = load_slot(S.pairs, p0 + slot_pos(v), p0, p1);
+        if (warp_active(v, p0, p1)) C.slot[v] = load_slot(S.pq, p0 + slot_pos(v), p0, p1);
         else C.slot[v] = invalid_slot();
     }
 }
@@ -91,9 +91,9 @@ __device__ __forceinline__ void issue_cached(const ShardArgs& S, int64_t p0, int
 #pragma unroll
     for (int v = 0; v < kCached; ++v) {
         if (warp_active(v, p0, p1)) {
-            R.slot[v] = issue_slot(S.pairs, p0 + slot_pos(v), p0, p1);
+            R.slot[v] = issue_slot(S.pq, p0 + slot_pos(v), p0, p1);
         } else {
-            R.slot[v].pr = make_int2(-1, -1);
+            R.slot[v].q = make_int4(-1, -1, 0, -1);
             R.slot[v].edge = -1;
             R.slot[v].first = false;
             R.slot[v].last_valid = false;
@@ -105,34 +105,32 @@ __device__ __forceinline__ void finalize_cached(const RawCached& R, Cached& C) {
 #pragma unroll
     for (int v = 0; v < kCached; ++v) {
         // warp-uniform: a warp whose tile is empty has every lane invalid
-        if (__any_sync(0xffffffffu, R.slot[v].pr.x >= 0)) C.slot[v] = finalize_slot(R.slot[v]);
+        if (__any_sync(0xffffffffu, R.slot[v].q.x >= 0)) C.slot[v] = finalize_slot(R.slot[v]);
         else C.slot[v] = invalid_slot();
     }
 }
 
-// Per-lane records of the register tiles.  Every lane gathers its own era
-// record; run heads also gather the subject record.  Runs are combined from
-// shared memory in ascending pair order, so a head never issues a dependent
-// global load unless its run spills past the register tiles.
+// Per-lane records of the register tiles.  Every lane gathers its era's
+// x'beta; run heads also gather their subject block's header {den, n} --
+// in the same 128-B line as the era for nearly every pair (engine.h).  Runs
+// are combined from shared memory in ascending pair order, so a head never
+// issues a dependent global load unless its run spills past the register
+// tiles.
 struct HeadRegs {
     double xb[kCached], le[kCached], den[kCached];
-    int len[kCached], n[kCached];
+    int n[kCached];
 };
 
 // loads only (the registers are consumed later): lets the speculative
 // gathers ride through the exchange without holding up the step broadcast
 template <bool kSS>
 __device__ __forceinline__ void issue_records(const ShardArgs& S, const Cached& C, HeadRegs& H) {
-    EraRec* era = S.era;
-    SubjRec* subj = S.subj;
 #pragma unroll
     for (int v = 0; v < kCached; ++v) {
         if (slot_valid(C.slot[v])) {
-            const Rec r = ld_rec(era + C.slot[v].pr.x);
-            H.xb[v] = r.xb;
-            H.len[v] = r.len;
+            H.xb[v] = ld_x(S.X, C.slot[v].xs);
             if (!kSS && C.slot[v].head) {
-                const Subj sr = ld_subj(subj + C.slot[v].pr.y);
+                const Subj sr = ld_hdr(S.X, C.slot[v].ds);
                 H.den[v] = sr.den;
                 H.n[v] = sr.n;
             }
@@ -143,38 +141,22 @@ __device__ __forceinline__ void issue_records(const ShardArgs& S, const Cached& 
 __device__ __forceinline__ void finish_records(const Cached& C, HeadRegs& H) {
 #pragma unroll
     for (int v = 0; v < kCached; ++v)
-        if (slot_valid(C.slot[v])) H.le[v] = lexp(H.len[v], H.xb[v]);
+        if (slot_valid(C.slot[v])) H.le[v] = lexp(C.slot[v].len, H.xb[v]);
 }
 
 template <bool kSS>
 __device__ __forceinline__ void gather_records(const ShardArgs& S, const Cached& C, HeadRegs& H) {
-    EraRec* era = S.era;
-    SubjRec* subj = S.subj;
-#pragma unroll
-    for (int v = 0; v < kCached; ++v) {
-        if (slot_valid(C.slot[v])) {
-            const Rec r = ld_rec(era + C.slot[v].pr.x);
-            H.xb[v] = r.xb;
-            H.len[v] = r.len;
-            if (!kSS && C.slot[v].head) {
-                const Subj sr = ld_subj(subj + C.slot[v].pr.y);
-                H.den[v] = sr.den;
-                H.n[v] = sr.n;
-            }
-        }
-    }
-#pragma unroll
-    for (int v = 0; v < kCached; ++v)
-        if (slot_valid(C.slot[v])) H.le[v] = lexp(H.len[v], H.xb[v]);
+    issue_records<kSS>(S, C, H);
+    finish_records(C, H);
 }
 
 template <bool kSS>
 __device__ __forceinline__ void prefetch_records(const ShardArgs& S, const RawCached& R) {
 #pragma unroll
     for (int v = 0; v < kCached; ++v) {
-        if (R.slot[v].pr.x >= 0) {
-            prefetch_l2(S.era + R.slot[v].pr.x);
-            if (!kSS) prefetch_l2(S.subj + R.slot[v].pr.y);
+        if (R.slot[v].q.x >= 0) {
+            prefetch_l2(S.X + R.slot[v].q.x);
+            if (!kSS && (R.slot[v].q.x ^ R.slot[v].q.y) >= kLineSlots) prefetch_l2(S.X + R.slot[v].q.y);
         }
     }
 }
@@ -197,19 +179,19 @@ struct TouchBits {
 
 template <bool kSS, bool kTouch>
 __device__ __forceinline__ void repair(const Cached& C, HeadRegs& H, const Smem& sm, const SubjTile& T,
-                                       int stamp_prev, const unsigned* bmprev = nullptr, int bbase = 0,
+                                       int stamp_prev, const unsigned* bmprev = nullptr,
                                        int nprev = 0) {
 #pragma unroll
     for (int v = 0; v < kCached; ++v) {
         if (!slot_valid(C.slot[v])) continue;
-        const int s = C.slot[v].pr.y;
+        const int s = C.slot[v].ls; // subject index within the CTA's range
         int val;
         if constexpr (kTouch) { // direct-mapped: the subject's entry carries the stamp of its last update
-            const int2 tc = T.touch[s - T.base];
+            const int2 tc = T.touch[s];
             if (tc.x != stamp_prev) continue;
             val = tc.y;
         } else if (bmprev) {
-            const int t = s - bbase;
+            const int t = s;
             if (!((bmprev[t >> 5] >> (t & 31)) & 1u)) continue;
             int lo = 0, hi = nprev; // first position of subject s in the previous slice
             while (lo < hi) {
@@ -233,7 +215,7 @@ __device__ __forceinline__ void repair(const Cached& C, HeadRegs& H, const Smem&
         }
         const int posj = val & 0xffff, runj = val >> 16;
         if (!kSS && C.slot[v].head) H.den[v] = sm.jden[posj];
-        const int row = C.slot[v].pr.x;
+        const int row = C.slot[v].xs; // era identity: its slot
         for (int q = posj; q < posj + runj; ++q) {
             if (sm.jrow[q] == row) {
                 H.xb[v] = sm.jxb[q];
@@ -247,9 +229,7 @@ __device__ __forceinline__ void repair(const Cached& C, HeadRegs& H, const Smem&
 template <bool kSS>
 __device__ STREAM_FN GhAcc gh_streamed(const ShardArgs& S, int64_t p0, int64_t b0, int64_t p1, GhAcc acc,
                                              Smem& sm, const SubjTile T, const StreamBuf X) {
-    const int2* __restrict__ pairs = S.pairs;
-    const EraRec* era = S.era;
-    const SubjRec* subj = S.subj;
+    const int4* __restrict__ pq = S.pq;
     double gs = acc.gs, hs = acc.hs;
     int err = acc.err;
     const int tid = static_cast<int>(threadIdx.x);
@@ -267,26 +247,26 @@ __device__ STREAM_FN GhAcc gh_streamed(const ShardArgs& S, int64_t p0, int64_t b
             sm.cr_on = 0;
         }
         for (int q0 = tid; q0 < ne; q0 += kSU * kT) {
-            int2 pr[kSU];
+            int4 pr[kSU];
 #pragma unroll
             for (int u = 0; u < kSU; ++u)
-                if (q0 + u * kT < ne) pr[u] = ld_pair(pairs + b + q0 + u * kT);
-            Rec rr[kSU];
+                if (q0 + u * kT < ne) pr[u] = ld_pq(pq + b + q0 + u * kT);
+            double xb[kSU];
 #pragma unroll
             for (int u = 0; u < kSU; ++u)
-                if (q0 + u * kT < ne) rr[u] = ld_rec(era + pr[u].x);
+                if (q0 + u * kT < ne) xb[u] = ld_x(S.X, pr[u].x);
 #pragma unroll
             for (int u = 0; u < kSU; ++u) {
                 const int q = q0 + u * kT;
                 if (q < ne) {
-                    X.x[q] = lexp(rr[u].len, rr[u].xb);
-                    X.sub[q] = pr[u].y;
+                    X.x[q] = lexp(pr[u].z, xb[u]);
+                    X.sub[q] = pr[u].w;
                 }
             }
         }
         __syncthreads();
-        const int before = b > p0 ? ld_pair(pairs + b - 1).y : -1; // subject just before the chunk
-        const int after = b + ne < p1 ? ld_pair(pairs + b + ne).y : -1; // ... and just past it
+        const int before = b > p0 ? ld_pq_sub(pq + b - 1) : -1; // subject just before the chunk
+        const int after = b + ne < p1 ? ld_pq_sub(pq + b + ne) : -1; // ... and just past it
         for (int q = tid; q < ne; q += kT) {
             const int s = X.sub[q];
             if ((q > 0 ? X.sub[q - 1] : before) == s) continue; // not a run head
@@ -296,10 +276,10 @@ __device__ STREAM_FN GhAcc gh_streamed(const ShardArgs& S, int64_t p0, int64_t b
             double den;
             int n;
             if constexpr (kSS) {
-                den = T.den[s - T.base];
-                n = T.n[s - T.base];
+                den = T.den[s];
+                n = T.n[s];
             } else {
-                const Subj sr = ld_subj(subj + s);
+                const Subj sr = ld_hdr(S.X, ld_pq(pq + b + q).y);
                 den = sr.den;
                 n = sr.n;
             }
@@ -337,67 +317,68 @@ __device__ STREAM_FN GhAcc gh_streamed(const ShardArgs& S, int64_t p0, int64_t b
 template <bool kSS>
 __device__ STREAM_FN UpdErr update_streamed(const ShardArgs& S, int64_t p0, int64_t b0, int64_t p1, double d,
                                                   UpdErr ue, Smem& sm, const SubjTile T, const StreamBuf X) {
-    const int2* __restrict__ pairs = S.pairs;
-    EraRec* era = S.era;
-    SubjRec* subj = S.subj;
+    const int4* __restrict__ pq = S.pq;
     int err = ue.err;
     double errv = ue.errv;
     const int tid = static_cast<int>(threadIdx.x);
     for (int64_t b = b0; b < p1; b += X.cap) {
         const int ne = static_cast<int>(min(p1 - b, static_cast<int64_t>(X.cap)));
         __syncthreads();
-        int cr_on = 0, cr_subj = -1;
+        int cr_on = 0, cr_subj = -1, cr_ds = 0;
         double cr_den = 0.0;
         if (tid == 0) {
             cr_on = sm.cr_on;
             cr_subj = sm.cr_subj;
             cr_den = sm.cr_den;
+            cr_ds = sm.cr_ds;
             sm.cr_on = 0;
         }
         for (int q0 = tid; q0 < ne; q0 += kSU * kT) {
-            int2 pr[kSU];
+            int4 pr[kSU];
 #pragma unroll
             for (int u = 0; u < kSU; ++u)
-                if (q0 + u * kT < ne) pr[u] = ld_pair(pairs + b + q0 + u * kT);
-            Rec rr[kSU];
+                if (q0 + u * kT < ne) pr[u] = ld_pq(pq + b + q0 + u * kT);
+            double xb[kSU];
 #pragma unroll
             for (int u = 0; u < kSU; ++u)
-                if (q0 + u * kT < ne) rr[u] = ld_rec(era + pr[u].x);
+                if (q0 + u * kT < ne) xb[u] = ld_x(S.X, pr[u].x);
 #pragma unroll
             for (int u = 0; u < kSU; ++u) {
                 const int q = q0 + u * kT;
                 if (q < ne) {
-                    const double updated = __dadd_rn(rr[u].xb, d);
+                    const double updated = __dadd_rn(xb[u], d);
                     double diff = 0.0;
                     if (!(fabs(updated) <= kXbBound)) {
                         err = DERR_OVERFLOW;
                         errv = fabs(updated);
                     } else {
-                        diff = __dsub_rn(lexp(rr[u].len, updated), lexp(rr[u].len, rr[u].xb));
-                        era[pr[u].x].xb = updated;
+                        diff = __dsub_rn(lexp(pr[u].z, updated), lexp(pr[u].z, xb[u]));
+                        S.X[pr[u].x] = updated;
                     }
                     X.x[q] = diff;
-                    X.sub[q] = pr[u].y;
+                    X.sub[q] = pr[u].w;
                 }
             }
         }
         __syncthreads();
-        const int before = b > p0 ? ld_pair(pairs + b - 1).y : -1;
-        const int after = b + ne < p1 ? ld_pair(pairs + b + ne).y : -1;
+        const int before = b > p0 ? ld_pq_sub(pq + b - 1) : -1;
+        const int after = b + ne < p1 ? ld_pq_sub(pq + b + ne) : -1;
         for (int q = tid; q < ne; q += kT) {
             const int s = X.sub[q];
             if ((q > 0 ? X.sub[q - 1] : before) == s) continue;
-            double den = kSS ? T.den[s - T.base] : subj[s].den;
+            const int ds = kSS ? 0 : ld_pq(pq + b + q).y;
+            double den = kSS ? T.den[s] : S.X[ds];
             int e = q;
             while (e < ne && X.sub[e] == s) den = __dadd_rn(den, X.x[e++]);
             if (e == ne && after == s) {
                 sm.cr_den = den;
                 sm.cr_subj = s;
+                sm.cr_ds = ds;
                 sm.cr_on = 1;
             } else if constexpr (kSS) {
-                T.den[s - T.base] = den;
+                T.den[s] = den;
             } else {
-                subj[s].den = den;
+                S.X[ds] = den;
             }
         }
         if (cr_on) {
@@ -407,11 +388,12 @@ __device__ STREAM_FN UpdErr update_streamed(const ShardArgs& S, int64_t p0, int6
             if (e == ne && after == cr_subj) {
                 sm.cr_den = den;
                 sm.cr_subj = cr_subj;
+                sm.cr_ds = cr_ds;
                 sm.cr_on = 1;
             } else if constexpr (kSS) {
-                T.den[cr_subj - T.base] = den;
+                T.den[cr_subj] = den;
             } else {
-                subj[cr_subj].den = den;
+                S.X[cr_ds] = den;
             }
         }
     }
@@ -422,7 +404,7 @@ template <bool kSS, bool kST>
 __device__ __forceinline__ void gh_compute(const ShardArgs& S, const Cached& C, int64_t p0, int64_t p1,
                                            const HeadRegs& H, double& gs, double& hs, int& err, Smem& sm,
                                            const SubjTile& T, const StreamBuf X) {
-    const int2* __restrict__ pairs = S.pairs;
+    const int4* __restrict__ pq = S.pq;
     const int ncached = static_cast<int>(min(p1 - p0, static_cast<int64_t>(kCap)));
     if (threadIdx.x == 0) sm.cr_on = 0;
 #pragma unroll
@@ -430,7 +412,7 @@ __device__ __forceinline__ void gh_compute(const ShardArgs& S, const Cached& C, 
         if (slot_valid(C.slot[v])) {
             const int pos = slot_pos(v);
             sm.stage[pos] = H.le[v];
-            sm.ssub[pos] = C.slot[v].pr.y;
+            sm.ssub[pos] = C.slot[v].ls;
         }
     }
     __syncthreads();
@@ -438,12 +420,12 @@ __device__ __forceinline__ void gh_compute(const ShardArgs& S, const Cached& C, 
     for (int v = 0; v < kCached; ++v) {
         if (C.slot[v].head) {
             double num = H.le[v];
-            const int s = C.slot[v].pr.y;
+            const int s = C.slot[v].ls;
             double den;
             int n;
             if constexpr (kSS) {
-                den = T.den[s - T.base];
-                n = T.n[s - T.base];
+                den = T.den[s];
+                n = T.n[s];
             } else {
                 den = H.den[v];
                 n = H.n[v];
@@ -452,7 +434,7 @@ __device__ __forceinline__ void gh_compute(const ShardArgs& S, const Cached& C, 
                 int q = slot_pos(v) + 1;
                 while (q < ncached && sm.ssub[q] == s) num = __dadd_rn(num, sm.stage[q++]);
                 if constexpr (kST) {
-                    if (q == ncached && p0 + q < p1 && ld_pair(pairs + p0 + q).y == s) {
+                    if (q == ncached && p0 + q < p1 && ld_pq_sub(pq + p0 + q) == s) {
                         // the run continues into the streamed part: carried there
                         sm.cr_num = num;
                         sm.cr_den = den;
@@ -480,11 +462,8 @@ template <bool kSS, bool kST>
 __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C, const HeadRegs& H, bool cached,
                                              int64_t p0, int64_t p1, double d, int& err, double& errv, Smem& sm,
                                              const SubjTile& T, const StreamBuf X, bool record = false,
-                                             int* myht = nullptr, int stamp = 0, unsigned* bmcur = nullptr,
-                                             int bbase = 0) {
-    const int2* __restrict__ pairs = S.pairs;
-    EraRec* era = S.era;
-    SubjRec* subj = S.subj;
+                                             int* myht = nullptr, int stamp = 0, unsigned* bmcur = nullptr) {
+    const int4* __restrict__ pq = S.pq;
     if (threadIdx.x == 0) sm.cr_on = 0;
     if (cached) {
         const int ncached = static_cast<int>(min(p1 - p0, static_cast<int64_t>(kCap)));
@@ -500,17 +479,17 @@ __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C
                     err = DERR_OVERFLOW;
                     errv = fabs(updated);
                 } else {
-                    const double fresh = lexp(H.len[v], updated);
+                    const double fresh = lexp(C.slot[v].len, updated);
                     diff = __dsub_rn(fresh, H.le[v]);
-                    era[C.slot[v].pr.x].xb = updated;
+                    S.X[C.slot[v].xs] = updated;
                     if (record) {
                         sm.jxb[pos] = updated;
                         sm.jle[pos] = fresh;
                     }
                 }
                 if (record) {
-                    sm.jrow[pos] = C.slot[v].pr.x;
-                    if constexpr (!kSS) sm.jsub[pos] = C.slot[v].pr.y;
+                    sm.jrow[pos] = C.slot[v].xs;
+                    if constexpr (!kSS) sm.jsub[pos] = C.slot[v].ls;
                 }
                 sm.stage[pos] = diff;
             }
@@ -521,32 +500,31 @@ __device__ __forceinline__ void update_slice(const ShardArgs& S, const Cached& C
         for (int v = 0; v < kCached; ++v) {
             if (C.slot[v].head) {
                 const int pos = slot_pos(v);
+                const int s = C.slot[v].ls;
                 int q = pos;
-                double den = __dadd_rn(kSS ? T.den[C.slot[v].pr.y - T.base] : H.den[v], sm.stage[q++]);
+                double den = __dadd_rn(kSS ? T.den[s] : H.den[v], sm.stage[q++]);
                 if (C.slot[v].cont) {
-                    const int s = C.slot[v].pr.y;
                     while (q < ncached && sm.ssub[q] == s) den = __dadd_rn(den, sm.stage[q++]);
                     if constexpr (kST) {
-                        if (q == ncached && p0 + q < p1 && ld_pair(pairs + p0 + q).y == s) {
+                        if (q == ncached && p0 + q < p1 && ld_pq_sub(pq + p0 + q) == s) {
                             // continues into the streamed part: carried there
                             sm.cr_den = den;
                             sm.cr_subj = s;
+                            sm.cr_ds = C.slot[v].ds;
                             sm.cr_on = 1;
                             continue;
                         }
                     }
                 }
-                if constexpr (kSS) T.den[C.slot[v].pr.y - T.base] = den;
-                else subj[C.slot[v].pr.y].den = den;
+                if constexpr (kSS) T.den[s] = den;
+                else S.X[C.slot[v].ds] = den;
                 if (record) { // publish (subject -> run) for the next coordinate's repair
-                    const int s = C.slot[v].pr.y;
                     if constexpr (kSS && !kST) {
-                        T.touch[s - T.base] = make_int2(stamp, pos | ((q - pos) << 16));
+                        T.touch[s] = make_int2(stamp, pos | ((q - pos) << 16));
                     } else {
                         if constexpr (!kSS) sm.jden[pos] = den;
                         if (!kSS && bmcur) {
-                            const int t = s - bbase;
-                            atomicOr(&bmcur[t >> 5], 1u << (t & 31));
+                            atomicOr(&bmcur[s >> 5], 1u << (s & 31));
                         } else {
                             int h = ht_hash(s);
                             while (atomicCAS(&sm.htk[h], -1, s) != -1) h = (h + 1) & (kHt - 1);
@@ -649,7 +627,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             int te;
             unsigned inexact[2];
             poll(A, S.xslots, seq, pv, tg, th, te, nullptr, inexact);
-            if (!te && (inexact[0] | inexact[1])) refine_sums(A, S.xslots, seq, pv, gs, hs, err, tg, th, te, inexact[0], inexact[1]);
+            BSCCS_REFINE(A, S.xslots, seq, pv, gs, hs, err, tg, th, te, inexact);
             if (c == 0 && threadIdx.x == 0) {
                 S.res->g = __dsub_rn(A.y_dot_x[j], tg);
                 S.res->h = th == 0.0 ? 0.0 : -th;
@@ -671,8 +649,13 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
     // Scalar work (exchange, penalized step, clamp) runs on warp 0 only and
     // is broadcast through shared memory at the one barrier that follows.
     long long nvisit = 0, nmoved = 0;
-    const int V = A.nvisit;
-    const longlong2* vs = S.vsplit + static_cast<size_t>(c) * static_cast<size_t>(V);
+    // this launch runs the visit list from A.visit_begin (a restart after a
+    // coordinate whose sums needed refinement, run_sweep) to its end
+    const int B0 = A.visit_begin;
+    const int V = A.nvisit - B0;
+    const longlong2* vs = S.vsplit + static_cast<size_t>(c) * static_cast<size_t>(A.nvisit) + B0;
+    const int32_t* visit = A.visit + B0;
+    int refine_at = -1;
     bool aborted = false;
     const bool w0 = threadIdx.x < 32;
     if (V > 0) {
@@ -692,7 +675,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             T.touch = kST ? nullptr : reinterpret_cast<int2*>(T.den + A.ss_cap);
             T.n = kST ? reinterpret_cast<int*>(T.den + A.ss_cap) : reinterpret_cast<int*>(T.touch + A.ss_cap);
             for (int t = threadIdx.x; t < ns; t += kT) {
-                const Subj sr = ld_subj(S.subj + T.base + t);
+                const Subj sr = ld_hdr(S.X, S.bstart[T.base + t]);
                 T.den[t] = sr.den;
                 T.n[t] = sr.n;
                 if constexpr (!kST) T.touch[t] = make_int2(0, 0);
@@ -700,7 +683,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         }
         const longlong2 z2 = make_longlong2(0, 0);
         longlong2 cur = vs[0];
-        int j = A.visit[0];
+        int j = visit[0];
         double bj = 0.0, rj = 1.0, ydx = 0.0;
         if (w0) {
             bj = S.beta[j];
@@ -709,7 +692,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         }
         load_cached(S, cur.x, cur.y, C);
         longlong2 nxt = V > 1 ? vs[1] : z2;
-        int jn = V > 1 ? A.visit[1] : 0;
+        int jn = V > 1 ? visit[1] : 0;
         Cached N;
         load_cached(S, nxt.x, nxt.y, N);
         longlong2 nxt2 = V > 2 ? vs[2] : z2;
@@ -735,7 +718,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                     if (spec) {
                         if (A.dbg & 64) finish_records(C, H);
                         repair<kSS, kSS && !kST>(C, H, sm, T, idx, // stamps: coordinate idx-1 wrote idx
-                                                 TB.b0 ? TB.of((idx + 1) & 1) : nullptr, TB.base, nprev);
+                                                 TB.b0 ? TB.of((idx + 1) & 1) : nullptr, nprev);
                     } else {
                         gather_records<kSS>(S, C, H);
                     }
@@ -785,7 +768,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                     rn = S.trust[jn];
                     yn = A.y_dot_x[jn];
                 }
-                jn2 = idx + 2 < V ? A.visit[idx + 2] : 0;
+                jn2 = idx + 2 < V ? visit[idx + 2] : 0;
                 if (tr && idx < A.ntrace) trb[idx * trs + 4] = gtimer();
                 // exchange, then the scalar step (prior.hpp:72-122,
                 // solver.hpp:131-150), broadcast with the next barrier
@@ -800,12 +783,17 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                     poll<!kSS>(A, S.xslots, seq, pv, tg, th, te, (tr && idx < A.ntrace) ? trb + idx * trs + 5 : nullptr,
                                inexact);
                 }
-                if (!te && (inexact[0] | inexact[1]))
-                    refine_sums(A, S.xslots, seq, pv, gs, hs, e, tg, th, te, inexact[0], inexact[1]);
                 int status = ST_OK;
                 double delta = 0.0;
                 if (te) {
                     status = ST_REMOTE_ERR;
+                } else if ((inexact[0] | inexact[1]) &&
+                           (needs_refine(tg, inexact[0], 0) || needs_refine(th, inexact[1], 0))) {
+                    // a sum below the exchange's resolution (degenerate fits only):
+                    // stop here; the host refines this coordinate and restarts the
+                    // sweep after it (run_sweep), keeping the refinement rounds out
+                    // of this loop's code
+                    status = ST_REFINE;
                 } else {
                     const double g = __dsub_rn(ydx, tg);
                     const double h = th == 0.0 ? 0.0 : -th;
@@ -826,7 +814,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                     sm.delta = delta;
                     sm.status = status;
                     if (c == 0 && status == ST_OK) {
-                        S.moved[idx] = delta != 0.0 ? 1 : 0;
+                        S.moved[B0 + idx] = delta != 0.0 ? 1 : 0;
                         S.beta[j] = __dadd_rn(bj, delta);
                         S.trust[j] = next_trust(delta, rj);
                     }
@@ -848,6 +836,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
             if (status != ST_OK) {
                 aborted = true;
                 if (status == ST_REMOTE_ERR && c == 0 && threadIdx.x == 0) S.res->err_remote = 1;
+                if (status == ST_REFINE) refine_at = B0 + idx;
                 break;
             }
             ++nvisit;
@@ -855,7 +844,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                 ++nmoved;
                 if (!(A.dbg & 2))
                     update_slice<kSS, kST>(S, C, H, true, p0, p1, delta, err, errv, sm, T, X, spec_next, myht,
-                                           idx + 1, TB.b0 ? TB.of(idx & 1) : nullptr, TB.base);
+                                           idx + 1, TB.b0 ? TB.of(idx & 1) : nullptr);
             }
             __syncthreads(); // slice writes of this coordinate before the next reads
             if (tr && idx < A.ntrace) trb[idx * trs + 3] = gtimer();
@@ -875,7 +864,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         }
         if constexpr (kSS) { // the cycle's denominators back to HBM (ordered by the loop's last barrier)
             const int ns = S.cta_subj[c + 1] - T.base;
-            for (int t = threadIdx.x; t < ns; t += kT) S.subj[T.base + t].den = T.den[t];
+            for (int t = threadIdx.x; t < ns; t += kT) S.X[S.bstart[T.base + t]] = T.den[t];
         }
     }
 
@@ -885,7 +874,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         const int e0 = S.cta_era[c], e1 = S.cta_era[c + 1];
         double ch = 0.0, mg = 0.0;
         for (int k = e0 + static_cast<int>(threadIdx.x); k < e1; k += kT) {
-            const double xb = S.era[k].xb;
+            const double xb = S.X[S.row_slot[k]];
             ch = __dadd_rn(ch, fabs(__dsub_rn(xb, S.snap[k])));
             if (A.normalized) mg = __dadd_rn(mg, fabs(xb));
             S.snap[k] = xb;
@@ -914,6 +903,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         S.res->visited = nvisit;
         S.res->moved = nmoved;
         S.res->counter = seq;
+        S.res->refine_at = refine_at;
         if (S.xowner) *S.xcounter = seq;
     }
     if (c == 0 && S.xowner) xprev_store(S.xslots, pv);
