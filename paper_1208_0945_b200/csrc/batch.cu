@@ -1226,6 +1226,7 @@ void batch_set_folds(Batch* b, const int32_t* fold_of_host, const int32_t* fold_
 // held: also evaluate the held-out weights' log likelihood (predictive LL).
 void batch_fit(Batch* b, int R, const PriorParams* priors, const double* const* init, const bsccs_solver_config* cfg,
                double* beta_out, bsccs_fit_result* res, int* err_code, double* pred_ll) {
+    NvtxRange nvtx_("fit_batch");
     const bsccs_dataset* ds = b->ds;
     const int RB = b->RB;
     if (R < 1 || R > RB) internal_error("batch: fit count out of range");

@@ -253,6 +253,7 @@ void drop_workspaces(const bsccs_dataset* ds) {
 // fit (solver.hpp:206-220) on a resident dataset, validated arguments.
 void fit_resident(const bsccs_dataset* ds, const PriorParams& p, const bsccs_solver_config* cfg,
                   const double* init_beta, double* beta_out, bsccs_fit_result* result) {
+    NvtxRange nvtx_("bsccs_fit");
     if (ds->N == 0) input_error("fit: dataset has no subjects");
     set_device(ds->device);
     std::memset(result, 0, sizeof *result);
@@ -713,6 +714,7 @@ bsccs_status bsccs_group_destroy(bsccs_group* g) {
 bsccs_status bsccs_group_fit(bsccs_group* g, const bsccs_prior* prior, const bsccs_solver_config* cfg,
                              const double* init_beta, double* beta_out, bsccs_fit_result* result) {
     return guard([&] {
+        NvtxRange nvtx_("bsccs_group_fit");
         if (!g || !beta_out || !result) input_error("group fit: null argument");
         validate_config(cfg);
         const PriorParams p = to_params(prior);

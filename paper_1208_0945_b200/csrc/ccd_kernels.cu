@@ -1392,6 +1392,7 @@ bsccs_dataset* dataset_create(int32_t N, int32_t K, int32_t J, int64_t nnz, cons
                               const int32_t* event_counts, const int64_t* col_ptr, const int32_t* rows,
                               const int32_t* subjects, const int64_t* y_dot_x_global,
                               const int64_t* col_nnz_global, int device, int ctas_override) {
+    NvtxRange nvtx_("bsccs_dataset_create");
     if (N < 1) input_error("dataset: no subjects");
     if (K < 1 || J < 1 || nnz < 0) input_error("dataset: invalid sizes");
     if (!subject_offsets || !events_per_subject || !era_lengths || !event_counts || !col_ptr)
@@ -1600,6 +1601,7 @@ void state_destroy(bsccs_state* st) {
 }
 
 void dense_recompute(bsccs_state* st, const double* beta_host) {
+    NvtxRange nvtx_("dense_recompute");
     const bsccs_dataset* ds = st->ds;
     if (beta_host)
         for (int32_t j = 0; j < ds->J; ++j)
@@ -1845,6 +1847,7 @@ void sparse_update(bsccs_state* st, int32_t j, double delta) {
 }
 
 double log_likelihood(bsccs_state* st) {
+    NvtxRange nvtx_("log_likelihood");
     const bsccs_dataset* ds = st->ds;
     DeviceGuard dg(ds->device);
     k_ll_partial<<<kLLBlocks, kLLThreads, 0, st->stream>>>(st->X, ds->row_slot, ds->event_counts, ds->bstart, ds->K,
@@ -2055,6 +2058,7 @@ bool refine_coordinate(const ExchangePlan& plan, const PriorParams& prior, int32
 } // namespace
 
 SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool normalized, bool dense) {
+    NvtxRange nvtx_("ccd_cycle");
     bsccs_state* s0 = plan.shards[0];
     if (dense && (plan.shards.size() != 1 || plan.dst.size() != 1))
         input_error("solver: the dense update path runs on an unsharded dataset");

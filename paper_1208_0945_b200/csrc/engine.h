@@ -25,6 +25,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h> // header-only NVTX v3: ranges cost nothing unless a tool attaches
 
 #include <cstdint>
 #include <string>
@@ -145,6 +146,14 @@ struct bsccs_state {
 };
 
 namespace bsccs_b200 {
+
+// NVTX range over a host-side phase (visible in nsys / ncu --nvtx timelines)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 void cuda_check(cudaError_t e, const char* what);
 void count_launches(int n);

@@ -143,6 +143,7 @@ void parse_chunk(Chunk& ch, const std::unordered_map<std::string_view, int32_t>*
 
 bsccs_dataset* load_long_format(const char* path, const char* const* dictionary, int32_t dict_size, int device,
                                 int ctas_override, int threads) {
+    NvtxRange nvtx_("read_long_format");
     if (!path) input_error("read_long_format: null path");
     const std::string spath(path);
     // ---- the file -------------------------------------------------------

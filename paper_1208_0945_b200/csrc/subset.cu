@@ -112,6 +112,7 @@ __global__ void k_export_pairs(const int2* __restrict__ pairs, int64_t nnz, int3
 
 bsccs_dataset* dataset_subset(const bsccs_dataset* parent, const int32_t* subject_indices, int64_t n,
                               int ctas_override) {
+    NvtxRange nvtx_("subset_dataset");
     if (!parent) input_error("subset_dataset: null dataset");
     if (n <= 0 || !subject_indices) input_error("subset_dataset: empty subject selection");
     if (n > 0x7fffffffll) input_error("subset_dataset: selection too large for int32 subject indices");

@@ -2,6 +2,8 @@
 golden reference fits.  Parity bar (BASELINE.json north_star): beta within
 1e-6 relative (1e-9 absolute for Laplace zeros), log-posterior within 1e-8
 relative, identical cycle count."""
+import hashlib
+
 import numpy as np
 import pytest
 
@@ -211,6 +213,11 @@ def test_full_size_golden(name, fname, zipf):
     assert bool(g.get("zipf", False)) == zipf
     ds = datagen.config_dataset(name, zipf)
     assert (ds.num_subjects, ds.num_eras, ds.nnz) == (g["sizes"]["N"], g["sizes"]["K"], g["sizes"]["nnz"])
+    # the very dataset the reference fitted (sha256 of the flat CSC arrays)
+    h = hashlib.sha256()
+    for a in ds.arrays():
+        h.update(np.ascontiguousarray(a).tobytes())
+    assert h.hexdigest() == g["digest"]
     res = B.fit(ds, prior_from(g["prior"]))
     assert_parity(res, fa(g["beta"]), float(g["log_posterior"]), g["cycles_run"])
     # repeat: bit-identical (fixed partition => fixed bits)
