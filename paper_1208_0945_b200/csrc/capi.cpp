@@ -9,6 +9,7 @@
 // 8-byte criterion.  Shuffled visit orders come from the reference RNG
 // stream (SolverState::order_rng, solver.hpp:81,109-114).
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <functional>
@@ -71,6 +72,13 @@ double log_density(const PriorParams& p, const double* beta, int32_t n) {
 namespace {
 
 void set_device(int dev) { CUDA_TRY(cudaSetDevice(dev)); }
+
+// Exchange of a multi-rank (or virtual-rank) group: hierarchical unless
+// BSCCS_XCHG=flat (every CTA adding into every rank's area, as round 1).
+bool group_hier_from_env() {
+    const char* e = std::getenv("BSCCS_XCHG");
+    return !(e && std::strcmp(e, "flat") == 0);
+}
 
 // Shards bound for one fit, plus their exchange plan.
 struct FitContext {
@@ -302,6 +310,10 @@ struct bsccs_group {
     std::vector<unsigned long long*> peer; // per rank (own = slots)
     // virtual ranks (one launch, one exchange area per shard)
     std::vector<unsigned long long*> vslots, vcounters;
+    // hierarchical exchange (ccd_kernels.cu forward_local): each area is two
+    // halves, [0, kXchgAreaWords) polled by the rank (one arrival per rank),
+    // [kXchgAreaWords, 2 kXchgAreaWords) taking the rank's own CTAs' adds
+    bool hier = false;
     int device = 0;
     int total = 0;
     int base = 0;
@@ -588,7 +600,8 @@ bsccs_status bsccs_fit(const bsccs_dataset* ds, const bsccs_prior* prior, const 
 
 int64_t bsccs_group_slot_bytes(int32_t total_ctas) {
     (void)total_ctas; // the fixed-point exchange area does not grow with P
-    return static_cast<int64_t>(kXchgAreaWords) * static_cast<int64_t>(sizeof(unsigned long long));
+    // polled half + local half (hierarchical exchange)
+    return 2 * static_cast<int64_t>(kXchgAreaWords) * static_cast<int64_t>(sizeof(unsigned long long));
 }
 
 bsccs_status bsccs_group_create_local(bsccs_dataset* const* shards, int32_t n, bsccs_group** out) {
@@ -635,6 +648,7 @@ bsccs_status bsccs_group_create_virtual(bsccs_dataset* const* shards, int32_t n,
         g->peer = g->vslots;
         g->slots = g->vslots[0];
         g->counter = g->vcounters[0];
+        g->hier = n > 1 && group_hier_from_env();
         *out = g.release();
     });
 }
@@ -662,6 +676,7 @@ bsccs_status bsccs_group_create_rank(bsccs_dataset* shard, int32_t rank, int32_t
         CUDA_TRY(cudaMemset(g->counter, 0, sizeof(unsigned long long)));
         g->peer.assign(static_cast<size_t>(world), nullptr);
         g->peer[static_cast<size_t>(rank)] = g->slots;
+        g->hier = world > 1 && group_hier_from_env();
         *out = g.release();
     });
 }
@@ -742,6 +757,12 @@ bsccs_status bsccs_group_fit(bsccs_group* g, const bsccs_prior* prior, const bsc
             fc.plan.participant_base = g->base;
             fc.plan.shard_slots = g->vslots;
             fc.plan.shard_counters = g->vcounters;
+            fc.plan.hier = g->hier;
+            if (g->hier) {
+                if (g->vslots.empty()) fc.plan.shard_local = {g->slots + kXchgAreaWords};
+                else
+                    for (auto* a : g->vslots) fc.plan.shard_local.push_back(a + kXchgAreaWords);
+            }
             // per-rank log-likelihood partials summed exactly in the exchange
             // area (positive and negative parts: the words carry values >= 0)
             auto allreduce = [&](double x) {

@@ -77,6 +77,8 @@ constexpr int kHt = 1 << kHtBits;
 
 struct ShardArgs {
     const unsigned long long* xslots; // exchange area this shard polls (its rank's)
+    unsigned long long* lslots;       // hierarchical exchange: its rank's local area (else null)
+    int p_local;                      // hierarchical exchange: participants of the local area
     unsigned long long* xcounter;     // exchange sequence word of that area
     int xowner;                       // this shard's CTA 0 stores the area's baseline / counter
     const int4* pq;                   // {era slot, block slot, era length, subject - cta_subj[c]} per pair
@@ -121,7 +123,8 @@ struct SweepArgs {
     unsigned long long* dst[kMaxRanks];
     int ndst;
     const unsigned long long* slots;
-    int P;
+    int P;      // arrivals per polled word: every participant (flat) or every rank (hier)
+    int hier;   // hierarchical exchange (multi-rank groups): see forward_local
     unsigned long long* counter;
     double red_a, red_b; // kModeReduce inputs (this rank's values)
     int prefetch; // L2 prefetch of the records two coordinates ahead (small slices only)
@@ -187,9 +190,83 @@ __device__ __forceinline__ int lane_id() { return static_cast<int>(threadIdx.x) 
 constexpr int kXStride = 32; // u64 words between exchange words (256 B)
 constexpr int kXWords = 7;
 constexpr int kXBase = 2 * kXWords * kXStride; // running totals at launch end
+// Running totals of the two buffers (lanes 0..6 of warp 0): of the polled
+// area (b0, b1) and, for the forwarding CTA of a hierarchical exchange, of
+// its rank's local area (l0, l1).
+struct XPrev {
+    unsigned long long b0, b1, l0, l1;
+};
+
+__device__ __forceinline__ void xprev_load(const ShardArgs& S, XPrev& pv) {
+    const int l = lane_id();
+    if (threadIdx.x < 32 && l < kXWords) {
+        pv.b0 = S.xslots[kXBase + l];
+        pv.b1 = S.xslots[kXBase + kXWords + l];
+        pv.l0 = S.lslots ? S.lslots[kXBase + l] : 0ull;
+        pv.l1 = S.lslots ? S.lslots[kXBase + kXWords + l] : 0ull;
+    }
+}
+
+__device__ __forceinline__ void xprev_store(const ShardArgs& S, const XPrev& pv) {
+    const int l = lane_id();
+    if (threadIdx.x < 32 && l < kXWords) {
+        const_cast<unsigned long long*>(S.xslots)[kXBase + l] = pv.b0;
+        const_cast<unsigned long long*>(S.xslots)[kXBase + kXWords + l] = pv.b1;
+        if (S.lslots) {
+            S.lslots[kXBase + l] = pv.l0;
+            S.lslots[kXBase + kXWords + l] = pv.l1;
+        }
+    }
+}
+
+// Hierarchical exchange (multi-rank groups): a rank's CTAs add into its LOCAL
+// area; its CTA 0 waits for all of them and adds the local integer sums,
+// unconverted, into every rank's polled area as ONE arrival -- so a polled
+// word takes `world` remote arrivals per exchange instead of world x CTAs,
+// and integer addition keeps the totals bit-identical to the flat exchange.
+// A local wait that times out forwards an error so that no peer hangs.
+struct LPrev {
+    unsigned long long l0, l1;
+};
+__device__ __noinline__ LPrev forward_local(const SweepArgs& A, const unsigned long long* lslots, int p_local,
+                                            unsigned long long seq, LPrev pv) {
+    const int l = lane_id();
+    const unsigned buf = static_cast<unsigned>(seq & 1ull);
+    const size_t off = static_cast<size_t>(buf) * kXWords * kXStride + static_cast<size_t>(l) * kXStride;
+    unsigned long long diff = 0;
+    bool timed_out = false;
+    if (l < kXWords) {
+        const unsigned long long prev = buf ? pv.l1 : pv.l0;
+        unsigned long long v, t_first = 0;
+        unsigned spins = 0;
+        do {
+            v = ld_poll(lslots + off);
+            diff = v - prev;
+            if ((++spins & 4095u) == 0u) {
+                const unsigned long long now = gtimer();
+                if (t_first == 0) t_first = now;
+                else if (now - t_first > A.poll_timeout_ns) {
+                    timed_out = true;
+                    break;
+                }
+            }
+        } while ((diff >> kXCntShift) < static_cast<unsigned long long>(p_local));
+        if (buf) pv.l1 = v;
+        else pv.l0 = v;
+    }
+    const bool to = __any_sync(0x7fu, timed_out);
+    if (l < kXWords) {
+        unsigned long long w = to ? (l == 6 ? 1ull : 0ull) : (diff & kXData);
+        w += kXCnt;
+        for (int d = 0; d < A.ndst; ++d) red_add_sys(A.dst[d] + off, w);
+    }
+    return pv;
+}
+
 // lanes 0..6 of warp 0 (all holding the same (a, b, e)) each add one word;
 // the error word also counts the partials that lost bits below 2^-80
-__device__ __forceinline__ void publish(const SweepArgs& A, unsigned long long seq, double a, double b, int e) {
+__device__ __forceinline__ void publish(const SweepArgs& A, const ShardArgs& S, int c, unsigned long long seq,
+                                        double a, double b, int e, XPrev& pv) {
     const int l = lane_id();
     if (threadIdx.x >= 32 || l >= kXWords) return;
     unsigned long long w;
@@ -204,31 +281,17 @@ __device__ __forceinline__ void publish(const SweepArgs& A, unsigned long long s
             ((lost & 8u) ? 1ull << kXInexB : 0ull);
     w += kXCnt;
     const size_t off = static_cast<size_t>(seq & 1ull) * kXWords * kXStride + static_cast<size_t>(l) * kXStride;
-    if (A.ndst == 1) {
+    if (A.hier) {
+        red_add(S.lslots + off, w);
+        if (c == 0) { // out of line, by value: single fits never take this path
+            const LPrev lp = forward_local(A, S.lslots, S.p_local, seq, LPrev{pv.l0, pv.l1});
+            pv.l0 = lp.l0;
+            pv.l1 = lp.l1;
+        }
+    } else if (A.ndst == 1) {
         red_add(A.dst[0] + off, w);
     } else {
         for (int d = 0; d < A.ndst; ++d) red_add_sys(A.dst[d] + off, w);
-    }
-}
-
-// Running totals of the two buffers (lanes 0..6 of warp 0).
-struct XPrev {
-    unsigned long long b0, b1;
-};
-
-__device__ __forceinline__ void xprev_load(const unsigned long long* slots, XPrev& pv) {
-    const int l = lane_id();
-    if (threadIdx.x < 32 && l < kXWords) {
-        pv.b0 = slots[kXBase + l];
-        pv.b1 = slots[kXBase + kXWords + l];
-    }
-}
-
-__device__ __forceinline__ void xprev_store(const unsigned long long* slots, const XPrev& pv) {
-    const int l = lane_id();
-    if (threadIdx.x < 32 && l < kXWords) {
-        const_cast<unsigned long long*>(slots)[kXBase + l] = pv.b0;
-        const_cast<unsigned long long*>(slots)[kXBase + kXWords + l] = pv.b1;
     }
 }
 
@@ -337,9 +400,10 @@ struct Refined {
     unsigned long long next_seq;
     XPrev prev;
 };
-__device__ __forceinline__ Refined refine_sums(const SweepArgs& A, const unsigned long long* slots, unsigned long long seq,
-                                            XPrev pv, double a, double b, int e, double ta, double tb, unsigned ia,
-                                            unsigned ib) {
+__device__ __forceinline__ Refined refine_sums(const SweepArgs& A, const ShardArgs& S, int c,
+                                              const unsigned long long* slots, unsigned long long seq, XPrev pv,
+                                              double a, double b, int e, double ta, double tb, unsigned ia,
+                                              unsigned ib) {
     int sa = 0, sb = 0;
     double va = ta, vb = tb;
     for (;;) {
@@ -348,7 +412,7 @@ __device__ __forceinline__ Refined refine_sums(const SweepArgs& A, const unsigne
         if (na) sa = next_scale(va, ia, sa);
         if (nb) sb = next_scale(vb, ib, sb);
         ++seq;
-        publish(A, seq, ldexp(a, sa), ldexp(b, sb), e);
+        publish(A, S, c, seq, ldexp(a, sa), ldexp(b, sb), e, pv);
         const PollOut o = poll_body(A, slots, seq, pv, nullptr);
         pv = o.pv;
         if (o.te) return Refined{va, vb, 1, seq, pv};
@@ -364,7 +428,7 @@ __device__ __forceinline__ Refined refine_sums(const SweepArgs& A, const unsigne
 #define BSCCS_REFINE(A, slots, seq, pv, a, b, e, ta, tb, te, inexact)                                \
     do {                                                                                              \
         if (!(te) && ((inexact)[0] | (inexact)[1])) {                                                 \
-            const Refined r_ = refine_sums(A, slots, seq, pv, a, b, e, ta, tb, (inexact)[0], (inexact)[1]); \
+            const Refined r_ = refine_sums(A, S, c, slots, seq, pv, a, b, e, ta, tb, (inexact)[0], (inexact)[1]); \
             ta = r_.sum_a;                                                                            \
             tb = r_.sum_b;                                                                            \
             te = r_.err;                                                                              \
@@ -605,7 +669,7 @@ __global__ void __launch_bounds__(kDT) k_ccd_dense(const __grid_constant__ Sweep
     const bool w0 = threadIdx.x < 32;
     unsigned long long seq = *S.xcounter;
     XPrev pv{0ull, 0ull};
-    xprev_load(S.xslots, pv);
+    xprev_load(S, pv);
     int err = 0;
     double errv = 0.0;
     long long nvisit = 0, nmoved = 0;
@@ -647,7 +711,7 @@ __global__ void __launch_bounds__(kDT) k_ccd_dense(const __grid_constant__ Sweep
         }
         int e = err | ((bj != bj) || (rj != rj) ? 1 : 0);
         dblock_reduce(gs, hs, e, sm);
-        publish(A, seq, gs, hs, e);
+        publish(A, S, c, seq, gs, hs, e, pv);
         if (w0) {
             double tg, th;
             int te = 0;
@@ -733,7 +797,7 @@ __global__ void __launch_bounds__(kDT) k_ccd_dense(const __grid_constant__ Sweep
         }
         int e = err;
         dblock_reduce(ch, mg, e, sm);
-        publish(A, seq, ch, mg, e);
+        publish(A, S, c, seq, ch, mg, e, pv);
         if (w0) {
             double tch, tmg;
             int te;
@@ -755,7 +819,7 @@ __global__ void __launch_bounds__(kDT) k_ccd_dense(const __grid_constant__ Sweep
         S.res->refine_at = -1; // refines in place
         if (S.xowner) *S.xcounter = seq;
     }
-    if (c == 0 && S.xowner) xprev_store(S.xslots, pv);
+    if (c == 0 && S.xowner) xprev_store(S, pv);
 }
 
 // ---- dense kernels ---------------------------------------------------------
@@ -1628,6 +1692,8 @@ SweepArgs base_args(const ExchangePlan& plan) {
         s.xslots = plan.shard_slots.empty() ? plan.local_slots : plan.shard_slots[i];
         s.xcounter = plan.shard_counters.empty() ? plan.counter : plan.shard_counters[i];
         s.xowner = plan.shard_slots.empty() ? (i == 0) : 1;
+        s.lslots = plan.hier ? plan.shard_local[i] : nullptr;
+        s.p_local = st->ds->ctas;
         s.pq = st->ds->pq;
         s.snap = st->snap;
         s.vsplit = st->vsplit;
@@ -1664,7 +1730,9 @@ SweepArgs base_args(const ExchangePlan& plan) {
     for (size_t d = 0; d < plan.dst.size(); ++d) a.dst[d] = plan.dst[d];
     a.ndst = static_cast<int>(plan.dst.size());
     a.slots = plan.local_slots;
-    a.P = plan.total_participants;
+    a.P = plan.hier ? static_cast<int>(plan.dst.size()) : plan.total_participants;
+    a.hier = plan.hier ? 1 : 0;
+    if (plan.hier && plan.shard_local.size() != plan.shards.size()) internal_error("exchange plan: local areas");
     a.counter = plan.counter;
     static const unsigned long long timeout_ns = [] {
         const char* e = std::getenv("BSCCS_XCHG_TIMEOUT_S");

@@ -223,6 +223,11 @@ struct ExchangePlan {
     std::vector<unsigned long long*> shard_slots, shard_counters;
     int total_participants;                // CTAs across all ranks
     int participant_base;                  // first participant of shard 0
+    // hierarchical exchange (multi-rank groups, ccd_kernels.cu forward_local):
+    // per local shard the local area its CTAs add into; `dst` then receives
+    // one arrival per rank
+    bool hier = false;
+    std::vector<unsigned long long*> shard_local;
 };
 
 SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool normalized, bool dense = false);

@@ -581,7 +581,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
     Cached C;
     HeadRegs H;
     XPrev pv{0ull, 0ull};
-    if (A.mode != kModeUpdate) xprev_load(S.xslots, pv);
+    if (A.mode != kModeUpdate) xprev_load(S, pv);
 
     if (A.mode == kModeUpdate) {
         const int j = A.single_j;
@@ -596,7 +596,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         // CTA 0 of the first local shard contributes this rank's values
         const bool src = (c == 0 && si == 0);
         const double a = src ? A.red_a : 0.0, b = src ? A.red_b : 0.0;
-        publish(A, seq, a, b, 0);
+        publish(A, S, c, seq, a, b, 0, pv);
         if (threadIdx.x < 32) {
             double ta, tb;
             int te;
@@ -607,7 +607,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                 S.res->err_remote = te;
                 if (S.xowner) *S.xcounter = seq + 1;
             }
-            if (c == 0 && S.xowner) xprev_store(S.xslots, pv);
+            if (c == 0 && S.xowner) xprev_store(S, pv);
         }
         return;
     }
@@ -621,7 +621,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         gh_compute<false, kST>(S, C, p0, p1, H, gs, hs, err, sm, T, X);
         if (err) record_error(S.err, err, 0.0);
         block_reduce(gs, hs, err, false, sm);
-        publish(A, seq, gs, hs, err);
+        publish(A, S, c, seq, gs, hs, err, pv);
         if (threadIdx.x < 32) {
             double tg, th;
             int te;
@@ -634,7 +634,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                 S.res->err_remote = te;
                 if (S.xowner) *S.xcounter = seq + 1;
             }
-            if (c == 0 && S.xowner) xprev_store(S.xslots, pv);
+            if (c == 0 && S.xowner) xprev_store(S, pv);
         }
         return;
     }
@@ -741,7 +741,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
                 }
             }
             if (tr && idx < A.ntrace) trb[idx * trs + 1] = gtimer();
-            if (!(A.dbg & 4)) publish(A, seq, gs, hs, e);
+            if (!(A.dbg & 4)) publish(A, S, c, seq, gs, hs, e, pv);
             if (TB.b0) { // the previous coordinate's marks were read above: clear them for the next update
                 unsigned* b = TB.of((idx + 1) & 1);
                 for (int i = threadIdx.x; i < A.bm_words; i += kT) b[i] = 0u;
@@ -882,7 +882,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         if (err) record_error(S.err, err, errv);
         int e = err;
         block_reduce(ch, mg, e, false, sm);
-        publish(A, seq, ch, mg, e);
+        publish(A, S, c, seq, ch, mg, e, pv);
         if (w0) {
             double tch, tmg;
             int te;
@@ -906,6 +906,6 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_ccd(const __grid_constant_
         S.res->refine_at = refine_at;
         if (S.xowner) *S.xcounter = seq;
     }
-    if (c == 0 && S.xowner) xprev_store(S.xslots, pv);
+    if (c == 0 && S.xowner) xprev_store(S, pv);
 }
 

@@ -218,3 +218,27 @@ def test_rank_group_world1_matches_single_fit():
     assert got[0] == "ok", got
     _, c1, c2, same, lp1, lp2 = got
     assert c1 == c2 and same and lp1 == lp2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nshards", [2, 4, 8])
+def test_hierarchical_exchange_bitwise_equals_flat(nshards, monkeypatch):
+    """virtual ranks with the hierarchical exchange (each rank's CTAs add into
+    its local area, its CTA 0 forwards the integer sums: one arrival per rank
+    on every polled word) and with the flat one (every CTA into every area):
+    the same integer sums, so the same bits -- and the unsharded fit to 1e-9"""
+    ds = datagen.config_dataset("10k")
+    prior = B.laplace_prior(0.1)
+    out = {}
+    for mode in ("flat", "hier"):
+        monkeypatch.setenv("BSCCS_XCHG", mode)
+        grp = sharding.LocalGroup(sharding.shard_dataset(ds, nshards), virtual_ranks=True)
+        out[mode] = grp.fit(prior)
+        grp.close()
+    a, b = out["flat"], out["hier"]
+    assert np.array_equal(a.beta_map, b.beta_map) and a.log_posterior == b.log_posterior
+    assert a.cycles_run == b.cycles_run
+    single = B.fit(ds, prior)
+    assert a.cycles_run == single.cycles_run
+    nz = single.beta_map != 0
+    assert np.all(np.abs(a.beta_map[nz] - single.beta_map[nz]) <= 1e-9 * np.abs(single.beta_map[nz]))
