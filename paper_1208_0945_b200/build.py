@@ -19,7 +19,7 @@ LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libbsccs_b200.so"
 
 SOURCES = ["ccd_kernels.cu", "subset.cu", "batch.cu", "capi.cpp", "drivers.cpp", "loader.cpp", "datagen.cpp"]
-HEADERS = ["engine.h", "devutil.h", "prior.h", "rng.h", "status.h", "xchg.cuh", "sweep_impl.cuh"]
+HEADERS = ["engine.h", "devutil.h", "prior.h", "rng.h", "status.h", "xchg.cuh", "sweep_impl.cuh", "rsweep.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

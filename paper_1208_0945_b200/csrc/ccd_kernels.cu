@@ -72,6 +72,9 @@ constexpr int kWarps = kT / 32;
 constexpr int kLLBlocks = 592;      // fixed => deterministic LL reduction
 constexpr int kLLThreads = 256;
 constexpr double kXbBound = 700.0;  // xbeta_bound<double> engine.hpp:20-23
+// the same bound on exp(x'beta) (k_rcd): exp(+-700) as doubles
+constexpr double kExpXbMax = 0x1.d945df4f8ec8ep+1009; // exp(700)
+constexpr double kExpXbMin = 0x1.14f2b0fb9307fp-1010; // exp(-700)
 constexpr int kHtBits = 11;         // subject hash table of the speculation repair
 constexpr int kHt = 1 << kHtBits;
 
@@ -96,6 +99,15 @@ struct ShardArgs {
     const int32_t* row_slot;  // [K] slot of each era
     const int32_t* bstart;    // [N] block of each subject
     const int32_t* era_len;   // [K] era lengths (dense path)
+    // resident-beta sweep (rsweep.cuh)
+    const RRec* rq;           // [nnz] pair records, CSC order
+    const uint16_t* rovf;     // overflow drug lists (eras with more than 8 other drugs)
+    double* denc;             // [N] denominators
+    const double* beta_prev;  // [J] beta at the start of the cycle (criterion)
+    const int64_t* csr_ptr;   // [K+1] row -> drugs (criterion)
+    const int32_t* csr_col;
+    const uint8_t* edeg;      // [K] drugs per era (criterion chunks)
+    const uint16_t* ecol;     // [nnz] csr_col as u16 (criterion chunks)
     double* beta;
     double* trust;
     DevErr* err;
@@ -131,14 +143,19 @@ struct SweepArgs {
     int stream_off, stream_cap; // streamed-slice staging buffer in dynamic shared memory (bytes offset, pairs)
     int bm_words; // touched-subject bitmaps (words each) instead of the hash table (no subject tile)
     int ss_cap; // capacity of the shared-memory subject tile (0: subjects stay in HBM)
+    int beta_cap; // k_rcd: doubles of shared memory reserved for beta (>= J, multiple of 16)
+    int crit_E, crit_cap; // k_rcd criterion: eras per chunk (multiple of the CTA size), drugs per chunk buffer
+    double beta_limit;    // k_rcd: |beta_j| above this stops the sweep (products of exp(beta) stay in range)
     int dbg; // profiling only: bit0 skip grad/hess, bit1 skip update, bit2 skip exchange, bit4 no speculation
     unsigned long long* trace; // profiling only: [ntrace][gridDim][kTr] globaltimer stamps
     int ntrace;
     unsigned long long poll_timeout_ns; // bounded exchange spin (DERR_XCHG_TIMEOUT)
 };
 
-constexpr int kTr = 8; // stamps: top, pre-publish, gather done, update done, post-issue, poll done,
-                       // data warp at the step barrier, step computed (warp 0)
+constexpr int kTr = 16; // stamps: top, pre-publish, gather done, update done, post-issue, poll done,
+                        // data warp at the step barrier, step computed (warp 0); k_rcd data warp 1:
+                        // 8 update diffs, 9 update staged, 10 heads done, 11 repaired, 12 gh staged,
+                        // 13 run terms done, 14 window issued, 15 records of idx+1 landed
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -605,6 +622,58 @@ struct UpdErr {
 
 enum StepStatus { ST_OK = 0, ST_REMOTE_ERR = 1, ST_STEP_ERR = 2, ST_NONFINITE = 3, ST_REFINE = 4 };
 
+// ---- resident-beta sweep helpers (rsweep.cuh) ---------------------------------
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+// generic-proxy accesses of a buffer before the async proxy (bulk copy) rewrites it
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    const unsigned a = smem_u32(bar);
+    unsigned done;
+    do {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(done)
+                     : "r"(a), "r"(parity)
+                     : "memory");
+    } while (!done);
+}
+// one bulk copy global -> shared (TMA), completion counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                                         uint64_t pol) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+                 : "memory");
+}
+// L2 eviction policies: the streamed pair records go first, the denominators stay
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double ld_keep(const double* p, uint64_t pol) {
+    double v;
+    // volatile (issued where written, in the speculative window, not sunk to
+    // the first use) but no memory clobber: the other loads stay free to move
+    asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st_keep(double* p, double v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+
 // ---- the sweep kernel, per register-tile count -------------------------------
 namespace t3 {
 #define SWEEP_TILES BSCCS_CACHED_TILES
@@ -616,6 +685,32 @@ namespace t1 {
 #include "sweep_impl.cuh"
 #undef SWEEP_TILES
 } // namespace t1
+// resident-beta sweep shapes: 1 slot x 384 threads (slices <= 352 pairs),
+// 2 x 512 (<= 960), 3 x 384 (<= 1,056)
+#ifndef RS_WIDE_THREADS
+#define RS_WIDE_THREADS 512
+#endif
+namespace r1 {
+#define RS_TILES 1
+#define RS_THREADS 384
+#include "rsweep.cuh"
+#undef RS_THREADS
+#undef RS_TILES
+} // namespace r1
+namespace r2 {
+#define RS_TILES 2
+#define RS_THREADS RS_WIDE_THREADS
+#include "rsweep.cuh"
+#undef RS_THREADS
+#undef RS_TILES
+} // namespace r2
+namespace r3 {
+#define RS_TILES 3
+#define RS_THREADS 384
+#include "rsweep.cuh"
+#undef RS_THREADS
+#undef RS_TILES
+} // namespace r3
 
 // ---- the dense update path (UpdatePath::dense) ---------------------------------
 //
@@ -858,14 +953,42 @@ __global__ void k_dense_xb(double* X, double* snap, const int64_t* __restrict__ 
 
 // denominators: per subject, ascending sum of l*exp(x'beta) (engine.hpp:76-89)
 __global__ void k_dense_den(double* X, const int32_t* __restrict__ len, const int32_t* __restrict__ off,
-                            const int32_t* __restrict__ bstart, int32_t N) {
+                            const int32_t* __restrict__ bstart, int32_t N, double* denc) {
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < N;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int b = bstart[i], k0 = off[i], k1 = off[i + 1];
         double total = 0.0;
         for (int k = k0; k < k1; ++k) total = __dadd_rn(total, lexp(len[k], X[b + kBlockHeader + (k - k0)]));
         X[b] = total;
+        if (denc) denc[i] = total;
     }
+}
+
+// criterion snapshot of the cycle start rebuilt from beta at that point (a
+// cycle the resident-beta sweep began and k_ccd finishes): k_dense_xb's sum
+__global__ void k_snap_from_beta(double* snap, const int64_t* __restrict__ csr_ptr, const int32_t* __restrict__ csr_col,
+                                 const double* __restrict__ beta, int32_t K) {
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < K;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double xb = 0.0;
+        for (int64_t q = csr_ptr[k]; q < csr_ptr[k + 1]; ++q) {
+            const double b = beta[csr_col[q]];
+            if (b != 0.0) xb = __dadd_rn(xb, b);
+        }
+        snap[k] = xb;
+    }
+}
+
+// resident-beta sweep state <-> subject-block headers
+__global__ void k_hdr_to_denc(const double* X, const int32_t* __restrict__ bstart, double* denc, int32_t N) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < N;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        denc[i] = X[bstart[i]];
+}
+__global__ void k_denc_to_hdr(double* X, const int32_t* __restrict__ bstart, const double* denc, int32_t N) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < N;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        X[bstart[i]] = denc[i];
 }
 
 __global__ void k_snapshot(const double* X, const int32_t* __restrict__ row_slot, double* snap, int32_t K) {
@@ -1163,6 +1286,106 @@ __global__ void k_build_pq(const int2* __restrict__ pairs, int64_t nnz, const in
     }
 }
 
+// ---- pair records of the resident-beta sweep (engine.h RRec) ---------------
+// The CSR sort carries each pair's CSC position with its column, so the
+// records are written per era from its (contiguous) drug list: one 32-B
+// store per pair, no per-pair search.
+__global__ void k_pack_pc(const int32_t* __restrict__ col_of, int64_t nnz, unsigned long long* out) {
+    for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < nnz;
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[p] = (static_cast<unsigned long long>(p) << 32) | static_cast<uint32_t>(col_of[p]);
+}
+__global__ void k_unpack_pc(const unsigned long long* __restrict__ v, int64_t nnz, int32_t* csr_col, uint32_t* pos) {
+    for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < nnz;
+         q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const unsigned long long x = v[q];
+        csr_col[q] = static_cast<int32_t>(x & 0xffffffffull);
+        pos[q] = static_cast<uint32_t>(x >> 32);
+    }
+}
+// the criterion's compact CSR: drugs per era (u8) and the drugs (u16)
+__global__ void k_compact_csr(const int64_t* __restrict__ csr_ptr, const int32_t* __restrict__ csr_col, int32_t K,
+                              int64_t nnz, uint8_t* edeg, uint16_t* ecol) {
+    const int64_t n = max(static_cast<int64_t>(K), nnz);
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        if (i < K) edeg[i] = static_cast<uint8_t>(csr_ptr[i + 1] - csr_ptr[i]);
+        if (i < nnz) ecol[i] = static_cast<uint16_t>(csr_col[i]);
+    }
+}
+// per subject: overflow drug entries of its pairs; bad |= 1 when an era has
+// more than kRMaxOthers + 1 drugs or n_i exceeds the record's field
+__global__ void k_rq_count(const int32_t* __restrict__ off, const int32_t* __restrict__ events,
+                           const int64_t* __restrict__ csr_ptr, int32_t N, long long* cnt, int* bad, int* max_deg) {
+    for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < N;
+         s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        long long o = 0, md = 0;
+        int b = events[s] > kRMaxEvents || events[s] < 0;
+        for (int k = off[s]; k < off[s + 1]; ++k) {
+            const long long deg = csr_ptr[k + 1] - csr_ptr[k];
+            if (deg - 1 > kRMaxOthers) b = 1;
+            if (deg - 1 > kRInline) o += deg * ((deg - 1 - kRInline + 7) & ~7ll); // lists padded to 16 B
+            md = deg > md ? deg : md;
+        }
+        cnt[s] = o;
+        if (b) atomicOr(bad, 1);
+        atomicMax(max_deg, static_cast<int>(md < (1 << 30) ? md : (1 << 30)));
+    }
+}
+__global__ void k_build_rq(const int32_t* __restrict__ off, const int32_t* __restrict__ events,
+                           const int32_t* __restrict__ len, const int64_t* __restrict__ csr_ptr,
+                           const int32_t* __restrict__ csr_col, const uint32_t* __restrict__ pos,
+                           const int32_t* __restrict__ cta_subj, int C, const long long* __restrict__ ovb, int32_t N,
+                           RRec* rq, uint16_t* rovf) {
+    for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < N;
+         s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        int lo = 0, hi = C + 1; // first c with cta_subj[c] > s
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (cta_subj[mid] > s) hi = mid;
+            else lo = mid + 1;
+        }
+        const int ls = static_cast<int>(s) - cta_subj[lo - 1];
+        const int n = events[s];
+        long long ov = ovb[s];
+        for (int k = off[s]; k < off[s + 1]; ++k) {
+            const int64_t q0 = csr_ptr[k];
+            const int deg = static_cast<int>(csr_ptr[k + 1] - q0);
+            for (int a = 0; a < deg; ++a) {
+                RRec r;
+                r.ls = ls;
+                r.len = len[k];
+                r.meta = (deg - 1) | (a << 8) | (n << 16); // a: the pair's drug sorts after a other drugs
+                r.ovf = deg - 1 > kRInline ? static_cast<int32_t>(ov) : 0;
+                int i = 0;
+                for (int b = 0; b < deg; ++b) {
+                    if (b == a) continue;
+                    const uint16_t d = static_cast<uint16_t>(csr_col[q0 + b]);
+                    if (i < kRInline) r.o[i] = d;
+                    else rovf[ov + (i - kRInline)] = d;
+                    ++i;
+                }
+                for (; i < kRInline; ++i) r.o[i] = 0xffff;
+                if (deg - 1 > kRInline) { // pad the overflow list to a multiple of 8 (one 16-B load per 8)
+                    const int ext = (deg - 1 - kRInline + 7) & ~7;
+                    for (int t = deg - 1 - kRInline; t < ext; ++t) rovf[ov + t] = 0xffff;
+                    ov += ext;
+                }
+                rq[pos[q0 + a]] = r;
+            }
+        }
+    }
+}
+
+// resident-beta sweep enabled (BSCCS_SWEEP=classic keeps every sweep on k_ccd)
+bool rcd_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("BSCCS_SWEEP");
+        return !(e && std::string(e) == "classic");
+    }();
+    return on;
+}
+
 // Small pinned result blocks for the per-state D2H of kernel scalars.
 struct PinnedResults {
     std::mutex m;
@@ -1245,7 +1468,10 @@ void ensure_kernel_attrs(int device) {
     for (void* fn : {reinterpret_cast<void*>(t3::k_ccd<false, false>), reinterpret_cast<void*>(t3::k_ccd<false, true>),
                      reinterpret_cast<void*>(t3::k_ccd<true, false>), reinterpret_cast<void*>(t3::k_ccd<true, true>),
                      reinterpret_cast<void*>(t1::k_ccd<false, false>), reinterpret_cast<void*>(t1::k_ccd<true, false>),
-                     reinterpret_cast<void*>(t1::k_ccd<false, true>), reinterpret_cast<void*>(t1::k_ccd<true, true>)})
+                     reinterpret_cast<void*>(t1::k_ccd<false, true>), reinterpret_cast<void*>(t1::k_ccd<true, true>),
+                     reinterpret_cast<void*>(r3::k_rcd<false>), reinterpret_cast<void*>(r3::k_rcd<true>),
+                     reinterpret_cast<void*>(r2::k_rcd<false>), reinterpret_cast<void*>(r2::k_rcd<true>),
+                     reinterpret_cast<void*>(r1::k_rcd<false>), reinterpret_cast<void*>(r1::k_rcd<true>)})
         CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSweepSmem));
     if (device < 32) done.fetch_or(1u << device);
 }
@@ -1311,6 +1537,9 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
     long long* d_excl = dalloc<long long>(static_cast<int64_t>(N) + 1, scratch_bytes, s);
     int* d_bad = dalloc<int>(1, scratch_bytes, s);
     CUDA_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
+    bool want_rq = false;
+    unsigned long long* d_pc = nullptr;  // (CSC position, column) per pair, then sorted by row
+    unsigned long long* d_spc = nullptr;
     if (nnz > 0) {
         k_interleave<<<grid_for(nnz, 256, sms), 256, 0, s>>>(d_rows, d_subj, ds->pairs, nnz);
         k_pair_meta<<<grid_for(nnz, 256, sms), 256, 0, s>>>(ds->pairs, ds->col_ptr, J, ds->subject_offsets, N, K,
@@ -1322,14 +1551,32 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
         size_t sort_bytes = 0;
         int end_bit = 1;
         while ((1ll << end_bit) < static_cast<long long>(K)) ++end_bit;
-        if (nnz > 0)
+        // resident-beta sweep records need each CSR entry's CSC position:
+        // the sort then carries (position, column) pairs
+        want_rq = rcd_enabled() && nnz > 0 && nnz < (1ll << 32) && J <= 65535;
+        if (want_rq) {
+            d_pc = dalloc<unsigned long long>(nnz, scratch_bytes, s);
+            d_spc = dalloc<unsigned long long>(nnz, scratch_bytes, s);
+            k_pack_pc<<<grid_for(nnz, 256, sms), 256, 0, s>>>(d_col, nnz, d_pc);
+            count_launches(1);
+            CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, d_rows, d_subj, d_pc, d_spc, nnz, 0,
+                                                     end_bit, s));
+        } else if (nnz > 0)
             CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, d_rows, d_subj, d_col, ds->csr_col, nnz, 0,
                                                      end_bit, s));
         size_t scan2 = 0;
         CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, scan2, d_w, d_excl, N + 1, s));
         const size_t tb = std::max(std::max(tmp_bytes, sort_bytes), scan2);
         unsigned char* tmp = dalloc<unsigned char>(static_cast<int64_t>(std::max<size_t>(tb, 16)), scratch_bytes, s);
-        if (nnz > 0) {
+        if (want_rq) {
+            CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, d_rows, d_subj, d_pc, d_spc, nnz, 0, end_bit, s));
+            // d_rows (the consumed keys) receives the CSC positions
+            k_unpack_pc<<<grid_for(nnz, 256, sms), 256, 0, s>>>(d_spc, nnz, ds->csr_col,
+                                                                 reinterpret_cast<uint32_t*>(d_rows));
+            count_launches(1);
+            dfree(d_pc, s);
+            dfree(d_spc, s);
+        } else if (nnz > 0) {
             // keys: rows (consumed); d_subj is free after interleave and
             // receives the sorted keys
             CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, d_rows, d_subj, d_col, ds->csr_col, nnz, 0,
@@ -1379,6 +1626,46 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
             dfree(d_cs, s);
             dfree(d_cb, s);
         }
+        if (want_rq) { // resident-beta sweep pair records (engine.h RRec)
+            int64_t b4 = 0;
+            long long* d_oc = dalloc<long long>(static_cast<int64_t>(N) + 1, b4, s);
+            long long* d_ob = dalloc<long long>(static_cast<int64_t>(N) + 1, b4, s);
+            int* d_rbad = dalloc<int>(2, b4, s); // [0] bad, [1] largest era
+            CUDA_TRY(cudaMemsetAsync(d_rbad, 0, 2 * sizeof(int), s));
+            CUDA_TRY(cudaMemsetAsync(d_oc + N, 0, sizeof(long long), s));
+            k_rq_count<<<grid_for(N, 256, sms), 256, 0, s>>>(ds->subject_offsets, ds->events_per_subject, ds->csr_ptr,
+                                                             N, d_oc, d_rbad, d_rbad + 1);
+            size_t sb = 0;
+            CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, sb, d_oc, d_ob, N + 1, s));
+            unsigned char* tmp3 = dalloc<unsigned char>(static_cast<int64_t>(std::max<size_t>(sb, 16)), b4, s);
+            CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp3, sb, d_oc, d_ob, N + 1, s));
+            long long novf = 0;
+            int rbad[2] = {0, 0};
+            CUDA_TRY(cudaMemcpyAsync(&novf, d_ob + N, sizeof(long long), cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaMemcpyAsync(rbad, d_rbad, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+            if (!rbad[0] && novf < (1ll << 31)) {
+                ds->novf = novf;
+                ds->max_deg = std::max(1, rbad[1]);
+                ds->rq = dalloc<RRec>(nnz, ds->device_bytes, s);
+                ds->rovf = dalloc<uint16_t>(std::max<long long>(novf, 8), ds->device_bytes, s);
+                k_build_rq<<<grid_for(N, 128, sms), 128, 0, s>>>(
+                    ds->subject_offsets, ds->events_per_subject, ds->era_lengths, ds->csr_ptr, ds->csr_col,
+                    reinterpret_cast<const uint32_t*>(d_rows), ds->cta_subj, C, d_ob, N, ds->rq, ds->rovf);
+                ds->edeg = dalloc<uint8_t>(static_cast<int64_t>(K) + 32, ds->device_bytes, s);
+                ds->ecol = dalloc<uint16_t>(nnz + 16, ds->device_bytes, s);
+                CUDA_TRY(cudaMemsetAsync(ds->edeg, 0, static_cast<size_t>(K) + 32, s));
+                CUDA_TRY(cudaMemsetAsync(ds->ecol, 0, sizeof(uint16_t) * (nnz + 16), s));
+                k_compact_csr<<<grid_for(std::max<int64_t>(K, nnz), 256, sms), 256, 0, s>>>(ds->csr_ptr, ds->csr_col,
+                                                                                            K, nnz, ds->edeg, ds->ecol);
+                count_launches(2);
+            }
+            count_launches(1);
+            dfree(tmp3, s);
+            dfree(d_oc, s);
+            dfree(d_ob, s);
+            dfree(d_rbad, s);
+        }
         if (y_dot_x_global) {
             std::vector<double> yd(static_cast<size_t>(J));
             for (int32_t j = 0; j < J; ++j) yd[static_cast<size_t>(j)] = static_cast<double>(y_dot_x_global[j]);
@@ -1395,6 +1682,7 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
     dfree(d_rows, s);
     dfree(d_subj, s);
     dfree(d_col, s);
+    dfree(d_spc, s);
     dfree(d_w, s);
     dfree(d_excl, s);
     dfree(d_bad, s);
@@ -1537,6 +1825,10 @@ void dataset_destroy(bsccs_dataset* ds) {
     dfree(ds->y_dot_x, s);
     dfree(ds->col_nonempty, s);
     dfree(ds->col_runs, s);
+    dfree(ds->rq, s);
+    dfree(ds->rovf, s);
+    dfree(ds->edeg, s);
+    dfree(ds->ecol, s);
     if (s) {
         cudaStreamSynchronize(s);
         cudaStreamDestroy(s);
@@ -1552,10 +1844,12 @@ void launch_dense(bsccs_state* st) {
     const int g = build_grid(ds->device);
     k_dense_xb<<<g, 256, 0, st->stream>>>(st->X, st->snap, ds->csr_ptr, ds->csr_col, st->beta, ds->row_slot, ds->K,
                                           st->err);
-    k_dense_den<<<g, 256, 0, st->stream>>>(st->X, ds->era_lengths, ds->subject_offsets, ds->bstart, ds->N);
+    k_dense_den<<<g, 256, 0, st->stream>>>(st->X, ds->era_lengths, ds->subject_offsets, ds->bstart, ds->N, st->denc);
     CUDA_TRY(cudaGetLastError());
     count_launches(2);
     st->snap_valid = true;
+    st->x_stale = false;
+    st->denc_valid = st->denc != nullptr;
 }
 
 void alloc_state(bsccs_state* st, const bsccs_dataset* ds) {
@@ -1576,6 +1870,10 @@ void alloc_state(bsccs_state* st, const bsccs_dataset* ds) {
     st->err = dalloc<DevErr>(1, b, s);
     st->res = dalloc<DevResult>(1, b, s);
     st->scratch = dalloc<double>(2 * kLLBlocks, b, s);
+    if (ds->rq) {
+        st->denc = dalloc<double>(ds->N, b, s);
+        st->beta_prev = dalloc<double>(ds->J, b, s);
+    }
     st->res_h = pinned_result();
     CUDA_TRY(cudaEventCreate(&st->ev0));
     CUDA_TRY(cudaEventCreate(&st->ev1));
@@ -1624,7 +1922,11 @@ bsccs_state* state_clone(const bsccs_state* src) {
         CUDA_TRY(cudaMemcpyAsync(st->X, src->X, sizeof(double) * ds->nslots, cudaMemcpyDeviceToDevice, st->stream));
         CUDA_TRY(cudaMemcpyAsync(st->snap, src->snap, sizeof(double) * ds->K, cudaMemcpyDeviceToDevice, st->stream));
         CUDA_TRY(cudaMemcpyAsync(st->beta, src->beta, sizeof(double) * ds->J, cudaMemcpyDeviceToDevice, st->stream));
+        if (st->denc && src->denc)
+            CUDA_TRY(cudaMemcpyAsync(st->denc, src->denc, sizeof(double) * ds->N, cudaMemcpyDeviceToDevice, st->stream));
         st->snap_valid = src->snap_valid;
+        st->x_stale = src->x_stale;
+        st->denc_valid = src->denc_valid;
         sync_and_check(st);
     } catch (...) {
         state_destroy(st);
@@ -1654,6 +1956,8 @@ void state_destroy(bsccs_state* st) {
         dfree(st->err, s);
         dfree(st->res, s);
         dfree(st->scratch, s);
+        dfree(st->denc, s);
+        dfree(st->beta_prev, s);
         cudaStreamSynchronize(s);
     }
     release_pinned_result(st->res_h);
@@ -1662,6 +1966,32 @@ void state_destroy(bsccs_state* st) {
     if (s) cudaStreamDestroy(s);
     if (prev >= 0) cudaSetDevice(prev);
     delete st;
+}
+
+// X (subject blocks) brought up to date after resident-beta sweeps: x'beta
+// rebuilt from beta (the value those sweeps use) with its snapshot, the
+// headers from the compact denominators.
+void sync_x(bsccs_state* st) {
+    if (!st->x_stale) return;
+    const bsccs_dataset* ds = st->ds;
+    const int g = build_grid(ds->device);
+    k_dense_xb<<<g, 256, 0, st->stream>>>(st->X, st->snap, ds->csr_ptr, ds->csr_col, st->beta, ds->row_slot, ds->K,
+                                          st->err);
+    k_denc_to_hdr<<<g, 256, 0, st->stream>>>(st->X, ds->bstart, st->denc, ds->N);
+    CUDA_TRY(cudaGetLastError());
+    count_launches(2);
+    st->x_stale = false;
+    st->snap_valid = true;
+}
+
+// compact denominators from the headers (after an op that wrote X)
+void sync_denc(bsccs_state* st) {
+    if (st->denc_valid || !st->denc) return;
+    const bsccs_dataset* ds = st->ds;
+    k_hdr_to_denc<<<build_grid(ds->device), 256, 0, st->stream>>>(st->X, ds->bstart, st->denc, ds->N);
+    CUDA_TRY(cudaGetLastError());
+    count_launches(1);
+    st->denc_valid = true;
 }
 
 void dense_recompute(bsccs_state* st, const double* beta_host) {
@@ -1710,6 +2040,14 @@ SweepArgs base_args(const ExchangePlan& plan) {
         s.row_slot = st->ds->row_slot;
         s.bstart = st->ds->bstart;
         s.era_len = st->ds->era_lengths;
+        s.rq = st->ds->rq;
+        s.rovf = st->ds->rovf;
+        s.denc = st->denc;
+        s.beta_prev = st->beta_prev;
+        s.csr_ptr = st->ds->csr_ptr;
+        s.csr_col = st->ds->csr_col;
+        s.edeg = st->ds->edeg;
+        s.ecol = st->ds->ecol;
         s.beta = st->beta;
         s.trust = st->trust;
         s.err = st->err;
@@ -1868,6 +2206,98 @@ void launch_ccd(const ExchangePlan& plan, SweepArgs& a) {
     count_launches(1);
 }
 
+// Launch shape of the resident-beta sweep, or ok = false when a shard does
+// not qualify (no pair records, a slice beyond three register tiles, or
+// beta plus the staging buffers and the touched-subject bitmaps beyond the
+// shared memory): those sweeps run k_ccd.
+struct RcdShape {
+    bool ok = false, kss = false;
+    int tiles = 0, threads = 0;
+    int ss_cap = 0, bm_words = 0, beta_cap = 0, crit_E = 0, crit_cap = 0;
+    double beta_limit = 0.0; // |beta_j| beyond this: partial products of exp(beta) could leave range
+    size_t bytes = 0;
+};
+RcdShape rcd_shape(const ExchangePlan& plan) {
+    RcdShape r;
+    if (!rcd_enabled()) return r;
+    int maxslice = 0, maxsub = 0, maxdeg = 1;
+    for (auto* st : plan.shards) {
+        if (!st->ds->rq || !st->ds->edeg || !st->denc) return r;
+        maxslice = std::max(maxslice, st->ds->max_slice);
+        maxsub = std::max(maxsub, st->ds->max_cta_subjects);
+        maxdeg = std::max(maxdeg, st->ds->max_deg);
+    }
+    r.beta_limit = 700.0 / maxdeg;
+    static const int tiles_forced = [] {
+        const char* e = std::getenv("BSCCS_RTILES"); // experiment hook: 1, 2 or 3
+        return e ? std::atoi(e) : 0;
+    }();
+    // the smallest shape whose slots hold every slice
+    size_t smem_fixed = 0, bufs = 0;
+    if ((tiles_forced == 0 || tiles_forced == 1) && maxslice <= r1::kRC) {
+        r.tiles = 1, r.threads = r1::kT, smem_fixed = r1::kRSmemBytes, bufs = r1::kRBufs * r1::kRBufBytes;
+    } else if ((tiles_forced == 0 || tiles_forced == 2) && maxslice <= r2::kRC) {
+        r.tiles = 2, r.threads = r2::kT, smem_fixed = r2::kRSmemBytes, bufs = r2::kRBufs * r2::kRBufBytes;
+    } else if (maxslice <= r3::kRC) {
+        r.tiles = 3, r.threads = r3::kT, smem_fixed = r3::kRSmemBytes, bufs = r3::kRBufs * r3::kRBufBytes;
+    } else {
+        return r;
+    }
+    r.beta_cap = (plan.shards[0]->ds->J + 15) / 16 * 16;
+    const size_t head = smem_fixed + 2 * static_cast<size_t>(r.beta_cap) * sizeof(double);
+    const size_t base = head + bufs;
+    static const bool tile_on = [] {
+        const char* e = std::getenv("BSCCS_SUBJ_SMEM");
+        return !(e && e[0] == '0');
+    }();
+    const int cap = std::max(2, (maxsub + 1) / 2 * 2);
+    if (tile_on && base + static_cast<size_t>(cap) * sizeof(double) <= static_cast<size_t>(kMaxSweepSmem)) {
+        r.kss = true;
+        r.ss_cap = cap;
+        r.bytes = base + static_cast<size_t>(cap) * sizeof(double);
+    } else {
+        r.bm_words = maxsub / 32 + 1;
+        r.bytes = base + 2 * static_cast<size_t>(r.bm_words) * sizeof(unsigned);
+        if (r.bytes > static_cast<size_t>(kMaxSweepSmem)) return r;
+    }
+    // criterion chunks in the union region: beta at cycle start plus two
+    // buffers of crit_E eras' degrees and ~1.25x their expected drugs
+    double deg = 0.0;
+    for (auto* st : plan.shards) deg = std::max(deg, static_cast<double>(st->ds->nnz) / std::max(1, st->ds->K));
+    for (int eper = 8; eper >= 1; eper /= 2) {
+        const int E = eper * r.threads;
+        const int ccap = (static_cast<int>(E * deg * 1.25) + 256 + 7) / 8 * 8;
+        const size_t crit = head + static_cast<size_t>(r.beta_cap) * sizeof(double) + 2 * static_cast<size_t>(E + 32) +
+                            2 * sizeof(uint16_t) * static_cast<size_t>(ccap + 16);
+        if (crit <= static_cast<size_t>(kMaxSweepSmem) || eper == 1) {
+            r.crit_E = E;
+            r.crit_cap = ccap;
+            r.bytes = std::max(r.bytes, (crit + 15) / 16 * 16);
+            break;
+        }
+    }
+    if (r.bytes > static_cast<size_t>(kMaxSweepSmem)) return r;
+    r.ok = true;
+    return r;
+}
+
+void launch_rcd(const ExchangePlan& plan, SweepArgs& a, const RcdShape& sh) {
+    bsccs_state* s0 = plan.shards[0];
+    ensure_kernel_attrs(s0->ds->device);
+    a.beta_cap = sh.beta_cap;
+    a.ss_cap = sh.kss ? sh.ss_cap : 0;
+    a.bm_words = sh.kss ? 0 : sh.bm_words;
+    a.crit_E = sh.crit_E;
+    a.crit_cap = sh.crit_cap;
+    a.beta_limit = sh.beta_limit;
+    void* params[] = {&a};
+    void* fn = sh.tiles == 1   ? (sh.kss ? reinterpret_cast<void*>(r1::k_rcd<true>) : reinterpret_cast<void*>(r1::k_rcd<false>))
+               : sh.tiles == 2 ? (sh.kss ? reinterpret_cast<void*>(r2::k_rcd<true>) : reinterpret_cast<void*>(r2::k_rcd<false>))
+                               : (sh.kss ? reinterpret_cast<void*>(r3::k_rcd<true>) : reinterpret_cast<void*>(r3::k_rcd<false>));
+    CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(plan_ctas(plan)), dim3(sh.threads), params, sh.bytes, s0->stream));
+    count_launches(1);
+}
+
 ExchangePlan single_plan(bsccs_state* st) {
     ExchangePlan p;
     p.shards = {st};
@@ -1885,6 +2315,7 @@ void grad_hess(bsccs_state* st, int32_t j, double* g, double* h) {
     const bsccs_dataset* ds = st->ds;
     if (j < 0 || j >= ds->J) input_error("fused_grad_hess: coordinate out of range");
     DeviceGuard dg(ds->device);
+    sync_x(st);
     ExchangePlan plan = single_plan(st);
     SweepArgs a = base_args(plan);
     a.mode = kModeGradHess;
@@ -1903,6 +2334,7 @@ void sparse_update(bsccs_state* st, int32_t j, double delta) {
     if (!std::isfinite(delta)) numeric_error("sparse_delta_update: non-finite step");
     if (delta == 0.0) return;
     DeviceGuard dg(ds->device);
+    sync_x(st);
     ExchangePlan plan = single_plan(st);
     SweepArgs a = base_args(plan);
     a.mode = kModeUpdate;
@@ -1910,6 +2342,7 @@ void sparse_update(bsccs_state* st, int32_t j, double delta) {
     a.single_delta = delta;
     launch_ccd(plan, a);
     st->snap_valid = false;
+    st->denc_valid = false;
     sync_and_check(st);
     check_err_block(st);
 }
@@ -1918,6 +2351,7 @@ double log_likelihood(bsccs_state* st) {
     NvtxRange nvtx_("log_likelihood");
     const bsccs_dataset* ds = st->ds;
     DeviceGuard dg(ds->device);
+    sync_x(st);
     k_ll_partial<<<kLLBlocks, kLLThreads, 0, st->stream>>>(st->X, ds->row_slot, ds->event_counts, ds->bstart, ds->K,
                                                            ds->N, st->scratch, st->err);
     k_ll_final<<<1, 32, 0, st->stream>>>(st->scratch, kLLBlocks, st->res);
@@ -1931,6 +2365,7 @@ double log_likelihood(bsccs_state* st) {
 void state_get(bsccs_state* st, double* beta, double* xbeta, double* le, double* den) {
     const bsccs_dataset* ds = st->ds;
     DeviceGuard dg(ds->device);
+    sync_x(st);
     CUDA_TRY(cudaStreamSynchronize(st->stream));
     if (beta) CUDA_TRY(cudaMemcpy(beta, st->beta, sizeof(double) * ds->J, cudaMemcpyDeviceToHost));
     if (!st->le_tmp) {
@@ -2155,8 +2590,26 @@ SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool 
         if (ds0->col_nonempty_h[static_cast<size_t>(j)] || (any_empty && beta_h[static_cast<size_t>(j)] != 0.0))
             visit.push_back(j);
     }
+    const RcdShape rcd = dense ? RcdShape{} : rcd_shape(plan);
+    // the products of exp(beta) stay in range while max|beta| <= beta_limit
+    auto beta_in_range = [&] {
+        std::vector<double> b(static_cast<size_t>(J));
+        CUDA_TRY(cudaMemcpyAsync(b.data(), s0->beta, sizeof(double) * J, cudaMemcpyDeviceToHost, s0->stream));
+        CUDA_TRY(cudaStreamSynchronize(s0->stream));
+        for (double x : b)
+            if (!(std::fabs(x) <= rcd.beta_limit)) return false;
+        return true;
+    };
+    bool use_rcd = rcd.ok && beta_in_range();
     for (auto* st : plan.shards) {
-        prepare_snapshot(st);
+        if (use_rcd) { // compact denominators current; beta at the start of the cycle for the criterion
+            sync_denc(st);
+            CUDA_TRY(cudaMemcpyAsync(st->beta_prev, st->beta, sizeof(double) * J, cudaMemcpyDeviceToDevice,
+                                     st->stream));
+        } else {
+            sync_x(st);
+            prepare_snapshot(st);
+        }
         if (!st->visit_valid || st->visit_h != visit) {
             st->visit_h = visit;
             st->visit_valid = true;
@@ -2194,6 +2647,9 @@ SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool 
             CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_ccd_dense), dim3(s0->ds->ctas), dim3(kDT),
                                                  params, 0, s0->stream));
             count_launches(1);
+        } else if (use_rcd) {
+            launch_rcd(plan, a, rcd);
+            for (auto* st : plan.shards) st->x_stale = true;
         } else {
             launch_ccd(plan, a);
         }
@@ -2208,7 +2664,25 @@ SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool 
         nmoved += s0->res_h->moved;
         const int ra = s0->res_h->refine_at;
         if (ra < 0) break;
+        if (use_rcd) // the single-coordinate launches run on the subject blocks
+            for (auto* st : plan.shards) sync_x(st);
         const bool mv = refine_coordinate(plan, prior, visit[static_cast<size_t>(ra)]);
+        if (use_rcd) {
+            for (auto* st : plan.shards) st->denc_valid = false;
+            if (beta_in_range()) {
+                for (auto* st : plan.shards) sync_denc(st);
+            } else { // the rest of the cycle on k_ccd, its criterion against the cycle start
+                use_rcd = false;
+                const bsccs_dataset* d0 = s0->ds;
+                for (auto* st : plan.shards) {
+                    k_snap_from_beta<<<build_grid(d0->device), 256, 0, st->stream>>>(
+                        st->snap, st->ds->csr_ptr, st->ds->csr_col, st->beta_prev, st->ds->K);
+                    CUDA_TRY(cudaGetLastError());
+                    count_launches(1);
+                    st->snap_valid = true;
+                }
+            }
+        }
         refined.emplace_back(ra, mv ? 1 : 0);
         ++visited;
         nmoved += mv ? 1 : 0;
@@ -2220,7 +2694,15 @@ SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool 
         CUDA_TRY(cudaMemcpyAsync(moved.data(), s0->moved, visit.size(), cudaMemcpyDeviceToHost, s0->stream));
     CUDA_TRY(cudaStreamSynchronize(s0->stream));
     for (const auto& r : refined) moved[static_cast<size_t>(r.first)] = r.second;
-    for (auto* st : plan.shards) st->snap_valid = true;
+    for (auto* st : plan.shards) {
+        if (use_rcd) { // X stays stale until an op reads it (sync_x)
+            st->x_stale = true;
+            st->snap_valid = false;
+        } else {
+            st->snap_valid = true;
+            st->denc_valid = false;
+        }
+    }
     float ms = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&ms, s0->ev0, s0->ev1));
     s0->sweep_ms += ms;

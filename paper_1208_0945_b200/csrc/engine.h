@@ -48,6 +48,23 @@ constexpr int kBlockHeader = 2;
 constexpr int kLineSlots = 16;    // 128-B line / 8-B slot
 constexpr int kBlockChunk = 64;   // subjects packed per build thread (each chunk starts on a line)
 
+// Pair record of the resident-beta sweep (k_rcd, rsweep.cuh), CSC order,
+// 32 B: the subject's index within its CTA's range, the era length, meta =
+// the number of OTHER drugs of the era (bits 0-7) | how many of them sort
+// before the pair's own drug (bits 8-15) | n_i (bits 16-31), the first
+// overflow entry (more than 8 other drugs; each list padded with 0xffff to
+// a multiple of 8 entries, 16-B aligned), and up to 8 other drugs of the
+// era ascending (0xffff padding).  A pair's x'beta is rebuilt from these and beta in the
+// order of engine.hpp:173-181.
+struct alignas(16) RRec {
+    int32_t ls, len, meta, ovf;
+    uint16_t o[8];
+};
+static_assert(sizeof(RRec) == 32, "pair record is 32 B");
+constexpr int kRInline = 8;          // other drugs carried in the record
+constexpr int kRMaxOthers = 254;     // meta bits 0-7 (an era of at most 255 drugs)
+constexpr int32_t kRMaxEvents = 65535; // meta bits 16-31
+
 // Per-state device scalars written by kernels, mirrored to pinned host.
 struct DevResult {
     double g, h;              // tier-1 grad/hess
@@ -107,6 +124,15 @@ struct bsccs_dataset {
     int32_t* col_runs = nullptr;      // [J] subject runs per column (this shard)
     int32_t max_cta_subjects = 0;     // largest CTA subject range (sizes the shared-memory subject tile)
     int32_t max_slice = 0;            // largest per-CTA slice of any column (streamed path needed above kCap)
+    // resident-beta sweep (rsweep.cuh): pair records and overflow drug lists;
+    // rq == nullptr when the dataset does not qualify (J > 65535, nnz >= 2^32,
+    // an era with more than 256 drugs, n_i >= 2^23, or BSCCS_SWEEP=classic)
+    bsccs_b200::RRec* rq = nullptr;
+    uint16_t* rovf = nullptr;
+    int64_t novf = 0;
+    uint8_t* edeg = nullptr;   // [K] drugs per era, [nnz] drugs as u16: the sweep's criterion pass
+    uint16_t* ecol = nullptr;
+    int32_t max_deg = 0;       // drugs of the largest era
     // host copies of small metadata
     std::vector<int64_t> col_ptr_h;
     std::vector<uint8_t> col_nonempty_h;
@@ -140,6 +166,15 @@ struct bsccs_state {
     bsccs_b200::DevResult* res_h = nullptr; // pinned host mirror
     double* scratch = nullptr;              // reduction partials
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // resident-beta sweep: compact denominators [N] and beta at cycle start.
+    // The sweep keeps denc current and leaves X's x'beta / headers stale
+    // (x_stale) until an op that reads X rebuilds them (sync_x); ops that
+    // write X leave denc stale (denc_valid false) until the next sweep
+    // gathers it from the headers.
+    double* denc = nullptr;
+    double* beta_prev = nullptr;
+    bool denc_valid = false;
+    bool x_stale = false;
     double sweep_ms = 0.0;  // accumulated sweep-kernel time
     double alg_bytes = 0.0; // accumulated algorithmic bytes of the sweeps
     bool snap_valid = false;

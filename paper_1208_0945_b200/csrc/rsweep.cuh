@@ -1,0 +1,701 @@
+// rsweep.cuh -- k_rcd, the resident-beta sweep (one persistent cooperative
+// launch per CCD cycle, run_cycle solver.hpp:101-166).  ccd_kernels.cu
+// includes it once per register-tile count (namespaces r3 / r1, RS_TILES).
+// No include guard, by design.
+//
+// What changes against k_ccd (sweep_impl.cuh): the state has no per-era
+// x'beta.  Every CTA holds beta and E_j = exp(beta_j) in shared memory (all
+// CTAs of all ranks compute the identical step, so every copy stays
+// identical), and a pair's l*exp(x'beta) is rebuilt when it is needed as
+// l * (prod of E over the era's other drugs) * E_j -- the reference's
+// l*exp(sum of beta) (engine.hpp:77-78,173-181) as a product of per-drug
+// exponentials -- from the era's drug list, which travels with the pair
+// record.  The only random-access state left is the per-subject
+// denominator (8 B per subject: 77 MB at 10M, L2-resident), so a pair visit
+// costs a streamed 32-B record instead of a random DRAM line, and no exp.
+//
+// Pair records (dataset rq, CSC order, 32 B): {subject index within the
+// CTA's range, era length, other-drug count | n_i << 8, overflow offset,
+// up to 8 other drugs of the era (u16, ascending)}; a CTA's slice of a
+// column is contiguous, so one bulk copy (TMA, cp.async.bulk) per
+// coordinate stages it in shared memory, two coordinates ahead.
+//
+// Numerics: the reference carries x'beta incrementally (x'beta += delta,
+// engine.hpp:219-229) and l*exp(x'beta) from it; here l*exp(x'beta) is the
+// product above.  The two agree to a few ulps (exp of a sum with rounded
+// increments against a product of rounded exponentials).  The update is
+// the reference's: fresh = l*exp(x'beta + delta) (the product with
+// E_j' = exp(beta_j + delta)), den += fresh - old in pair order, the x'beta
+// bound (engine.hpp:17-28) checked on exp(x'beta + delta).  Partial products
+// stay in range while max|beta| * (largest era) <= 700 (ds->max_deg): the
+// host runs the sweep only then, and a step that leaves that range stops
+// the sweep (ST_REFINE) so the host finishes the cycle on k_ccd.
+
+// experiment hooks (build_native(variant=...))
+#ifndef RCD_DEN_EARLY
+#define RCD_DEN_EARLY 0 // heads' denominator loads before (1) or after (0) the products
+#endif
+#ifndef RCD_GH_FLAT
+#define RCD_GH_FLAT 0 // grad/hess terms of all heads without branches (divisions overlap)
+#endif
+#ifndef RCD_OVF_PREFETCH
+#define RCD_OVF_PREFETCH 1 // 16-B loads of drugs 9..16 issued before the inline products
+#endif
+
+// CTA shape of this instantiation: RS_THREADS threads (warp 0 the control
+// warp), RS_TILES pair slots per data thread.  These shadow the k_ccd shape
+// (kT, kD, kWarps and the slot mapping) inside this namespace.
+constexpr int kT = RS_THREADS;
+constexpr int kD = kT - 32;
+constexpr int kWarps = kT / 32;
+static_assert(kT % 32 == 0 && kT >= 64, "CTA shape");
+__device__ __forceinline__ int data_warp() {
+    const int w = static_cast<int>(threadIdx.x) >> 5;
+    constexpr int kMates = (kWarps - 1) / 4; // warps 4, 8, ...: warp 0's scheduler mates take the last data ranks
+    if ((w & 3) == 0) return (kWarps - 1 - kMates) + (w >> 2) - 1;
+    return w - (w >> 2) - 1;
+}
+__device__ __forceinline__ int data_tid() { return data_warp() * 32 + (static_cast<int>(threadIdx.x) & 31); }
+__device__ __forceinline__ int slot_pos(int v) { return v * kD + data_tid(); }
+
+constexpr int kRT = RS_TILES;
+constexpr int kRC = kRT * kD; // pairs a CTA stages per coordinate (largest slice this instantiation runs)
+constexpr int kRBufs = 3;     // record buffers: coordinate idx, idx+1 (speculated), idx+2 (in flight)
+
+struct RSmem {
+    double stage[kRC];  // l*exp (grad/hess) or fresh - old (update), per pair slot
+    int ssub[2][kRC];   // subject per slot, by coordinate parity (the repair searches the previous slice)
+    double jden[kRC];   // no subject tile: the denominator each head of the previous update wrote
+    double ra[kWarps], rb[kWarps];
+    int re[kWarps];
+    double delta, bnew, enew;
+    int status;
+    unsigned long long bar[kRBufs]; // mbarriers of the record buffers
+    unsigned long long cbar[2];     // mbarriers of the criterion chunk buffers
+    int wscan[kWarps];              // block scan of the criterion's per-thread era offsets
+};
+constexpr size_t kRSmemBytes = (sizeof(RSmem) + 127) / 128 * 128;
+constexpr size_t kRBufBytes = static_cast<size_t>(kRC) * sizeof(RRec);
+
+// CTA reduction of (a, b, e); result in every lane of warp 0 (fixed order)
+__device__ __forceinline__ void block_reduce_r(double& a, double& b, int& e, bool idle, RSmem& sm) {
+    if (!idle) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            a = __dadd_rn(a, __shfl_xor_sync(0xffffffffu, a, o));
+            b = __dadd_rn(b, __shfl_xor_sync(0xffffffffu, b, o));
+        }
+    } else {
+        a = 0.0;
+        b = 0.0;
+    }
+    e = __reduce_or_sync(0xffffffffu, e);
+    if (lane_id() == 0) {
+        sm.ra[warp_id()] = a;
+        sm.rb[warp_id()] = b;
+        sm.re[warp_id()] = e;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double x = 0.0, y = 0.0;
+        int z = 0;
+#pragma unroll
+        for (int i = 0; i < kWarps; ++i) {
+            x = __dadd_rn(x, sm.ra[i]);
+            y = __dadd_rn(y, sm.rb[i]);
+            z |= sm.re[i];
+        }
+        a = x;
+        b = y;
+        e = z;
+    }
+}
+
+__device__ __forceinline__ bool r_slot_valid(int v, int n) { return slot_pos(v) < n && threadIdx.x >= 32; }
+
+// Per-thread state of one coordinate's slots: the rebuilt x'beta and its
+// l*exp, the head's denominator (no subject tile), and the record fields
+// the later phases need.
+struct RSpec {
+    double pre[kRT], le[kRT], den[kRT]; // pre: product of E over the era's other drugs
+    int ls[kRT], len[kRT], n[kRT], ovf[kRT];
+    unsigned head; // bit v: slot v starts a subject run
+    unsigned dep;  // bit v: the era also holds the coordinate visited just before (its x'beta waits for that step)
+};
+
+// exp(x'beta) of a pair without its own drug: the product of E over the
+// era's other drugs in ascending order (the inline ones, then the overflow
+// list); dep: one of them is `jdep`
+__device__ __forceinline__ double r_pre(const RRec& r, const double* se, const uint16_t* __restrict__ rovf, int jdep,
+                                        bool& dep) {
+    const int cnt = r.meta & 0xff;
+    double p = 1.0;
+    dep = false;
+    for (int i = 0; i < cnt; ++i) {
+        const int d = i < kRInline ? r.o[i] : __ldg(rovf + r.ovf + (i - kRInline));
+        p = __dmul_rn(p, se[d]);
+        dep = dep || d == jdep;
+    }
+    return p;
+}
+
+// The coordinate `jn` (records in `rb`, n pairs) speculated while the
+// previous coordinate's partials travel: every slot's product of E over the
+// era's other drugs (the slots' chains interleaved; the drugs past the 8
+// inline ones through the scalar r_pre), l*exp(x'beta) = l * (pre * E_jn),
+// run heads, and (no subject tile) the heads' denominators.  dep marks the
+// eras that also hold `jprev`, whose step is still in flight.
+template <bool kSS>
+__device__ __forceinline__ void r_speculate(const RRec* rb, int n, int jn, int jprev, const double* se,
+                                            const uint16_t* __restrict__ rovf, const double* __restrict__ denc,
+                                            int subj_base, uint64_t pol_keep, RSpec& P) {
+    uint32_t w[kRT][4];
+    int cnt[kRT];
+    P.dep = 0u;
+    bool any_ovf = false;
+#pragma unroll
+    for (int v = 0; v < kRT; ++v) {
+        const bool ok = r_slot_valid(v, n);
+        const uint4* q = reinterpret_cast<const uint4*>(rb + slot_pos(v));
+        const uint4 a = ok ? q[0] : make_uint4(0xffffffffu, 0, 0, 0);
+        const uint4 o = ok ? q[1] : make_uint4(0, 0, 0, 0);
+        P.ls[v] = static_cast<int>(a.x);
+        P.len[v] = static_cast<int>(a.y);
+        cnt[v] = static_cast<int>(a.z & 0xffu);
+        P.n[v] = static_cast<int>(a.z >> 16);
+        w[v][0] = o.x;
+        w[v][1] = o.y;
+        w[v][2] = o.z;
+        w[v][3] = o.w;
+        P.pre[v] = 1.0;
+        any_ovf = any_ovf || cnt[v] > kRInline;
+        if (cnt[v] > kRInline) P.ovf[v] = static_cast<int>(a.w);
+    }
+    // run heads (the subject changes from the previous pair; lane 0 reads it)
+    P.head = 0u;
+#pragma unroll
+    for (int v = 0; v < kRT; ++v) {
+        const int pos = slot_pos(v);
+        int prev = __shfl_up_sync(0xffffffffu, P.ls[v], 1);
+        if (lane_id() == 0) prev = pos > 0 && pos < n ? rb[pos - 1].ls : -1;
+        if (r_slot_valid(v, n) && (pos == 0 || prev != P.ls[v])) P.head |= 1u << v;
+    }
+#if RCD_DEN_EARLY
+    if constexpr (!kSS) {
+#pragma unroll
+        for (int v = 0; v < kRT; ++v)
+            if ((P.head >> v) & 1u) P.den[v] = ld_keep(denc + subj_base + P.ls[v], pol_keep);
+    }
+#endif
+    // drugs 9..16 of eras with more than 8 others: one 16-B load each, in
+    // flight while the inline products run
+    uint4 ov[kRT];
+    if (RCD_OVF_PREFETCH && any_ovf) {
+#pragma unroll
+        for (int v = 0; v < kRT; ++v)
+            if (cnt[v] > kRInline) ov[v] = __ldg(reinterpret_cast<const uint4*>(rovf + P.ovf[v]));
+    }
+#pragma unroll
+    for (int i = 0; i < kRInline; ++i) {
+#pragma unroll
+        for (int v = 0; v < kRT; ++v) {
+            if (i < cnt[v]) {
+                const int d = static_cast<int>((w[v][i >> 1] >> (16 * (i & 1))) & 0xffffu);
+                P.pre[v] = __dmul_rn(P.pre[v], se[d]);
+                if (d == jprev) P.dep |= 1u << v;
+            }
+        }
+    }
+    if (any_ovf) { // rare
+#pragma unroll
+        for (int v = 0; v < kRT; ++v) {
+            if (cnt[v] <= kRInline) continue;
+            if (!RCD_OVF_PREFETCH) ov[v] = __ldg(reinterpret_cast<const uint4*>(rovf + P.ovf[v]));
+            const uint32_t x[4] = {ov[v].x, ov[v].y, ov[v].z, ov[v].w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (kRInline + i < cnt[v]) {
+                    const int d = static_cast<int>((x[i >> 1] >> (16 * (i & 1))) & 0xffffu);
+                    P.pre[v] = __dmul_rn(P.pre[v], se[d]);
+                    if (d == jprev) P.dep |= 1u << v;
+                }
+            }
+            for (int i = kRInline + 8; i < cnt[v]; ++i) { // more than 16 other drugs
+                const int d = __ldg(rovf + P.ovf[v] + (i - kRInline));
+                P.pre[v] = __dmul_rn(P.pre[v], se[d]);
+                if (d == jprev) P.dep |= 1u << v;
+            }
+        }
+    }
+    const double ej = se[jn];
+#pragma unroll
+    for (int v = 0; v < kRT; ++v) P.le[v] = __dmul_rn(__dmul_rn(P.pre[v], ej), static_cast<double>(P.len[v]));
+#if !RCD_DEN_EARLY
+    if constexpr (!kSS) {
+#pragma unroll
+        for (int v = 0; v < kRT; ++v)
+            if ((P.head >> v) & 1u) P.den[v] = ld_keep(denc + subj_base + P.ls[v], pol_keep);
+    }
+#endif
+}
+
+template <bool kSS>
+__global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs A) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    RSmem& sm = *reinterpret_cast<RSmem*>(smem_raw);
+    // dynamic shared memory: RSmem | beta | exp(beta) | union { the sweep:
+    // record buffers, subject tile or bitmaps ; the criterion: beta at
+    // cycle start, two chunk buffers }
+    double* sb = reinterpret_cast<double*>(smem_raw + kRSmemBytes);
+    double* se = sb + A.beta_cap;
+    unsigned char* uni = smem_raw + kRSmemBytes + 2 * static_cast<size_t>(A.beta_cap) * sizeof(double);
+    RRec* rbuf = reinterpret_cast<RRec*>(uni);
+    double* tile = reinterpret_cast<double*>(uni + kRBufs * kRBufBytes); // subject tile (kSS) or bitmaps (!kSS)
+    int si = 0;
+    while (si + 1 < A.nsh && static_cast<int>(blockIdx.x) >= A.sh[si + 1].cta_begin) ++si;
+    const ShardArgs& S = A.sh[si];
+    const int c = static_cast<int>(blockIdx.x) - S.cta_begin;
+    const int tid = static_cast<int>(threadIdx.x);
+    const bool w0 = tid < 32;
+    const bool issuer = tid == 32; // stages the record buffers (a data thread: warp 0 polls)
+    unsigned long long seq = *S.xcounter;
+    int err = 0;
+    double errv = 0.0;
+    XPrev pv{0ull, 0ull, 0ull, 0ull};
+    xprev_load(S, pv);
+    const uint64_t pol_stream = policy_evict_first();
+    const uint64_t pol_keep = policy_evict_last();
+    const int subj_base = S.cta_subj[c];
+    const int nsubj = S.cta_subj[c + 1] - subj_base;
+    unsigned* bm0 = reinterpret_cast<unsigned*>(tile);
+    unsigned* bm1 = bm0 + A.bm_words;
+
+    // beta into shared memory; the CTA's denominators into the tile
+    for (int j = tid; j < A.J; j += kT) {
+        const double b = S.beta[j];
+        sb[j] = b;
+        se[j] = exp(b);
+    }
+    if constexpr (kSS) {
+        for (int t = tid; t < nsubj; t += kT) tile[t] = S.denc[subj_base + t];
+    } else {
+        for (int i = tid; i < 2 * A.bm_words; i += kT) bm0[i] = 0u;
+    }
+    if (tid == 0) {
+        for (int b = 0; b < kRBufs; ++b) mbar_init(&sm.bar[b], 1);
+        for (int b = 0; b < 2; ++b) mbar_init(&sm.cbar[b], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    const int B0 = A.visit_begin;
+    const int V = A.nvisit - B0;
+    const longlong2* vs = S.vsplit + static_cast<size_t>(c) * static_cast<size_t>(A.nvisit) + B0;
+    const int32_t* visit = A.visit + B0;
+    long long nvisit = 0, nmoved = 0;
+    int refine_at = -1;
+    bool aborted = false;
+
+    // stage coordinate i's records into buffer i % 3 (one bulk copy; every
+    // use of a buffer completes exactly one phase of its mbarrier)
+    auto stage = [&](int i) {
+        const longlong2 sl = vs[i];
+        const unsigned bytes = static_cast<unsigned>((sl.y - sl.x) * static_cast<long long>(sizeof(RRec)));
+        unsigned long long* bar = &sm.bar[i % kRBufs];
+        fence_proxy_async();
+        mbar_arrive_tx(bar, bytes);
+        if (bytes) bulk_g2s(rbuf + static_cast<size_t>(i % kRBufs) * kRC, S.rq + sl.x, bytes, bar, pol_stream);
+    };
+    auto wait_records = [&](int i) { mbar_wait(&sm.bar[i % kRBufs], static_cast<unsigned>((i / kRBufs) & 1)); };
+
+    if (V > 0) {
+        if (issuer) {
+            stage(0);
+            if (V > 1) stage(1);
+        }
+        int j = visit[0];
+        double bj = 0.0, rj = 1.0, ydx = 0.0;
+        if (w0) {
+            bj = sb[j];
+            rj = S.trust[j];
+            ydx = A.y_dot_x[j];
+        }
+        RSpec P; // coordinate idx
+        RSpec Q; // coordinate idx+1, speculated during idx's window
+        int ncur = static_cast<int>(vs[0].y - vs[0].x);
+        if (!w0) {
+            wait_records(0);
+            r_speculate<kSS>(rbuf, ncur, j, -1, se, S.rovf, S.denc, subj_base, pol_keep, P);
+        }
+        bool moved_prev = false; // did coordinate idx-1 move (its x'beta / den repairs apply)
+        int nprev = 0;
+        // subjects whose touched bit the last update set (cleared one window later)
+        int clr_sub[kRT];
+        unsigned clr = 0u;
+        // profiling only: globaltimer stamps per coordinate (scripts/trace_sweep.py)
+        const size_t trs = static_cast<size_t>(gridDim.x) * kTr;
+        unsigned long long* trb =
+            (A.trace != nullptr && (tid == 0 || tid == 32)) ? A.trace + static_cast<size_t>(blockIdx.x) * kTr : nullptr;
+        for (int idx = 0; idx < V; ++idx) {
+            const RRec* rc = rbuf + static_cast<size_t>(idx % kRBufs) * kRC;
+            int* ssub = sm.ssub[idx & 1];
+            const bool tr = trb && idx < A.ntrace;
+            if (tr && tid == 0) trb[idx * trs + 0] = gtimer();
+            double gs = 0.0, hs = 0.0;
+            // ---- repair the speculated values, stage, run sums -------------
+            if (!w0) {
+                if (moved_prev) {
+                    const int* sprev = sm.ssub[(idx + 1) & 1];
+                    const unsigned* bmprev = (idx & 1) ? bm0 : bm1; // marks of coordinate idx-1
+#pragma unroll
+                    for (int v = 0; v < kRT; ++v) {
+                        if ((P.dep >> v) & 1u) { // the era also holds the previous coordinate's drug
+                            bool d;
+                            P.pre[v] = r_pre(rc[slot_pos(v)], se, S.rovf, -1, d);
+                            P.le[v] = __dmul_rn(__dmul_rn(P.pre[v], se[j]), static_cast<double>(P.len[v]));
+                        }
+                        if constexpr (!kSS) {
+                            if ((P.head >> v) & 1u) {
+                                const int s = P.ls[v];
+                                if ((bmprev[s >> 5] >> (s & 31)) & 1u) { // touched: its run head in the previous slice
+                                    int lo = 0, hi = nprev;
+                                    while (lo < hi) {
+                                        const int mid = (lo + hi) >> 1;
+                                        if (sprev[mid] < s) lo = mid + 1;
+                                        else hi = mid;
+                                    }
+                                    P.den[v] = sm.jden[lo];
+                                }
+                            }
+                        }
+                    }
+                }
+                if (tr && tid == 32) trb[idx * trs + 11] = gtimer();
+#pragma unroll
+                for (int v = 0; v < kRT; ++v) {
+                    if (r_slot_valid(v, ncur)) {
+                        sm.stage[slot_pos(v)] = P.le[v];
+                        ssub[slot_pos(v)] = P.ls[v];
+                    }
+                }
+            }
+            __syncthreads();
+            if (tr && tid == 32) trb[idx * trs + 12] = gtimer();
+#if !RCD_GH_FLAT
+            if (!w0) {
+#pragma unroll
+                for (int v = 0; v < kRT; ++v) {
+                    if (!((P.head >> v) & 1u)) continue;
+                    const int pos = slot_pos(v);
+                    const int s = P.ls[v];
+                    double num = P.le[v];
+                    int q = pos + 1;
+                    while (q < ncur && ssub[q] == s) num = __dadd_rn(num, sm.stage[q++]);
+                    run_terms(num, kSS ? tile[s] : P.den[v], P.n[v], gs, hs, err);
+                }
+            }
+#else
+            if (!w0) {
+                // run numerators (data-dependent loops) first, then every
+                // head's term without branches so the divisions overlap,
+                // then the sums in slot order
+                double num[kRT];
+#pragma unroll
+                for (int v = 0; v < kRT; ++v) {
+                    num[v] = P.le[v];
+                    if (!((P.head >> v) & 1u)) continue;
+                    int q = slot_pos(v) + 1;
+                    while (q < ncur && ssub[q] == P.ls[v]) num[v] = __dadd_rn(num[v], sm.stage[q++]);
+                }
+#pragma unroll
+                for (int v = 0; v < kRT; ++v) {
+                    const bool h = (P.head >> v) & 1u;
+                    const double den = h ? (kSS ? tile[P.ls[v]] : P.den[v]) : 1.0;
+                    double a = 0.0, b = 0.0;
+                    int e2 = 0;
+                    run_terms(h ? num[v] : 0.0, den, P.n[v], a, b, e2);
+                    if (h) {
+                        gs = __dadd_rn(gs, a);
+                        hs = __dadd_rn(hs, b);
+                        err |= e2;
+                    }
+                }
+            }
+#endif
+            if (tr && tid == 32) trb[idx * trs + 13] = gtimer() + (gs == 1.2345 ? 1 : 0);
+            if (err) record_error(S.err, err, errv);
+            int e = err | ((bj != bj) || (rj != rj) ? 1 : 0);
+            const bool idle = w0 || !__any_sync(0xffffffffu, slot_pos(0) < ncur);
+            block_reduce_r(gs, hs, e, idle, sm);
+            if (tr && tid == 0) trb[idx * trs + 1] = gtimer();
+            publish(A, S, c, seq, gs, hs, e, pv);
+            // ---- while the partials travel ------------------------------------
+            const bool more = idx + 1 < V;
+            const int jn = more ? visit[idx + 1] : 0;
+            const int nnext = more ? static_cast<int>(vs[idx + 1].y - vs[idx + 1].x) : 0;
+            if (!w0) {
+                if (issuer && idx + 2 < V) stage(idx + 2);
+                if constexpr (!kSS) { // the marks of idx-1 were read above: clear them for this update
+                    unsigned* b = (idx & 1) ? bm0 : bm1;
+#pragma unroll
+                    for (int v = 0; v < kRT; ++v)
+                        if ((clr >> v) & 1u) b[clr_sub[v] >> 5] = 0u;
+                    clr = 0u;
+                }
+                if (tr && tid == 32) trb[idx * trs + 14] = gtimer();
+                if (more) {
+                    wait_records(idx + 1);
+                    if (tr && tid == 32) trb[idx * trs + 15] = gtimer();
+                    r_speculate<kSS>(rbuf + static_cast<size_t>((idx + 1) % kRBufs) * kRC, nnext, jn, j, se, S.rovf,
+                                     S.denc, subj_base, pol_keep, Q);
+                }
+                if (tr && tid == 32) { // the stamp waits for the speculated values
+                    double dep = 0.0;
+#pragma unroll
+                    for (int v = 0; v < kRT; ++v) dep += r_slot_valid(v, nnext) ? Q.le[v] : 0.0;
+                    trb[idx * trs + 6] = gtimer() + (dep == 1.2345 ? 1 : 0);
+                }
+            } else {
+                double bn = 0.0, rn = 1.0, yn = 0.0;
+                if (more) {
+                    bn = sb[jn];
+                    rn = S.trust[jn];
+                    yn = A.y_dot_x[jn];
+                }
+                const double bv = beta_over_v(A.prior, bj);
+                double tg, th;
+                int te = 0;
+                unsigned inexact[2] = {0u, 0u};
+                if (tr && tid == 0) trb[idx * trs + 4] = gtimer();
+                poll<false>(A, S.xslots, seq, pv, tg, th, te, tr ? trb + idx * trs + 5 : nullptr, inexact);
+                int status = ST_OK;
+                double delta = 0.0;
+                if (te) {
+                    status = ST_REMOTE_ERR;
+                } else if ((inexact[0] | inexact[1]) &&
+                           (needs_refine(tg, inexact[0], 0) || needs_refine(th, inexact[1], 0))) {
+                    status = ST_REFINE; // the host finishes this coordinate (run_sweep)
+                } else {
+                    const double g = __dsub_rn(ydx, tg);
+                    const double h = th == 0.0 ? 0.0 : -th;
+                    double step = 0.0;
+                    const int serr = penalized_step_pre(A.prior, bj, bv, g, h, &step);
+                    if (serr) {
+                        status = ST_STEP_ERR;
+                        if (c == 0 && tid == 0) record_error(S.err, serr, h);
+                    } else {
+                        delta = clamp_step(step, rj);
+                        if (delta != 0.0 && !isfinite(delta)) {
+                            status = ST_NONFINITE;
+                            if (c == 0 && tid == 0) record_error(S.err, DERR_STEP_NONFINITE, delta);
+                        } else if (fabs(__dadd_rn(bj, delta)) > A.beta_limit) {
+                            status = ST_REFINE; // partial products could leave range: the host takes over
+                        }
+                    }
+                }
+                if (tid == 0) {
+                    const double bnew = __dadd_rn(bj, delta);
+                    sm.delta = delta;
+                    sm.bnew = bnew;
+                    sm.enew = exp(bnew);
+                    sm.status = status;
+                    if (c == 0 && status == ST_OK) {
+                        S.moved[B0 + idx] = delta != 0.0 ? 1 : 0;
+                        S.beta[j] = __dadd_rn(bj, delta);
+                        S.trust[j] = next_trust(delta, rj);
+                    }
+                }
+                bj = bn;
+                rj = rn;
+                ydx = yn;
+                if (tr && tid == 0) trb[idx * trs + 7] = gtimer();
+            }
+            ++seq;
+            __syncthreads();
+            if (tr && tid == 0) trb[idx * trs + 2] = gtimer();
+            const int status = sm.status;
+            const double delta = sm.delta;
+            if (status != ST_OK) {
+                aborted = true;
+                // a bulk copy still in flight must land before the CTA exits
+                if (issuer && idx + 2 < V) wait_records(idx + 2);
+                if (status == ST_REMOTE_ERR && c == 0 && tid == 0) S.res->err_remote = 1;
+                if (status == ST_REFINE) refine_at = B0 + idx;
+                break;
+            }
+            ++nvisit;
+            moved_prev = delta != 0.0;
+            if (moved_prev) {
+                ++nmoved;
+                // beta_j in shared memory (the window's readers are past the
+                // barrier; the update below does not read beta)
+                const double enew = sm.enew;
+                if (tid == 0) {
+                    sb[j] = sm.bnew;
+                    se[j] = enew;
+                }
+                // ---- sparse update (engine.hpp:205-231): updated = x'beta + delta,
+                // fresh = l*exp(updated), den += fresh - old in pair order
+                if (!w0) {
+                    double diff[kRT];
+#pragma unroll
+                    for (int v = 0; v < kRT; ++v) {
+                        const double x = __dmul_rn(P.pre[v], enew); // exp(x'beta + delta)
+                        diff[v] = 0.0;
+                        if (!r_slot_valid(v, ncur)) continue;
+                        if (!(x >= kExpXbMin && x <= kExpXbMax)) { // |x'beta + delta| > 700
+                            err = DERR_OVERFLOW;
+                            errv = fabs(log(x));
+                        } else {
+                            diff[v] = __dsub_rn(__dmul_rn(x, static_cast<double>(P.len[v])), P.le[v]);
+                        }
+                    }
+                    if (tr && tid == 32) trb[idx * trs + 8] = gtimer() + (diff[0] == 1.2345 ? 1 : 0);
+#pragma unroll
+                    for (int v = 0; v < kRT; ++v)
+                        if (r_slot_valid(v, ncur)) sm.stage[slot_pos(v)] = diff[v];
+                }
+                __syncthreads();
+                if (tr && tid == 32) trb[idx * trs + 9] = gtimer();
+                if (!w0) {
+                    unsigned* bmcur = (idx & 1) ? bm1 : bm0;
+                    double den[kRT];
+#pragma unroll
+                    for (int v = 0; v < kRT; ++v) { // run sums for every head first ...
+                        if (!((P.head >> v) & 1u)) continue;
+                        const int pos = slot_pos(v);
+                        const int s = P.ls[v];
+                        double dv = __dadd_rn(kSS ? tile[s] : P.den[v], sm.stage[pos]);
+                        int q = pos + 1;
+                        while (q < ncur && ssub[q] == s) dv = __dadd_rn(dv, sm.stage[q++]);
+                        den[v] = dv;
+                    }
+#pragma unroll
+                    for (int v = 0; v < kRT; ++v) { // ... then the stores
+                        if (!((P.head >> v) & 1u)) continue;
+                        const int s = P.ls[v];
+                        if constexpr (kSS) {
+                            tile[s] = den[v];
+                        } else {
+                            st_keep(S.denc + subj_base + s, den[v], pol_keep);
+                            sm.jden[slot_pos(v)] = den[v];
+                            atomicOr(&bmcur[s >> 5], 1u << (s & 31));
+                            clr_sub[v] = s;
+                        }
+                    }
+                    if constexpr (!kSS) clr = P.head;
+                    if (tr && tid == 32) trb[idx * trs + 10] = gtimer();
+                }
+            }
+            __syncthreads(); // slice writes of this coordinate before the next reads
+            if (tr && tid == 0) trb[idx * trs + 3] = gtimer();
+            P = Q;
+            nprev = ncur;
+            ncur = nnext;
+            j = jn;
+        }
+        if constexpr (kSS) { // the cycle's denominators back to HBM (ordered by the loop's last barrier)
+            for (int t = tid; t < nsubj; t += kT) S.denc[subj_base + t] = tile[t];
+        }
+    }
+
+    if (!aborted) {
+        // criterion (solver.hpp:154-165): |x'beta - snapshot| over the CTA's
+        // eras, both sides rebuilt from beta (now: sb; cycle start: sbp).
+        // The eras' drug lists stream through two chunk buffers (bulk
+        // copies of the degrees and drugs of A.crit_E eras, one chunk ahead);
+        // each thread sums crit_E / kT consecutive eras.
+        double ch = 0.0, mg = 0.0;
+        const int e0 = S.cta_era[c], e1 = S.cta_era[c + 1];
+        const int E = A.crit_E, cap = A.crit_cap, eper = E / kT;
+        double* sbp = reinterpret_cast<double*>(uni);
+        uint8_t* dbuf = reinterpret_cast<uint8_t*>(sbp + A.beta_cap);         // [2][E + 32]
+        uint16_t* cbuf = reinterpret_cast<uint16_t*>(dbuf + 2 * (E + 32));     // [2][cap + 16]
+        __syncthreads(); // the sweep's last readers of the union region are done
+        for (int jj = tid; jj < A.J; jj += kT) sbp[jj] = S.beta_prev[jj];
+        const int nch = (e1 - e0 + E - 1) / E;
+        // chunk i: eras [a, b), drugs [ca, cb); staged when they fit the buffer
+        auto crit_stage = [&](int i) {
+            const int a = e0 + i * E, b = min(e1, a + E);
+            const int64_t ca = S.csr_ptr[a], cb = S.csr_ptr[b];
+            const int a16 = a & ~15, b16 = (b + 15) & ~15;
+            const int64_t ca8 = ca & ~7ll, cb8 = (cb + 7) & ~7ll;
+            unsigned long long* bar = &sm.cbar[i & 1];
+            fence_proxy_async();
+            const bool fits = cb8 - ca8 <= cap;
+            const unsigned bytes = static_cast<unsigned>(b16 - a16) + (fits ? static_cast<unsigned>(2 * (cb8 - ca8)) : 0u);
+            mbar_arrive_tx(bar, bytes);
+            bulk_g2s(dbuf + (i & 1) * (E + 32), S.edeg + a16, static_cast<unsigned>(b16 - a16), bar, pol_stream);
+            if (fits) bulk_g2s(cbuf + (i & 1) * (cap + 16), S.ecol + ca8, static_cast<unsigned>(2 * (cb8 - ca8)), bar,
+                               pol_stream);
+        };
+        if (tid == 0) {
+            if (nch > 0) crit_stage(0);
+            if (nch > 1) crit_stage(1);
+        }
+        __syncthreads(); // sbp
+        for (int i = 0; i < nch; ++i) {
+            const int a = e0 + i * E, b = min(e1, a + E);
+            const int64_t ca = S.csr_ptr[a];
+            const int64_t cb = S.csr_ptr[b];
+            const bool fits = ((cb + 7) & ~7ll) - (ca & ~7ll) <= cap;
+            mbar_wait(&sm.cbar[i & 1], static_cast<unsigned>((i >> 1) & 1));
+            const uint8_t* dg = dbuf + (i & 1) * (E + 32) + (a - (a & ~15));
+            const uint16_t* cl = cbuf + (i & 1) * (cap + 16) + (ca - (ca & ~7ll));
+            // this thread's eras [k0, k1) of the chunk and their first drug
+            const int k0 = min(b - a, tid * eper), k1 = min(b - a, k0 + eper);
+            int tot = 0;
+            for (int k = k0; k < k1; ++k) tot += dg[k];
+            int incl = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane_id() >= o) incl += y;
+            }
+            if (lane_id() == 31) sm.wscan[warp_id()] = incl;
+            __syncthreads();
+            int wbase = 0;
+            for (int w = 0; w < warp_id(); ++w) wbase += sm.wscan[w];
+            int off = wbase + incl - tot;
+            for (int k = k0; k < k1; ++k) {
+                const int deg = dg[k];
+                double xn = 0.0, xo = 0.0;
+                for (int q = 0; q < deg; ++q) {
+                    const int d = fits ? cl[off + q] : __ldg(S.ecol + ca + off + q);
+                    xn = __dadd_rn(xn, sb[d]);
+                    xo = __dadd_rn(xo, sbp[d]);
+                }
+                off += deg;
+                ch = __dadd_rn(ch, fabs(__dsub_rn(xn, xo)));
+                if (A.normalized) mg = __dadd_rn(mg, fabs(xn));
+            }
+            __syncthreads(); // the chunk buffer and wscan are free again
+            if (tid == 0 && i + 2 < nch) crit_stage(i + 2);
+        }
+        if (err) record_error(S.err, err, errv);
+        int e = err;
+        block_reduce_r(ch, mg, e, false, sm);
+        publish(A, S, c, seq, ch, mg, e, pv);
+        if (w0) {
+            double tch, tmg;
+            int te;
+            poll(A, S.xslots, seq, pv, tch, tmg, te, nullptr);
+            if (c == 0 && tid == 0) {
+                S.res->change = tch;
+                S.res->magnitude = tmg;
+                S.res->criterion = A.normalized ? tch / (1.0 + tmg) : tch;
+                S.res->err_remote = te;
+            }
+        }
+        ++seq;
+    }
+    if (err) record_error(S.err, err, errv);
+    if (c == 0 && tid == 0) {
+        S.res->visited = nvisit;
+        S.res->moved = nmoved;
+        S.res->counter = seq;
+        S.res->refine_at = refine_at;
+        if (S.xowner) *S.xcounter = seq;
+    }
+    if (c == 0 && S.xowner) xprev_store(S, pv);
+}

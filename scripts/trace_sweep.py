@@ -24,11 +24,12 @@ B.run_cycle(dds, st, solver, prior, cfg)  # warm
 lib.bsccs_debug_set_sweep_flags(flags)
 lib.bsccs_debug_trace(NT, ctas, None, 0)
 B.run_cycle(dds, st, solver, prior, cfg)
-buf = np.zeros(NT * ctas * 8, dtype=np.uint64)
+KT = 16  # stamps per CTA and coordinate (ccd_kernels.cu kTr)
+buf = np.zeros(NT * ctas * KT, dtype=np.uint64)
 lib.bsccs_debug_trace(NT, ctas, buf.ctypes.data_as(C.c_void_p), buf.size)
 lib.bsccs_debug_trace(0, ctas, None, 0)
 lib.bsccs_debug_set_sweep_flags(0)
-t = buf.reshape(NT, ctas, 8).astype(np.int64)
+t = buf.reshape(NT, ctas, KT).astype(np.int64)
 if per_coord:  # first coordinates in visit order (fixed order: j = 0, 1, ...): the head columns of a skewed set
     full = t[:NT - 1, 0, 0]
     nnz = np.diff(ds.col_ptr)
@@ -73,3 +74,22 @@ print(f"  poll done -> step computed (warp 0): median {np.median(stp - poll):.0f
 print(f"  poll done -> data warp 1 at barrier: median {np.median(dat - poll):.0f}  "
       f"(publish -> data warp at barrier {np.median(dat - pub):.0f})")
 print(f"  data warp at barrier -> released: median {np.median(got - dat):.0f}")
+
+if t[:, :, 12].any():  # resident-beta sweep: data warp 1 phase stamps (k_rcd)
+    def ph(a, b, label):
+        d = t[:, :, b] - t[:, :, a]
+        ok = (t[:, :, a] > 0) & (t[:, :, b] > 0)
+        if ok.any():
+            dm = np.where(ok, d, 0)
+            print(f"  [warp 1] {label}: median {np.median(d[ok]):.0f}  max-over-CTAs median {np.median(dm.max(1)):.0f} ns")
+    ph(0, 11, "top -> repaired")
+    ph(11, 12, "repaired -> gh staged (barrier)")
+    ph(12, 13, "gh staged -> run terms done")
+    ph(13, 1, "run terms -> reduced (tid 0)")
+    ph(1, 14, "publish -> window issued")
+    ph(14, 15, "wait records of idx+1")
+    ph(15, 6, "speculate idx+1")
+    ph(2, 8, "step barrier -> update diffs")
+    ph(8, 9, "diffs -> staged (barrier)")
+    ph(9, 10, "staged -> heads done")
+    ph(10, 3, "heads done -> end barrier")
