@@ -663,11 +663,18 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+#ifndef RCD_DEN_CG
+#define RCD_DEN_CG 0 // experiment hook: the heads' denominator loads bypass L1
+#endif
 __device__ __forceinline__ double ld_keep(const double* p, uint64_t pol) {
     double v;
     // volatile (issued where written, in the speculative window, not sunk to
     // the first use) but no memory clobber: the other loads stay free to move
+#if RCD_DEN_CG
+    asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+#else
     asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+#endif
     return v;
 }
 __device__ __forceinline__ void st_keep(double* p, double v, uint64_t pol) {
@@ -690,6 +697,10 @@ namespace t1 {
 #ifndef RS_WIDE_THREADS
 #define RS_WIDE_THREADS 512
 #endif
+#ifndef RS_WIDE_TILES
+#define RS_WIDE_TILES 2
+#endif
+
 namespace r1 {
 #define RS_TILES 1
 #define RS_THREADS 384
@@ -698,7 +709,7 @@ namespace r1 {
 #undef RS_TILES
 } // namespace r1
 namespace r2 {
-#define RS_TILES 2
+#define RS_TILES RS_WIDE_TILES
 #define RS_THREADS RS_WIDE_THREADS
 #include "rsweep.cuh"
 #undef RS_THREADS

@@ -38,6 +38,12 @@
 #ifndef RCD_GH_FLAT
 #define RCD_GH_FLAT 0 // grad/hess terms of all heads without branches (divisions overlap)
 #endif
+#ifndef RCD_TRACE
+#define RCD_TRACE 0 // globaltimer phase stamps (scripts/trace_sweep.py builds the variant with 1)
+#endif
+#ifndef RCD_DIAG_NODEN
+#define RCD_DIAG_NODEN 0
+#endif
 #ifndef RCD_OVF_PREFETCH
 #define RCD_OVF_PREFETCH 1 // 16-B loads of drugs 9..16 issued before the inline products
 #endif
@@ -234,7 +240,11 @@ __device__ __forceinline__ void r_speculate(const RRec* rb, int n, int jn, int j
     if constexpr (!kSS) {
 #pragma unroll
         for (int v = 0; v < kRT; ++v)
+#if RCD_DIAG_NODEN // diagnostic only (wrong results): no denominator gathers
+            if ((P.head >> v) & 1u) P.den[v] = 20.0 * P.le[v];
+#else
             if ((P.head >> v) & 1u) P.den[v] = ld_keep(denc + subj_base + P.ls[v], pol_keep);
+#endif
     }
 #endif
 }
@@ -323,6 +333,7 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
         RSpec P; // coordinate idx
         RSpec Q; // coordinate idx+1, speculated during idx's window
         int ncur = static_cast<int>(vs[0].y - vs[0].x);
+        int nn1 = V > 1 ? static_cast<int>(vs[1].y - vs[1].x) : 0; // slice length of idx+1 (loaded a window ahead)
         if (!w0) {
             wait_records(0);
             r_speculate<kSS>(rbuf, ncur, j, -1, se, S.rovf, S.denc, subj_base, pol_keep, P);
@@ -334,12 +345,13 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
         unsigned clr = 0u;
         // profiling only: globaltimer stamps per coordinate (scripts/trace_sweep.py)
         const size_t trs = static_cast<size_t>(gridDim.x) * kTr;
-        unsigned long long* trb =
-            (A.trace != nullptr && (tid == 0 || tid == 32)) ? A.trace + static_cast<size_t>(blockIdx.x) * kTr : nullptr;
+        unsigned long long* trb = (RCD_TRACE && A.trace != nullptr && (tid == 0 || tid == 32))
+                                      ? A.trace + static_cast<size_t>(blockIdx.x) * kTr
+                                      : nullptr;
         for (int idx = 0; idx < V; ++idx) {
             const RRec* rc = rbuf + static_cast<size_t>(idx % kRBufs) * kRC;
             int* ssub = sm.ssub[idx & 1];
-            const bool tr = trb && idx < A.ntrace;
+            const bool tr = RCD_TRACE && trb && idx < A.ntrace;
             if (tr && tid == 0) trb[idx * trs + 0] = gtimer();
             double gs = 0.0, hs = 0.0;
             // ---- repair the speculated values, stage, run sums -------------
@@ -432,7 +444,8 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
             // ---- while the partials travel ------------------------------------
             const bool more = idx + 1 < V;
             const int jn = more ? visit[idx + 1] : 0;
-            const int nnext = more ? static_cast<int>(vs[idx + 1].y - vs[idx + 1].x) : 0;
+            const int nnext = nn1;
+            nn1 = idx + 2 < V ? static_cast<int>(vs[idx + 2].y - vs[idx + 2].x) : 0;
             if (!w0) {
                 if (issuer && idx + 2 < V) stage(idx + 2);
                 if constexpr (!kSS) { // the marks of idx-1 were read above: clear them for this update

@@ -6,6 +6,11 @@ from pathlib import Path
 import numpy as np
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import os  # noqa: E402
+if "BSCCS_B200_LIB" not in os.environ:  # the resident-beta sweep stamps only in the RCD_TRACE=1 variant
+    # (build_native(variant={"RCD_TRACE": 1}) makes it; set before the package loads its library)
+    os.environ["BSCCS_B200_LIB"] = str(Path(__file__).resolve().parents[1] / "paper_1208_0945_b200" / "_lib" /
+                                       "libbsccs_b200_rcdtrace1.so")
 from paper_1208_0945_b200 import _native, bsccs as B, datagen  # noqa: E402
 
 wl = sys.argv[1] if len(sys.argv) > 1 else "1M"
