@@ -112,6 +112,14 @@ void bsccs_debug_set_sweep_flags(int32_t flags);
 /* Profiling hook: host_out == NULL arms per-CTA globaltimer stamps for the
  * first ncoords coordinates of later sweeps; otherwise copies them out. */
 int32_t bsccs_debug_trace(int32_t ncoords, int32_t ctas, uint64_t* host_out, int64_t words);
+/* Test hooks, not reference entry points.  Sweep kernel for later cycles:
+ * 0 automatic (the resident-beta sweep k_rcd when the dataset qualifies,
+ * else k_ccd), 1 always k_ccd.  beta_limit > 0 lowers the |beta_j| bound
+ * above which k_rcd hands the cycle to k_ccd (0 = the automatic
+ * 700 / largest era).  bsccs_debug_last_sweep: kernel of the last cycle's
+ * launches, 1 = k_ccd only, 2 = k_rcd only, 3 = both (handed over). */
+void bsccs_debug_set_sweep(int32_t kind, double beta_limit);
+int32_t bsccs_debug_last_sweep(void);
 /* Self-test of the exact all-reduce encoding, not a
  * reference entry point: n (<= 2048) partials in [0, 2^43) are split into
  * limbs and added into one set of exchange words on `device` exactly as n

@@ -1397,6 +1397,10 @@ bool rcd_enabled() {
     return on;
 }
 
+std::atomic<int> g_sweep_kind{0};       // tests: 1 forces k_ccd
+std::atomic<double> g_beta_limit{0.0};  // tests: lower k_rcd's |beta| bound
+std::atomic<int> g_last_sweep{0};
+
 // Small pinned result blocks for the per-state D2H of kernel scalars.
 struct PinnedResults {
     std::mutex m;
@@ -2230,7 +2234,7 @@ struct RcdShape {
 };
 RcdShape rcd_shape(const ExchangePlan& plan) {
     RcdShape r;
-    if (!rcd_enabled()) return r;
+    if (!rcd_enabled() || g_sweep_kind.load() == 1) return r;
     int maxslice = 0, maxsub = 0, maxdeg = 1;
     for (auto* st : plan.shards) {
         if (!st->ds->rq || !st->ds->edeg || !st->denc) return r;
@@ -2239,6 +2243,7 @@ RcdShape rcd_shape(const ExchangePlan& plan) {
         maxdeg = std::max(maxdeg, st->ds->max_deg);
     }
     r.beta_limit = 700.0 / maxdeg;
+    if (g_beta_limit.load() > 0.0) r.beta_limit = std::min(r.beta_limit, g_beta_limit.load());
     static const int tiles_forced = [] {
         const char* e = std::getenv("BSCCS_RTILES"); // experiment hook: 1, 2 or 3
         return e ? std::atoi(e) : 0;
@@ -2469,6 +2474,11 @@ void debug_exchange_sum(int device, const double* partials, int n, double* sum, 
 }
 
 void set_debug_flags(int f) { g_debug_flags = f; }
+void set_debug_sweep(int kind, double beta_limit) {
+    g_sweep_kind = kind;
+    g_beta_limit = beta_limit;
+}
+int debug_last_sweep() { return g_last_sweep; }
 void set_debug_trace(int ncoords, int ctas) {
     if (g_trace) cudaFree(g_trace);
     g_trace = nullptr;
@@ -2612,6 +2622,7 @@ SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool 
         return true;
     };
     bool use_rcd = rcd.ok && beta_in_range();
+    int kinds = 0; // 1: k_ccd launched, 2: k_rcd launched
     for (auto* st : plan.shards) {
         if (use_rcd) { // compact denominators current; beta at the start of the cycle for the criterion
             sync_denc(st);
@@ -2659,9 +2670,11 @@ SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool 
                                                  params, 0, s0->stream));
             count_launches(1);
         } else if (use_rcd) {
+            kinds |= 2;
             launch_rcd(plan, a, rcd);
             for (auto* st : plan.shards) st->x_stale = true;
         } else {
+            kinds |= 1;
             launch_ccd(plan, a);
         }
         for (size_t i = 0; i < plan.shards.size(); ++i) {
@@ -2700,6 +2713,7 @@ SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool 
         begin = ra + 1;
     }
     CUDA_TRY(cudaEventRecord(s0->ev1, s0->stream));
+    g_last_sweep = kinds;
     std::vector<uint8_t> moved(visit.size());
     if (!visit.empty())
         CUDA_TRY(cudaMemcpyAsync(moved.data(), s0->moved, visit.size(), cudaMemcpyDeviceToHost, s0->stream));

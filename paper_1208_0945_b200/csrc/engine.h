@@ -269,6 +269,8 @@ SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool 
 void plan_allreduce(const ExchangePlan& plan, double a, double b, double* ta, double* tb);
 void prepare_snapshot(bsccs_state* st);
 void set_debug_flags(int flags); // profiling only
+void set_debug_sweep(int kind, double beta_limit); // tests only (bsccs_debug_set_sweep)
+int debug_last_sweep();
 void set_debug_trace(int ncoords, int ctas);
 void read_debug_trace(unsigned long long* host, size_t words);
 void debug_exchange_sum(int device, const double* partials, int n, double* sum, int* status);
