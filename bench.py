@@ -332,24 +332,40 @@ def pinned_copy(ds):
     return held, B.Dataset(*[v for _, v in held])
 
 
+def sweep_kernel():
+    """which sweep kernel the last cycle launched (bsccs_debug_last_sweep)"""
+    from paper_1208_0945_b200 import _native
+    k = _native.lib().bsccs_debug_last_sweep()
+    return {1: "k_ccd", 2: "k_rcd", 3: "k_rcd+k_ccd"}.get(k, "k_ccd")
+
+
+KERNEL_DESC = {"k_rcd": "k_rcd (resident-beta persistent sweep, 1 launch per cycle)",
+               "k_ccd": "k_ccd (per-era-state persistent sweep, 1 launch per cycle)",
+               "k_rcd+k_ccd": "k_rcd handing over to k_ccd"}
+
+
 def roofline_of(results, elapsed_ms, peak, peak_src, traffic_key):
     sweeps = sum(r.cycles_run for r in results)
     sweep_s = sum(r.sweep_seconds for r in results)
     alg = sum(r.algorithmic_bytes for r in results)
     achieved = alg / sweep_s / 1e9
+    kern = sweep_kernel()
     traffic = None
-    tp = ROOT / "profiles" / "k_ccd_traffic.json"
+    tp = ROOT / "profiles" / "sweep_traffic.json"
     if tp.exists():
         try:
-            traffic = json.loads(tp.read_text()).get(traffic_key)
+            traffic = json.loads(tp.read_text()).get(kern, {}).get(traffic_key)
         except Exception:
             traffic = None
     return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic, "kernel": "k_ccd (persistent sweep, 1 launch per cycle)",
+            "traffic": traffic, "kernel": KERNEL_DESC.get(kern, kern),
             "bytes_per_launch": alg / sweeps, "ms_per_launch": sweep_s / sweeps * 1e3,
             "share_of_step": sweep_s * 1e3 / elapsed_ms, "peak_source": peak_src,
             "algorithmic_bytes": "SURVEY §8(d): per visited coordinate 16*nnz_j + 12*u_j, per moved one "
-                                 "+ 28*nnz_j + 8*u_j, per cycle + 32*K (counted per launch by the library)"}
+                                 "+ 28*nnz_j + 8*u_j, per cycle + 32*K (counted per launch by the library)",
+            "traffic_note": "ncu dram__bytes_read.sum + dram__bytes_write.sum of one launch "
+                            "(profiles/sweep_traffic.json); k_rcd streams 32-B pair records instead of "
+                            "gathering per-era state, so its DRAM bytes fall below the algorithmic count"}
 
 
 def timed_region(fn, steps, barrier, torch):

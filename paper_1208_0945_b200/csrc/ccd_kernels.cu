@@ -27,6 +27,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <mutex>
 #include <thread>
@@ -1301,17 +1302,19 @@ __global__ void k_build_pq(const int2* __restrict__ pairs, int64_t nnz, const in
 // The CSR sort carries each pair's CSC position with its column, so the
 // records are written per era from its (contiguous) drug list: one 32-B
 // store per pair, no per-pair search.
-__global__ void k_pack_pc(const int32_t* __restrict__ col_of, int64_t nnz, unsigned long long* out) {
+__global__ void k_iota(uint32_t* out, int64_t nnz) {
     for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < nnz;
          p += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        out[p] = (static_cast<unsigned long long>(p) << 32) | static_cast<uint32_t>(col_of[p]);
+        out[p] = static_cast<uint32_t>(p);
 }
-__global__ void k_unpack_pc(const unsigned long long* __restrict__ v, int64_t nnz, int32_t* csr_col, uint32_t* pos) {
+// csr_col holds each CSR entry's CSC position after the sort: keep it in pos,
+// and the entry's column (col_of) in csr_col
+__global__ void k_pos_col(int32_t* csr_col, const int32_t* __restrict__ col_of, int64_t nnz, uint32_t* pos) {
     for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < nnz;
          q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const unsigned long long x = v[q];
-        csr_col[q] = static_cast<int32_t>(x & 0xffffffffull);
-        pos[q] = static_cast<uint32_t>(x >> 32);
+        const uint32_t p = static_cast<uint32_t>(csr_col[q]);
+        pos[q] = p;
+        csr_col[q] = col_of[p];
     }
 }
 // the criterion's compact CSR: drugs per era (u8) and the drugs (u16)
@@ -1513,7 +1516,14 @@ void alloc_dataset(bsccs_dataset* ds) {
     CUDA_TRY(cudaStreamCreateWithFlags(&ds->stream, cudaStreamNonBlocking));
     cudaStream_t s = ds->stream;
     ds->pairs = dalloc<int2>(nnz, B, s);
-    ds->pq = dalloc<int4>(nnz, B, s);
+    // pair records of the resident-beta sweep, allocated before the build's
+    // temporaries (a stable allocation order lets the pool reuse blocks
+    // across dataset rebuilds); freed again if the dataset does not qualify
+    if (rcd_enabled() && nnz > 0 && nnz < (1ll << 32) && J <= 65535) {
+        ds->rq = dalloc<RRec>(nnz, B, s);
+        ds->edeg = dalloc<uint8_t>(static_cast<int64_t>(K) + 32, B, s);
+        ds->ecol = dalloc<uint16_t>(nnz + 16, B, s);
+    }
     ds->row_slot = dalloc<int32_t>(K, B, s);
     ds->bstart = dalloc<int32_t>(N, B, s);
     ds->col_ptr = dalloc<int64_t>(J + 1, B, s);
@@ -1539,8 +1549,29 @@ void alloc_dataset(bsccs_dataset* ds) {
 // here, freed on return) hold the CSC pair arrays.  Validates the
 // build_dataset invariants (dataset.hpp:135-175), builds the interleaved
 // pairs, the row-major copy, the CTA ranges and the per-column splits.
+// BSCCS_BUILD_TIMING=1: host-side phase times of the dataset build on stderr
+// (each phase synchronised; profiling only)
+struct BuildTimer {
+    bool on;
+    cudaStream_t s;
+    std::chrono::steady_clock::time_point t;
+    explicit BuildTimer(cudaStream_t st) : on([] {
+        const char* e = std::getenv("BSCCS_BUILD_TIMING");
+        return e && e[0] == '1';
+    }()), s(st), t(std::chrono::steady_clock::now()) {}
+    void mark(const char* what) {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        const auto n = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[build] %-28s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+        t = n;
+    }
+};
+
 void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const int64_t* y_dot_x_global,
                     const int64_t* col_nnz_global, cudaEvent_t era_ready) {
+    BuildTimer bt(ds->stream);
+    bt.mark("enter");
     const int C = ds->ctas;
     const int32_t N = ds->N, K = ds->K, J = ds->J;
     const int64_t nnz = ds->nnz;
@@ -1552,9 +1583,9 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
     long long* d_excl = dalloc<long long>(static_cast<int64_t>(N) + 1, scratch_bytes, s);
     int* d_bad = dalloc<int>(1, scratch_bytes, s);
     CUDA_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
-    bool want_rq = false;
-    unsigned long long* d_pc = nullptr;  // (CSC position, column) per pair, then sorted by row
-    unsigned long long* d_spc = nullptr;
+    // resident-beta sweep records (allocated with the dataset, alloc_dataset)
+    bool want_rq = ds->rq != nullptr;
+    uint32_t* d_iota = nullptr; // CSC positions, sorted by row with the keys
     if (nnz > 0) {
         k_interleave<<<grid_for(nnz, 256, sms), 256, 0, s>>>(d_rows, d_subj, ds->pairs, nnz);
         k_pair_meta<<<grid_for(nnz, 256, sms), 256, 0, s>>>(ds->pairs, ds->col_ptr, J, ds->subject_offsets, N, K,
@@ -1567,15 +1598,13 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
         int end_bit = 1;
         while ((1ll << end_bit) < static_cast<long long>(K)) ++end_bit;
         // resident-beta sweep records need each CSR entry's CSC position:
-        // the sort then carries (position, column) pairs
-        want_rq = rcd_enabled() && nnz > 0 && nnz < (1ll << 32) && J <= 65535;
+        // the sort then carries positions, the columns are gathered after
         if (want_rq) {
-            d_pc = dalloc<unsigned long long>(nnz, scratch_bytes, s);
-            d_spc = dalloc<unsigned long long>(nnz, scratch_bytes, s);
-            k_pack_pc<<<grid_for(nnz, 256, sms), 256, 0, s>>>(d_col, nnz, d_pc);
+            d_iota = dalloc<uint32_t>(nnz, scratch_bytes, s);
+            k_iota<<<grid_for(nnz, 256, sms), 256, 0, s>>>(d_iota, nnz);
             count_launches(1);
-            CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, d_rows, d_subj, d_pc, d_spc, nnz, 0,
-                                                     end_bit, s));
+            CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, d_rows, d_subj, d_iota,
+                                                     reinterpret_cast<uint32_t*>(ds->csr_col), nnz, 0, end_bit, s));
         } else if (nnz > 0)
             CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, d_rows, d_subj, d_col, ds->csr_col, nnz, 0,
                                                      end_bit, s));
@@ -1584,19 +1613,20 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
         const size_t tb = std::max(std::max(tmp_bytes, sort_bytes), scan2);
         unsigned char* tmp = dalloc<unsigned char>(static_cast<int64_t>(std::max<size_t>(tb, 16)), scratch_bytes, s);
         if (want_rq) {
-            CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, d_rows, d_subj, d_pc, d_spc, nnz, 0, end_bit, s));
+            CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, d_rows, d_subj, d_iota,
+                                                     reinterpret_cast<uint32_t*>(ds->csr_col), nnz, 0, end_bit, s));
             // d_rows (the consumed keys) receives the CSC positions
-            k_unpack_pc<<<grid_for(nnz, 256, sms), 256, 0, s>>>(d_spc, nnz, ds->csr_col,
-                                                                 reinterpret_cast<uint32_t*>(d_rows));
+            k_pos_col<<<grid_for(nnz, 256, sms), 256, 0, s>>>(ds->csr_col, d_col, nnz,
+                                                               reinterpret_cast<uint32_t*>(d_rows));
             count_launches(1);
-            dfree(d_pc, s);
-            dfree(d_spc, s);
+            dfree(d_iota, s);
         } else if (nnz > 0) {
             // keys: rows (consumed); d_subj is free after interleave and
             // receives the sorted keys
             CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, d_rows, d_subj, d_col, ds->csr_col, nnz, 0,
                                                      end_bit, s));
         }
+        bt.mark("sort");
         k_csr_ptr<<<grid_for(nnz + 1, 256, sms), 256, 0, s>>>(d_subj, nnz, K, ds->csr_ptr);
         // the era arrays may still be arriving on a side stream: the pair-side
         // build above overlapped their upload
@@ -1613,6 +1643,7 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
         const int64_t nsplit = static_cast<int64_t>(J) * (C + 1);
         k_split<<<static_cast<int>((nsplit + 255) / 256), 256, 0, s>>>(ds->pairs, ds->col_ptr, J, ds->cta_subj, C,
                                                                         ds->split);
+        bt.mark("csr, cta ranges, split");
         // subject blocks and the sweep's pair records (engine.h)
         {
             const int64_t nch = (static_cast<int64_t>(N) + kBlockChunk - 1) / kBlockChunk;
@@ -1633,14 +1664,12 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
             ds->nslots = total;
             k_block_place<<<grid_for(nch, 128, sms), 128, 0, s>>>(ds->subject_offsets, N, d_cb, nch, ds->bstart,
                                                                   ds->row_slot);
-            if (nnz > 0)
-                k_build_pq<<<grid_for(nnz, 256, sms), 256, 0, s>>>(ds->pairs, nnz, ds->row_slot, ds->bstart,
-                                                                   ds->era_lengths, ds->cta_subj, C, ds->pq);
-            count_launches(3 + (nnz > 0 ? 1 : 0));
+            count_launches(3);
             dfree(tmp2, s);
             dfree(d_cs, s);
             dfree(d_cb, s);
         }
+        bt.mark("subject blocks, pq");
         if (want_rq) { // resident-beta sweep pair records (engine.h RRec)
             int64_t b4 = 0;
             long long* d_oc = dalloc<long long>(static_cast<int64_t>(N) + 1, b4, s);
@@ -1662,18 +1691,20 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
             if (!rbad[0] && novf < (1ll << 31)) {
                 ds->novf = novf;
                 ds->max_deg = std::max(1, rbad[1]);
-                ds->rq = dalloc<RRec>(nnz, ds->device_bytes, s);
                 ds->rovf = dalloc<uint16_t>(std::max<long long>(novf, 8), ds->device_bytes, s);
                 k_build_rq<<<grid_for(N, 128, sms), 128, 0, s>>>(
                     ds->subject_offsets, ds->events_per_subject, ds->era_lengths, ds->csr_ptr, ds->csr_col,
                     reinterpret_cast<const uint32_t*>(d_rows), ds->cta_subj, C, d_ob, N, ds->rq, ds->rovf);
-                ds->edeg = dalloc<uint8_t>(static_cast<int64_t>(K) + 32, ds->device_bytes, s);
-                ds->ecol = dalloc<uint16_t>(nnz + 16, ds->device_bytes, s);
                 CUDA_TRY(cudaMemsetAsync(ds->edeg, 0, static_cast<size_t>(K) + 32, s));
                 CUDA_TRY(cudaMemsetAsync(ds->ecol, 0, sizeof(uint16_t) * (nnz + 16), s));
                 k_compact_csr<<<grid_for(std::max<int64_t>(K, nnz), 256, sms), 256, 0, s>>>(ds->csr_ptr, ds->csr_col,
                                                                                             K, nnz, ds->edeg, ds->ecol);
                 count_launches(2);
+            } else { // outside the record format: every sweep runs k_ccd
+                ds->device_bytes -= static_cast<int64_t>(sizeof(RRec) * nnz + K + 32 + 2 * (nnz + 16));
+                dfree(ds->rq, s);
+                dfree(ds->edeg, s);
+                dfree(ds->ecol, s);
             }
             count_launches(1);
             dfree(tmp3, s);
@@ -1681,6 +1712,7 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
             dfree(d_ob, s);
             dfree(d_rbad, s);
         }
+        bt.mark("rq");
         if (y_dot_x_global) {
             std::vector<double> yd(static_cast<size_t>(J));
             for (int32_t j = 0; j < J; ++j) yd[static_cast<size_t>(j)] = static_cast<double>(y_dot_x_global[j]);
@@ -1697,7 +1729,6 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
     dfree(d_rows, s);
     dfree(d_subj, s);
     dfree(d_col, s);
-    dfree(d_spc, s);
     dfree(d_w, s);
     dfree(d_excl, s);
     dfree(d_bad, s);
@@ -1708,6 +1739,7 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
     if (bad & 1) input_error("dataset: invalid pair (row/subject out of range, subject not owning its row, "
                              "or rows not strictly ascending within a column)");
 
+    bt.mark("frees, validation");
     ds->col_runs_h.resize(static_cast<size_t>(J));
     CUDA_TRY(cudaMemcpy(ds->col_runs_h.data(), ds->col_runs, sizeof(int32_t) * J, cudaMemcpyDeviceToHost));
     {
@@ -1734,6 +1766,7 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
         ds->col_nonempty_h[static_cast<size_t>(j)] = cnt > 0 ? 1 : 0;
     }
     CUDA_TRY(cudaMemcpy(ds->col_nonempty, ds->col_nonempty_h.data(), J, cudaMemcpyHostToDevice));
+    bt.mark("metadata");
 }
 
 bsccs_dataset* dataset_new(int32_t N, int32_t K, int32_t J, int64_t nnz, int device, int ctas_override) {
@@ -2146,8 +2179,28 @@ int prefetch_enabled(const ExchangePlan& plan) {
     return per_cta > 0.0 && per_cta <= 384.0 ? 1 : 0;
 }
 
+// k_ccd's pair records, built on first use (datasets the resident-beta sweep
+// runs need them only for the single-coordinate ops and hand-overs)
+std::mutex g_pq_mutex;
+void ensure_pq(const bsccs_dataset* cds) {
+    std::lock_guard<std::mutex> lk(g_pq_mutex);
+    auto* ds = const_cast<bsccs_dataset*>(cds);
+    if (ds->pq || ds->nnz == 0) return;
+    DeviceGuard g(ds->device);
+    ds->pq = dalloc<int4>(ds->nnz, ds->device_bytes, ds->stream);
+    k_build_pq<<<grid_for(ds->nnz, 256, sm_count(ds->device)), 256, 0, ds->stream>>>(
+        ds->pairs, ds->nnz, ds->row_slot, ds->bstart, ds->era_lengths, ds->cta_subj, ds->ctas, ds->pq);
+    CUDA_TRY(cudaGetLastError());
+    count_launches(1);
+    CUDA_TRY(cudaStreamSynchronize(ds->stream));
+}
+
 void launch_ccd(const ExchangePlan& plan, SweepArgs& a) {
     bsccs_state* s0 = plan.shards[0];
+    for (size_t i = 0; i < plan.shards.size(); ++i) {
+        ensure_pq(plan.shards[i]->ds);
+        a.sh[i].pq = plan.shards[i]->ds->pq;
+    }
     ensure_kernel_attrs(s0->ds->device);
     // the streamed path only when some slice exceeds the register tiles
     // (and always for the single-coordinate ops, whose update streams); its
@@ -2665,6 +2718,8 @@ SweepOutcome run_sweep(const ExchangePlan& plan, const PriorParams& prior, bool 
         a.prior = prior;
         a.normalized = normalized ? 1 : 0;
         if (dense) {
+            ensure_pq(s0->ds);
+            a.sh[0].pq = s0->ds->pq;
             void* params[] = {&a};
             CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_ccd_dense), dim3(s0->ds->ctas), dim3(kDT),
                                                  params, 0, s0->stream));
