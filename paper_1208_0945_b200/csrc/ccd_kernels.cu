@@ -1350,7 +1350,7 @@ __global__ void k_build_rq(const int32_t* __restrict__ off, const int32_t* __res
                            const int32_t* __restrict__ len, const int64_t* __restrict__ csr_ptr,
                            const int32_t* __restrict__ csr_col, const uint32_t* __restrict__ pos,
                            const int32_t* __restrict__ cta_subj, int C, const long long* __restrict__ ovb, int32_t N,
-                           RRec* rq, uint16_t* rovf) {
+                           int32_t J, RRec* rq, uint16_t* rovf) {
     for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < N;
          s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         int lo = 0, hi = C + 1; // first c with cta_subj[c] > s
@@ -1379,10 +1379,10 @@ __global__ void k_build_rq(const int32_t* __restrict__ off, const int32_t* __res
                     else rovf[ov + (i - kRInline)] = d;
                     ++i;
                 }
-                for (; i < kRInline; ++i) r.o[i] = 0xffff;
+                for (; i < kRInline; ++i) r.o[i] = static_cast<uint16_t>(J); // the unit drug: exp(beta) = 1
                 if (deg - 1 > kRInline) { // pad the overflow list to a multiple of 8 (one 16-B load per 8)
                     const int ext = (deg - 1 - kRInline + 7) & ~7;
-                    for (int t = deg - 1 - kRInline; t < ext; ++t) rovf[ov + t] = 0xffff;
+                    for (int t = deg - 1 - kRInline; t < ext; ++t) rovf[ov + t] = static_cast<uint16_t>(J);
                     ov += ext;
                 }
                 rq[pos[q0 + a]] = r;
@@ -1519,7 +1519,7 @@ void alloc_dataset(bsccs_dataset* ds) {
     // pair records of the resident-beta sweep, allocated before the build's
     // temporaries (a stable allocation order lets the pool reuse blocks
     // across dataset rebuilds); freed again if the dataset does not qualify
-    if (rcd_enabled() && nnz > 0 && nnz < (1ll << 32) && J <= 65535) {
+    if (rcd_enabled() && nnz > 0 && nnz < (1ll << 32) && J < 65535) { // u16 drugs, index J the unit drug
         ds->rq = dalloc<RRec>(nnz, B, s);
         ds->edeg = dalloc<uint8_t>(static_cast<int64_t>(K) + 32, B, s);
         ds->ecol = dalloc<uint16_t>(nnz + 16, B, s);
@@ -1694,7 +1694,7 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
                 ds->rovf = dalloc<uint16_t>(std::max<long long>(novf, 8), ds->device_bytes, s);
                 k_build_rq<<<grid_for(N, 128, sms), 128, 0, s>>>(
                     ds->subject_offsets, ds->events_per_subject, ds->era_lengths, ds->csr_ptr, ds->csr_col,
-                    reinterpret_cast<const uint32_t*>(d_rows), ds->cta_subj, C, d_ob, N, ds->rq, ds->rovf);
+                    reinterpret_cast<const uint32_t*>(d_rows), ds->cta_subj, C, d_ob, N, J, ds->rq, ds->rovf);
                 CUDA_TRY(cudaMemsetAsync(ds->edeg, 0, static_cast<size_t>(K) + 32, s));
                 CUDA_TRY(cudaMemsetAsync(ds->ecol, 0, sizeof(uint16_t) * (nnz + 16), s));
                 k_compact_csr<<<grid_for(std::max<int64_t>(K, nnz), 256, sms), 256, 0, s>>>(ds->csr_ptr, ds->csr_col,
@@ -2312,7 +2312,7 @@ RcdShape rcd_shape(const ExchangePlan& plan) {
     } else {
         return r;
     }
-    r.beta_cap = (plan.shards[0]->ds->J + 15) / 16 * 16;
+    r.beta_cap = (plan.shards[0]->ds->J + 1 + 15) / 16 * 16; // + the unit drug J
     const size_t head = smem_fixed + 2 * static_cast<size_t>(r.beta_cap) * sizeof(double);
     const size_t base = head + bufs;
     static const bool tile_on = [] {

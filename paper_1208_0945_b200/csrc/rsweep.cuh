@@ -152,19 +152,20 @@ __device__ __forceinline__ double r_pre(const RRec& r, const double* se, const u
 // run heads, and (no subject tile) the heads' denominators.  dep marks the
 // eras that also hold `jprev`, whose step is still in flight.
 template <bool kSS>
-__device__ __forceinline__ void r_speculate(const RRec* rb, int n, int jn, int jprev, const double* se,
+__device__ __forceinline__ void r_speculate(const RRec* rb, int n, int jn, int jprev, int junit, const double* se,
                                             const uint16_t* __restrict__ rovf, const double* __restrict__ denc,
                                             int subj_base, uint64_t pol_keep, RSpec& P) {
     uint32_t w[kRT][4];
     int cnt[kRT];
     P.dep = 0u;
     bool any_ovf = false;
+    const uint32_t unit2 = static_cast<uint32_t>(junit) * 0x10001u; // two unit drugs (padding)
 #pragma unroll
     for (int v = 0; v < kRT; ++v) {
         const bool ok = r_slot_valid(v, n);
         const uint4* q = reinterpret_cast<const uint4*>(rb + slot_pos(v));
         const uint4 a = ok ? q[0] : make_uint4(0xffffffffu, 0, 0, 0);
-        const uint4 o = ok ? q[1] : make_uint4(0, 0, 0, 0);
+        const uint4 o = ok ? q[1] : make_uint4(unit2, unit2, unit2, unit2);
         P.ls[v] = static_cast<int>(a.x);
         P.len[v] = static_cast<int>(a.y);
         cnt[v] = static_cast<int>(a.z & 0xffu);
@@ -201,6 +202,8 @@ __device__ __forceinline__ void r_speculate(const RRec* rb, int n, int jn, int j
         for (int v = 0; v < kRT; ++v)
             if (cnt[v] > kRInline) ov[v] = __ldg(reinterpret_cast<const uint4*>(rovf + P.ovf[v]));
     }
+    // the inline drugs (predicated: padding lanes issue no shared-memory
+    // load -- measured faster than multiplying the unit drug's E = 1)
 #pragma unroll
     for (int i = 0; i < kRInline; ++i) {
 #pragma unroll
@@ -208,8 +211,21 @@ __device__ __forceinline__ void r_speculate(const RRec* rb, int n, int jn, int j
             if (i < cnt[v]) {
                 const int d = static_cast<int>((w[v][i >> 1] >> (16 * (i & 1))) & 0xffffu);
                 P.pre[v] = __dmul_rn(P.pre[v], se[d]);
-                if (d == jprev) P.dep |= 1u << v;
             }
+        }
+    }
+    // eras holding jprev: a zero 16-bit lane of (drugs ^ jprev), two per word
+    if (jprev >= 0) {
+        const uint32_t jj = static_cast<uint32_t>(jprev) * 0x10001u;
+#pragma unroll
+        for (int v = 0; v < kRT; ++v) {
+            uint32_t z = 0u;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t x = w[v][k] ^ jj;
+                z |= (x - 0x00010001u) & ~x & 0x80008000u;
+            }
+            if (z) P.dep |= 1u << v;
         }
     }
     if (any_ovf) { // rare
@@ -219,12 +235,10 @@ __device__ __forceinline__ void r_speculate(const RRec* rb, int n, int jn, int j
             if (!RCD_OVF_PREFETCH) ov[v] = __ldg(reinterpret_cast<const uint4*>(rovf + P.ovf[v]));
             const uint32_t x[4] = {ov[v].x, ov[v].y, ov[v].z, ov[v].w};
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                if (kRInline + i < cnt[v]) {
-                    const int d = static_cast<int>((x[i >> 1] >> (16 * (i & 1))) & 0xffffu);
-                    P.pre[v] = __dmul_rn(P.pre[v], se[d]);
-                    if (d == jprev) P.dep |= 1u << v;
-                }
+            for (int i = 0; i < 8; ++i) { // padded with the unit drug as well
+                const int d = static_cast<int>((x[i >> 1] >> (16 * (i & 1))) & 0xffffu);
+                P.pre[v] = __dmul_rn(P.pre[v], se[d]);
+                if (d == jprev) P.dep |= 1u << v;
             }
             for (int i = kRInline + 8; i < cnt[v]; ++i) { // more than 16 other drugs
                 const int d = __ldg(rovf + P.ovf[v] + (i - kRInline));
@@ -286,6 +300,7 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
         sb[j] = b;
         se[j] = exp(b);
     }
+    if (tid == 0) se[A.J] = 1.0; // the unit drug (record padding)
     if constexpr (kSS) {
         for (int t = tid; t < nsubj; t += kT) tile[t] = S.denc[subj_base + t];
     } else {
@@ -336,7 +351,7 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
         int nn1 = V > 1 ? static_cast<int>(vs[1].y - vs[1].x) : 0; // slice length of idx+1 (loaded a window ahead)
         if (!w0) {
             wait_records(0);
-            r_speculate<kSS>(rbuf, ncur, j, -1, se, S.rovf, S.denc, subj_base, pol_keep, P);
+            r_speculate<kSS>(rbuf, ncur, j, -1, A.J, se, S.rovf, S.denc, subj_base, pol_keep, P);
         }
         bool moved_prev = false; // did coordinate idx-1 move (its x'beta / den repairs apply)
         int nprev = 0;
@@ -459,7 +474,7 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
                 if (more) {
                     wait_records(idx + 1);
                     if (tr && tid == 32) trb[idx * trs + 15] = gtimer();
-                    r_speculate<kSS>(rbuf + static_cast<size_t>((idx + 1) % kRBufs) * kRC, nnext, jn, j, se, S.rovf,
+                    r_speculate<kSS>(rbuf + static_cast<size_t>((idx + 1) % kRBufs) * kRC, nnext, jn, j, A.J, se, S.rovf,
                                      S.denc, subj_base, pol_keep, Q);
                 }
                 if (tr && tid == 32) { // the stamp waits for the speculated values
@@ -614,7 +629,8 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
 
     if (!aborted) {
         // criterion (solver.hpp:154-165): |x'beta - snapshot| over the CTA's
-        // eras, both sides rebuilt from beta (now: sb; cycle start: sbp).
+        // eras -- x'beta at the end minus x'beta at the start of the cycle,
+        // taken as the sum of the era's coefficient changes (sbp).
         // The eras' drug lists stream through two chunk buffers (bulk
         // copies of the degrees and drugs of A.crit_E eras, one chunk ahead);
         // each thread sums crit_E / kT consecutive eras.
@@ -625,7 +641,9 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
         uint8_t* dbuf = reinterpret_cast<uint8_t*>(sbp + A.beta_cap);         // [2][E + 32]
         uint16_t* cbuf = reinterpret_cast<uint16_t*>(dbuf + 2 * (E + 32));     // [2][cap + 16]
         __syncthreads(); // the sweep's last readers of the union region are done
-        for (int jj = tid; jj < A.J; jj += kT) sbp[jj] = S.beta_prev[jj];
+        // the cycle's change of each coefficient: an era's x'beta change is
+        // their sum over its drugs (ascending, like x'beta itself)
+        for (int jj = tid; jj < A.J; jj += kT) sbp[jj] = __dsub_rn(sb[jj], S.beta_prev[jj]);
         const int nch = (e1 - e0 + E - 1) / E;
         // chunk i: eras [a, b), drugs [ca, cb); staged when they fit the buffer
         auto crit_stage = [&](int i) {
@@ -670,17 +688,30 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
             int wbase = 0;
             for (int w = 0; w < warp_id(); ++w) wbase += sm.wscan[w];
             int off = wbase + incl - tot;
-            for (int k = k0; k < k1; ++k) {
-                const int deg = dg[k];
-                double xn = 0.0, xo = 0.0;
-                for (int q = 0; q < deg; ++q) {
-                    const int d = fits ? cl[off + q] : __ldg(S.ecol + ca + off + q);
-                    xn = __dadd_rn(xn, sb[d]);
-                    xo = __dadd_rn(xo, sbp[d]);
+            if (!A.normalized) {
+                for (int k = k0; k < k1; ++k) {
+                    const int deg = dg[k];
+                    double dx = 0.0;
+                    for (int q = 0; q < deg; ++q) {
+                        const int d = fits ? cl[off + q] : __ldg(S.ecol + ca + off + q);
+                        dx = __dadd_rn(dx, sbp[d]);
+                    }
+                    off += deg;
+                    ch = __dadd_rn(ch, fabs(dx));
                 }
-                off += deg;
-                ch = __dadd_rn(ch, fabs(__dsub_rn(xn, xo)));
-                if (A.normalized) mg = __dadd_rn(mg, fabs(xn));
+            } else { // normalized: also |x'beta| (solver.hpp:159-161)
+                for (int k = k0; k < k1; ++k) {
+                    const int deg = dg[k];
+                    double dx = 0.0, xn = 0.0;
+                    for (int q = 0; q < deg; ++q) {
+                        const int d = fits ? cl[off + q] : __ldg(S.ecol + ca + off + q);
+                        dx = __dadd_rn(dx, sbp[d]);
+                        xn = __dadd_rn(xn, sb[d]);
+                    }
+                    off += deg;
+                    ch = __dadd_rn(ch, fabs(dx));
+                    mg = __dadd_rn(mg, fabs(xn));
+                }
             }
             __syncthreads(); // the chunk buffer and wscan are free again
             if (tid == 0 && i + 2 < nch) crit_stage(i + 2);
