@@ -8,11 +8,21 @@ import numpy as np
 import ctypes as C
 from paper_1208_0945_b200 import _native, bootstrap as BT, bsccs as B, cross_validation as CV, datagen, sharding
 
+set_sweep = _native.lib().bsccs_debug_set_sweep
 ds = datagen.fast_sccs(3000, 20, 3.0)
 dds = ds.on_device()
-r = B.fit(dds, B.laplace_prior(0.1))
-few = B.DeviceDataset(ds, 0, 2)  # two CTAs: slices beyond the register tiles take the streamed path
+r = B.fit(dds, B.laplace_prior(0.1))  # k_rcd, subject tile
+set_sweep(0, 0.05)
+B.fit(dds, B.normal_prior(2.0))  # k_rcd handing cycles over to k_ccd (lowered range bound)
+set_sweep(0, 0.0)
+big = datagen.fast_sccs(50000, 1500, 3.0)
+bdd = B.DeviceDataset(big, 0, 2)  # k_rcd without the subject tile (touched-subject bitmaps), 2 CTAs
+B.fit(bdd, B.laplace_prior(0.1), B.SolverConfig(max_cycles=2))
+bdd.close()
+few = B.DeviceDataset(ds, 0, 2)  # two CTAs: k_ccd's slices beyond the register tiles take the streamed path
+set_sweep(1, 0.0)
 B.fit(few, B.laplace_prior(0.1))
+set_sweep(0, 0.0)
 stf = B.init_state(few)
 B.fused_grad_hess(few, stf, 1)
 B.sparse_delta_update(few, stf, 1, 0.05)
