@@ -38,6 +38,9 @@
 #ifndef RCD_GH_FLAT
 #define RCD_GH_FLAT 0 // grad/hess terms of all heads without branches (divisions overlap)
 #endif
+#ifndef RCD_GH_WINDOW
+#define RCD_GH_WINDOW 0 // subject-tile shapes: the next coordinate's run terms formed in the window (measured slower)
+#endif
 #ifndef RCD_TRACE
 #define RCD_TRACE 0 // globaltimer phase stamps (scripts/trace_sweep.py builds the variant with 1)
 #endif
@@ -70,6 +73,7 @@ constexpr int kRBufs = 3;     // record buffers: coordinate idx, idx+1 (speculat
 
 struct RSmem {
     double stage[kRC];  // l*exp (grad/hess) or fresh - old (update), per pair slot
+    double stage2[kRC]; // l*exp of the next coordinate, staged in the window (run terms formed there)
     int ssub[2][kRC];   // subject per slot, by coordinate parity (the repair searches the previous slice)
     double jden[kRC];   // no subject tile: the denominator each head of the previous update wrote
     double ra[kWarps], rb[kWarps];
@@ -79,6 +83,7 @@ struct RSmem {
     unsigned long long bar[kRBufs]; // mbarriers of the record buffers
     unsigned long long cbar[2];     // mbarriers of the criterion chunk buffers
     int wscan[kWarps];              // block scan of the criterion's per-thread era offsets
+    XPrev xpv[32];                  // warp 0: the exchange's running totals per lane between uses
 };
 constexpr size_t kRSmemBytes = (sizeof(RSmem) + 127) / 128 * 128;
 constexpr size_t kRBufBytes = static_cast<size_t>(kRC) * sizeof(RRec);
@@ -127,6 +132,12 @@ struct RSpec {
     int ls[kRT], len[kRT], n[kRT], ovf[kRT];
     unsigned head; // bit v: slot v starts a subject run
     unsigned dep;  // bit v: the era also holds the coordinate visited just before (its x'beta waits for that step)
+};
+// ... plus the run terms formed in the window (subject-tile shapes): the
+// run's numerator, the denominator used, (n w, n w (1 - w)), runs of one pair
+struct RSpecG : RSpec {
+    double num[kRT], dn[kRT], ta[kRT], tb[kRT];
+    unsigned single;
 };
 
 // exp(x'beta) of a pair without its own drug: the product of E over the
@@ -265,6 +276,7 @@ __device__ __forceinline__ void r_speculate(const RRec* rb, int n, int jn, int j
 
 template <bool kSS>
 __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs A) {
+    constexpr bool kGW = kSS && RCD_GH_WINDOW && kRT == 1; // run terms formed in the window
     extern __shared__ __align__(128) unsigned char smem_raw[];
     RSmem& sm = *reinterpret_cast<RSmem*>(smem_raw);
     // dynamic shared memory: RSmem | beta | exp(beta) | union { the sweep:
@@ -285,8 +297,13 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
     unsigned long long seq = *S.xcounter;
     int err = 0;
     double errv = 0.0;
-    XPrev pv{0ull, 0ull, 0ull, 0ull};
-    xprev_load(S, pv);
+    // the exchange's running totals live in shared memory between uses (warp
+    // 0 only): registers held through the data warps' phases cost a spill
+    if (w0) {
+        XPrev pv{0ull, 0ull, 0ull, 0ull};
+        xprev_load(S, pv);
+        sm.xpv[tid] = pv;
+    }
     const uint64_t pol_stream = policy_evict_first();
     const uint64_t pol_keep = policy_evict_last();
     const int subj_base = S.cta_subj[c];
@@ -345,13 +362,43 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
             rj = S.trust[j];
             ydx = A.y_dot_x[j];
         }
-        RSpec P; // coordinate idx
-        RSpec Q; // coordinate idx+1, speculated during idx's window
+        using Spec = typename std::conditional<kGW, RSpecG, RSpec>::type;
+        Spec P; // coordinate idx
+        Spec Q; // coordinate idx+1, speculated during idx's window
         int ncur = static_cast<int>(vs[0].y - vs[0].x);
         int nn1 = V > 1 ? static_cast<int>(vs[1].y - vs[1].x) : 0; // slice length of idx+1 (loaded a window ahead)
         if (!w0) {
             wait_records(0);
             r_speculate<kSS>(rbuf, ncur, j, -1, A.J, se, S.rovf, S.denc, subj_base, pol_keep, P);
+        }
+        if constexpr (kGW) { // the first coordinate's run terms (the later ones come from the window)
+            int* ss0 = sm.ssub[0];
+            if (!w0) {
+#pragma unroll
+                for (int v = 0; v < kRT; ++v)
+                    if (r_slot_valid(v, ncur)) {
+                        sm.stage2[slot_pos(v)] = P.le[v];
+                        ss0[slot_pos(v)] = P.ls[v];
+                    }
+            }
+            __syncthreads();
+            if (!w0) {
+                P.single = 0u;
+#pragma unroll
+                for (int v = 0; v < kRT; ++v) {
+                    if (!((P.head >> v) & 1u)) continue;
+                    const int pos = slot_pos(v);
+                    double num = P.le[v];
+                    int q = pos + 1;
+                    while (q < ncur && ss0[q] == P.ls[v]) num = __dadd_rn(num, sm.stage2[q++]);
+                    if (q == pos + 1) P.single |= 1u << v;
+                    P.num[v] = num;
+                    P.dn[v] = tile[P.ls[v]];
+                    P.ta[v] = 0.0;
+                    P.tb[v] = 0.0;
+                    run_terms(num, P.dn[v], P.n[v], P.ta[v], P.tb[v], err);
+                }
+            }
         }
         bool moved_prev = false; // did coordinate idx-1 move (its x'beta / den repairs apply)
         int nprev = 0;
@@ -370,8 +417,55 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
             if (tr && tid == 0) trb[idx * trs + 0] = gtimer();
             double gs = 0.0, hs = 0.0;
             // ---- repair the speculated values, stage, run sums -------------
-            if (!w0) {
-                if (moved_prev) {
+            // Subject-tile shapes: the window of idx-1 formed this coordinate's
+            // run terms; only the runs the previous update changed are redone
+            // (a pair of a multi-pair run whose era holds the previous drug:
+            // the whole CTA takes the staged path below).
+            bool fast = false;
+            if constexpr (kGW) {
+                fast = true;
+                unsigned redo = 0u;
+                if (!w0 && moved_prev) {
+#pragma unroll
+                    for (int v = 0; v < kRT; ++v) {
+                        if ((P.dep >> v) & 1u) { // new l*exp, restaged for its run's head
+                            bool d;
+                            P.pre[v] = r_pre(rc[slot_pos(v)], se, S.rovf, -1, d);
+                            P.le[v] = __dmul_rn(__dmul_rn(P.pre[v], se[j]), static_cast<double>(P.len[v]));
+                            sm.stage2[slot_pos(v)] = P.le[v];
+                        }
+                    }
+                }
+                // one barrier, as the staged path has; any pair of the CTA
+                // with a new l*exp makes the heads of multi-pair runs re-sum
+                const bool anydep = __syncthreads_or(!w0 && moved_prev && P.dep != 0u);
+                if (!w0) {
+                    const int* ssc = sm.ssub[idx & 1];
+#pragma unroll
+                    for (int v = 0; v < kRT; ++v) {
+                        if (!((P.head >> v) & 1u)) continue;
+                        if ((P.single >> v) & 1u) {
+                            if ((P.dep >> v) & 1u) P.num[v] = P.le[v], redo |= 1u << v;
+                        } else if (anydep) {
+                            double num = P.le[v];
+                            int q = slot_pos(v) + 1;
+                            while (q < ncur && ssc[q] == P.ls[v]) num = __dadd_rn(num, sm.stage2[q++]);
+                            if (num != P.num[v]) P.num[v] = num, redo |= 1u << v;
+                        }
+                        if (moved_prev && tile[P.ls[v]] != P.dn[v]) redo |= 1u << v; // den changed
+                        if ((redo >> v) & 1u) {
+                            P.dn[v] = tile[P.ls[v]];
+                            P.ta[v] = 0.0;
+                            P.tb[v] = 0.0;
+                            run_terms(P.num[v], P.dn[v], P.n[v], P.ta[v], P.tb[v], err);
+                        }
+                        gs = __dadd_rn(gs, P.ta[v]);
+                        hs = __dadd_rn(hs, P.tb[v]);
+                    }
+                }
+            }
+            if (!fast && !w0) {
+                if (!kGW && moved_prev) {
                     const int* sprev = sm.ssub[(idx + 1) & 1];
                     const unsigned* bmprev = (idx & 1) ? bm0 : bm1; // marks of coordinate idx-1
 #pragma unroll
@@ -406,10 +500,10 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
                     }
                 }
             }
-            __syncthreads();
+            if (!fast) __syncthreads(); // (fast is CTA-uniform)
             if (tr && tid == 32) trb[idx * trs + 12] = gtimer();
 #if !RCD_GH_FLAT
-            if (!w0) {
+            if (!fast && !w0) {
 #pragma unroll
                 for (int v = 0; v < kRT; ++v) {
                     if (!((P.head >> v) & 1u)) continue;
@@ -455,7 +549,11 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
             const bool idle = w0 || !__any_sync(0xffffffffu, slot_pos(0) < ncur);
             block_reduce_r(gs, hs, e, idle, sm);
             if (tr && tid == 0) trb[idx * trs + 1] = gtimer();
-            publish(A, S, c, seq, gs, hs, e, pv);
+            if (w0) {
+                XPrev pv = sm.xpv[tid];
+                publish(A, S, c, seq, gs, hs, e, pv);
+                sm.xpv[tid] = pv;
+            }
             // ---- while the partials travel ------------------------------------
             const bool more = idx + 1 < V;
             const int jn = more ? visit[idx + 1] : 0;
@@ -477,6 +575,34 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
                     r_speculate<kSS>(rbuf + static_cast<size_t>((idx + 1) % kRBufs) * kRC, nnext, jn, j, A.J, se, S.rovf,
                                      S.denc, subj_base, pol_keep, Q);
                 }
+                if constexpr (kGW) {
+                    if (more) { // idx+1's run terms, with the denominators as they are now
+                        int* ssn = sm.ssub[(idx + 1) & 1];
+#pragma unroll
+                        for (int v = 0; v < kRT; ++v) {
+                            if (r_slot_valid(v, nnext)) {
+                                sm.stage2[slot_pos(v)] = Q.le[v];
+                                ssn[slot_pos(v)] = Q.ls[v];
+                            }
+                        }
+                        asm volatile("bar.sync 1, %0;" ::"r"(kD) : "memory"); // data warps only (warp 0 polls)
+                        Q.single = 0u;
+#pragma unroll
+                        for (int v = 0; v < kRT; ++v) {
+                            if (!((Q.head >> v) & 1u)) continue;
+                            const int pos = slot_pos(v);
+                            double num = Q.le[v];
+                            int q = pos + 1;
+                            while (q < nnext && ssn[q] == Q.ls[v]) num = __dadd_rn(num, sm.stage2[q++]);
+                            if (q == pos + 1) Q.single |= 1u << v;
+                            Q.num[v] = num;
+                            Q.dn[v] = tile[Q.ls[v]];
+                            Q.ta[v] = 0.0;
+                            Q.tb[v] = 0.0;
+                            run_terms(num, Q.dn[v], Q.n[v], Q.ta[v], Q.tb[v], err);
+                        }
+                    }
+                }
                 if (tr && tid == 32) { // the stamp waits for the speculated values
                     double dep = 0.0;
 #pragma unroll
@@ -495,7 +621,9 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
                 int te = 0;
                 unsigned inexact[2] = {0u, 0u};
                 if (tr && tid == 0) trb[idx * trs + 4] = gtimer();
+                XPrev pv = sm.xpv[tid];
                 poll<false>(A, S.xslots, seq, pv, tg, th, te, tr ? trb + idx * trs + 5 : nullptr, inexact);
+                sm.xpv[tid] = pv;
                 int status = ST_OK;
                 double delta = 0.0;
                 if (te) {
@@ -719,11 +847,13 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
         if (err) record_error(S.err, err, errv);
         int e = err;
         block_reduce_r(ch, mg, e, false, sm);
+        XPrev pv = w0 ? sm.xpv[tid & 31] : XPrev{0ull, 0ull, 0ull, 0ull};
         publish(A, S, c, seq, ch, mg, e, pv);
         if (w0) {
             double tch, tmg;
             int te;
             poll(A, S.xslots, seq, pv, tch, tmg, te, nullptr);
+            sm.xpv[tid] = pv;
             if (c == 0 && tid == 0) {
                 S.res->change = tch;
                 S.res->magnitude = tmg;
@@ -741,5 +871,5 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
         S.res->refine_at = refine_at;
         if (S.xowner) *S.xcounter = seq;
     }
-    if (c == 0 && S.xowner) xprev_store(S, pv);
+    if (c == 0 && S.xowner && w0) xprev_store(S, sm.xpv[tid]);
 }
