@@ -2326,8 +2326,8 @@ RcdShape rcd_shape(const ExchangePlan& plan) {
         r.ss_cap = cap;
         r.bytes = base + static_cast<size_t>(cap) * sizeof(double);
     } else {
-        r.bm_words = maxsub / 32 + 1;
-        r.bytes = base + 2 * static_cast<size_t>(r.bm_words) * sizeof(unsigned);
+        r.bm_words = (maxsub / 32 + 2) & ~1; // even: the lookup table after the bitmaps stays 8-B aligned
+        r.bytes = base + 2 * static_cast<size_t>(r.bm_words) * sizeof(unsigned) + r3::kHTab * sizeof(int2);
         if (r.bytes > static_cast<size_t>(kMaxSweepSmem)) return r;
     }
     // criterion chunks in the union region: beta at cycle start plus two

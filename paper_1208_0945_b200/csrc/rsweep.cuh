@@ -35,12 +35,6 @@
 #ifndef RCD_DEN_EARLY
 #define RCD_DEN_EARLY 0 // heads' denominator loads before (1) or after (0) the products
 #endif
-#ifndef RCD_GH_FLAT
-#define RCD_GH_FLAT 0 // grad/hess terms of all heads without branches (divisions overlap)
-#endif
-#ifndef RCD_GH_WINDOW
-#define RCD_GH_WINDOW 0 // subject-tile shapes: the next coordinate's run terms formed in the window (measured slower)
-#endif
 #ifndef RCD_TRACE
 #define RCD_TRACE 0 // globaltimer phase stamps (scripts/trace_sweep.py builds the variant with 1)
 #endif
@@ -70,10 +64,12 @@ __device__ __forceinline__ int slot_pos(int v) { return v * kD + data_tid(); }
 constexpr int kRT = RS_TILES;
 constexpr int kRC = kRT * kD; // pairs a CTA stages per coordinate (largest slice this instantiation runs)
 constexpr int kRBufs = 3;     // record buffers: coordinate idx, idx+1 (speculated), idx+2 (in flight)
+constexpr int kHTab = 2048;   // touched-subject lookup entries (no subject tile)
 
 struct RSmem {
     double stage[kRC];  // l*exp (grad/hess) or fresh - old (update), per pair slot
-    double stage2[kRC]; // l*exp of the next coordinate, staged in the window (run terms formed there)
+    double stageD[kRC]; // the update's fresh - old per pair slot (its own array: no barrier between the
+                        // update's heads and the next coordinate's staging)
     int ssub[2][kRC];   // subject per slot, by coordinate parity (the repair searches the previous slice)
     double jden[kRC];   // no subject tile: the denominator each head of the previous update wrote
     double ra[kWarps], rb[kWarps];
@@ -132,12 +128,6 @@ struct RSpec {
     int ls[kRT], len[kRT], n[kRT], ovf[kRT];
     unsigned head; // bit v: slot v starts a subject run
     unsigned dep;  // bit v: the era also holds the coordinate visited just before (its x'beta waits for that step)
-};
-// ... plus the run terms formed in the window (subject-tile shapes): the
-// run's numerator, the denominator used, (n w, n w (1 - w)), runs of one pair
-struct RSpecG : RSpec {
-    double num[kRT], dn[kRT], ta[kRT], tb[kRT];
-    unsigned single;
 };
 
 // exp(x'beta) of a pair without its own drug: the product of E over the
@@ -276,7 +266,6 @@ __device__ __forceinline__ void r_speculate(const RRec* rb, int n, int jn, int j
 
 template <bool kSS>
 __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs A) {
-    constexpr bool kGW = kSS && RCD_GH_WINDOW && kRT == 1; // run terms formed in the window
     extern __shared__ __align__(128) unsigned char smem_raw[];
     RSmem& sm = *reinterpret_cast<RSmem*>(smem_raw);
     // dynamic shared memory: RSmem | beta | exp(beta) | union { the sweep:
@@ -310,6 +299,8 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
     const int nsubj = S.cta_subj[c + 1] - subj_base;
     unsigned* bm0 = reinterpret_cast<unsigned*>(tile);
     unsigned* bm1 = bm0 + A.bm_words;
+    // no subject tile: direct-mapped (subject, head position) of the last update's heads
+    int2* htab = reinterpret_cast<int2*>(bm1 + A.bm_words);
 
     // beta into shared memory; the CTA's denominators into the tile
     for (int j = tid; j < A.J; j += kT) {
@@ -362,43 +353,13 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
             rj = S.trust[j];
             ydx = A.y_dot_x[j];
         }
-        using Spec = typename std::conditional<kGW, RSpecG, RSpec>::type;
-        Spec P; // coordinate idx
-        Spec Q; // coordinate idx+1, speculated during idx's window
+        RSpec P; // coordinate idx
+        RSpec Q; // coordinate idx+1, speculated during idx's window
         int ncur = static_cast<int>(vs[0].y - vs[0].x);
         int nn1 = V > 1 ? static_cast<int>(vs[1].y - vs[1].x) : 0; // slice length of idx+1 (loaded a window ahead)
         if (!w0) {
             wait_records(0);
             r_speculate<kSS>(rbuf, ncur, j, -1, A.J, se, S.rovf, S.denc, subj_base, pol_keep, P);
-        }
-        if constexpr (kGW) { // the first coordinate's run terms (the later ones come from the window)
-            int* ss0 = sm.ssub[0];
-            if (!w0) {
-#pragma unroll
-                for (int v = 0; v < kRT; ++v)
-                    if (r_slot_valid(v, ncur)) {
-                        sm.stage2[slot_pos(v)] = P.le[v];
-                        ss0[slot_pos(v)] = P.ls[v];
-                    }
-            }
-            __syncthreads();
-            if (!w0) {
-                P.single = 0u;
-#pragma unroll
-                for (int v = 0; v < kRT; ++v) {
-                    if (!((P.head >> v) & 1u)) continue;
-                    const int pos = slot_pos(v);
-                    double num = P.le[v];
-                    int q = pos + 1;
-                    while (q < ncur && ss0[q] == P.ls[v]) num = __dadd_rn(num, sm.stage2[q++]);
-                    if (q == pos + 1) P.single |= 1u << v;
-                    P.num[v] = num;
-                    P.dn[v] = tile[P.ls[v]];
-                    P.ta[v] = 0.0;
-                    P.tb[v] = 0.0;
-                    run_terms(num, P.dn[v], P.n[v], P.ta[v], P.tb[v], err);
-                }
-            }
         }
         bool moved_prev = false; // did coordinate idx-1 move (its x'beta / den repairs apply)
         int nprev = 0;
@@ -410,84 +371,22 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
         unsigned long long* trb = (RCD_TRACE && A.trace != nullptr && (tid == 0 || tid == 32))
                                       ? A.trace + static_cast<size_t>(blockIdx.x) * kTr
                                       : nullptr;
-        for (int idx = 0; idx < V; ++idx) {
+#pragma unroll 1
+        for (int idx = 0; idx < A.nvisit - A.visit_begin; ++idx) { // (bound from the parameters: no register held)
             const RRec* rc = rbuf + static_cast<size_t>(idx % kRBufs) * kRC;
             int* ssub = sm.ssub[idx & 1];
             const bool tr = RCD_TRACE && trb && idx < A.ntrace;
             if (tr && tid == 0) trb[idx * trs + 0] = gtimer();
             double gs = 0.0, hs = 0.0;
             // ---- repair the speculated values, stage, run sums -------------
-            // Subject-tile shapes: the window of idx-1 formed this coordinate's
-            // run terms; only the runs the previous update changed are redone
-            // (a pair of a multi-pair run whose era holds the previous drug:
-            // the whole CTA takes the staged path below).
-            bool fast = false;
-            if constexpr (kGW) {
-                fast = true;
-                unsigned redo = 0u;
-                if (!w0 && moved_prev) {
+            if (!w0) {
+                if (moved_prev) { // eras that also hold the previous coordinate's drug
 #pragma unroll
                     for (int v = 0; v < kRT; ++v) {
-                        if ((P.dep >> v) & 1u) { // new l*exp, restaged for its run's head
+                        if ((P.dep >> v) & 1u) {
                             bool d;
                             P.pre[v] = r_pre(rc[slot_pos(v)], se, S.rovf, -1, d);
                             P.le[v] = __dmul_rn(__dmul_rn(P.pre[v], se[j]), static_cast<double>(P.len[v]));
-                            sm.stage2[slot_pos(v)] = P.le[v];
-                        }
-                    }
-                }
-                // one barrier, as the staged path has; any pair of the CTA
-                // with a new l*exp makes the heads of multi-pair runs re-sum
-                const bool anydep = __syncthreads_or(!w0 && moved_prev && P.dep != 0u);
-                if (!w0) {
-                    const int* ssc = sm.ssub[idx & 1];
-#pragma unroll
-                    for (int v = 0; v < kRT; ++v) {
-                        if (!((P.head >> v) & 1u)) continue;
-                        if ((P.single >> v) & 1u) {
-                            if ((P.dep >> v) & 1u) P.num[v] = P.le[v], redo |= 1u << v;
-                        } else if (anydep) {
-                            double num = P.le[v];
-                            int q = slot_pos(v) + 1;
-                            while (q < ncur && ssc[q] == P.ls[v]) num = __dadd_rn(num, sm.stage2[q++]);
-                            if (num != P.num[v]) P.num[v] = num, redo |= 1u << v;
-                        }
-                        if (moved_prev && tile[P.ls[v]] != P.dn[v]) redo |= 1u << v; // den changed
-                        if ((redo >> v) & 1u) {
-                            P.dn[v] = tile[P.ls[v]];
-                            P.ta[v] = 0.0;
-                            P.tb[v] = 0.0;
-                            run_terms(P.num[v], P.dn[v], P.n[v], P.ta[v], P.tb[v], err);
-                        }
-                        gs = __dadd_rn(gs, P.ta[v]);
-                        hs = __dadd_rn(hs, P.tb[v]);
-                    }
-                }
-            }
-            if (!fast && !w0) {
-                if (!kGW && moved_prev) {
-                    const int* sprev = sm.ssub[(idx + 1) & 1];
-                    const unsigned* bmprev = (idx & 1) ? bm0 : bm1; // marks of coordinate idx-1
-#pragma unroll
-                    for (int v = 0; v < kRT; ++v) {
-                        if ((P.dep >> v) & 1u) { // the era also holds the previous coordinate's drug
-                            bool d;
-                            P.pre[v] = r_pre(rc[slot_pos(v)], se, S.rovf, -1, d);
-                            P.le[v] = __dmul_rn(__dmul_rn(P.pre[v], se[j]), static_cast<double>(P.len[v]));
-                        }
-                        if constexpr (!kSS) {
-                            if ((P.head >> v) & 1u) {
-                                const int s = P.ls[v];
-                                if ((bmprev[s >> 5] >> (s & 31)) & 1u) { // touched: its run head in the previous slice
-                                    int lo = 0, hi = nprev;
-                                    while (lo < hi) {
-                                        const int mid = (lo + hi) >> 1;
-                                        if (sprev[mid] < s) lo = mid + 1;
-                                        else hi = mid;
-                                    }
-                                    P.den[v] = sm.jden[lo];
-                                }
-                            }
                         }
                     }
                 }
@@ -500,10 +399,36 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
                     }
                 }
             }
-            if (!fast) __syncthreads(); // (fast is CTA-uniform)
+            // this barrier also orders the previous update's denominators,
+            // marks and records before the reads below (no end-of-coordinate
+            // barrier: the update stages its differences in its own array)
+            __syncthreads();
             if (tr && tid == 32) trb[idx * trs + 12] = gtimer();
-#if !RCD_GH_FLAT
-            if (!fast && !w0) {
+            if (!w0) {
+                if (!kSS && moved_prev) { // heads whose subject the previous update touched
+                    const int* sprev = sm.ssub[(idx + 1) & 1];
+                    const unsigned* bmprev = (idx & 1) ? bm0 : bm1; // marks of coordinate idx-1
+#pragma unroll
+                    for (int v = 0; v < kRT; ++v) {
+                        if (!((P.head >> v) & 1u)) continue;
+                        const int s = P.ls[v];
+                        if (!((bmprev[s >> 5] >> (s & 31)) & 1u)) continue;
+                        int lo;
+                        const int2 e = htab[s & (kHTab - 1)]; // direct-mapped (subject, head position)
+                        if (e.x == s) {
+                            lo = e.y;
+                        } else { // evicted by a colliding subject: search the previous slice
+                            int hi = nprev;
+                            lo = 0;
+                            while (lo < hi) {
+                                const int mid = (lo + hi) >> 1;
+                                if (sprev[mid] < s) lo = mid + 1;
+                                else hi = mid;
+                            }
+                        }
+                        P.den[v] = sm.jden[lo];
+                    }
+                }
 #pragma unroll
                 for (int v = 0; v < kRT; ++v) {
                     if (!((P.head >> v) & 1u)) continue;
@@ -515,34 +440,6 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
                     run_terms(num, kSS ? tile[s] : P.den[v], P.n[v], gs, hs, err);
                 }
             }
-#else
-            if (!w0) {
-                // run numerators (data-dependent loops) first, then every
-                // head's term without branches so the divisions overlap,
-                // then the sums in slot order
-                double num[kRT];
-#pragma unroll
-                for (int v = 0; v < kRT; ++v) {
-                    num[v] = P.le[v];
-                    if (!((P.head >> v) & 1u)) continue;
-                    int q = slot_pos(v) + 1;
-                    while (q < ncur && ssub[q] == P.ls[v]) num[v] = __dadd_rn(num[v], sm.stage[q++]);
-                }
-#pragma unroll
-                for (int v = 0; v < kRT; ++v) {
-                    const bool h = (P.head >> v) & 1u;
-                    const double den = h ? (kSS ? tile[P.ls[v]] : P.den[v]) : 1.0;
-                    double a = 0.0, b = 0.0;
-                    int e2 = 0;
-                    run_terms(h ? num[v] : 0.0, den, P.n[v], a, b, e2);
-                    if (h) {
-                        gs = __dadd_rn(gs, a);
-                        hs = __dadd_rn(hs, b);
-                        err |= e2;
-                    }
-                }
-            }
-#endif
             if (tr && tid == 32) trb[idx * trs + 13] = gtimer() + (gs == 1.2345 ? 1 : 0);
             if (err) record_error(S.err, err, errv);
             int e = err | ((bj != bj) || (rj != rj) ? 1 : 0);
@@ -574,34 +471,6 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
                     if (tr && tid == 32) trb[idx * trs + 15] = gtimer();
                     r_speculate<kSS>(rbuf + static_cast<size_t>((idx + 1) % kRBufs) * kRC, nnext, jn, j, A.J, se, S.rovf,
                                      S.denc, subj_base, pol_keep, Q);
-                }
-                if constexpr (kGW) {
-                    if (more) { // idx+1's run terms, with the denominators as they are now
-                        int* ssn = sm.ssub[(idx + 1) & 1];
-#pragma unroll
-                        for (int v = 0; v < kRT; ++v) {
-                            if (r_slot_valid(v, nnext)) {
-                                sm.stage2[slot_pos(v)] = Q.le[v];
-                                ssn[slot_pos(v)] = Q.ls[v];
-                            }
-                        }
-                        asm volatile("bar.sync 1, %0;" ::"r"(kD) : "memory"); // data warps only (warp 0 polls)
-                        Q.single = 0u;
-#pragma unroll
-                        for (int v = 0; v < kRT; ++v) {
-                            if (!((Q.head >> v) & 1u)) continue;
-                            const int pos = slot_pos(v);
-                            double num = Q.le[v];
-                            int q = pos + 1;
-                            while (q < nnext && ssn[q] == Q.ls[v]) num = __dadd_rn(num, sm.stage2[q++]);
-                            if (q == pos + 1) Q.single |= 1u << v;
-                            Q.num[v] = num;
-                            Q.dn[v] = tile[Q.ls[v]];
-                            Q.ta[v] = 0.0;
-                            Q.tb[v] = 0.0;
-                            run_terms(num, Q.dn[v], Q.n[v], Q.ta[v], Q.tb[v], err);
-                        }
-                    }
                 }
                 if (tr && tid == 32) { // the stamp waits for the speculated values
                     double dep = 0.0;
@@ -709,7 +578,7 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
                     if (tr && tid == 32) trb[idx * trs + 8] = gtimer() + (diff[0] == 1.2345 ? 1 : 0);
 #pragma unroll
                     for (int v = 0; v < kRT; ++v)
-                        if (r_slot_valid(v, ncur)) sm.stage[slot_pos(v)] = diff[v];
+                        if (r_slot_valid(v, ncur)) sm.stageD[slot_pos(v)] = diff[v];
                 }
                 __syncthreads();
                 if (tr && tid == 32) trb[idx * trs + 9] = gtimer();
@@ -721,9 +590,9 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
                         if (!((P.head >> v) & 1u)) continue;
                         const int pos = slot_pos(v);
                         const int s = P.ls[v];
-                        double dv = __dadd_rn(kSS ? tile[s] : P.den[v], sm.stage[pos]);
+                        double dv = __dadd_rn(kSS ? tile[s] : P.den[v], sm.stageD[pos]);
                         int q = pos + 1;
-                        while (q < ncur && ssub[q] == s) dv = __dadd_rn(dv, sm.stage[q++]);
+                        while (q < ncur && ssub[q] == s) dv = __dadd_rn(dv, sm.stageD[q++]);
                         den[v] = dv;
                     }
 #pragma unroll
@@ -735,6 +604,7 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
                         } else {
                             st_keep(S.denc + subj_base + s, den[v], pol_keep);
                             sm.jden[slot_pos(v)] = den[v];
+                            htab[s & (kHTab - 1)] = make_int2(s, slot_pos(v));
                             atomicOr(&bmcur[s >> 5], 1u << (s & 31));
                             clr_sub[v] = s;
                         }
@@ -743,14 +613,14 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
                     if (tr && tid == 32) trb[idx * trs + 10] = gtimer();
                 }
             }
-            __syncthreads(); // slice writes of this coordinate before the next reads
             if (tr && tid == 0) trb[idx * trs + 3] = gtimer();
             P = Q;
             nprev = ncur;
             ncur = nnext;
             j = jn;
         }
-        if constexpr (kSS) { // the cycle's denominators back to HBM (ordered by the loop's last barrier)
+        __syncthreads(); // the last update's writes
+        if constexpr (kSS) { // the cycle's denominators back to HBM
             for (int t = tid; t < nsubj; t += kT) S.denc[subj_base + t] = tile[t];
         }
     }
