@@ -58,7 +58,7 @@ typedef struct bsccs_prior {
  * precision: 1 Double (0 Single is rejected with BSCCS_INPUT_ERROR: the
  * device path is fp64 only).  path: 0 sparse, 1 dense (the reference's
  * UpdatePath::dense benchmark route, run by k_ccd_dense on an unsharded
- * dataset; DESIGN.md §4.7).
+ * dataset; DESIGN.md §4.8).
  * partitions / min_parallel_nnz are accepted and ignored: the device
  * reduction fixes its own partition (one per CTA), see DESIGN.md. */
 typedef struct bsccs_solver_config {
