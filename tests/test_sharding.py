@@ -242,3 +242,30 @@ def test_hierarchical_exchange_bitwise_equals_flat(nshards, monkeypatch):
     assert a.cycles_run == single.cycles_run
     nz = single.beta_map != 0
     assert np.all(np.abs(a.beta_map[nz] - single.beta_map[nz]) <= 1e-9 * np.abs(single.beta_map[nz]))
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+@pytest.mark.parametrize("nshards,virtual", [(2, False), (4, True)])
+def test_sharded_config3_matches_reference_golden(nshards, virtual):
+    """the north-star configuration (10M x 4,000, Laplace 0.1) patient-sharded:
+    2 shards in one launch, and 4 virtual ranks (every CTA adds into every
+    rank's exchange area, the multi-GPU protocol on one device) -- against
+    the reference's fit of the same dataset"""
+    from conftest import GOLDEN, load_golden
+    from helpers import fa, prior_from
+    if not (GOLDEN / "fit_10M_laplace.json").exists():
+        pytest.skip("fit_10M_laplace.json not generated")
+    g = load_golden("fit_10M_laplace.json")
+    ds = datagen.config_dataset("10M")
+    assert (ds.num_subjects, ds.num_eras, ds.nnz) == (g["sizes"]["N"], g["sizes"]["K"], g["sizes"]["nnz"])
+    grp = sharding.LocalGroup(sharding.shard_dataset(ds, nshards), virtual_ranks=virtual)
+    res = grp.fit(prior_from(g["prior"]))
+    grp.close()
+    ref = fa(g["beta"])
+    assert res.cycles_run == g["cycles_run"]
+    zero = ref == 0.0
+    assert np.all(np.abs(res.beta_map[zero]) <= 1e-9)
+    assert np.all(np.abs(res.beta_map[~zero] - ref[~zero]) <= 1e-6 * np.abs(ref[~zero]))
+    lp = float(g["log_posterior"])
+    assert abs(res.log_posterior - lp) <= 1e-8 * abs(lp)
