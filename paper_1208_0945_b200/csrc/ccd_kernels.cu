@@ -1328,6 +1328,11 @@ __global__ void k_compact_csr(const int64_t* __restrict__ csr_ptr, const int32_t
         if (i < nnz) ecol[i] = static_cast<uint16_t>(csr_col[i]);
     }
 }
+// overflow entries of one era's pairs (each pair's list padded to 8)
+__device__ __forceinline__ long long era_overflow(int deg) {
+    return deg - 1 > kRInline ? static_cast<long long>(deg) * ((deg - 1 - kRInline + 7) & ~7) : 0;
+}
+
 // per subject: overflow drug entries of its pairs; bad |= 1 when an era has
 // more than kRMaxOthers + 1 drugs or n_i exceeds the record's field
 __global__ void k_rq_count(const int32_t* __restrict__ off, const int32_t* __restrict__ events,
@@ -1339,7 +1344,7 @@ __global__ void k_rq_count(const int32_t* __restrict__ off, const int32_t* __res
         for (int k = off[s]; k < off[s + 1]; ++k) {
             const long long deg = csr_ptr[k + 1] - csr_ptr[k];
             if (deg - 1 > kRMaxOthers) b = 1;
-            if (deg - 1 > kRInline) o += deg * ((deg - 1 - kRInline + 7) & ~7ll); // lists padded to 16 B
+            o += era_overflow(static_cast<int>(deg)); // lists padded to 16 B
             md = deg > md ? deg : md;
         }
         cnt[s] = o;
@@ -1347,47 +1352,61 @@ __global__ void k_rq_count(const int32_t* __restrict__ off, const int32_t* __res
         atomicMax(max_deg, static_cast<int>(md < (1 << 30) ? md : (1 << 30)));
     }
 }
-__global__ void k_build_rq(const int32_t* __restrict__ off, const int32_t* __restrict__ events,
-                           const int32_t* __restrict__ len, const int64_t* __restrict__ csr_ptr,
-                           const int32_t* __restrict__ csr_col, const uint32_t* __restrict__ pos,
-                           const int32_t* __restrict__ cta_subj, int C, const long long* __restrict__ ovb, int32_t N,
-                           int32_t J, RRec* rq, uint16_t* rovf) {
+// subject of every era (one thread per subject writes its eras)
+__global__ void k_era_subject(const int32_t* __restrict__ off, int32_t N, int32_t* esub) {
     for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < N;
-         s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+         s += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        for (int k = off[s]; k < off[s + 1]; ++k) esub[k] = static_cast<int32_t>(s);
+}
+
+// The pair records, one thread per era: the era's drug list (contiguous in
+// the CSR) gives every pair's other drugs; each record is one 32-B store at
+// the pair's CSC position.  Overflow lists: the subject's offset (scan over
+// subjects) plus its earlier eras' (only subjects that have any).
+__global__ void k_build_rq(const int32_t* __restrict__ off, const int32_t* __restrict__ esub,
+                           const int32_t* __restrict__ events, const int32_t* __restrict__ len,
+                           const int64_t* __restrict__ csr_ptr, const int32_t* __restrict__ csr_col,
+                           const uint32_t* __restrict__ pos, const int32_t* __restrict__ cta_subj, int C,
+                           const long long* __restrict__ ovb, int32_t K, int32_t J, RRec* rq, uint16_t* rovf) {
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < K;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t q0 = csr_ptr[k];
+        const int deg = static_cast<int>(csr_ptr[k + 1] - q0);
+        if (deg == 0) continue;
+        const int s = esub[k];
         int lo = 0, hi = C + 1; // first c with cta_subj[c] > s
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
             if (cta_subj[mid] > s) hi = mid;
             else lo = mid + 1;
         }
-        const int ls = static_cast<int>(s) - cta_subj[lo - 1];
+        const int ls = s - cta_subj[lo - 1];
         const int n = events[s];
+        const int lk = len[k];
         long long ov = ovb[s];
-        for (int k = off[s]; k < off[s + 1]; ++k) {
-            const int64_t q0 = csr_ptr[k];
-            const int deg = static_cast<int>(csr_ptr[k + 1] - q0);
-            for (int a = 0; a < deg; ++a) {
-                RRec r;
-                r.ls = ls;
-                r.len = len[k];
-                r.meta = (deg - 1) | (a << 8) | (n << 16); // a: the pair's drug sorts after a other drugs
-                r.ovf = deg - 1 > kRInline ? static_cast<int32_t>(ov) : 0;
-                int i = 0;
-                for (int b = 0; b < deg; ++b) {
-                    if (b == a) continue;
-                    const uint16_t d = static_cast<uint16_t>(csr_col[q0 + b]);
-                    if (i < kRInline) r.o[i] = d;
-                    else rovf[ov + (i - kRInline)] = d;
-                    ++i;
-                }
-                for (; i < kRInline; ++i) r.o[i] = static_cast<uint16_t>(J); // the unit drug: exp(beta) = 1
-                if (deg - 1 > kRInline) { // pad the overflow list to a multiple of 8 (one 16-B load per 8)
-                    const int ext = (deg - 1 - kRInline + 7) & ~7;
-                    for (int t = deg - 1 - kRInline; t < ext; ++t) rovf[ov + t] = static_cast<uint16_t>(J);
-                    ov += ext;
-                }
-                rq[pos[q0 + a]] = r;
+        if (ovb[s + 1] != ov)
+            for (int k2 = off[s]; k2 < k; ++k2) ov += era_overflow(static_cast<int>(csr_ptr[k2 + 1] - csr_ptr[k2]));
+        for (int a = 0; a < deg; ++a) {
+            RRec r;
+            r.ls = ls;
+            r.len = lk;
+            r.meta = (deg - 1) | (a << 8) | (n << 16); // a: the pair's drug sorts after a other drugs
+            r.ovf = deg - 1 > kRInline ? static_cast<int32_t>(ov) : 0;
+            int i = 0;
+            for (int b = 0; b < deg; ++b) {
+                if (b == a) continue;
+                const uint16_t d = static_cast<uint16_t>(csr_col[q0 + b]);
+                if (i < kRInline) r.o[i] = d;
+                else rovf[ov + (i - kRInline)] = d;
+                ++i;
             }
+            for (; i < kRInline; ++i) r.o[i] = static_cast<uint16_t>(J); // the unit drug: exp(beta) = 1
+            if (deg - 1 > kRInline) { // pad the overflow list to a multiple of 8 (one 16-B load per 8)
+                const int ext = (deg - 1 - kRInline + 7) & ~7;
+                for (int t = deg - 1 - kRInline; t < ext; ++t) rovf[ov + t] = static_cast<uint16_t>(J);
+                ov += ext;
+            }
+            rq[pos[q0 + a]] = r;
         }
     }
 }
@@ -1693,9 +1712,16 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
                 ds->novf = novf;
                 ds->max_deg = std::max(1, rbad[1]);
                 ds->rovf = dalloc<uint16_t>(std::max<long long>(novf, 8), ds->device_bytes, s);
-                k_build_rq<<<grid_for(N, 128, sms), 128, 0, s>>>(
-                    ds->subject_offsets, ds->events_per_subject, ds->era_lengths, ds->csr_ptr, ds->csr_col,
-                    reinterpret_cast<const uint32_t*>(d_rows), ds->cta_subj, C, d_ob, N, J, ds->rq, ds->rovf);
+                int64_t b5 = 0;
+                int32_t* d_esub = nnz >= K ? d_col : dalloc<int32_t>(K, b5, s); // d_col is free by now
+                k_era_subject<<<grid_for(N, 256, sms), 256, 0, s>>>(ds->subject_offsets, N, d_esub);
+                const int g_rq = static_cast<int>(std::min<int64_t>((static_cast<int64_t>(K) + 255) / 256, 1 << 20));
+                k_build_rq<<<g_rq, 256, 0, s>>>(ds->subject_offsets, d_esub, ds->events_per_subject,
+                                                ds->era_lengths, ds->csr_ptr, ds->csr_col,
+                                                reinterpret_cast<const uint32_t*>(d_rows), ds->cta_subj, C, d_ob, K, J,
+                                                ds->rq, ds->rovf);
+                if (d_esub != d_col) dfree(d_esub, s);
+                count_launches(1);
                 CUDA_TRY(cudaMemsetAsync(ds->edeg, 0, static_cast<size_t>(K) + 32, s));
                 CUDA_TRY(cudaMemsetAsync(ds->ecol, 0, sizeof(uint16_t) * (nnz + 16), s));
                 k_compact_csr<<<grid_for(std::max<int64_t>(K, nnz), 256, sms), 256, 0, s>>>(ds->csr_ptr, ds->csr_col,
