@@ -1785,6 +1785,9 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
         CUDA_TRY(cudaMemcpy(cs.data(), ds->cta_subj, sizeof(int32_t) * (C + 1), cudaMemcpyDeviceToHost));
         ds->max_cta_subjects = 0;
         for (int c = 0; c < C; ++c) ds->max_cta_subjects = std::max(ds->max_cta_subjects, cs[c + 1] - cs[c]);
+        CUDA_TRY(cudaMemcpy(cs.data(), ds->cta_era, sizeof(int32_t) * (C + 1), cudaMemcpyDeviceToHost));
+        ds->max_cta_eras = 0;
+        for (int c = 0; c < C; ++c) ds->max_cta_eras = std::max(ds->max_cta_eras, cs[c + 1] - cs[c]);
     }
     ds->col_nonempty_h.resize(static_cast<size_t>(J));
     for (int32_t j = 0; j < J; ++j) {
@@ -2357,14 +2360,19 @@ RcdShape rcd_shape(const ExchangePlan& plan) {
         if (r.bytes > static_cast<size_t>(kMaxSweepSmem)) return r;
     }
     // criterion chunks in the union region: beta at cycle start plus two
-    // buffers of crit_E eras' degrees and ~1.25x their expected drugs
+    // buffers of crit_E eras' degrees and ~1.25x their expected drugs, and
+    // the chunks' first-drug offsets
     double deg = 0.0;
     for (auto* st : plan.shards) deg = std::max(deg, static_cast<double>(st->ds->nnz) / std::max(1, st->ds->K));
+    constexpr int kCB = r1::kCBufs; // the same in every shape
+    int maxera = 0;
+    for (auto* st : plan.shards) maxera = std::max(maxera, st->ds->max_cta_eras);
     for (int eper = 8; eper >= 1; eper /= 2) {
         const int E = eper * r.threads;
         const int ccap = (static_cast<int>(E * deg * 1.25) + 256 + 7) / 8 * 8;
-        const size_t crit = head + static_cast<size_t>(r.beta_cap) * sizeof(double) + 2 * static_cast<size_t>(E + 32) +
-                            2 * sizeof(uint16_t) * static_cast<size_t>(ccap + 16);
+        const size_t nchunk = static_cast<size_t>(maxera) / E + 2; // chunk offsets kept in shared memory
+        const size_t crit = head + static_cast<size_t>(r.beta_cap) * sizeof(double) + kCB * static_cast<size_t>(E + 32) +
+                            kCB * sizeof(uint16_t) * static_cast<size_t>(ccap + 16) + 8 + nchunk * sizeof(int64_t);
         if (crit <= static_cast<size_t>(kMaxSweepSmem) || eper == 1) {
             r.crit_E = E;
             r.crit_cap = ccap;

@@ -123,6 +123,7 @@ struct bsccs_dataset {
     uint8_t* col_nonempty = nullptr;  // [J] global
     int32_t* col_runs = nullptr;      // [J] subject runs per column (this shard)
     int32_t max_cta_subjects = 0;     // largest CTA subject range (sizes the shared-memory subject tile)
+    int32_t max_cta_eras = 0;         // largest CTA era range (sizes the criterion's chunk table)
     int32_t max_slice = 0;            // largest per-CTA slice of any column (streamed path needed above kCap)
     // resident-beta sweep (rsweep.cuh): pair records and overflow drug lists;
     // rq == nullptr when the dataset does not qualify (J > 65535, nnz >= 2^32,

@@ -38,6 +38,9 @@
 #ifndef RCD_TRACE
 #define RCD_TRACE 0 // globaltimer phase stamps (scripts/trace_sweep.py builds the variant with 1)
 #endif
+#ifndef RCD_DIAG_NOCRIT
+#define RCD_DIAG_NOCRIT 0
+#endif
 #ifndef RCD_DIAG_NODEN
 #define RCD_DIAG_NODEN 0
 #endif
@@ -65,6 +68,7 @@ constexpr int kRT = RS_TILES;
 constexpr int kRC = kRT * kD; // pairs a CTA stages per coordinate (largest slice this instantiation runs)
 constexpr int kRBufs = 3;     // record buffers: coordinate idx, idx+1 (speculated), idx+2 (in flight)
 constexpr int kHTab = 2048;   // touched-subject lookup entries (no subject tile)
+constexpr int kCBufs = 2;     // criterion chunk buffers (one chunk in flight)
 
 struct RSmem {
     double stage[kRC];  // l*exp (grad/hess) or fresh - old (update), per pair slot
@@ -77,7 +81,7 @@ struct RSmem {
     double delta, bnew, enew;
     int status;
     unsigned long long bar[kRBufs]; // mbarriers of the record buffers
-    unsigned long long cbar[2];     // mbarriers of the criterion chunk buffers
+    unsigned long long cbar[kCBufs]; // mbarriers of the criterion chunk buffers
     int wscan[kWarps];              // block scan of the criterion's per-thread era offsets
     XPrev xpv[32];                  // warp 0: the exchange's running totals per lane between uses
 };
@@ -316,7 +320,7 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
     }
     if (tid == 0) {
         for (int b = 0; b < kRBufs; ++b) mbar_init(&sm.bar[b], 1);
-        for (int b = 0; b < 2; ++b) mbar_init(&sm.cbar[b], 1);
+        for (int b = 0; b < kCBufs; ++b) mbar_init(&sm.cbar[b], 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -636,41 +640,44 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
         const int e0 = S.cta_era[c], e1 = S.cta_era[c + 1];
         const int E = A.crit_E, cap = A.crit_cap, eper = E / kT;
         double* sbp = reinterpret_cast<double*>(uni);
-        uint8_t* dbuf = reinterpret_cast<uint8_t*>(sbp + A.beta_cap);         // [2][E + 32]
-        uint16_t* cbuf = reinterpret_cast<uint16_t*>(dbuf + 2 * (E + 32));     // [2][cap + 16]
+        uint8_t* dbuf = reinterpret_cast<uint8_t*>(sbp + A.beta_cap);           // [kCBufs][E + 32]
+        uint16_t* cbuf = reinterpret_cast<uint16_t*>(dbuf + kCBufs * (E + 32));  // [kCBufs][cap + 16]
+        int64_t* cpt = reinterpret_cast<int64_t*>(cbuf + kCBufs * (cap + 16));   // [nch + 1] chunk drug offsets
         __syncthreads(); // the sweep's last readers of the union region are done
         // the cycle's change of each coefficient: an era's x'beta change is
         // their sum over its drugs (ascending, like x'beta itself)
         for (int jj = tid; jj < A.J; jj += kT) sbp[jj] = __dsub_rn(sb[jj], S.beta_prev[jj]);
-        const int nch = (e1 - e0 + E - 1) / E;
+        const int nch = RCD_DIAG_NOCRIT ? 0 : (e1 - e0 + E - 1) / E; // (diagnostic: no criterion)
+        // every chunk's first drug, loaded once (not on each chunk's path)
+        for (int i = tid; i <= nch; i += kT) cpt[i] = S.csr_ptr[min(e1, e0 + i * E)];
+        __syncthreads();
         // chunk i: eras [a, b), drugs [ca, cb); staged when they fit the buffer
         auto crit_stage = [&](int i) {
             const int a = e0 + i * E, b = min(e1, a + E);
-            const int64_t ca = S.csr_ptr[a], cb = S.csr_ptr[b];
+            const int64_t ca = cpt[i], cb = cpt[i + 1];
             const int a16 = a & ~15, b16 = (b + 15) & ~15;
             const int64_t ca8 = ca & ~7ll, cb8 = (cb + 7) & ~7ll;
-            unsigned long long* bar = &sm.cbar[i & 1];
+            unsigned long long* bar = &sm.cbar[i % kCBufs];
             fence_proxy_async();
             const bool fits = cb8 - ca8 <= cap;
             const unsigned bytes = static_cast<unsigned>(b16 - a16) + (fits ? static_cast<unsigned>(2 * (cb8 - ca8)) : 0u);
             mbar_arrive_tx(bar, bytes);
-            bulk_g2s(dbuf + (i & 1) * (E + 32), S.edeg + a16, static_cast<unsigned>(b16 - a16), bar, pol_stream);
-            if (fits) bulk_g2s(cbuf + (i & 1) * (cap + 16), S.ecol + ca8, static_cast<unsigned>(2 * (cb8 - ca8)), bar,
+            bulk_g2s(dbuf + (i % kCBufs) * (E + 32), S.edeg + a16, static_cast<unsigned>(b16 - a16), bar, pol_stream);
+            if (fits) bulk_g2s(cbuf + (i % kCBufs) * (cap + 16), S.ecol + ca8, static_cast<unsigned>(2 * (cb8 - ca8)), bar,
                                pol_stream);
         };
         if (tid == 0) {
-            if (nch > 0) crit_stage(0);
-            if (nch > 1) crit_stage(1);
+            for (int i = 0; i < kCBufs && i < nch; ++i) crit_stage(i);
         }
         __syncthreads(); // sbp
         for (int i = 0; i < nch; ++i) {
             const int a = e0 + i * E, b = min(e1, a + E);
-            const int64_t ca = S.csr_ptr[a];
-            const int64_t cb = S.csr_ptr[b];
+            const int64_t ca = cpt[i];
+            const int64_t cb = cpt[i + 1];
             const bool fits = ((cb + 7) & ~7ll) - (ca & ~7ll) <= cap;
-            mbar_wait(&sm.cbar[i & 1], static_cast<unsigned>((i >> 1) & 1));
-            const uint8_t* dg = dbuf + (i & 1) * (E + 32) + (a - (a & ~15));
-            const uint16_t* cl = cbuf + (i & 1) * (cap + 16) + (ca - (ca & ~7ll));
+            mbar_wait(&sm.cbar[i % kCBufs], static_cast<unsigned>((i / kCBufs) & 1));
+            const uint8_t* dg = dbuf + (i % kCBufs) * (E + 32) + (a - (a & ~15));
+            const uint16_t* cl = cbuf + (i % kCBufs) * (cap + 16) + (ca - (ca & ~7ll));
             // this thread's eras [k0, k1) of the chunk and their first drug
             const int k0 = min(b - a, tid * eper), k1 = min(b - a, k0 + eper);
             int tot = 0;
@@ -690,9 +697,19 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
                 for (int k = k0; k < k1; ++k) {
                     const int deg = dg[k];
                     double dx = 0.0;
-                    for (int q = 0; q < deg; ++q) {
-                        const int d = fits ? cl[off + q] : __ldg(S.ecol + ca + off + q);
-                        dx = __dadd_rn(dx, sbp[d]);
+                    if (fits && deg <= 8) {
+                        // the era's gathers issued together, summed in order
+                        double v[8];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) v[q] = q < deg ? sbp[cl[off + q]] : 0.0;
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            if (q < deg) dx = __dadd_rn(dx, v[q]);
+                    } else {
+                        for (int q = 0; q < deg; ++q) {
+                            const int d = fits ? cl[off + q] : __ldg(S.ecol + ca + off + q);
+                            dx = __dadd_rn(dx, sbp[d]);
+                        }
                     }
                     off += deg;
                     ch = __dadd_rn(ch, fabs(dx));
@@ -712,7 +729,7 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
                 }
             }
             __syncthreads(); // the chunk buffer and wscan are free again
-            if (tid == 0 && i + 2 < nch) crit_stage(i + 2);
+            if (tid == 0 && i + kCBufs < nch) crit_stage(i + kCBufs);
         }
         if (err) record_error(S.err, err, errv);
         int e = err;
