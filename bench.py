@@ -232,7 +232,7 @@ def reference_sample(rds, cols, args, steps, threads=1, partitions=1):
 
 
 def golden_for(args):
-    names = {"1M": "fit_1M_laplace.json", "10M": "fit_10M_laplace.json"}
+    names = {"1M": "fit_1M_laplace.json", "10M": "fit_10M_laplace.json", "10k": "fast_10k.json"}
     if args.zipf:
         names = {"1M": "fit_1M_zipf_laplace.json"}
     name = names.get(args.workload)
@@ -386,10 +386,19 @@ def main_ours(args, rank, world, local):
     from paper_1208_0945_b200 import bsccs as B
     from paper_1208_0945_b200 import datagen
 
+    # test hook: BSCCS_BENCH_SHARE_GPU=1 puts every rank on device 0 (the
+    # protocol on one GPU, time-sliced; NCCL refuses two ranks per device, so
+    # the host collectives then run on gloo)
+    share = os.environ.get("BSCCS_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     sharded = world > 1 and not args.replicas
 
     def barrier():
@@ -400,7 +409,7 @@ def main_ours(args, rank, world, local):
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        t = torch.tensor([x], device="cpu" if share else "cuda", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
