@@ -129,8 +129,9 @@ __device__ __forceinline__ bool r_slot_valid(int v, int n) { return slot_pos(v) 
 // the later phases need.
 struct RSpec {
     double pre[kRT], le[kRT], den[kRT]; // pre: product of E over the era's other drugs
-    int ls[kRT], len[kRT], n[kRT], ovf[kRT];
+    int ls[kRT], len[kRT]; // (n_i is read from the record where a head needs it)
     unsigned head; // bit v: slot v starts a subject run
+    unsigned cont; // bit v: the next pair belongs to the same subject (multi-pair run)
     unsigned dep;  // bit v: the era also holds the coordinate visited just before (its x'beta waits for that step)
 };
 
@@ -161,7 +162,7 @@ __device__ __forceinline__ void r_speculate(const RRec* rb, int n, int jn, int j
                                             const uint16_t* __restrict__ rovf, const double* __restrict__ denc,
                                             int subj_base, uint64_t pol_keep, RSpec& P) {
     uint32_t w[kRT][4];
-    int cnt[kRT];
+    int cnt[kRT], ovo[kRT];
     P.dep = 0u;
     bool any_ovf = false;
     const uint32_t unit2 = static_cast<uint32_t>(junit) * 0x10001u; // two unit drugs (padding)
@@ -174,23 +175,28 @@ __device__ __forceinline__ void r_speculate(const RRec* rb, int n, int jn, int j
         P.ls[v] = static_cast<int>(a.x);
         P.len[v] = static_cast<int>(a.y);
         cnt[v] = static_cast<int>(a.z & 0xffu);
-        P.n[v] = static_cast<int>(a.z >> 16);
         w[v][0] = o.x;
         w[v][1] = o.y;
         w[v][2] = o.z;
         w[v][3] = o.w;
         P.pre[v] = 1.0;
         any_ovf = any_ovf || cnt[v] > kRInline;
-        if (cnt[v] > kRInline) P.ovf[v] = static_cast<int>(a.w);
+        ovo[v] = static_cast<int>(a.w);
     }
     // run heads (the subject changes from the previous pair; lane 0 reads it)
     P.head = 0u;
+    P.cont = 0u;
 #pragma unroll
     for (int v = 0; v < kRT; ++v) {
         const int pos = slot_pos(v);
         int prev = __shfl_up_sync(0xffffffffu, P.ls[v], 1);
+        int next = __shfl_down_sync(0xffffffffu, P.ls[v], 1);
         if (lane_id() == 0) prev = pos > 0 && pos < n ? rb[pos - 1].ls : -1;
-        if (r_slot_valid(v, n) && (pos == 0 || prev != P.ls[v])) P.head |= 1u << v;
+        if (lane_id() == 31) next = pos + 1 < n ? rb[pos + 1].ls : -2;
+        if (r_slot_valid(v, n)) {
+            if (pos == 0 || prev != P.ls[v]) P.head |= 1u << v;
+            if (pos + 1 < n && next == P.ls[v]) P.cont |= 1u << v;
+        }
     }
 #if RCD_DEN_EARLY
     if constexpr (!kSS) {
@@ -205,7 +211,7 @@ __device__ __forceinline__ void r_speculate(const RRec* rb, int n, int jn, int j
     if (RCD_OVF_PREFETCH && any_ovf) {
 #pragma unroll
         for (int v = 0; v < kRT; ++v)
-            if (cnt[v] > kRInline) ov[v] = __ldg(reinterpret_cast<const uint4*>(rovf + P.ovf[v]));
+            if (cnt[v] > kRInline) ov[v] = __ldg(reinterpret_cast<const uint4*>(rovf + ovo[v]));
     }
     // the inline drugs (predicated: padding lanes issue no shared-memory
     // load -- measured faster than multiplying the unit drug's E = 1)
@@ -237,7 +243,7 @@ __device__ __forceinline__ void r_speculate(const RRec* rb, int n, int jn, int j
 #pragma unroll
         for (int v = 0; v < kRT; ++v) {
             if (cnt[v] <= kRInline) continue;
-            if (!RCD_OVF_PREFETCH) ov[v] = __ldg(reinterpret_cast<const uint4*>(rovf + P.ovf[v]));
+            if (!RCD_OVF_PREFETCH) ov[v] = __ldg(reinterpret_cast<const uint4*>(rovf + ovo[v]));
             const uint32_t x[4] = {ov[v].x, ov[v].y, ov[v].z, ov[v].w};
 #pragma unroll
             for (int i = 0; i < 8; ++i) { // padded with the unit drug as well
@@ -246,7 +252,7 @@ __device__ __forceinline__ void r_speculate(const RRec* rb, int n, int jn, int j
                 if (d == jprev) P.dep |= 1u << v;
             }
             for (int i = kRInline + 8; i < cnt[v]; ++i) { // more than 16 other drugs
-                const int d = __ldg(rovf + P.ovf[v] + (i - kRInline));
+                const int d = __ldg(rovf + ovo[v] + (i - kRInline));
                 P.pre[v] = __dmul_rn(P.pre[v], se[d]);
                 if (d == jprev) P.dep |= 1u << v;
             }
@@ -439,9 +445,12 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
                     const int pos = slot_pos(v);
                     const int s = P.ls[v];
                     double num = P.le[v];
-                    int q = pos + 1;
-                    while (q < ncur && ssub[q] == s) num = __dadd_rn(num, sm.stage[q++]);
-                    run_terms(num, kSS ? tile[s] : P.den[v], P.n[v], gs, hs, err);
+                    if ((P.cont >> v) & 1u) { // a multi-pair run: the other pairs' l*exp in order
+                        int q = pos + 1;
+                        while (q < ncur && ssub[q] == s) num = __dadd_rn(num, sm.stage[q++]);
+                    }
+                    run_terms(num, kSS ? tile[s] : P.den[v], static_cast<int>(static_cast<unsigned>(rc[pos].meta) >> 16), gs,
+                              hs, err);
                 }
             }
             if (tr && tid == 32) trb[idx * trs + 13] = gtimer() + (gs == 1.2345 ? 1 : 0);
@@ -595,8 +604,10 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
                         const int pos = slot_pos(v);
                         const int s = P.ls[v];
                         double dv = __dadd_rn(kSS ? tile[s] : P.den[v], sm.stageD[pos]);
-                        int q = pos + 1;
-                        while (q < ncur && ssub[q] == s) dv = __dadd_rn(dv, sm.stageD[q++]);
+                        if ((P.cont >> v) & 1u) {
+                            int q = pos + 1;
+                            while (q < ncur && ssub[q] == s) dv = __dadd_rn(dv, sm.stageD[q++]);
+                        }
                         den[v] = dv;
                     }
 #pragma unroll
