@@ -82,7 +82,6 @@ struct RSmem {
     int status;
     unsigned long long bar[kRBufs]; // mbarriers of the record buffers
     unsigned long long cbar[kCBufs]; // mbarriers of the criterion chunk buffers
-    int wscan[kWarps];              // block scan of the criterion's per-thread era offsets
     XPrev xpv[32];                  // warp 0: the exchange's running totals per lane between uses
 };
 constexpr size_t kRSmemBytes = (sizeof(RSmem) + 127) / 128 * 128;
@@ -646,7 +645,8 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
         // taken as the sum of the era's coefficient changes (sbp).
         // The eras' drug lists stream through two chunk buffers (bulk
         // copies of the degrees and drugs of A.crit_E eras, one chunk ahead);
-        // each thread sums crit_E / kT consecutive eras.
+        // each thread sums crit_E / kT consecutive eras from its first era's
+        // CSR offset.
         double ch = 0.0, mg = 0.0;
         const int e0 = S.cta_era[c], e1 = S.cta_era[c + 1];
         const int E = A.crit_E, cap = A.crit_cap, eper = E / kT;
@@ -681,29 +681,22 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
             for (int i = 0; i < kCBufs && i < nch; ++i) crit_stage(i);
         }
         __syncthreads(); // sbp
+        // this thread's first drug in each chunk (its first era's CSR offset),
+        // loaded one chunk ahead: no block scan of the degrees
+        int64_t first = nch > 0 ? S.csr_ptr[min(e1, e0 + tid * eper)] : 0;
         for (int i = 0; i < nch; ++i) {
             const int a = e0 + i * E, b = min(e1, a + E);
             const int64_t ca = cpt[i];
             const int64_t cb = cpt[i + 1];
             const bool fits = ((cb + 7) & ~7ll) - (ca & ~7ll) <= cap;
+            const int64_t mine = first;
+            if (i + 1 < nch) first = S.csr_ptr[min(e1, a + E + tid * eper)];
             mbar_wait(&sm.cbar[i % kCBufs], static_cast<unsigned>((i / kCBufs) & 1));
             const uint8_t* dg = dbuf + (i % kCBufs) * (E + 32) + (a - (a & ~15));
             const uint16_t* cl = cbuf + (i % kCBufs) * (cap + 16) + (ca - (ca & ~7ll));
             // this thread's eras [k0, k1) of the chunk and their first drug
             const int k0 = min(b - a, tid * eper), k1 = min(b - a, k0 + eper);
-            int tot = 0;
-            for (int k = k0; k < k1; ++k) tot += dg[k];
-            int incl = tot;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane_id() >= o) incl += y;
-            }
-            if (lane_id() == 31) sm.wscan[warp_id()] = incl;
-            __syncthreads();
-            int wbase = 0;
-            for (int w = 0; w < warp_id(); ++w) wbase += sm.wscan[w];
-            int off = wbase + incl - tot;
+            int off = static_cast<int>(mine - ca);
             if (!A.normalized) {
                 for (int k = k0; k < k1; ++k) {
                     const int deg = dg[k];
@@ -739,7 +732,7 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
                     mg = __dadd_rn(mg, fabs(xn));
                 }
             }
-            __syncthreads(); // the chunk buffer and wscan are free again
+            __syncthreads(); // the chunk buffer is free again
             if (tid == 0 && i + kCBufs < nch) crit_stage(i + kCBufs);
         }
         if (err) record_error(S.err, err, errv);
