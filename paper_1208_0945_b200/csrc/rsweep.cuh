@@ -68,7 +68,10 @@ constexpr int kRT = RS_TILES;
 constexpr int kRC = kRT * kD; // pairs a CTA stages per coordinate (largest slice this instantiation runs)
 constexpr int kRBufs = 3;     // record buffers: coordinate idx, idx+1 (speculated), idx+2 (in flight)
 constexpr int kHTab = 2048;   // touched-subject lookup entries (no subject tile)
-constexpr int kCBufs = 2;     // criterion chunk buffers (one chunk in flight)
+#ifndef RCD_CBUFS
+#define RCD_CBUFS 2
+#endif
+constexpr int kCBufs = RCD_CBUFS; // criterion chunk buffers (kCBufs - 1 chunks in flight)
 
 struct RSmem {
     double stage[kRC];  // l*exp (grad/hess) or fresh - old (update), per pair slot
