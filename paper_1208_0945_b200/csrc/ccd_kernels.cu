@@ -1309,13 +1309,21 @@ __global__ void k_iota(uint32_t* out, int64_t nnz) {
         out[p] = static_cast<uint32_t>(p);
 }
 // csr_col holds each CSR entry's CSC position after the sort: keep it in pos,
-// and the entry's column (col_of) in csr_col
-__global__ void k_pos_col(int32_t* csr_col, const int32_t* __restrict__ col_of, int64_t nnz, uint32_t* pos) {
+// and the entry's column in csr_col -- found by binary search in col_ptr
+// (L1-resident) rather than a random gather of the per-pair column array
+__global__ void k_pos_col(int32_t* csr_col, const int64_t* __restrict__ col_ptr, int32_t J, int64_t nnz,
+                          uint32_t* pos) {
     for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < nnz;
          q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const uint32_t p = static_cast<uint32_t>(csr_col[q]);
         pos[q] = p;
-        csr_col[q] = col_of[p];
+        int lo = 0, hi = J; // last column j with col_ptr[j] <= p
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (__ldg(col_ptr + mid) <= static_cast<int64_t>(p)) lo = mid;
+            else hi = mid;
+        }
+        csr_col[q] = lo;
     }
 }
 // the criterion's compact CSR: drugs per era (u8) and the drugs (u16)
@@ -1636,7 +1644,7 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
             CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, d_rows, d_subj, d_iota,
                                                      reinterpret_cast<uint32_t*>(ds->csr_col), nnz, 0, end_bit, s));
             // d_rows (the consumed keys) receives the CSC positions
-            k_pos_col<<<grid_for(nnz, 256, sms), 256, 0, s>>>(ds->csr_col, d_col, nnz,
+            k_pos_col<<<grid_for(nnz, 256, sms), 256, 0, s>>>(ds->csr_col, ds->col_ptr, J, nnz,
                                                                reinterpret_cast<uint32_t*>(d_rows));
             count_launches(1);
             dfree(d_iota, s);
