@@ -120,6 +120,9 @@ int32_t bsccs_debug_trace(int32_t ncoords, int32_t ctas, uint64_t* host_out, int
  * launches, 1 = k_ccd only, 2 = k_rcd only, 3 = both (handed over). */
 void bsccs_debug_set_sweep(int32_t kind, double beta_limit);
 int32_t bsccs_debug_last_sweep(void);
+/* Test hook: shape of the last k_rcd launch, slots per thread | 16 if the
+ * subject tile was in shared memory (0: none yet). */
+int32_t bsccs_debug_last_rcd_shape(void);
 /* Self-test of the exact all-reduce encoding, not a
  * reference entry point: n (<= 2048) partials in [0, 2^43) are split into
  * limbs and added into one set of exchange words on `device` exactly as n

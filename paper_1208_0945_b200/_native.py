@@ -68,6 +68,7 @@ _SIGS = [
     ("bsccs_debug_set_sweep_flags", None, [i32]),
     ("bsccs_debug_set_sweep", None, [i32, C.c_double]),
     ("bsccs_debug_last_sweep", i32, []),
+    ("bsccs_debug_last_rcd_shape", i32, []),
     ("bsccs_debug_trace", i32, [i32, i32, C.c_void_p, i64]),
     ("bsccs_debug_exchange_sum", i32, [i32, C.c_void_p, i32, C.POINTER(C.c_double), C.POINTER(C.c_int32)]),
     ("bsccs_dataset_create", C.c_int, [i32, i32, i32, i64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,

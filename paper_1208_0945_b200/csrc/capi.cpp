@@ -343,6 +343,7 @@ int32_t bsccs_debug_trace(int32_t ncoords, int32_t ctas, uint64_t* host_out, int
 
 void bsccs_debug_set_sweep(int32_t kind, double beta_limit) { set_debug_sweep(kind, beta_limit); }
 int32_t bsccs_debug_last_sweep(void) { return debug_last_sweep(); }
+int32_t bsccs_debug_last_rcd_shape(void) { return debug_last_rcd_shape(); }
 
 bsccs_status bsccs_debug_exchange_sum(int32_t device, const double* partials, int32_t n, double* sum,
                                       int32_t* status) {

@@ -1431,6 +1431,7 @@ bool rcd_enabled() {
 std::atomic<int> g_sweep_kind{0};       // tests: 1 forces k_ccd
 std::atomic<double> g_beta_limit{0.0};  // tests: lower k_rcd's |beta| bound
 std::atomic<int> g_last_sweep{0};
+std::atomic<int> g_last_rcd_shape{0};
 
 // Small pinned result blocks for the per-state D2H of kernel scalars.
 struct PinnedResults {
@@ -2402,6 +2403,7 @@ void launch_rcd(const ExchangePlan& plan, SweepArgs& a, const RcdShape& sh) {
     a.crit_E = sh.crit_E;
     a.crit_cap = sh.crit_cap;
     a.beta_limit = sh.beta_limit;
+    g_last_rcd_shape = sh.tiles | (sh.kss ? 16 : 0);
     void* params[] = {&a};
     void* fn = sh.tiles == 1   ? (sh.kss ? reinterpret_cast<void*>(r1::k_rcd<true>) : reinterpret_cast<void*>(r1::k_rcd<false>))
                : sh.tiles == 2 ? (sh.kss ? reinterpret_cast<void*>(r2::k_rcd<true>) : reinterpret_cast<void*>(r2::k_rcd<false>))
@@ -2575,6 +2577,7 @@ void set_debug_sweep(int kind, double beta_limit) {
     g_beta_limit = beta_limit;
 }
 int debug_last_sweep() { return g_last_sweep; }
+int debug_last_rcd_shape() { return g_last_rcd_shape; }
 void set_debug_trace(int ncoords, int ctas) {
     if (g_trace) cudaFree(g_trace);
     g_trace = nullptr;

@@ -272,6 +272,7 @@ void prepare_snapshot(bsccs_state* st);
 void set_debug_flags(int flags); // profiling only
 void set_debug_sweep(int kind, double beta_limit); // tests only (bsccs_debug_set_sweep)
 int debug_last_sweep();
+int debug_last_rcd_shape();
 void set_debug_trace(int ncoords, int ctas);
 void read_debug_trace(unsigned long long* host, size_t words);
 void debug_exchange_sum(int device, const double* partials, int n, double* sum, int* status);

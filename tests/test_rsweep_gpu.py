@@ -185,3 +185,24 @@ def test_local_group_on_resident_sweep(shards):
     nz = single.beta_map != 0.0
     assert np.array_equal(res.beta_map == 0.0, ~nz)
     assert np.all(np.abs(res.beta_map[nz] - single.beta_map[nz]) <= 1e-10 * np.abs(single.beta_map[nz]))
+
+
+@pytest.mark.parametrize("ctas,drugs,subjects,lam,shape", [
+    (4, 400, 3000, 3.0, 1 | 16),  # ~60 pairs per slice: one slot x 384 threads, subject tile
+    (4, 60, 3000, 3.0, 2 | 16),   # ~560: two slots x 512 threads
+    (4, 35, 3000, 3.0, 3 | 16),   # ~960: three slots x 384 threads
+    (2, 1500, 50000, 3.0, 2),     # ~25k subjects per CTA: no subject tile (touched-subject bitmaps + lookup)
+])
+def test_every_shape_matches_reference(port, ctas, drugs, subjects, lam, shape):
+    """each k_rcd shape (forced by the CTA count and the drug count) against
+    the C oracle, Laplace and Normal"""
+    from paper_1208_0945_b200 import datagen
+    ds = datagen.fast_sccs(subjects, drugs, lam)
+    dds = B.DeviceDataset(ds, 0, ctas)
+    for prior in (B.laplace_prior(0.1), B.normal_prior(0.5)):
+        cfg = B.SolverConfig(epsilon=1e-7)
+        res = B.fit(dds, prior, cfg)
+        assert last_sweep() == K_RCD
+        assert _native.lib().bsccs_debug_last_rcd_shape() == shape
+        assert_parity(res, port.fit(ds, prior, cfg))
+    dds.close()
