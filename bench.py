@@ -332,6 +332,13 @@ def pinned_copy(ds):
     return held, B.Dataset(*[v for _, v in held])
 
 
+def upload_bytes(host):
+    """bytes the e2e legs copy host -> device: every CSC array but the per-pair
+    subjects, which bsccs_dataset_create derives on the device from the rows
+    (subjects = NULL)"""
+    return int(sum(a.nbytes for a in host.arrays()) - host.subjects.nbytes)
+
+
 def sweep_kernel():
     """which sweep kernel the last cycle launched (bsccs_debug_last_sweep)"""
     from paper_1208_0945_b200 import _native
@@ -457,7 +464,7 @@ def main_ours(args, rank, world, local):
     e2e = None
     if not args.no_e2e:
         held, host = pinned_copy(shard.dataset if sharded else ds)
-        h2d = int(sum(a.nbytes for a in host.arrays()))
+        h2d = upload_bytes(host)
         d2h = ds.num_drugs * 8
 
         def e2e_step():
@@ -465,11 +472,11 @@ def main_ours(args, rank, world, local):
                 from paper_1208_0945_b200 import sharding
                 sh = sharding.Shard(host, shard.subject_begin, shard.subject_end, shard.era_begin,
                                     shard.y_dot_x_global, shard.col_nnz_global)
-                gg = sharding.RankGroup(sh, local)
+                gg = sharding.RankGroup(sh, local, upload_subjects=False)
                 r = gg.fit(prior, cfg)
                 gg.close()
                 return r
-            d = B.DeviceDataset(host, device=local)
+            d = B.DeviceDataset(host, device=local, upload_subjects=False)
             r = B.fit(d, prior, cfg)
             d.close()
             return r
@@ -483,7 +490,8 @@ def main_ours(args, rank, world, local):
                "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e_ms / args.steps,
                "path": ("bsccs_dataset_create_shard + RankGroup (IPC handles over torch.distributed) + "
                         "bsccs_group_fit" if sharded else "bsccs_dataset_create") +
-                       " (pinned host CSC arrays -> HBM, device CSR/split build) + fit + beta to host + destroy",
+                       " (pinned host CSC arrays -> HBM, per-pair subjects derived on the device, CSR/split build) + fit + "
+                       "beta to host + destroy",
                "gpu_launches": B.launch_count() - l0}
         del held, host
 
@@ -547,7 +555,7 @@ def bench_config2(args, B, datagen, torch, barrier, peak, peak_src, local):
     held, host = pinned_copy(ds)
 
     def e2e_step():
-        d = B.DeviceDataset(host, device=local)
+        d = B.DeviceDataset(host, device=local, upload_subjects=False)
         r = B.fit(d, prior, cfg)
         d.close()
         return r
@@ -564,7 +572,7 @@ def bench_config2(args, B, datagen, torch, barrier, peak, peak_src, local):
            "time_to_convergence_s": ms / args.steps * 1e-3, "cycles_per_fit": r0.cycles_run,
            "roofline": roofline_of(res, ms, peak, peak_src, "1M"),
            "e2e": {"value": sum(r.coordinates_visited for r in eres) / (ems * 1e-3), "unit": UNIT,
-                   "h2d_bytes_per_step": int(sum(a.nbytes for a in host.arrays())),
+                   "h2d_bytes_per_step": upload_bytes(host),
                    "d2h_bytes_per_step": ds.num_drugs * 8, "ms_per_step": ems / args.steps},
            "parity_vs_reference_golden": parity_vs(g, r0.beta_map, r0.log_posterior, r0.cycles_run,
                                                    digest(ds) == g["digest"] if g else None)}
@@ -616,7 +624,7 @@ def bench_many_fit(args, B, datagen, torch, barrier, peak, peak_src, local):
     held, host = pinned_copy(ds)
 
     def e2e_step():
-        d = B.DeviceDataset(host, device=local)
+        d = B.DeviceDataset(host, device=local, upload_subjects=False)
         f, _ = B.fit_batch(d, [mprior] * R, W, init, cfg)
         d.close()
         return f
@@ -625,7 +633,7 @@ def bench_many_fit(args, B, datagen, torch, barrier, peak, peak_src, local):
     eres, ems = timed_region(e2e_step, 1, barrier, torch)
     e2e = {"value": R / (ems * 1e-3), "unit": "fits/s", "ms_per_step": ems, "fits_per_step": R,
            "coordinate_updates_per_s": sum(f.coordinates_visited for f in eres[0]) / (ems * 1e-3),
-           "h2d_bytes_per_step": int(sum(a.nbytes for a in host.arrays()) + W.nbytes + init.nbytes),
+           "h2d_bytes_per_step": int(upload_bytes(host) + W.nbytes + init.nbytes),
            "d2h_bytes_per_step": int(R * ds.num_drugs * 8),
            "path": "bsccs_dataset_create (pinned host CSC) + bsccs_fit_batch (weights, warm starts from the host) + "
                    "betas to host + destroy"}

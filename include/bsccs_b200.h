@@ -138,7 +138,10 @@ bsccs_status bsccs_debug_exchange_sum(int32_t device, const double* partials, in
  * ::subjects concatenated, dataset.hpp:38-43).  y_dot_x may be NULL (it is
  * then recomputed on device from event_counts).  Validates the structural
  * invariants of build_dataset (dataset.hpp:74-152): offsets fenceposts,
- * rows ascending within a column, subject[p] owning rows[p].
+ * rows ascending within a column, subject[p] owning rows[p].  subjects may
+ * be NULL: each pair's subject is then derived on the device as the owner of
+ * its row (what build_dataset stores, dataset.hpp:134), which saves the
+ * upload of an array as large as rows.
  * num_ctas_override <= 0 selects the device default. */
 bsccs_status bsccs_dataset_create(
     int32_t num_subjects, int32_t num_eras, int32_t num_drugs, int64_t nnz,
@@ -148,7 +151,7 @@ bsccs_status bsccs_dataset_create(
     const int32_t* event_counts,       /* [num_eras]         */
     const int64_t* col_ptr,            /* [num_drugs + 1]    */
     const int32_t* rows,               /* [nnz]              */
-    const int32_t* subjects,           /* [nnz]              */
+    const int32_t* subjects,           /* [nnz] or NULL      */
     const int64_t* y_dot_x,            /* [num_drugs] or NULL */
     int32_t device, int32_t num_ctas_override,
     bsccs_dataset** out);

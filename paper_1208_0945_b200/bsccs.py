@@ -432,7 +432,11 @@ def write_long_format(path: str, records: Sequence[SubjectRecord], drug_ids: Seq
 class DeviceDataset:
     """Device-resident dataset handle (bsccs_dataset_create)."""
 
-    def __init__(self, ds: Optional[Dataset], device: int = 0, ctas: int = 0, shard_globals=None, handle=None):
+    def __init__(self, ds: Optional[Dataset], device: int = 0, ctas: int = 0, shard_globals=None, handle=None,
+                 upload_subjects: bool = True):
+        """upload_subjects=False passes NULL for the per-pair subjects: the
+        device derives them from the rows (each era's owner) instead of
+        copying them, and their agreement with the rows is then not checked."""
         self.host = ds
         self.device = device
         if handle is not None:  # built on the device (subset)
@@ -440,14 +444,16 @@ class DeviceDataset:
             self._sizes = None
             return
         h = C.c_void_p()
-        a = ds.arrays()
+        a = [_ptr(x) for x in ds.arrays()]
+        if not upload_subjects:
+            a[6] = None
         if shard_globals is None:
             _check(lib().bsccs_dataset_create(ds.num_subjects, ds.num_eras, ds.num_drugs, ds.nnz,
-                                              *[_ptr(x) for x in a], device, ctas, C.byref(h)))
+                                              *a, device, ctas, C.byref(h)))
         else:
             ydx, cnnz = (np.ascontiguousarray(x, dtype=np.int64) for x in shard_globals)
             _check(lib().bsccs_dataset_create_shard(ds.num_subjects, ds.num_eras, ds.num_drugs, ds.nnz,
-                                                    *[_ptr(x) for x in a[:7]], _ptr(ydx), _ptr(cnnz), device, ctas,
+                                                    *a[:7], _ptr(ydx), _ptr(cnnz), device, ctas,
                                                     C.byref(h)))
         self.handle = h
         self._sizes = None

@@ -1070,6 +1070,27 @@ __global__ void k_ll_final(const double* partial, int n, DevResult* res) {
 
 // ---- dataset build kernels -------------------------------------------------
 
+// bsccs_dataset_create with subjects == NULL: each pair's subject derived
+// from its row (build_dataset pushes the era's owner with the era,
+// dataset.hpp:134-136): the era -> subject table, then one gather per pair.
+// Offsets that are not monotone or out of range are clamped here and
+// rejected by k_validate_small; a row out of range gets subject -1 (k_pair_meta).
+__global__ void k_era_owner(const int32_t* __restrict__ off, int32_t N, int32_t K, int32_t* esub) {
+    for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < N;
+         s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int k1 = min(K, off[s + 1]);
+        for (int k = max(0, off[s]); k < k1; ++k) esub[k] = static_cast<int32_t>(s);
+    }
+}
+__global__ void k_subject_of_row(const int32_t* __restrict__ rows, const int32_t* __restrict__ esub, int32_t K,
+                                 int64_t nnz, int32_t* subj) {
+    for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < nnz;
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int r = rows[p];
+        subj[p] = (r >= 0 && r < K) ? esub[r] : -1;
+    }
+}
+
 __global__ void k_interleave(const int32_t* rows, const int32_t* subjects, int2* pairs, int64_t nnz) {
     for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < nnz;
          p += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -1836,7 +1857,7 @@ bsccs_dataset* dataset_create(int32_t N, int32_t K, int32_t J, int64_t nnz, cons
     if (K < 1 || J < 1 || nnz < 0) input_error("dataset: invalid sizes");
     if (!subject_offsets || !events_per_subject || !era_lengths || !event_counts || !col_ptr)
         input_error("dataset: null array");
-    if (nnz > 0 && (!rows || !subjects)) input_error("dataset: null pair arrays");
+    if (nnz > 0 && !rows) input_error("dataset: null pair arrays"); // subjects may be NULL: derived from rows
     // small-array invariants on the host (dataset.hpp:45-60)
     if (subject_offsets[0] != 0 || subject_offsets[N] != K) input_error("dataset: subject offsets must span [0, num_eras]");
     if (col_ptr[0] != 0 || col_ptr[J] != nnz) input_error("dataset: column pointers must span [0, nnz]");
@@ -1861,7 +1882,18 @@ bsccs_dataset* dataset_create(int32_t N, int32_t K, int32_t J, int64_t nnz, cons
         // arrays upload on a side stream (copy and compute overlap)
         if (nnz > 0) {
             h2d(d_rows, rows, sizeof(int32_t) * nnz, s, device);
-            h2d(d_subj, subjects, sizeof(int32_t) * nnz, s, device);
+            if (subjects) {
+                h2d(d_subj, subjects, sizeof(int32_t) * nnz, s, device);
+            } else { // derived on the device: no upload of the redundant array
+                const int sms = sm_count(device);
+                int64_t eb = 0;
+                int32_t* d_esub = dalloc<int32_t>(K, eb, s);
+                k_era_owner<<<grid_for(N, 256, sms), 256, 0, s>>>(ds->subject_offsets, N, K, d_esub);
+                k_subject_of_row<<<grid_for(nnz, 256, sms), 256, 0, s>>>(d_rows, d_esub, K, nnz, d_subj);
+                CUDA_TRY(cudaGetLastError());
+                count_launches(2);
+                dfree(d_esub, s);
+            }
         }
         CUDA_TRY(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
         CUDA_TRY(cudaEventCreateWithFlags(&ev_alloc, cudaEventDisableTiming));

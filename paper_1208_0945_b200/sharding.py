@@ -170,10 +170,11 @@ class RankGroup:
     the sweep kernel -- no host collective on the per-coordinate path.  The
     per-fit log-likelihood is summed exactly through the same words."""
 
-    def __init__(self, shard: Shard, device: int, ctas: int = 0):
+    def __init__(self, shard: Shard, device: int, ctas: int = 0, upload_subjects: bool = True):
         import torch.distributed as dist
         self.rank, self.world = dist.get_rank(), dist.get_world_size()
-        self.dds = DeviceDataset(shard.dataset, device, ctas, (shard.y_dot_x_global, shard.col_nnz_global))
+        self.dds = DeviceDataset(shard.dataset, device, ctas, (shard.y_dot_x_global, shard.col_nnz_global),
+                                 upload_subjects=upload_subjects)
         self.J = shard.dataset.num_drugs
         all_ctas = [None] * self.world
         dist.all_gather_object(all_ctas, self.dds.ctas)

@@ -298,6 +298,48 @@ def test_device_build_validation(corrupt, message):
         B.DeviceDataset(bad, 0)
 
 
+@pytest.mark.parametrize("corrupt,message", [
+    ("row_out_of_range", "invalid pair"),
+    ("rows_not_ascending", "invalid pair"),
+    ("subject_without_eras", "every subject needs at least one era"),
+])
+def test_device_build_validation_derived_subjects(corrupt, message):
+    """subjects = NULL (derived on the device from the rows): the same
+    invariants are still rejected, nothing is read out of range"""
+    from paper_1208_0945_b200 import datagen
+    ds = datagen.fast_sccs(20_000, 30, 3.0)
+    a = [x.copy() for x in ds.arrays()]
+    off, eps, lens, cnts, cptr, rows, subs, ydx = a
+    p = int(cptr[17]) + 5
+    if corrupt == "row_out_of_range":
+        rows[p] = lens.size
+    elif corrupt == "rows_not_ascending":
+        rows[p], rows[p + 1] = rows[p + 1], rows[p]
+    elif corrupt == "subject_without_eras":
+        i = (off.size - 1) // 2
+        off[i + 1] = off[i]
+    bad = B.Dataset(off, eps, lens, cnts, cptr, rows, subs, ydx)
+    with pytest.raises(B.InputError, match=message):
+        B.DeviceDataset(bad, 0, upload_subjects=False)
+
+
+def test_derived_subjects_same_fit():
+    """a dataset created without its per-pair subjects (derived on the
+    device) fits bit for bit like the one created with them"""
+    from paper_1208_0945_b200 import datagen
+    ds = datagen.fast_sccs(60_000, 80, 3.0)
+    prior, cfg = B.laplace_prior(0.2), B.SolverConfig(epsilon=1e-8)
+    a = B.DeviceDataset(ds, 0)
+    b = B.DeviceDataset(ds, 0, upload_subjects=False)
+    assert a.info() == b.info()
+    ra, rb = B.fit(a, prior, cfg), B.fit(b, prior, cfg)
+    assert ra.cycles_run == rb.cycles_run
+    assert np.array_equal(ra.beta_map, rb.beta_map)
+    assert ra.log_posterior == rb.log_posterior
+    a.close()
+    b.close()
+
+
 def test_three_tile_sweep_with_subject_tile():
     """Mean slices of ~500 pairs per CTA (beyond the one-tile kernel's 352,
     inside the three-tile kernel's 1,056) with the subject tile: the
