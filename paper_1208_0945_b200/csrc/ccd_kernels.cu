@@ -1397,6 +1397,9 @@ __global__ void k_build_rq(const int32_t* __restrict__ off, const int32_t* __res
                            const int64_t* __restrict__ csr_ptr, const int32_t* __restrict__ csr_col,
                            const uint32_t* __restrict__ pos, const int32_t* __restrict__ cta_subj, int C,
                            const long long* __restrict__ ovb, int32_t K, int32_t J, RRec* rq, uint16_t* rovf) {
+    extern __shared__ int cs[]; // [C + 1] the CTA subject ranges (searched per era)
+    for (int i = threadIdx.x; i <= C; i += blockDim.x) cs[i] = cta_subj[i];
+    __syncthreads();
     for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < K;
          k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t q0 = csr_ptr[k];
@@ -1406,12 +1409,36 @@ __global__ void k_build_rq(const int32_t* __restrict__ off, const int32_t* __res
         int lo = 0, hi = C + 1; // first c with cta_subj[c] > s
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
-            if (cta_subj[mid] > s) hi = mid;
+            if (cs[mid] > s) hi = mid;
             else lo = mid + 1;
         }
-        const int ls = s - cta_subj[lo - 1];
+        const int ls = s - cs[lo - 1];
         const int n = events[s];
         const int lk = len[k];
+        if (deg - 1 <= kRInline) { // no overflow list: the record is built in registers
+            // the era's drugs, the unit drug J past the end
+            // (every load issued before the first store: one round trip per era)
+            unsigned c[kRInline + 1], pp[kRInline + 1];
+#pragma unroll
+            for (int b = 0; b <= kRInline; ++b) {
+                c[b] = b < deg ? static_cast<unsigned>(csr_col[q0 + b]) : static_cast<unsigned>(J);
+                pp[b] = b < deg ? pos[q0 + b] : 0u;
+            }
+#pragma unroll
+            for (int a = 0; a <= kRInline; ++a) {
+                if (a >= deg) break;
+                unsigned o[kRInline]; // the era's drugs without drug a, in order
+#pragma unroll
+                for (int i = 0; i < kRInline; ++i) o[i] = i < a ? c[i] : c[i + 1];
+                const int4 head = make_int4(ls, lk, (deg - 1) | (a << 8) | (n << 16), 0);
+                const int4 tail = make_int4(static_cast<int>(o[0] | (o[1] << 16)), static_cast<int>(o[2] | (o[3] << 16)),
+                                            static_cast<int>(o[4] | (o[5] << 16)), static_cast<int>(o[6] | (o[7] << 16)));
+                int4* dst = reinterpret_cast<int4*>(rq + pp[a]);
+                dst[0] = head;
+                dst[1] = tail;
+            }
+            continue;
+        }
         long long ov = ovb[s];
         if (ovb[s + 1] != ov)
             for (int k2 = off[s]; k2 < k; ++k2) ov += era_overflow(static_cast<int>(csr_ptr[k2 + 1] - csr_ptr[k2]));
@@ -1738,6 +1765,7 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
             CUDA_TRY(cudaMemcpyAsync(&novf, d_ob + N, sizeof(long long), cudaMemcpyDeviceToHost, s));
             CUDA_TRY(cudaMemcpyAsync(rbad, d_rbad, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
             CUDA_TRY(cudaStreamSynchronize(s));
+            bt.mark("rq: count, scan");
             if (!rbad[0] && novf < (1ll << 31)) {
                 ds->novf = novf;
                 ds->max_deg = std::max(1, rbad[1]);
@@ -1746,12 +1774,13 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
                 int32_t* d_esub = nnz >= K ? d_col : dalloc<int32_t>(K, b5, s); // d_col is free by now
                 k_era_subject<<<grid_for(N, 256, sms), 256, 0, s>>>(ds->subject_offsets, N, d_esub);
                 const int g_rq = static_cast<int>(std::min<int64_t>((static_cast<int64_t>(K) + 255) / 256, 1 << 20));
-                k_build_rq<<<g_rq, 256, 0, s>>>(ds->subject_offsets, d_esub, ds->events_per_subject,
+                k_build_rq<<<g_rq, 256, sizeof(int) * (C + 1), s>>>(ds->subject_offsets, d_esub, ds->events_per_subject,
                                                 ds->era_lengths, ds->csr_ptr, ds->csr_col,
                                                 reinterpret_cast<const uint32_t*>(d_rows), ds->cta_subj, C, d_ob, K, J,
                                                 ds->rq, ds->rovf);
                 if (d_esub != d_col) dfree(d_esub, s);
                 count_launches(1);
+                bt.mark("rq: records");
                 CUDA_TRY(cudaMemsetAsync(ds->edeg, 0, static_cast<size_t>(K) + 32, s));
                 CUDA_TRY(cudaMemsetAsync(ds->ecol, 0, sizeof(uint16_t) * (nnz + 16), s));
                 k_compact_csr<<<grid_for(std::max<int64_t>(K, nnz), 256, sms), 256, 0, s>>>(ds->csr_ptr, ds->csr_col,

@@ -23,7 +23,7 @@ prior = B.laplace_prior(0.1)
 for r in range(reps):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    d = B.DeviceDataset(host, device=0)
+    d = B.DeviceDataset(host, device=0, upload_subjects=False)
     t1 = time.perf_counter()
     res = B.fit(d, prior)
     t2 = time.perf_counter()
