@@ -1324,20 +1324,32 @@ __global__ void k_build_pq(const int2* __restrict__ pairs, int64_t nnz, const in
 // The CSR sort carries each pair's CSC position with its column, so the
 // records are written per era from its (contiguous) drug list: one 32-B
 // store per pair, no per-pair search.
-__global__ void k_iota(uint32_t* out, int64_t nnz) {
+// Each CSC position with its run flags in bits 30 / 31 (the sort carries
+// them to the CSR order, where k_build_rq puts them into the record): the
+// pair heads a run of its subject in its column (the previous pair is in
+// another column or another subject's), the next pair continues the run.
+// CTA slices are subject-aligned, so these are the per-slice run flags.
+constexpr uint32_t kPosMask = (1u << 30) - 1;
+__global__ void k_iota_flags(const int2* __restrict__ pairs, const int32_t* __restrict__ col_of, int64_t nnz,
+                             uint32_t* out) {
     for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < nnz;
-         p += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        out[p] = static_cast<uint32_t>(p);
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int s = pairs[p].y, j = col_of[p];
+        const bool head = p == 0 || col_of[p - 1] != j || pairs[p - 1].y != s;
+        const bool cont = p + 1 < nnz && col_of[p + 1] == j && pairs[p + 1].y == s;
+        out[p] = static_cast<uint32_t>(p) | (head ? 1u << 30 : 0u) | (cont ? 1u << 31 : 0u);
+    }
 }
-// csr_col holds each CSR entry's CSC position after the sort: keep it in pos,
+// csr_col holds each CSR entry's CSC position (and run flags) after the sort: keep it in pos,
 // and the entry's column in csr_col -- found by binary search in col_ptr
 // (L1-resident) rather than a random gather of the per-pair column array
 __global__ void k_pos_col(int32_t* csr_col, const int64_t* __restrict__ col_ptr, int32_t J, int64_t nnz,
                           uint32_t* pos) {
     for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < nnz;
          q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const uint32_t p = static_cast<uint32_t>(csr_col[q]);
-        pos[q] = p;
+        const uint32_t raw = static_cast<uint32_t>(csr_col[q]);
+        const uint32_t p = raw & kPosMask;
+        pos[q] = raw; // (with the run flags)
         int lo = 0, hi = J; // last column j with col_ptr[j] <= p
         while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
@@ -1422,7 +1434,7 @@ __global__ void k_build_rq(const int32_t* __restrict__ off, const int32_t* __res
 #pragma unroll
             for (int b = 0; b <= kRInline; ++b) {
                 c[b] = b < deg ? static_cast<unsigned>(csr_col[q0 + b]) : static_cast<unsigned>(J);
-                pp[b] = b < deg ? pos[q0 + b] : 0u;
+                pp[b] = b < deg ? pos[q0 + b] : 0u; // CSC position | run flags << 30
             }
 #pragma unroll
             for (int a = 0; a <= kRInline; ++a) {
@@ -1430,10 +1442,10 @@ __global__ void k_build_rq(const int32_t* __restrict__ off, const int32_t* __res
                 unsigned o[kRInline]; // the era's drugs without drug a, in order
 #pragma unroll
                 for (int i = 0; i < kRInline; ++i) o[i] = i < a ? c[i] : c[i + 1];
-                const int4 head = make_int4(ls, lk, (deg - 1) | (a << 8) | (n << 16), 0);
+                const int4 head = make_int4(ls, lk, (deg - 1) | static_cast<int>((pp[a] >> 30) << 8) | (n << 16), 0);
                 const int4 tail = make_int4(static_cast<int>(o[0] | (o[1] << 16)), static_cast<int>(o[2] | (o[3] << 16)),
                                             static_cast<int>(o[4] | (o[5] << 16)), static_cast<int>(o[6] | (o[7] << 16)));
-                int4* dst = reinterpret_cast<int4*>(rq + pp[a]);
+                int4* dst = reinterpret_cast<int4*>(rq + (pp[a] & kPosMask));
                 dst[0] = head;
                 dst[1] = tail;
             }
@@ -1446,7 +1458,8 @@ __global__ void k_build_rq(const int32_t* __restrict__ off, const int32_t* __res
             RRec r;
             r.ls = ls;
             r.len = lk;
-            r.meta = (deg - 1) | (a << 8) | (n << 16); // a: the pair's drug sorts after a other drugs
+            const uint32_t pa = pos[q0 + a];
+            r.meta = (deg - 1) | static_cast<int>((pa >> 30) << 8) | (n << 16); // run flags: head bit 8, cont bit 9
             r.ovf = deg - 1 > kRInline ? static_cast<int32_t>(ov) : 0;
             int i = 0;
             for (int b = 0; b < deg; ++b) {
@@ -1462,7 +1475,7 @@ __global__ void k_build_rq(const int32_t* __restrict__ off, const int32_t* __res
                 for (int t = deg - 1 - kRInline; t < ext; ++t) rovf[ov + t] = static_cast<uint16_t>(J);
                 ov += ext;
             }
-            rq[pos[q0 + a]] = r;
+            rq[pa & kPosMask] = r;
         }
     }
 }
@@ -1596,7 +1609,7 @@ void alloc_dataset(bsccs_dataset* ds) {
     // pair records of the resident-beta sweep, allocated before the build's
     // temporaries (a stable allocation order lets the pool reuse blocks
     // across dataset rebuilds); freed again if the dataset does not qualify
-    if (rcd_enabled() && nnz > 0 && nnz < (1ll << 32) && J < 65535) { // u16 drugs, index J the unit drug
+    if (rcd_enabled() && nnz > 0 && nnz < (1ll << 30) && J < 65535) { // u16 drugs, index J the unit drug; 30-bit positions
         ds->rq = dalloc<RRec>(nnz, B, s);
         ds->edeg = dalloc<uint8_t>(static_cast<int64_t>(K) + 32, B, s);
         ds->ecol = dalloc<uint16_t>(nnz + 16, B, s);
@@ -1678,7 +1691,7 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
         // the sort then carries positions, the columns are gathered after
         if (want_rq) {
             d_iota = dalloc<uint32_t>(nnz, scratch_bytes, s);
-            k_iota<<<grid_for(nnz, 256, sms), 256, 0, s>>>(d_iota, nnz);
+            k_iota_flags<<<grid_for(nnz, 256, sms), 256, 0, s>>>(ds->pairs, d_col, nnz, d_iota);
             count_launches(1);
             CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, d_rows, d_subj, d_iota,
                                                      reinterpret_cast<uint32_t*>(ds->csr_col), nnz, 0, end_bit, s));

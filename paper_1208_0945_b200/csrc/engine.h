@@ -57,6 +57,7 @@ constexpr int kBlockChunk = 64;   // subjects packed per build thread (each chun
 // era ascending (0xffff padding).  A pair's x'beta is rebuilt from these and beta in the
 // order of engine.hpp:173-181.
 struct alignas(16) RRec {
+    // meta: other drugs (bits 0-7) | run head (bit 8) | run continues (bit 9) | n_i << 16
     int32_t ls, len, meta, ovf;
     uint16_t o[8];
 };

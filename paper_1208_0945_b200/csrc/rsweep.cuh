@@ -166,6 +166,8 @@ __device__ __forceinline__ void r_speculate(const RRec* rb, int n, int jn, int j
     uint32_t w[kRT][4];
     int cnt[kRT], ovo[kRT];
     P.dep = 0u;
+    P.head = 0u;
+    P.cont = 0u;
     bool any_ovf = false;
     const uint32_t unit2 = static_cast<uint32_t>(junit) * 0x10001u; // two unit drugs (padding)
 #pragma unroll
@@ -177,6 +179,10 @@ __device__ __forceinline__ void r_speculate(const RRec* rb, int n, int jn, int j
         P.ls[v] = static_cast<int>(a.x);
         P.len[v] = static_cast<int>(a.y);
         cnt[v] = static_cast<int>(a.z & 0xffu);
+        // run head / continuation: static per slice, carried in the record
+        // (meta bits 8 and 9, k_iota_flags); an empty slot reads 0
+        P.head |= ((a.z >> 8) & 1u) << v;
+        P.cont |= ((a.z >> 9) & 1u) << v;
         w[v][0] = o.x;
         w[v][1] = o.y;
         w[v][2] = o.z;
@@ -184,21 +190,6 @@ __device__ __forceinline__ void r_speculate(const RRec* rb, int n, int jn, int j
         P.pre[v] = 1.0;
         any_ovf = any_ovf || cnt[v] > kRInline;
         ovo[v] = static_cast<int>(a.w);
-    }
-    // run heads (the subject changes from the previous pair; lane 0 reads it)
-    P.head = 0u;
-    P.cont = 0u;
-#pragma unroll
-    for (int v = 0; v < kRT; ++v) {
-        const int pos = slot_pos(v);
-        int prev = __shfl_up_sync(0xffffffffu, P.ls[v], 1);
-        int next = __shfl_down_sync(0xffffffffu, P.ls[v], 1);
-        if (lane_id() == 0) prev = pos > 0 && pos < n ? rb[pos - 1].ls : -1;
-        if (lane_id() == 31) next = pos + 1 < n ? rb[pos + 1].ls : -2;
-        if (r_slot_valid(v, n)) {
-            if (pos == 0 || prev != P.ls[v]) P.head |= 1u << v;
-            if (pos + 1 < n && next == P.ls[v]) P.cont |= 1u << v;
-        }
     }
 #if RCD_DEN_EARLY
     if constexpr (!kSS) {
