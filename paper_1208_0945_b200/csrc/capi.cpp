@@ -167,15 +167,14 @@ void fit_loop(FitContext& fc, const PriorParams& prior, const bsccs_solver_confi
             ++res->dense_refreshes;
         }
     }
-    agreed(agree, [&] {
-        for (auto* st : fc.states) dense_recompute(st, nullptr); // report from a clean rebuild
-    });
-    ++res->dense_refreshes;
+    // report from a clean rebuild (solver.hpp:192-196): the refresh and the
+    // log-likelihood in one pass, the state rebuilt on its next use
     CUDA_TRY(cudaMemcpy(beta_out, s0->beta, sizeof(double) * J, cudaMemcpyDeviceToHost));
     double ll = 0.0;
     agreed(agree, [&] {
-        for (auto* st : fc.states) ll += log_likelihood(st);
+        for (auto* st : fc.states) ll += final_log_likelihood(st);
     });
+    ++res->dense_refreshes;
     ll = allreduce_sum(ll);
     res->log_posterior = ll + log_density(prior, beta_out, J);
     res->sweep_seconds = s0->sweep_ms * 1e-3;
@@ -207,13 +206,12 @@ bsccs_state* acquire_state(const bsccs_dataset* ds, const double* init_beta) {
                     if (init_beta)
                         CUDA_TRY(cudaMemcpyAsync(st->beta, init_beta, sizeof(double) * ds->J, cudaMemcpyHostToDevice,
                                                  st->stream));
-                    else
-                        CUDA_TRY(cudaMemsetAsync(st->beta, 0, sizeof(double) * ds->J, st->stream));
                 } catch (...) {
                     e.second.busy = false;
                     throw;
                 }
-                dense_recompute(st, nullptr);
+                if (init_beta) dense_recompute(st, nullptr);
+                else dense_recompute_zero(st); // cold start: no CSR pass
                 return st;
             }
         }

@@ -73,6 +73,7 @@ constexpr int kD = kT - 32;         // data threads (warps 1..): tile v holds pa
 constexpr int kWarps = kT / 32;
 constexpr int kLLBlocks = 592;      // fixed => deterministic LL reduction
 constexpr int kLLThreads = 256;
+constexpr int kFLBlocks = 2 * kLLBlocks; // k_final_xb / k_final_den (a fit's closing log-likelihood)
 constexpr double kXbBound = 700.0;  // xbeta_bound<double> engine.hpp:20-23
 // the same bound on exp(x'beta) (k_rcd): exp(+-700) as doubles
 constexpr double kExpXbMax = 0x1.d945df4f8ec8ep+1009; // exp(700)
@@ -1056,13 +1057,86 @@ __global__ void k_ll_partial(const double* X, const int32_t* __restrict__ row_sl
     }
 }
 
-__global__ void k_ll_final(const double* partial, int n, DevResult* res) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        double x = 0.0, y = 0.0;
-        for (int b = 0; b < n; ++b) {
-            x = __dadd_rn(x, partial[2 * b]);
-            y = __dadd_rn(y, partial[2 * b + 1]);
+// block sum of (a, b) in a fixed order into partial[2 * block + slot] (slot
+// 0: a, 1: b; the k_ll_final layout)
+__device__ __forceinline__ void ll_block_sum(double v, double* partial, int slot) {
+    __shared__ double sv[kLLThreads / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((threadIdx.x & 31) == 0) sv[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double x = 0.0;
+        for (int w = 0; w < kLLThreads / 32; ++w) x = __dadd_rn(x, sv[w]);
+        partial[2 * blockIdx.x + slot] = x;
+    }
+}
+
+// The fit's closing refresh and log-likelihood (solver.hpp:192-196:
+// dense_recompute, then log_likelihood, engine.hpp:68-90,404-425) without
+// rebuilding the subject blocks.  Pass 1, one thread per era: x'beta from the
+// row-major copy (k_dense_xb's sum and overflow check) into the criterion
+// snapshot (what the refresh leaves there) and the linear term.  Pass 2, one
+// thread per subject: the denominator from the snapshot (k_dense_den's sum)
+// and the log term.  The blocks are rebuilt from beta on the state's next
+// use (bsccs_state::dense_pending).
+__global__ void k_final_xb(const int64_t* __restrict__ csr_ptr, const int32_t* __restrict__ csr_col,
+                           const double* __restrict__ beta, const int32_t* __restrict__ y, int32_t K, double* snap,
+                           double* partial, DevErr* err) {
+    double lin = 0.0;
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < K;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double xb = 0.0;
+        for (int64_t q = csr_ptr[k]; q < csr_ptr[k + 1]; ++q) {
+            const double b = beta[csr_col[q]];
+            if (b != 0.0) xb = __dadd_rn(xb, b);
         }
+        if (!(fabs(xb) <= kXbBound)) record_error(err, DERR_OVERFLOW, fabs(xb));
+        snap[k] = xb;
+        const int yk = y[k];
+        if (yk != 0) lin = __dadd_rn(lin, __dmul_rn(static_cast<double>(yk), xb));
+    }
+    ll_block_sum(lin, partial, 0);
+}
+__global__ void k_final_den(const double* __restrict__ snap, const int32_t* __restrict__ len,
+                            const int32_t* __restrict__ off, const int32_t* __restrict__ eps, int32_t N,
+                            double* partial, DevErr* err) {
+    double lg = 0.0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < N;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double total = 0.0;
+        for (int k = off[i]; k < off[i + 1]; ++k) total = __dadd_rn(total, lexp(len[k], snap[k]));
+        if (!(total > 0.0)) record_error(err, DERR_LL_DEN_NONPOSITIVE, total);
+        lg = __dadd_rn(lg, __dmul_rn(static_cast<double>(eps[i]), log(total)));
+    }
+    ll_block_sum(lg, partial, 1);
+}
+
+// cold start (beta = 0): x'beta = 0 in every era without reading the CSR
+// (k_dense_den then sums l * exp(0))
+__global__ void k_zero_xb(double* X, double* snap, const int32_t* __restrict__ row_slot, int32_t K) {
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < K;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        X[row_slot[k]] = 0.0;
+        snap[k] = 0.0;
+    }
+}
+
+// one warp, fixed order: lane l sums the partials b = l mod 32 ascending,
+// then a butterfly
+__global__ void k_ll_final(const double* partial, int n, DevResult* res) {
+    if (blockIdx.x != 0 || threadIdx.x >= 32) return;
+    double x = 0.0, y = 0.0;
+    for (int b = static_cast<int>(threadIdx.x); b < n; b += 32) {
+        x = __dadd_rn(x, partial[2 * b]);
+        y = __dadd_rn(y, partial[2 * b + 1]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        x = __dadd_rn(x, __shfl_xor_sync(0xffffffffu, x, o));
+        y = __dadd_rn(y, __shfl_xor_sync(0xffffffffu, y, o));
+    }
+    if (threadIdx.x == 0) {
         res->ll_linear = x;
         res->ll_logden = y;
     }
@@ -2000,14 +2074,18 @@ void dataset_destroy(bsccs_dataset* ds) {
 
 namespace {
 
-void launch_dense(bsccs_state* st) {
+void launch_dense(bsccs_state* st, bool beta_zero = false) {
     const bsccs_dataset* ds = st->ds;
     const int g = build_grid(ds->device);
-    k_dense_xb<<<g, 256, 0, st->stream>>>(st->X, st->snap, ds->csr_ptr, ds->csr_col, st->beta, ds->row_slot, ds->K,
-                                          st->err);
+    if (beta_zero)
+        k_zero_xb<<<g, 256, 0, st->stream>>>(st->X, st->snap, ds->row_slot, ds->K);
+    else
+        k_dense_xb<<<g, 256, 0, st->stream>>>(st->X, st->snap, ds->csr_ptr, ds->csr_col, st->beta, ds->row_slot,
+                                              ds->K, st->err);
     k_dense_den<<<g, 256, 0, st->stream>>>(st->X, ds->era_lengths, ds->subject_offsets, ds->bstart, ds->N, st->denc);
-    CUDA_TRY(cudaGetLastError());
     count_launches(2);
+    CUDA_TRY(cudaGetLastError());
+    st->dense_pending = false;
     st->snap_valid = true;
     st->x_stale = false;
     st->denc_valid = st->denc != nullptr;
@@ -2030,7 +2108,7 @@ void alloc_state(bsccs_state* st, const bsccs_dataset* ds) {
     st->counter = dalloc<unsigned long long>(1, b, s);
     st->err = dalloc<DevErr>(1, b, s);
     st->res = dalloc<DevResult>(1, b, s);
-    st->scratch = dalloc<double>(2 * kLLBlocks, b, s);
+    st->scratch = dalloc<double>(2 * kFLBlocks, b, s);
     if (ds->rq) {
         st->denc = dalloc<double>(ds->N, b, s);
         st->beta_prev = dalloc<double>(ds->J, b, s);
@@ -2063,7 +2141,7 @@ bsccs_state* state_create(const bsccs_dataset* ds, const double* beta_host) {
             CUDA_TRY(cudaMemcpyAsync(st->beta, beta_host, sizeof(double) * ds->J, cudaMemcpyHostToDevice, st->stream));
         else
             CUDA_TRY(cudaMemsetAsync(st->beta, 0, sizeof(double) * ds->J, st->stream));
-        launch_dense(st);
+        launch_dense(st, beta_host == nullptr);
         sync_and_check(st);
         check_err_block(st);
     } catch (...) {
@@ -2132,7 +2210,17 @@ void state_destroy(bsccs_state* st) {
 // X (subject blocks) brought up to date after resident-beta sweeps: x'beta
 // rebuilt from beta (the value those sweeps use) with its snapshot, the
 // headers from the compact denominators.
+// the closing refresh a fit skipped (k_final_xb / k_final_den), done before the state's
+// next use
+void settle_dense(bsccs_state* st) {
+    if (!st->dense_pending) return;
+    launch_dense(st);
+    sync_and_check(st);
+    check_err_block(st);
+}
+
 void sync_x(bsccs_state* st) {
+    settle_dense(st);
     if (!st->x_stale) return;
     const bsccs_dataset* ds = st->ds;
     const int g = build_grid(ds->device);
@@ -2147,12 +2235,40 @@ void sync_x(bsccs_state* st) {
 
 // compact denominators from the headers (after an op that wrote X)
 void sync_denc(bsccs_state* st) {
+    settle_dense(st);
     if (st->denc_valid || !st->denc) return;
     const bsccs_dataset* ds = st->ds;
     k_hdr_to_denc<<<build_grid(ds->device), 256, 0, st->stream>>>(st->X, ds->bstart, st->denc, ds->N);
     CUDA_TRY(cudaGetLastError());
     count_launches(1);
     st->denc_valid = true;
+}
+
+void dense_recompute_zero(bsccs_state* st) {
+    NvtxRange nvtx_("dense_recompute (beta = 0)");
+    DeviceGuard g(st->ds->device);
+    CUDA_TRY(cudaMemsetAsync(st->beta, 0, sizeof(double) * st->ds->J, st->stream));
+    launch_dense(st, true);
+    sync_and_check(st);
+    check_err_block(st);
+}
+
+double final_log_likelihood(bsccs_state* st) {
+    NvtxRange nvtx_("final refresh + log_likelihood");
+    const bsccs_dataset* ds = st->ds;
+    DeviceGuard dg(ds->device);
+    k_final_xb<<<kFLBlocks, kLLThreads, 0, st->stream>>>(ds->csr_ptr, ds->csr_col, st->beta, ds->event_counts, ds->K,
+                                                         st->snap, st->scratch, st->err);
+    k_final_den<<<kFLBlocks, kLLThreads, 0, st->stream>>>(st->snap, ds->era_lengths, ds->subject_offsets,
+                                                          ds->events_per_subject, ds->N, st->scratch, st->err);
+    k_ll_final<<<1, 32, 0, st->stream>>>(st->scratch, kFLBlocks, st->res);
+    count_launches(3);
+    CUDA_TRY(cudaMemcpyAsync(st->res_h, st->res, sizeof(DevResult), cudaMemcpyDeviceToHost, st->stream));
+    sync_and_check(st);
+    check_err_block(st);
+    st->dense_pending = true; // the blocks are rebuilt on their next use
+    st->snap_valid = true;
+    return st->res_h->ll_linear - st->res_h->ll_logden;
 }
 
 void dense_recompute(bsccs_state* st, const double* beta_host) {

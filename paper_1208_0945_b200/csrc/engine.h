@@ -180,6 +180,9 @@ struct bsccs_state {
     double sweep_ms = 0.0;  // accumulated sweep-kernel time
     double alg_bytes = 0.0; // accumulated algorithmic bytes of the sweeps
     bool snap_valid = false;
+    // a fit ended with k_final_xb / k_final_den (its closing refresh computed, not
+    // written): the next use of the state rebuilds it (settle_dense)
+    bool dense_pending = false;
 };
 
 namespace bsccs_b200 {
@@ -237,6 +240,10 @@ void state_destroy(bsccs_state* st);
 
 // ---- engine ops (all synchronous on the state's stream) -----------------
 void dense_recompute(bsccs_state* st, const double* beta_host); // nullptr: from state beta
+void dense_recompute_zero(bsccs_state* st);                      // beta := 0 and the state it implies
+// the closing dense refresh and log-likelihood of a fit, without writing the
+// state back (rebuilt on its next use)
+double final_log_likelihood(bsccs_state* st);
 void grad_hess(bsccs_state* st, int32_t j, double* g, double* h);
 void sparse_update(bsccs_state* st, int32_t j, double delta);
 double log_likelihood(bsccs_state* st);
