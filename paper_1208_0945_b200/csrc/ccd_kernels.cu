@@ -1994,26 +1994,46 @@ bsccs_dataset* dataset_create(int32_t N, int32_t K, int32_t J, int64_t nnz, cons
         int64_t scratch_bytes = 0;
         int32_t* d_rows = dalloc<int32_t>(nnz, scratch_bytes, s);
         int32_t* d_subj = dalloc<int32_t>(nnz, scratch_bytes, s);
-        // the pair arrays first: the build starts on them while the era
-        // arrays upload on a side stream (copy and compute overlap)
-        if (nnz > 0) {
-            h2d(d_rows, rows, sizeof(int32_t) * nnz, s, device);
-            if (subjects) {
-                h2d(d_subj, subjects, sizeof(int32_t) * nnz, s, device);
-            } else { // derived on the device: no upload of the redundant array
-                const int sms = sm_count(device);
-                int64_t eb = 0;
-                int32_t* d_esub = dalloc<int32_t>(K, eb, s);
-                k_era_owner<<<grid_for(N, 256, sms), 256, 0, s>>>(ds->subject_offsets, N, K, d_esub);
-                k_subject_of_row<<<grid_for(nnz, 256, sms), 256, 0, s>>>(d_rows, d_esub, K, nnz, d_subj);
-                CUDA_TRY(cudaGetLastError());
-                count_launches(2);
-                dfree(d_esub, s);
-            }
-        }
         CUDA_TRY(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
         CUDA_TRY(cudaEventCreateWithFlags(&ev_alloc, cudaEventDisableTiming));
         CUDA_TRY(cudaEventCreateWithFlags(&ev_era, cudaEventDisableTiming));
+        // the pair arrays first: the build starts on them while the era
+        // arrays upload on a side stream (copy and compute overlap)
+        if (nnz > 0 && subjects) {
+            h2d(d_rows, rows, sizeof(int32_t) * nnz, s, device);
+            h2d(d_subj, subjects, sizeof(int32_t) * nnz, s, device);
+        } else if (nnz > 0) { // subjects derived on the device: no upload of the redundant array
+            // rows in chunks on the side stream; each chunk's owners are looked
+            // up (a gather per pair) while the next chunk is on the link
+            const int sms = sm_count(device);
+            int64_t eb = 0;
+            int32_t* d_esub = dalloc<int32_t>(K, eb, s);
+            k_era_owner<<<grid_for(N, 256, sms), 256, 0, s>>>(ds->subject_offsets, N, K, d_esub);
+            CUDA_TRY(cudaEventRecord(ev_alloc, s));
+            CUDA_TRY(cudaStreamWaitEvent(s2, ev_alloc, 0));
+            constexpr int kRowChunks = 4;
+            cudaEvent_t evc[kRowChunks] = {};
+            try {
+                for (int c = 0; c < kRowChunks; ++c) {
+                    const int64_t a = nnz * c / kRowChunks, b = nnz * (c + 1) / kRowChunks;
+                    CUDA_TRY(cudaEventCreateWithFlags(&evc[c], cudaEventDisableTiming));
+                    if (b > a) h2d(d_rows + a, rows + a, sizeof(int32_t) * (b - a), s2, device);
+                    CUDA_TRY(cudaEventRecord(evc[c], s2));
+                    CUDA_TRY(cudaStreamWaitEvent(s, evc[c], 0));
+                    if (b > a)
+                        k_subject_of_row<<<grid_for(b - a, 256, sms), 256, 0, s>>>(d_rows + a, d_esub, K, b - a,
+                                                                                    d_subj + a);
+                }
+            } catch (...) {
+                for (auto e : evc)
+                    if (e) cudaEventDestroy(e);
+                throw;
+            }
+            for (auto e : evc) cudaEventDestroy(e);
+            CUDA_TRY(cudaGetLastError());
+            count_launches(1 + kRowChunks);
+            dfree(d_esub, s);
+        }
         CUDA_TRY(cudaEventRecord(ev_alloc, s)); // the era arrays were allocated on s
         CUDA_TRY(cudaStreamWaitEvent(s2, ev_alloc, 0));
         h2d(ds->era_lengths, era_lengths, sizeof(int32_t) * K, s2, device);
