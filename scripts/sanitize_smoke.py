@@ -12,6 +12,10 @@ set_sweep = _native.lib().bsccs_debug_set_sweep
 ds = datagen.fast_sccs(3000, 20, 3.0)
 dds = ds.on_device()
 r = B.fit(dds, B.laplace_prior(0.1))  # k_rcd, subject tile
+dnull = B.DeviceDataset(ds, 0, upload_subjects=False)  # per-pair subjects derived on the device (chunked rows)
+B.fit(dnull, B.laplace_prior(0.1))
+B.fit(dnull, B.laplace_prior(0.1), init_beta=np.full(ds.num_drugs, 0.01))  # warm start: full dense prologue
+dnull.close()
 set_sweep(0, 0.05)
 B.fit(dds, B.normal_prior(2.0))  # k_rcd handing cycles over to k_ccd (lowered range bound)
 set_sweep(0, 0.0)
