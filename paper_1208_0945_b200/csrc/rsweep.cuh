@@ -612,7 +612,12 @@ __global__ void __launch_bounds__(kT, 1) k_rcd(const __grid_constant__ SweepArgs
                         } else {
                             st_keep(S.denc + subj_base + s, den[v], pol_keep);
                             sm.jden[slot_pos(v)] = den[v];
-                            htab[s & (kHTab - 1)] = make_int2(s, slot_pos(v));
+                            // colliding subjects may race for an entry: either
+                            // (subject, position) pair is valid, the reader checks the
+                            // subject (an atomic exchange: one 8-B write, no torn pair)
+                            atomicExch(reinterpret_cast<unsigned long long*>(&htab[s & (kHTab - 1)]),
+                                       static_cast<unsigned long long>(static_cast<unsigned>(s)) |
+                                           (static_cast<unsigned long long>(static_cast<unsigned>(slot_pos(v))) << 32));
                             atomicOr(&bmcur[s >> 5], 1u << (s & 31));
                             clr_sub[v] = s;
                         }
