@@ -1417,14 +1417,32 @@ __global__ void k_iota_flags(const int2* __restrict__ pairs, const int32_t* __re
 // csr_col holds each CSR entry's CSC position (and run flags) after the sort: keep it in pos,
 // and the entry's column in csr_col -- found by binary search in col_ptr
 // (L1-resident) rather than a random gather of the per-pair column array
-__global__ void k_pos_col(int32_t* csr_col, const int64_t* __restrict__ col_ptr, int32_t J, int64_t nnz,
-                          uint32_t* pos) {
+// (the search starts from a bucket table: the column holding position
+// b << kPosBucketBits, so a column of typical size takes one or two steps)
+constexpr int kPosBucketBits = 14;
+__global__ void k_pos_buckets(const int64_t* __restrict__ col_ptr, int32_t J, int64_t nnz, int32_t* bucket) {
+    const int64_t nb = ((nnz - 1) >> kPosBucketBits) + 2;
+    for (int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; b < nb;
+         b += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t p = min(b << kPosBucketBits, nnz - 1);
+        int lo = 0, hi = J; // last column j with col_ptr[j] <= p
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (col_ptr[mid] <= p) lo = mid;
+            else hi = mid;
+        }
+        bucket[b] = lo;
+    }
+}
+__global__ void k_pos_col(int32_t* csr_col, const int64_t* __restrict__ col_ptr, const int32_t* __restrict__ bucket,
+                          int64_t nnz, uint32_t* pos) {
     for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < nnz;
          q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const uint32_t raw = static_cast<uint32_t>(csr_col[q]);
         const uint32_t p = raw & kPosMask;
         pos[q] = raw; // (with the run flags)
-        int lo = 0, hi = J; // last column j with col_ptr[j] <= p
+        const int b = static_cast<int>(p >> kPosBucketBits);
+        int lo = __ldg(bucket + b), hi = __ldg(bucket + b + 1) + 1; // last column j in [lo, hi) with col_ptr[j] <= p
         while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
             if (__ldg(col_ptr + mid) <= static_cast<int64_t>(p)) lo = mid;
@@ -1780,9 +1798,13 @@ void finish_dataset(bsccs_dataset* ds, int32_t* d_rows, int32_t* d_subj, const i
             CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, d_rows, d_subj, d_iota,
                                                      reinterpret_cast<uint32_t*>(ds->csr_col), nnz, 0, end_bit, s));
             // d_rows (the consumed keys) receives the CSC positions
-            k_pos_col<<<grid_for(nnz, 256, sms), 256, 0, s>>>(ds->csr_col, ds->col_ptr, J, nnz,
+            const int64_t nbk = ((nnz - 1) >> kPosBucketBits) + 2;
+            int32_t* d_bk = dalloc<int32_t>(nbk, scratch_bytes, s);
+            k_pos_buckets<<<grid_for(nbk, 256, sms), 256, 0, s>>>(ds->col_ptr, J, nnz, d_bk);
+            k_pos_col<<<grid_for(nnz, 256, sms), 256, 0, s>>>(ds->csr_col, ds->col_ptr, d_bk, nnz,
                                                                reinterpret_cast<uint32_t*>(d_rows));
-            count_launches(1);
+            count_launches(2);
+            dfree(d_bk, s);
             dfree(d_iota, s);
         } else if (nnz > 0) {
             // keys: rows (consumed); d_subj is free after interleave and
