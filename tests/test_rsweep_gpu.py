@@ -206,3 +206,28 @@ def test_every_shape_matches_reference(port, ctas, drugs, subjects, lam, shape):
         assert _native.lib().bsccs_debug_last_rcd_shape() == shape
         assert_parity(res, port.fit(ds, prior, cfg))
     dds.close()
+
+
+def test_skewed_and_empty_columns(port):
+    """Zipf drug prevalence over 3,000 drugs (a few columns hold most pairs,
+    many a handful, many none): the build's column lookup (bucket table over
+    the column pointers) and the records of tiny columns, with the per-pair
+    subjects uploaded or derived on the device, against the C oracle"""
+    g = np.random.default_rng(5)
+    J = 3000
+    recs = []
+    for sidx in range(4000):
+        eras = []
+        for _ in range(int(g.integers(1, 6))):
+            drugs = sorted({int(min(J - 1, g.zipf(1.3) - 1)) for _ in range(int(g.integers(0, 5)))})
+            eras.append(B.Era(int(g.integers(1, 60)), int(g.integers(0, 3)), drugs))
+        recs.append(B.SubjectRecord(f"s{sidx}", eras))
+    ds = B.build_dataset(recs, J)
+    nnz_col = np.diff(ds.col_ptr)
+    assert (nnz_col == 0).sum() > J // 2 and nnz_col.max() > 1000
+    cfg = B.SolverConfig(epsilon=1e-7)
+    for upload in (True, False):
+        dds = B.DeviceDataset(ds, 0, upload_subjects=upload)
+        res = B.fit(dds, B.laplace_prior(0.1), cfg)
+        assert_parity(res, port.fit(ds, B.laplace_prior(0.1), cfg))
+        dds.close()
