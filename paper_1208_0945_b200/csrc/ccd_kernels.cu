@@ -1112,6 +1112,18 @@ __global__ void k_final_den(const double* __restrict__ snap, const int32_t* __re
     ll_block_sum(lg, partial, 1);
 }
 
+// cold start (beta = 0) for the resident-beta sweep: the compact
+// denominators sum l * exp(0) (k_dense_den's value); x'beta and the subject
+// blocks are rebuilt from beta when an op reads them (x_stale)
+__global__ void k_den_zero(const int32_t* __restrict__ len, const int32_t* __restrict__ off, int32_t N, double* denc) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < N;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double total = 0.0;
+        for (int k = off[i]; k < off[i + 1]; ++k) total = __dadd_rn(total, lexp(len[k], 0.0));
+        denc[i] = total;
+    }
+}
+
 // cold start (beta = 0): x'beta = 0 in every era without reading the CSR
 // (k_dense_den then sums l * exp(0))
 __global__ void k_zero_xb(double* X, double* snap, const int32_t* __restrict__ row_slot, int32_t K) {
@@ -2288,9 +2300,21 @@ void sync_denc(bsccs_state* st) {
 
 void dense_recompute_zero(bsccs_state* st) {
     NvtxRange nvtx_("dense_recompute (beta = 0)");
-    DeviceGuard g(st->ds->device);
-    CUDA_TRY(cudaMemsetAsync(st->beta, 0, sizeof(double) * st->ds->J, st->stream));
-    launch_dense(st, true);
+    const bsccs_dataset* ds = st->ds;
+    DeviceGuard g(ds->device);
+    CUDA_TRY(cudaMemsetAsync(st->beta, 0, sizeof(double) * ds->J, st->stream));
+    if (st->denc) { // the resident-beta sweep needs only the denominators
+        k_den_zero<<<build_grid(ds->device), 256, 0, st->stream>>>(ds->era_lengths, ds->subject_offsets, ds->N,
+                                                                    st->denc);
+        CUDA_TRY(cudaGetLastError());
+        count_launches(1);
+        st->denc_valid = true;
+        st->x_stale = true; // x'beta (0) and the headers on first use (sync_x)
+        st->snap_valid = false;
+        st->dense_pending = false;
+    } else {
+        launch_dense(st, true);
+    }
     sync_and_check(st);
     check_err_block(st);
 }
