@@ -2195,7 +2195,15 @@ bsccs_state* state_create(const bsccs_dataset* ds, const double* beta_host) {
             CUDA_TRY(cudaMemcpyAsync(st->beta, beta_host, sizeof(double) * ds->J, cudaMemcpyHostToDevice, st->stream));
         else
             CUDA_TRY(cudaMemsetAsync(st->beta, 0, sizeof(double) * ds->J, st->stream));
-        launch_dense(st, beta_host == nullptr);
+        if (!beta_host && st->denc) { // cold start for the resident-beta sweep (dense_recompute_zero)
+            k_den_zero<<<grid, 256, 0, st->stream>>>(ds->era_lengths, ds->subject_offsets, ds->N, st->denc);
+            count_launches(1);
+            st->denc_valid = true;
+            st->x_stale = true;
+            st->snap_valid = false;
+        } else {
+            launch_dense(st, beta_host == nullptr);
+        }
         sync_and_check(st);
         check_err_block(st);
     } catch (...) {
