@@ -155,7 +155,7 @@ void cv_select(const std::vector<double>& grid, int32_t folds, const bsccs_cv_ce
         if (!usable) continue;
         const double mean = total / static_cast<double>(folds);
         if (mean_out) mean_out[g] = mean;
-        // ascending grid plus strict inequality breaks ties downward
+        // first maximum wins: an equal mean later in the grid never replaces it
         if (mean > best) {
             best = mean;
             res->selected_index = g;
