@@ -1,3 +1,5 @@
+"""How many coordinates of a fit move (delta != 0) against those visited, and
+the fit's log posterior: python scripts/probe_moved.py 1M|10M."""
 import sys
 sys.path[:0] = ['.', 'oracle']
 from paper_1208_0945_b200 import bsccs as B, datagen
