@@ -1,3 +1,5 @@
+"""Fit time against the CTA count of the dataset split (148 / 128 / 112 / 96 / 74
+of the 148 SMs): python scripts/probe_ctas.py 1M 10M."""
 import sys
 sys.path[:0] = ['.', 'oracle']
 import numpy as np
