@@ -1504,6 +1504,14 @@ __global__ void k_era_subject(const int32_t* __restrict__ off, int32_t N, int32_
         for (int k = off[s]; k < off[s + 1]; ++k) esub[k] = static_cast<int32_t>(s);
 }
 
+// one 32-B record in a single 256-bit store (sm_100: STG.256 -- one L2
+// request per record instead of two for the scattered writes)
+__device__ __forceinline__ void st_global_256(void* p, int4 a, int4 b) {
+    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z),
+                 "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+                 : "memory");
+}
+
 // The pair records, one thread per era: the era's drug list (contiguous in
 // the CSR) gives every pair's other drugs; each record is one 32-B store at
 // the pair's CSC position.  Overflow lists: the subject's offset (scan over
@@ -1549,9 +1557,7 @@ __global__ void k_build_rq(const int32_t* __restrict__ off, const int32_t* __res
                 const int4 head = make_int4(ls, lk, (deg - 1) | static_cast<int>((pp[a] >> 30) << 8) | (n << 16), 0);
                 const int4 tail = make_int4(static_cast<int>(o[0] | (o[1] << 16)), static_cast<int>(o[2] | (o[3] << 16)),
                                             static_cast<int>(o[4] | (o[5] << 16)), static_cast<int>(o[6] | (o[7] << 16)));
-                int4* dst = reinterpret_cast<int4*>(rq + (pp[a] & kPosMask));
-                dst[0] = head;
-                dst[1] = tail;
+                st_global_256(rq + (pp[a] & kPosMask), head, tail);
             }
             continue;
         }
@@ -1715,6 +1721,7 @@ void alloc_dataset(bsccs_dataset* ds) {
     // across dataset rebuilds); freed again if the dataset does not qualify
     if (rcd_enabled() && nnz > 0 && nnz < (1ll << 30) && J < 65535) { // u16 drugs, index J the unit drug; 30-bit positions
         ds->rq = dalloc<RRec>(nnz, B, s);
+        if (reinterpret_cast<uintptr_t>(ds->rq) % 32 != 0) internal_error("pair records not 32-B aligned (STG.256)");
         ds->edeg = dalloc<uint8_t>(static_cast<int64_t>(K) + 32, B, s);
         ds->ecol = dalloc<uint16_t>(nnz + 16, B, s);
     }

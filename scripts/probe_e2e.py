@@ -9,6 +9,7 @@ import torch
 from paper_1208_0945_b200 import bsccs as B, datagen
 
 wl = sys.argv[1] if len(sys.argv) > 1 else "1M"
+derive = "--derive-subjects" in sys.argv  # bench.py's e2e leg: per-pair subjects derived on the device
 ds = datagen.config_dataset(wl)
 prior = B.laplace_prior(0.1)
 
@@ -22,11 +23,11 @@ def pinned(a):
 
 held = [pinned(a) for a in ds.arrays()]
 ds_host = B.Dataset(*[v for _, v in held])
-nbytes = sum(a.nbytes for a in ds_host.arrays())
+nbytes = sum(a.nbytes for a in ds_host.arrays()) - (ds_host.subjects.nbytes if derive else 0)
 for it in range(5):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    d = B.DeviceDataset(ds_host, 0)
+    d = B.DeviceDataset(ds_host, 0, upload_subjects=not derive)
     t1 = time.perf_counter()
     r = B.fit(d, prior)
     t2 = time.perf_counter()
